@@ -1,0 +1,115 @@
+"""In-tree build of the two native libraries (no JIT cache, no site-packages install).
+
+  lib/libpf_host.so    C++20 host layer: schedule, DAG, timing, freeze-ratio LP,
+                       freeze controller (namespace pipefreeze) + its C-ABI.
+  lib/libpf_device.so  sm_100a kernels (nvcc -gencode arch=compute_100a,code=sm_100a)
+                       + the per-stage step engine + its C-ABI.
+
+Usage: python -m paper_2602_05754_b200.build [--force] [--host-only]
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+INC = os.path.join(ROOT, "include")
+HOST_SRC = os.path.join(PKG, "csrc", "host")
+DEV_SRC = os.path.join(PKG, "csrc", "device")
+LIB = os.path.join(PKG, "lib")
+OBJ = os.path.join(ROOT, "build", "obj")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _torch_paths():
+    import torch  # noqa: F401  (only for include / lib paths of ATen, used by attention glue)
+
+    tdir = os.path.dirname(os.path.abspath(sys.modules["torch"].__file__))
+    return [os.path.join(tdir, "include"), os.path.join(tdir, "include", "torch", "csrc", "api", "include")], os.path.join(tdir, "lib")
+
+
+def _newer(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} {cmd[-1]}")
+
+
+def build_host(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "libpf_host.so")
+    srcs = sorted(glob.glob(os.path.join(HOST_SRC, "*.cpp")))
+    deps = srcs + glob.glob(os.path.join(HOST_SRC, "*.hpp")) + glob.glob(os.path.join(INC, "*.h"))
+    if force or _newer(out, deps):
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra",
+               "-I", INC, "-I", HOST_SRC, *srcs, "-o", out]
+        _run(cmd)
+    return out
+
+
+def build_device(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    os.makedirs(OBJ, exist_ok=True)
+    out = os.path.join(LIB, "libpf_device.so")
+    tinc, tlib = _torch_paths()
+    cu = sorted(glob.glob(os.path.join(DEV_SRC, "*.cu")))
+    cpp = sorted(glob.glob(os.path.join(DEV_SRC, "*.cpp")))
+    headers = glob.glob(os.path.join(DEV_SRC, "*.cuh")) + glob.glob(os.path.join(DEV_SRC, "*.hpp")) + glob.glob(os.path.join(INC, "*.h"))
+    common = ["-I", INC, "-I", DEV_SRC, "-I", HOST_SRC]
+    tflags = [f"-I{p}" for p in tinc] + ["-D_GLIBCXX_USE_CXX11_ABI=1"]
+    jobs = []
+    objs = []
+    for src in cu + cpp:
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not (force or _newer(obj, [src] + headers)):
+            continue
+        uses_torch = os.path.basename(src).startswith("aten_")
+        if src.endswith(".cu"):
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+                   "-Xcompiler", "-fPIC", *common, *(tflags if uses_torch else []), "-c", src, "-o", obj]
+        else:
+            cmd = ["g++", "-std=c++17", "-O2", "-fPIC", *common, f"-I{CUDA_HOME}/include",
+                   *(tflags if uses_torch else []), "-c", src, "-o", obj]
+        jobs.append(cmd)
+    if jobs:
+        with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+            list(ex.map(_run, jobs))
+    if force or jobs or _newer(out, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out,
+               f"-L{tlib}", f"-Xlinker", f"-rpath={tlib}",
+               "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart"]
+        _run(cmd)
+    return out
+
+
+def build(force: bool = False, host_only: bool = False) -> list[str]:
+    outs = [build_host(force)]
+    if not host_only:
+        outs.append(build_device(force))
+    return outs
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--host-only", action="store_true")
+    a = ap.parse_args()
+    for o in build(a.force, a.host_only):
+        print(o)

@@ -1,0 +1,49 @@
+// extern "C" wrappers for the standalone kernels (include/pf_device.h).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "pf_device.h"
+#include "pf_device_internal.hpp"
+
+namespace {
+thread_local std::string g_last_error;
+int record(int rc) {
+  if (rc == PF_ERR_CUDA) {
+    cudaError_t e = cudaGetLastError();
+    g_last_error = cudaGetErrorString(e);
+  }
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int pf_gemm_bf16(const void* A, int a_mn_major, long long lda, const void* B, int b_mn_major,
+                 long long ldb, void* C, long long ldc, int M, int N, int K, float alpha,
+                 int epilogue, int block_n, int* unit_stamp, int stamp, void* stream) {
+  if (!A || !B || !C) return PF_ERR_INVALID;
+  pf::GemmOperand a{A, lda, a_mn_major != 0};
+  pf::GemmOperand b{B, ldb, b_mn_major != 0};
+  pf::GemmOut c{C, ldc, unit_stamp, 0, stamp};
+  return record(pf::gemm_bf16(a, b, c, M, N, K, alpha, epilogue, block_n,
+                              static_cast<cudaStream_t>(stream)));
+}
+
+int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B, int b_mn_major,
+                     long long ldb, float* G, long long ldg, int M, int N, int K, float alpha,
+                     const int* unit_list, const int* unit_count, int max_units,
+                     int* unit_stamp, int stamp_offset, int stamp, void* stream) {
+  if (!A || !B || !G) return PF_ERR_INVALID;
+  pf::GemmOperand a{A, lda, a_mn_major != 0};
+  pf::GemmOperand b{B, ldb, b_mn_major != 0};
+  pf::GemmOut c{G, ldg, unit_stamp, stamp_offset, stamp};
+  return record(pf::gemm_bf16_units(a, b, c, M, N, K, alpha, unit_list, unit_count, max_units,
+                                    static_cast<cudaStream_t>(stream)));
+}
+
+int pf_device_sm_count(void) { return pf::num_sms(); }
+
+const char* pf_device_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,449 @@
+// K1 / K2 / K3: persistent warp-specialized tcgen05 GEMM for sm_100a.
+//
+//   C[M,N] (op)= alpha * A[M,K] . B[N,K]^T      bf16 in, fp32 accumulate in TMEM
+//
+// A and B are each either K-major (row-major [rows][K]) or MN-major (row-major
+// [K][rows]); the MMA consumes both straight from SWIZZLE_128B shared memory,
+// so the three training GEMMs need no transposes:
+//   forward  Y  = X  . W^T      A = X  (K-major)  B = W (K-major)
+//   dX       dX = dY . W        A = dY (K-major)  B = W (MN-major)
+//   dW       dW = dY^T . X      A = dY (MN-major) B = X (MN-major)
+// The dW launch runs over a device-resident work list of unfrozen 128x128
+// units (K5 output), so its time is linear in the unfrozen count; this is the
+// device realisation of w = w_max - r (w_max - w_min) (reference
+// proj/src/timing.cpp:53) and of the masked accumulation sum_m U_m . g_m
+// (reference proj/src/sandbox.cpp:232-249).
+//
+// Roles (192 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0      TMA producer (one lane): smem ring of STAGES {A,B} k-blocks
+//   warp 1      TMEM allocator + MMA issuer (one lane): tcgen05.mma into a
+//               double-buffered TMEM accumulator (2 x BN fp32 columns)
+//   warps 2..5  epilogue: tcgen05.ld -> registers -> global (bf16 / fp32)
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "ptx.cuh"
+#include "pf_device_internal.hpp"
+
+namespace pf {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle span of bf16
+constexpr int GROUP_M = 16;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+struct GemmParams {
+  int M, N, K;
+  void* C;
+  long long ldc;
+  float alpha;
+  int tiles_m, tiles_n;
+  int num_tiles;          // plain mode
+  const int* tile_list;   // list mode: unit ids (mb * tiles_n + nb)
+  const int* tile_count;  // list mode: device-resident count
+  int* unit_stamp;        // EPI_ACC_F32 first-touch stamps (indexed by unit id + stamp_offset)
+  int stamp_offset;
+  int stamp;
+};
+
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb, int& nb) {
+  if (p.tile_list != nullptr) {
+    const int u = p.tile_list[t];
+    mb = u / p.tiles_n;
+    nb = u - mb * p.tiles_n;
+    return;
+  }
+  const int group_size = GROUP_M * p.tiles_n;
+  const int g = t / group_size;
+  const int first_m = g * GROUP_M;
+  const int gm = min(p.tiles_m - first_m, GROUP_M);
+  const int local = t - g * group_size;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+
+  const int ntiles = p.tile_list != nullptr ? *p.tile_count : p.num_tiles;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mb, nb;
+        decode_tile(p, t, mb, nb);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+          if constexpr (!A_MN) {
+            tma_load_2d(a_dst, &tmA, &full_bar[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              tma_load_2d(a_dst + c * 8192, &tmA, &full_bar[stage], mb * BM + c * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(b_dst, &tmB, &full_bar[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d(b_dst + c * 8192, &tmB, &full_bar[stage], nb * BN + c * 64, kb * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 16 elements = 32 B inside the swizzle atom.
+            // MN-major: advance 16 K-rows = 2 atoms of 8 rows x 128 B.
+            const uint64_t adesc = A_MN ? sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                                        : sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                                        : sdesc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[abuf]);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + static_cast<int>(lane);
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int mb, nb;
+      decode_tile(p, t, mb, nb);
+      bool first_touch = false;
+      int unit = 0;
+      if constexpr (EPI == EPI_ACC_F32) {
+        unit = p.stamp_offset + mb * p.tiles_n + nb;
+        first_touch = p.unit_stamp[unit] != p.stamp;
+      }
+      mbar_wait(&tfull_bar[abuf], aphase);
+      tc_fence_after();
+      const long long grow = static_cast<long long>(mb) * BM + row;
+      const bool row_ok = grow < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                               static_cast<uint32_t>(abuf * BN + c * 32),
+                           r);
+        tmem_ld_wait();
+        const int gcol = nb * BN + c * 32;
+        if (!row_ok || gcol >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+        const bool full = gcol + 32 <= p.N;
+        if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
+          if (full) {
+            uint4* c4 = reinterpret_cast<uint4*>(cp);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = v[j * 8 + i];
+              if constexpr (EPI == EPI_ADD_BF16) {
+                const uint4 old = c4[j];
+                const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(o[i]);
+                  w[2 * i] += f.x;
+                  w[2 * i + 1] += f.y;
+                }
+              }
+              uint4 out;
+              out.x = pack_bf16x2(w[0], w[1]);
+              out.y = pack_bf16x2(w[2], w[3]);
+              out.z = pack_bf16x2(w[4], w[5]);
+              out.w = pack_bf16x2(w[6], w[7]);
+              c4[j] = out;
+            }
+          } else {
+            for (int i = 0; i < 32 && gcol + i < p.N; ++i) {
+              float w = v[i];
+              if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(cp[i]);
+              cp[i] = __float2bfloat16_rn(w);
+            }
+          }
+        } else {
+          float* cp = reinterpret_cast<float*>(p.C) + grow * p.ldc + gcol;
+          if (full) {
+            float4* c4 = reinterpret_cast<float4*>(cp);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              if (EPI == EPI_ACC_F32 && !first_touch) {
+                const float4 o = c4[j];
+                w.x += o.x;
+                w.y += o.y;
+                w.z += o.z;
+                w.w += o.w;
+              }
+              c4[j] = w;
+            }
+          } else {
+            for (int i = 0; i < 32 && gcol + i < p.N; ++i) {
+              float w = v[i];
+              if (EPI == EPI_ACC_F32 && !first_touch) w += cp[i];
+              cp[i] = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[abuf]);
+      if constexpr (EPI == EPI_ACC_F32) {
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) p.unit_stamp[unit] = p.stamp;
+      }
+      abuf ^= 1;
+      if (abuf == 0) aphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// Row-major bf16 matrix [rows][cols] with row stride ld (elements); box
+// {box_cols (inner), box_rows}.
+int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
+              int box_cols, int box_rows) {
+  auto encode = get_encode();
+  if (!encode) return PF_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  // invalid geometry (row stride not a multiple of 16 B, misaligned base, ...)
+  return r == CUDA_SUCCESS ? PF_OK : PF_ERR_INVALID;
+}
+
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+int launch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int grid_limit,
+           cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ta, tb;
+  // A logical [M, K]; B logical [N, K]
+  int rc = A_MN ? make_tmap(&ta, A.ptr, p.K, p.M, A.ld, 64, 64)
+                : make_tmap(&ta, A.ptr, p.M, p.K, A.ld, 64, BM);
+  if (rc) return rc;
+  rc = B_MN ? make_tmap(&tb, B.ptr, p.K, p.N, B.ld, 64, 64)
+            : make_tmap(&tb, B.ptr, p.N, p.K, B.ld, 64, BN);
+  if (rc) return rc;
+  auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::SMEM_BYTES) != cudaSuccess)
+      return PF_ERR_CUDA;
+    attr_set = true;
+  }
+  int grid = std::min(grid_limit, num_sms());
+  if (grid <= 0) return PF_OK;
+  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, p);
+  return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
+
+template <int BN>
+int dispatch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int epi, int grid_limit,
+             cudaStream_t s) {
+  const int key = (A.mn_major ? 1 : 0) | (B.mn_major ? 2 : 0);
+#define PF_GEMM_CASE(AM, BMN, E)                                            \
+  if (key == ((AM) | ((BMN) << 1)) && epi == (E))                           \
+    return launch<BN, (AM) != 0, (BMN) != 0, (E)>(A, B, p, grid_limit, s);
+#define PF_GEMM_EPIS(AM, BMN)                                               \
+  PF_GEMM_CASE(AM, BMN, EPI_STORE_BF16)                                     \
+  PF_GEMM_CASE(AM, BMN, EPI_ADD_BF16)                                       \
+  PF_GEMM_CASE(AM, BMN, EPI_ACC_F32)                                        \
+  PF_GEMM_CASE(AM, BMN, EPI_STORE_F32)
+  PF_GEMM_EPIS(0, 0)
+  PF_GEMM_EPIS(0, 1)
+  PF_GEMM_EPIS(1, 0)
+  PF_GEMM_EPIS(1, 1)
+#undef PF_GEMM_EPIS
+#undef PF_GEMM_CASE
+  return PF_ERR_INVALID;
+}
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,
+              float alpha, int epi, int block_n, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
+  if (block_n != 128 && block_n != 256) return PF_ERR_INVALID;
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.C = C.ptr;
+  p.ldc = C.ld;
+  p.alpha = alpha;
+  p.tiles_m = (M + BM - 1) / BM;
+  p.tiles_n = (N + block_n - 1) / block_n;
+  p.num_tiles = p.tiles_m * p.tiles_n;
+  p.unit_stamp = C.unit_stamp;
+  p.stamp_offset = C.stamp_offset;
+  p.stamp = C.stamp;
+  if (epi == EPI_ACC_F32 && (C.unit_stamp == nullptr || block_n != 128)) return PF_ERR_INVALID;
+  return block_n == 256 ? dispatch<256>(A, B, p, epi, p.num_tiles, stream)
+                        : dispatch<128>(A, B, p, epi, p.num_tiles, stream);
+}
+
+int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N,
+                    int K, float alpha, const int* unit_list, const int* unit_count,
+                    int max_units, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
+  if (C.unit_stamp == nullptr || unit_list == nullptr || unit_count == nullptr)
+    return PF_ERR_INVALID;
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.C = C.ptr;
+  p.ldc = C.ld;
+  p.alpha = alpha;
+  p.tiles_m = (M + BM - 1) / BM;
+  p.tiles_n = (N + 127) / 128;
+  p.num_tiles = 0;
+  p.tile_list = unit_list;
+  p.tile_count = unit_count;
+  p.unit_stamp = C.unit_stamp;
+  p.stamp_offset = C.stamp_offset;
+  p.stamp = C.stamp;
+  return dispatch<128>(A, B, p, EPI_ACC_F32, max_units, stream);
+}
+
+}  // namespace pf

@@ -1,0 +1,42 @@
+// Internal (C++) declarations shared by the device translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pf_status.h"
+
+namespace pf {
+
+enum GemmEpilogue : int {
+  EPI_STORE_BF16 = 0,  // C = bf16(alpha * acc)
+  EPI_ADD_BF16 = 1,    // C = bf16(C + alpha * acc)
+  EPI_ACC_F32 = 2,     // fp32 C; first touch of a 128x128 unit in this step stores, later add
+  EPI_STORE_F32 = 3,   // C = alpha * acc (fp32)
+};
+
+struct GemmOperand {
+  const void* ptr;    // bf16
+  long long ld;       // row stride in elements of the stored matrix
+  bool mn_major;      // false: stored [rows][K]; true: stored [K][rows]
+};
+
+struct GemmOut {
+  void* ptr;
+  long long ld;
+  int* unit_stamp = nullptr;  // EPI_ACC_F32 only
+  int stamp_offset = 0;
+  int stamp = 0;
+};
+
+int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,
+              float alpha, int epi, int block_n, cudaStream_t stream);
+
+// Masked weight-gradient GEMM over a device-resident list of 128x128 units.
+int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N,
+                    int K, float alpha, const int* unit_list, const int* unit_count,
+                    int max_units, cudaStream_t stream);
+
+int num_sms();
+
+}  // namespace pf

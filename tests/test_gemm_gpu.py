@@ -1,0 +1,107 @@
+"""K1/K2/K3 tcgen05 GEMM parity vs a torch fp32 reference of the same op (bf16 inputs)."""
+import ctypes
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2602_05754_b200 import _native
+
+    return _native.device(), _native
+
+
+def _run(A, a_mn, B, b_mn, C, M, N, K, epi=0, bn=256, alpha=1.0, stamps=None, stamp=0):
+    import torch
+
+    lib, nat = _lib()
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = lib.pf_gemm_bf16(A.data_ptr(), int(a_mn), A.stride(0), B.data_ptr(), int(b_mn), B.stride(0),
+                          C.data_ptr(), C.stride(0), M, N, K, alpha, epi, bn,
+                          stamps.data_ptr() if stamps is not None else None, stamp, stream)
+    nat.check(rc, "pf_gemm_bf16")
+    torch.cuda.synchronize()
+
+
+def _ref(A, a_mn, B, b_mn):
+    a = (A.t() if a_mn else A).float()
+    b = (B.t() if b_mn else B).float()
+    return a @ b.t()
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("bn", [256, 128])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 320), (296, 392, 200), (128, 256, 64), (1024, 768, 1024)])
+def test_gemm_store_bf16(cuda, a_mn, b_mn, bn, M, N, K):
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn((K, M) if a_mn else (M, K), generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn((K, N) if b_mn else (N, K), generator=g).to(torch.bfloat16).cuda()
+    C = torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    _run(A, a_mn, B, b_mn, C, M, N, K, epi=0, bn=bn)
+    ref = _ref(A, a_mn, B, b_mn)
+    err = (C.float() - ref).abs().max().item()
+    tol = 1e-2 * ref.abs().max().item() + 1e-2
+    assert err <= tol, f"max err {err} > {tol}"
+
+
+@pytest.mark.parametrize("epi", [1, 3])
+def test_gemm_add_and_f32(cuda, epi):
+    import torch
+
+    M, N, K = 384, 512, 448
+    g = torch.Generator(device="cpu").manual_seed(5)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn(K, N, generator=g).to(torch.bfloat16).cuda()
+    ref = _ref(A, 0, B, 1) * 0.5
+    if epi == 1:
+        C0 = torch.randn(M, N, generator=g).to(torch.bfloat16).cuda()
+        C = C0.clone()
+        _run(A, 0, B, 1, C, M, N, K, epi=1, alpha=0.5)
+        ref = ref + C0.float()
+        assert (C.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-2
+    else:
+        C = torch.zeros(M, N, dtype=torch.float32, device=cuda)
+        _run(A, 0, B, 1, C, M, N, K, epi=3, alpha=0.5)
+        assert (C - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+
+
+def test_gemm_dw_unit_list_accumulates(cuda):
+    """dW over unit lists: first touch stores, later microbatches accumulate; untouched units keep stale data."""
+    import torch
+
+    lib, nat = _lib()
+    T, O, I = 512, 384, 512  # dY [T, O], X [T, I] -> G [O, I], 3 x 4 units
+    g = torch.Generator(device="cpu").manual_seed(11)
+    G = torch.full((O, I), 7.0, dtype=torch.float32, device=cuda)
+    stamps = torch.zeros(3 * 4, dtype=torch.int32, device=cuda)
+    expect = torch.full((O, I), 7.0, dtype=torch.float64)
+    lists = [[0, 5, 6, 11], [5, 1, 11], [2]]
+    stream = torch.cuda.current_stream().cuda_stream
+    seen = set()
+    for units in lists:
+        dY = torch.randn(T, O, generator=g).to(torch.bfloat16).cuda()
+        X = torch.randn(T, I, generator=g).to(torch.bfloat16).cuda()
+        ul = torch.tensor(units, dtype=torch.int32, device=cuda)
+        cnt = torch.tensor([len(units)], dtype=torch.int32, device=cuda)
+        rc = lib.pf_gemm_dw_units(dY.data_ptr(), 1, dY.stride(0), X.data_ptr(), 1, X.stride(0), G.data_ptr(),
+                                  G.stride(0), O, I, T, 1.0, ul.data_ptr(), cnt.data_ptr(), 12,
+                                  stamps.data_ptr(), 0, 42, stream)
+        nat.check(rc, "pf_gemm_dw_units")
+        full = dY.double().cpu().t() @ X.double().cpu()
+        for u in units:
+            r, c = divmod(u, 4)
+            blk = full[r * 128:(r + 1) * 128, c * 128:(c + 1) * 128]
+            if u in seen:
+                expect[r * 128:(r + 1) * 128, c * 128:(c + 1) * 128] += blk
+            else:
+                expect[r * 128:(r + 1) * 128, c * 128:(c + 1) * 128] = blk
+        seen |= set(units)
+    torch.cuda.synchronize()
+    err = (G.double().cpu() - expect).abs().max().item()
+    assert err <= 1e-3 * expect.abs().max().item()
+    st = stamps.cpu().tolist()
+    for u in range(12):
+        assert st[u] == (42 if u in {0, 5, 6, 11, 1, 2} else 0)
