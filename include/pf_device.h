@@ -44,7 +44,98 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
                      int* unit_stamp, int stamp_offset, int stamp, void* stream);
 
 int pf_device_sm_count(void);
-const char* pf_device_last_error(void);
+const char* pf_device_last_error(void);  /* message of the last failed kernel-level call */
+const char* pf_engine_last_error(void);  /* message of the last failed engine / K4-K7 call */
+
+/* One freezable weight matrix of a stage (device-side table entry, 32 bytes). */
+typedef struct pf_unit_matrix {
+  long long elem_offset; /* into the stage's flat parameter buffers */
+  int rows, cols;
+  int unit_offset;       /* first unit id of the matrix within the stage */
+  int tiles_n;           /* ceil(cols / 128) */
+  int units;             /* ceil(rows/128) * tiles_n */
+  int pad_;
+} pf_unit_matrix;
+
+/* K5: frozen-unit bitmask (sample_mask bit order, one bit per 128x128 unit, +1
+ * pad word) -> per-matrix lists of unfrozen local unit ids (lists[unit_offset..])
+ * and counts[matrix]. mats is a DEVICE array of nmats entries. */
+int pf_mask_to_unit_lists(const uint64_t* frozen_words, const pf_unit_matrix* mats, int nmats, int* lists,
+                          int* counts, void* stream);
+
+/* K6 (+ fused K4): theta -= scale * G over units whose stamp == `stamp`
+ * (reference masked update proj/src/sandbox.cpp:221,250). When ema != NULL the
+ * APF state of every unit is advanced with delta = -scale*G (0 for untouched
+ * units) and eligible[u] counts elements with score < apf_threshold. */
+int pf_masked_sgd_units(float* master, void* weights_bf16, const float* grad, const int* unit_stamp, int stamp,
+                        float scale, const pf_unit_matrix* mats, int nmats, int total_units, float* ema,
+                        float* ema_abs, float apf_alpha, float apf_threshold, int* eligible, void* stream);
+int pf_sgd_dense(float* master, void* weights_bf16, const float* grad, long long n, float scale, void* stream);
+
+/* K4: apf_update (reference proj/src/freezectl.cpp:147-156) in fp32 on the device. */
+int pf_apf_update(float* ema, float* ema_abs, const float* delta, float* score, long long n, float alpha,
+                  void* stream);
+
+/* K7 glue (bf16 activations, fp32 statistics) */
+int pf_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int T, int h, float eps, void* stream);
+int pf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* residual, void* dx,
+                   float* dg, int T, int h, void* stream);
+int pf_swiglu_fwd(const void* gu, void* a, int T, int ffn, void* stream);
+int pf_swiglu_bwd(const void* gu, const void* da, void* dgu, int T, int ffn, void* stream);
+int pf_rope_fwd(void* qkv, int T, int seq, int nh, int nkv, int hd, float theta, void* stream);
+int pf_cross_entropy(void* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
+                     float loss_scale, void* stream);
+
+/* ------------------------------------------------------------ stage step engine */
+
+typedef struct pf_model_cfg {
+  int hidden, ffn, n_heads, n_kv_heads, head_dim, vocab, layers, seq, micro_batch;
+  float rope_theta, norm_eps, init_std;
+} pf_model_cfg;
+
+typedef struct pf_train_cfg {
+  int kind;             /* 0 gpipe, 1 1f1b, 2 interleaved-1f1b, 3 zbv */
+  int ranks, stages_per_rank, microbatches, rank;
+  int phases[4];        /* T_w, T_m, T_f, T_total (PhasePlan) */
+  double r_max, lr;
+  uint64_t seed;
+  int apf, apf_every;
+  float apf_alpha, apf_threshold;
+  int device, mask_threads;
+} pf_train_cfg;
+
+typedef struct pf_step_result {
+  double loss, batch_ms, optimizer_ms, predicted_ms, mean_ratio, mask_ms;
+  long long frozen_units, total_units;
+  int phase;
+} pf_step_result;
+
+typedef struct pf_trainer_info {
+  long long tokens_per_step, params, unit_params, matmul_flops_fwd_per_mb;
+  int units, local_stages, actions;
+  double lp_solve_ms;
+} pf_trainer_info;
+
+/* Alg. 1 driver for this rank: schedule + DAG + controller on the host,
+ * Stage engine on the device. */
+int pf_trainer_create(const pf_model_cfg* model, const pf_train_cfg* cfg, pf_ctx** out);
+int pf_trainer_destroy(pf_ctx* ctx);
+/* One training step t (1-based). host_tokens/host_targets: [M][micro_batch*seq]
+ * int32 or NULL (device-resident synthetic tokens). */
+int pf_trainer_step(pf_ctx* ctx, int t, const int32_t* host_tokens, const int32_t* host_targets,
+                    pf_step_result* out);
+/* ratio < 0: the phase controller + LP plan; ratio in [0,1]: every cell frozen at `ratio`. */
+int pf_trainer_set_override(pf_ctx* ctx, double ratio);
+int pf_trainer_set_plan(pf_ctx* ctx, const double* ratios /* (s-1)*M + (m-1) */);
+/* plan ratios and {base, opt, floor} makespans of the LP on monitored bounds; returns PF_ERR_DOMAIN before T_m. */
+int pf_trainer_get_plan(pf_ctx* ctx, double* ratios, double* out3, double* w_min, double* w_max);
+int pf_trainer_action_ms(pf_ctx* ctx, double* ms, int* kinds, int* microbatches, int* stages);
+int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
+/* Raw buffers of local stage i (tests): fp32 master / grad, bf16 weights, unit stamps, device unit table. */
+int pf_trainer_stage_buffers(pf_ctx* ctx, int local_stage, void** master, void** weights, void** grad,
+                             void** stamps, long long* n_params, int* n_units);
+/* The last step's frozen-unit masks of local stage i: M masks of ceil(units/64) words. */
+int pf_trainer_last_masks(pf_ctx* ctx, int local_stage, uint64_t* out);
 
 #ifdef __cplusplus
 }

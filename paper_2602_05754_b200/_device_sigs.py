@@ -1,5 +1,65 @@
-"""ctypes signatures of libpf_device.so beyond the GEMM entry points (filled as the ABI grows)."""
+"""ctypes signatures of libpf_device.so (include/pf_device.h) beyond the GEMM entry points."""
+import ctypes
+
+c_int = ctypes.c_int
+c_ll = ctypes.c_longlong
+c_f = ctypes.c_float
+c_d = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_cp = ctypes.c_char_p
 
 
-def register(lib, sig) -> None:  # noqa: D401
-    return None
+class PfModelCfg(ctypes.Structure):
+    _fields_ = [(n, c_int) for n in ("hidden", "ffn", "n_heads", "n_kv_heads", "head_dim", "vocab", "layers", "seq",
+                                     "micro_batch")] + [("rope_theta", c_f), ("norm_eps", c_f), ("init_std", c_f)]
+
+
+class PfTrainCfg(ctypes.Structure):
+    _fields_ = [("kind", c_int), ("ranks", c_int), ("stages_per_rank", c_int), ("microbatches", c_int),
+                ("rank", c_int), ("phases", c_int * 4), ("r_max", c_d), ("lr", c_d), ("seed", ctypes.c_uint64),
+                ("apf", c_int), ("apf_every", c_int), ("apf_alpha", c_f), ("apf_threshold", c_f),
+                ("device", c_int), ("mask_threads", c_int)]
+
+
+class PfStepResult(ctypes.Structure):
+    _fields_ = [("loss", c_d), ("batch_ms", c_d), ("optimizer_ms", c_d), ("predicted_ms", c_d),
+                ("mean_ratio", c_d), ("mask_ms", c_d), ("frozen_units", c_ll), ("total_units", c_ll),
+                ("phase", c_int)]
+
+
+class PfTrainerInfo(ctypes.Structure):
+    _fields_ = [("tokens_per_step", c_ll), ("params", c_ll), ("unit_params", c_ll),
+                ("matmul_flops_fwd_per_mb", c_ll), ("units", c_int), ("local_stages", c_int), ("actions", c_int),
+                ("lp_solve_ms", c_d)]
+
+
+DEVICE_SIGNATURES = {
+    "pf_engine_last_error": ([], c_cp),
+    "pf_mask_to_unit_lists": ([c_vp, c_vp, c_int, c_vp, c_vp, c_vp], c_int),
+    "pf_masked_sgd_units": ([c_vp, c_vp, c_vp, c_vp, c_int, c_f, c_vp, c_int, c_int, c_vp, c_vp, c_f, c_f, c_vp,
+                             c_vp], c_int),
+    "pf_sgd_dense": ([c_vp, c_vp, c_vp, c_ll, c_f, c_vp], c_int),
+    "pf_apf_update": ([c_vp, c_vp, c_vp, c_vp, c_ll, c_f, c_vp], c_int),
+    "pf_rmsnorm_fwd": ([c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f, c_vp], c_int),
+    "pf_rmsnorm_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_vp], c_int),
+    "pf_swiglu_fwd": ([c_vp, c_vp, c_int, c_int, c_vp], c_int),
+    "pf_swiglu_bwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_vp], c_int),
+    "pf_rope_fwd": ([c_vp, c_int, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
+    "pf_cross_entropy": ([c_vp, c_vp, c_vp, c_int, c_int, c_f, c_f, c_vp], c_int),
+    "pf_trainer_create": ([ctypes.POINTER(PfModelCfg), ctypes.POINTER(PfTrainCfg), ctypes.POINTER(c_vp)], c_int),
+    "pf_trainer_destroy": ([c_vp], c_int),
+    "pf_trainer_step": ([c_vp, c_int, c_vp, c_vp, ctypes.POINTER(PfStepResult)], c_int),
+    "pf_trainer_set_override": ([c_vp, c_d], c_int),
+    "pf_trainer_set_plan": ([c_vp, c_vp], c_int),
+    "pf_trainer_get_plan": ([c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pf_trainer_action_ms": ([c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pf_trainer_get_info": ([c_vp, ctypes.POINTER(PfTrainerInfo)], c_int),
+    "pf_trainer_stage_buffers": ([c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                  ctypes.POINTER(c_vp), ctypes.POINTER(c_ll), ctypes.POINTER(c_int)], c_int),
+    "pf_trainer_last_masks": ([c_vp, c_int, c_vp], c_int),
+}
+
+
+def register(lib, sig) -> None:
+    for name, (args, res) in DEVICE_SIGNATURES.items():
+        sig(lib, name, args, res)

@@ -85,7 +85,7 @@ def build_device(force: bool = False) -> str:
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                    "-Xcompiler", "-fPIC", *common, *(tflags if uses_torch else []), "-c", src, "-o", obj]
         else:
-            cmd = ["g++", "-std=c++17", "-O2", "-fPIC", *common, f"-I{CUDA_HOME}/include",
+            cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", *common, f"-I{CUDA_HOME}/include",
                    *(tflags if uses_torch else []), "-c", src, "-o", obj]
         jobs.append(cmd)
     if jobs:
@@ -94,7 +94,8 @@ def build_device(force: bool = False) -> str:
     if force or jobs or _newer(out, objs):
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out,
                f"-L{tlib}", f"-Xlinker", f"-rpath={tlib}",
-               "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart"]
+               "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart",
+               f"-L{LIB}", "-lpf_host", "-Xlinker", "-rpath=$ORIGIN"]
         _run(cmd)
     return out
 
@@ -102,7 +103,7 @@ def build_device(force: bool = False) -> str:
 def build(force: bool = False, host_only: bool = False) -> list[str]:
     outs = [build_host(force)]
     if not host_only:
-        outs.append(build_device(force))
+        outs.append(build_device(force or _newer(os.path.join(LIB, "libpf_device.so"), [outs[0]])))
     return outs
 
 

@@ -1,0 +1,118 @@
+// Causal GQA attention for the LLaMA stage (K7 glue), delegated to ATen's
+// flash-attention ops (library code, like cuBLAS; the only non-hand-written
+// kernels on the step). q/k/v are zero-copy views into the packed qkv
+// activation [T, (nh + 2 nkv) hd]; outputs stay on the caller's stream.
+#include <ATen/ATen.h>
+#include <c10/cuda/CUDAGuard.h>
+#include <c10/cuda/CUDAStream.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "attention.hpp"
+#include "pf_status.h"
+
+namespace pf {
+
+struct AttnState {
+  at::Tensor out, lse, cum_q, cum_k, seed, offset;
+  at::Tensor dq, dk, dv;
+  int64_t max_q = 0, max_k = 0;
+};
+
+namespace {
+
+thread_local std::string g_attn_err;
+
+struct Views {
+  at::Tensor q, k, v;
+};
+
+Views make_views(const void* qkv, int B, int S, int nh, int nkv, int hd) {
+  const auto opts = at::TensorOptions().dtype(at::kBFloat16).device(at::kCUDA, c10::cuda::current_device());
+  const int64_t W = static_cast<int64_t>(nh + 2 * nkv) * hd;
+  auto* base = static_cast<at::BFloat16*>(const_cast<void*>(qkv));
+  auto view = [&](int64_t off, int heads) {
+    return at::from_blob(base + off, {B, S, heads, hd}, {S * W, W, hd, 1}, opts).transpose(1, 2);
+  };
+  return Views{view(0, nh), view(static_cast<int64_t>(nh) * hd, nkv), view(static_cast<int64_t>(nh + nkv) * hd, nkv)};
+}
+
+c10::cuda::CUDAStream wrap(cudaStream_t s) {
+  return c10::cuda::getStreamFromExternal(s, c10::cuda::current_device());
+}
+
+}  // namespace
+
+AttnState* attn_state_new() { return new AttnState(); }
+void attn_state_free(AttnState* st) { delete st; }
+const char* attn_last_error() { return g_attn_err.c_str(); }
+
+int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int hd, float scale, void** out,
+             long long* out_token_stride, cudaStream_t stream) {
+  try {
+    c10::cuda::CUDAStreamGuard guard(wrap(stream));
+    const auto v = make_views(qkv, B, S, nh, nkv, hd);
+    auto r = at::_scaled_dot_product_flash_attention(v.q, v.k, v.v, 0.0, true, false, static_cast<double>(scale));
+    at::Tensor o = std::get<0>(r);
+    // Wo GEMM wants [T, nh*hd] row-major = [B, S, H, D] contiguous
+    at::Tensor bshd = o.transpose(1, 2);
+    if (!bshd.is_contiguous()) o = bshd.contiguous().transpose(1, 2);
+    st->out = o;
+    st->lse = std::get<1>(r);
+    st->cum_q = std::get<2>(r);
+    st->cum_k = std::get<3>(r);
+    st->max_q = std::get<4>(r).expect_int();
+    st->max_k = std::get<5>(r).expect_int();
+    st->seed = std::get<6>(r);
+    st->offset = std::get<7>(r);
+    *out = st->out.data_ptr();
+    *out_token_stride = st->out.stride(2);
+    return PF_OK;
+  } catch (const std::exception& e) {
+    g_attn_err = e.what();
+    return PF_ERR_CUDA;
+  }
+}
+
+int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int nh, int nkv, int hd, float scale,
+             AttnGrads* g, cudaStream_t stream) {
+  try {
+    c10::cuda::CUDAStreamGuard guard(wrap(stream));
+    const auto v = make_views(qkv, B, S, nh, nkv, hd);
+    const auto opts = at::TensorOptions().dtype(at::kBFloat16).device(at::kCUDA, c10::cuda::current_device());
+    auto* dptr = static_cast<at::BFloat16*>(const_cast<void*>(dout));
+    const int64_t W = static_cast<int64_t>(nh) * hd;
+    at::Tensor go = at::from_blob(dptr, {B, S, nh, hd}, {S * W, W, hd, 1}, opts).transpose(1, 2);
+    auto r = at::_scaled_dot_product_flash_attention_backward(go, v.q, v.k, v.v, st->out, st->lse, st->cum_q,
+                                                              st->cum_k, st->max_q, st->max_k, 0.0, true, st->seed,
+                                                              st->offset, static_cast<double>(scale));
+    // token-major [B, S, H, D] so (b, s) flattens to t with one stride
+    st->dq = std::get<0>(r).transpose(1, 2).contiguous();
+    st->dk = std::get<1>(r).transpose(1, 2).contiguous();
+    st->dv = std::get<2>(r).transpose(1, 2).contiguous();
+    g->dq = st->dq.data_ptr();
+    g->dk = st->dk.data_ptr();
+    g->dv = st->dv.data_ptr();
+    g->dq_tok = st->dq.stride(1);
+    g->dk_tok = st->dk.stride(1);
+    g->dv_tok = st->dv.stride(1);
+    g->dq_head = st->dq.stride(2);
+    g->dk_head = st->dk.stride(2);
+    g->dv_head = st->dv.stride(2);
+    return PF_OK;
+  } catch (const std::exception& e) {
+    g_attn_err = e.what();
+    return PF_ERR_CUDA;
+  }
+}
+
+void attn_release(AttnState* st) {
+  st->out = at::Tensor();
+  st->lse = at::Tensor();
+  st->dq = at::Tensor();
+  st->dk = at::Tensor();
+  st->dv = at::Tensor();
+}
+
+}  // namespace pf

@@ -1,0 +1,32 @@
+// Opaque bridge to the ATen flash-attention glue (aten_attention.cpp), so the
+// CUDA translation units never include torch headers.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace pf {
+
+struct AttnState;
+
+struct AttnGrads {
+  const void* dq;
+  const void* dk;
+  const void* dv;
+  long long dq_tok, dk_tok, dv_tok;     // element stride between tokens
+  long long dq_head, dk_head, dv_head;  // element stride between heads
+};
+
+AttnState* attn_state_new();
+void attn_state_free(AttnState* st);
+const char* attn_last_error();
+
+// qkv: packed [B*S, (nh + 2 nkv) hd] bf16 after RoPE. *out receives the
+// attention output [B*S, nh*hd] (row stride *out_token_stride), owned by st.
+int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int hd, float scale, void** out,
+             long long* out_token_stride, cudaStream_t stream);
+// dout: [B*S, nh*hd] gradient of the attention output. Gradients stay owned by st.
+int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int nh, int nkv, int hd, float scale,
+             AttnGrads* g, cudaStream_t stream);
+// release saved forward tensors (after the backward consumed them)
+void attn_release(AttnState* st);
+
+}  // namespace pf

@@ -1,0 +1,633 @@
+// Memory-bound sm_100a kernels of the stage step:
+//   K4  APF freeze metric (standalone and fused into the optimizer)
+//   K5  frozen-unit bitmask -> per-matrix work lists for the masked dW GEMM
+//   K6  masked SGD step over 128x128 units (skips units frozen in every microbatch)
+//   K7  LLaMA glue: embedding, RMSNorm, RoPE, SwiGLU, fused cross-entropy, init
+// All loads/stores are 16-byte vectorised and coalesced along rows; grids are
+// sized as multiples of the SM count (persistent grid-stride loops).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+#include "pf_device_internal.hpp"
+
+namespace pf {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+int grid_for(long long work_items, int per_sm = 8) {
+  const long long cap = static_cast<long long>(num_sms()) * per_sm;
+  long long g = work_items < cap ? work_items : cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+int status() { return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_isum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct bf16x8 {
+  __nv_bfloat162 v[4];
+};
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ const UnitMatrix& find_matrix(const UnitMatrix* mats, int nmats, int u) {
+  int lo = 0, hi = nmats - 1;
+  while (lo < hi) {  // last matrix with unit_offset <= u
+    const int mid = (lo + hi + 1) >> 1;
+    if (mats[mid].unit_offset <= u) lo = mid;
+    else hi = mid - 1;
+  }
+  return mats[lo];
+}
+
+// ------------------------------------------------------------------ K5
+__global__ void __launch_bounds__(kBlock) mask_to_lists_kernel(const uint64_t* __restrict__ words,
+                                                               const UnitMatrix* __restrict__ mats,
+                                                               int* __restrict__ lists, int* __restrict__ counts) {
+  const UnitMatrix m = mats[blockIdx.x];
+  __shared__ int warp_tot[kBlock / 32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // each thread owns 32 consecutive units of the chunk
+  for (int chunk = 0; chunk < m.units; chunk += kBlock * 32) {
+    const int first = chunk + threadIdx.x * 32;
+    uint32_t unfrozen = 0;
+    if (first < m.units) {
+      const long long g = static_cast<long long>(m.unit_offset) + first;  // global unit id
+      const uint64_t w0 = words[g >> 6];
+      const uint64_t w1 = ((g & 63) != 0) ? words[(g >> 6) + 1] : 0;  // may read one word past a segment; buffer is padded
+      const uint64_t bits = (g & 63) ? ((w0 >> (g & 63)) | (w1 << (64 - (g & 63)))) : w0;
+      unfrozen = ~static_cast<uint32_t>(bits);
+      const int valid = m.units - first;
+      if (valid < 32) unfrozen &= (1u << valid) - 1u;
+    }
+    const int cnt = __popc(unfrozen);
+    // block exclusive scan of cnt
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int warp_base = 0;
+    for (int w = 0; w < warp; ++w) warp_base += warp_tot[w];
+    int pos = carry + warp_base + incl - cnt;
+    int* out = lists + m.unit_offset;
+    for (uint32_t b = unfrozen; b; b &= b - 1) out[pos++] = first + __ffs(b) - 1;
+    __syncthreads();
+    if (threadIdx.x == kBlock - 1) carry += warp_base + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) counts[blockIdx.x] = carry;
+}
+
+// ------------------------------------------------------------------ K6 (+K4 fused)
+__global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int red[kBlock / 32];
+  const bool apf = a.apf_ema != nullptr;
+  for (int u = blockIdx.x; u < a.total_units; u += gridDim.x) {
+    const bool touched = a.unit_stamp[u] == a.stamp;
+    if (!touched && !apf) continue;  // frozen in every microbatch: no update (sandbox.cpp:250)
+    const UnitMatrix& m = find_matrix(a.mats, a.nmats, u);
+    const int lu = u - m.unit_offset;
+    const int rb = lu / m.tiles_n, cb = lu - rb * m.tiles_n;
+    const int r0 = rb * 128, c0 = cb * 128;
+    const int nrows = min(128, m.rows - r0), ncols = min(128, m.cols - c0);
+    int eligible = 0;
+    const int col = lane * 4;
+    if (col < ncols) {
+#pragma unroll 4
+      for (int r = warp; r < nrows; r += kBlock / 32) {
+        const long long e = m.elem_offset + static_cast<long long>(r0 + r) * m.cols + c0 + col;
+        float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (touched) {
+          const float4 g = __ldcs(reinterpret_cast<const float4*>(a.grad + e));
+          float4 th = *reinterpret_cast<const float4*>(a.master + e);
+          d = make_float4(-a.scale * g.x, -a.scale * g.y, -a.scale * g.z, -a.scale * g.w);
+          th.x += d.x;
+          th.y += d.y;
+          th.z += d.z;
+          th.w += d.w;
+          *reinterpret_cast<float4*>(a.master + e) = th;
+          uint2 packed;
+          packed.x = pack_bf16x2(th.x, th.y);
+          packed.y = pack_bf16x2(th.z, th.w);
+          *reinterpret_cast<uint2*>(a.weights + e) = packed;
+        }
+        if (apf) {
+          const long long i = e - a.apf_elem_base;
+          float4 E = *reinterpret_cast<const float4*>(a.apf_ema + i);
+          float4 A = *reinterpret_cast<const float4*>(a.apf_ema_abs + i);
+          const float al = a.apf_alpha, be = 1.0f - a.apf_alpha;
+          E.x = al * E.x + be * d.x;
+          E.y = al * E.y + be * d.y;
+          E.z = al * E.z + be * d.z;
+          E.w = al * E.w + be * d.w;
+          A.x = al * A.x + be * fabsf(d.x);
+          A.y = al * A.y + be * fabsf(d.y);
+          A.z = al * A.z + be * fabsf(d.z);
+          A.w = al * A.w + be * fabsf(d.w);
+          *reinterpret_cast<float4*>(a.apf_ema + i) = E;
+          *reinterpret_cast<float4*>(a.apf_ema_abs + i) = A;
+          auto below = [&](float ev, float av) { return (av == 0.f ? 1.f : fabsf(ev) / av) < a.apf_threshold; };
+          eligible += below(E.x, A.x) + below(E.y, A.y) + below(E.z, A.z) + below(E.w, A.w);
+        }
+      }
+    }
+    if (apf && a.apf_eligible != nullptr) {
+      eligible = warp_isum(eligible);
+      if (lane == 0) red[warp] = eligible;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+        a.apf_eligible[u] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void sgd_dense_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
+                                 const float* __restrict__ g, long long n4, float scale) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    float4 t = reinterpret_cast<float4*>(master)[i];
+    t.x -= scale * gv.x;
+    t.y -= scale * gv.y;
+    t.z -= scale * gv.z;
+    t.w -= scale * gv.w;
+    reinterpret_cast<float4*>(master)[i] = t;
+    uint2 p;
+    p.x = pack_bf16x2(t.x, t.y);
+    p.y = pack_bf16x2(t.z, t.w);
+    reinterpret_cast<uint2*>(w)[i] = p;
+  }
+}
+
+__global__ void apf_update_kernel(float* __restrict__ ema, float* __restrict__ ema_abs,
+                                  const float* __restrict__ delta, float* __restrict__ score, long long n,
+                                  float alpha) {
+  const float be = 1.0f - alpha;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float d = delta[i];
+    const float e = alpha * ema[i] + be * d;
+    const float a = alpha * ema_abs[i] + be * fabsf(d);
+    ema[i] = e;
+    ema_abs[i] = a;
+    if (score) score[i] = a == 0.f ? 1.f : fabsf(e) / a;
+  }
+}
+
+// ------------------------------------------------------------------ K7 glue
+__global__ void embedding_fwd_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                                     __nv_bfloat16* __restrict__ out, int T, int h) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nw) {
+    const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<long long>(tok[t]) * h);
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<long long>(t) * h);
+    for (int c = lane; c < h / 8; c += 32) dst[c] = src[c];
+  }
+}
+
+__global__ void embedding_bwd_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ dout,
+                                     float* __restrict__ gtable, int T, int h) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nw) {
+    float* dst = gtable + static_cast<long long>(tok[t]) * h;
+    const __nv_bfloat16* src = dout + static_cast<long long>(t) * h;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8];
+      load8(src + c, f);
+      atomicAdd(reinterpret_cast<float4*>(dst + c), make_float4(f[0], f[1], f[2], f[3]));
+      atomicAdd(reinterpret_cast<float4*>(dst + c + 4), make_float4(f[4], f[5], f[6], f[7]));
+    }
+  }
+}
+
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                   __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h,
+                                   float eps) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < T; t += nw) {
+    const __nv_bfloat16* xr = x + static_cast<long long>(t) * h;
+    float ss = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8];
+      load8(xr + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss / h + eps);
+    if (lane == 0) rstd[t] = r;
+    __nv_bfloat16* yr = y + static_cast<long long>(t) * h;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8], gg[8];
+      load8(xr + c, f);
+      load8(g + c, gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = f[i] * r * gg[i];
+      store8(yr + c, f);
+    }
+  }
+}
+
+// block: 8 warps, each warp one row at a time; dg partials in shared memory
+__global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                             const __nv_bfloat16* __restrict__ g,
+                                                             const float* __restrict__ rstd,
+                                                             const __nv_bfloat16* __restrict__ dy,
+                                                             const __nv_bfloat16* __restrict__ residual,
+                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ dg,
+                                                             int T, int h) {
+  extern __shared__ float sdg[];
+  for (int c = threadIdx.x; c < h; c += blockDim.x) sdg[c] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
+    const long long off = static_cast<long long>(t) * h;
+    const float r = rstd[t];
+    float dot = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+      float xv[8], gv[8], dv[8];
+      load8(x + off + c, xv);
+      load8(g + c, gv);
+      load8(dy + off + c, dv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        dot += gv[i] * dv[i] * xv[i];
+        atomicAdd(&sdg[c + i], dv[i] * xv[i] * r);
+      }
+    }
+    dot = warp_sum(dot);
+    const float k = dot * r * r * r / h;
+    for (int c = lane * 8; c < h; c += 256) {
+      float xv[8], gv[8], dv[8], out[8];
+      load8(x + off + c, xv);
+      load8(g + c, gv);
+      load8(dy + off + c, dv);
+      if (residual) load8(residual + off + c, out);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = (residual ? out[i] : 0.f) + r * gv[i] * dv[i] - k * xv[i];
+      store8(dx + off + c, out);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x) atomicAdd(&dg[c], sdg[c]);
+}
+
+// rotate-half RoPE on the q and k heads of the packed qkv activation, in place
+__global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int T, int seq,
+                                int nh, int nkv, int hd) {
+  const int half = hd / 2;
+  const int heads = nh + nkv;
+  const long long total = static_cast<long long>(T) * heads * half;
+  const long long row = static_cast<long long>(nh + 2 * nkv) * hd;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % half);
+    const long long th = i / half;
+    const int head = static_cast<int>(th % heads);
+    const int t = static_cast<int>(th / heads);
+    const float2 c = cs[(t % seq) * half + j];
+    __nv_bfloat16* p = qkv + t * row + static_cast<long long>(head) * hd;
+    const float a = __bfloat162float(p[j]), b = __bfloat162float(p[j + half]);
+    p[j] = __float2bfloat16_rn(a * c.x - b * c.y);
+    p[j + half] = __float2bfloat16_rn(b * c.x + a * c.y);
+  }
+}
+
+__global__ void rope_bwd_pack_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
+                                     const __nv_bfloat16* __restrict__ dv, long long qts, long long kts,
+                                     long long vts, long long qhs, long long khs, long long vhs,
+                                     __nv_bfloat16* __restrict__ dqkv, const float2* __restrict__ cs, int T, int seq,
+                                     int nh, int nkv, int hd) {
+  const int half = hd / 2;
+  const int heads = nh + 2 * nkv;
+  const long long total = static_cast<long long>(T) * heads * half;
+  const long long row = static_cast<long long>(heads) * hd;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % half);
+    const long long th = i / half;
+    const int head = static_cast<int>(th % heads);
+    const int t = static_cast<int>(th / heads);
+    const __nv_bfloat16* src;
+    if (head < nh) src = dq + t * qts + head * qhs;
+    else if (head < nh + nkv) src = dk + t * kts + (head - nh) * khs;
+    else src = dv + t * vts + (head - nh - nkv) * vhs;
+    const float a = __bfloat162float(src[j]), b = __bfloat162float(src[j + half]);
+    float oa = a, ob = b;
+    if (head < nh + nkv) {  // inverse rotation (transpose of the forward rotation)
+      const float2 c = cs[(t % seq) * half + j];
+      oa = a * c.x + b * c.y;
+      ob = b * c.x - a * c.y;
+    }
+    __nv_bfloat16* d = dqkv + t * row + static_cast<long long>(head) * hd;
+    d[j] = __float2bfloat16_rn(oa);
+    d[j + half] = __float2bfloat16_rn(ob);
+  }
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int T,
+                                  int ffn) {
+  const long long per_row = ffn / 8;
+  const long long total = static_cast<long long>(T) * per_row;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = i / per_row;
+    const int c = static_cast<int>(i - t * per_row) * 8;
+    float g[8], u[8], o[8];
+    load8(gu + t * 2 * ffn + c, g);
+    load8(gu + t * 2 * ffn + ffn + c, u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
+    store8(a + t * ffn + c, o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
+                                  __nv_bfloat16* __restrict__ dgu, int T, int ffn) {
+  const long long per_row = ffn / 8;
+  const long long total = static_cast<long long>(T) * per_row;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = i / per_row;
+    const int c = static_cast<int>(i - t * per_row) * 8;
+    float g[8], u[8], d[8], dg[8], du[8];
+    load8(gu + t * 2 * ffn + c, g);
+    load8(gu + t * 2 * ffn + ffn + c, u);
+    load8(da + t * ffn + c, d);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float s = sigmoidf_(g[k]);
+      const float silu = g[k] * s;
+      du[k] = d[k] * silu;
+      dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
+    }
+    store8(dgu + t * 2 * ffn + c, dg);
+    store8(dgu + t * 2 * ffn + ffn + c, du);
+  }
+}
+
+// one block per row: online max/sum-exp, then dlogits in place
+__global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __restrict__ logits,
+                                                               const int* __restrict__ targets,
+                                                               float* __restrict__ loss_sum, int V,
+                                                               float grad_scale, float loss_scale) {
+  const long long t = blockIdx.x;
+  __nv_bfloat16* row = logits + t * V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ float sm[kBlock / 32], ss[kBlock / 32];
+  float mx = -INFINITY, sum = 0.f;
+  for (int c = threadIdx.x * 8; c < V; c += kBlock * 8) {
+    float f[8];
+    load8(row + c, f);
+    float lm = f[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) lm = fmaxf(lm, f[i]);
+    const float nm = fmaxf(mx, lm);
+    sum *= __expf(mx - nm);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += __expf(f[i] - nm);
+    mx = nm;
+  }
+  // combine (max, sum) across the block
+  float wm = warp_max(mx);
+  float ws = warp_sum(sum * __expf(mx - wm));
+  if (lane == 0) {
+    sm[warp] = wm;
+    ss[warp] = ws;
+  }
+  __syncthreads();
+  float bm = -INFINITY;
+  for (int w = 0; w < kBlock / 32; ++w) bm = fmaxf(bm, sm[w]);
+  float bs = 0.f;
+  for (int w = 0; w < kBlock / 32; ++w) bs += ss[w] * __expf(sm[w] - bm);
+  const float lse = bm + __logf(bs);
+  const int tgt = targets[t];
+  const float xt = __bfloat162float(row[tgt]);
+  __syncthreads();
+  for (int c = threadIdx.x * 8; c < V; c += kBlock * 8) {
+    float f[8];
+    load8(row + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = (__expf(f[i] - lse) - (c + i == tgt ? 1.f : 0.f)) * grad_scale;
+    store8(row + c, f);
+  }
+  if (threadIdx.x == 0) atomicAdd(loss_sum, (lse - xt) * loss_scale);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_normal_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w, long long n,
+                                   float stddev, uint64_t seed) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint64_t r = mix64(seed + 0x9e3779b97f4a7c15ULL * static_cast<uint64_t>(i + 1));
+    const float u1 = (static_cast<float>(r >> 40) + 1.0f) * (1.0f / 16777217.0f);
+    const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.0f / 16777216.0f);
+    const float v = stddev * sqrtf(-2.f * __logf(u1)) * __cosf(6.28318530718f * u2);
+    master[i] = v;
+    w[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void fill_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w, long long n, float v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    master[i] = v;
+    w[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void rope_table_kernel(float2* cs, int seq, int hd, float theta) {
+  const int half = hd / 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < seq * half; i += gridDim.x * blockDim.x) {
+    const int p = i / half, j = i % half;
+    const double inv = pow(static_cast<double>(theta), -2.0 * j / hd);
+    const double ang = p * inv;
+    cs[i] = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
+  }
+}
+
+__global__ void random_tokens_kernel(int* tok, long long n, int vocab, uint64_t seed) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    tok[i] = static_cast<int>(mix64(seed + 0x9e3779b97f4a7c15ULL * static_cast<uint64_t>(i + 1)) %
+                              static_cast<uint64_t>(vocab));
+}
+
+}  // namespace
+
+int launch_mask_to_unit_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* lists, int* counts,
+                              cudaStream_t s) {
+  if (nmats <= 0) return PF_OK;
+  mask_to_lists_kernel<<<nmats, kBlock, 0, s>>>(words, mats, lists, counts);
+  return status();
+}
+
+int launch_masked_sgd_units(const OptimArgs& a, cudaStream_t s) {
+  if (a.total_units <= 0) return PF_OK;
+  masked_sgd_units_kernel<<<grid_for(a.total_units, 8), kBlock, 0, s>>>(a);
+  return status();
+}
+
+int launch_sgd_dense(float* master, __nv_bfloat16* w, const float* g, long long n, float scale, cudaStream_t s) {
+  if (n <= 0) return PF_OK;
+  if (n % 4) return PF_ERR_INVALID;
+  sgd_dense_kernel<<<grid_for((n / 4 + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, g, n / 4, scale);
+  return status();
+}
+
+int launch_apf_update(float* ema, float* ema_abs, const float* delta, float* score, long long n, float alpha,
+                      cudaStream_t s) {
+  if (n <= 0) return PF_OK;
+  apf_update_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(ema, ema_abs, delta, score, n, alpha);
+  return status();
+}
+
+int launch_embedding_fwd(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int T, int h,
+                         cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  embedding_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(tok, table, out, T, h);
+  return status();
+}
+
+int launch_embedding_bwd(const int* tok, const __nv_bfloat16* dout, float* g, int T, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  embedding_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(tok, dout, g, T, h);
+  return status();
+}
+
+int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
+                       float eps, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  rmsnorm_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, y, rstd, T, h, eps);
+  return status();
+}
+
+int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
+                       const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  const size_t smem = static_cast<size_t>(h) * sizeof(float);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+  rmsnorm_bwd_kernel<<<grid_for((T + 7) / 8, 2), kBlock, smem, s>>>(x, g, rstd, dy, residual, dx, dg, T, h);
+  return status();
+}
+
+int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh, int nkv, int hd, cudaStream_t s) {
+  const long long total = static_cast<long long>(T) * (nh + nkv) * (hd / 2);
+  rope_fwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(qkv, cs, T, seq, nh, nkv, hd);
+  return status();
+}
+
+int launch_rope_bwd_pack(const __nv_bfloat16* dq, const __nv_bfloat16* dk, const __nv_bfloat16* dv, long long qts,
+                         long long kts, long long vts, long long qhs, long long khs, long long vhs,
+                         __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh, int nkv, int hd,
+                         cudaStream_t s) {
+  const long long total = static_cast<long long>(T) * (nh + 2 * nkv) * (hd / 2);
+  rope_bwd_pack_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      dq, dk, dv, qts, kts, vts, qhs, khs, vhs, dqkv, cs, T, seq, nh, nkv, hd);
+  return status();
+}
+
+int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s) {
+  if (ffn % 8) return PF_ERR_INVALID;
+  const long long total = static_cast<long long>(T) * ffn / 8;
+  swiglu_fwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(gu, a, T, ffn);
+  return status();
+}
+
+int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
+                      cudaStream_t s) {
+  if (ffn % 8) return PF_ERR_INVALID;
+  const long long total = static_cast<long long>(T) * ffn / 8;
+  swiglu_bwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(gu, da, dgu, T, ffn);
+  return status();
+}
+
+int launch_cross_entropy(__nv_bfloat16* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
+                         float loss_scale, cudaStream_t s) {
+  if (V % 8) return PF_ERR_INVALID;
+  cross_entropy_kernel<<<T, kBlock, 0, s>>>(logits, targets, loss_sum, V, grad_scale, loss_scale);
+  return status();
+}
+
+int launch_init_normal(float* master, __nv_bfloat16* w, long long n, float stddev, uint64_t seed, cudaStream_t s) {
+  if (n <= 0) return PF_OK;
+  init_normal_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, n, stddev, seed);
+  return status();
+}
+
+int launch_fill(float* master, __nv_bfloat16* w, long long n, float v, cudaStream_t s) {
+  if (n <= 0) return PF_OK;
+  fill_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, n, v);
+  return status();
+}
+
+int launch_rope_table(float2* cs, int seq, int hd, float theta, cudaStream_t s) {
+  rope_table_kernel<<<grid_for((static_cast<long long>(seq) * hd / 2 + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      cs, seq, hd, theta);
+  return status();
+}
+
+int launch_random_tokens(int* tok, long long n, int vocab, uint64_t seed, cudaStream_t s) {
+  random_tokens_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(tok, n, vocab, seed);
+  return status();
+}
+
+}  // namespace pf

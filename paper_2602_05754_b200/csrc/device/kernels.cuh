@@ -1,0 +1,86 @@
+// Declarations of the memory-bound sm_100a kernels (kernels.cu) and their
+// host launchers. All launchers are asynchronous on `stream`.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pf {
+
+// One freezable weight matrix of a stage: 128x128 units, row-major storage.
+struct UnitMatrix {
+  long long elem_offset;  // into the stage's flat parameter buffers
+  int rows, cols;
+  int unit_offset;        // first unit id of this matrix in the stage
+  int tiles_n;            // ceil(cols / 128)
+  int units;              // tiles_m * tiles_n
+};
+
+constexpr int kMaxUnitMatrices = 512;
+
+// ---- K5: frozen-unit bitmask -> per-matrix lists of unfrozen local unit ids
+// (reference sample_mask bit order, proj/include/pipefreeze/freezectl.hpp:47)
+int launch_mask_to_unit_lists(const uint64_t* frozen_words, const UnitMatrix* mats_dev, int nmats,
+                              int* lists, int* counts, cudaStream_t s);
+
+// ---- K6: masked SGD over unit matrices, theta -= scale * G for units whose
+// stamp equals `stamp` (touched this step); optional fused APF (K4) update of
+// E / E_abs with delta = -scale * G (0 for untouched units) and a per-unit
+// count of APF-eligible elements (score < threshold).
+struct OptimArgs {
+  float* master;                  // fp32 theta
+  __nv_bfloat16* weights;         // bf16 copy used by the GEMMs
+  const float* grad;              // fp32 G
+  const int* unit_stamp;
+  int stamp;
+  float scale;                    // eta / M
+  const UnitMatrix* mats;         // device table
+  int nmats;
+  int total_units;
+  float* apf_ema;                 // nullptr: no APF this step
+  float* apf_ema_abs;
+  float apf_alpha;
+  float apf_threshold;
+  int* apf_eligible;              // per unit count (may be nullptr)
+  long long apf_elem_base;        // elem offset of the APF buffers (param index of first unit matrix)
+};
+int launch_masked_sgd_units(const OptimArgs& a, cudaStream_t s);
+
+// dense parameters (norm gains, embedding): theta -= scale * G, bf16 copy
+int launch_sgd_dense(float* master, __nv_bfloat16* weights, const float* grad, long long n, float scale,
+                     cudaStream_t s);
+
+// ---- K4 standalone APF update (reference apf_update, freezectl.cpp:147-156)
+int launch_apf_update(float* ema, float* ema_abs, const float* delta, float* score, long long n, float alpha,
+                      cudaStream_t s);
+
+// ---- LLaMA glue (K7)
+int launch_embedding_fwd(const int* tokens, const __nv_bfloat16* table, __nv_bfloat16* out, int T, int h,
+                         cudaStream_t s);
+int launch_embedding_bwd(const int* tokens, const __nv_bfloat16* dout, float* gtable, int T, int h, cudaStream_t s);
+int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
+                       float eps, cudaStream_t s);
+// dx = residual + rmsnorm_bwd(dy); dg += sum_t dy * x * rstd
+int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
+                       const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s);
+int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh, int nkv, int hd, cudaStream_t s);
+// dq, dk, dv (strided, [B, S, H, D] memory) -> rotated back and packed into dqkv [T, (nh+2nkv)hd]
+int launch_rope_bwd_pack(const __nv_bfloat16* dq, const __nv_bfloat16* dk, const __nv_bfloat16* dv,
+                         long long q_tok_stride, long long k_tok_stride, long long v_tok_stride,
+                         long long q_head_stride, long long k_head_stride, long long v_head_stride,
+                         __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh, int nkv, int hd,
+                         cudaStream_t s);
+int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s);
+int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
+                      cudaStream_t s);
+// in place: logits -> dlogits = (softmax - onehot) * grad_scale; loss_sum += sum_t (lse - x_target) * loss_scale
+int launch_cross_entropy(__nv_bfloat16* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
+                         float loss_scale, cudaStream_t s);
+int launch_init_normal(float* master, __nv_bfloat16* weights, long long n, float stddev, uint64_t seed,
+                       cudaStream_t s);
+int launch_fill(float* master, __nv_bfloat16* weights, long long n, float value, cudaStream_t s);
+int launch_rope_table(float2* cs, int seq, int hd, float theta, cudaStream_t s);
+int launch_random_tokens(int* tokens, long long n, int vocab, uint64_t seed, cudaStream_t s);
+
+}  // namespace pf

@@ -1,0 +1,330 @@
+#include "stage.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+namespace pf {
+
+namespace {
+
+constexpr long long kAlign = 64;  // elements: 256 B fp32 / 128 B bf16 (TMA and float4 alignment)
+
+long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
+
+#define PF_TRY(expr)                \
+  do {                              \
+    const int _rc = (expr);         \
+    if (_rc != PF_OK) return _rc;   \
+  } while (0)
+
+#define PF_CUDA(expr)                                      \
+  do {                                                     \
+    if ((expr) != cudaSuccess) return PF_ERR_CUDA;         \
+  } while (0)
+
+int gemm_fwd(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
+             int M, int N, int K, int epi, cudaStream_t s) {
+  // Y[M,N] (+)= A[M,K] . W[N,K]^T, both K-major
+  return gemm_bf16(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, GemmOut{C, ldc}, M, N, K, 1.0f, epi,
+                   N >= 256 ? 256 : 128, s);
+}
+
+int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
+            int M, int N, int K, int epi, cudaStream_t s) {
+  // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
+  return gemm_bf16(GemmOperand{dY, ldy, false}, GemmOperand{W, ldw, true}, GemmOut{C, ldc}, M, N, K, 1.0f, epi,
+                   N >= 256 ? 256 : 128, s);
+}
+
+}  // namespace
+
+ParamSlice Stage::add_matrix(int rows, int cols, bool freezable) {
+  ParamSlice p;
+  p.offset = n_params_;
+  p.count = static_cast<long long>(rows) * cols;
+  p.rows = rows;
+  p.cols = cols;
+  n_params_ = round_up(n_params_ + p.count, kAlign);
+  if (freezable) {
+    UnitMatrix m{};
+    m.elem_offset = p.offset;
+    m.rows = rows;
+    m.cols = cols;
+    m.unit_offset = total_units_;
+    m.tiles_n = (cols + 127) / 128;
+    m.units = ((rows + 127) / 128) * m.tiles_n;
+    total_units_ += m.units;
+    p.unit_matrix = static_cast<int>(mats_.size());
+    mats_.push_back(m);
+  }
+  return p;
+}
+
+ParamSlice Stage::add_dense(long long n) {
+  ParamSlice p;
+  p.offset = n_params_;
+  p.count = n;
+  p.rows = 1;
+  p.cols = static_cast<int>(n);
+  n_params_ = round_up(n_params_ + n, kAlign);
+  return p;
+}
+
+Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device)
+    : cfg_(cfg), spec_(spec), device_(device) {
+  if (cfg.hidden % 128 || cfg.ffn % 64 || cfg.head_dim % 8 || cfg.vocab % 8 || cfg.tokens() % 128)
+    throw std::invalid_argument("stage: unsupported model shape (hidden % 128, ffn % 64, vocab % 8, T % 128)");
+  cudaSetDevice(device);
+  const int h = cfg.hidden;
+  const int nl = spec.layer_end - spec.layer_begin;
+  layers_.resize(static_cast<std::size_t>(nl));
+  // freezable 128x128-unit matrices first (contiguous APF state), then dense params
+  for (auto& L : layers_) {
+    L.wqkv = add_matrix(cfg.qkv_dim(), h, true);
+    L.wo = add_matrix(h, cfg.attn_dim(), true);
+    L.wgu = add_matrix(2 * cfg.ffn, h, true);
+    L.wd = add_matrix(h, cfg.ffn, true);
+  }
+  if (spec.last) wlm_ = add_matrix(cfg.vocab, h, true);
+  n_unit_params_ = n_params_;
+  dense_begin_ = n_params_;
+  for (auto& L : layers_) {
+    L.g1 = add_dense(h);
+    L.g2 = add_dense(h);
+  }
+  if (spec.last) gf_ = add_dense(h);
+  if (spec.first) emb_ = add_matrix(cfg.vocab, h, false);
+
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 256)) != cudaSuccess)
+      throw std::runtime_error("stage: cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    allocations_.push_back(p);
+    return p;
+  };
+  master_ = static_cast<float*>(alloc(static_cast<size_t>(n_params_) * 4));
+  weights_ = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(n_params_) * 2));
+  grad_ = static_cast<float*>(alloc(static_cast<size_t>(n_params_) * 4));
+  stamps_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_) * 4));
+  cudaMemset(stamps_, 0, static_cast<size_t>(total_units_) * 4);
+  unit_lists_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_ + 64) * 4));
+  unit_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
+  mats_dev_ = static_cast<UnitMatrix*>(alloc(mats_.size() * sizeof(UnitMatrix)));
+  cudaMemcpy(mats_dev_, mats_.data(), mats_.size() * sizeof(UnitMatrix), cudaMemcpyHostToDevice);
+  rope_ = static_cast<float2*>(alloc(static_cast<size_t>(cfg.seq) * (cfg.head_dim / 2) * sizeof(float2)));
+  launch_rope_table(rope_, cfg.seq, cfg.head_dim, cfg.rope_theta, nullptr);
+
+  // init: N(0, init_std) for matrices, ones for norm gains (fixed seed per stage)
+  launch_init_normal(master_, weights_, n_unit_params_, cfg.init_std, seed * 1000003ULL + static_cast<uint64_t>(spec.stage), nullptr);
+  for (auto& L : layers_) {
+    launch_fill(master_ + L.g1.offset, weights_ + L.g1.offset, h, 1.0f, nullptr);
+    launch_fill(master_ + L.g2.offset, weights_ + L.g2.offset, h, 1.0f, nullptr);
+  }
+  if (spec.last) launch_fill(master_ + gf_.offset, weights_ + gf_.offset, h, 1.0f, nullptr);
+  if (spec.first)
+    launch_init_normal(master_ + emb_.offset, weights_ + emb_.offset, emb_.count, cfg.init_std,
+                       seed * 7919ULL + 17ULL, nullptr);
+  cudaMemset(grad_, 0, static_cast<size_t>(n_params_) * 4);
+
+  const long long T = cfg.tokens();
+  auto abf = [&](long long elems) { return static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(elems) * 2)); };
+  auto af32 = [&](long long elems) { return static_cast<float*>(alloc(static_cast<size_t>(elems) * 4)); };
+  slots_.resize(static_cast<std::size_t>(slots));
+  for (auto& sl : slots_) {
+    sl.layers.resize(static_cast<std::size_t>(nl));
+    for (auto& L : sl.layers) {
+      L.x = abf(T * h);
+      L.h1 = abf(T * h);
+      L.qkv = abf(T * cfg.qkv_dim());
+      L.x2 = abf(T * h);
+      L.h2 = abf(T * h);
+      L.gu = abf(T * 2 * cfg.ffn);
+      L.a = abf(T * cfg.ffn);
+      L.rstd1 = af32(T);
+      L.rstd2 = af32(T);
+      L.attn = attn_state_new();
+    }
+    sl.x_out = abf(T * h);
+    if (spec.last) {
+      sl.hf = abf(T * h);
+      sl.rstdf = af32(T);
+      sl.logits = abf(T * cfg.vocab);
+    }
+  }
+  d_a_ = abf(T * cfg.ffn);
+  d_gu_ = abf(T * 2 * cfg.ffn);
+  d_h_ = abf(T * h);
+  d_x2_ = abf(T * h);
+  d_attn_ = abf(T * cfg.attn_dim());
+  d_qkv_ = abf(T * cfg.qkv_dim());
+  d_y_ = abf(T * h);
+  d_tmp_ = abf(T * h);
+  if (cudaDeviceSynchronize() != cudaSuccess) throw std::runtime_error("stage: initialisation kernels failed");
+}
+
+Stage::~Stage() {
+  cudaSetDevice(device_);
+  for (auto& sl : slots_)
+    for (auto& L : sl.layers) attn_state_free(L.attn);
+  for (void* p : allocations_) cudaFree(p);
+}
+
+long long Stage::matmul_flops_fwd() const {
+  long long p = 0;
+  for (const auto& m : mats_) p += static_cast<long long>(m.rows) * m.cols;
+  return 2LL * cfg_.tokens() * p;
+}
+
+int Stage::zero_dense_grads(cudaStream_t s) {
+  PF_CUDA(cudaMemsetAsync(grad_ + dense_begin_, 0, static_cast<size_t>(n_params_ - dense_begin_) * 4, s));
+  return PF_OK;
+}
+
+int Stage::forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
+                   float* loss_sum, cudaStream_t s) {
+  if (slot < 0 || slot >= static_cast<int>(slots_.size())) return PF_ERR_INVALID;
+  Slot& sl = slots_[static_cast<std::size_t>(slot)];
+  sl.microbatch = microbatch;
+  const int T = cfg_.tokens(), h = cfg_.hidden;
+  const size_t act = static_cast<size_t>(T) * h * 2;
+  const int nl = static_cast<int>(layers_.size());
+  __nv_bfloat16* x0 = nl > 0 ? sl.layers[0].x : sl.x_out;
+  if (spec_.first) {
+    if (!tokens) return PF_ERR_INVALID;
+    PF_TRY(launch_embedding_fwd(tokens, weights_ + emb_.offset, x0, T, h, s));
+  } else {
+    if (!x_in) return PF_ERR_INVALID;
+    PF_CUDA(cudaMemcpyAsync(x0, x_in, act, cudaMemcpyDeviceToDevice, s));
+  }
+  const float scale = 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim));
+  for (int li = 0; li < nl; ++li) {
+    SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
+    const LayerParams& P = layers_[static_cast<std::size_t>(li)];
+    PF_TRY(launch_rmsnorm_fwd(L.x, weights_ + P.g1.offset, L.h1, L.rstd1, T, h, cfg_.norm_eps, s));
+    PF_TRY(gemm_fwd(L.h1, h, weights_ + P.wqkv.offset, h, L.qkv, cfg_.qkv_dim(), T, cfg_.qkv_dim(), h,
+                    EPI_STORE_BF16, s));
+    PF_TRY(launch_rope_fwd(L.qkv, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
+    void* ao = nullptr;
+    long long ald = 0;
+    PF_TRY(attn_fwd(L.attn, L.qkv, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, scale,
+                    &ao, &ald, s));
+    L.attn_out = static_cast<const __nv_bfloat16*>(ao);
+    L.attn_ld = ald;
+    PF_CUDA(cudaMemcpyAsync(L.x2, L.x, act, cudaMemcpyDeviceToDevice, s));
+    PF_TRY(gemm_fwd(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, h, T, h,
+                    cfg_.attn_dim(), EPI_ADD_BF16, s));
+    PF_TRY(launch_rmsnorm_fwd(L.x2, weights_ + P.g2.offset, L.h2, L.rstd2, T, h, cfg_.norm_eps, s));
+    PF_TRY(gemm_fwd(L.h2, h, weights_ + P.wgu.offset, h, L.gu, 2 * cfg_.ffn, T, 2 * cfg_.ffn, h, EPI_STORE_BF16, s));
+    PF_TRY(launch_swiglu_fwd(L.gu, L.a, T, cfg_.ffn, s));
+    __nv_bfloat16* next = li + 1 < nl ? sl.layers[static_cast<std::size_t>(li + 1)].x : sl.x_out;
+    PF_CUDA(cudaMemcpyAsync(next, L.x2, act, cudaMemcpyDeviceToDevice, s));
+    PF_TRY(gemm_fwd(L.a, cfg_.ffn, weights_ + P.wd.offset, cfg_.ffn, next, h, T, h, cfg_.ffn, EPI_ADD_BF16, s));
+  }
+  if (spec_.last) {
+    if (!targets || !loss_sum) return PF_ERR_INVALID;
+    PF_TRY(launch_rmsnorm_fwd(sl.x_out, weights_ + gf_.offset, sl.hf, sl.rstdf, T, h, cfg_.norm_eps, s));
+    PF_TRY(gemm_fwd(sl.hf, h, weights_ + wlm_.offset, h, sl.logits, cfg_.vocab, T, cfg_.vocab, h, EPI_STORE_BF16, s));
+    // mean token loss of the microbatch; dlogits = (softmax - onehot) / T in place
+    PF_TRY(launch_cross_entropy(sl.logits, targets, loss_sum, T, cfg_.vocab, 1.0f / T, 1.0f / T, s));
+  }
+  return PF_OK;
+}
+
+int Stage::dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                       long long ldx, int stamp, cudaStream_t s) {
+  const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
+  GemmOut out{grad_ + w.offset, w.cols, stamps_, m.unit_offset, stamp};
+  // dW[out, in] += dY^T . X over the unfrozen units; both operands MN-major (no transposes)
+  return gemm_bf16_units(GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, out, w.rows, w.cols,
+                         cfg_.tokens(), 1.0f, unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, s);
+}
+
+int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
+                    __nv_bfloat16* dx_out, int stamp, cudaStream_t s) {
+  if (slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
+  Slot& sl = slots_[static_cast<std::size_t>(slot)];
+  const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
+  const int nl = static_cast<int>(layers_.size());
+  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units
+  PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
+                                   unit_counts_, s));
+  const __nv_bfloat16* dcur = dy;
+  if (spec_.last) {
+    PF_TRY(gemm_dx(sl.logits, cfg_.vocab, weights_ + wlm_.offset, h, d_h_, h, T, h, cfg_.vocab, EPI_STORE_BF16, s));
+    PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
+    PF_TRY(launch_rmsnorm_bwd(sl.x_out, weights_ + gf_.offset, sl.rstdf, d_h_, nullptr, d_y_, grad_ + gf_.offset, T,
+                              h, s));
+    dcur = d_y_;
+  }
+  if (!dcur) return PF_ERR_INVALID;
+  for (int li = nl - 1; li >= 0; --li) {
+    SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
+    const LayerParams& P = layers_[static_cast<std::size_t>(li)];
+    // MLP
+    PF_TRY(gemm_dx(dcur, h, weights_ + P.wd.offset, ffn, d_a_, ffn, T, ffn, h, EPI_STORE_BF16, s));
+    PF_TRY(dgemm_units(P.wd, dcur, h, L.a, ffn, stamp, s));
+    PF_TRY(launch_swiglu_bwd(L.gu, d_a_, d_gu_, T, ffn, s));
+    PF_TRY(gemm_dx(d_gu_, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
+    PF_TRY(dgemm_units(P.wgu, d_gu_, 2 * ffn, L.h2, h, stamp, s));
+    PF_TRY(launch_rmsnorm_bwd(L.x2, weights_ + P.g2.offset, L.rstd2, d_h_, dcur, d_x2_, grad_ + P.g2.offset, T, h, s));
+    // attention
+    PF_TRY(gemm_dx(d_x2_, h, weights_ + P.wo.offset, cfg_.attn_dim(), d_attn_, cfg_.attn_dim(), T, cfg_.attn_dim(), h,
+                   EPI_STORE_BF16, s));
+    PF_TRY(dgemm_units(P.wo, d_x2_, h, L.attn_out, L.attn_ld, stamp, s));
+    AttnGrads ag{};
+    PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
+                    1.0f / std::sqrt(static_cast<float>(cfg_.head_dim)), &ag, s));
+    PF_TRY(launch_rope_bwd_pack(static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
+                                static_cast<const __nv_bfloat16*>(ag.dv), ag.dq_tok, ag.dk_tok, ag.dv_tok, ag.dq_head,
+                                ag.dk_head, ag.dv_head, d_qkv_, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads,
+                                cfg_.head_dim, s));
+    PF_TRY(gemm_dx(d_qkv_, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
+                   EPI_STORE_BF16, s));
+    PF_TRY(dgemm_units(P.wqkv, d_qkv_, cfg_.qkv_dim(), L.h1, h, stamp, s));
+    __nv_bfloat16* out = li > 0 ? (dcur == d_y_ ? d_tmp_ : d_y_) : (spec_.first ? d_tmp_ : dx_out);
+    if (!out) return PF_ERR_INVALID;
+    PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, d_x2_, out, grad_ + P.g1.offset, T, h, s));
+    attn_release(L.attn);
+    dcur = out;
+  }
+  if (spec_.first) PF_TRY(launch_embedding_bwd(tokens, dcur, grad_ + emb_.offset, T, h, s));
+  else if (nl == 0 && dx_out && dcur != dx_out)
+    PF_CUDA(cudaMemcpyAsync(dx_out, dcur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, s));
+  return PF_OK;
+}
+
+int Stage::optimizer_step(float scale, int stamp, bool apf, float apf_alpha, float apf_threshold, cudaStream_t s) {
+  if (apf && !apf_ema_) {
+    PF_CUDA(cudaMalloc(&apf_ema_, static_cast<size_t>(n_unit_params_) * 4));
+    PF_CUDA(cudaMalloc(&apf_ema_abs_, static_cast<size_t>(n_unit_params_) * 4));
+    PF_CUDA(cudaMalloc(&apf_eligible_, static_cast<size_t>(total_units_) * 4));
+    allocations_.push_back(apf_ema_);
+    allocations_.push_back(apf_ema_abs_);
+    allocations_.push_back(apf_eligible_);
+    PF_CUDA(cudaMemsetAsync(apf_ema_, 0, static_cast<size_t>(n_unit_params_) * 4, s));
+    PF_CUDA(cudaMemsetAsync(apf_ema_abs_, 0, static_cast<size_t>(n_unit_params_) * 4, s));
+  }
+  OptimArgs a{};
+  a.master = master_;
+  a.weights = weights_;
+  a.grad = grad_;
+  a.unit_stamp = stamps_;
+  a.stamp = stamp;
+  a.scale = scale;
+  a.mats = mats_dev_;
+  a.nmats = static_cast<int>(mats_.size());
+  a.total_units = total_units_;
+  a.apf_ema = apf ? apf_ema_ : nullptr;
+  a.apf_ema_abs = apf ? apf_ema_abs_ : nullptr;
+  a.apf_alpha = apf_alpha;
+  a.apf_threshold = apf_threshold;
+  a.apf_eligible = apf ? apf_eligible_ : nullptr;
+  a.apf_elem_base = 0;
+  PF_TRY(launch_masked_sgd_units(a, s));
+  return launch_sgd_dense(master_ + dense_begin_, weights_ + dense_begin_, grad_ + dense_begin_,
+                          n_params_ - dense_begin_, scale, s);
+}
+
+}  // namespace pf

@@ -1,0 +1,156 @@
+// One pipeline stage of a LLaMA-shaped decoder on one GPU: parameters,
+// per-microbatch saved activations, forward / backward with the masked
+// weight-gradient GEMM, and the masked optimizer step.
+//
+// The reference has no model; its stage step is the pair of CPU stand-ins
+// sample_execution (duration, proj/src/timing.cpp:58-65) and run_masked_sgd
+// (numerics, proj/src/sandbox.cpp:191-257). Here:
+//   forward(m)   f(m,s): K1 GEMMs + glue; w_f is its device time
+//   backward(m)  b(m,s): K2 dX GEMMs (w_min part) + K3 dW GEMMs over the
+//                unfrozen 128x128 units of mask U_{m,s} (the (1-r) w_param part)
+//   optimizer    theta -= (eta/M) * sum_m U_m . g_m  (sandbox.cpp:221,250),
+//                units frozen in every microbatch are skipped.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "attention.hpp"
+#include "kernels.cuh"
+#include "pf_device_internal.hpp"
+
+namespace pf {
+
+struct ModelConfig {
+  int hidden = 256;
+  int ffn = 1024;
+  int n_heads = 4;
+  int n_kv_heads = 4;
+  int head_dim = 64;
+  int vocab = 1024;
+  int layers = 8;
+  int seq = 128;
+  int micro_batch = 4;
+  float rope_theta = 500000.f;
+  float norm_eps = 1e-5f;
+  float init_std = 0.02f;
+
+  int tokens() const { return seq * micro_batch; }
+  int qkv_dim() const { return (n_heads + 2 * n_kv_heads) * head_dim; }
+  int attn_dim() const { return n_heads * head_dim; }
+};
+
+struct StageSpec {
+  int stage = 1;         // 1-based virtual stage
+  int layer_begin = 0;   // [begin, end)
+  int layer_end = 0;
+  bool first = false;    // embedding lives here
+  bool last = false;     // final norm + LM head + loss live here
+};
+
+struct ParamSlice {
+  long long offset = 0;  // element offset in the flat buffers
+  long long count = 0;
+  int rows = 0, cols = 0;
+  int unit_matrix = -1;  // index into the unit table, -1 for dense params
+};
+
+struct LayerParams {
+  ParamSlice g1, wqkv, wo, g2, wgu, wd;
+};
+
+struct SavedLayer {  // per layer per microbatch slot
+  __nv_bfloat16 *x = nullptr, *h1 = nullptr, *qkv = nullptr, *x2 = nullptr, *h2 = nullptr, *gu = nullptr,
+                *a = nullptr;
+  float *rstd1 = nullptr, *rstd2 = nullptr;
+  AttnState* attn = nullptr;
+  const __nv_bfloat16* attn_out = nullptr;
+  long long attn_ld = 0;
+};
+
+struct Slot {  // one in-flight microbatch
+  std::vector<SavedLayer> layers;
+  __nv_bfloat16* x_out = nullptr;   // stage output (last layer output / residual stream)
+  __nv_bfloat16* hf = nullptr;      // last stage: final norm output
+  float* rstdf = nullptr;
+  __nv_bfloat16* logits = nullptr;  // last stage: logits -> dlogits in place
+  int microbatch = 0;
+};
+
+class Stage {
+ public:
+  Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device);
+  ~Stage();
+  Stage(const Stage&) = delete;
+  Stage& operator=(const Stage&) = delete;
+
+  // x_in: stage input activations [T, h] (ignored on the first stage, which
+  // embeds tokens). Returns a pointer to the stage output [T, h] inside the slot.
+  int forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
+              float* loss_sum, cudaStream_t s);
+  // frozen_words: device bitmask over this stage's units for this microbatch.
+  // dy: gradient of the stage output (ignored on the last stage). dx_out
+  // receives the gradient of the stage input (ignored on the first stage).
+  int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
+               __nv_bfloat16* dx_out, int stamp, cudaStream_t s);
+  int optimizer_step(float scale, int stamp, bool apf, float apf_alpha, float apf_threshold, cudaStream_t s);
+  int zero_dense_grads(cudaStream_t s);
+
+  const __nv_bfloat16* output(int slot) const { return slots_[slot].x_out; }
+  int units() const { return total_units_; }
+  int words() const { return (total_units_ + 63) / 64; }
+  long long param_count() const { return n_params_; }
+  long long unit_param_count() const { return n_unit_params_; }
+  long long matmul_flops_fwd() const;  // 2 * T * (matmul params of the stage)
+  const std::vector<UnitMatrix>& unit_matrices() const { return mats_; }
+  const ModelConfig& config() const { return cfg_; }
+  const StageSpec& spec() const { return spec_; }
+
+  // raw buffers (tests / parity)
+  float* master() const { return master_; }
+  __nv_bfloat16* weights() const { return weights_; }
+  float* grad() const { return grad_; }
+  int* unit_stamps() const { return stamps_; }
+  int* apf_eligible() const { return apf_eligible_; }
+  float* apf_ema() const { return apf_ema_; }
+  float* apf_ema_abs() const { return apf_ema_abs_; }
+  int last_unfrozen_units() const { return last_unfrozen_; }
+
+ private:
+  ParamSlice add_matrix(int rows, int cols, bool freezable);
+  ParamSlice add_dense(long long n);
+  int dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                  long long ldx, int stamp, cudaStream_t s);
+
+  ModelConfig cfg_;
+  StageSpec spec_;
+  int device_;
+  std::vector<LayerParams> layers_;
+  ParamSlice emb_, gf_, wlm_;
+  std::vector<UnitMatrix> mats_;
+  UnitMatrix* mats_dev_ = nullptr;
+  long long n_params_ = 0, n_unit_params_ = 0, dense_begin_ = 0;
+  int total_units_ = 0;
+  float* master_ = nullptr;
+  __nv_bfloat16* weights_ = nullptr;
+  float* grad_ = nullptr;
+  int* stamps_ = nullptr;
+  float* apf_ema_ = nullptr;
+  float* apf_ema_abs_ = nullptr;
+  int* apf_eligible_ = nullptr;
+  int* unit_lists_ = nullptr;
+  int* unit_counts_ = nullptr;
+  float2* rope_ = nullptr;
+  std::vector<Slot> slots_;
+  // backward workspace
+  __nv_bfloat16 *d_a_ = nullptr, *d_gu_ = nullptr, *d_h_ = nullptr, *d_x2_ = nullptr, *d_attn_ = nullptr,
+                *d_qkv_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr;
+  std::vector<void*> allocations_;
+  int last_unfrozen_ = 0;
+};
+
+}  // namespace pf

@@ -1,0 +1,312 @@
+#include "trainer.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+namespace pf {
+
+using namespace pipefreeze;
+
+namespace {
+
+#define PF_TRY(expr)              \
+  do {                            \
+    const int _rc = (expr);       \
+    if (_rc != PF_OK) return _rc; \
+  } while (0)
+#define PF_CUDA(expr)                              \
+  do {                                             \
+    if ((expr) != cudaSuccess) return PF_ERR_CUDA; \
+  } while (0)
+
+// Layers [begin, end) of virtual stage s (1-based) out of S: the first L % S
+// stages take one extra layer (e.g. 40 layers / 16 stages = 8 x 3 + 8 x 2).
+StageSpec stage_spec(const ModelConfig& m, int s, int S) {
+  const int base = m.layers / S, extra = m.layers % S;
+  StageSpec sp;
+  sp.stage = s;
+  sp.layer_begin = (s - 1) * base + std::min(s - 1, extra);
+  sp.layer_end = sp.layer_begin + base + (s - 1 < extra ? 1 : 0);
+  sp.first = s == 1;
+  sp.last = s == S;
+  return sp;
+}
+
+int units_of(int rows, int cols) { return ((rows + 127) / 128) * ((cols + 127) / 128); }
+
+// Unit count of a stage without allocating it (same matrix list as Stage).
+int stage_units(const ModelConfig& m, const StageSpec& sp) {
+  const int per_layer = units_of(m.qkv_dim(), m.hidden) + units_of(m.hidden, m.attn_dim()) +
+                        units_of(2 * m.ffn, m.hidden) + units_of(m.hidden, m.ffn);
+  return (sp.layer_end - sp.layer_begin) * per_layer + (sp.last ? units_of(m.vocab, m.hidden) : 0);
+}
+
+}  // namespace
+
+Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(model), cfg_(cfg) {
+  cudaSetDevice(cfg.device);
+  timeline_ = build_schedule(cfg.pipeline);
+  dag_ = std::make_unique<PipelineDag>(build_dag(timeline_));
+  validate_phase_plan(cfg.phases);
+  const int S = cfg.pipeline.total_stages();
+  const int M = cfg.pipeline.num_microbatches;
+  if (cfg.rank < 0 || cfg.rank >= cfg.pipeline.num_ranks) throw std::invalid_argument("trainer: rank out of range");
+  if (model.layers < S) throw std::invalid_argument("trainer: fewer layers than pipeline stages");
+  actions_ = timeline_.rank_order[static_cast<std::size_t>(cfg.rank)];
+  for (int s = 1; s <= S; ++s)
+    if (stage_to_rank(cfg.pipeline, s) == cfg.rank) stage_ids_.push_back(s);
+  for (int s : stage_ids_) {
+    if (s > 1 && local_index(s - 1) < 0) throw std::invalid_argument("trainer: multi-rank P2P transport not built in this binary");
+    if (s < S && local_index(s + 1) < 0) throw std::invalid_argument("trainer: multi-rank P2P transport not built in this binary");
+  }
+  // in-flight microbatches per stage = slot count
+  for (int s : stage_ids_) {
+    int live = 0, peak = 0;
+    for (const auto& a : actions_) {
+      if (a.stage != s) continue;
+      live += a.kind == ActionKind::Forward ? 1 : -1;
+      peak = std::max(peak, live);
+    }
+    slots_.push_back(std::max(1, peak));
+  }
+  for (std::size_t i = 0; i < stage_ids_.size(); ++i)
+    stages_.push_back(std::make_unique<Stage>(model, stage_spec(model, stage_ids_[i], S), slots_[i], cfg.seed,
+                                              cfg.device));
+  const long long T = model.tokens();
+  grad_bufs_.resize(stage_ids_.size());
+  for (std::size_t i = 0; i < stage_ids_.size(); ++i)
+    for (int k = 0; k < slots_[i]; ++k) {
+      __nv_bfloat16* p = nullptr;
+      if (cudaMalloc(&p, static_cast<size_t>(T) * model.hidden * 2) != cudaSuccess)
+        throw std::runtime_error("trainer: cudaMalloc failed");
+      grad_bufs_[i].push_back(p);
+    }
+  if (cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking) != cudaSuccess)
+    throw std::runtime_error("trainer: stream creation failed");
+  ev_.resize(2 * actions_.size());
+  for (auto& e : ev_) cudaEventCreate(&e);
+  cudaEventCreate(&ev_opt0_);
+  cudaEventCreate(&ev_opt1_);
+  cudaMalloc(&tokens_dev_, static_cast<size_t>(M) * T * 4);
+  cudaMalloc(&targets_dev_, static_cast<size_t>(M) * T * 4);
+  cudaMalloc(&loss_dev_, 4);
+  launch_random_tokens(tokens_dev_, static_cast<long long>(M) * T, model.vocab, cfg.seed * 31 + 1, stream_);
+  launch_random_tokens(targets_dev_, static_cast<long long>(M) * T, model.vocab, cfg.seed * 31 + 2, stream_);
+  long long words = 0;
+  for (auto& st : stages_) {
+    mask_offsets_.push_back(words);
+    words += static_cast<long long>(M) * (st->words() + 1);  // +1 pad word per mask (K5 reads one past)
+  }
+  mask_offsets_.push_back(words);
+  cudaMalloc(&masks_dev_, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
+  cudaMallocHost(&masks_host_, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
+  std::memset(masks_host_, 0, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
+  cudaMallocHost(&loss_host_, 4);
+  plan_ratios_.assign(static_cast<std::size_t>(S * M), 0.0);
+  if (cudaStreamSynchronize(stream_) != cudaSuccess) throw std::runtime_error("trainer: setup failed");
+}
+
+Trainer::~Trainer() {
+  cudaSetDevice(cfg_.device);
+  if (stream_) cudaStreamSynchronize(stream_);
+  stages_.clear();
+  for (auto& v : grad_bufs_)
+    for (auto* p : v) cudaFree(p);
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (ev_opt0_) cudaEventDestroy(ev_opt0_);
+  if (ev_opt1_) cudaEventDestroy(ev_opt1_);
+  cudaFree(tokens_dev_);
+  cudaFree(targets_dev_);
+  cudaFree(loss_dev_);
+  cudaFree(masks_dev_);
+  cudaFreeHost(masks_host_);
+  cudaFreeHost(loss_host_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+int Trainer::local_index(int stage) const {
+  for (std::size_t i = 0; i < stage_ids_.size(); ++i)
+    if (stage_ids_[i] == stage) return static_cast<int>(i);
+  return -1;
+}
+
+std::vector<Stage*> Trainer::local_stages() {
+  std::vector<Stage*> out;
+  for (auto& s : stages_) out.push_back(s.get());
+  return out;
+}
+
+long long Trainer::tokens_per_step() const {
+  return static_cast<long long>(model_.tokens()) * cfg_.pipeline.num_microbatches;
+}
+
+int Trainer::units_total() const {
+  int u = 0;
+  for (const auto& s : stages_) u += s->units();
+  return u;
+}
+
+void Trainer::set_plan(const std::vector<double>& ratios) {
+  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+  if (static_cast<int>(ratios.size()) != S * M) throw std::invalid_argument("set_plan: need M*S ratios");
+  plan_ratios_ = ratios;
+  plan_ready_ = true;
+}
+
+TimingProfile Trainer::measured_profile() const { return aggregate_monitoring(monitor_); }
+
+// Alg. 1 line at t = T_m: aggregate the monitored durations into bounds, solve
+// the freeze-ratio LP, keep the plan (reference cmd_optimize, pipefreeze.cpp:61-83).
+void Trainer::solve_plan_from_monitoring() {
+  const auto t0 = std::chrono::steady_clock::now();
+  plan_profile_ = aggregate_monitoring(monitor_);
+  const auto lp = build_lp(*dag_, plan_profile_, cfg_.r_max);
+  const auto sol = solve_lp(lp);
+  plan_ = extract_freeze_plan(*dag_, plan_profile_, sol, cfg_.r_max);
+  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+  for (int s = 1; s <= S; ++s)
+    for (int m = 1; m <= M; ++m)
+      plan_ratios_[static_cast<std::size_t>((s - 1) * M + (m - 1))] = plan_.ratio_of(backward_action(m, s));
+  plan_ready_ = true;
+  lp_solve_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepResult* out) {
+  cudaSetDevice(cfg_.device);
+  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+  const int T = model_.tokens();
+  StepResult res;
+  Phase phase = Phase::StableFreeze;
+  const bool controller = override_ratio_ < 0.0;
+  if (controller) {
+    phase = phase_of(t, cfg_.phases);
+    if (phase == Phase::Solve && !plan_ready_) solve_plan_from_monitoring();
+  }
+  res.phase = static_cast<int>(phase);
+
+  // ---- masks for this step's cells (host, jump-ahead into the single stream)
+  const auto tm0 = std::chrono::steady_clock::now();
+  std::vector<int> units_all;
+  for (int s = 1; s <= S; ++s) units_all.push_back(stage_units(model_, stage_spec(model_, s, S)));
+  for (std::size_t li = 0; li < stages_.size(); ++li) {
+    const int s = stage_ids_[li];
+    const int units = stages_[li]->units();
+    const int words = stages_[li]->words();
+    std::vector<uint64_t> tmp(static_cast<std::size_t>(M) * static_cast<std::size_t>(words));
+    if (controller) {
+      MaskStream ms(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
+      ms.stage_step_masks(t, s, tmp.data(), cfg_.mask_threads);
+    } else {
+      for (int m = 1; m <= M; ++m) {
+        Rng rng(cfg_.seed ^ (0x51ed270b27f2e6a1ULL * static_cast<uint64_t>(t * 4096 + s * 64 + m)));
+        const auto mk = sample_mask(units, override_ratio_, rng);
+        std::memcpy(tmp.data() + static_cast<std::size_t>(m - 1) * static_cast<std::size_t>(words), mk.words().data(),
+                    static_cast<size_t>(words) * 8);
+      }
+    }
+    for (int m = 0; m < M; ++m) {
+      uint64_t* dst = masks_host_ + mask_offsets_[li] + static_cast<long long>(m) * (words + 1);
+      std::memcpy(dst, tmp.data() + static_cast<std::size_t>(m) * static_cast<std::size_t>(words),
+                  static_cast<size_t>(words) * 8);
+      dst[words] = 0;
+      long long pc = 0;
+      for (int w = 0; w < words; ++w) pc += __builtin_popcountll(dst[w]);
+      res.frozen_units += pc;
+      res.total_units += units;
+    }
+  }
+  res.mean_ratio = res.total_units ? static_cast<double>(res.frozen_units) / static_cast<double>(res.total_units) : 0.0;
+  res.mask_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
+
+  PF_CUDA(cudaMemcpyAsync(masks_dev_, masks_host_, static_cast<size_t>(mask_offsets_.back()) * 8,
+                          cudaMemcpyHostToDevice, stream_));
+  if (host_tokens)
+    PF_CUDA(cudaMemcpyAsync(tokens_dev_, host_tokens, static_cast<size_t>(M) * T * 4, cudaMemcpyHostToDevice, stream_));
+  if (host_targets)
+    PF_CUDA(cudaMemcpyAsync(targets_dev_, host_targets, static_cast<size_t>(M) * T * 4, cudaMemcpyHostToDevice,
+                            stream_));
+  PF_CUDA(cudaMemsetAsync(loss_dev_, 0, 4, stream_));
+  for (auto& st : stages_) PF_TRY(st->zero_dense_grads(stream_));
+
+  // ---- the rank's action list (schedule order), one microbatch action at a time
+  for (std::size_t i = 0; i < actions_.size(); ++i) {
+    const ActionId a = actions_[i];
+    const int li = local_index(a.stage);
+    Stage& st = *stages_[static_cast<std::size_t>(li)];
+    const int slot = (a.microbatch - 1) % slots_[static_cast<std::size_t>(li)];
+    const int* tok = tokens_dev_ + static_cast<long long>(a.microbatch - 1) * T;
+    const int* tgt = targets_dev_ + static_cast<long long>(a.microbatch - 1) * T;
+    PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
+    if (a.kind == ActionKind::Forward) {
+      const __nv_bfloat16* x_in = nullptr;
+      if (a.stage > 1) {
+        const int lp = local_index(a.stage - 1);
+        x_in = stages_[static_cast<std::size_t>(lp)]->output((a.microbatch - 1) % slots_[static_cast<std::size_t>(lp)]);
+      }
+      PF_TRY(st.forward(slot, a.microbatch, tok, tgt, x_in, loss_dev_, stream_));
+    } else {
+      const __nv_bfloat16* dy = a.stage < S ? grad_bufs_[static_cast<std::size_t>(li)][static_cast<std::size_t>(slot)] : nullptr;
+      __nv_bfloat16* dx = nullptr;
+      if (a.stage > 1) {
+        const int lp = local_index(a.stage - 1);
+        dx = grad_bufs_[static_cast<std::size_t>(lp)][static_cast<std::size_t>((a.microbatch - 1) % slots_[static_cast<std::size_t>(lp)])];
+      }
+      const uint64_t* mw = masks_dev_ + mask_offsets_[static_cast<std::size_t>(li)] +
+                           static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+      PF_TRY(st.backward(slot, tok, mw, dy, dx, t, stream_));
+    }
+    PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
+  }
+  // ---- masked optimizer step: theta -= (eta / M) * sum_m U_m . g_m
+  PF_CUDA(cudaEventRecord(ev_opt0_, stream_));
+  const bool apf_step = cfg_.apf && (t % std::max(1, cfg_.apf_every) == 0);
+  for (auto& st : stages_)
+    PF_TRY(st->optimizer_step(static_cast<float>(cfg_.lr / M), t, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
+  PF_CUDA(cudaEventRecord(ev_opt1_, stream_));
+  PF_CUDA(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, stream_));
+  PF_CUDA(cudaStreamSynchronize(stream_));
+
+  action_ms_.assign(actions_.size(), 0.0);
+  for (std::size_t i = 0; i < actions_.size(); ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev_[2 * i], ev_[2 * i + 1]);
+    action_ms_[i] = ms;
+  }
+  float bms = 0.f, oms = 0.f;
+  if (!actions_.empty()) cudaEventElapsedTime(&bms, ev_[0], ev_[2 * actions_.size() - 1]);
+  cudaEventElapsedTime(&oms, ev_opt0_, ev_opt1_);
+  res.batch_ms = bms;
+  res.optimizer_ms = oms;
+  const bool has_last = local_index(S) >= 0;
+  res.loss = has_last ? static_cast<double>(*loss_host_) / M : std::nan("");
+
+  // ---- monitoring (Alg. 1): upper bounds unfrozen, lower bounds fully frozen
+  if (controller && (phase == Phase::MonitorUpper || phase == Phase::MonitorLower)) {
+    for (std::size_t i = 0; i < actions_.size(); ++i) {
+      const ActionId a = actions_[i];
+      const FreezeState fs =
+          (a.kind == ActionKind::Backward && phase == Phase::MonitorLower) ? FreezeState::Full : FreezeState::None;
+      monitor_.record(a, t, action_ms_[i], fs);
+    }
+  }
+  // ---- LP / DAG prediction of this step's batch time
+  if (plan_ready_ && !plan_profile_.all().empty()) {
+    double scale = 1.0;
+    if (controller && phase == Phase::ProgressiveFreeze && cfg_.phases.t_freeze > cfg_.phases.t_monitor)
+      scale = std::min(1.0, static_cast<double>(t - cfg_.phases.t_monitor) /
+                                (cfg_.phases.t_freeze - cfg_.phases.t_monitor));
+    if (!controller || phase == Phase::ProgressiveFreeze || phase == Phase::StableFreeze) {
+      FreezePlan p = plan_;
+      if (!controller)
+        for (auto& [k, r] : p.ratios) r = override_ratio_;
+      res.predicted_ms = longest_path_start_times(*dag_, plan_weights(*dag_, plan_profile_, p, scale)).makespan;
+    }
+  }
+  if (out) *out = res;
+  return PF_OK;
+}
+
+}  // namespace pf

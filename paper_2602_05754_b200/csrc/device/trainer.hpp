@@ -1,0 +1,107 @@
+// Per-rank training-step driver: the paper's Alg. 1 with
+// the reference's controller semantics. The host side is the C++ pipefreeze
+// layer (schedule, DAG, monitoring aggregation, LP, masks); the device side is
+// the Stage engine. One instance per GPU/process.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "dag.hpp"
+#include "freezectl.hpp"
+#include "lp.hpp"
+#include "schedule.hpp"
+#include "stage.hpp"
+#include "timing.hpp"
+
+namespace pf {
+
+struct TrainConfig {
+  pipefreeze::PipelineConfig pipeline;
+  int rank = 0;
+  pipefreeze::PhasePlan phases{2, 8, 10, 20};
+  double r_max = 0.8;
+  double lr = 1e-3;
+  uint64_t seed = 42;
+  bool apf = false;
+  float apf_alpha = 0.9f;
+  float apf_threshold = 1e-4f;
+  int apf_every = 1;
+  int device = 0;
+  int mask_threads = 0;
+};
+
+struct StepResult {
+  double loss = 0.0;           // mean over microbatches (last stage on this rank; NaN otherwise)
+  double batch_ms = 0.0;       // device time from start of the first action to end of the last
+  double optimizer_ms = 0.0;
+  double predicted_ms = 0.0;   // LP/DAG makespan for this step's ratios (longest path)
+  int phase = 0;
+  double mean_ratio = 0.0;     // mean realised frozen-unit fraction over this rank's cells
+  long long frozen_units = 0;  // sum over cells
+  long long total_units = 0;   // units * cells
+  double mask_ms = 0.0;        // host time to generate this step's masks
+};
+
+class Trainer {
+ public:
+  Trainer(const ModelConfig& model, const TrainConfig& cfg);
+  ~Trainer();
+
+  // host_tokens / host_targets: [M][T] int32 (pinned or pageable) or null to
+  // use device-resident synthetic tokens.
+  int step(int t, const int* host_tokens, const int* host_targets, StepResult* out);
+
+  void set_override(double ratio) { override_ratio_ = ratio; }
+  void set_plan(const std::vector<double>& ratios);
+  bool has_plan() const { return plan_ready_; }
+  const std::vector<double>& plan_ratios() const { return plan_ratios_; }
+  const pipefreeze::FreezePlan& plan() const { return plan_; }
+  const std::vector<double>& action_ms() const { return action_ms_; }
+  const std::vector<pipefreeze::ActionId>& actions() const { return actions_; }
+  std::vector<Stage*> local_stages();
+  long long tokens_per_step() const;
+  double lp_solve_ms() const { return lp_solve_ms_; }
+  pipefreeze::TimingProfile measured_profile() const;
+  int units_total() const;
+  cudaStream_t stream() const { return stream_; }
+  // this step's frozen-unit masks of local stage li: M masks of (words + 1) uint64 each
+  const uint64_t* masks_host(int li) const { return masks_host_ + mask_offsets_[static_cast<std::size_t>(li)]; }
+
+ private:
+  int local_index(int stage) const;
+  void solve_plan_from_monitoring();
+
+  ModelConfig model_;
+  TrainConfig cfg_;
+  pipefreeze::RankTimeline timeline_;
+  std::unique_ptr<pipefreeze::PipelineDag> dag_;
+  std::vector<pipefreeze::ActionId> actions_;
+  std::vector<int> stage_ids_;                  // local stages (1-based)
+  std::vector<std::unique_ptr<Stage>> stages_;  // parallel to stage_ids_
+  std::vector<int> slots_;                      // per local stage
+  std::vector<std::vector<__nv_bfloat16*>> grad_bufs_;  // [local stage][slot]: dL/d(stage output)
+  cudaStream_t stream_ = nullptr;
+  std::vector<cudaEvent_t> ev_;
+  cudaEvent_t ev_opt0_ = nullptr, ev_opt1_ = nullptr;
+  int* tokens_dev_ = nullptr;
+  int* targets_dev_ = nullptr;
+  float* loss_dev_ = nullptr;
+  uint64_t* masks_dev_ = nullptr;
+  uint64_t* masks_host_ = nullptr;  // pinned
+  std::vector<long long> mask_offsets_;  // words offset per local stage
+  float* loss_host_ = nullptr;           // pinned
+  pipefreeze::MonitorLog monitor_;
+  bool plan_ready_ = false;
+  std::vector<double> plan_ratios_;  // (s-1)*M + (m-1)
+  pipefreeze::FreezePlan plan_;
+  pipefreeze::TimingProfile plan_profile_;
+  double override_ratio_ = -1.0;
+  std::vector<double> action_ms_;
+  double lp_solve_ms_ = 0.0;
+};
+
+}  // namespace pf

@@ -234,9 +234,15 @@ MaskHistory run_freezing_masks(const std::map<ActionId, double>& expected, const
 // ------------------------------------------------------------------ MaskStream
 
 MaskStream::MaskStream(std::vector<double> ratios, PhasePlan phases, int M, int S, int units, std::uint64_t seed)
-    : ratios_(std::move(ratios)), phases_(phases), M_(M), S_(S), units_(units), seed_(seed) {
-  if (static_cast<int>(ratios_.size()) != M * S) throw std::domain_error("mask stream: ratios must have M*S entries");
-  if (units < 0) throw std::domain_error("mask stream: units must be nonnegative");
+    : MaskStream(std::move(ratios), phases, M, std::vector<int>(static_cast<std::size_t>(std::max(S, 0)), units), seed) {}
+
+MaskStream::MaskStream(std::vector<double> ratios, PhasePlan phases, int M, std::vector<int> stage_units,
+                       std::uint64_t seed)
+    : ratios_(std::move(ratios)), phases_(phases), M_(M), S_(static_cast<int>(stage_units.size())),
+      units_(std::move(stage_units)), seed_(seed) {
+  if (static_cast<int>(ratios_.size()) != M_ * S_) throw std::domain_error("mask stream: ratios must have M*S entries");
+  for (int u : units_)
+    if (u < 0) throw std::domain_error("mask stream: units must be nonnegative");
   validate_phase_plan(phases_);
   step_prefix_.push_back(0);
 }
@@ -245,7 +251,7 @@ double MaskStream::ratio(int t, int s, int m) const {
   return cell_ratio(t, phases_, ratios_[static_cast<std::size_t>((s - 1) * M_ + (m - 1))]);
 }
 
-int MaskStream::cell_count(int t, int s, int m) const { return mask_count(units_, ratio(t, s, m)); }
+int MaskStream::cell_count(int t, int s, int m) const { return mask_count(units(s), ratio(t, s, m)); }
 
 void MaskStream::ensure_prefix(int t) const {
   while (static_cast<int>(step_prefix_.size()) < t) {
@@ -271,7 +277,8 @@ std::uint64_t MaskStream::offset(int t, int s, int m) const {
 }
 
 bool MaskStream::stage_step_masks(int t, int s, std::uint64_t* out, int threads) const {
-  const int words = words_per_mask();
+  const int words = words_per_mask(s);
+  const int n = units(s);
   std::vector<std::uint64_t> base(static_cast<std::size_t>(M_));
   std::vector<int> counts(static_cast<std::size_t>(M_));
   for (int m = 1; m <= M_; ++m) {
@@ -288,8 +295,8 @@ bool MaskStream::stage_step_masks(int t, int s, std::uint64_t* out, int threads)
       return;
     }
     Rng rng = Rng::at_offset(seed_, draw_offset);
-    auto& pool = scratch_pool(units_);
-    used[static_cast<std::size_t>(mi)] = partial_shuffle(pool.data(), units_, k, rng);
+    auto& pool = scratch_pool(n);
+    used[static_cast<std::size_t>(mi)] = partial_shuffle(pool.data(), n, k, rng);
     fill_words(pool.data(), k, w, words);
   };
   const int nthreads = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));

@@ -119,6 +119,10 @@ class MaskStream {
  public:
   MaskStream(std::vector<double> expected_ratios /* (s-1)*M + (m-1) */, PhasePlan phases,
              int num_microbatches, int total_stages, int units, std::uint64_t seed);
+  // Generalisation for stages of different sizes (unit count per stage); with
+  // equal counts it is the reference stream.
+  MaskStream(std::vector<double> expected_ratios, PhasePlan phases, int num_microbatches,
+             std::vector<int> stage_units, std::uint64_t seed);
 
   // RNG draws consumed by all cells strictly before (t, s, m).
   std::uint64_t offset(int t, int s, int m) const;
@@ -130,14 +134,15 @@ class MaskStream {
   // event forced a sequential replay (result is still exact).
   bool stage_step_masks(int t, int s, std::uint64_t* words_out, int threads = 0) const;
 
-  int units() const { return units_; }
-  int words_per_mask() const { return (units_ + 63) / 64; }
+  int units(int s = 1) const { return units_[static_cast<std::size_t>(s - 1)]; }
+  int words_per_mask(int s = 1) const { return (units(s) + 63) / 64; }
 
  private:
   void ensure_prefix(int t) const;
   std::vector<double> ratios_;
   PhasePlan phases_;
-  int M_, S_, units_;
+  int M_, S_;
+  std::vector<int> units_;
   std::uint64_t seed_;
   mutable std::vector<std::uint64_t> step_prefix_;  // draws before step t (index t-1)
 };

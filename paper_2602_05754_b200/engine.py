@@ -1,0 +1,208 @@
+"""Python handle on the device stage engine (libpf_device.so, include/pf_device.h).
+
+`Trainer` drives Alg. 1 for one rank: schedule/DAG/LP/controller in the host C++
+layer, the LLaMA-shaped stage step in hand-written sm_100a kernels. There is no
+Python or CPU compute path: every method calls the native library.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+from . import _native
+from ._device_sigs import PfModelCfg, PfStepResult, PfTrainCfg, PfTrainerInfo
+from .pipefreeze import KINDS
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    hidden: int
+    ffn: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    vocab: int
+    layers: int
+    seq: int
+    micro_batch: int
+    rope_theta: float = 500000.0
+    norm_eps: float = 1e-5
+    init_std: float = 0.02
+
+    @property
+    def tokens(self) -> int:
+        return self.seq * self.micro_batch
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    def matmul_params_per_layer(self) -> int:
+        h = self.hidden
+        return self.qkv_dim * h + h * self.n_heads * self.head_dim + 2 * self.ffn * h + h * self.ffn
+
+
+PRESETS = {
+    # unit tests / CPU-oracle parity (config 1 model step)
+    "tiny": ModelShape(256, 512, 4, 2, 64, 1024, 4, 128, 2),
+    # LLaMA-3.2-1B shapes (BASELINE configs[1]); untied LM head
+    "llama-1b": ModelShape(2048, 8192, 32, 8, 64, 128256, 16, 2048, 2),
+    # LLaMA-3-8B shapes (configs[2])
+    "llama-8b": ModelShape(4096, 14336, 32, 8, 128, 128256, 32, 2048, 2),
+    # LLaMA-2-13B shapes (configs[3])
+    "llama-13b": ModelShape(5120, 13824, 40, 40, 128, 32000, 40, 2048, 1, rope_theta=10000.0),
+}
+
+
+def stage_layers(layers: int, S: int, s: int) -> tuple[int, int]:
+    """Layers [begin, end) of 1-based stage s; the first L % S stages take one extra (trainer.cpp stage_spec)."""
+    base, extra = divmod(layers, S)
+    begin = (s - 1) * base + min(s - 1, extra)
+    return begin, begin + base + (1 if s - 1 < extra else 0)
+
+
+def param_layout(shape: ModelShape, s: int, S: int) -> dict:
+    """Offsets of every parameter in a stage's flat buffers (mirror of Stage's constructor)."""
+    align = 64
+    off = 0
+    out = {"units": [], "dense": []}
+
+    def add(name, rows, cols, freezable):
+        nonlocal off
+        ent = dict(name=name, offset=off, rows=rows, cols=cols, freezable=freezable)
+        off = (off + rows * cols + align - 1) // align * align
+        (out["units"] if freezable else out["dense"]).append(ent)
+        return ent
+
+    b, e = stage_layers(shape.layers, S, s)
+    h = shape.hidden
+    for layer in range(b, e):
+        add(f"l{layer}.wqkv", shape.qkv_dim, h, True)
+        add(f"l{layer}.wo", h, shape.n_heads * shape.head_dim, True)
+        add(f"l{layer}.wgu", 2 * shape.ffn, h, True)
+        add(f"l{layer}.wd", h, shape.ffn, True)
+    if s == S:
+        add("wlm", shape.vocab, h, True)
+    for layer in range(b, e):
+        add(f"l{layer}.g1", 1, h, False)
+        add(f"l{layer}.g2", 1, h, False)
+    if s == S:
+        add("gf", 1, h, False)
+    if s == 1:
+        add("emb", shape.vocab, h, False)
+    u = 0
+    for ent in out["units"]:
+        ent["unit_offset"] = u
+        ent["tiles_n"] = (ent["cols"] + 127) // 128
+        ent["units"] = ((ent["rows"] + 127) // 128) * ent["tiles_n"]
+        u += ent["units"]
+    out["n_units"] = u
+    out["n_params"] = off
+    return out
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        lib = _native.device()
+        msg = lib.pf_engine_last_error().decode() or lib.pf_device_last_error().decode()
+        raise _native.PfError(rc, f"{what} failed with status {rc}: {msg}")
+
+
+class Trainer:
+    """One rank of the TimelyFreeze pipeline step on the local GPU."""
+
+    def __init__(self, shape: ModelShape, schedule: str = "gpipe", ranks: int = 1, stages_per_rank: int = 1,
+                 microbatches: int = 8, rank: int = 0, phases=(2, 8, 10, 20), r_max: float = 0.8, lr: float = 1e-3,
+                 seed: int = 42, apf: bool = False, apf_alpha: float = 0.9, apf_threshold: float = 1e-4,
+                 apf_every: int = 1, device: int = 0, mask_threads: int = 0):
+        self.lib = _native.device()
+        self.shape = shape
+        self.M = microbatches
+        self.S = ranks * stages_per_rank
+        m = PfModelCfg(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.vocab,
+                       shape.layers, shape.seq, shape.micro_batch, shape.rope_theta, shape.norm_eps, shape.init_std)
+        c = PfTrainCfg()
+        c.kind = KINDS[schedule]
+        c.ranks, c.stages_per_rank, c.microbatches, c.rank = ranks, stages_per_rank, microbatches, rank
+        c.phases[:] = list(phases)
+        c.r_max, c.lr, c.seed = r_max, lr, seed
+        c.apf, c.apf_every, c.apf_alpha, c.apf_threshold = int(apf), apf_every, apf_alpha, apf_threshold
+        c.device, c.mask_threads = device, mask_threads
+        self.phases = tuple(phases)
+        self._ctx = ctypes.c_void_p()
+        _check(self.lib.pf_trainer_create(ctypes.byref(m), ctypes.byref(c), ctypes.byref(self._ctx)), "trainer_create")
+        self.info = self.get_info()
+
+    def close(self) -> None:
+        if self._ctx:
+            self.lib.pf_trainer_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, t: int, tokens: np.ndarray | None = None, targets: np.ndarray | None = None) -> dict:
+        r = PfStepResult()
+        tp = tokens.ctypes.data_as(ctypes.c_void_p) if tokens is not None else None
+        gp = targets.ctypes.data_as(ctypes.c_void_p) if targets is not None else None
+        _check(self.lib.pf_trainer_step(self._ctx, t, tp, gp, ctypes.byref(r)), f"trainer_step(t={t})")
+        return {k: getattr(r, k) for k, _ in PfStepResult._fields_}
+
+    def set_override(self, ratio: float | None) -> None:
+        _check(self.lib.pf_trainer_set_override(self._ctx, -1.0 if ratio is None else float(ratio)), "set_override")
+
+    def set_plan(self, ratios) -> None:
+        r = np.ascontiguousarray(ratios, dtype=np.float64)
+        _check(self.lib.pf_trainer_set_plan(self._ctx, r.ctypes.data_as(ctypes.c_void_p)), "set_plan")
+
+    def get_plan(self):
+        ratios = np.zeros(self.S * self.M)
+        out3 = np.zeros(3)
+        wmin = np.zeros(2 * self.S * self.M)
+        wmax = np.zeros(2 * self.S * self.M)
+        rc = self.lib.pf_trainer_get_plan(self._ctx, *(a.ctypes.data_as(ctypes.c_void_p) for a in (ratios, out3, wmin, wmax)))
+        if rc == _native.PF_ERR_DOMAIN:
+            return None
+        _check(rc, "get_plan")
+        return dict(ratios=ratios, makespan_base=out3[0], makespan_opt=out3[1], makespan_floor=out3[2],
+                    w_min=wmin, w_max=wmax)
+
+    def action_ms(self):
+        n = self.info["actions"]
+        ms = np.zeros(n)
+        kinds = np.zeros(n, dtype=np.int32)
+        mbs = np.zeros(n, dtype=np.int32)
+        st = np.zeros(n, dtype=np.int32)
+        _check(self.lib.pf_trainer_action_ms(self._ctx, *(a.ctypes.data_as(ctypes.c_void_p) for a in (ms, kinds, mbs, st))),
+               "action_ms")
+        return ms, kinds, mbs, st
+
+    def get_info(self) -> dict:
+        i = PfTrainerInfo()
+        _check(self.lib.pf_trainer_get_info(self._ctx, ctypes.byref(i)), "get_info")
+        return {k: getattr(i, k) for k, _ in PfTrainerInfo._fields_}
+
+    def stage_buffers(self, local_stage: int = 0) -> dict:
+        ptrs = [ctypes.c_void_p() for _ in range(4)]
+        n = ctypes.c_longlong()
+        u = ctypes.c_int()
+        _check(self.lib.pf_trainer_stage_buffers(self._ctx, local_stage, *(ctypes.byref(p) for p in ptrs),
+                                                 ctypes.byref(n), ctypes.byref(u)), "stage_buffers")
+        return dict(master=ptrs[0].value, weights=ptrs[1].value, grad=ptrs[2].value, stamps=ptrs[3].value,
+                    n_params=n.value, n_units=u.value)
+
+    def last_masks(self, local_stage: int = 0) -> np.ndarray:
+        units = self.stage_buffers(local_stage)["n_units"]
+        words = (units + 63) // 64
+        out = np.zeros((self.M, words), dtype=np.uint64)
+        _check(self.lib.pf_trainer_last_masks(self._ctx, local_stage, out.ctypes.data_as(ctypes.c_void_p)), "last_masks")
+        return out
+
+
+def shape_dict(shape: ModelShape) -> dict:
+    return asdict(shape)

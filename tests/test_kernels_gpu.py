@@ -1,0 +1,222 @@
+"""K4/K5/K6/K7 device kernels vs a plain PyTorch fp32 reference or the golden oracle vectors."""
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def lib():
+    from paper_2602_05754_b200 import _native
+
+    return _native.device()
+
+
+def chk(rc, what=""):
+    assert rc == 0, f"{what}: {rc} {lib().pf_engine_last_error().decode()}"
+
+
+def sp():
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def bf(x):
+    import torch
+
+    return x.to(torch.bfloat16)
+
+
+def test_rmsnorm_fwd_bwd(cuda):
+    import torch
+
+    T, h = 256, 1024
+    g = torch.Generator().manual_seed(1)
+    x = bf(torch.randn(T, h, generator=g)).cuda()
+    w = bf(1 + 0.1 * torch.randn(h, generator=g)).cuda()
+    dy = bf(torch.randn(T, h, generator=g)).cuda()
+    res = bf(torch.randn(T, h, generator=g)).cuda()
+    y = torch.empty_like(x)
+    rstd = torch.empty(T, device=cuda)
+    chk(lib().pf_rmsnorm_fwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), rstd.data_ptr(), T, h, 1e-5, sp()))
+    xf = x.float().requires_grad_(True)
+    wf = w.float().requires_grad_(True)
+    ref = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * wf
+    torch.cuda.synchronize()
+    assert (y.float() - ref).abs().max().item() < 2e-2 * ref.abs().max().item()
+    ref.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(h, device=cuda)
+    chk(lib().pf_rmsnorm_bwd(x.data_ptr(), w.data_ptr(), rstd.data_ptr(), dy.data_ptr(), res.data_ptr(), dx.data_ptr(),
+                             dg.data_ptr(), T, h, sp()))
+    torch.cuda.synchronize()
+    exp = xf.grad + res.float()
+    assert (dx.float() - exp).abs().max().item() < 2e-2 * exp.abs().max().item()
+    assert torch.allclose(dg, wf.grad, rtol=1e-3, atol=1e-3 * wf.grad.abs().max().item())
+
+
+def test_swiglu_fwd_bwd(cuda):
+    import torch
+    import torch.nn.functional as F
+
+    T, ffn = 256, 512
+    g = torch.Generator().manual_seed(2)
+    gu = bf(torch.randn(T, 2 * ffn, generator=g)).cuda()
+    da = bf(torch.randn(T, ffn, generator=g)).cuda()
+    a = torch.empty(T, ffn, dtype=torch.bfloat16, device=cuda)
+    chk(lib().pf_swiglu_fwd(gu.data_ptr(), a.data_ptr(), T, ffn, sp()))
+    guf = gu.float().requires_grad_(True)
+    ref = F.silu(guf[:, :ffn]) * guf[:, ffn:]
+    ref.backward(da.float())
+    dgu = torch.empty_like(gu)
+    chk(lib().pf_swiglu_bwd(gu.data_ptr(), da.data_ptr(), dgu.data_ptr(), T, ffn, sp()))
+    torch.cuda.synchronize()
+    assert (a.float() - ref).abs().max().item() < 1e-2 * ref.abs().max().item() + 1e-2
+    assert (dgu.float() - guf.grad).abs().max().item() < 1e-2 * guf.grad.abs().max().item() + 1e-2
+
+
+def test_rope_matches_reference(cuda):
+    import torch
+
+    from llama_ref import rope
+
+    B, S, nh, nkv, hd = 2, 64, 4, 2, 64
+    T = B * S
+    W = (nh + 2 * nkv) * hd
+    g = torch.Generator().manual_seed(3)
+    qkv = bf(torch.randn(T, W, generator=g)).cuda()
+    ref = qkv.float().view(B, S, nh + 2 * nkv, hd).clone()
+    ref[:, :, : nh + nkv] = rope(ref[:, :, : nh + nkv], S, 500000.0)
+    chk(lib().pf_rope_fwd(qkv.data_ptr(), T, S, nh, nkv, hd, 500000.0, sp()))
+    torch.cuda.synchronize()
+    assert (qkv.float().view_as(ref) - ref).abs().max().item() < 2e-2
+
+
+def test_cross_entropy_fused(cuda):
+    import torch
+    import torch.nn.functional as F
+
+    T, V = 128, 4096
+    g = torch.Generator().manual_seed(4)
+    logits = bf(3 * torch.randn(T, V, generator=g)).cuda()
+    tgt = torch.randint(0, V, (T,), generator=g).int().cuda()
+    lf = logits.float().requires_grad_(True)
+    loss = F.cross_entropy(lf, tgt.long())
+    loss.backward()
+    ls = torch.zeros(1, device=cuda)
+    chk(lib().pf_cross_entropy(logits.data_ptr(), tgt.data_ptr(), ls.data_ptr(), T, V, 1.0 / T, 1.0 / T, sp()))
+    torch.cuda.synchronize()
+    assert abs(ls.item() - loss.item()) < 1e-3 * loss.item()
+    assert (logits.float() - lf.grad).abs().max().item() < 2e-2 * lf.grad.abs().max().item()
+
+
+def test_apf_update_vs_reference_golden(cuda):
+    """K4 fp32 on device vs the reference's fp64 apf_update (freezectl.cpp:147-156)."""
+    import torch
+
+    with open(os.path.join(GOLD, "apf.json")) as f:
+        cases = json.load(f)
+    for case in cases:
+        n = case["n"]
+        d = np.array([float.fromhex(x) for x in case["deltas"]]).reshape(-1, n)
+        e = torch.zeros(n, device=cuda)
+        ea = torch.zeros(n, device=cuda)
+        sc = torch.zeros(n, device=cuda)
+        for row in d:
+            dd = torch.tensor(row, dtype=torch.float32, device=cuda)
+            chk(lib().pf_apf_update(e.data_ptr(), ea.data_ptr(), dd.data_ptr(), sc.data_ptr(), n, case["alpha"], sp()))
+        torch.cuda.synchronize()
+        ref_e = np.array([float.fromhex(x) for x in case["ema"]])
+        ref_a = np.array([float.fromhex(x) for x in case["ema_abs"]])
+        ref_s = np.array([float.fromhex(x) for x in case["scores"]])
+        np.testing.assert_allclose(e.cpu().numpy(), ref_e, rtol=2e-5, atol=1e-12)
+        np.testing.assert_allclose(ea.cpu().numpy(), ref_a, rtol=2e-5, atol=1e-12)
+        np.testing.assert_allclose(sc.cpu().numpy(), ref_s, rtol=1e-4, atol=1e-6)
+
+
+def _unit_table(shapes):
+    """pf_unit_matrix table for matrices laid out back to back (64-element aligned)."""
+    dt = np.dtype([("elem_offset", "<i8"), ("rows", "<i4"), ("cols", "<i4"), ("unit_offset", "<i4"),
+                   ("tiles_n", "<i4"), ("units", "<i4"), ("pad", "<i4")])
+    tab = np.zeros(len(shapes), dtype=dt)
+    off = u = 0
+    for i, (r, c) in enumerate(shapes):
+        tn = (c + 127) // 128
+        units = ((r + 127) // 128) * tn
+        tab[i] = (off, r, c, u, tn, units, 0)
+        off = (off + r * c + 63) // 64 * 64
+        u += units
+    return tab, off, u
+
+
+def test_mask_to_unit_lists_matches_numpy(cuda):
+    import torch
+
+    from paper_2602_05754_b200 import pipefreeze as pf
+
+    tab, _, U = _unit_table([(384, 256), (256, 640), (1000, 128), (128, 128)])
+    words = pf.sample_masks(7, U, [0.55])[0]
+    w = np.concatenate([words, np.zeros(1, dtype=np.uint64)])
+    wd = torch.tensor(w.view(np.int64), device=cuda)
+    td = torch.tensor(tab.view(np.uint8), device=cuda)
+    lists = torch.full((U + 64,), -1, dtype=torch.int32, device=cuda)
+    counts = torch.zeros(len(tab), dtype=torch.int32, device=cuda)
+    chk(lib().pf_mask_to_unit_lists(wd.data_ptr(), td.data_ptr(), len(tab), lists.data_ptr(), counts.data_ptr(), sp()))
+    torch.cuda.synchronize()
+    frozen = pf.unpack_mask(words, U)
+    L = lists.cpu().numpy()
+    for i, ent in enumerate(tab):
+        lo, n = int(ent["unit_offset"]), int(ent["units"])
+        expect = [j for j in range(n) if not frozen[lo + j]]
+        assert counts[i].item() == len(expect)
+        assert L[lo:lo + len(expect)].tolist() == expect
+
+
+def test_masked_sgd_units_and_fused_apf(cuda):
+    """theta -= scale*G only on touched units (stamp == step); APF advances every unit."""
+    import torch
+
+    tab, nparam, U = _unit_table([(256, 384), (128, 256)])
+    g = torch.Generator().manual_seed(9)
+    master = torch.randn(nparam, generator=g).cuda()
+    weights = master.to(torch.bfloat16)
+    grad = torch.randn(nparam, generator=g).cuda()
+    stamps = torch.zeros(U, dtype=torch.int32)
+    touched = [0, 2, 3, 6, 7]
+    stamps[touched] = 5
+    stamps = stamps.cuda()
+    ema = torch.zeros(nparam, device=cuda)
+    ema_abs = torch.zeros(nparam, device=cuda)
+    elig = torch.zeros(U, dtype=torch.int32, device=cuda)
+    td = torch.tensor(tab.view(np.uint8), device=cuda)
+    m0 = master.clone()
+    scale = 0.01
+    chk(lib().pf_masked_sgd_units(master.data_ptr(), weights.data_ptr(), grad.data_ptr(), stamps.data_ptr(), 5, scale,
+                                  td.data_ptr(), len(tab), U, ema.data_ptr(), ema_abs.data_ptr(), 0.9, 0.5,
+                                  elig.data_ptr(), sp()))
+    torch.cuda.synchronize()
+    # expected: numpy restatement of sandbox.cpp:250 per unit
+    m_exp = m0.cpu().numpy().copy()
+    e_exp = np.zeros(nparam, dtype=np.float32)
+    gnp = grad.cpu().numpy()
+    for ent in tab:
+        for lu in range(int(ent["units"])):
+            u = int(ent["unit_offset"]) + lu
+            rb, cb = divmod(lu, int(ent["tiles_n"]))
+            for r in range(rb * 128, min(int(ent["rows"]), rb * 128 + 128)):
+                s = int(ent["elem_offset"]) + r * int(ent["cols"]) + cb * 128
+                e = s + min(128, int(ent["cols"]) - cb * 128)
+                if u in touched:
+                    m_exp[s:e] -= scale * gnp[s:e]
+                    e_exp[s:e] = 0.1 * (-scale * gnp[s:e])
+    np.testing.assert_allclose(master.cpu().numpy(), m_exp, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(ema.cpu().numpy(), e_exp, rtol=1e-5, atol=1e-9)
+    assert torch.equal(weights, master.to(torch.bfloat16))
+    # untouched units: score = 1 (E_abs == 0) -> not eligible; touched: |E|/E_abs = 1 -> not eligible (thr 0.5)
+    assert elig.sum().item() == 0
