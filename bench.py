@@ -1,0 +1,370 @@
+"""Benchmark: TimelyFreeze pipeline training step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model llama-1b]
+
+Workload (BASELINE.json configs[1], the single-GPU-sized config): LLaMA-3.2-1B-shaped
+decoder, GPipe, PP = N (N=1: one stage holds all 16 layers), M = 8 microbatches of
+2 x 2048 tokens, synthetic uniform tokens and N(0, 0.02) random-init weights.
+
+Procedure (ours): run the Alg. 1 controller untimed through warm-up, the two
+monitoring halves (CUDA-event action times), the LP solve at T_m and the AFR ramp,
+then W stable-phase warm-up steps, then K timed stable-phase steps (device time,
+CUDA events on the trainer's stream, max over ranks). The same K steps are timed
+with every unit unfrozen (no-freeze) for the speed-up, and once more end-to-end
+through the C-ABI with host (pinned) token buffers (e2e).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/sec per PP step at 1/2/4/8 B200 vs no-freeze; batch time vs LP makespan"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        load = [s for s in sm if s > 500] or sm
+        reasons = set()
+        for r in rows:
+            for name, col in (("hw_slowdown", 5), ("hw_thermal_slowdown", 6), ("sw_thermal_slowdown", 7), ("sw_power_cap", 8)):
+                if r[col].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": float(rows[0][2]),
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def step_flops(shape, M: int, mean_ratio: float, S: int = 1) -> dict:
+    """Algorithmic FLOPs of one step: matmul fwd 2TP, dX 2TP, dW (1-r) 2TP, causal attention fwd 2Tsh and bwd 5Tsh."""
+    T = shape.tokens
+    P = shape.layers * shape.matmul_params_per_layer() + shape.vocab * shape.hidden
+    mm = 2 * T * P
+    attn_f = 2.0 * T * shape.seq * shape.n_heads * shape.head_dim * shape.layers  # causal: half of 4Tsh
+    attn_b = 2.5 * attn_f
+    return {"fwd": M * (mm + attn_f), "dx": M * (mm + attn_b), "dw": M * mm * (1.0 - mean_ratio)}
+
+
+def gemm_roofline(peaks: dict, shape, iters: int = 20) -> dict:
+    """Dominant kernel: the K1 tcgen05 GEMM at the stage's largest per-layer shape (gate|up forward),
+    timed live with CUDA events on the launching stream."""
+    import torch
+
+    from paper_2602_05754_b200 import _native
+
+    lib = _native.device()
+    T, h, N = shape.tokens, shape.hidden, 2 * shape.ffn
+    A = torch.randn(T, h, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, h, device="cuda").to(torch.bfloat16)
+    C = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        sp = s.cuda_stream
+        for _ in range(3):
+            _native.check(lib.pf_gemm_bf16(A.data_ptr(), 0, h, B.data_ptr(), 0, h, C.data_ptr(), N, T, N, h, 1.0, 0, 256, None, 0, sp), "gemm")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(iters):
+            lib.pf_gemm_bf16(A.data_ptr(), 0, h, B.data_ptr(), 0, h, C.data_ptr(), N, T, N, h, 1.0, 0, 256, None, 0, sp)
+        e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    flops = 2.0 * T * N * h
+    achieved = flops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": f"gemm_tcgen05 fwd {T}x{N}x{h} (K1, gate|up)", "achieved": round(achieved, 1),
+            "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
+            "traffic": None, "avg_launch_ms": round(ms, 4), "peak_source": peaks["source"]}
+
+
+def cpu_reference_step(shape, M: int, S: int, units: int, n_params: int, ratio: float, budget_s: float = 12.0):
+    """Reference CPU path (oracle/_ref: the unmodified reference compiled here) for one step of this
+    workload: schedule + DAG + longest path, S*M exact-count masks over the stage units, apf_update and
+    the masked SGD update over the stage parameters. The per-parameter part runs on a bounded sample
+    and is scaled linearly to the full parameter count."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref  # noqa: E402  (oracle: reference arm / cpu_baseline only)
+
+    if not ref.available():
+        raise RuntimeError("oracle/_ref/libpfref.so is not built")
+    d1, d2 = 2_000_000, 8_000_000
+    t1 = min(ref.cpu_step_seconds("gpipe", S, 1, M, units, d1, ratio) for _ in range(2))
+    t2 = min(ref.cpu_step_seconds("gpipe", S, 1, M, units, d2, ratio) for _ in range(2))
+    per_param = max(0.0, (t2 - t1) / (d2 - d1))
+    fixed = max(0.0, t1 - per_param * d1)
+    est = fixed + per_param * n_params
+    return est, {"fixed_s": fixed, "per_param_ns": per_param * 1e9, "sample_params": [d1, d2],
+                 "sample": f"reference step (schedule+DAG+longest path, {S * M} sample_mask over {units} units, "
+                           f"apf_update + masked SGD) on {d1:,} and {d2:,} params, scaled linearly to {n_params:,} params"}
+
+
+def run_reference(args) -> None:
+    from paper_2602_05754_b200.engine import PRESETS
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    shape = PRESETS[args.model]
+    M = args.microbatches
+    S = args.gpus
+    units = _units_for(shape, S)
+    n_params = shape.layers * shape.matmul_params_per_layer() // S + shape.vocab * shape.hidden
+    step_s, info = cpu_reference_step(shape, M, S, units, n_params, 0.8 * 0.8)
+    timed = []
+    for _ in range(args.warmup):
+        cpu_reference_step(shape, M, S, units, n_params, 0.64)
+    for _ in range(args.steps):
+        s, _ = cpu_reference_step(shape, M, S, units, n_params, 0.64)
+        timed.append(s)
+    step_s = statistics.mean(timed) if timed else step_s
+    tokens = M * shape.tokens
+    value = tokens / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(args, shape),
+            "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": 1, "kind": "reference",
+                             "sample": info["sample"]},
+            "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "the reference has no transformer math; its step is the CPU stand-in (controller masks, APF, masked SGD)"}
+    print(json.dumps(line), flush=True)
+
+
+def _units_for(shape, S: int) -> int:
+    from paper_2602_05754_b200.engine import param_layout
+
+    return param_layout(shape, S, S)["n_units"] if S >= 1 else 0
+
+
+def _config(args, shape) -> dict:
+    return {"workload": f"{args.model}-shaped {args.schedule} PP={args.gpus} (BASELINE configs[1])",
+            "model": args.model, "hidden": shape.hidden, "layers": shape.layers, "ffn": shape.ffn,
+            "heads": shape.n_heads, "kv_heads": shape.n_kv_heads, "vocab": shape.vocab,
+            "global_batch": args.microbatches * shape.micro_batch, "seq_len": shape.seq,
+            "microbatches": args.microbatches, "micro_batch": shape.micro_batch, "schedule": args.schedule,
+            "parallelism": f"pp{args.gpus}", "r_max": args.r_max, "phases": list(args.phases),
+            "l2": "inputs larger than L2 (>2 GB of weights and activations touched per step)"}
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_2602_05754_b200 import _native
+    from paper_2602_05754_b200.engine import PRESETS, Trainer
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    shape = PRESETS[args.model]
+    M = args.microbatches
+    phases = tuple(args.phases)
+    tr = Trainer(shape, args.schedule, world, 1, M, rank=rank, phases=phases, r_max=args.r_max, lr=1e-4,
+                 seed=args.seed, device=local)
+    lib = _native.device()
+    stream = torch.cuda.ExternalStream(lib.pf_trainer_stream(tr._ctx))
+    tokens_per_step = M * shape.tokens
+
+    # ---- controller: warm-up, monitoring, LP solve, ramp (untimed)
+    t = 0
+    ctl = []
+    for t in range(1, phases[2] + 1):
+        ctl.append(tr.step(t))
+    plan = tr.get_plan()
+
+    def timed_steps(start_t: int, k: int, host=None):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        res = []
+        c0 = lib.pf_device_launch_count()
+        e0.record(stream)
+        w0 = time.perf_counter()
+        for i in range(k):
+            if host is not None:
+                res.append(tr.step(start_t + i, host[0], host[1]))
+            else:
+                res.append(tr.step(start_t + i))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        launches = lib.pf_device_launch_count() - c0
+        return e0.elapsed_time(e1), wall, res, launches
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        v = torch.tensor([x], device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return v.item()
+
+    # ---- stable freeze: warm-up then timed
+    t = phases[2] + 1
+    for i in range(args.warmup):
+        tr.step(t + i)
+    t += args.warmup
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        dev_ms, wall_s, res, launches = timed_steps(t, args.steps)
+    t += args.steps
+    dev_ms = max_over_ranks(dev_ms)
+    ms_step = dev_ms / args.steps
+    value = tokens_per_step / (ms_step * 1e-3)
+
+    # ---- no-freeze comparison (same steps, every unit updated)
+    tr.set_override(0.0)
+    for i in range(max(1, args.warmup // 2)):
+        tr.step(t + i)
+    t += max(1, args.warmup // 2)
+    nf_ms, _, nf_res, _ = timed_steps(t, args.steps)
+    t += args.steps
+    nf_ms = max_over_ranks(nf_ms) / args.steps
+    tr.set_override(None)
+
+    # ---- e2e through the C-ABI with host (pinned) token buffers; loss read back each step
+    T = shape.tokens
+    host_tok = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32).pin_memory()
+    host_tgt = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32).pin_memory()
+    hp = (host_tok.numpy(), host_tgt.numpy())
+    e2e_dev, e2e_wall, e2e_res, _ = timed_steps(t, args.steps, host=hp)
+    t += args.steps
+    e2e_wall = max_over_ranks(e2e_wall)
+    words = sum(((u + 63) // 64 + 1) for u in [tr.stage_buffers(0)["n_units"]]) * M
+    h2d = 2 * M * T * 4 + words * 8
+
+    peaks = load_peaks() if rank == 0 else None
+    if rank == 0:
+        mean_ratio = statistics.mean(r["mean_ratio"] for r in res)
+        fl = step_flops(shape, M, mean_ratio)
+        total_flops = sum(fl.values())
+        batch_ms = statistics.mean(r["batch_ms"] for r in res)
+        pred_ms = statistics.mean(r["predicted_ms"] for r in res)
+        roof = gemm_roofline(peaks, shape)
+        try:
+            units = tr.stage_buffers(0)["n_units"]
+            cpu_s, cpu_info = cpu_reference_step(shape, M, world, units, tr.info["params"], mean_ratio)
+            cpu = {"value": round(tokens_per_step / cpu_s, 2), "unit": "tokens/s", "cores": 1, "kind": "reference",
+                   "sample": cpu_info["sample"]}
+        except Exception as e:  # pragma: no cover - oracle missing on the box
+            cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, N(0,0.02) random-init weights)",
+            "config": _config(args, shape),
+            "nofreeze": {"value": round(tokens_per_step / (nf_ms * 1e-3), 1), "ms_per_step": round(nf_ms, 3)},
+            "freeze_speedup": round(nf_ms / ms_step, 4),
+            "batch_vs_lp": {"batch_ms": round(batch_ms, 3), "lp_makespan_ms": round(pred_ms, 3),
+                            "ratio": round(batch_ms / pred_ms, 4) if pred_ms else None,
+                            "plan_makespan_base_ms": round(plan["makespan_base"], 3) if plan else None,
+                            "plan_makespan_opt_ms": round(plan["makespan_opt"], 3) if plan else None,
+                            "plan_mean_ratio": round(float(plan["ratios"].mean()), 4) if plan else None,
+                            "lp_solve_ms": round(tr.get_info()["lp_solve_ms"], 3)},
+            "realised_frozen_fraction": round(mean_ratio, 4),
+            "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 1),
+            "mfu_of_measured_peak": round(total_flops / (ms_step * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"], 4),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(tokens_per_step * args.steps / e2e_wall, 1), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "loss": {"first": round(ctl[0]["loss"], 4), "last": round(res[-1]["loss"], 4)},
+        }
+        print(json.dumps(line), flush=True)
+    tr.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="llama-1b")
+    ap.add_argument("--schedule", default="gpipe")
+    ap.add_argument("--microbatches", type=int, default=8)
+    ap.add_argument("--r-max", type=float, default=0.8)
+    ap.add_argument("--phases", type=int, nargs=4, default=[2, 8, 10, 10000])
+    ap.add_argument("--seed", type=int, default=42)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -134,6 +134,10 @@ int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
 /* Raw buffers of local stage i (tests): fp32 master / grad, bf16 weights, unit stamps, device unit table. */
 int pf_trainer_stage_buffers(pf_ctx* ctx, int local_stage, void** master, void** weights, void** grad,
                              void** stamps, long long* n_params, int* n_units);
+/* The cudaStream_t the trainer enqueues its step on (for device-side timing by the caller). */
+void* pf_trainer_stream(pf_ctx* ctx);
+/* Kernels launched by this library so far (all hand-written kernels, not the ATen attention). */
+long long pf_device_launch_count(void);
 /* The last step's frozen-unit masks of local stage i: M masks of ceil(units/64) words. */
 int pf_trainer_last_masks(pf_ctx* ctx, int local_stage, uint64_t* out);
 

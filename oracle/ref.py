@@ -32,7 +32,7 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(LIB_PATH)
         L.ref_last_error.restype = ctypes.c_char_p
         L.ref_cpu_step.restype = ctypes.c_double
-        L.ref_cpu_step.argtypes = [ctypes.c_int] * 6 + [ctypes.c_long, ctypes.c_double, ctypes.c_uint64]
+        L.ref_cpu_step.argtypes = [ctypes.c_int] * 5 + [ctypes.c_long, ctypes.c_double, ctypes.c_uint64]
         _lib = L
     return _lib
 

@@ -57,6 +57,8 @@ DEVICE_SIGNATURES = {
     "pf_trainer_stage_buffers": ([c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                   ctypes.POINTER(c_vp), ctypes.POINTER(c_ll), ctypes.POINTER(c_int)], c_int),
     "pf_trainer_last_masks": ([c_vp, c_int, c_vp], c_int),
+    "pf_trainer_stream": ([c_vp], c_vp),
+    "pf_device_launch_count": ([], c_ll),
 }
 
 

@@ -317,3 +317,5 @@ int pf_trainer_last_masks(pf_ctx* ctx, int i, uint64_t* out) {
 }
 
 }  // extern "C"
+
+extern "C" void* pf_trainer_stream(pf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->trainer->stream()) : nullptr; }

@@ -47,3 +47,15 @@ int pf_device_sm_count(void) { return pf::num_sms(); }
 const char* pf_device_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"
+
+#include <atomic>
+
+namespace pf {
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+}  // namespace pf
+
+extern "C" long long pf_device_launch_count(void) { return pf::launch_count(); }

@@ -363,6 +363,7 @@ int launch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int grid_li
   int grid = std::min(grid_limit, num_sms());
   if (grid <= 0) return PF_OK;
   kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, p);
+  count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
 }
 

@@ -26,7 +26,10 @@ int grid_for(long long work_items, int per_sm = 8) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
-int status() { return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA; }
+int status() {
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -442,7 +445,8 @@ __global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __
   }
   // combine (max, sum) across the block
   float wm = warp_max(mx);
-  float ws = warp_sum(sum * __expf(mx - wm));
+  // threads (or whole warps) without elements carry mx = -inf, sum = 0
+  float ws = warp_sum(mx == -INFINITY ? 0.f : sum * __expf(mx - wm));
   if (lane == 0) {
     sm[warp] = wm;
     ss[warp] = ws;
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __
   float bm = -INFINITY;
   for (int w = 0; w < kBlock / 32; ++w) bm = fmaxf(bm, sm[w]);
   float bs = 0.f;
-  for (int w = 0; w < kBlock / 32; ++w) bs += ss[w] * __expf(sm[w] - bm);
+  for (int w = 0; w < kBlock / 32; ++w) bs += sm[w] == -INFINITY ? 0.f : ss[w] * __expf(sm[w] - bm);
   const float lse = bm + __logf(bs);
   const int tgt = targets[t];
   const float xt = __bfloat162float(row[tgt]);

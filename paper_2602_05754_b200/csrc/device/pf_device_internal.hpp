@@ -39,4 +39,8 @@ int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C
 
 int num_sms();
 
+// Number of kernels this library has launched (evidence for bench.py gpu_launches).
+void count_launch();
+long long launch_count();
+
 }  // namespace pf

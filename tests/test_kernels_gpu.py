@@ -98,11 +98,12 @@ def test_rope_matches_reference(cuda):
     assert (qkv.float().view_as(ref) - ref).abs().max().item() < 2e-2
 
 
-def test_cross_entropy_fused(cuda):
+@pytest.mark.parametrize("V", [4096, 1024, 1000, 128256])
+def test_cross_entropy_fused(cuda, V):
     import torch
     import torch.nn.functional as F
 
-    T, V = 128, 4096
+    T = 128
     g = torch.Generator().manual_seed(4)
     logits = bf(3 * torch.randn(T, V, generator=g)).cuda()
     tgt = torch.randint(0, V, (T,), generator=g).int().cuda()
