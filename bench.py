@@ -226,6 +226,8 @@ def run_ours(args) -> None:
     tr = Trainer(shape, args.schedule, world, 1, M, rank=rank, phases=phases, r_max=args.r_max, lr=1e-4,
                  seed=args.seed, device=local)
     lib = _native.device()
+    if world > 1:
+        tr.init_comm()
     stream = torch.cuda.ExternalStream(lib.pf_trainer_stream(tr._ctx))
     tokens_per_step = M * shape.tokens
 
@@ -335,6 +337,7 @@ def run_ours(args) -> None:
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
+            "attention_backend": lib.pf_attention_backend().decode(),
             "loss": {"first": round(ctl[0]["loss"], 4), "last": round(res[-1]["loss"], 4)},
         }
         print(json.dumps(line), flush=True)

@@ -134,6 +134,13 @@ int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
 /* Raw buffers of local stage i (tests): fp32 master / grad, bf16 weights, unit stamps, device unit table. */
 int pf_trainer_stage_buffers(pf_ctx* ctx, int local_stage, void** master, void** weights, void** grad,
                              void** stamps, long long* n_params, int* n_units);
+/* Multi-rank pipeline: `count` ncclUniqueId blobs (128 B each) created on one rank and
+ * shared with all; pf_trainer_init_comm takes 4 of them (activation and gradient
+ * chains, two communicators each) and must be called on every rank before step 1. */
+int pf_nccl_unique_ids(void* out, int count);
+/* Library backend used for the attention glue: "cudnn" or "flash" (ATen). */
+const char* pf_attention_backend(void);
+int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank);
 /* The cudaStream_t the trainer enqueues its step on (for device-side timing by the caller). */
 void* pf_trainer_stream(pf_ctx* ctx);
 /* Kernels launched by this library so far (all hand-written kernels, not the ATen attention). */

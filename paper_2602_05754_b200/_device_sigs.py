@@ -58,6 +58,9 @@ DEVICE_SIGNATURES = {
                                   ctypes.POINTER(c_vp), ctypes.POINTER(c_ll), ctypes.POINTER(c_int)], c_int),
     "pf_trainer_last_masks": ([c_vp, c_int, c_vp], c_int),
     "pf_trainer_stream": ([c_vp], c_vp),
+    "pf_nccl_unique_ids": ([c_vp, c_int], c_int),
+    "pf_attention_backend": ([], c_cp),
+    "pf_trainer_init_comm": ([c_vp, c_vp, c_int, c_int], c_int),
     "pf_device_launch_count": ([], c_ll),
 }
 

@@ -95,7 +95,7 @@ def build_device(force: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out,
                f"-L{tlib}", f"-Xlinker", f"-rpath={tlib}",
                "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart",
-               f"-L{LIB}", "-lpf_host", "-Xlinker", "-rpath=$ORIGIN"]
+               f"-L{LIB}", "-lpf_host", "-Xlinker", "-rpath=$ORIGIN", "-lnccl"]
         _run(cmd)
     return out
 

@@ -1,12 +1,16 @@
 // Causal GQA attention for the LLaMA stage (K7 glue), delegated to ATen's
-// flash-attention ops (library code, like cuBLAS; the only non-hand-written
-// kernels on the step). q/k/v are zero-copy views into the packed qkv
-// activation [T, (nh + 2 nkv) hd]; outputs stay on the caller's stream.
+// fused-attention ops (library code, like cuBLAS; the only non-hand-written
+// kernels on the step). Backend: cuDNN fused attention (Blackwell kernels) by
+// default, FlashAttention-2 with PF_ATTN_BACKEND=flash or if cuDNN rejects the
+// shape. q/k/v are zero-copy views into the packed qkv activation
+// [T, (nh + 2 nkv) hd]; for cuDNN, K/V are expanded to nh heads (and dK/dV
+// group-summed). Outputs stay on the caller's stream.
 #include <ATen/ATen.h>
 #include <c10/cuda/CUDAGuard.h>
 #include <c10/cuda/CUDAStream.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "attention.hpp"
@@ -18,11 +22,23 @@ struct AttnState {
   at::Tensor out, lse, cum_q, cum_k, seed, offset;
   at::Tensor dq, dk, dv;
   int64_t max_q = 0, max_k = 0;
+  bool cudnn = false;
 };
 
 namespace {
 
 thread_local std::string g_attn_err;
+
+// 1 = cuDNN, 0 = flash; cuDNN is disabled for the process after its first failure
+int g_backend = -1;
+
+int backend() {
+  if (g_backend < 0) {
+    const char* e = std::getenv("PF_ATTN_BACKEND");
+    g_backend = (e && std::string(e) == "flash") ? 0 : 1;
+  }
+  return g_backend;
+}
 
 struct Views {
   at::Tensor q, k, v;
@@ -38,6 +54,8 @@ Views make_views(const void* qkv, int B, int S, int nh, int nkv, int hd) {
   return Views{view(0, nh), view(static_cast<int64_t>(nh) * hd, nkv), view(static_cast<int64_t>(nh + nkv) * hd, nkv)};
 }
 
+at::Tensor expand_heads(const at::Tensor& t, int rep) { return rep == 1 ? t : t.repeat_interleave(rep, 1); }
+
 c10::cuda::CUDAStream wrap(cudaStream_t s) {
   return c10::cuda::getStreamFromExternal(s, c10::cuda::current_device());
 }
@@ -47,25 +65,50 @@ c10::cuda::CUDAStream wrap(cudaStream_t s) {
 AttnState* attn_state_new() { return new AttnState(); }
 void attn_state_free(AttnState* st) { delete st; }
 const char* attn_last_error() { return g_attn_err.c_str(); }
+int attn_backend_is_cudnn() { return backend(); }
 
 int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int hd, float scale, void** out,
              long long* out_token_stride, cudaStream_t stream) {
   try {
     c10::cuda::CUDAStreamGuard guard(wrap(stream));
     const auto v = make_views(qkv, B, S, nh, nkv, hd);
-    auto r = at::_scaled_dot_product_flash_attention(v.q, v.k, v.v, 0.0, true, false, static_cast<double>(scale));
-    at::Tensor o = std::get<0>(r);
+    at::Tensor o;
+    st->cudnn = false;
+    if (backend() == 1) {
+      try {
+        const int rep = nh / nkv;
+        auto r = at::_scaled_dot_product_cudnn_attention(v.q, expand_heads(v.k, rep), expand_heads(v.v, rep),
+                                                         std::nullopt, true, 0.0, true, false,
+                                                         static_cast<double>(scale));
+        o = std::get<0>(r);
+        st->lse = std::get<1>(r);
+        st->cum_q = std::get<2>(r);
+        st->cum_k = std::get<3>(r);
+        st->max_q = std::get<4>(r).expect_int();
+        st->max_k = std::get<5>(r).expect_int();
+        st->seed = std::get<6>(r);
+        st->offset = std::get<7>(r);
+        st->cudnn = true;
+      } catch (const std::exception& e) {
+        g_backend = 0;  // fall back to the flash kernels for the rest of the run
+        g_attn_err = std::string("cudnn attention unavailable, using flash: ") + e.what();
+      }
+    }
+    if (!st->cudnn) {
+      auto r = at::_scaled_dot_product_flash_attention(v.q, v.k, v.v, 0.0, true, false, static_cast<double>(scale));
+      o = std::get<0>(r);
+      st->lse = std::get<1>(r);
+      st->cum_q = std::get<2>(r);
+      st->cum_k = std::get<3>(r);
+      st->max_q = std::get<4>(r).expect_int();
+      st->max_k = std::get<5>(r).expect_int();
+      st->seed = std::get<6>(r);
+      st->offset = std::get<7>(r);
+    }
     // Wo GEMM wants [T, nh*hd] row-major = [B, S, H, D] contiguous
     at::Tensor bshd = o.transpose(1, 2);
     if (!bshd.is_contiguous()) o = bshd.contiguous().transpose(1, 2);
     st->out = o;
-    st->lse = std::get<1>(r);
-    st->cum_q = std::get<2>(r);
-    st->cum_k = std::get<3>(r);
-    st->max_q = std::get<4>(r).expect_int();
-    st->max_k = std::get<5>(r).expect_int();
-    st->seed = std::get<6>(r);
-    st->offset = std::get<7>(r);
     *out = st->out.data_ptr();
     *out_token_stride = st->out.stride(2);
     return PF_OK;
@@ -84,13 +127,31 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
     auto* dptr = static_cast<at::BFloat16*>(const_cast<void*>(dout));
     const int64_t W = static_cast<int64_t>(nh) * hd;
     at::Tensor go = at::from_blob(dptr, {B, S, nh, hd}, {S * W, W, hd, 1}, opts).transpose(1, 2);
-    auto r = at::_scaled_dot_product_flash_attention_backward(go, v.q, v.k, v.v, st->out, st->lse, st->cum_q,
-                                                              st->cum_k, st->max_q, st->max_k, 0.0, true, st->seed,
-                                                              st->offset, static_cast<double>(scale));
+    at::Tensor dq, dk, dv;
+    if (st->cudnn) {
+      const int rep = nh / nkv;
+      auto r = at::_scaled_dot_product_cudnn_attention_backward(
+          go, v.q, expand_heads(v.k, rep), expand_heads(v.v, rep), st->out, st->lse, st->seed, st->offset,
+          at::Tensor(), st->cum_q, st->cum_k, st->max_q, st->max_k, 0.0, true, static_cast<double>(scale));
+      dq = std::get<0>(r);
+      dk = std::get<1>(r);
+      dv = std::get<2>(r);
+      if (rep > 1) {  // sum the expanded heads back onto their KV group
+        dk = dk.reshape({B, nkv, rep, S, hd}).sum(2);
+        dv = dv.reshape({B, nkv, rep, S, hd}).sum(2);
+      }
+    } else {
+      auto r = at::_scaled_dot_product_flash_attention_backward(go, v.q, v.k, v.v, st->out, st->lse, st->cum_q,
+                                                                st->cum_k, st->max_q, st->max_k, 0.0, true, st->seed,
+                                                                st->offset, static_cast<double>(scale));
+      dq = std::get<0>(r);
+      dk = std::get<1>(r);
+      dv = std::get<2>(r);
+    }
     // token-major [B, S, H, D] so (b, s) flattens to t with one stride
-    st->dq = std::get<0>(r).transpose(1, 2).contiguous();
-    st->dk = std::get<1>(r).transpose(1, 2).contiguous();
-    st->dv = std::get<2>(r).transpose(1, 2).contiguous();
+    st->dq = dq.transpose(1, 2).contiguous();
+    st->dk = dk.transpose(1, 2).contiguous();
+    st->dv = dv.transpose(1, 2).contiguous();
     g->dq = st->dq.data_ptr();
     g->dk = st->dk.data_ptr();
     g->dv = st->dv.data_ptr();

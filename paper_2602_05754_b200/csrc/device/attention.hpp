@@ -28,5 +28,7 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
              AttnGrads* g, cudaStream_t stream);
 // release saved forward tensors (after the backward consumed them)
 void attn_release(AttnState* st);
+// 1 while the cuDNN fused-attention backend is in use, 0 for flash-attention
+int attn_backend_is_cudnn();
 
 }  // namespace pf

@@ -1,6 +1,7 @@
 // extern "C" surface of the stage engine and the memory-bound kernels (include/pf_device.h).
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -319,3 +320,23 @@ int pf_trainer_last_masks(pf_ctx* ctx, int i, uint64_t* out) {
 }  // extern "C"
 
 extern "C" void* pf_trainer_stream(pf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->trainer->stream()) : nullptr; }
+
+#include <nccl.h>
+
+extern "C" int pf_nccl_unique_ids(void* out, int count) {
+  return guard([&] {
+    if (!out || count <= 0) return PF_ERR_INVALID;
+    for (int k = 0; k < count; ++k) {
+      ncclUniqueId id;
+      if (ncclGetUniqueId(&id) != ncclSuccess) return PF_ERR_NCCL;
+      std::memcpy(static_cast<char*>(out) + static_cast<size_t>(k) * sizeof(id), &id, sizeof(id));
+    }
+    return PF_OK;
+  });
+}
+
+extern "C" const char* pf_attention_backend(void) { return pf::attn_backend_is_cudnn() ? "cudnn" : "flash"; }
+
+extern "C" int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank) {
+  return guard([&] { return ctx ? ctx->trainer->init_comm(ids, nranks, rank) : PF_ERR_INVALID; });
+}

@@ -8,11 +8,12 @@
 //   forward  Y  = X  . W^T      A = X  (K-major)  B = W (K-major)
 //   dX       dX = dY . W        A = dY (K-major)  B = W (MN-major)
 //   dW       dW = dY^T . X      A = dY (MN-major) B = X (MN-major)
-// The dW launch runs over a device-resident work list of unfrozen 128x128
-// units (K5 output), so its time is linear in the unfrozen count; this is the
-// device realisation of w = w_max - r (w_max - w_min) (reference
-// proj/src/timing.cpp:53) and of the masked accumulation sum_m U_m . g_m
-// (reference proj/src/sandbox.cpp:232-249).
+// The dW launch runs over device-resident work lists of unfrozen 128x128 units
+// (K5 output) of up to kMaxProblems weight matrices at once (grouped, so a
+// layer's four matrices fill the GPU together), so its time is linear in the
+// unfrozen count: the device realisation of w = w_max - r (w_max - w_min)
+// (reference proj/src/timing.cpp:53) and of the masked accumulation
+// sum_m U_m . g_m (reference proj/src/sandbox.cpp:232-249).
 //
 // Roles (192 threads, 1 CTA per SM, persistent over tiles):
 //   warp 0      TMA producer (one lane): smem ring of STAGES {A,B} k-blocks
@@ -23,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 
@@ -48,40 +50,68 @@ struct GemmCfg {
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
 };
 
-struct GemmParams {
-  int M, N, K;
+struct alignas(64) Problem {
+  CUtensorMap ta;  // A operand (TMA descriptor, lives in kernel-parameter space)
+  CUtensorMap tb;  // B operand
   void* C;
   long long ldc;
-  float alpha;
+  int M, N;
   int tiles_m, tiles_n;
-  int num_tiles;          // plain mode
-  const int* tile_list;   // list mode: unit ids (mb * tiles_n + nb)
-  const int* tile_count;  // list mode: device-resident count
-  int* unit_stamp;        // EPI_ACC_F32 first-touch stamps (indexed by unit id + stamp_offset)
-  int stamp_offset;
+  const int* list;   // list mode: local unit ids (mb * tiles_n + nb)
+  const int* count;  // list mode: device-resident count
+  int stamp_offset;  // first global unit id of this matrix (EPI_ACC_F32)
+  int num_tiles;     // plain mode
+};
+
+struct GemmParams {
+  Problem prob[kMaxGemmProblems];
+  int nprob;
+  int K;
+  float alpha;
+  int list_mode;
+  int* unit_stamp;  // EPI_ACC_F32 first-touch stamps
   int stamp;
 };
 
-__device__ __forceinline__ void decode_tile(const GemmParams& p, int t, int& mb, int& nb) {
-  if (p.tile_list != nullptr) {
-    const int u = p.tile_list[t];
-    mb = u / p.tiles_n;
-    nb = u - mb * p.tiles_n;
+struct TileMap {
+  int prefix[kMaxGemmProblems + 1];
+  int total;
+};
+
+__device__ __forceinline__ TileMap tile_map(const GemmParams& p) {
+  TileMap m;
+  m.prefix[0] = 0;
+  for (int i = 0; i < kMaxGemmProblems; ++i) {
+    const int n = i < p.nprob ? (p.list_mode ? *p.prob[i].count : p.prob[i].num_tiles) : 0;
+    m.prefix[i + 1] = m.prefix[i] + n;
+  }
+  m.total = m.prefix[kMaxGemmProblems];
+  return m;
+}
+
+__device__ __forceinline__ void decode_tile(const GemmParams& p, const TileMap& tm, int t, int& pi, int& mb,
+                                            int& nb) {
+  pi = 0;
+  while (pi + 1 < p.nprob && t >= tm.prefix[pi + 1]) ++pi;
+  const Problem& pr = p.prob[pi];
+  const int lt = t - tm.prefix[pi];
+  if (p.list_mode) {
+    const int u = pr.list[lt];
+    mb = u / pr.tiles_n;
+    nb = u - mb * pr.tiles_n;
     return;
   }
-  const int group_size = GROUP_M * p.tiles_n;
-  const int g = t / group_size;
+  const int group_size = GROUP_M * pr.tiles_n;
+  const int g = lt / group_size;
   const int first_m = g * GROUP_M;
-  const int gm = min(p.tiles_m - first_m, GROUP_M);
-  const int local = t - g * group_size;
+  const int gm = min(pr.tiles_m - first_m, GROUP_M);
+  const int local = lt - g * group_size;
   mb = first_m + local % gm;
   nb = local / gm;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
@@ -100,7 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
 
-  const int ntiles = p.tile_list != nullptr ? *p.tile_count : p.num_tiles;
+  const TileMap tm = tile_map(p);
+  const int ntiles = tm.total;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -114,9 +145,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+  if (warp == 0 && lane < static_cast<uint32_t>(p.nprob)) {
+    tma_prefetch(&p.prob[lane].ta);
+    tma_prefetch(&p.prob[lane].tb);
   }
   if (warp == 1) {
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -133,26 +164,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int mb, nb;
-        decode_tile(p, t, mb, nb);
+        int pi, mb, nb;
+        decode_tile(p, tm, t, pi, mb, nb);
+        const CUtensorMap* ta = &p.prob[pi].ta;
+        const CUtensorMap* tb = &p.prob[pi].tb;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
           uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
           if constexpr (!A_MN) {
-            tma_load_2d(a_dst, &tmA, &full_bar[stage], kb * BK, mb * BM);
+            tma_load_2d(a_dst, ta, &full_bar[stage], kb * BK, mb * BM);
           } else {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c)
-              tma_load_2d(a_dst + c * 8192, &tmA, &full_bar[stage], mb * BM + c * 64, kb * BK);
+              tma_load_2d(a_dst + c * 8192, ta, &full_bar[stage], mb * BM + c * 64, kb * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(b_dst, &tmB, &full_bar[stage], kb * BK, nb * BN);
+            tma_load_2d(b_dst, tb, &full_bar[stage], kb * BK, nb * BN);
           } else {
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c)
-              tma_load_2d(b_dst + c * 8192, &tmB, &full_bar[stage], nb * BN + c * 64, kb * BK);
+              tma_load_2d(b_dst + c * 8192, tb, &full_bar[stage], nb * BN + c * 64, kb * BK);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -205,18 +238,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int abuf = 0;
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      int mb, nb;
-      decode_tile(p, t, mb, nb);
+      int pi, mb, nb;
+      decode_tile(p, tm, t, pi, mb, nb);
+      const Problem& pr = p.prob[pi];
       bool first_touch = false;
       int unit = 0;
       if constexpr (EPI == EPI_ACC_F32) {
-        unit = p.stamp_offset + mb * p.tiles_n + nb;
+        unit = pr.stamp_offset + mb * pr.tiles_n + nb;
         first_touch = p.unit_stamp[unit] != p.stamp;
       }
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
       const long long grow = static_cast<long long>(mb) * BM + row;
-      const bool row_ok = grow < p.M;
+      const bool row_ok = grow < pr.M;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -225,13 +259,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                            r);
         tmem_ld_wait();
         const int gcol = nb * BN + c * 32;
-        if (!row_ok || gcol >= p.N) continue;
+        if (!row_ok || gcol >= pr.N) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
-        const bool full = gcol + 32 <= p.N;
+        const bool full = gcol + 32 <= pr.N;
         if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
-          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(pr.C) + grow * pr.ldc + gcol;
           if (full) {
             uint4* c4 = reinterpret_cast<uint4*>(cp);
 #pragma unroll
@@ -257,14 +291,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               c4[j] = out;
             }
           } else {
-            for (int i = 0; i < 32 && gcol + i < p.N; ++i) {
-              float w = v[i];
-              if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(cp[i]);
-              cp[i] = __float2bfloat16_rn(w);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (gcol + i < pr.N) {
+                float w = v[i];
+                if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(cp[i]);
+                cp[i] = __float2bfloat16_rn(w);
+              }
             }
           }
         } else {
-          float* cp = reinterpret_cast<float*>(p.C) + grow * p.ldc + gcol;
+          float* cp = reinterpret_cast<float*>(pr.C) + grow * pr.ldc + gcol;
           if (full) {
             float4* c4 = reinterpret_cast<float4*>(cp);
 #pragma unroll
@@ -280,10 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               c4[j] = w;
             }
           } else {
-            for (int i = 0; i < 32 && gcol + i < p.N; ++i) {
-              float w = v[i];
-              if (EPI == EPI_ACC_F32 && !first_touch) w += cp[i];
-              cp[i] = w;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (gcol + i < pr.N) {
+                float w = v[i];
+                if (EPI == EPI_ACC_F32 && !first_touch) w += cp[i];
+                cp[i] = w;
+              }
             }
           }
         }
@@ -313,8 +353,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   std::call_once(once, [] {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
   });
@@ -323,61 +362,47 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // Row-major bf16 matrix [rows][cols] with row stride ld (elements); box
 // {box_cols (inner), box_rows}.
-int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
-              int box_cols, int box_rows) {
+int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+              int box_rows) {
   auto encode = get_encode();
   if (!encode) return PF_ERR_CUDA;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
-                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   // invalid geometry (row stride not a multiple of 16 B, misaligned base, ...)
   return r == CUDA_SUCCESS ? PF_OK : PF_ERR_INVALID;
 }
 
-
 template <int BN, bool A_MN, bool B_MN, int EPI>
-int launch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int grid_limit,
-           cudaStream_t stream) {
+int launch(const GemmParams& p, int grid_limit, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  CUtensorMap ta, tb;
-  // A logical [M, K]; B logical [N, K]
-  int rc = A_MN ? make_tmap(&ta, A.ptr, p.K, p.M, A.ld, 64, 64)
-                : make_tmap(&ta, A.ptr, p.M, p.K, A.ld, 64, BM);
-  if (rc) return rc;
-  rc = B_MN ? make_tmap(&tb, B.ptr, p.K, p.N, B.ld, 64, 64)
-            : make_tmap(&tb, B.ptr, p.N, p.K, B.ld, 64, BN);
-  if (rc) return rc;
   auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg::SMEM_BYTES) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
       return PF_ERR_CUDA;
     attr_set = true;
   }
-  int grid = std::min(grid_limit, num_sms());
+  const int grid = std::min(grid_limit, num_sms());
   if (grid <= 0) return PF_OK;
-  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(ta, tb, p);
+  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
 }
 
 template <int BN>
-int dispatch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int epi, int grid_limit,
-             cudaStream_t s) {
-  const int key = (A.mn_major ? 1 : 0) | (B.mn_major ? 2 : 0);
-#define PF_GEMM_CASE(AM, BMN, E)                                            \
-  if (key == ((AM) | ((BMN) << 1)) && epi == (E))                           \
-    return launch<BN, (AM) != 0, (BMN) != 0, (E)>(A, B, p, grid_limit, s);
-#define PF_GEMM_EPIS(AM, BMN)                                               \
-  PF_GEMM_CASE(AM, BMN, EPI_STORE_BF16)                                     \
-  PF_GEMM_CASE(AM, BMN, EPI_ADD_BF16)                                       \
-  PF_GEMM_CASE(AM, BMN, EPI_ACC_F32)                                        \
+int dispatch(bool a_mn, bool b_mn, const GemmParams& p, int epi, int grid_limit, cudaStream_t s) {
+  const int key = (a_mn ? 1 : 0) | (b_mn ? 2 : 0);
+#define PF_GEMM_CASE(AM, BMN, E) \
+  if (key == ((AM) | ((BMN) << 1)) && epi == (E)) return launch<BN, (AM) != 0, (BMN) != 0, (E)>(p, grid_limit, s);
+#define PF_GEMM_EPIS(AM, BMN)                 \
+  PF_GEMM_CASE(AM, BMN, EPI_STORE_BF16)       \
+  PF_GEMM_CASE(AM, BMN, EPI_ADD_BF16)         \
+  PF_GEMM_CASE(AM, BMN, EPI_ACC_F32)          \
   PF_GEMM_CASE(AM, BMN, EPI_STORE_F32)
   PF_GEMM_EPIS(0, 0)
   PF_GEMM_EPIS(0, 1)
@@ -386,6 +411,20 @@ int dispatch(const GemmOperand& A, const GemmOperand& B, GemmParams p, int epi, 
 #undef PF_GEMM_EPIS
 #undef PF_GEMM_CASE
   return PF_ERR_INVALID;
+}
+
+// TMA descriptors of one problem: A logical [M, K], B logical [N, K]
+int fill_problem(Problem& pr, const GemmOperand& A, const GemmOperand& B, int M, int N, int K, int block_n) {
+  int rc = A.mn_major ? make_tmap(&pr.ta, A.ptr, K, M, A.ld, 64, 64) : make_tmap(&pr.ta, A.ptr, M, K, A.ld, 64, BM);
+  if (rc) return rc;
+  rc = B.mn_major ? make_tmap(&pr.tb, B.ptr, K, N, B.ld, 64, 64) : make_tmap(&pr.tb, B.ptr, N, K, B.ld, 64, block_n);
+  if (rc) return rc;
+  pr.M = M;
+  pr.N = N;
+  pr.tiles_m = (M + BM - 1) / BM;
+  pr.tiles_n = (N + block_n - 1) / block_n;
+  pr.num_tiles = pr.tiles_m * pr.tiles_n;
+  return PF_OK;
 }
 
 }  // namespace
@@ -401,50 +440,59 @@ int num_sms() {
   return n;
 }
 
-int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,
-              float alpha, int epi, int block_n, cudaStream_t stream) {
+int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
+              int epi, int block_n, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
   if (block_n != 128 && block_n != 256) return PF_ERR_INVALID;
-  GemmParams p{};
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.C = C.ptr;
-  p.ldc = C.ld;
-  p.alpha = alpha;
-  p.tiles_m = (M + BM - 1) / BM;
-  p.tiles_n = (N + block_n - 1) / block_n;
-  p.num_tiles = p.tiles_m * p.tiles_n;
-  p.unit_stamp = C.unit_stamp;
-  p.stamp_offset = C.stamp_offset;
-  p.stamp = C.stamp;
   if (epi == EPI_ACC_F32 && (C.unit_stamp == nullptr || block_n != 128)) return PF_ERR_INVALID;
-  return block_n == 256 ? dispatch<256>(A, B, p, epi, p.num_tiles, stream)
-                        : dispatch<128>(A, B, p, epi, p.num_tiles, stream);
+  GemmParams p{};
+  p.nprob = 1;
+  p.K = K;
+  p.alpha = alpha;
+  p.list_mode = 0;
+  p.unit_stamp = C.unit_stamp;
+  p.stamp = C.stamp;
+  Problem& pr = p.prob[0];
+  if (int rc = fill_problem(pr, A, B, M, N, K, block_n)) return rc;
+  pr.C = C.ptr;
+  pr.ldc = C.ld;
+  pr.stamp_offset = C.stamp_offset;
+  return block_n == 256 ? dispatch<256>(A.mn_major, B.mn_major, p, epi, pr.num_tiles, stream)
+                        : dispatch<128>(A.mn_major, B.mn_major, p, epi, pr.num_tiles, stream);
 }
 
-int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N,
-                    int K, float alpha, const int* unit_list, const int* unit_count,
-                    int max_units, cudaStream_t stream) {
-  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
-  if (C.unit_stamp == nullptr || unit_list == nullptr || unit_count == nullptr)
-    return PF_ERR_INVALID;
+int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
+                            cudaStream_t stream) {
+  if (n <= 0 || n > kMaxGemmProblems || K <= 0 || (K % 8) != 0 || unit_stamp == nullptr) return PF_ERR_INVALID;
   GemmParams p{};
-  p.M = M;
-  p.N = N;
+  p.nprob = n;
   p.K = K;
-  p.C = C.ptr;
-  p.ldc = C.ld;
   p.alpha = alpha;
-  p.tiles_m = (M + BM - 1) / BM;
-  p.tiles_n = (N + 127) / 128;
-  p.num_tiles = 0;
-  p.tile_list = unit_list;
-  p.tile_count = unit_count;
-  p.unit_stamp = C.unit_stamp;
-  p.stamp_offset = C.stamp_offset;
-  p.stamp = C.stamp;
-  return dispatch<128>(A, B, p, EPI_ACC_F32, max_units, stream);
+  p.list_mode = 1;
+  p.unit_stamp = unit_stamp;
+  p.stamp = stamp;
+  int max_units = 0;
+  const bool a_mn = items[0].A.mn_major, b_mn = items[0].B.mn_major;
+  for (int i = 0; i < n; ++i) {
+    const UnitGemm& it = items[i];
+    if (it.A.mn_major != a_mn || it.B.mn_major != b_mn || !it.unit_list || !it.unit_count) return PF_ERR_INVALID;
+    Problem& pr = p.prob[i];
+    if (int rc = fill_problem(pr, it.A, it.B, it.M, it.N, K, 128)) return rc;
+    pr.C = it.C;
+    pr.ldc = it.ldc;
+    pr.list = it.unit_list;
+    pr.count = it.unit_count;
+    pr.stamp_offset = it.stamp_offset;
+    max_units += it.max_units;
+  }
+  return dispatch<128>(a_mn, b_mn, p, EPI_ACC_F32, max_units, stream);
+}
+
+int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
+                    const int* unit_list, const int* unit_count, int max_units, cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return PF_ERR_INVALID;
+  UnitGemm it{A, B, C.ptr, C.ld, M, N, unit_list, unit_count, max_units, C.stamp_offset};
+  return gemm_bf16_units_grouped(&it, 1, K, alpha, C.unit_stamp, C.stamp, stream);
 }
 
 }  // namespace pf

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -281,17 +282,48 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __
   }
 }
 
-// block: 8 warps, each warp one row at a time; dg partials in shared memory
+// dg[c] += sum_t dy[t,c] * x[t,c] * rstd[t]: column reduction. Block = 32 column
+// groups of 8 (256 columns) x 8 row lanes; each thread sums its rows in registers.
+__global__ void __launch_bounds__(kBlock) rmsnorm_dg_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            const float* __restrict__ rstd,
+                                                            const __nv_bfloat16* __restrict__ dy,
+                                                            float* __restrict__ dg, int T, int h, int rows_per_block) {
+  __shared__ float part[8][256 + 4];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 256 + cg * 8;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(T, r0 + rows_per_block);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < h) {
+    for (int t = r0 + rl; t < r1; t += 8) {
+      float xv[8], dv[8];
+      const long long off = static_cast<long long>(t) * h + c;
+      load8(x + off, xv);
+      load8(dy + off, dv);
+      const float r = rstd[t];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += dv[i] * xv[i] * r;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[rl][cg * 8 + i] = acc[i];
+  __syncthreads();
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  if (col < h) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += part[k][threadIdx.x];
+    atomicAdd(&dg[col], s);
+  }
+}
+
+// dx = residual + rstd * g * dy - rstd^3 * x * mean(g * dy * x); one warp per row
 __global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                              const __nv_bfloat16* __restrict__ g,
                                                              const float* __restrict__ rstd,
                                                              const __nv_bfloat16* __restrict__ dy,
                                                              const __nv_bfloat16* __restrict__ residual,
-                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ dg,
-                                                             int T, int h) {
-  extern __shared__ float sdg[];
-  for (int c = threadIdx.x; c < h; c += blockDim.x) sdg[c] = 0.f;
-  __syncthreads();
+                                                             __nv_bfloat16* __restrict__ dx, int T, int h) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
     const long long off = static_cast<long long>(t) * h;
@@ -303,10 +335,7 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16
       load8(g + c, gv);
       load8(dy + off + c, dv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        dot += gv[i] * dv[i] * xv[i];
-        atomicAdd(&sdg[c + i], dv[i] * xv[i] * r);
-      }
+      for (int i = 0; i < 8; ++i) dot += gv[i] * dv[i] * xv[i];
     }
     dot = warp_sum(dot);
     const float k = dot * r * r * r / h;
@@ -321,73 +350,74 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16
       store8(dx + off + c, out);
     }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < h; c += blockDim.x) atomicAdd(&dg[c], sdg[c]);
 }
 
-// rotate-half RoPE on the q and k heads of the packed qkv activation, in place
-__global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int T, int seq,
-                                int nh, int nkv, int hd) {
-  const int half = hd / 2;
-  const int heads = nh + nkv;
-  const long long total = static_cast<long long>(T) * heads * half;
-  const long long row = static_cast<long long>(nh + 2 * nkv) * hd;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(i % half);
-    const long long th = i / half;
-    const int head = static_cast<int>(th % heads);
-    const int t = static_cast<int>(th / heads);
-    const float2 c = cs[(t % seq) * half + j];
-    __nv_bfloat16* p = qkv + t * row + static_cast<long long>(head) * hd;
-    const float a = __bfloat162float(p[j]), b = __bfloat162float(p[j + half]);
-    p[j] = __float2bfloat16_rn(a * c.x - b * c.y);
-    p[j + half] = __float2bfloat16_rn(b * c.x + a * c.y);
+// rotate-half RoPE on the q and k heads of the packed qkv activation, in place.
+// grid.y = token; each thread rotates 8 consecutive pairs (16-byte loads).
+__global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int seq, int nh,
+                                int nkv, int hd) {
+  const int half = hd / 2, chunks = half / 8;
+  const int t = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (nh + nkv) * chunks) return;
+  const int head = idx / chunks, j = (idx - head * chunks) * 8;
+  __nv_bfloat16* p = qkv + static_cast<long long>(t) * (nh + 2 * nkv) * hd + static_cast<long long>(head) * hd;
+  const float2* c = cs + static_cast<long long>(t % seq) * half + j;
+  float a[8], b[8], oa[8], ob[8];
+  load8(p + j, a);
+  load8(p + j + half, b);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 cc = c[i];
+    oa[i] = a[i] * cc.x - b[i] * cc.y;
+    ob[i] = b[i] * cc.x + a[i] * cc.y;
   }
+  store8(p + j, oa);
+  store8(p + j + half, ob);
 }
 
 __global__ void rope_bwd_pack_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
                                      const __nv_bfloat16* __restrict__ dv, long long qts, long long kts,
                                      long long vts, long long qhs, long long khs, long long vhs,
-                                     __nv_bfloat16* __restrict__ dqkv, const float2* __restrict__ cs, int T, int seq,
+                                     __nv_bfloat16* __restrict__ dqkv, const float2* __restrict__ cs, int seq,
                                      int nh, int nkv, int hd) {
-  const int half = hd / 2;
+  const int half = hd / 2, chunks = half / 8;
   const int heads = nh + 2 * nkv;
-  const long long total = static_cast<long long>(T) * heads * half;
-  const long long row = static_cast<long long>(heads) * hd;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(i % half);
-    const long long th = i / half;
-    const int head = static_cast<int>(th % heads);
-    const int t = static_cast<int>(th / heads);
-    const __nv_bfloat16* src;
-    if (head < nh) src = dq + t * qts + head * qhs;
-    else if (head < nh + nkv) src = dk + t * kts + (head - nh) * khs;
-    else src = dv + t * vts + (head - nh - nkv) * vhs;
-    const float a = __bfloat162float(src[j]), b = __bfloat162float(src[j + half]);
-    float oa = a, ob = b;
-    if (head < nh + nkv) {  // inverse rotation (transpose of the forward rotation)
-      const float2 c = cs[(t % seq) * half + j];
-      oa = a * c.x + b * c.y;
-      ob = b * c.x - a * c.y;
+  const int t = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= heads * chunks) return;
+  const int head = idx / chunks, j = (idx - head * chunks) * 8;
+  const __nv_bfloat16* src;
+  if (head < nh) src = dq + t * qts + head * qhs;
+  else if (head < nh + nkv) src = dk + t * kts + (head - nh) * khs;
+  else src = dv + t * vts + (head - nh - nkv) * vhs;
+  float a[8], b[8];
+  load8(src + j, a);
+  load8(src + j + half, b);
+  if (head < nh + nkv) {  // inverse rotation (transpose of the forward rotation)
+    const float2* c = cs + static_cast<long long>(t % seq) * half + j;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 cc = c[i];
+      const float x = a[i], y = b[i];
+      a[i] = x * cc.x + y * cc.y;
+      b[i] = y * cc.x - x * cc.y;
     }
-    __nv_bfloat16* d = dqkv + t * row + static_cast<long long>(head) * hd;
-    d[j] = __float2bfloat16_rn(oa);
-    d[j + half] = __float2bfloat16_rn(ob);
   }
+  __nv_bfloat16* d = dqkv + static_cast<long long>(t) * heads * hd + static_cast<long long>(head) * hd;
+  store8(d + j, a);
+  store8(d + j + half, b);
 }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
+// grid.y = token, x covers the row in 8-element chunks (no 64-bit index division)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int T,
                                   int ffn) {
-  const long long per_row = ffn / 8;
-  const long long total = static_cast<long long>(T) * per_row;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long t = i / per_row;
-    const int c = static_cast<int>(i - t * per_row) * 8;
+  {
+    const long long t = blockIdx.y;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= ffn) return;
     float g[8], u[8], o[8];
     load8(gu + t * 2 * ffn + c, g);
     load8(gu + t * 2 * ffn + ffn + c, u);
@@ -399,12 +429,10 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
                                   __nv_bfloat16* __restrict__ dgu, int T, int ffn) {
-  const long long per_row = ffn / 8;
-  const long long total = static_cast<long long>(T) * per_row;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long t = i / per_row;
-    const int c = static_cast<int>(i - t * per_row) * 8;
+  {
+    const long long t = blockIdx.y;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= ffn) return;
     float g[8], u[8], d[8], dg[8], du[8];
     load8(gu + t * 2 * ffn + c, g);
     load8(gu + t * 2 * ffn + ffn + c, u);
@@ -566,16 +594,23 @@ int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bflo
 int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
                        const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  const size_t smem = static_cast<size_t>(h) * sizeof(float);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-  rmsnorm_bwd_kernel<<<grid_for((T + 7) / 8, 2), kBlock, smem, s>>>(x, g, rstd, dy, residual, dx, dg, T, h);
+  rmsnorm_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, rstd, dy, residual, dx, T, h);
+  int rc = status();
+  if (rc != PF_OK || dg == nullptr) return rc;
+  // column blocks x row chunks so the grid covers ~2 waves
+  const int col_blocks = (h + 255) / 256;
+  int row_chunks = std::max(1, (2 * num_sms()) / col_blocks);
+  const int rows_per_block = std::max(8, (T + row_chunks - 1) / row_chunks);
+  row_chunks = (T + rows_per_block - 1) / rows_per_block;
+  rmsnorm_dg_kernel<<<dim3(col_blocks, row_chunks), kBlock, 0, s>>>(x, rstd, dy, dg, T, h, rows_per_block);
   return status();
 }
 
 int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh, int nkv, int hd, cudaStream_t s) {
-  const long long total = static_cast<long long>(T) * (nh + nkv) * (hd / 2);
-  rope_fwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(qkv, cs, T, seq, nh, nkv, hd);
+  if (hd % 16) return PF_ERR_INVALID;
+  const int work = (nh + nkv) * (hd / 16);
+  const int threads = std::min(kBlock, (work + 31) / 32 * 32);
+  rope_fwd_kernel<<<dim3((work + threads - 1) / threads, T), threads, 0, s>>>(qkv, cs, seq, nh, nkv, hd);
   return status();
 }
 
@@ -583,24 +618,24 @@ int launch_rope_bwd_pack(const __nv_bfloat16* dq, const __nv_bfloat16* dk, const
                          long long kts, long long vts, long long qhs, long long khs, long long vhs,
                          __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh, int nkv, int hd,
                          cudaStream_t s) {
-  const long long total = static_cast<long long>(T) * (nh + 2 * nkv) * (hd / 2);
-  rope_bwd_pack_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-      dq, dk, dv, qts, kts, vts, qhs, khs, vhs, dqkv, cs, T, seq, nh, nkv, hd);
+  if (hd % 16) return PF_ERR_INVALID;
+  const int work = (nh + 2 * nkv) * (hd / 16);
+  const int threads = std::min(kBlock, (work + 31) / 32 * 32);
+  rope_bwd_pack_kernel<<<dim3((work + threads - 1) / threads, T), threads, 0, s>>>(
+      dq, dk, dv, qts, kts, vts, qhs, khs, vhs, dqkv, cs, seq, nh, nkv, hd);
   return status();
 }
 
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s) {
   if (ffn % 8) return PF_ERR_INVALID;
-  const long long total = static_cast<long long>(T) * ffn / 8;
-  swiglu_fwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(gu, a, T, ffn);
+  swiglu_fwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, a, T, ffn);
   return status();
 }
 
 int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
                       cudaStream_t s) {
   if (ffn % 8) return PF_ERR_INVALID;
-  const long long total = static_cast<long long>(T) * ffn / 8;
-  swiglu_bwd_kernel<<<grid_for((total + kBlock - 1) / kBlock), kBlock, 0, s>>>(gu, da, dgu, T, ffn);
+  swiglu_bwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, da, dgu, T, ffn);
   return status();
 }
 

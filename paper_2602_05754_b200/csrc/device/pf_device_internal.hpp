@@ -37,6 +37,23 @@ int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C
                     int K, float alpha, const int* unit_list, const int* unit_count,
                     int max_units, cudaStream_t stream);
 
+// Grouped masked dW: up to kMaxGemmProblems weight matrices (same K = tokens,
+// same operand majorness) in one persistent launch over their unit lists.
+constexpr int kMaxGemmProblems = 4;
+struct UnitGemm {
+  GemmOperand A;  // dY  (logical [M = out, K = T])
+  GemmOperand B;  // X   (logical [N = in,  K = T])
+  void* C;        // fp32 gradient of the matrix
+  long long ldc;
+  int M, N;
+  const int* unit_list;
+  const int* unit_count;
+  int max_units;
+  int stamp_offset;
+};
+int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
+                            cudaStream_t stream);
+
 int num_sms();
 
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).

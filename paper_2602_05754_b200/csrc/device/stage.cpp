@@ -264,15 +264,12 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
     const LayerParams& P = layers_[static_cast<std::size_t>(li)];
     // MLP
     PF_TRY(gemm_dx(dcur, h, weights_ + P.wd.offset, ffn, d_a_, ffn, T, ffn, h, EPI_STORE_BF16, s));
-    PF_TRY(dgemm_units(P.wd, dcur, h, L.a, ffn, stamp, s));
     PF_TRY(launch_swiglu_bwd(L.gu, d_a_, d_gu_, T, ffn, s));
     PF_TRY(gemm_dx(d_gu_, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
-    PF_TRY(dgemm_units(P.wgu, d_gu_, 2 * ffn, L.h2, h, stamp, s));
     PF_TRY(launch_rmsnorm_bwd(L.x2, weights_ + P.g2.offset, L.rstd2, d_h_, dcur, d_x2_, grad_ + P.g2.offset, T, h, s));
     // attention
     PF_TRY(gemm_dx(d_x2_, h, weights_ + P.wo.offset, cfg_.attn_dim(), d_attn_, cfg_.attn_dim(), T, cfg_.attn_dim(), h,
                    EPI_STORE_BF16, s));
-    PF_TRY(dgemm_units(P.wo, d_x2_, h, L.attn_out, L.attn_ld, stamp, s));
     AttnGrads ag{};
     PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
                     1.0f / std::sqrt(static_cast<float>(cfg_.head_dim)), &ag, s));
@@ -282,7 +279,23 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
                                 cfg_.head_dim, s));
     PF_TRY(gemm_dx(d_qkv_, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
                    EPI_STORE_BF16, s));
-    PF_TRY(dgemm_units(P.wqkv, d_qkv_, cfg_.qkv_dim(), L.h1, h, stamp, s));
+    // K3: the layer's four masked weight gradients in ONE grouped launch over
+    // their unfrozen units (all four dY buffers are still live here)
+    {
+      const ParamSlice* w[4] = {&P.wd, &P.wgu, &P.wo, &P.wqkv};
+      const __nv_bfloat16* dys[4] = {dcur, d_gu_, d_x2_, d_qkv_};
+      const long long ldys[4] = {h, 2LL * ffn, h, cfg_.qkv_dim()};
+      const __nv_bfloat16* xs[4] = {L.a, L.h2, L.attn_out, L.h1};
+      const long long ldxs[4] = {ffn, h, L.attn_ld, h};
+      UnitGemm items[4];
+      for (int k = 0; k < 4; ++k) {
+        const UnitMatrix& m = mats_[static_cast<std::size_t>(w[k]->unit_matrix)];
+        items[k] = UnitGemm{GemmOperand{dys[k], ldys[k], true}, GemmOperand{xs[k], ldxs[k], true},
+                            grad_ + w[k]->offset, w[k]->cols, w[k]->rows, w[k]->cols,
+                            unit_lists_ + m.unit_offset, unit_counts_ + w[k]->unit_matrix, m.units, m.unit_offset};
+      }
+      PF_TRY(gemm_bf16_units_grouped(items, 4, T, 1.0f, stamps_, stamp, s));
+    }
     __nv_bfloat16* out = li > 0 ? (dcur == d_y_ ? d_tmp_ : d_y_) : (spec_.first ? d_tmp_ : dx_out);
     if (!out) return PF_ERR_INVALID;
     PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, d_x2_, out, grad_ + P.g1.offset, T, h, s));

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include <nccl.h>
+
 namespace pf {
 
 using namespace pipefreeze;
@@ -58,10 +60,9 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   actions_ = timeline_.rank_order[static_cast<std::size_t>(cfg.rank)];
   for (int s = 1; s <= S; ++s)
     if (stage_to_rank(cfg.pipeline, s) == cfg.rank) stage_ids_.push_back(s);
-  for (int s : stage_ids_) {
-    if (s > 1 && local_index(s - 1) < 0) throw std::invalid_argument("trainer: multi-rank P2P transport not built in this binary");
-    if (s < S && local_index(s + 1) < 0) throw std::invalid_argument("trainer: multi-rank P2P transport not built in this binary");
-  }
+  if (cfg.pipeline.num_ranks > 1 && cfg.pipeline.schedule_kind != ScheduleKind::GPipe &&
+      cfg.pipeline.schedule_kind != ScheduleKind::OneFOneB)
+    throw std::invalid_argument("trainer: multi-rank transport supports gpipe and 1f1b (one stage per rank)");
   // in-flight microbatches per stage = slot count
   for (int s : stage_ids_) {
     int live = 0, peak = 0;
@@ -76,6 +77,25 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
     stages_.push_back(std::make_unique<Stage>(model, stage_spec(model, stage_ids_[i], S), slots_[i], cfg.seed,
                                               cfg.device));
   const long long T = model.tokens();
+  auto act_alloc = [&]() {
+    __nv_bfloat16* p = nullptr;
+    if (cudaMalloc(&p, static_cast<size_t>(T) * model.hidden * 2) != cudaSuccess)
+      throw std::runtime_error("trainer: cudaMalloc failed");
+    return p;
+  };
+  x_recv_.resize(stage_ids_.size());
+  dy_recv_.resize(stage_ids_.size());
+  dx_send_.resize(stage_ids_.size());
+  for (std::size_t i = 0; i < stage_ids_.size(); ++i) {
+    const int s = stage_ids_[i];
+    for (int k = 0; k < slots_[i]; ++k) {
+      if (s > 1 && local_index(s - 1) < 0) {
+        x_recv_[i].push_back(act_alloc());
+        dx_send_[i].push_back(act_alloc());
+      }
+      if (s < S && local_index(s + 1) < 0) dy_recv_[i].push_back(act_alloc());
+    }
+  }
   grad_bufs_.resize(stage_ids_.size());
   for (std::size_t i = 0; i < stage_ids_.size(); ++i)
     for (int k = 0; k < slots_[i]; ++k) {
@@ -115,6 +135,19 @@ Trainer::~Trainer() {
   stages_.clear();
   for (auto& v : grad_bufs_)
     for (auto* p : v) cudaFree(p);
+  for (auto* vv : {&x_recv_, &dy_recv_, &dx_send_})
+    for (auto& v : *vv)
+      for (auto* p : v) cudaFree(p);
+  for (auto& e : comm_ev_) cudaEventDestroy(e);
+  for (auto* vv : {&x_free_ev_, &out_sent_ev_, &dy_free_ev_, &dx_sent_ev_})
+    for (auto& v : *vv)
+      for (auto e : v) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (comm_act_[k]) ncclCommDestroy(static_cast<ncclComm_t>(comm_act_[k]));
+    if (comm_grad_[k]) ncclCommDestroy(static_cast<ncclComm_t>(comm_grad_[k]));
+  }
+  for (cudaStream_t s : {act_send_, act_recv_, grad_send_, grad_recv_})
+    if (s) cudaStreamDestroy(s);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (ev_opt0_) cudaEventDestroy(ev_opt0_);
   if (ev_opt1_) cudaEventDestroy(ev_opt1_);
@@ -156,13 +189,69 @@ void Trainer::set_plan(const std::vector<double>& ratios) {
   plan_ready_ = true;
 }
 
-TimingProfile Trainer::measured_profile() const { return aggregate_monitoring(monitor_); }
+TimingProfile Trainer::measured_profile() const { return plan_profile_.all().empty() ? aggregate_monitoring(monitor_) : plan_profile_; }
+
+int Trainer::init_comm(const void* ids, int nranks, int rank) {
+  if (nranks != cfg_.pipeline.num_ranks || rank != cfg_.rank || !ids) return PF_ERR_INVALID;
+  cudaSetDevice(cfg_.device);
+  ncclUniqueId u[4];
+  std::memcpy(u, ids, sizeof(u));
+  ncclComm_t c[4];
+  for (int k = 0; k < 4; ++k)  // same order on every rank
+    if (ncclCommInitRank(&c[k], nranks, u[k], rank) != ncclSuccess) return PF_ERR_NCCL;
+  comm_act_[0] = c[0];
+  comm_act_[1] = c[1];
+  comm_grad_[0] = c[2];
+  comm_grad_[1] = c[3];
+  for (cudaStream_t* s : {&act_send_, &act_recv_, &grad_send_, &grad_recv_})
+    if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) return PF_ERR_CUDA;
+  for (auto* vv : {&x_free_ev_, &out_sent_ev_, &dy_free_ev_, &dx_sent_ev_}) {
+    vv->resize(stage_ids_.size());
+    for (std::size_t i = 0; i < stage_ids_.size(); ++i) {
+      (*vv)[i].resize(static_cast<std::size_t>(slots_[i]));
+      for (auto& e : (*vv)[i])
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return PF_ERR_CUDA;
+    }
+  }
+  return PF_OK;
+}
+
+// Alg. 1 at T_m gathers every rank's monitored durations: each
+// rank aggregates its own actions, one all-reduce (sum; each node owned by one
+// rank) gives every rank the same bounds, so every rank solves the same LP.
+int Trainer::exchange_monitoring(TimingProfile* merged) {
+  const auto local = aggregate_monitoring(monitor_);
+  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+  const std::size_t n = static_cast<std::size_t>(2 * S * M);
+  std::vector<double> host(2 * n, 0.0);
+  for (const auto& [a, b] : local.all()) {
+    const int v = dag_->index_of(a) - 1;
+    host[static_cast<std::size_t>(v)] = b.w_min;
+    host[n + static_cast<std::size_t>(v)] = b.w_max;
+  }
+  if (distributed()) {
+    double* dev = nullptr;
+    if (cudaMalloc(&dev, host.size() * sizeof(double)) != cudaSuccess) return PF_ERR_CUDA;
+    cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, act_send_);
+    if (ncclAllReduce(dev, dev, host.size(), ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm_act_[0]),
+                      act_send_) != ncclSuccess)
+      return PF_ERR_NCCL;
+    cudaMemcpyAsync(host.data(), dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost, act_send_);
+    cudaStreamSynchronize(act_send_);
+    cudaFree(dev);
+  }
+  TimingProfile p;
+  for (int v = 1; v + 1 < dag_->node_count(); ++v)
+    p.set_bounds(dag_->action_at(v), {host[static_cast<std::size_t>(v - 1)], host[n + static_cast<std::size_t>(v - 1)]});
+  *merged = p;
+  return PF_OK;
+}
 
 // Alg. 1 line at t = T_m: aggregate the monitored durations into bounds, solve
 // the freeze-ratio LP, keep the plan (reference cmd_optimize, pipefreeze.cpp:61-83).
 void Trainer::solve_plan_from_monitoring() {
   const auto t0 = std::chrono::steady_clock::now();
-  plan_profile_ = aggregate_monitoring(monitor_);
+  if (exchange_monitoring(&plan_profile_) != PF_OK) throw numerical_error("monitoring exchange failed");
   const auto lp = build_lp(*dag_, plan_profile_, cfg_.r_max);
   const auto sol = solve_lp(lp);
   plan_ = extract_freeze_plan(*dag_, plan_profile_, sol, cfg_.r_max);
@@ -231,34 +320,102 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   PF_CUDA(cudaMemsetAsync(loss_dev_, 0, 4, stream_));
   for (auto& st : stages_) PF_TRY(st->zero_dense_grads(stream_));
 
-  // ---- the rank's action list (schedule order), one microbatch action at a time
+  // ---- the rank's action list (schedule order), one microbatch action at a time.
+  // Remote neighbours (DAG rule-3 edges across ranks) go over NCCL P2P on the
+  // activation / gradient streams, ordered against compute with events.
+  const size_t act_bytes = static_cast<size_t>(T) * model_.hidden * 2;
+  int ev_next = 0;
+  auto fresh_event = [&]() -> cudaEvent_t {
+    if (ev_next >= static_cast<int>(comm_ev_.size())) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      comm_ev_.push_back(e);
+    }
+    return comm_ev_[static_cast<std::size_t>(ev_next++)];
+  };
+  auto after = [&](cudaStream_t waiter, cudaStream_t producer) -> int {
+    cudaEvent_t e = fresh_event();
+    PF_CUDA(cudaEventRecord(e, producer));
+    PF_CUDA(cudaStreamWaitEvent(waiter, e, 0));
+    return PF_OK;
+  };
+  bool needs_comm = false;
+  for (std::size_t i = 0; i < stage_ids_.size(); ++i) needs_comm |= !x_recv_[i].empty() || !dy_recv_[i].empty();
+  if (needs_comm && !distributed()) return PF_ERR_NCCL;  // init_comm() first
+  auto nccl_ok = [](ncclResult_t r) { return r == ncclSuccess ? PF_OK : PF_ERR_NCCL; };
+  const int r = cfg_.rank;
+  auto comm = [](void* c) { return static_cast<ncclComm_t>(c); };
   for (std::size_t i = 0; i < actions_.size(); ++i) {
     const ActionId a = actions_[i];
     const int li = local_index(a.stage);
-    Stage& st = *stages_[static_cast<std::size_t>(li)];
-    const int slot = (a.microbatch - 1) % slots_[static_cast<std::size_t>(li)];
+    const auto ls = static_cast<std::size_t>(li);
+    Stage& st = *stages_[ls];
+    const int slot = (a.microbatch - 1) % slots_[ls];
+    const auto ss = static_cast<std::size_t>(slot);
     const int* tok = tokens_dev_ + static_cast<long long>(a.microbatch - 1) * T;
     const int* tgt = targets_dev_ + static_cast<long long>(a.microbatch - 1) * T;
-    PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
     if (a.kind == ActionKind::Forward) {
       const __nv_bfloat16* x_in = nullptr;
-      if (a.stage > 1) {
+      const bool recv_x = a.stage > 1 && local_index(a.stage - 1) < 0;
+      const bool send_y = a.stage < S && local_index(a.stage + 1) < 0;
+      if (recv_x) {  // f(m, s-1) output over NVLink into this slot's receive buffer
+        PF_CUDA(cudaStreamWaitEvent(act_recv_, x_free_ev_[ls][ss], 0));
+        PF_TRY(nccl_ok(ncclRecv(x_recv_[ls][ss], act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage - 1),
+                                comm(comm_act_[(r - 1) & 1]), act_recv_)));
+        PF_TRY(after(stream_, act_recv_));
+        x_in = x_recv_[ls][ss];
+      } else if (a.stage > 1) {
         const int lp = local_index(a.stage - 1);
         x_in = stages_[static_cast<std::size_t>(lp)]->output((a.microbatch - 1) % slots_[static_cast<std::size_t>(lp)]);
       }
+      if (send_y) PF_CUDA(cudaStreamWaitEvent(stream_, out_sent_ev_[ls][ss], 0));  // slot output has left
+      PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
       PF_TRY(st.forward(slot, a.microbatch, tok, tgt, x_in, loss_dev_, stream_));
-    } else {
-      const __nv_bfloat16* dy = a.stage < S ? grad_bufs_[static_cast<std::size_t>(li)][static_cast<std::size_t>(slot)] : nullptr;
-      __nv_bfloat16* dx = nullptr;
-      if (a.stage > 1) {
-        const int lp = local_index(a.stage - 1);
-        dx = grad_bufs_[static_cast<std::size_t>(lp)][static_cast<std::size_t>((a.microbatch - 1) % slots_[static_cast<std::size_t>(lp)])];
+      PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
+      if (recv_x) PF_CUDA(cudaEventRecord(x_free_ev_[ls][ss], stream_));
+      if (send_y) {  // to f(m, s+1)
+        PF_TRY(after(act_send_, stream_));
+        PF_TRY(nccl_ok(ncclSend(st.output(slot), act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage + 1),
+                                comm(comm_act_[r & 1]), act_send_)));
+        PF_CUDA(cudaEventRecord(out_sent_ev_[ls][ss], act_send_));
       }
-      const uint64_t* mw = masks_dev_ + mask_offsets_[static_cast<std::size_t>(li)] +
-                           static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+    } else {
+      const bool recv_dy = a.stage < S && local_index(a.stage + 1) < 0;
+      const bool send_dx = a.stage > 1 && local_index(a.stage - 1) < 0;
+      const __nv_bfloat16* dy = nullptr;
+      if (recv_dy) {  // b(m, s+1) input gradient
+        PF_CUDA(cudaStreamWaitEvent(grad_recv_, dy_free_ev_[ls][ss], 0));
+        PF_TRY(nccl_ok(ncclRecv(dy_recv_[ls][ss], act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage + 1),
+                                comm(comm_grad_[(r + 1) & 1]), grad_recv_)));
+        PF_TRY(after(stream_, grad_recv_));
+        dy = dy_recv_[ls][ss];
+      } else if (a.stage < S) {
+        dy = grad_bufs_[ls][ss];
+      }
+      __nv_bfloat16* dx = nullptr;
+      if (send_dx) {
+        PF_CUDA(cudaStreamWaitEvent(stream_, dx_sent_ev_[ls][ss], 0));
+        dx = dx_send_[ls][ss];
+      } else if (a.stage > 1) {
+        const int lp = local_index(a.stage - 1);
+        dx = grad_bufs_[static_cast<std::size_t>(lp)][static_cast<std::size_t>((a.microbatch - 1) %
+                                                                               slots_[static_cast<std::size_t>(lp)])];
+      }
+      const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+      PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
       PF_TRY(st.backward(slot, tok, mw, dy, dx, t, stream_));
+      PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
+      if (recv_dy) PF_CUDA(cudaEventRecord(dy_free_ev_[ls][ss], stream_));
+      if (send_dx) {  // to b(m, s-1)
+        PF_TRY(after(grad_send_, stream_));
+        PF_TRY(nccl_ok(ncclSend(dx, act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage - 1),
+                                comm(comm_grad_[r & 1]), grad_send_)));
+        PF_CUDA(cudaEventRecord(dx_sent_ev_[ls][ss], grad_send_));
+      }
     }
-    PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
+  }
+  if (distributed()) {  // the step ends when its last transfers have landed
+    for (cudaStream_t cs : {act_send_, act_recv_, grad_send_, grad_recv_}) PF_TRY(after(stream_, cs));
   }
   // ---- masked optimizer step: theta -= (eta / M) * sum_m U_m . g_m
   PF_CUDA(cudaEventRecord(ev_opt0_, stream_));

@@ -10,6 +10,8 @@
 #include <memory>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "dag.hpp"
 #include "freezectl.hpp"
 #include "lp.hpp"
@@ -71,9 +73,27 @@ class Trainer {
   // this step's frozen-unit masks of local stage li: M masks of (words + 1) uint64 each
   const uint64_t* masks_host(int li) const { return masks_host_ + mask_offsets_[static_cast<std::size_t>(li)]; }
 
+  // Multi-rank P2P (NCCL over NVLink). Four communicators over the same ranks:
+  // activations r->r+1 use comm_act[r % 2], gradients r->r-1 use comm_grad[r % 2],
+  // so on every rank each communicator is driven by exactly one stream and only
+  // in one direction (sends never queue behind receives). ids: 4 x 128 bytes.
+  int init_comm(const void* ids, int nranks, int rank);
+  bool distributed() const { return comm_act_[0] != nullptr; }
+
  private:
   int local_index(int stage) const;
   void solve_plan_from_monitoring();
+  int exchange_monitoring(pipefreeze::TimingProfile* merged);
+
+  void* comm_act_[2] = {nullptr, nullptr};   // ncclComm_t
+  void* comm_grad_[2] = {nullptr, nullptr};  // ncclComm_t
+  cudaStream_t act_send_ = nullptr, act_recv_ = nullptr, grad_send_ = nullptr, grad_recv_ = nullptr;
+  std::vector<std::vector<__nv_bfloat16*>> x_recv_;   // [local stage][slot] activations from rank_of(s-1)
+  std::vector<std::vector<__nv_bfloat16*>> dy_recv_;  // [local stage][slot] gradients from rank_of(s+1)
+  std::vector<std::vector<__nv_bfloat16*>> dx_send_;  // [local stage][slot] gradient of the stage input
+  // per [local stage][slot]: buffer-reuse guards between compute and comm streams
+  std::vector<std::vector<cudaEvent_t>> x_free_ev_, out_sent_ev_, dy_free_ev_, dx_sent_ev_;
+  std::vector<cudaEvent_t> comm_ev_;  // data-ready events, pool reused every step
 
   ModelConfig model_;
   TrainConfig cfg_;

@@ -135,6 +135,23 @@ class Trainer:
         _check(self.lib.pf_trainer_create(ctypes.byref(m), ctypes.byref(c), ctypes.byref(self._ctx)), "trainer_create")
         self.info = self.get_info()
 
+    def init_comm(self) -> None:
+        """Set up the NCCL P2P transport for a multi-rank pipeline (call on every rank).
+
+        Rank 0 creates the four ncclUniqueIds (activation and gradient chains, two
+        communicators each) and shares them over the default torch.distributed group."""
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(), dist.get_rank()
+        obj = [None]
+        if rank == 0:
+            buf = ctypes.create_string_buffer(4 * 128)
+            _check(self.lib.pf_nccl_unique_ids(buf, 4), "nccl_unique_ids")
+            obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        ids = ctypes.create_string_buffer(obj[0], 4 * 128)
+        _check(self.lib.pf_trainer_init_comm(self._ctx, ids, world, rank), "trainer_init_comm")
+
     def close(self) -> None:
         if self._ctx:
             self.lib.pf_trainer_destroy(self._ctx)
