@@ -29,7 +29,8 @@ typedef struct pf_ctx pf_ctx; /* opaque per-GPU stage context */
  * A is logical [M,K]; a_mn_major=0: stored row-major [M][lda], 1: stored [K][lda].
  * B is logical [N,K]; b_mn_major=0: stored [N][ldb],       1: stored [K][ldb].
  * epilogue: 0 store bf16, 1 add into bf16 C, 2 fp32 unit-stamped accumulate
- * (requires unit_stamp, block_n=128), 3 store fp32. block_n in {128, 256}. */
+ * (requires unit_stamp, block_n=128), 3 store fp32. block_n in {128, 256}, or 512 for the
+ * CTA-pair kernel (tcgen05.mma.cta_group::2, 256 x 256 tiles; A K-major; epilogues 0, 1, 3). */
 int pf_gemm_bf16(const void* A, int a_mn_major, long long lda, const void* B, int b_mn_major,
                  long long ldb, void* C, long long ldc, int M, int N, int K, float alpha,
                  int epilogue, int block_n, int* unit_stamp, int stamp, void* stream);

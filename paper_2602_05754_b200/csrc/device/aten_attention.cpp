@@ -23,6 +23,7 @@ struct AttnState {
   at::Tensor dq, dk, dv;
   int64_t max_q = 0, max_k = 0;
   bool cudnn = false;
+  int rep = 1;  // K/V head expansion used for this forward (1 = native GQA)
 };
 
 namespace {
@@ -76,10 +77,25 @@ int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int 
     st->cudnn = false;
     if (backend() == 1) {
       try {
-        const int rep = nh / nkv;
-        auto r = at::_scaled_dot_product_cudnn_attention(v.q, expand_heads(v.k, rep), expand_heads(v.v, rep),
+        // native GQA (nkv < nh K/V heads) when cuDNN accepts it, else expanded K/V
+        static int native_gqa = -1;
+        const int full_rep = nh / nkv;
+        auto run = [&](int rep) {
+          return at::_scaled_dot_product_cudnn_attention(v.q, expand_heads(v.k, rep), expand_heads(v.v, rep),
                                                          std::nullopt, true, 0.0, true, false,
                                                          static_cast<double>(scale));
+        };
+        decltype(run(1)) r;
+        if (full_rep > 1 && native_gqa != 0) {
+          try {
+            r = run(1);
+            native_gqa = 1;
+          } catch (const std::exception&) {
+            native_gqa = 0;
+          }
+        }
+        st->rep = (full_rep > 1 && native_gqa == 1) ? 1 : full_rep;
+        if (full_rep == 1 || native_gqa == 0) r = run(st->rep);
         o = std::get<0>(r);
         st->lse = std::get<1>(r);
         st->cum_q = std::get<2>(r);
@@ -128,18 +144,15 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
     const int64_t W = static_cast<int64_t>(nh) * hd;
     at::Tensor go = at::from_blob(dptr, {B, S, nh, hd}, {S * W, W, hd, 1}, opts).transpose(1, 2);
     at::Tensor dq, dk, dv;
+    int rep = 1;
     if (st->cudnn) {
-      const int rep = nh / nkv;
+      rep = st->rep;
       auto r = at::_scaled_dot_product_cudnn_attention_backward(
           go, v.q, expand_heads(v.k, rep), expand_heads(v.v, rep), st->out, st->lse, st->seed, st->offset,
           at::Tensor(), st->cum_q, st->cum_k, st->max_q, st->max_k, 0.0, true, static_cast<double>(scale));
       dq = std::get<0>(r);
-      dk = std::get<1>(r);
+      dk = std::get<1>(r);  // nkv * rep heads; the pack kernel sums each group of rep
       dv = std::get<2>(r);
-      if (rep > 1) {  // sum the expanded heads back onto their KV group
-        dk = dk.reshape({B, nkv, rep, S, hd}).sum(2);
-        dv = dv.reshape({B, nkv, rep, S, hd}).sum(2);
-      }
     } else {
       auto r = at::_scaled_dot_product_flash_attention_backward(go, v.q, v.k, v.v, st->out, st->lse, st->cum_q,
                                                                 st->cum_k, st->max_q, st->max_k, 0.0, true, st->seed,
@@ -148,19 +161,23 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
       dk = std::get<1>(r);
       dv = std::get<2>(r);
     }
-    // token-major [B, S, H, D] so (b, s) flattens to t with one stride
-    st->dq = dq.transpose(1, 2).contiguous();
-    st->dk = dk.transpose(1, 2).contiguous();
-    st->dv = dv.transpose(1, 2).contiguous();
-    g->dq = st->dq.data_ptr();
-    g->dk = st->dk.data_ptr();
-    g->dv = st->dv.data_ptr();
-    g->dq_tok = st->dq.stride(1);
-    g->dk_tok = st->dk.stride(1);
-    g->dv_tok = st->dv.stride(1);
-    g->dq_head = st->dq.stride(2);
-    g->dk_head = st->dk.stride(2);
-    g->dv_head = st->dv.stride(2);
+    // strided [B, H, S, D] views straight into the pack kernel (no copies)
+    st->dq = dq;
+    st->dk = dk;
+    st->dv = dv;
+    g->dq = dq.data_ptr();
+    g->dk = dk.data_ptr();
+    g->dv = dv.data_ptr();
+    g->q_b = dq.stride(0);
+    g->q_h = dq.stride(1);
+    g->q_t = dq.stride(2);
+    g->k_b = dk.stride(0);
+    g->k_h = dk.stride(1);
+    g->k_t = dk.stride(2);
+    g->v_b = dv.stride(0);
+    g->v_h = dv.stride(1);
+    g->v_t = dv.stride(2);
+    g->rep = rep;
     return PF_OK;
   } catch (const std::exception& e) {
     g_attn_err = e.what();

@@ -7,12 +7,14 @@ namespace pf {
 
 struct AttnState;
 
+// Gradients w.r.t. q, k, v as [B, H, S, D] views with element strides; dk/dv
+// carry nkv * rep heads when K/V were expanded for the library call.
 struct AttnGrads {
   const void* dq;
   const void* dk;
   const void* dv;
-  long long dq_tok, dk_tok, dv_tok;     // element stride between tokens
-  long long dq_head, dk_head, dv_head;  // element stride between heads
+  long long q_b, q_t, q_h, k_b, k_t, k_h, v_b, v_t, v_h;
+  int rep;
 };
 
 AttnState* attn_state_new();

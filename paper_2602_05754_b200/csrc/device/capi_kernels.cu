@@ -26,6 +26,8 @@ int pf_gemm_bf16(const void* A, int a_mn_major, long long lda, const void* B, in
   pf::GemmOperand a{A, lda, a_mn_major != 0};
   pf::GemmOperand b{B, ldb, b_mn_major != 0};
   pf::GemmOut c{C, ldc, unit_stamp, 0, stamp};
+  if (block_n == 512)  // CTA-pair kernel, 256 x 256 tiles
+    return record(pf::gemm_bf16_pair(a, b, c, M, N, K, alpha, epilogue, static_cast<cudaStream_t>(stream)));
   return record(pf::gemm_bf16(a, b, c, M, N, K, alpha, epilogue, block_n,
                               static_cast<cudaStream_t>(stream)));
 }

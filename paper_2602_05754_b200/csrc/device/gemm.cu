@@ -429,6 +429,11 @@ int fill_problem(Problem& pr, const GemmOperand& A, const GemmOperand& B, int M,
 
 }  // namespace
 
+int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                     int box_rows) {
+  return make_tmap(map, ptr, rows, cols, ld, box_cols, box_rows);
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {

@@ -1,0 +1,315 @@
+// K1 / K2 on a CTA pair: tcgen05.mma.cta_group::2, 256 x BN tiles.
+//
+// Same contract as gemm.cu (C (op)= alpha * A . B^T, A K-major, B K- or
+// MN-major) but each tile is computed by two CTAs of a cluster on two SMs of
+// one TPC: CTA r stages rows [128 r, 128 r + 128) of A and half of B's BN rows;
+// the leader (even) CTA issues the 256 x BN x 16 MMAs, which read A and B from
+// both CTAs' shared memory and accumulate rows of CTA r into CTA r's TMEM. Per
+// SM this halves the B traffic from L2 and shared memory relative to the
+// 1-CTA 128 x BN tile, the limiter of the 1-CTA kernel (tensor pipe 57-73%).
+//
+// Pipelines: smem ring (each CTA's TMA signals the LEADER's full barrier with
+// .cta_group::2; the leader expects both CTAs' bytes; the leader's commit
+// multicasts the empty barrier to both CTAs), TMEM double buffer (leader
+// commit multicasts tmem-full to both; both CTAs' epilogues arrive on the
+// leader's tmem-empty barrier through shared::cluster addresses).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "pf_device_internal.hpp"
+#include "ptx.cuh"
+
+namespace pf {
+
+int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                     int box_rows);
+
+namespace {
+
+constexpr int BM2 = 256;  // rows per CTA pair
+constexpr int BK = 64;
+constexpr int GROUP_M = 8;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg2 {
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's half of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+struct alignas(64) Params2 {
+  CUtensorMap ta;
+  CUtensorMap tb;
+  void* C;
+  long long ldc;
+  int M, N, K;
+  int tiles_m, tiles_n;
+  float alpha;
+};
+
+template <int BN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tcgen05_pair_kernel(const __grid_constant__ Params2 p) {
+  using Cfg = Cfg2<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  constexpr uint32_t IDESC = idesc_bf16_f32(BM2, BN, false, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 2 * 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.ta);
+    tma_prefetch(&p.tb);
+  }
+  if (warp == 1) {
+    tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits and TMEM allocation visible to both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int t, int& tm, int& tn) {
+    const int group_size = GROUP_M * p.tiles_n;
+    const int g = t / group_size;
+    const int first_m = g * GROUP_M;
+    const int gm = min(p.tiles_m - first_m, GROUP_M);
+    const int local = t - g * group_size;
+    tm = first_m + local % gm;
+    tn = local / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        int tm, tn;
+        decode(t, tm, tn);
+        const int m0 = tm * BM2 + static_cast<int>(rank) * 128;
+        const int n0 = tn * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          uint8_t* b_dst = sB + stage * Cfg::B_BYTES;
+          tma_load_2d_pair(a_dst, &p.ta, &full_bar[stage], kb * BK, m0);
+          if constexpr (!B_MN) {
+            tma_load_2d_pair(b_dst, &p.tb, &full_bar[stage], kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < (BN / 2) / 64; ++c)
+              tma_load_2d_pair(b_dst + c * 8192, &p.tb, &full_bar[stage], n0 + c * 64, kb * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------------------------------------------------- MMA issuer (leader CTA)
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int t = cluster; t < ntiles; t += nclusters) {
+        mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc = sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                                        : sdesc_sw128(b_base + k * 32, 16, 1024);
+            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair_multicast(&empty_bar[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair_multicast(&tfull_bar[abuf], 0x3);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const int row = q * 32 + static_cast<int>(lane);
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int t = cluster; t < ntiles; t += nclusters) {
+      int tm, tn;
+      decode(t, tm, tn);
+      mbar_wait(&tfull_bar[abuf], aphase);
+      tc_fence_after();
+      const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
+      const bool row_ok = grow < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                               static_cast<uint32_t>(abuf * BN + c * 32),
+                           r);
+        tmem_ld_wait();
+        const int gcol = tn * BN + c * 32;
+        if (!row_ok || gcol >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+        const bool full = gcol + 32 <= p.N;
+        if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
+          if (full) {
+            uint4* c4 = reinterpret_cast<uint4*>(cp);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = v[j * 8 + i];
+              if constexpr (EPI == EPI_ADD_BF16) {
+                const uint4 old = c4[j];
+                const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(o[i]);
+                  w[2 * i] += f.x;
+                  w[2 * i + 1] += f.y;
+                }
+              }
+              uint4 out;
+              out.x = pack_bf16x2(w[0], w[1]);
+              out.y = pack_bf16x2(w[2], w[3]);
+              out.z = pack_bf16x2(w[4], w[5]);
+              out.w = pack_bf16x2(w[6], w[7]);
+              c4[j] = out;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (gcol + i < p.N) {
+                float w = v[i];
+                if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(cp[i]);
+                cp[i] = __float2bfloat16_rn(w);
+              }
+            }
+          }
+        } else {
+          float* cp = reinterpret_cast<float*>(p.C) + grow * p.ldc + gcol;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (gcol + i < p.N) cp[i] = v[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+      abuf ^= 1;
+      if (abuf == 0) aphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+template <int BN, bool B_MN, int EPI>
+int launch2(const Params2& p, cudaStream_t stream) {
+  using Cfg = Cfg2<BN>;
+  auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
+      return PF_ERR_CUDA;
+    attr_set = true;
+  }
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int clusters = std::min(ntiles, num_sms() / 2);
+  if (clusters <= 0) return PF_OK;
+  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
+
+}  // namespace
+
+int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
+                   int epi, cudaStream_t stream) {
+  constexpr int BN = 256;
+  if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0 || A.mn_major) return PF_ERR_INVALID;
+  Params2 p{};
+  int rc = tma_desc_bf16_2d(&p.ta, A.ptr, M, K, A.ld, 64, 128);
+  if (rc) return rc;
+  rc = B.mn_major ? tma_desc_bf16_2d(&p.tb, B.ptr, K, N, B.ld, 64, 64)
+                  : tma_desc_bf16_2d(&p.tb, B.ptr, N, K, B.ld, 64, BN / 2);
+  if (rc) return rc;
+  p.C = C.ptr;
+  p.ldc = C.ld;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.tiles_m = (M + BM2 - 1) / BM2;
+  p.tiles_n = (N + BN - 1) / BN;
+  p.alpha = alpha;
+  const bool bmn = B.mn_major;
+  switch (epi) {
+    case EPI_STORE_BF16: return bmn ? launch2<BN, true, EPI_STORE_BF16>(p, stream) : launch2<BN, false, EPI_STORE_BF16>(p, stream);
+    case EPI_ADD_BF16: return bmn ? launch2<BN, true, EPI_ADD_BF16>(p, stream) : launch2<BN, false, EPI_ADD_BF16>(p, stream);
+    case EPI_STORE_F32: return bmn ? launch2<BN, true, EPI_STORE_F32>(p, stream) : launch2<BN, false, EPI_STORE_F32>(p, stream);
+    default: return PF_ERR_INVALID;
+  }
+}
+
+}  // namespace pf

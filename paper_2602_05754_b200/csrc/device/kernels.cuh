@@ -65,12 +65,15 @@ int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bflo
 int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
                        const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s);
 int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh, int nkv, int hd, cudaStream_t s);
-// dq, dk, dv (strided, [B, S, H, D] memory) -> rotated back and packed into dqkv [T, (nh+2nkv)hd]
-int launch_rope_bwd_pack(const __nv_bfloat16* dq, const __nv_bfloat16* dk, const __nv_bfloat16* dv,
-                         long long q_tok_stride, long long k_tok_stride, long long v_tok_stride,
-                         long long q_head_stride, long long k_head_stride, long long v_head_stride,
-                         __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh, int nkv, int hd,
-                         cudaStream_t s);
+// attention input gradients as strided [B, H, S, D] views (element strides)
+struct AttnGradView {
+  const __nv_bfloat16 *dq, *dk, *dv;
+  long long q_b, q_t, q_h, k_b, k_t, k_h, v_b, v_t, v_h;
+  int rep;  // dk/dv carry nkv * rep heads; each group of rep is summed (GQA with expanded K/V)
+};
+// dq, dk, dv -> rotated back (inverse RoPE on q, k) and packed into dqkv [T, (nh+2nkv)hd]
+int launch_rope_bwd_pack(const AttnGradView& g, __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh,
+                         int nkv, int hd, cudaStream_t s);
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s);
 int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
                       cudaStream_t s);

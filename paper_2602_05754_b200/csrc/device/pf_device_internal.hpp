@@ -54,6 +54,10 @@ struct UnitGemm {
 int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
                             cudaStream_t stream);
 
+// K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.
+int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
+                   int epi, cudaStream_t stream);
+
 int num_sms();
 
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -24,18 +25,31 @@ long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
     if ((expr) != cudaSuccess) return PF_ERR_CUDA;         \
   } while (0)
 
+// CTA-pair (cta_group::2) kernel for the large K1/K2 GEMMs unless PF_GEMM_PAIR=0
+bool use_pair() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int gemm_any(const GemmOperand& A, const GemmOperand& B, void* C, long long ldc, int M, int N, int K, int epi,
+             cudaStream_t s) {
+  if (use_pair() && M >= 256 && N >= 256) return gemm_bf16_pair(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, s);
+  return gemm_bf16(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, N >= 256 ? 256 : 128, s);
+}
+
 int gemm_fwd(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
              int M, int N, int K, int epi, cudaStream_t s) {
   // Y[M,N] (+)= A[M,K] . W[N,K]^T, both K-major
-  return gemm_bf16(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, GemmOut{C, ldc}, M, N, K, 1.0f, epi,
-                   N >= 256 ? 256 : 128, s);
+  return gemm_any(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, C, ldc, M, N, K, epi, s);
 }
 
 int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
             int M, int N, int K, int epi, cudaStream_t s) {
   // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
-  return gemm_bf16(GemmOperand{dY, ldy, false}, GemmOperand{W, ldw, true}, GemmOut{C, ldc}, M, N, K, 1.0f, epi,
-                   N >= 256 ? 256 : 128, s);
+  return gemm_any(GemmOperand{dY, ldy, false}, GemmOperand{W, ldw, true}, C, ldc, M, N, K, epi, s);
 }
 
 }  // namespace
@@ -273,10 +287,12 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
     AttnGrads ag{};
     PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
                     1.0f / std::sqrt(static_cast<float>(cfg_.head_dim)), &ag, s));
-    PF_TRY(launch_rope_bwd_pack(static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
-                                static_cast<const __nv_bfloat16*>(ag.dv), ag.dq_tok, ag.dk_tok, ag.dv_tok, ag.dq_head,
-                                ag.dk_head, ag.dv_head, d_qkv_, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads,
-                                cfg_.head_dim, s));
+    {
+      AttnGradView gv{static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
+                      static_cast<const __nv_bfloat16*>(ag.dv), ag.q_b, ag.q_t, ag.q_h, ag.k_b, ag.k_t, ag.k_h,
+                      ag.v_b, ag.v_t, ag.v_h, ag.rep};
+      PF_TRY(launch_rope_bwd_pack(gv, d_qkv_, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
+    }
     PF_TRY(gemm_dx(d_qkv_, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
                    EPI_STORE_BF16, s));
     // K3: the layer's four masked weight gradients in ONE grouped launch over

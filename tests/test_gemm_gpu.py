@@ -105,3 +105,27 @@ def test_gemm_dw_unit_list_accumulates(cuda):
     st = stamps.cpu().tolist()
     for u in range(12):
         assert st[u] == (42 if u in {0, 5, 6, 11, 1, 2} else 0)
+
+
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 320), (512, 768, 1024), (296, 392, 200), (1024, 2048, 512)])
+def test_gemm_cta_pair(cuda, b_mn, epi, M, N, K):
+    """CTA-pair kernel (tcgen05.mma.cta_group::2, 256x256 tiles) through block_n=512."""
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(M + N + K + epi)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn((K, N) if b_mn else (N, K), generator=g).to(torch.bfloat16).cuda()
+    ref = _ref(A, 0, B, b_mn)
+    if epi == 3:
+        C = torch.zeros(M, N, dtype=torch.float32, device=cuda)
+        _run(A, 0, B, b_mn, C, M, N, K, epi=3, bn=512)
+        assert (C - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+        return
+    C0 = torch.randn(M, N, generator=g).to(torch.bfloat16).cuda() if epi == 1 else torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+    C = C0.clone()
+    _run(A, 0, B, b_mn, C, M, N, K, epi=epi, bn=512)
+    if epi == 1:
+        ref = ref + C0.float()
+    assert (C.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-2

@@ -84,6 +84,66 @@ def test_stage_step_matches_torch_reference(cuda, override):
     tr.close()
 
 
+@pytest.mark.parametrize("stages_per_rank", [2, 4])
+def test_multi_stage_rank_matches_torch_reference(cuda, stages_per_rank):
+    """Interleaved schedule with several virtual stages on one GPU: activations and gradients
+    hand over between local stages; the update must equal the single-model reference."""
+    import torch
+
+    from gpu_util import device_view
+    from llama_ref import stage_loss, unflatten
+    from paper_2602_05754_b200 import pipefreeze as pf
+    from paper_2602_05754_b200.engine import PRESETS, Trainer, param_layout
+
+    shape = PRESETS["tiny"]
+    M, lr, S = 2, 0.5, stages_per_rank
+    tr = Trainer(shape, "interleaved-1f1b", 1, S, M, lr=lr, seed=5)
+    tr.set_override(0.5)
+    lays = [param_layout(shape, s, S) for s in range(1, S + 1)]
+    bufs = [tr.stage_buffers(i) for i in range(S)]
+    theta0 = [device_view(b["master"], b["n_params"]).clone() for b in bufs]
+    w0 = [device_view(b["weights"], b["n_params"], torch.bfloat16).clone() for b in bufs]
+    rng = np.random.default_rng(1)
+    T = shape.tokens
+    tokens = rng.integers(0, shape.vocab, size=(M, T), dtype=np.int32)
+    targets = rng.integers(0, shape.vocab, size=(M, T), dtype=np.int32)
+    res = tr.step(1, tokens, targets)
+    torch.cuda.synchronize()
+    theta1 = [device_view(b["master"], b["n_params"]).clone() for b in bufs]
+    frozen = [[pf.unpack_mask(mk, lays[i]["n_units"]) for mk in tr.last_masks(i)] for i in range(S)]
+
+    params = {}
+    for i in range(S):
+        params.update({k: v.detach().clone().requires_grad_(True) for k, v in unflatten(w0[i].float(), lays[i]).items()})
+    owner = {ent["name"]: i for i in range(S) for ent in lays[i]["units"] + lays[i]["dense"]}
+    grads = {k: torch.zeros_like(v) for k, v in params.items()}
+    losses = []
+    for m in range(M):
+        for v in params.values():
+            v.grad = None
+        loss = stage_loss(params, shape, range(shape.layers), torch.tensor(tokens[m], device=cuda).long(),
+                          torch.tensor(targets[m], device=cuda).long(), True, True)
+        loss.backward()
+        losses.append(loss.item())
+        for i in range(S):
+            for ent in lays[i]["units"]:
+                upd = torch.tensor(_expand_unit_mask(frozen[i][m], ent), device=cuda)
+                grads[ent["name"]] += params[ent["name"]].grad * upd
+            for ent in lays[i]["dense"]:
+                grads[ent["name"]] += params[ent["name"]].grad
+    assert abs(res["loss"] - np.mean(losses)) < 2e-2 * abs(np.mean(losses))
+    d_dev = {}
+    for i in range(S):
+        d_dev.update(unflatten(theta1[i] - theta0[i], lays[i]))
+    for name, exp_g in grads.items():
+        exp = -(lr / M) * exp_g
+        if exp.abs().max().item() == 0:
+            continue
+        rel = (d_dev[name] - exp).norm().item() / exp.norm().item()
+        assert rel < 6e-2, (name, owner[name], rel)
+    tr.close()
+
+
 def test_controller_phases_plan_and_bit_exact_masks(cuda):
     import torch  # noqa: F401
 
