@@ -95,6 +95,13 @@ int pf_simulate_monitoring(int M, int S, const double* fwd, const double* bact,
                            const double* bparam, const int* plan, double sigma, uint64_t seed,
                            double* w_min, double* w_max);
 
+/* run_masked_sgd (sandbox.hpp:111) on a diagonal quadratic: policy 0 none,
+ * 1 uniform_bernoulli(param = update probability), 2 uniform_exact_count(param =
+ * freeze ratio). Outputs the final theta [d] and ||grad||^2 per step [steps]. */
+int pf_masked_sgd_host(int d, const double* diag, const double* theta0, double eta, int M, int steps,
+                       double sigma, int policy, double param, uint64_t seed, double* theta_out,
+                       double* grad_sq_out);
+
 /* apf_update (freezectl.hpp:88) in fp64 on the host. */
 int pf_apf_update_host(int n, double alpha, double* ema, double* ema_abs, const double* delta,
                        double* scores);

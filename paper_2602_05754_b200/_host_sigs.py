@@ -28,6 +28,7 @@ HOST_SIGNATURES = {
     "pf_monitor_aggregate": ([c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "pf_simulate_monitoring": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_d, c_u64, c_vp, c_vp], c_int),
     "pf_apf_update_host": ([c_int, c_d, c_vp, c_vp, c_vp, c_vp], c_int),
+    "pf_masked_sgd_host": ([c_int, c_vp, c_vp, c_d, c_int, c_int, c_d, c_int, c_d, c_u64, c_vp, c_vp], c_int),
 }
 
 

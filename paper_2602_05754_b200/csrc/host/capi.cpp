@@ -7,6 +7,7 @@
 #include "freezectl.hpp"
 #include "lp.hpp"
 #include "pipefreeze_c.h"
+#include "sandbox.hpp"
 #include "schedule.hpp"
 #include "timing.hpp"
 
@@ -349,6 +350,25 @@ int pf_simulate_monitoring(int M, int S, const double* fwd, const double* bact, 
       w_min[v - 1] = b.w_min;
       w_max[v - 1] = b.w_max;
     }
+  });
+}
+
+int pf_masked_sgd_host(int d, const double* diag, const double* theta0, double eta, int M, int steps, double sigma,
+                       int policy, double param, uint64_t seed, double* theta_out, double* grad_sq_out) {
+  return guard([&] {
+    need(diag, "diag");
+    need(theta0, "theta0");
+    const auto obj = SyntheticObjective::quadratic(Vec(diag, diag + d), sigma);
+    const MaskPolicy pol = policy == 0   ? MaskPolicy::none()
+                           : policy == 1 ? MaskPolicy::uniform_bernoulli(param)
+                                         : MaskPolicy::uniform_exact_count(param);
+    SgdHyper h;
+    h.eta = eta;
+    h.microbatches = M;
+    h.total_steps = steps;
+    const auto run = run_masked_sgd(obj, pol, h, Vec(theta0, theta0 + d), seed);
+    if (theta_out) std::copy(run.theta_final.begin(), run.theta_final.end(), theta_out);
+    if (grad_sq_out) std::copy(run.grad_sq_norms.begin(), run.grad_sq_norms.end(), grad_sq_out);
   });
 }
 

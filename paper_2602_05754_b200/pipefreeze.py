@@ -392,6 +392,18 @@ def simulate_monitoring(M: int, S: int, fwd, bact, bparam, plan: PhasePlan, sigm
     return wmin, wmax
 
 
+def run_masked_sgd_quadratic(diag, theta0, eta: float, microbatches: int, steps: int, sigma: float, policy: int,
+                             param: float, seed: int):
+    """run_masked_sgd (sandbox.cpp:191-257) on a diagonal quadratic -> (theta_final, grad_sq_norms)."""
+    dg = np.ascontiguousarray(diag, dtype=np.float64)
+    t0 = np.ascontiguousarray(theta0, dtype=np.float64)
+    th = np.zeros_like(t0)
+    gs = np.zeros(steps)
+    _check(_native.host().pf_masked_sgd_host(len(dg), _p(dg), _p(t0), eta, microbatches, steps, sigma, policy, param,
+                                             seed, _p(th), _p(gs)), "run_masked_sgd")
+    return th, gs
+
+
 def apf_update_host(ema: np.ndarray, ema_abs: np.ndarray, delta, alpha: float = 0.9) -> np.ndarray:
     d = np.ascontiguousarray(delta, dtype=np.float64)
     sc = np.zeros_like(d)
