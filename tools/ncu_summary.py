@@ -16,10 +16,10 @@ UNIT = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0
 
 
 def short(name: str) -> str:
-    m = re.search(r"gemm_tcgen05_pair_kernel<(\d+), (true|false), (\d)>", name)
+    m = re.search(r"gemm_tcgen05_pair_kernel<(\d+), (true|false|0|1), (\d)>", name)
     if m:
         bn, bmn, epi = m.groups()
-        return f"gemm_tcgen05_pair<256x{bn},{'dX K2' if bmn == 'true' else 'fwd K1'},epi={epi}>"
+        return f"gemm_tcgen05_pair<256x{bn},{'dX K2' if bmn in ('true', '1') else 'fwd K1'},epi={epi}>"
     m = re.search(r"gemm_tcgen05_kernel<(\d+), (\d), (\d), (\d)>", name)
     if m:
         bn, amn, bmn, epi = m.groups()
