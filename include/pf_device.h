@@ -131,6 +131,8 @@ int pf_trainer_set_plan(pf_ctx* ctx, const double* ratios /* (s-1)*M + (m-1) */)
 /* plan ratios and {base, opt, floor} makespans of the LP on monitored bounds; returns PF_ERR_DOMAIN before T_m. */
 int pf_trainer_get_plan(pf_ctx* ctx, double* ratios, double* out3, double* w_min, double* w_max);
 int pf_trainer_action_ms(pf_ctx* ctx, double* ms, int* kinds, int* microbatches, int* stages);
+/* start of each action of the last step relative to the rank's first action (ms, CUDA events) */
+int pf_trainer_action_starts(pf_ctx* ctx, double* start_ms);
 int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
 /* Raw buffers of local stage i (tests): fp32 master / grad, bf16 weights, unit stamps, device unit table. */
 int pf_trainer_stage_buffers(pf_ctx* ctx, int local_stage, void** master, void** weights, void** grad,

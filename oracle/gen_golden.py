@@ -212,3 +212,29 @@ if __name__ == "__main__":
     gen_lp(fx)
     gen_monitor()
     gen_sgd()
+
+
+def gen_artifacts(fx):
+    """Reference JSON artifacts (plan.json, report.json, gantt timelines, mask history, timing profile)."""
+    out = []
+    for name in ("default_1f1b_s4m8", "gpipe_s2m2", "interleaved_r2c2m4", "zbv_r2m4"):
+        f = fx[name]
+        pl = f["pipeline"]
+        R, C, M = pl["num_ranks"], pl["stages_per_rank"], pl["num_microbatches"]
+        S = R * C
+        t = f["timing"]["per_stage"]
+        plan_txt, report_txt = ref.plan_json(pl["schedule"], R, C, M, t["forward_ms"], t["backward_act_ms"],
+                                             t["backward_param_ms"], f["r_max"])
+        n = 2 * M * S + 2
+        w = np.array([0.0] + [t["forward_ms"]] * (M * S) + [t["backward_act_ms"] + t["backward_param_ms"]] * (M * S) + [0.0])
+        pr = ref.plan(pl["schedule"], R, C, M, t["forward_ms"], t["backward_act_ms"], t["backward_param_ms"], f["r_max"])
+        masks_txt = ref.masks_json(M, S, [2, 8, 10, 20], pr["ratios"], 500, f["seed"])
+        out.append({"fixture": name, "plan_json": plan_txt, "report_json": report_txt,
+                    "gantt_json": ref.gantt_json(pl["schedule"], R, C, M, w),
+                    "masks_json": masks_txt, "profile_json": ref.profile_json(M, S, t["forward_ms"], t["backward_act_ms"],
+                                                                               t["backward_param_ms"])})
+    dump("artifacts.json", out)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "artifacts":
+    gen_artifacts(fixtures())

@@ -205,3 +205,39 @@ def masked_sgd(diag, theta0, eta, M, steps, sigma, policy, param, seed):
 
 def cpu_step_seconds(kind, R, C, M, n_units, n_params, ratio, seed=42) -> float:
     return lib().ref_cpu_step(KIND[kind], R, C, M, n_units, n_params, ratio, seed)
+
+
+def _text(fn, *args, cap=1 << 24):
+    buf = ctypes.create_string_buffer(cap)
+    _chk(fn(*args, buf, cap))
+    return buf.value.decode()
+
+
+def plan_json(kind, R, C, M, fwd, bact, bparam, r_max):
+    """freeze_plan_to_json_text + throughput_report_to_json_text of the reference plan (config.cpp:188-257)."""
+    S = R * C
+    f = np.broadcast_to(np.asarray(fwd, dtype=np.float64), (S,)).copy()
+    a = np.broadcast_to(np.asarray(bact, dtype=np.float64), (S,)).copy()
+    b = np.broadcast_to(np.asarray(bparam, dtype=np.float64), (S,)).copy()
+    pb = ctypes.create_string_buffer(1 << 22)
+    rb = ctypes.create_string_buffer(1 << 20)
+    _chk(lib().ref_plan_json(KIND[kind], R, C, M, _p(f), _p(a), _p(b), ctypes.c_double(r_max), pb, 1 << 22, rb, 1 << 20))
+    return pb.value.decode(), rb.value.decode()
+
+
+def gantt_json(kind, R, C, M, weights):
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    return _text(lib().ref_gantt_json, KIND[kind], R, C, M, _p(w))
+
+
+def masks_json(M, S, plan, ratios, n, seed):
+    p = np.array(plan, dtype=np.int32)
+    r = np.ascontiguousarray(ratios, dtype=np.float64)
+    return _text(lib().ref_masks_json, M, S, _p(p), _p(r), n, ctypes.c_uint64(seed))
+
+
+def profile_json(M, S, fwd, bact, bparam):
+    f = np.broadcast_to(np.asarray(fwd, dtype=np.float64), (S,)).copy()
+    a = np.broadcast_to(np.asarray(bact, dtype=np.float64), (S,)).copy()
+    b = np.broadcast_to(np.asarray(bparam, dtype=np.float64), (S,)).copy()
+    return _text(lib().ref_profile_json, M, S, _p(f), _p(a), _p(b))

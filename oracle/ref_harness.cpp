@@ -13,8 +13,11 @@
 #include <string>
 #include <vector>
 
+#include "pipefreeze/analysis.hpp"
+#include "pipefreeze/config.hpp"
 #include "pipefreeze/dag.hpp"
 #include "pipefreeze/freezectl.hpp"
+#include "pipefreeze/gantt.hpp"
 #include "pipefreeze/lp.hpp"
 #include "pipefreeze/sandbox.hpp"
 #include "pipefreeze/schedule.hpp"
@@ -339,6 +342,53 @@ int ref_masked_sgd(int d, const double* diag, const double* theta0, double eta, 
     for (int t = 0; t < static_cast<int>(run.grad_sq_norms.size()); ++t)
       gradsq_out[t] = run.grad_sq_norms[t];
   });
+}
+
+namespace {
+int copy_text(const std::string& s, char* out, int cap) {
+  if (!out || cap <= 0) return static_cast<int>(s.size()) + 1;
+  std::strncpy(out, s.c_str(), static_cast<size_t>(cap - 1));
+  out[cap - 1] = 0;
+  return static_cast<int>(s.size()) + 1;
+}
+}  // namespace
+
+// Reference artifacts (config.cpp / gantt.cpp / analysis.cpp writers) for I/O parity.
+int ref_plan_json(int kind, int R, int C, int M, const double* fwd, const double* bact, const double* bparam,
+                  double r_max, char* plan_out, int plan_cap, char* report_out, int report_cap) {
+  return guard([&] {
+    const auto pc = cfg(kind, R, C, M);
+    const int S = pc.total_stages();
+    const auto dag = build_dag(build_schedule(pc));
+    const auto prof = profile_from(M, S, fwd, bact, bparam);
+    const auto plan = extract_freeze_plan(dag, prof, solve_lp(build_lp(dag, prof, r_max)), r_max);
+    copy_text(freeze_plan_to_json_text(plan), plan_out, plan_cap);
+    copy_text(throughput_report_to_json_text(build_report(plan, nullptr, nullptr, std::nullopt)), report_out,
+              report_cap);
+  });
+}
+
+int ref_gantt_json(int kind, int R, int C, int M, const double* weights, char* out, int cap) {
+  return guard([&] {
+    const auto tl = build_schedule(cfg(kind, R, C, M));
+    const auto dag = build_dag(tl);
+    copy_text(gantt_to_json_text(build_gantt(tl, dag, std::vector<double>(weights, weights + dag.node_count()))), out,
+              cap);
+  });
+}
+
+int ref_masks_json(int M, int S, const int* plan, const double* ratios, int n, uint64_t seed, char* out, int cap) {
+  return guard([&] {
+    std::map<ActionId, double> expected;
+    for (int s = 1; s <= S; ++s)
+      for (int m = 1; m <= M; ++m) expected[backward_action(m, s)] = ratios[(s - 1) * M + (m - 1)];
+    Rng rng(seed);
+    copy_text(mask_history_to_json_text(run_freezing_masks(expected, phases(plan), M, S, n, rng)), out, cap);
+  });
+}
+
+int ref_profile_json(int M, int S, const double* fwd, const double* bact, const double* bparam, char* out, int cap) {
+  return guard([&] { copy_text(timing_profile_to_json_text(profile_from(M, S, fwd, bact, bparam)), out, cap); });
 }
 
 // One "reference step" of the path on CPU, for bench.py's reference arm:

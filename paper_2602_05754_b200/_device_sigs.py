@@ -60,6 +60,7 @@ DEVICE_SIGNATURES = {
     "pf_trainer_stream": ([c_vp], c_vp),
     "pf_nccl_unique_ids": ([c_vp, c_int], c_int),
     "pf_attention_backend": ([], c_cp),
+    "pf_trainer_action_starts": ([c_vp, c_vp], c_int),
     "pf_trainer_init_comm": ([c_vp, c_vp, c_int, c_int], c_int),
     "pf_device_launch_count": ([], c_ll),
 }

@@ -335,6 +335,15 @@ extern "C" int pf_nccl_unique_ids(void* out, int count) {
   });
 }
 
+extern "C" int pf_trainer_action_starts(pf_ctx* ctx, double* start_ms) {
+  return guard([&] {
+    if (!ctx || !start_ms) return PF_ERR_INVALID;
+    const auto& v = ctx->trainer->action_start_ms();
+    std::copy(v.begin(), v.end(), start_ms);
+    return PF_OK;
+  });
+}
+
 extern "C" const char* pf_attention_backend(void) { return pf::attn_backend_is_cudnn() ? "cudnn" : "flash"; }
 
 extern "C" int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank) {

@@ -427,10 +427,13 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   PF_CUDA(cudaStreamSynchronize(stream_));
 
   action_ms_.assign(actions_.size(), 0.0);
+  action_start_ms_.assign(actions_.size(), 0.0);
   for (std::size_t i = 0; i < actions_.size(); ++i) {
-    float ms = 0.f;
+    float ms = 0.f, st = 0.f;
     cudaEventElapsedTime(&ms, ev_[2 * i], ev_[2 * i + 1]);
+    cudaEventElapsedTime(&st, ev_[0], ev_[2 * i]);
     action_ms_[i] = ms;
+    action_start_ms_[i] = st;
   }
   float bms = 0.f, oms = 0.f;
   if (!actions_.empty()) cudaEventElapsedTime(&bms, ev_[0], ev_[2 * actions_.size() - 1]);

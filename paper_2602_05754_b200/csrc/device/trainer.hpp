@@ -63,6 +63,8 @@ class Trainer {
   const std::vector<double>& plan_ratios() const { return plan_ratios_; }
   const pipefreeze::FreezePlan& plan() const { return plan_; }
   const std::vector<double>& action_ms() const { return action_ms_; }
+  // start of each action relative to the rank's first action of the last step (CUDA events)
+  const std::vector<double>& action_start_ms() const { return action_start_ms_; }
   const std::vector<pipefreeze::ActionId>& actions() const { return actions_; }
   std::vector<Stage*> local_stages();
   long long tokens_per_step() const;
@@ -121,6 +123,7 @@ class Trainer {
   pipefreeze::TimingProfile plan_profile_;
   double override_ratio_ = -1.0;
   std::vector<double> action_ms_;
+  std::vector<double> action_start_ms_;
   double lp_solve_ms_ = 0.0;
 };
 

@@ -199,6 +199,13 @@ class Trainer:
                "action_ms")
         return ms, kinds, mbs, st
 
+    def action_times(self):
+        """(start_ms, end_ms, kinds, microbatches, stages) of the last step's actions on this rank."""
+        ms, kinds, mbs, st = self.action_ms()
+        start = np.zeros(len(ms))
+        _check(self.lib.pf_trainer_action_starts(self._ctx, start.ctypes.data_as(ctypes.c_void_p)), "action_starts")
+        return start, start + ms, kinds, mbs, st
+
     def get_info(self) -> dict:
         i = PfTrainerInfo()
         _check(self.lib.pf_trainer_get_info(self._ctx, ctypes.byref(i)), "get_info")
