@@ -103,6 +103,8 @@ typedef struct pf_train_cfg {
   int apf, apf_every;
   float apf_alpha, apf_threshold;
   int device, mask_threads;
+  int hybrid;                 /* TimelyFreeze + APF masks via reconcile_mask (Alg. 2) */
+  float hybrid_unit_fraction; /* unit joins the APF base set when this fraction is eligible */
 } pf_train_cfg;
 
 typedef struct pf_step_result {
@@ -148,6 +150,9 @@ int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank);
 void* pf_trainer_stream(pf_ctx* ctx);
 /* Kernels launched by this library so far (all hand-written kernels, not the ATen attention). */
 long long pf_device_launch_count(void);
+/* Hybrid mode: the APF base set of local stage i from the last APF step (ceil(units/64) words);
+ * returns PF_ERR_DOMAIN before the first APF step. */
+int pf_trainer_apf_base(pf_ctx* ctx, int local_stage, uint64_t* out);
 /* The last step's frozen-unit masks of local stage i: M masks of ceil(units/64) words. */
 int pf_trainer_last_masks(pf_ctx* ctx, int local_stage, uint64_t* out);
 

@@ -18,7 +18,7 @@ class PfTrainCfg(ctypes.Structure):
     _fields_ = [("kind", c_int), ("ranks", c_int), ("stages_per_rank", c_int), ("microbatches", c_int),
                 ("rank", c_int), ("phases", c_int * 4), ("r_max", c_d), ("lr", c_d), ("seed", ctypes.c_uint64),
                 ("apf", c_int), ("apf_every", c_int), ("apf_alpha", c_f), ("apf_threshold", c_f),
-                ("device", c_int), ("mask_threads", c_int)]
+                ("device", c_int), ("mask_threads", c_int), ("hybrid", c_int), ("hybrid_unit_fraction", c_f)]
 
 
 class PfStepResult(ctypes.Structure):
@@ -61,6 +61,7 @@ DEVICE_SIGNATURES = {
     "pf_nccl_unique_ids": ([c_vp, c_int], c_int),
     "pf_attention_backend": ([], c_cp),
     "pf_trainer_action_starts": ([c_vp, c_vp], c_int),
+    "pf_trainer_apf_base": ([c_vp, c_int, c_vp], c_int),
     "pf_trainer_init_comm": ([c_vp, c_vp, c_int, c_int], c_int),
     "pf_device_launch_count": ([], c_ll),
 }

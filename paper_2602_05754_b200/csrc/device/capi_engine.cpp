@@ -177,6 +177,9 @@ int pf_trainer_create(const pf_model_cfg* m, const pf_train_cfg* c, pf_ctx** out
     tc.apf_threshold = c->apf_threshold;
     tc.device = c->device;
     tc.mask_threads = c->mask_threads;
+    tc.hybrid = c->hybrid != 0;
+    tc.hybrid_unit_fraction = c->hybrid_unit_fraction > 0.f ? c->hybrid_unit_fraction : 0.5f;
+    if (tc.hybrid && !tc.apf) return PF_ERR_CONFIG;  // hybrid needs the APF metric
     auto ctx = std::make_unique<pf_ctx>();
     ctx->trainer = std::make_unique<pf::Trainer>(mc, tc);
     *out = ctx.release();
@@ -331,6 +334,18 @@ extern "C" int pf_nccl_unique_ids(void* out, int count) {
       if (ncclGetUniqueId(&id) != ncclSuccess) return PF_ERR_NCCL;
       std::memcpy(static_cast<char*>(out) + static_cast<size_t>(k) * sizeof(id), &id, sizeof(id));
     }
+    return PF_OK;
+  });
+}
+
+extern "C" int pf_trainer_apf_base(pf_ctx* ctx, int i, uint64_t* out) {
+  return guard([&] {
+    if (!ctx || !out) return PF_ERR_INVALID;
+    auto st = ctx->trainer->local_stages();
+    if (i < 0 || i >= static_cast<int>(st.size())) return PF_ERR_INVALID;
+    if (!ctx->trainer->apf_base_ready()) return PF_ERR_DOMAIN;
+    const auto base = ctx->trainer->apf_base_mask(i);
+    std::copy(base.words().begin(), base.words().end(), out);
     return PF_OK;
   });
 }

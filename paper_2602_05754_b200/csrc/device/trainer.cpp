@@ -157,6 +157,7 @@ Trainer::~Trainer() {
   cudaFree(masks_dev_);
   cudaFreeHost(masks_host_);
   cudaFreeHost(loss_host_);
+  if (apf_pinned_) cudaFreeHost(apf_pinned_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -187,6 +188,21 @@ void Trainer::set_plan(const std::vector<double>& ratios) {
   if (static_cast<int>(ratios.size()) != S * M) throw std::invalid_argument("set_plan: need M*S ratios");
   plan_ratios_ = ratios;
   plan_ready_ = true;
+}
+
+FreezeMask Trainer::apf_base_mask(int li) const {
+  const Stage& st = *stages_[static_cast<std::size_t>(li)];
+  FreezeMask base(st.units());
+  if (static_cast<std::size_t>(li) >= apf_eligible_host_.size()) return base;
+  const auto& elig = apf_eligible_host_[static_cast<std::size_t>(li)];
+  for (const auto& m : st.unit_matrices())
+    for (int lu = 0; lu < m.units; ++lu) {
+      const int rb = lu / m.tiles_n, cb = lu % m.tiles_n;
+      const int elems = std::min(128, m.rows - rb * 128) * std::min(128, m.cols - cb * 128);
+      const int u = m.unit_offset + lu;
+      if (elig[static_cast<std::size_t>(u)] >= cfg_.hybrid_unit_fraction * static_cast<float>(elems)) base.set(u);
+    }
+  return base;
 }
 
 TimingProfile Trainer::measured_profile() const { return plan_profile_.all().empty() ? aggregate_monitoring(monitor_) : plan_profile_; }
@@ -285,7 +301,19 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
     const int units = stages_[li]->units();
     const int words = stages_[li]->words();
     std::vector<uint64_t> tmp(static_cast<std::size_t>(M) * static_cast<std::size_t>(words));
-    if (controller) {
+    const bool hybrid_cell = controller && cfg_.hybrid && apf_base_ready_ &&
+                             (phase == Phase::ProgressiveFreeze || phase == Phase::StableFreeze);
+    if (hybrid_cell) {
+      // Alg. 2: grow / shrink the APF base set to the cell's exact TimelyFreeze count
+      MaskStream ms(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
+      const FreezeMask base = apf_base_mask(static_cast<int>(li));
+      for (int m = 1; m <= M; ++m) {
+        Rng rng(cfg_.seed ^ (0x2545f4914f6cdd1dULL * static_cast<uint64_t>((t * 4096 + s) * 4096 + m)));
+        const auto mk = reconcile_mask(base, ms.cell_count(t, s, m), rng);
+        std::memcpy(tmp.data() + static_cast<std::size_t>(m - 1) * static_cast<std::size_t>(words), mk.words().data(),
+                    static_cast<size_t>(words) * 8);
+      }
+    } else if (controller) {
       MaskStream ms(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
       ms.stage_step_masks(t, s, tmp.data(), cfg_.mask_threads);
     } else {
@@ -424,7 +452,27 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
     PF_TRY(st->optimizer_step(static_cast<float>(cfg_.lr / M), t, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
   PF_CUDA(cudaEventRecord(ev_opt1_, stream_));
   PF_CUDA(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, stream_));
+  if (apf_step && cfg_.hybrid) {  // per-unit APF eligibility counts for the next steps' base sets
+    if (!apf_pinned_) {
+      PF_CUDA(cudaMallocHost(&apf_pinned_, static_cast<size_t>(std::max(1, units_total())) * 4));
+      apf_eligible_host_.resize(stages_.size());
+    }
+    int off = 0;
+    for (auto& st : stages_) {
+      PF_CUDA(cudaMemcpyAsync(apf_pinned_ + off, st->apf_eligible(), static_cast<size_t>(st->units()) * 4,
+                              cudaMemcpyDeviceToHost, stream_));
+      off += st->units();
+    }
+  }
   PF_CUDA(cudaStreamSynchronize(stream_));
+  if (apf_step && cfg_.hybrid) {
+    int off = 0;
+    for (std::size_t li = 0; li < stages_.size(); ++li) {
+      apf_eligible_host_[li].assign(apf_pinned_ + off, apf_pinned_ + off + stages_[li]->units());
+      off += stages_[li]->units();
+    }
+    apf_base_ready_ = true;
+  }
 
   action_ms_.assign(actions_.size(), 0.0);
   action_start_ms_.assign(actions_.size(), 0.0);

@@ -34,6 +34,11 @@ struct TrainConfig {
   int apf_every = 1;
   int device = 0;
   int mask_threads = 0;
+  // Hybrid TimelyFreeze + APF (paper Alg. 2): in the freezing phases each cell's
+  // mask is reconcile_mask(APF base set, floor(AFR * units)); a unit joins the
+  // base set when at least this fraction of its elements is APF-eligible.
+  bool hybrid = false;
+  float hybrid_unit_fraction = 0.5f;
 };
 
 struct StepResult {
@@ -72,6 +77,9 @@ class Trainer {
   pipefreeze::TimingProfile measured_profile() const;
   int units_total() const;
   cudaStream_t stream() const { return stream_; }
+  bool apf_base_ready() const { return apf_base_ready_; }
+  // APF base set of local stage li (hybrid mode) as a unit mask
+  pipefreeze::FreezeMask apf_base_mask(int li) const;
   // this step's frozen-unit masks of local stage li: M masks of (words + 1) uint64 each
   const uint64_t* masks_host(int li) const { return masks_host_ + mask_offsets_[static_cast<std::size_t>(li)]; }
 
@@ -124,6 +132,9 @@ class Trainer {
   double override_ratio_ = -1.0;
   std::vector<double> action_ms_;
   std::vector<double> action_start_ms_;
+  std::vector<std::vector<int>> apf_eligible_host_;  // [local stage][unit], last APF step
+  bool apf_base_ready_ = false;
+  int* apf_pinned_ = nullptr;
   double lp_solve_ms_ = 0.0;
 };
 

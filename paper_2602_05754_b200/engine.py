@@ -116,7 +116,8 @@ class Trainer:
     def __init__(self, shape: ModelShape, schedule: str = "gpipe", ranks: int = 1, stages_per_rank: int = 1,
                  microbatches: int = 8, rank: int = 0, phases=(2, 8, 10, 20), r_max: float = 0.8, lr: float = 1e-3,
                  seed: int = 42, apf: bool = False, apf_alpha: float = 0.9, apf_threshold: float = 1e-4,
-                 apf_every: int = 1, device: int = 0, mask_threads: int = 0):
+                 apf_every: int = 1, device: int = 0, mask_threads: int = 0, hybrid: bool = False,
+                 hybrid_unit_fraction: float = 0.5):
         self.lib = _native.device()
         self.shape = shape
         self.M = microbatches
@@ -130,6 +131,7 @@ class Trainer:
         c.r_max, c.lr, c.seed = r_max, lr, seed
         c.apf, c.apf_every, c.apf_alpha, c.apf_threshold = int(apf), apf_every, apf_alpha, apf_threshold
         c.device, c.mask_threads = device, mask_threads
+        c.hybrid, c.hybrid_unit_fraction = int(hybrid), hybrid_unit_fraction
         self.phases = tuple(phases)
         self._ctx = ctypes.c_void_p()
         _check(self.lib.pf_trainer_create(ctypes.byref(m), ctypes.byref(c), ctypes.byref(self._ctx)), "trainer_create")
@@ -219,6 +221,16 @@ class Trainer:
                                                  ctypes.byref(n), ctypes.byref(u)), "stage_buffers")
         return dict(master=ptrs[0].value, weights=ptrs[1].value, grad=ptrs[2].value, stamps=ptrs[3].value,
                     n_params=n.value, n_units=u.value)
+
+    def apf_base(self, local_stage: int = 0):
+        """Hybrid mode: APF base unit set of the last APF step (None before the first one)."""
+        units = self.stage_buffers(local_stage)["n_units"]
+        out = np.zeros(max(1, (units + 63) // 64), dtype=np.uint64)
+        rc = self.lib.pf_trainer_apf_base(self._ctx, local_stage, out.ctypes.data_as(ctypes.c_void_p))
+        if rc == _native.PF_ERR_DOMAIN:
+            return None
+        _check(rc, "apf_base")
+        return out[: (units + 63) // 64]
 
     def last_masks(self, local_stage: int = 0) -> np.ndarray:
         units = self.stage_buffers(local_stage)["n_units"]

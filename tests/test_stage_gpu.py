@@ -144,6 +144,42 @@ def test_multi_stage_rank_matches_torch_reference(cuda, stages_per_rank):
     tr.close()
 
 
+def test_hybrid_apf_reconcile_masks(cuda):
+    """Hybrid TimelyFreeze+APF: each freezing-phase cell holds exactly floor(AFR*units) frozen units
+    and relates to the APF base set as reconcile_mask (Alg. 2) does: superset when growing,
+    subset when shrinking."""
+    from paper_2602_05754_b200 import pipefreeze as pf
+    from paper_2602_05754_b200.engine import PRESETS, Trainer
+
+    shape = PRESETS["tiny"]
+    M, phases = 2, (2, 8, 10, 14)
+    # threshold 1.0: every element whose EMA update direction is not constant is eligible
+    tr = Trainer(shape, "gpipe", 1, 1, M, phases=phases, r_max=0.8, lr=1e-2, seed=3, apf=True,
+                 apf_threshold=0.999, hybrid=True, hybrid_unit_fraction=0.5)
+    units = tr.stage_buffers(0)["n_units"]
+    checked = 0
+    for t in range(1, phases[3] + 1):
+        base = tr.apf_base(0)  # base used by this step = last step's APF result
+        r = tr.step(t)
+        if t <= phases[1] or base is None:
+            continue
+        plan = tr.get_plan()
+        bset = set(np.flatnonzero(pf.unpack_mask(base, units)).tolist())
+        ms = tr.last_masks(0)
+        for m in range(M):
+            target = int(np.floor(pf.actual_freeze_ratio(t, pf.PhasePlan(*phases), plan["ratios"][m]) * units))
+            got = set(np.flatnonzero(pf.unpack_mask(ms[m], units)).tolist())
+            assert len(got) == target
+            if target >= len(bset):
+                assert bset <= got
+            else:
+                assert got <= bset
+            checked += 1
+        assert np.isfinite(r["loss"])
+    assert checked >= 4
+    tr.close()
+
+
 def test_controller_phases_plan_and_bit_exact_masks(cuda):
     import torch  # noqa: F401
 
