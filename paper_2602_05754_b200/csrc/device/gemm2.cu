@@ -1,4 +1,4 @@
-// K1 / K2 on a CTA pair: tcgen05.mma.cta_group::2, 256 x BN tiles.
+// K1 / K2 on a CTA pair: tcgen05.mma.cta_group::2, 256 x BN tiles, stream-K.
 //
 // Same contract as gemm.cu (C (op)= alpha * A . B^T, A K-major, B K- or
 // MN-major) but each tile is computed by two CTAs of a cluster on two SMs of
@@ -13,11 +13,19 @@
 // multicasts the empty barrier to both CTAs), TMEM double buffer (leader
 // commit multicasts tmem-full to both; both CTAs' epilogues arrive on the
 // leader's tmem-empty barrier through shared::cluster addresses).
+//
+// Stream-K: when the tile count leaves the last wave of clusters mostly idle
+// (the N = hidden GEMMs of a LLaMA layer: 128 tiles on 74 clusters), the
+// tile x k-block iteration space is split evenly over the clusters. A tile is
+// then cut at most once: the cluster whose range STARTS inside it computes the
+// tail first and parks the fp32 partial in a workspace; the cluster whose range
+// ENDS inside it computes the head last, adds the parked partial and writes C.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "pf_device_internal.hpp"
 #include "ptx.cuh"
@@ -52,7 +60,68 @@ struct alignas(64) Params2 {
   int M, N, K;
   int tiles_m, tiles_n;
   float alpha;
+  int streamk;   // 0: one tile per work item; 1: even split of tile x k-block iterations
+  float* ws;     // stream-K partials: [cluster][rank][128][BN] fp32
+  int* flags;    // stream-K: [cluster][rank] == epoch once the partial is parked
+  int epoch;
 };
+
+struct Seg {
+  int tile, kb0, kb1;
+};
+
+// Work items of one cluster, identical for the producer, MMA and epilogue roles.
+struct SegIter {
+  long long next, end;  // stream-K iteration cursor
+  int t;                // data-parallel tile cursor
+};
+
+__device__ __forceinline__ bool next_seg(const Params2& p, int cluster, int nclusters, int num_kb, SegIter& it,
+                                         Seg& s) {
+  const int ntiles = p.tiles_m * p.tiles_n;
+  if (!p.streamk) {
+    if (it.t >= ntiles) return false;
+    s = Seg{it.t, 0, num_kb};
+    it.t += nclusters;
+    return true;
+  }
+  if (it.next >= it.end) return false;
+  s.tile = static_cast<int>(it.next / num_kb);
+  s.kb0 = static_cast<int>(it.next - static_cast<long long>(s.tile) * num_kb);
+  s.kb1 = static_cast<int>(std::min<long long>(num_kb, s.kb0 + (it.end - it.next)));
+  it.next += s.kb1 - s.kb0;
+  return true;
+}
+
+__device__ __forceinline__ SegIter seg_begin(const Params2& p, int cluster, int nclusters, int num_kb) {
+  SegIter it{0, 0, cluster};
+  if (p.streamk) {
+    const long long total = static_cast<long long>(p.tiles_m) * p.tiles_n * num_kb;
+    const long long q = (total + nclusters - 1) / nclusters;
+    it.next = std::min<long long>(total, static_cast<long long>(cluster) * q);
+    it.end = std::min<long long>(total, it.next + q);
+  }
+  return it;
+}
+
+__device__ __forceinline__ void decode(const Params2& p, int t, int& tm, int& tn) {
+  const int group_size = GROUP_M * p.tiles_n;
+  const int g = t / group_size;
+  const int first_m = g * GROUP_M;
+  const int gm = min(p.tiles_m - first_m, GROUP_M);
+  const int local = t - g * group_size;
+  tm = first_m + local % gm;
+  tn = local / gm;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int BN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -78,7 +147,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
-  const int ntiles = p.tiles_m * p.tiles_n;
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -105,27 +173,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto decode = [&](int t, int& tm, int& tn) {
-    const int group_size = GROUP_M * p.tiles_n;
-    const int g = t / group_size;
-    const int first_m = g * GROUP_M;
-    const int gm = min(p.tiles_m - first_m, GROUP_M);
-    const int local = t - g * group_size;
-    tm = first_m + local % gm;
-    tn = local / gm;
-  };
-
   if (warp == 0) {
     if (lane == 0) {
       // ---------------------------------------------------------- producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < ntiles; t += nclusters) {
+      SegIter it = seg_begin(p, cluster, nclusters, num_kb);
+      Seg sg;
+      while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
         int tm, tn;
-        decode(t, tm, tn);
+        decode(p, sg.tile, tm, tn);
         const int m0 = tm * BM2 + static_cast<int>(rank) * 128;
         const int n0 = tn * BN + static_cast<int>(rank) * (BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
@@ -152,11 +212,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int abuf = 0;
       uint32_t aphase = 0;
-      for (int t = cluster; t < ntiles; t += nclusters) {
+      SegIter it = seg_begin(p, cluster, nclusters, num_kb);
+      Seg sg;
+      while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -166,7 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t adesc = sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb != sg.kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit_pair_multicast(&empty_bar[stage], 0x3);
           if (++stage == STAGES) {
@@ -187,9 +249,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
     int abuf = 0;
     uint32_t aphase = 0;
-    for (int t = cluster; t < ntiles; t += nclusters) {
+    SegIter it = seg_begin(p, cluster, nclusters, num_kb);
+    Seg sg;
+    while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
       int tm, tn;
-      decode(t, tm, tn);
+      decode(p, sg.tile, tm, tn);
+      // stream-K roles: a tail (kb0 > 0) parks its partial in this cluster's slot; a head
+      // (kb1 < num_kb) adds the partial parked by the next cluster, whose range starts
+      // with this tile's tail, then writes C.
+      const bool park = sg.kb0 > 0;
+      const bool fixup = sg.kb0 == 0 && sg.kb1 < num_kb;
+      const int slot = park ? cluster : cluster + 1;
+      float* ws_rows = p.streamk ? p.ws + (static_cast<long long>(slot) * 2 + rank) * 128 * BN : nullptr;
+      if (fixup) {
+        if (threadIdx.x == 64) {
+          const int* f = p.flags + slot * 2 + rank;
+          while (ld_acquire(f) != p.epoch) __nanosleep(64);
+        }
+        named_bar_sync(1, 128);
+      }
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
       const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
@@ -201,11 +279,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                static_cast<uint32_t>(abuf * BN + c * 32),
                            r);
         tmem_ld_wait();
-        const int gcol = tn * BN + c * 32;
-        if (!row_ok || gcol >= p.N) continue;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (park) {  // raw fp32 partial, row-major within the slot
+          float4* w = reinterpret_cast<float4*>(ws_rows + static_cast<long long>(row) * BN + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          continue;
+        }
+        if (fixup) {
+          const float4* w = reinterpret_cast<const float4*>(ws_rows + static_cast<long long>(row) * BN + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 o = __ldcg(w + j);
+            v[4 * j] += o.x;
+            v[4 * j + 1] += o.y;
+            v[4 * j + 2] += o.z;
+            v[4 * j + 3] += o.w;
+          }
+        }
+        const int gcol = tn * BN + c * 32;
+        if (!row_ok || gcol >= p.N) continue;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
         const bool full = gcol + 32 <= p.N;
         if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
           __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
@@ -252,6 +349,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+      if (park) {  // publish the partial once all 128 epilogue threads wrote their rows
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) {
+          __threadfence();
+          st_release(p.flags + slot * 2 + rank, p.epoch);
+        }
+      }
       abuf ^= 1;
       if (abuf == 0) aphase ^= 1;
     }
@@ -266,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 template <int BN, bool B_MN, int EPI>
-int launch2(const Params2& p, cudaStream_t stream) {
+int launch2(const Params2& p, int clusters, cudaStream_t stream) {
   using Cfg = Cfg2<BN>;
   auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
   static bool attr_set = false;
@@ -275,12 +379,31 @@ int launch2(const Params2& p, cudaStream_t stream) {
       return PF_ERR_CUDA;
     attr_set = true;
   }
-  const int ntiles = p.tiles_m * p.tiles_n;
-  const int clusters = std::min(ntiles, num_sms() / 2);
   if (clusters <= 0) return PF_OK;
   kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
+
+// Stream-K workspace (per device process; kernels on one stream use it in order).
+struct StreamKState {
+  float* ws = nullptr;
+  int* flags = nullptr;
+  int slots = 0;
+  int epoch = 0;
+};
+
+StreamKState& sk_state() {
+  static StreamKState st;
+  return st;
+}
+
+int streamk_mode() {
+  static int mode = [] {
+    const char* e = std::getenv("PF_GEMM_STREAMK");
+    return e ? std::atoi(e) : -1;  // -1 auto, 0 off, 1 force
+  }();
+  return mode;
 }
 
 }  // namespace
@@ -303,11 +426,43 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.tiles_m = (M + BM2 - 1) / BM2;
   p.tiles_n = (N + BN - 1) / BN;
   p.alpha = alpha;
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int max_clusters = num_sms() / 2;
+  int clusters = std::min(ntiles, max_clusters);
+  // stream-K when the data-parallel last wave would leave > 8% of the clusters idle
+  const int num_kb = (K + BK - 1) / BK;
+  const int waves = (ntiles + max_clusters - 1) / max_clusters;
+  const double eff = static_cast<double>(ntiles) / (static_cast<double>(waves) * max_clusters);
+  const int mode = streamk_mode();
+  const bool sk = ntiles > max_clusters && num_kb >= 8 && (mode == 1 || (mode < 0 && eff < 0.92));
+  if (sk) {
+    StreamKState& st = sk_state();
+    clusters = max_clusters;
+    if (st.slots < clusters + 1) {
+      if (st.ws) cudaFree(st.ws);
+      if (st.flags) cudaFree(st.flags);
+      if (cudaMalloc(&st.ws, static_cast<size_t>(clusters + 1) * 2 * 128 * BN * sizeof(float)) != cudaSuccess ||
+          cudaMalloc(&st.flags, static_cast<size_t>(clusters + 1) * 2 * sizeof(int)) != cudaSuccess)
+        return PF_ERR_CUDA;
+      cudaMemset(st.flags, 0, static_cast<size_t>(clusters + 1) * 2 * sizeof(int));
+      st.slots = clusters + 1;
+    }
+    p.streamk = 1;
+    p.ws = st.ws;
+    p.flags = st.flags;
+    p.epoch = ++st.epoch;
+  }
   const bool bmn = B.mn_major;
   switch (epi) {
-    case EPI_STORE_BF16: return bmn ? launch2<BN, true, EPI_STORE_BF16>(p, stream) : launch2<BN, false, EPI_STORE_BF16>(p, stream);
-    case EPI_ADD_BF16: return bmn ? launch2<BN, true, EPI_ADD_BF16>(p, stream) : launch2<BN, false, EPI_ADD_BF16>(p, stream);
-    case EPI_STORE_F32: return bmn ? launch2<BN, true, EPI_STORE_F32>(p, stream) : launch2<BN, false, EPI_STORE_F32>(p, stream);
+    case EPI_STORE_BF16:
+      return bmn ? launch2<BN, true, EPI_STORE_BF16>(p, clusters, stream)
+                 : launch2<BN, false, EPI_STORE_BF16>(p, clusters, stream);
+    case EPI_ADD_BF16:
+      return bmn ? launch2<BN, true, EPI_ADD_BF16>(p, clusters, stream)
+                 : launch2<BN, false, EPI_ADD_BF16>(p, clusters, stream);
+    case EPI_STORE_F32:
+      return bmn ? launch2<BN, true, EPI_STORE_F32>(p, clusters, stream)
+                 : launch2<BN, false, EPI_STORE_F32>(p, clusters, stream);
     default: return PF_ERR_INVALID;
   }
 }

@@ -129,3 +129,27 @@ def test_gemm_cta_pair(cuda, b_mn, epi, M, N, K):
     if epi == 1:
         ref = ref + C0.float()
     assert (C.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-2
+
+
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+@pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512)])
+def test_gemm_cta_pair_stream_k(cuda, b_mn, epi, M, N, K):
+    """Tile counts just above the 74 clusters select stream-K (split tiles, parked fp32 partials)."""
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(M * 3 + N + K + epi)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn((K, N) if b_mn else (N, K), generator=g).to(torch.bfloat16).cuda()
+    ref = _ref(A, 0, B, b_mn)
+    for _ in range(2):  # back-to-back launches reuse the workspace (epoch-tagged flags)
+        if epi == 3:
+            C = torch.zeros(M, N, dtype=torch.float32, device=cuda)
+            _run(A, 0, B, b_mn, C, M, N, K, epi=3, bn=512)
+            assert (C - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+            continue
+        C0 = torch.randn(M, N, generator=g).to(torch.bfloat16).cuda() if epi == 1 else torch.zeros(M, N, dtype=torch.bfloat16, device=cuda)
+        C = C0.clone()
+        _run(A, 0, B, b_mn, C, M, N, K, epi=epi, bn=512)
+        r = ref + C0.float() if epi == 1 else ref
+        assert (C.float() - r).abs().max().item() <= 1e-2 * r.abs().max().item() + 1e-2
