@@ -44,6 +44,21 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
                      const int* unit_list, const int* unit_count, int max_units,
                      int* unit_stamp, int stamp_offset, int stamp, void* stream);
 
+/* K1 gate|up projection with the SwiGLU activation fused in the CTA-pair epilogue:
+ * gu[T, 2*ffn] = h[T, K] . Wgu^T (bf16, Wgu rows interleave 128-blocks [gate b | up b]),
+ * a[T, ffn] = silu(gate) * up from the bf16-rounded gu (== pf_swiglu_fwd(gu)). ffn % 128 == 0. */
+int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw, void* gu, void* a, int T, int ffn,
+                   int K, void* stream);
+
+/* K2 down-projection backward with the SwiGLU backward fused in the CTA-pair epilogue:
+ * d_act = dY[T, K] . Wd[K, ffn] (Wd stored [K][ffn], read MN-major), rounded to bf16, then
+ * dgu = swiglu_bwd(gu, d_act) in the interleaved gate|up layout (== pf_swiglu_bwd). */
+int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw, const void* gu, void* dgu, int T,
+                    int ffn, int K, void* stream);
+
+/* Stream-K split of the CTA-pair GEMM: -1 auto, 0 off (default), 1 force. */
+int pf_gemm_set_streamk(int mode);
+
 int pf_device_sm_count(void);
 const char* pf_device_last_error(void);  /* message of the last failed kernel-level call */
 const char* pf_engine_last_error(void);  /* message of the last failed engine / K4-K7 call */
@@ -81,6 +96,7 @@ int pf_apf_update(float* ema, float* ema_abs, const float* delta, float* score, 
 int pf_rmsnorm_fwd(const void* x, const void* g, void* y, float* rstd, int T, int h, float eps, void* stream);
 int pf_rmsnorm_bwd(const void* x, const void* g, const float* rstd, const void* dy, const void* residual, void* dx,
                    float* dg, int T, int h, void* stream);
+/* gu rows hold gate|up interleaved in 128-blocks: gate j at column (j/128)*256 + j%128, up j 128 later. */
 int pf_swiglu_fwd(const void* gu, void* a, int T, int ffn, void* stream);
 int pf_swiglu_bwd(const void* gu, const void* da, void* dgu, int T, int ffn, void* stream);
 int pf_rope_fwd(void* qkv, int T, int seq, int nh, int nkv, int hd, float theta, void* stream);

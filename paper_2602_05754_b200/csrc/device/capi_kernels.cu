@@ -44,6 +44,32 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
                                     static_cast<cudaStream_t>(stream)));
 }
 
+int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw, void* gu, void* a, int T, int ffn,
+                   int K, void* stream) {
+  if (!h || !Wgu || !gu || !a || ffn % 128 != 0) return PF_ERR_INVALID;
+  pf::GemmOut c{gu, 2LL * ffn};
+  c.aux = a;
+  c.ldaux = ffn;
+  return record(pf::gemm_bf16_pair(pf::GemmOperand{h, ldh, false}, pf::GemmOperand{Wgu, ldw, false}, c, T, 2 * ffn,
+                                   K, 1.0f, pf::EPI_SWIGLU, static_cast<cudaStream_t>(stream)));
+}
+
+int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw, const void* gu, void* dgu, int T,
+                    int ffn, int K, void* stream) {
+  if (!dY || !Wd || !gu || !dgu || ffn % 128 != 0) return PF_ERR_INVALID;
+  pf::GemmOut c{dgu, 2LL * ffn};
+  c.residual = gu;
+  c.ldr = 2LL * ffn;
+  return record(pf::gemm_bf16_pair(pf::GemmOperand{dY, ldy, false}, pf::GemmOperand{Wd, ldw, true}, c, T, ffn, K,
+                                   1.0f, pf::EPI_DSWIGLU, static_cast<cudaStream_t>(stream)));
+}
+
+int pf_gemm_set_streamk(int mode) {
+  if (mode < -1 || mode > 1) return PF_ERR_INVALID;
+  pf::gemm_set_streamk(mode);
+  return PF_OK;
+}
+
 int pf_device_sm_count(void) { return pf::num_sms(); }
 
 const char* pf_device_last_error(void) { return g_last_error.c_str(); }

@@ -40,7 +40,9 @@ namespace {
 constexpr int BM2 = 256;  // rows per CTA pair
 constexpr int BK = 64;
 constexpr int GROUP_M = 8;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, alternating 32-column chunks
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;
 
 template <int BN>
 struct Cfg2 {
@@ -60,6 +62,10 @@ struct alignas(64) Params2 {
   int M, N, K;
   int tiles_m, tiles_n;
   float alpha;
+  const __nv_bfloat16* R;  // EPI_ADD_BF16 residual source (defaults to C)
+  long long ldr;
+  __nv_bfloat16* aux;  // EPI_SWIGLU activation output
+  long long ldaux;
   int streamk;   // 0: one tile per work item; 1: even split of tile x k-block iterations
   float* ws;     // stream-K partials: [cluster][rank][128][BN] fp32
   int* flags;    // stream-K: [cluster][rank] == epoch once the partial is parked
@@ -156,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 2 * 128);
+      mbar_init(&tempty_bar[b], 2 * kEpiThreads);
     }
     fence_barrier_init();
   }
@@ -243,7 +249,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    const int q = warp & 3;
+    const int q = warp & 3;                // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;      // which alternate 32-column chunks it drains
     const int row = q * 32 + static_cast<int>(lane);
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
@@ -266,14 +273,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int* f = p.flags + slot * 2 + rank;
           while (ld_acquire(f) != p.epoch) __nanosleep(64);
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
+      }
+      const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
+      const bool row_ok = grow < p.M;
+      if constexpr (EPI == EPI_DSWIGLU) {
+        // acc = d(act) for activation columns [tn*BN, tn*BN + BN); gate/up of those columns sit
+        // in gu at (j / 128) * 256 + j % 128 (+128). They do not depend on the accumulator, so
+        // chunk 0 is fetched while the MMAs still run and chunk c+1 while chunk c computes.
+        // Same arithmetic as swiglu_bwd_kernel on the bf16-rounded d(act). No stream-K.
+        uint4 gb[4], ub[4];
+        auto fetch = [&](int c) {
+          const int gcol = tn * BN + c * 32;
+          if (!row_ok || gcol >= p.N) return;
+          const long long gc = grow * p.ldr + ((gcol >> 7) << 8) + (gcol & 127);
+          const uint4* g4 = reinterpret_cast<const uint4*>(p.R + gc);
+          const uint4* u4 = reinterpret_cast<const uint4*>(p.R + gc + 128);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            gb[j] = __ldcs(g4 + j);
+            ub[j] = __ldcs(u4 + j);
+          }
+        };
+        fetch(half);
+        mbar_wait(&tfull_bar[abuf], aphase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(abuf * BN + c * 32),
+                             r);
+          const uint4 gcur[4] = {gb[0], gb[1], gb[2], gb[3]};
+          const uint4 ucur[4] = {ub[0], ub[1], ub[2], ub[3]};
+          if (c + 2 < BN / 32) fetch(c + 2);
+          tmem_ld_wait();
+          const int gcol = tn * BN + c * 32;
+          if (!row_ok || gcol >= p.N) continue;
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + ((gcol >> 7) << 8) + (gcol & 127);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gcur[j]);
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ucur[j]);
+            uint32_t dgw[4], duw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 g = __bfloat1622float2(g2[i]);
+              const float2 u = __bfloat1622float2(u2[i]);
+              const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * j + 2 * i]),
+                                                                        p.alpha * __uint_as_float(r[8 * j + 2 * i + 1])));
+              const float s0 = sigmoid_fast(g.x), s1 = sigmoid_fast(g.y);
+              duw[i] = pack_bf16x2(d.x * (g.x * s0), d.y * (g.y * s1));
+              dgw[i] = pack_bf16x2(d.x * u.x * s0 * (1.f + g.x * (1.f - s0)), d.y * u.y * s1 * (1.f + g.y * (1.f - s1)));
+            }
+            reinterpret_cast<uint4*>(dst)[j] = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
+            reinterpret_cast<uint4*>(dst + 128)[j] = make_uint4(duw[0], duw[1], duw[2], duw[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+        continue;
       }
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
-      const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
-      const bool row_ok = grow < p.M;
+      if constexpr (EPI == EPI_SWIGLU) {
+        // columns [0, BN/2) of the tile are gate j, [BN/2, BN) up j (host: N % BN == 0, no stream-K);
+        // the activation uses the bf16-rounded gate/up exactly as swiglu_fwd_kernel does.
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half; c < BN / 64; c += 2) {
+          uint32_t rg[32], ru[32];
+          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(abuf * BN);
+          tmem_ld_32x32b_x32(tbase + c * 32, rg);
+          tmem_ld_32x32b_x32(tbase + BN / 2 + c * 32, ru);
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          __nv_bfloat16* gp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + tn * BN + c * 32;
+          __nv_bfloat16* ap = p.aux + grow * p.ldaux + tn * (BN / 2) + c * 32;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t gw[4], uw[4], aw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const __nv_bfloat162 g2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(rg[8 * j + 2 * i]),
+                                                              p.alpha * __uint_as_float(rg[8 * j + 2 * i + 1]));
+              const __nv_bfloat162 u2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(ru[8 * j + 2 * i]),
+                                                              p.alpha * __uint_as_float(ru[8 * j + 2 * i + 1]));
+              const float2 g = __bfloat1622float2(g2);
+              const float2 u = __bfloat1622float2(u2);
+              const float a0 = g.x * sigmoid_fast(g.x) * u.x;
+              const float a1 = g.y * sigmoid_fast(g.y) * u.y;
+              gw[i] = *reinterpret_cast<const uint32_t*>(&g2);
+              uw[i] = *reinterpret_cast<const uint32_t*>(&u2);
+              aw[i] = pack_bf16x2(a0, a1);
+            }
+            reinterpret_cast<uint4*>(gp)[j] = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+            reinterpret_cast<uint4*>(gp + BN / 2)[j] = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+            reinterpret_cast<uint4*>(ap)[j] = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+        continue;
+      }
+#pragma unroll 1
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(abuf * BN + c * 32),
@@ -306,15 +413,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool full = gcol + 32 <= p.N;
         if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
           __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
+          const __nv_bfloat16* rp = p.R + grow * p.ldr + gcol;
           if (full) {
             uint4* c4 = reinterpret_cast<uint4*>(cp);
+            const uint4* r4 = reinterpret_cast<const uint4*>(rp);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               float w[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) w[i] = v[j * 8 + i];
               if constexpr (EPI == EPI_ADD_BF16) {
-                const uint4 old = c4[j];
+                const uint4 old = r4[j];
                 const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -335,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) {
               if (gcol + i < p.N) {
                 float w = v[i];
-                if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(cp[i]);
+                if constexpr (EPI == EPI_ADD_BF16) w += __bfloat162float(rp[i]);
                 cp[i] = __float2bfloat16_rn(w);
               }
             }
@@ -350,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
       if (park) {  // publish the partial once all 128 epilogue threads wrote their rows
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == 64) {
           __threadfence();
           st_release(p.flags + slot * 2 + rank, p.epoch);
@@ -369,8 +478,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// Co-resident CTA pairs for this kernel (stream-K waits across clusters, so its
+// grid must never exceed what the GPU can hold at once).
 template <int BN, bool B_MN, int EPI>
-int launch2(const Params2& p, int clusters, cudaStream_t stream) {
+int max_active_clusters() {
+  using Cfg = Cfg2<BN>;
+  static int n = -1;
+  if (n < 0) {
+    auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (num_sms() / 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / 2;
+    }
+    n = std::min(c, num_sms() / 2);
+  }
+  return n;
+}
+
+template <int BN, bool B_MN, int EPI>
+int launch2(Params2 p, int clusters, cudaStream_t stream) {
   using Cfg = Cfg2<BN>;
   auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
   static bool attr_set = false;
@@ -379,6 +518,7 @@ int launch2(const Params2& p, int clusters, cudaStream_t stream) {
       return PF_ERR_CUDA;
     attr_set = true;
   }
+  clusters = std::min(clusters, max_active_clusters<BN, B_MN, EPI>());
   if (clusters <= 0) return PF_OK;
   kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
   count_launch();
@@ -398,15 +538,20 @@ StreamKState& sk_state() {
   return st;
 }
 
-int streamk_mode() {
+int& streamk_mode_ref() {
+  // Default off: measured on B200 (profiles/r1_gemm_bench_streamk.txt) the split tiles'
+  // fixup waits and lost L2 locality cost more than the idle last wave they recover.
   static int mode = [] {
     const char* e = std::getenv("PF_GEMM_STREAMK");
-    return e ? std::atoi(e) : -1;  // -1 auto, 0 off, 1 force
+    return e ? std::atoi(e) : 0;  // -1 auto, 0 off, 1 force
   }();
   return mode;
 }
+int streamk_mode() { return streamk_mode_ref(); }
 
 }  // namespace
+
+void gemm_set_streamk(int mode) { streamk_mode_ref() = mode; }
 
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
                    int epi, cudaStream_t stream) {
@@ -420,6 +565,12 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   if (rc) return rc;
   p.C = C.ptr;
   p.ldc = C.ld;
+  p.R = static_cast<const __nv_bfloat16*>(C.residual ? C.residual : C.ptr);
+  p.ldr = C.residual ? C.ldr : C.ld;
+  p.aux = static_cast<__nv_bfloat16*>(C.aux);
+  p.ldaux = C.ldaux;
+  if (epi == EPI_SWIGLU && (N % BN != 0 || B.mn_major || !C.aux)) return PF_ERR_INVALID;
+  if (epi == EPI_DSWIGLU && (N % 128 != 0 || !B.mn_major || !C.residual)) return PF_ERR_INVALID;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -434,7 +585,9 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   const int waves = (ntiles + max_clusters - 1) / max_clusters;
   const double eff = static_cast<double>(ntiles) / (static_cast<double>(waves) * max_clusters);
   const int mode = streamk_mode();
-  const bool sk = ntiles > max_clusters && num_kb >= 8 && (mode == 1 || (mode < 0 && eff < 0.92));
+  // Clusters at different k offsets share little L2; keep stream-K to operands that fit in L2.
+  const bool fits_l2 = (static_cast<long long>(M) + N) * K * 2 <= (48LL << 20);
+  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && ntiles > max_clusters && num_kb >= 8 && (mode == 1 || (mode < 0 && eff < 0.92 && fits_l2));
   if (sk) {
     StreamKState& st = sk_state();
     clusters = max_clusters;
@@ -463,6 +616,10 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     case EPI_STORE_F32:
       return bmn ? launch2<BN, true, EPI_STORE_F32>(p, clusters, stream)
                  : launch2<BN, false, EPI_STORE_F32>(p, clusters, stream);
+    case EPI_SWIGLU:
+      return launch2<BN, false, EPI_SWIGLU>(p, clusters, stream);
+    case EPI_DSWIGLU:
+      return launch2<BN, true, EPI_DSWIGLU>(p, clusters, stream);
     default: return PF_ERR_INVALID;
   }
 }

@@ -426,7 +426,12 @@ __global__ void rope_bwd_pack_kernel(const AttnGradView g, __nv_bfloat16* __rest
   store8(d + j + half, b);
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+__device__ __forceinline__ float sigmoidf_(float x) { return sigmoid_fast(x); }
+
+// gate|up rows are interleaved in 128-blocks (kGuBlock): gu column of gate j is
+// (j / 128) * 256 + j % 128, up j sits 128 further (so one 256-wide GEMM tile holds
+// matching gate and up columns and the GEMM epilogue can apply SwiGLU).
+__device__ __forceinline__ int gate_col(int j) { return ((j >> 7) << 8) + (j & 127); }
 
 // grid.y = token, x covers the row in 8-element chunks (no 64-bit index division)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int T,
@@ -436,8 +441,9 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (c >= ffn) return;
     float g[8], u[8], o[8];
-    load8(gu + t * 2 * ffn + c, g);
-    load8(gu + t * 2 * ffn + ffn + c, u);
+    const __nv_bfloat16* row = gu + t * 2 * ffn + gate_col(c);
+    load8(row, g);
+    load8(row + 128, u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
     store8(a + t * ffn + c, o);
@@ -451,8 +457,9 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (c >= ffn) return;
     float g[8], u[8], d[8], dg[8], du[8];
-    load8(gu + t * 2 * ffn + c, g);
-    load8(gu + t * 2 * ffn + ffn + c, u);
+    const long long off = t * 2 * ffn + gate_col(c);
+    load8(gu + off, g);
+    load8(gu + off + 128, u);
     load8(da + t * ffn + c, d);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -461,8 +468,8 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
       du[k] = d[k] * silu;
       dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
     }
-    store8(dgu + t * 2 * ffn + c, dg);
-    store8(dgu + t * 2 * ffn + ffn + c, du);
+    store8(dgu + off, dg);
+    store8(dgu + off + 128, du);
   }
 }
 
@@ -641,14 +648,14 @@ int launch_rope_bwd_pack(const AttnGradView& g, __nv_bfloat16* dqkv, const float
 }
 
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s) {
-  if (ffn % 8) return PF_ERR_INVALID;
+  if (ffn % 128) return PF_ERR_INVALID;
   swiglu_fwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, a, T, ffn);
   return status();
 }
 
 int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
                       cudaStream_t s) {
-  if (ffn % 8) return PF_ERR_INVALID;
+  if (ffn % 128) return PF_ERR_INVALID;
   swiglu_bwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, da, dgu, T, ffn);
   return status();
 }

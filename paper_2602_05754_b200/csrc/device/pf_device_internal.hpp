@@ -13,6 +13,8 @@ enum GemmEpilogue : int {
   EPI_ADD_BF16 = 1,    // C = bf16(C + alpha * acc)
   EPI_ACC_F32 = 2,     // fp32 C; first touch of a 128x128 unit in this step stores, later add
   EPI_STORE_F32 = 3,   // C = alpha * acc (fp32)
+  EPI_SWIGLU = 4,      // CTA pair only: C = bf16(gate|up), aux = silu(gate) * up (interleaved 128-blocks)
+  EPI_DSWIGLU = 5,     // CTA pair only: acc = d(act) [M][ffn]; residual = gu; C = d(gate|up), same layout as gu
 };
 
 struct GemmOperand {
@@ -27,6 +29,10 @@ struct GemmOut {
   int* unit_stamp = nullptr;  // EPI_ACC_F32 only
   int stamp_offset = 0;
   int stamp = 0;
+  const void* residual = nullptr;  // EPI_ADD_BF16 on the CTA-pair kernel: C = R + acc (R may differ from C)
+  long long ldr = 0;
+  void* aux = nullptr;  // EPI_SWIGLU: [M][N/2] bf16 activation
+  long long ldaux = 0;
 };
 
 int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,
@@ -57,6 +63,9 @@ int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, in
 // K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
                    int epi, cudaStream_t stream);
+
+// Stream-K for the CTA-pair kernel: -1 auto, 0 off (default, or PF_GEMM_STREAMK), 1 force.
+void gemm_set_streamk(int mode);
 
 int num_sms();
 

@@ -34,6 +34,17 @@ bool use_pair() {
   return on;
 }
 
+// SwiGLU forward/backward in the CTA-pair GEMM epilogues only with PF_FUSE_SWIGLU=1: measured
+// on B200 (tools/swiglu_bench.py) the per-row epilogue loads of gu stall on latency and the
+// fused backward is slower than GEMM + the HBM-roofline swiglu_bwd kernel.
+bool fuse_swiglu() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_FUSE_SWIGLU");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int gemm_any(const GemmOperand& A, const GemmOperand& B, void* C, long long ldc, int M, int N, int K, int epi,
              cudaStream_t s) {
   if (use_pair() && M >= 256 && N >= 256) return gemm_bf16_pair(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, s);
@@ -46,10 +57,57 @@ int gemm_fwd(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long
   return gemm_any(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, C, ldc, M, N, K, epi, s);
 }
 
+// Y = R + A . W^T (residual add fused in the epilogue on the CTA-pair kernel)
+int gemm_fwd_resid(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* C,
+                   const __nv_bfloat16* R, long long ld, int M, int N, int K, cudaStream_t s) {
+  if (use_pair() && M >= 256 && N >= 256) {
+    GemmOut out{C, ld};
+    out.residual = R;
+    out.ldr = ld;
+    return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, N, K, 1.0f, EPI_ADD_BF16,
+                          s);
+  }
+  if (cudaMemcpyAsync(C, R, static_cast<size_t>(M) * ld * 2, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return PF_ERR_CUDA;
+  return gemm_bf16(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, GemmOut{C, ld}, M, N, K, 1.0f,
+                   EPI_ADD_BF16, N >= 256 ? 256 : 128, s);
+}
+
+// gu = h . Wgu^T (gate|up interleaved in 128-row blocks) and a = silu(gate) * up; on the
+// CTA-pair kernel the activation is computed in the GEMM epilogue from the same tile.
+int gemm_fwd_swiglu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* gu,
+                    __nv_bfloat16* a, int M, int ffn, int K, cudaStream_t s) {
+  if (use_pair() && fuse_swiglu() && M >= 256 && (2 * ffn) % 256 == 0) {
+    GemmOut out{gu, 2LL * ffn};
+    out.aux = a;
+    out.ldaux = ffn;
+    return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, 2 * ffn, K, 1.0f,
+                          EPI_SWIGLU, s);
+  }
+  const int rc = gemm_fwd(A, lda, W, ldw, gu, 2LL * ffn, M, 2 * ffn, K, EPI_STORE_BF16, s);
+  return rc ? rc : launch_swiglu_fwd(gu, a, M, ffn, s);
+}
+
 int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
             int M, int N, int K, int epi, cudaStream_t s) {
   // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
   return gemm_any(GemmOperand{dY, ldy, false}, GemmOperand{W, ldw, true}, C, ldc, M, N, K, epi, s);
+}
+
+// d(gate|up) from d(out) = dY . Wd: on the CTA-pair kernel the SwiGLU backward runs in the
+// epilogue (d(act) never reaches HBM); otherwise GEMM into d_act then swiglu_bwd.
+int gemm_dx_dswiglu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* Wd, long long ldw,
+                    const __nv_bfloat16* gu, __nv_bfloat16* d_act, __nv_bfloat16* dgu, int M, int ffn, int K,
+                    cudaStream_t s) {
+  if (use_pair() && fuse_swiglu() && M >= 256 && ffn >= 256) {
+    GemmOut out{dgu, 2LL * ffn};
+    out.residual = gu;
+    out.ldr = 2LL * ffn;
+    return gemm_bf16_pair(GemmOperand{dY, ldy, false}, GemmOperand{Wd, ldw, true}, out, M, ffn, K, 1.0f,
+                          EPI_DSWIGLU, s);
+  }
+  const int rc = gemm_dx(dY, ldy, Wd, ldw, d_act, ffn, M, ffn, K, EPI_STORE_BF16, s);
+  return rc ? rc : launch_swiglu_bwd(gu, d_act, dgu, M, ffn, s);
 }
 
 }  // namespace
@@ -226,15 +284,12 @@ int Stage::forward(int slot, int microbatch, const int* tokens, const int* targe
                     &ao, &ald, s));
     L.attn_out = static_cast<const __nv_bfloat16*>(ao);
     L.attn_ld = ald;
-    PF_CUDA(cudaMemcpyAsync(L.x2, L.x, act, cudaMemcpyDeviceToDevice, s));
-    PF_TRY(gemm_fwd(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, h, T, h,
-                    cfg_.attn_dim(), EPI_ADD_BF16, s));
+    PF_TRY(gemm_fwd_resid(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, L.x, h, T, h,
+                          cfg_.attn_dim(), s));
     PF_TRY(launch_rmsnorm_fwd(L.x2, weights_ + P.g2.offset, L.h2, L.rstd2, T, h, cfg_.norm_eps, s));
-    PF_TRY(gemm_fwd(L.h2, h, weights_ + P.wgu.offset, h, L.gu, 2 * cfg_.ffn, T, 2 * cfg_.ffn, h, EPI_STORE_BF16, s));
-    PF_TRY(launch_swiglu_fwd(L.gu, L.a, T, cfg_.ffn, s));
+    PF_TRY(gemm_fwd_swiglu(L.h2, h, weights_ + P.wgu.offset, h, L.gu, L.a, T, cfg_.ffn, h, s));
     __nv_bfloat16* next = li + 1 < nl ? sl.layers[static_cast<std::size_t>(li + 1)].x : sl.x_out;
-    PF_CUDA(cudaMemcpyAsync(next, L.x2, act, cudaMemcpyDeviceToDevice, s));
-    PF_TRY(gemm_fwd(L.a, cfg_.ffn, weights_ + P.wd.offset, cfg_.ffn, next, h, T, h, cfg_.ffn, EPI_ADD_BF16, s));
+    PF_TRY(gemm_fwd_resid(L.a, cfg_.ffn, weights_ + P.wd.offset, cfg_.ffn, next, L.x2, h, T, h, cfg_.ffn, s));
   }
   if (spec_.last) {
     if (!targets || !loss_sum) return PF_ERR_INVALID;
@@ -277,8 +332,7 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
     SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
     const LayerParams& P = layers_[static_cast<std::size_t>(li)];
     // MLP
-    PF_TRY(gemm_dx(dcur, h, weights_ + P.wd.offset, ffn, d_a_, ffn, T, ffn, h, EPI_STORE_BF16, s));
-    PF_TRY(launch_swiglu_bwd(L.gu, d_a_, d_gu_, T, ffn, s));
+    PF_TRY(gemm_dx_dswiglu(dcur, h, weights_ + P.wd.offset, ffn, L.gu, d_a_, d_gu_, T, ffn, h, s));
     PF_TRY(gemm_dx(d_gu_, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
     PF_TRY(launch_rmsnorm_bwd(L.x2, weights_ + P.g2.offset, L.rstd2, d_h_, dcur, d_x2_, grad_ + P.g2.offset, T, h, s));
     // attention

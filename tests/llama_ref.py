@@ -40,6 +40,15 @@ def rope(x, seq, theta):
     return torch.cat([a * c - b * s, b * c + a * s], dim=-1)
 
 
+def gate_index(ffn, device=None):
+    """Columns of gate j in the gate|up output: rows of Wgu interleave 128-blocks
+    [gate b | up b] (kernels.cu gate_col); up j is 128 columns further."""
+    import torch
+
+    j = torch.arange(ffn, device=device)
+    return (j // 128) * 256 + j % 128
+
+
 def stage_loss(params: dict, shape, layers: range, tokens: torch.Tensor, targets: torch.Tensor, first: bool,
                last: bool, x_in: torch.Tensor | None = None):
     """tokens/targets: [T] int64 of one microbatch. Returns (loss or output activations)."""
@@ -62,7 +71,8 @@ def stage_loss(params: dict, shape, layers: range, tokens: torch.Tensor, targets
         x = x + att @ p("wo").t()
         h2 = rms(x, p("g2"), shape.norm_eps)
         gu = h2 @ p("wgu").t()
-        g, u = gu[:, : shape.ffn], gu[:, shape.ffn:]
+        gi = gate_index(shape.ffn, gu.device)
+        g, u = gu[:, gi], gu[:, gi + 128]
         x = x + (F.silu(g) * u) @ p("wd").t()
     if not last:
         return x

@@ -135,7 +135,16 @@ def test_gemm_cta_pair(cuda, b_mn, epi, M, N, K):
 @pytest.mark.parametrize("epi", [0, 1, 3])
 @pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512)])
 def test_gemm_cta_pair_stream_k(cuda, b_mn, epi, M, N, K):
-    """Tile counts just above the 74 clusters select stream-K (split tiles, parked fp32 partials)."""
+    """Forced stream-K (split tiles, parked fp32 partials) on tile counts just above the 74 clusters."""
+    lib, nat = _lib()
+    nat.check(lib.pf_gemm_set_streamk(1), "pf_gemm_set_streamk")
+    try:
+        _stream_k_case(cuda, b_mn, epi, M, N, K)
+    finally:
+        lib.pf_gemm_set_streamk(0)
+
+
+def _stream_k_case(cuda, b_mn, epi, M, N, K):
     import torch
 
     g = torch.Generator(device="cpu").manual_seed(M * 3 + N + K + epi)

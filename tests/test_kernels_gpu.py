@@ -71,14 +71,67 @@ def test_swiglu_fwd_bwd(cuda):
     da = bf(torch.randn(T, ffn, generator=g)).cuda()
     a = torch.empty(T, ffn, dtype=torch.bfloat16, device=cuda)
     chk(lib().pf_swiglu_fwd(gu.data_ptr(), a.data_ptr(), T, ffn, sp()))
+    from llama_ref import gate_index
+
+    gi = gate_index(ffn, cuda)
     guf = gu.float().requires_grad_(True)
-    ref = F.silu(guf[:, :ffn]) * guf[:, ffn:]
+    ref = F.silu(guf[:, gi]) * guf[:, gi + 128]
     ref.backward(da.float())
     dgu = torch.empty_like(gu)
     chk(lib().pf_swiglu_bwd(gu.data_ptr(), da.data_ptr(), dgu.data_ptr(), T, ffn, sp()))
     torch.cuda.synchronize()
     assert (a.float() - ref).abs().max().item() < 1e-2 * ref.abs().max().item() + 1e-2
     assert (dgu.float() - guf.grad).abs().max().item() < 1e-2 * guf.grad.abs().max().item() + 1e-2
+
+
+def test_gemm_swiglu_epilogue_matches_unfused(cuda):
+    """Pair-GEMM SwiGLU epilogue == GEMM (bf16 store) followed by swiglu_fwd, bit for bit."""
+    import torch
+
+    T, D, ffn = 512, 256, 768
+    g = torch.Generator().manual_seed(9)
+    h = bf(torch.randn(T, D, generator=g)).cuda()
+    w = bf(torch.randn(2 * ffn, D, generator=g) * 0.1).cuda()
+    gu = torch.empty(T, 2 * ffn, dtype=torch.bfloat16, device=cuda)
+    a = torch.empty(T, ffn, dtype=torch.bfloat16, device=cuda)
+    chk(lib().pf_gemm_swiglu(h.data_ptr(), h.stride(0), w.data_ptr(), w.stride(0), gu.data_ptr(), a.data_ptr(), T,
+                             ffn, D, sp()))
+    gu_ref = torch.empty_like(gu)
+    chk(lib().pf_gemm_bf16(h.data_ptr(), 0, h.stride(0), w.data_ptr(), 0, w.stride(0), gu_ref.data_ptr(),
+                           gu_ref.stride(0), T, 2 * ffn, D, 1.0, 0, 512, None, 0, sp()))
+    a_ref = torch.empty_like(a)
+    chk(lib().pf_swiglu_fwd(gu_ref.data_ptr(), a_ref.data_ptr(), T, ffn, sp()))
+    torch.cuda.synchronize()
+    assert torch.equal(gu, gu_ref)
+    assert torch.equal(a, a_ref)
+
+
+@pytest.mark.parametrize("T,ffn,D", [(512, 768, 256), (4096, 2048, 1024)])
+def test_gemm_dswiglu_epilogue_matches_unfused(cuda, T, ffn, D):
+    """Pair-GEMM SwiGLU-backward epilogue == GEMM (bf16 d_act) followed by swiglu_bwd, bit for bit
+    (stream-K sums the split K in another order, so that run is checked to bf16 tolerance)."""
+    import torch
+
+    g = torch.Generator().manual_seed(T + ffn)
+    dy = bf(torch.randn(T, D, generator=g)).cuda()
+    wd = bf(torch.randn(D, ffn, generator=g) * 0.1).cuda()
+    gu = bf(torch.randn(T, 2 * ffn, generator=g)).cuda()
+    dgus = []
+    for mode in (0, 1):  # data-parallel tiles, then forced stream-K (fixup before the epilogue math)
+        chk(lib().pf_gemm_set_streamk(mode))
+        dgu = torch.empty_like(gu)
+        chk(lib().pf_gemm_dswiglu(dy.data_ptr(), dy.stride(0), wd.data_ptr(), wd.stride(0), gu.data_ptr(),
+                                  dgu.data_ptr(), T, ffn, D, sp()))
+        dgus.append(dgu)
+    chk(lib().pf_gemm_set_streamk(0))
+    da = torch.empty(T, ffn, dtype=torch.bfloat16, device=cuda)
+    chk(lib().pf_gemm_bf16(dy.data_ptr(), 0, dy.stride(0), wd.data_ptr(), 1, wd.stride(0), da.data_ptr(),
+                           da.stride(0), T, ffn, D, 1.0, 0, 512, None, 0, sp()))
+    dgu_ref = torch.empty_like(gu)
+    chk(lib().pf_swiglu_bwd(gu.data_ptr(), da.data_ptr(), dgu_ref.data_ptr(), T, ffn, sp()))
+    torch.cuda.synchronize()
+    assert torch.equal(dgus[0], dgu_ref)
+    assert (dgus[1].float() - dgu_ref.float()).abs().max().item() <= 1e-2 * dgu_ref.float().abs().max().item()
 
 
 def test_rope_matches_reference(cuda):
