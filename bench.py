@@ -203,6 +203,7 @@ def _config(args, shape) -> dict:
             "global_batch": args.microbatches * shape.micro_batch, "seq_len": shape.seq,
             "microbatches": args.microbatches, "micro_batch": shape.micro_batch, "schedule": args.schedule,
             "parallelism": f"pp{args.gpus}", "r_max": args.r_max, "phases": list(args.phases),
+            "optimizer": args.optimizer,
             "l2": "inputs larger than L2 (>2 GB of weights and activations touched per step)"}
 
 
@@ -225,7 +226,7 @@ def run_ours(args) -> None:
     M = args.microbatches
     phases = tuple(args.phases)
     tr = Trainer(shape, args.schedule, world, 1, M, rank=rank, phases=phases, r_max=args.r_max, lr=1e-4,
-                 seed=args.seed, device=local)
+                 seed=args.seed, device=local, optimizer=args.optimizer, weight_decay=0.1 if args.optimizer == "adamw" else 0.0)
     lib = _native.device()
     if world > 1:
         tr.init_comm()
@@ -361,6 +362,8 @@ def main() -> None:
     ap.add_argument("--r-max", type=float, default=0.8)
     ap.add_argument("--phases", type=int, nargs=4, default=[2, 8, 10, 10000])
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--optimizer", choices=["sgd", "adamw"], default="sgd",
+                    help="sgd = the reference's masked update (sandbox.cpp:250); adamw = the paper's optimizer")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

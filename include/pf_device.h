@@ -121,6 +121,9 @@ typedef struct pf_train_cfg {
   int device, mask_threads;
   int hybrid;                 /* TimelyFreeze + APF masks via reconcile_mask (Alg. 2) */
   float hybrid_unit_fraction; /* unit joins the APF base set when this fraction is eligible */
+  int optimizer;              /* 0 SGD (reference sandbox.cpp:250), 1 AdamW (lr above; per-unit bias correction) */
+  double beta1, beta2;        /* AdamW only (bias corrections 1 - beta^k are formed in fp64) */
+  float eps, weight_decay;
 } pf_train_cfg;
 
 typedef struct pf_step_result {
@@ -170,6 +173,9 @@ long long pf_device_launch_count(void);
  * returns PF_ERR_DOMAIN before the first APF step. */
 int pf_trainer_apf_base(pf_ctx* ctx, int local_stage, uint64_t* out);
 /* The last step's frozen-unit masks of local stage i: M masks of ceil(units/64) words. */
+/* AdamW state of a local stage (NULL pointers before the first AdamW step): fp32 m, v
+ * (indexed like master) and the per-unit step counts. */
+int pf_trainer_optim_state(pf_ctx* ctx, int local_stage, void** m, void** v, void** unit_steps);
 int pf_trainer_last_masks(pf_ctx* ctx, int local_stage, uint64_t* out);
 
 #ifdef __cplusplus

@@ -18,7 +18,8 @@ class PfTrainCfg(ctypes.Structure):
     _fields_ = [("kind", c_int), ("ranks", c_int), ("stages_per_rank", c_int), ("microbatches", c_int),
                 ("rank", c_int), ("phases", c_int * 4), ("r_max", c_d), ("lr", c_d), ("seed", ctypes.c_uint64),
                 ("apf", c_int), ("apf_every", c_int), ("apf_alpha", c_f), ("apf_threshold", c_f),
-                ("device", c_int), ("mask_threads", c_int), ("hybrid", c_int), ("hybrid_unit_fraction", c_f)]
+                ("device", c_int), ("mask_threads", c_int), ("hybrid", c_int), ("hybrid_unit_fraction", c_f),
+                ("optimizer", c_int), ("beta1", c_d), ("beta2", c_d), ("eps", c_f), ("weight_decay", c_f)]
 
 
 class PfStepResult(ctypes.Structure):
@@ -60,6 +61,8 @@ DEVICE_SIGNATURES = {
     "pf_trainer_stage_buffers": ([c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                   ctypes.POINTER(c_vp), ctypes.POINTER(c_ll), ctypes.POINTER(c_int)], c_int),
     "pf_trainer_last_masks": ([c_vp, c_int, c_vp], c_int),
+    "pf_trainer_optim_state": ([c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)],
+                               c_int),
     "pf_trainer_stream": ([c_vp], c_vp),
     "pf_nccl_unique_ids": ([c_vp, c_int], c_int),
     "pf_attention_backend": ([], c_cp),

@@ -179,6 +179,16 @@ int pf_trainer_create(const pf_model_cfg* m, const pf_train_cfg* c, pf_ctx** out
     tc.mask_threads = c->mask_threads;
     tc.hybrid = c->hybrid != 0;
     tc.hybrid_unit_fraction = c->hybrid_unit_fraction > 0.f ? c->hybrid_unit_fraction : 0.5f;
+    if (c->optimizer < 0 || c->optimizer > 1) return PF_ERR_CONFIG;
+    tc.optim.adamw = c->optimizer;
+    if (c->optimizer == 1) {
+      tc.optim.beta1 = c->beta1;
+      tc.optim.beta2 = c->beta2;
+      tc.optim.eps = c->eps;
+      tc.optim.weight_decay = c->weight_decay;
+      if (!(c->beta1 >= 0.f && c->beta1 < 1.f && c->beta2 >= 0.f && c->beta2 < 1.f && c->eps > 0.f))
+        return PF_ERR_CONFIG;
+    }
     if (tc.hybrid && !tc.apf) return PF_ERR_CONFIG;  // hybrid needs the APF metric
     auto ctx = std::make_unique<pf_ctx>();
     ctx->trainer = std::make_unique<pf::Trainer>(mc, tc);
@@ -302,6 +312,18 @@ int pf_trainer_stage_buffers(pf_ctx* ctx, int i, void** master, void** weights, 
     if (stamps) *stamps = st[static_cast<size_t>(i)]->unit_stamps();
     if (n_params) *n_params = st[static_cast<size_t>(i)]->param_count();
     if (n_units) *n_units = st[static_cast<size_t>(i)]->units();
+    return PF_OK;
+  });
+}
+
+int pf_trainer_optim_state(pf_ctx* ctx, int i, void** m, void** v, void** unit_steps) {
+  return guard([&] {
+    if (!ctx) return PF_ERR_INVALID;
+    auto st = ctx->trainer->local_stages();
+    if (i < 0 || i >= static_cast<int>(st.size())) return PF_ERR_INVALID;
+    if (m) *m = st[static_cast<size_t>(i)]->adam_m();
+    if (v) *v = st[static_cast<size_t>(i)]->adam_v();
+    if (unit_steps) *unit_steps = st[static_cast<size_t>(i)]->unit_steps();
     return PF_OK;
   });
 }

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -125,6 +126,44 @@ __global__ void __launch_bounds__(kBlock) mask_to_lists_kernel(const uint64_t* _
 }
 
 // ------------------------------------------------------------------ K6 (+K4 fused)
+struct AdamCoef {
+  float step_size;  // lr / bc1
+  float rsqrt_bc2;  // 1 / sqrt(bc2)
+  float decay;      // 1 - lr * weight_decay
+};
+
+__device__ __forceinline__ AdamCoef adam_coef(const OptimArgs& a, int k) {
+  const double bc1 = 1.0 - pow(a.beta1_d, static_cast<double>(k));
+  const double bc2 = 1.0 - pow(a.beta2_d, static_cast<double>(k));
+  return AdamCoef{static_cast<float>(a.lr / bc1), static_cast<float>(1.0 / sqrt(bc2)), 1.f - a.lr * a.weight_decay};
+}
+
+// One AdamW element (torch.optim.AdamW, foreach=False order): theta *= 1 - lr*wd;
+// m, v EMAs of g; theta -= (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps). Returns the change.
+__device__ __forceinline__ float adamw1(const OptimArgs& a, const AdamCoef& c, float g, float& m, float& v,
+                                        float& th) {
+  const float old = th;
+  th *= c.decay;
+  m = a.beta1 * m + a.one_minus_beta1 * g;
+  v = a.beta2 * v + a.one_minus_beta2 * g * g;
+  th -= c.step_size * m / (sqrtf(v) * c.rsqrt_bc2 + a.eps);
+  return th - old;
+}
+
+__device__ __forceinline__ float4 adamw4(const OptimArgs& a, const AdamCoef& c, long long e, const float4 G,
+                                         float4& th) {
+  float4 m = *reinterpret_cast<const float4*>(a.adam_m + e);
+  float4 v = *reinterpret_cast<const float4*>(a.adam_v + e);
+  float4 d;
+  d.x = adamw1(a, c, a.scale * G.x, m.x, v.x, th.x);
+  d.y = adamw1(a, c, a.scale * G.y, m.y, v.y, th.y);
+  d.z = adamw1(a, c, a.scale * G.z, m.z, v.z, th.z);
+  d.w = adamw1(a, c, a.scale * G.w, m.w, v.w, th.w);
+  *reinterpret_cast<float4*>(a.adam_m + e) = m;
+  *reinterpret_cast<float4*>(a.adam_v + e) = v;
+  return d;
+}
+
 __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int red[kBlock / 32];
@@ -132,6 +171,8 @@ __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArg
   for (int u = blockIdx.x; u < a.total_units; u += gridDim.x) {
     const bool touched = a.unit_stamp[u] == a.stamp;
     if (!touched && !apf) continue;  // frozen in every microbatch: no update (sandbox.cpp:250)
+    AdamCoef ac{};
+    if (a.adamw && touched) ac = adam_coef(a, a.unit_steps[u] + 1);
     const UnitMatrix& m = find_matrix(a.mats, a.nmats, u);
     const int lu = u - m.unit_offset;
     const int rb = lu / m.tiles_n, cb = lu - rb * m.tiles_n;
@@ -147,11 +188,15 @@ __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArg
         if (touched) {
           const float4 g = __ldcs(reinterpret_cast<const float4*>(a.grad + e));
           float4 th = *reinterpret_cast<const float4*>(a.master + e);
-          d = make_float4(-a.scale * g.x, -a.scale * g.y, -a.scale * g.z, -a.scale * g.w);
-          th.x += d.x;
-          th.y += d.y;
-          th.z += d.z;
-          th.w += d.w;
+          if (a.adamw) {
+            d = adamw4(a, ac, e, g, th);
+          } else {
+            d = make_float4(-a.scale * g.x, -a.scale * g.y, -a.scale * g.z, -a.scale * g.w);
+            th.x += d.x;
+            th.y += d.y;
+            th.z += d.z;
+            th.w += d.w;
+          }
           *reinterpret_cast<float4*>(a.master + e) = th;
           uint2 packed;
           packed.x = pack_bf16x2(th.x, th.y);
@@ -177,6 +222,10 @@ __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArg
           eligible += below(E.x, A.x) + below(E.y, A.y) + below(E.z, A.z) + below(E.w, A.w);
         }
       }
+    }
+    if (a.adamw && touched) {  // every thread has read the old count (adam_coef) before this write
+      __syncthreads();
+      if (threadIdx.x == 0) a.unit_steps[u] += 1;
     }
     if (apf && a.apf_eligible != nullptr) {
       eligible = warp_isum(eligible);
@@ -585,6 +634,38 @@ int launch_sgd_dense(float* master, __nv_bfloat16* w, const float* g, long long 
   if (n <= 0) return PF_OK;
   if (n % 4) return PF_ERR_INVALID;
   sgd_dense_kernel<<<grid_for((n / 4 + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, g, n / 4, scale);
+  return status();
+}
+
+__global__ void adamw_dense_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
+                                   const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                                   long long n, const OptimArgs a, const AdamCoef c) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float th = master[i], mi = m[i], vi = v[i];
+    adamw1(a, c, a.scale * g[i], mi, vi, th);
+    master[i] = th;
+    m[i] = mi;
+    v[i] = vi;
+    w[i] = __float2bfloat16_rn(th);
+  }
+}
+
+int launch_adamw_dense(float* master, __nv_bfloat16* w, const float* g, float* m, float* v, long long n, float scale,
+                       float lr, float beta1, float beta2, float one_minus_beta1, float one_minus_beta2, float eps,
+                       float weight_decay, double bc1, double bc2, cudaStream_t s) {
+  if (n <= 0) return PF_OK;
+  OptimArgs a{};
+  a.scale = scale;
+  a.lr = lr;
+  a.beta1 = beta1;
+  a.beta2 = beta2;
+  a.one_minus_beta1 = one_minus_beta1;
+  a.one_minus_beta2 = one_minus_beta2;
+  a.eps = eps;
+  a.weight_decay = weight_decay;
+  const AdamCoef c{static_cast<float>(lr / bc1), static_cast<float>(1.0 / std::sqrt(bc2)), 1.f - lr * weight_decay};
+  adamw_dense_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, g, m, v, n, a, c);
   return status();
 }
 

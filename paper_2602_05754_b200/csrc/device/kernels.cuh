@@ -44,12 +44,27 @@ struct OptimArgs {
   float apf_threshold;
   int* apf_eligible;              // per unit count (may be nullptr)
   long long apf_elem_base;        // elem offset of the APF buffers (param index of first unit matrix)
+  // AdamW (decoupled weight decay, torch.optim.AdamW order) instead of SGD when adamw != 0:
+  // g = scale * G; per-unit step counts give each unit its own bias correction, so a unit
+  // frozen in every microbatch keeps theta, m, v and its step count unchanged.
+  int adamw;
+  float* adam_m;                  // fp32 first moment, same indexing as master
+  float* adam_v;                  // fp32 second moment
+  int* unit_steps;                // per-unit AdamW step count
+  float lr, beta1, beta2, eps, weight_decay;
+  float one_minus_beta1, one_minus_beta2;  // formed in fp64, then rounded (1 - 0.99f loses 1e-6)
+  double beta1_d, beta2_d;       // bias corrections 1 - beta^k in fp64 (fp32 loses ~1e-6 to cancellation)
 };
 int launch_masked_sgd_units(const OptimArgs& a, cudaStream_t s);
 
 // dense parameters (norm gains, embedding): theta -= scale * G, bf16 copy
 int launch_sgd_dense(float* master, __nv_bfloat16* weights, const float* grad, long long n, float scale,
                      cudaStream_t s);
+
+// dense parameters under AdamW: global step bias corrections bc1 = 1 - beta1^k, bc2 = 1 - beta2^k
+int launch_adamw_dense(float* master, __nv_bfloat16* weights, const float* grad, float* m, float* v, long long n,
+                       float scale, float lr, float beta1, float beta2, float one_minus_beta1,
+                       float one_minus_beta2, float eps, float weight_decay, double bc1, double bc2, cudaStream_t s);
 
 // ---- K4 standalone APF update (reference apf_update, freezectl.cpp:147-156)
 int launch_apf_update(float* ema, float* ema_abs, const float* delta, float* score, long long n, float alpha,

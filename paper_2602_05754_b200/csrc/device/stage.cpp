@@ -378,7 +378,8 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
   return PF_OK;
 }
 
-int Stage::optimizer_step(float scale, int stamp, bool apf, float apf_alpha, float apf_threshold, cudaStream_t s) {
+int Stage::optimizer_step(const OptimCfg& oc, int microbatches, int stamp, bool apf, float apf_alpha,
+                          float apf_threshold, cudaStream_t s) {
   if (apf && !apf_ema_) {
     PF_CUDA(cudaMalloc(&apf_ema_, static_cast<size_t>(n_unit_params_) * 4));
     PF_CUDA(cudaMalloc(&apf_ema_abs_, static_cast<size_t>(n_unit_params_) * 4));
@@ -389,13 +390,25 @@ int Stage::optimizer_step(float scale, int stamp, bool apf, float apf_alpha, flo
     PF_CUDA(cudaMemsetAsync(apf_ema_, 0, static_cast<size_t>(n_unit_params_) * 4, s));
     PF_CUDA(cudaMemsetAsync(apf_ema_abs_, 0, static_cast<size_t>(n_unit_params_) * 4, s));
   }
+  if (oc.adamw && !adam_m_) {
+    PF_CUDA(cudaMalloc(&adam_m_, static_cast<size_t>(n_params_) * 4));
+    PF_CUDA(cudaMalloc(&adam_v_, static_cast<size_t>(n_params_) * 4));
+    PF_CUDA(cudaMalloc(&unit_steps_, static_cast<size_t>(std::max(1, total_units_)) * 4));
+    allocations_.push_back(adam_m_);
+    allocations_.push_back(adam_v_);
+    allocations_.push_back(unit_steps_);
+    PF_CUDA(cudaMemsetAsync(adam_m_, 0, static_cast<size_t>(n_params_) * 4, s));
+    PF_CUDA(cudaMemsetAsync(adam_v_, 0, static_cast<size_t>(n_params_) * 4, s));
+    PF_CUDA(cudaMemsetAsync(unit_steps_, 0, static_cast<size_t>(std::max(1, total_units_)) * 4, s));
+  }
+  const float inv_m = 1.0f / static_cast<float>(microbatches);
   OptimArgs a{};
   a.master = master_;
   a.weights = weights_;
   a.grad = grad_;
   a.unit_stamp = stamps_;
   a.stamp = stamp;
-  a.scale = scale;
+  a.scale = oc.adamw ? inv_m : oc.lr * inv_m;
   a.mats = mats_dev_;
   a.nmats = static_cast<int>(mats_.size());
   a.total_units = total_units_;
@@ -405,9 +418,29 @@ int Stage::optimizer_step(float scale, int stamp, bool apf, float apf_alpha, flo
   a.apf_threshold = apf_threshold;
   a.apf_eligible = apf ? apf_eligible_ : nullptr;
   a.apf_elem_base = 0;
+  a.adamw = oc.adamw;
+  a.adam_m = adam_m_;
+  a.adam_v = adam_v_;
+  a.unit_steps = unit_steps_;
+  a.lr = oc.lr;
+  a.beta1 = static_cast<float>(oc.beta1);
+  a.beta2 = static_cast<float>(oc.beta2);
+  a.beta1_d = oc.beta1;
+  a.beta2_d = oc.beta2;
+  a.one_minus_beta1 = static_cast<float>(1.0 - oc.beta1);
+  a.one_minus_beta2 = static_cast<float>(1.0 - oc.beta2);
+  a.eps = oc.eps;
+  a.weight_decay = oc.weight_decay;
   PF_TRY(launch_masked_sgd_units(a, s));
-  return launch_sgd_dense(master_ + dense_begin_, weights_ + dense_begin_, grad_ + dense_begin_,
-                          n_params_ - dense_begin_, scale, s);
+  const long long nd = n_params_ - dense_begin_;
+  if (!oc.adamw)
+    return launch_sgd_dense(master_ + dense_begin_, weights_ + dense_begin_, grad_ + dense_begin_, nd, a.scale, s);
+  ++dense_steps_;
+  const double bc1 = 1.0 - std::pow(oc.beta1, dense_steps_);
+  const double bc2 = 1.0 - std::pow(oc.beta2, dense_steps_);
+  return launch_adamw_dense(master_ + dense_begin_, weights_ + dense_begin_, grad_ + dense_begin_,
+                            adam_m_ + dense_begin_, adam_v_ + dense_begin_, nd, inv_m, oc.lr, a.beta1, a.beta2,
+                            a.one_minus_beta1, a.one_minus_beta2, oc.eps, oc.weight_decay, bc1, bc2, s);
 }
 
 }  // namespace pf

@@ -81,6 +81,12 @@ struct Slot {  // one in-flight microbatch
   int microbatch = 0;
 };
 
+struct OptimCfg {
+  int adamw = 0;  // 0: SGD (the reference's optimizer), 1: AdamW
+  float lr = 0.f, eps = 1e-8f, weight_decay = 0.f;
+  double beta1 = 0.9, beta2 = 0.999;
+};
+
 class Stage {
  public:
   Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device);
@@ -97,7 +103,10 @@ class Stage {
   // receives the gradient of the stage input (ignored on the first stage).
   int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
                __nv_bfloat16* dx_out, int stamp, cudaStream_t s);
-  int optimizer_step(float scale, int stamp, bool apf, float apf_alpha, float apf_threshold, cudaStream_t s);
+  // SGD: theta -= lr * G / M (sandbox.cpp:250). AdamW: g = G / M into per-unit-step AdamW.
+  // Units frozen in every microbatch of the step (stamp != this step) are not touched.
+  int optimizer_step(const OptimCfg& oc, int microbatches, int stamp, bool apf, float apf_alpha,
+                     float apf_threshold, cudaStream_t s);
   int zero_dense_grads(cudaStream_t s);
 
   const __nv_bfloat16* output(int slot) const { return slots_[slot].x_out; }
@@ -117,6 +126,9 @@ class Stage {
   int* unit_stamps() const { return stamps_; }
   int* apf_eligible() const { return apf_eligible_; }
   float* apf_ema() const { return apf_ema_; }
+  float* adam_m() const { return adam_m_; }
+  float* adam_v() const { return adam_v_; }
+  int* unit_steps() const { return unit_steps_; }
   float* apf_ema_abs() const { return apf_ema_abs_; }
   int last_unfrozen_units() const { return last_unfrozen_; }
 
@@ -142,6 +154,10 @@ class Stage {
   float* apf_ema_ = nullptr;
   float* apf_ema_abs_ = nullptr;
   int* apf_eligible_ = nullptr;
+  float* adam_m_ = nullptr;
+  float* adam_v_ = nullptr;
+  int* unit_steps_ = nullptr;
+  int dense_steps_ = 0;
   int* unit_lists_ = nullptr;
   int* unit_counts_ = nullptr;
   float2* rope_ = nullptr;

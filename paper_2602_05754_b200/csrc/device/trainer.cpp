@@ -448,8 +448,10 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   // ---- masked optimizer step: theta -= (eta / M) * sum_m U_m . g_m
   PF_CUDA(cudaEventRecord(ev_opt0_, stream_));
   const bool apf_step = cfg_.apf && (t % std::max(1, cfg_.apf_every) == 0);
+  OptimCfg oc = cfg_.optim;
+  oc.lr = static_cast<float>(cfg_.lr);
   for (auto& st : stages_)
-    PF_TRY(st->optimizer_step(static_cast<float>(cfg_.lr / M), t, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
+    PF_TRY(st->optimizer_step(oc, M, t, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
   PF_CUDA(cudaEventRecord(ev_opt1_, stream_));
   PF_CUDA(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, stream_));
   if (apf_step && cfg_.hybrid) {  // per-unit APF eligibility counts for the next steps' base sets

@@ -39,6 +39,8 @@ struct TrainConfig {
   // base set when at least this fraction of its elements is APF-eligible.
   bool hybrid = false;
   float hybrid_unit_fraction = 0.5f;
+  // optimizer: SGD (reference, sandbox.cpp:250) or AdamW (the paper's optimizer; lr as above)
+  OptimCfg optim{};
 };
 
 struct StepResult {

@@ -117,7 +117,8 @@ class Trainer:
                  microbatches: int = 8, rank: int = 0, phases=(2, 8, 10, 20), r_max: float = 0.8, lr: float = 1e-3,
                  seed: int = 42, apf: bool = False, apf_alpha: float = 0.9, apf_threshold: float = 1e-4,
                  apf_every: int = 1, device: int = 0, mask_threads: int = 0, hybrid: bool = False,
-                 hybrid_unit_fraction: float = 0.5):
+                 hybrid_unit_fraction: float = 0.5, optimizer: str = "sgd", betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.0):
         self.lib = _native.device()
         self.shape = shape
         self.M = microbatches
@@ -132,6 +133,10 @@ class Trainer:
         c.apf, c.apf_every, c.apf_alpha, c.apf_threshold = int(apf), apf_every, apf_alpha, apf_threshold
         c.device, c.mask_threads = device, mask_threads
         c.hybrid, c.hybrid_unit_fraction = int(hybrid), hybrid_unit_fraction
+        if optimizer not in ("sgd", "adamw"):
+            raise ValueError(f"optimizer must be 'sgd' or 'adamw', got {optimizer!r}")
+        c.optimizer = 1 if optimizer == "adamw" else 0
+        c.beta1, c.beta2, c.eps, c.weight_decay = betas[0], betas[1], eps, weight_decay
         self.phases = tuple(phases)
         self._ctx = ctypes.c_void_p()
         _check(self.lib.pf_trainer_create(ctypes.byref(m), ctypes.byref(c), ctypes.byref(self._ctx)), "trainer_create")
@@ -221,6 +226,13 @@ class Trainer:
                                                  ctypes.byref(n), ctypes.byref(u)), "stage_buffers")
         return dict(master=ptrs[0].value, weights=ptrs[1].value, grad=ptrs[2].value, stamps=ptrs[3].value,
                     n_params=n.value, n_units=u.value)
+
+    def optim_state(self, local_stage: int = 0) -> dict:
+        """AdamW state pointers of a local stage (None before the first AdamW step)."""
+        ptrs = [ctypes.c_void_p() for _ in range(3)]
+        _check(self.lib.pf_trainer_optim_state(self._ctx, local_stage, *(ctypes.byref(p) for p in ptrs)),
+               "optim_state")
+        return dict(m=ptrs[0].value, v=ptrs[1].value, unit_steps=ptrs[2].value)
 
     def apf_base(self, local_stage: int = 0):
         """Hybrid mode: APF base unit set of the last APF step (None before the first one)."""
