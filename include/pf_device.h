@@ -111,7 +111,7 @@ typedef struct pf_model_cfg {
 } pf_model_cfg;
 
 typedef struct pf_train_cfg {
-  int kind;             /* 0 gpipe, 1 1f1b, 2 interleaved-1f1b, 3 zbv */
+  int kind;             /* 0 gpipe, 1 1f1b, 2 interleaved-1f1b, 3 zbv, 4 zbv-split (B = dX, W = dW actions) */
   int ranks, stages_per_rank, microbatches, rank;
   int phases[4];        /* T_w, T_m, T_f, T_total (PhasePlan) */
   double r_max, lr;
@@ -149,7 +149,8 @@ int pf_trainer_step(pf_ctx* ctx, int t, const int32_t* host_tokens, const int32_
 /* ratio < 0: the phase controller + LP plan; ratio in [0,1]: every cell frozen at `ratio`. */
 int pf_trainer_set_override(pf_ctx* ctx, double ratio);
 int pf_trainer_set_plan(pf_ctx* ctx, const double* ratios /* (s-1)*M + (m-1) */);
-/* plan ratios and {base, opt, floor} makespans of the LP on monitored bounds; returns PF_ERR_DOMAIN before T_m. */
+/* plan ratios and {base, opt, floor} makespans of the LP on monitored bounds; returns PF_ERR_DOMAIN before T_m.
+ * w_min / w_max: one entry per action node in ActionId order (2*S*M, or 3*S*M for zbv-split). */
 int pf_trainer_get_plan(pf_ctx* ctx, double* ratios, double* out3, double* w_min, double* w_max);
 int pf_trainer_action_ms(pf_ctx* ctx, double* ms, int* kinds, int* microbatches, int* stages);
 /* start of each action of the last step relative to the rank's first action (ms, CUDA events) */

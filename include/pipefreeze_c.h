@@ -6,7 +6,9 @@
  * below. Each cites the reference function it replaces.
  *
  * Conventions
- *   kind       0 gpipe, 1 1f1b, 2 interleaved-1f1b, 3 zbv  (ScheduleKind order)
+ *   kind       0 gpipe, 1 1f1b, 2 interleaved-1f1b, 3 zbv  (ScheduleKind order),
+ *              4 zbv-split (ZBV with B = dX and W = dW actions; not in the reference:
+ *              3*M*S action nodes, plan ratios and masks keyed by the w nodes)
  *   plan[4]    {t_warmup, t_monitor, t_freeze, t_total}     (PhasePlan)
  *   node id    DAG node numbering of proj/src/dag.cpp:18-23: 0 = src,
  *              1 + [b ? M*S : 0] + (s-1)*M + (m-1), N-1 = dst; per-action
@@ -31,7 +33,8 @@ extern "C" {
 const char* pf_last_error(void);
 
 /* build_schedule (proj/include/pipefreeze/schedule.hpp:41). actions: R blocks of
- * 2*M*C triples (kind 0/1, microbatch, stage); lens[r] = actions on rank r. */
+ * 2*M*C triples (kind 0 f / 1 b / 2 w, microbatch, stage; 3*M*C for zbv-split);
+ * lens[r] = actions on rank r. */
 int pf_schedule_build(int kind, int R, int C, int M, int* actions, int* lens);
 /* stage_to_rank (schedule.hpp:30) */
 int pf_stage_to_rank(int kind, int R, int C, int M, int stage, int* rank);
@@ -67,6 +70,10 @@ int pf_freezing_masks_horizon(int M, int S, const int* plan, const double* ratio
 int pf_mask_stream_stage_step(int M, int S, const int* plan, const double* ratios, int n_units,
                               uint64_t seed, int t, int s, uint64_t* words, int threads,
                               int* exact_parallel);
+/* As pf_mask_stream_stage_step with per-stage unit counts stage_units[S] (stages of one
+ * model differ: the first holds the embedding, the last the LM head). */
+int pf_mask_stream_stage_step_units(int M, int S, const int* plan, const double* ratios, const int* stage_units,
+                                    uint64_t seed, int t, int s, uint64_t* words, int threads, int* exact_parallel);
 int pf_mask_stream_offset(int M, int S, const int* plan, const double* ratios, int n_units,
                           uint64_t seed, int t, int s, int m, uint64_t* offset);
 
@@ -85,7 +92,8 @@ int pf_plan_weights(int kind, int R, int C, int M, const double* w_min, const do
                     const double* ratios, double afr_scale, double* weights);
 
 /* aggregate_monitoring (timing.hpp:83) over n samples: node id - 1, step,
- * duration (ms), frozen flag (FreezeState::Full). Outputs per-node bounds. */
+ * duration (ms), frozen flag (FreezeState::Full). Outputs per-node bounds.
+ * Node ids >= 2*M*S are w nodes of a zbv-split DAG (3*M*S outputs; b nodes fixed). */
 int pf_monitor_aggregate(int M, int S, int n, const int* node, const int* step,
                          const double* sample_ms, const int* frozen, double* w_min,
                          double* w_max);

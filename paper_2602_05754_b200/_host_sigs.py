@@ -21,6 +21,8 @@ HOST_SIGNATURES = {
     "pf_reconcile_mask": ([c_u64, c_int, c_vp, c_int, c_vp], c_int),
     "pf_freezing_masks_horizon": ([c_int, c_int, c_vp, c_vp, c_int, c_u64, c_vp, c_vp], c_int),
     "pf_mask_stream_stage_step": ([c_int, c_int, c_vp, c_vp, c_int, c_u64, c_int, c_int, c_vp, c_int, c_vp], c_int),
+    "pf_mask_stream_stage_step_units": ([c_int, c_int, c_vp, c_vp, c_vp, c_u64, c_int, c_int, c_vp, c_int, c_vp],
+                                        c_int),
     "pf_mask_stream_offset": ([c_int, c_int, c_vp, c_vp, c_int, c_u64, c_int, c_int, c_int, c_vp], c_int),
     "pf_plan_solve": ([c_int, c_int, c_int, c_int, c_vp, c_vp, c_d, c_int, c_int, c_vp, c_vp, c_vp, c_vp], c_int),
     "pf_plan_verify": ([c_int, c_int, c_int, c_int, c_vp, c_vp, c_d, c_vp, c_vp, c_d, c_vp, c_vp], c_int),

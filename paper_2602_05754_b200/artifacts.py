@@ -90,7 +90,7 @@ def gantt(config: pf.PipelineConfig, weights) -> dict:
     for rank, lst in enumerate(pf.build_schedule(config).rank_order):
         for a in lst:
             v = dag.index_of(a)
-            blocks.append({"end_ms": float(st.start[v] + w[v]), "kind": "fb"[a.kind], "microbatch": a.microbatch,
+            blocks.append({"end_ms": float(st.start[v] + w[v]), "kind": "fbw"[a.kind], "microbatch": a.microbatch,
                            "rank": rank, "stage": a.stage, "start_ms": float(st.start[v])})
     return {"blocks": blocks, "makespan_ms": float(st.makespan), "num_ranks": config.num_ranks}
 
@@ -99,7 +99,7 @@ def measured_gantt(trainer, rank: int = 0) -> dict:
     """Timeline of the trainer's last step in the same schema, from its CUDA-event action times
     (start/end relative to the rank's first action)."""
     start, end, kinds, mbs, stages = trainer.action_times()
-    blocks = [{"end_ms": float(e), "kind": "fb"[int(k)], "microbatch": int(m), "rank": rank, "stage": int(s),
+    blocks = [{"end_ms": float(e), "kind": "fbw"[int(k)], "microbatch": int(m), "rank": rank, "stage": int(s),
                "start_ms": float(b)} for b, e, k, m, s in zip(start, end, kinds, mbs, stages)]
     return {"blocks": blocks, "makespan_ms": float(max(end) if len(end) else 0.0), "num_ranks": 1}
 
@@ -123,9 +123,9 @@ def mask_history_to_json(popcounts: np.ndarray, n_units: int) -> str:
 def timing_profile_to_json(w_min, w_max, M: int, S: int) -> str:
     """Per-node bounds in ActionId order -> timing profile json (config.cpp:166-175)."""
     nodes = []
-    for kind in (0, 1):
+    for kind in range(len(w_min) // (S * M)):  # f, b (, w for a split backward)
         for s in range(1, S + 1):
             for m in range(1, M + 1):
                 i = kind * S * M + (s - 1) * M + (m - 1)
-                nodes.append({"kind": "fb"[kind], "m": m, "s": s, "w_max": float(w_max[i]), "w_min": float(w_min[i])})
+                nodes.append({"kind": "fbw"[kind], "m": m, "s": s, "w_max": float(w_max[i]), "w_min": float(w_min[i])})
     return _dump({"per_node": nodes})

@@ -185,6 +185,13 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
   }
 }
 
+void attn_release_keep_out(AttnState* st) {
+  st->lse = at::Tensor();
+  st->dq = at::Tensor();
+  st->dk = at::Tensor();
+  st->dv = at::Tensor();
+}
+
 void attn_release(AttnState* st) {
   st->out = at::Tensor();
   st->lse = at::Tensor();

@@ -30,6 +30,9 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
              AttnGrads* g, cudaStream_t stream);
 // release saved forward tensors (after the backward consumed them)
 void attn_release(AttnState* st);
+// Split backward: drop the softmax statistics and dQ/dK/dV after B but keep the
+// attention output, which W still reads as the X operand of dWo.
+void attn_release_keep_out(AttnState* st);
 // 1 while the cuDNN fused-attention backend is in use, 0 for flash-attention
 int attn_backend_is_cudnn();
 

@@ -161,7 +161,7 @@ int pf_trainer_create(const pf_model_cfg* m, const pf_train_cfg* c, pf_ctx** out
     mc.norm_eps = m->norm_eps;
     mc.init_std = m->init_std;
     pf::TrainConfig tc;
-    if (c->kind < 0 || c->kind > 3) return PF_ERR_CONFIG;
+    if (c->kind < 0 || c->kind > 4) return PF_ERR_CONFIG;
     tc.pipeline.schedule_kind = static_cast<pipefreeze::ScheduleKind>(c->kind);
     tc.pipeline.num_ranks = c->ranks;
     tc.pipeline.stages_per_rank = c->stages_per_rank;
@@ -271,7 +271,7 @@ int pf_trainer_action_ms(pf_ctx* ctx, double* ms, int* kinds, int* mbs, int* sta
     const auto& tr = *ctx->trainer;
     for (size_t i = 0; i < tr.actions().size(); ++i) {
       if (ms) ms[i] = i < tr.action_ms().size() ? tr.action_ms()[i] : 0.0;
-      if (kinds) kinds[i] = tr.actions()[i].kind == pipefreeze::ActionKind::Forward ? 0 : 1;
+      if (kinds) kinds[i] = static_cast<int>(tr.actions()[i].kind);  // 0 f, 1 b, 2 w
       if (mbs) mbs[i] = tr.actions()[i].microbatch;
       if (stages) stages[i] = tr.actions()[i].stage;
     }
@@ -334,7 +334,7 @@ int pf_trainer_last_masks(pf_ctx* ctx, int i, uint64_t* out) {
     auto st = ctx->trainer->local_stages();
     if (i < 0 || i >= static_cast<int>(st.size())) return PF_ERR_INVALID;
     const int words = st[static_cast<size_t>(i)]->words();
-    const int M = static_cast<int>(ctx->trainer->actions().size()) / (2 * static_cast<int>(st.size()));
+    const int M = ctx->trainer->config().pipeline.num_microbatches;
     const uint64_t* src = ctx->trainer->masks_host(i);
     for (int m = 0; m < M; ++m)
       for (int w = 0; w < words; ++w) out[static_cast<size_t>(m) * words + w] = src[static_cast<size_t>(m) * (words + 1) + w];

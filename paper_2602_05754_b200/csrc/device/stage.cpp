@@ -144,8 +144,9 @@ ParamSlice Stage::add_dense(long long n) {
   return p;
 }
 
-Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device)
-    : cfg_(cfg), spec_(spec), device_(device) {
+Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
+             bool split_backward)
+    : cfg_(cfg), spec_(spec), device_(device), split_(split_backward) {
   if (cfg.hidden % 128 || cfg.ffn % 64 || cfg.head_dim % 8 || cfg.vocab % 8 || cfg.tokens() % 128)
     throw std::invalid_argument("stage: unsupported model shape (hidden % 128, ffn % 64, vocab % 8, T % 128)");
   cudaSetDevice(device);
@@ -217,6 +218,10 @@ Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t 
       L.rstd1 = af32(T);
       L.rstd2 = af32(T);
       L.attn = attn_state_new();
+      if (split_) {
+        L.dy = abf(T * h);
+        L.dx2 = abf(T * h);
+      }
     }
     sl.x_out = abf(T * h);
     if (spec.last) {
@@ -312,31 +317,41 @@ int Stage::dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long l
 
 int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
                     __nv_bfloat16* dx_out, int stamp, cudaStream_t s) {
-  if (slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
+  if (slot < 0 || slot >= static_cast<int>(slots_.size()) || (!frozen_words && !split_)) return PF_ERR_INVALID;
   Slot& sl = slots_[static_cast<std::size_t>(slot)];
   const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
   const int nl = static_cast<int>(layers_.size());
-  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units
-  PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
-                                   unit_counts_, s));
+  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units (W does it when split)
+  if (!split_)
+    PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
+                                     unit_counts_, s));
+  // split: every layer's output gradient lands in its slot buffer, the top one included
+  __nv_bfloat16* top = split_ && nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
   const __nv_bfloat16* dcur = dy;
   if (spec_.last) {
     PF_TRY(gemm_dx(sl.logits, cfg_.vocab, weights_ + wlm_.offset, h, d_h_, h, T, h, cfg_.vocab, EPI_STORE_BF16, s));
-    PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
-    PF_TRY(launch_rmsnorm_bwd(sl.x_out, weights_ + gf_.offset, sl.rstdf, d_h_, nullptr, d_y_, grad_ + gf_.offset, T,
+    if (!split_) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
+    PF_TRY(launch_rmsnorm_bwd(sl.x_out, weights_ + gf_.offset, sl.rstdf, d_h_, nullptr, top, grad_ + gf_.offset, T,
                               h, s));
-    dcur = d_y_;
+    dcur = top;
+  } else if (split_ && nl > 0 && dcur) {
+    PF_CUDA(cudaMemcpyAsync(top, dcur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, s));
+    dcur = top;
   }
   if (!dcur) return PF_ERR_INVALID;
   for (int li = nl - 1; li >= 0; --li) {
     SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
     const LayerParams& P = layers_[static_cast<std::size_t>(li)];
+    // split: d(gate|up) over gu and dqkv over qkv (both dead after their use here), dx2 kept
+    __nv_bfloat16* dgu = split_ ? L.gu : d_gu_;
+    __nv_bfloat16* dx2 = split_ ? L.dx2 : d_x2_;
+    __nv_bfloat16* dqkv = split_ ? L.qkv : d_qkv_;
     // MLP
-    PF_TRY(gemm_dx_dswiglu(dcur, h, weights_ + P.wd.offset, ffn, L.gu, d_a_, d_gu_, T, ffn, h, s));
-    PF_TRY(gemm_dx(d_gu_, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
-    PF_TRY(launch_rmsnorm_bwd(L.x2, weights_ + P.g2.offset, L.rstd2, d_h_, dcur, d_x2_, grad_ + P.g2.offset, T, h, s));
+    PF_TRY(gemm_dx_dswiglu(dcur, h, weights_ + P.wd.offset, ffn, L.gu, d_a_, dgu, T, ffn, h, s));
+    PF_TRY(gemm_dx(dgu, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
+    PF_TRY(launch_rmsnorm_bwd(L.x2, weights_ + P.g2.offset, L.rstd2, d_h_, dcur, dx2, grad_ + P.g2.offset, T, h, s));
     // attention
-    PF_TRY(gemm_dx(d_x2_, h, weights_ + P.wo.offset, cfg_.attn_dim(), d_attn_, cfg_.attn_dim(), T, cfg_.attn_dim(), h,
+    PF_TRY(gemm_dx(dx2, h, weights_ + P.wo.offset, cfg_.attn_dim(), d_attn_, cfg_.attn_dim(), T, cfg_.attn_dim(), h,
                    EPI_STORE_BF16, s));
     AttnGrads ag{};
     PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
@@ -345,36 +360,59 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
       AttnGradView gv{static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
                       static_cast<const __nv_bfloat16*>(ag.dv), ag.q_b, ag.q_t, ag.q_h, ag.k_b, ag.k_t, ag.k_h,
                       ag.v_b, ag.v_t, ag.v_h, ag.rep};
-      PF_TRY(launch_rope_bwd_pack(gv, d_qkv_, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
+      PF_TRY(launch_rope_bwd_pack(gv, dqkv, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
     }
-    PF_TRY(gemm_dx(d_qkv_, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
+    PF_TRY(gemm_dx(dqkv, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
                    EPI_STORE_BF16, s));
     // K3: the layer's four masked weight gradients in ONE grouped launch over
     // their unfrozen units (all four dY buffers are still live here)
-    {
-      const ParamSlice* w[4] = {&P.wd, &P.wgu, &P.wo, &P.wqkv};
-      const __nv_bfloat16* dys[4] = {dcur, d_gu_, d_x2_, d_qkv_};
-      const long long ldys[4] = {h, 2LL * ffn, h, cfg_.qkv_dim()};
-      const __nv_bfloat16* xs[4] = {L.a, L.h2, L.attn_out, L.h1};
-      const long long ldxs[4] = {ffn, h, L.attn_ld, h};
-      UnitGemm items[4];
-      for (int k = 0; k < 4; ++k) {
-        const UnitMatrix& m = mats_[static_cast<std::size_t>(w[k]->unit_matrix)];
-        items[k] = UnitGemm{GemmOperand{dys[k], ldys[k], true}, GemmOperand{xs[k], ldxs[k], true},
-                            grad_ + w[k]->offset, w[k]->cols, w[k]->rows, w[k]->cols,
-                            unit_lists_ + m.unit_offset, unit_counts_ + w[k]->unit_matrix, m.units, m.unit_offset};
-      }
-      PF_TRY(gemm_bf16_units_grouped(items, 4, T, 1.0f, stamps_, stamp, s));
-    }
-    __nv_bfloat16* out = li > 0 ? (dcur == d_y_ ? d_tmp_ : d_y_) : (spec_.first ? d_tmp_ : dx_out);
+    if (!split_) PF_TRY(layer_weight_grads(L, P, dcur, dgu, dx2, dqkv, stamp, s));
+    __nv_bfloat16* out;
+    if (li > 0) out = split_ ? sl.layers[static_cast<std::size_t>(li - 1)].dy : (dcur == d_y_ ? d_tmp_ : d_y_);
+    else out = spec_.first ? d_tmp_ : dx_out;
     if (!out) return PF_ERR_INVALID;
-    PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, d_x2_, out, grad_ + P.g1.offset, T, h, s));
-    attn_release(L.attn);
+    PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, dx2, out, grad_ + P.g1.offset, T, h, s));
+    if (split_) attn_release_keep_out(L.attn);
+    else attn_release(L.attn);
     dcur = out;
   }
   if (spec_.first) PF_TRY(launch_embedding_bwd(tokens, dcur, grad_ + emb_.offset, T, h, s));
   else if (nl == 0 && dx_out && dcur != dx_out)
     PF_CUDA(cudaMemcpyAsync(dx_out, dcur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, s));
+  return PF_OK;
+}
+
+int Stage::layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
+                              const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv,
+                              int stamp, cudaStream_t s) {
+  const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
+  const ParamSlice* w[4] = {&P.wd, &P.wgu, &P.wo, &P.wqkv};
+  const __nv_bfloat16* dys[4] = {dy, dgu, dx2, dqkv};
+  const long long ldys[4] = {h, 2LL * ffn, h, cfg_.qkv_dim()};
+  const __nv_bfloat16* xs[4] = {L.a, L.h2, L.attn_out, L.h1};
+  const long long ldxs[4] = {ffn, h, L.attn_ld, h};
+  UnitGemm items[4];
+  for (int k = 0; k < 4; ++k) {
+    const UnitMatrix& m = mats_[static_cast<std::size_t>(w[k]->unit_matrix)];
+    items[k] = UnitGemm{GemmOperand{dys[k], ldys[k], true}, GemmOperand{xs[k], ldxs[k], true},
+                        grad_ + w[k]->offset, w[k]->cols, w[k]->rows, w[k]->cols,
+                        unit_lists_ + m.unit_offset, unit_counts_ + w[k]->unit_matrix, m.units, m.unit_offset};
+  }
+  return gemm_bf16_units_grouped(items, 4, T, 1.0f, stamps_, stamp, s);
+}
+
+int Stage::backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) {
+  if (!split_ || slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
+  Slot& sl = slots_[static_cast<std::size_t>(slot)];
+  const int h = cfg_.hidden;
+  PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
+                                   unit_counts_, s));
+  if (spec_.last) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
+  for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
+    SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
+    PF_TRY(layer_weight_grads(L, layers_[static_cast<std::size_t>(li)], L.dy, L.gu, L.dx2, L.qkv, stamp, s));
+    attn_release(L.attn);
+  }
   return PF_OK;
 }
 

@@ -70,6 +70,9 @@ struct SavedLayer {  // per layer per microbatch slot
   AttnState* attn = nullptr;
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
+  // split backward only: the layer's output gradient and post-attention residual
+  // gradient, kept from B to W (dgu and dqkv are written over gu and qkv)
+  __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;
 };
 
 struct Slot {  // one in-flight microbatch
@@ -89,7 +92,10 @@ struct OptimCfg {
 
 class Stage {
  public:
-  Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device);
+  // split_backward: backward() computes only input gradients (B) and keeps what
+  // backward_weight() (W) needs in the slot (zbv-split schedules).
+  Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
+        bool split_backward = false);
   ~Stage();
   Stage(const Stage&) = delete;
   Stage& operator=(const Stage&) = delete;
@@ -103,6 +109,10 @@ class Stage {
   // receives the gradient of the stage input (ignored on the first stage).
   int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
                __nv_bfloat16* dx_out, int stamp, cudaStream_t s);
+  // W of a split backward: the masked weight gradients of the microbatch in `slot`
+  // (K5 lists + grouped K3) from the gradients its B left in the slot.
+  int backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s);
+  bool split_backward() const { return split_; }
   // SGD: theta -= lr * G / M (sandbox.cpp:250). AdamW: g = G / M into per-unit-step AdamW.
   // Units frozen in every microbatch of the step (stamp != this step) are not touched.
   int optimizer_step(const OptimCfg& oc, int microbatches, int stamp, bool apf, float apf_alpha,
@@ -135,6 +145,9 @@ class Stage {
  private:
   ParamSlice add_matrix(int rows, int cols, bool freezable);
   ParamSlice add_dense(long long n);
+  int layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
+                         const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv, int stamp,
+                         cudaStream_t s);
   int dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
                   long long ldx, int stamp, cudaStream_t s);
 
@@ -158,6 +171,7 @@ class Stage {
   float* adam_v_ = nullptr;
   int* unit_steps_ = nullptr;
   int dense_steps_ = 0;
+  bool split_ = false;
   int* unit_lists_ = nullptr;
   int* unit_counts_ = nullptr;
   float2* rope_ = nullptr;

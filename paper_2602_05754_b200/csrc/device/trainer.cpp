@@ -63,19 +63,22 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   if (cfg.pipeline.num_ranks > 1 && cfg.pipeline.schedule_kind != ScheduleKind::GPipe &&
       cfg.pipeline.schedule_kind != ScheduleKind::OneFOneB)
     throw std::invalid_argument("trainer: multi-rank transport supports gpipe and 1f1b (one stage per rank)");
-  // in-flight microbatches per stage = slot count
+  // in-flight microbatches per stage = slot count; a slot is held from F until the
+  // action that last reads it: b, or w when the backward is split
+  const bool split = splits_weight_grad(cfg.pipeline);
+  const ActionKind release = split ? ActionKind::Weight : ActionKind::Backward;
   for (int s : stage_ids_) {
     int live = 0, peak = 0;
     for (const auto& a : actions_) {
       if (a.stage != s) continue;
-      live += a.kind == ActionKind::Forward ? 1 : -1;
+      live += a.kind == ActionKind::Forward ? 1 : (a.kind == release ? -1 : 0);
       peak = std::max(peak, live);
     }
     slots_.push_back(std::max(1, peak));
   }
   for (std::size_t i = 0; i < stage_ids_.size(); ++i)
     stages_.push_back(std::make_unique<Stage>(model, stage_spec(model, stage_ids_[i], S), slots_[i], cfg.seed,
-                                              cfg.device));
+                                              cfg.device, split));
   const long long T = model.tokens();
   auto act_alloc = [&]() {
     __nv_bfloat16* p = nullptr;
@@ -237,8 +240,7 @@ int Trainer::init_comm(const void* ids, int nranks, int rank) {
 // rank) gives every rank the same bounds, so every rank solves the same LP.
 int Trainer::exchange_monitoring(TimingProfile* merged) {
   const auto local = aggregate_monitoring(monitor_);
-  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
-  const std::size_t n = static_cast<std::size_t>(2 * S * M);
+  const std::size_t n = static_cast<std::size_t>(dag_->node_count() - 2);
   std::vector<double> host(2 * n, 0.0);
   for (const auto& [a, b] : local.all()) {
     const int v = dag_->index_of(a) - 1;
@@ -274,7 +276,7 @@ void Trainer::solve_plan_from_monitoring() {
   const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
   for (int s = 1; s <= S; ++s)
     for (int m = 1; m <= M; ++m)
-      plan_ratios_[static_cast<std::size_t>((s - 1) * M + (m - 1))] = plan_.ratio_of(backward_action(m, s));
+      plan_ratios_[static_cast<std::size_t>((s - 1) * M + (m - 1))] = plan_.ratio_of(freeze_node(cfg_.pipeline, m, s));
   plan_ready_ = true;
   lp_solve_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -407,6 +409,11 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
                                 comm(comm_act_[r & 1]), act_send_)));
         PF_CUDA(cudaEventRecord(out_sent_ev_[ls][ss], act_send_));
       }
+    } else if (a.kind == ActionKind::Weight) {  // split backward: dW of the slot's microbatch
+      const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+      PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
+      PF_TRY(st.backward_weight(slot, mw, t, stream_));
+      PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
     } else {
       const bool recv_dy = a.stage < S && local_index(a.stage + 1) < 0;
       const bool send_dx = a.stage > 1 && local_index(a.stage - 1) < 0;
@@ -497,8 +504,9 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   if (controller && (phase == Phase::MonitorUpper || phase == Phase::MonitorLower)) {
     for (std::size_t i = 0; i < actions_.size(); ++i) {
       const ActionId a = actions_[i];
-      const FreezeState fs =
-          (a.kind == ActionKind::Backward && phase == Phase::MonitorLower) ? FreezeState::Full : FreezeState::None;
+      const FreezeState fs = (a == freeze_node(cfg_.pipeline, a.microbatch, a.stage) && phase == Phase::MonitorLower)
+                                 ? FreezeState::Full
+                                 : FreezeState::None;
       monitor_.record(a, t, action_ms_[i], fs);
     }
   }

@@ -58,6 +58,7 @@ struct StepResult {
 class Trainer {
  public:
   Trainer(const ModelConfig& model, const TrainConfig& cfg);
+  const TrainConfig& config() const { return cfg_; }
   ~Trainer();
 
   // host_tokens / host_targets: [M][T] int32 (pinned or pageable) or null to

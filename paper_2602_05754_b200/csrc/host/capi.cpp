@@ -42,7 +42,7 @@ int guard(F&& f) {
 }
 
 PipelineConfig make_cfg(int kind, int R, int C, int M) {
-  if (kind < 0 || kind > 3) throw config_error("unknown schedule kind code " + std::to_string(kind));
+  if (kind < 0 || kind > 4) throw config_error("unknown schedule kind code " + std::to_string(kind));
   PipelineConfig c;
   c.schedule_kind = static_cast<ScheduleKind>(kind);
   c.num_ranks = R;
@@ -88,7 +88,7 @@ int pf_schedule_build(int kind, int R, int C, int M, int* actions, int* lens) {
     for (int r = 0; r < R; ++r) {
       lens[r] = static_cast<int>(tl.rank_order[static_cast<std::size_t>(r)].size());
       for (const auto& a : tl.rank_order[static_cast<std::size_t>(r)]) {
-        actions[k++] = a.kind == ActionKind::Forward ? 0 : 1;
+        actions[k++] = static_cast<int>(a.kind);  // 0 f, 1 b, 2 w (zbv-split)
         actions[k++] = a.microbatch;
         actions[k++] = a.stage;
       }
@@ -231,6 +231,18 @@ int pf_mask_stream_stage_step(int M, int S, const int* plan, const double* ratio
   });
 }
 
+int pf_mask_stream_stage_step_units(int M, int S, const int* plan, const double* ratios, const int* stage_units,
+                                    uint64_t seed, int t, int s, uint64_t* words, int threads, int* exact_parallel) {
+  return guard([&] {
+    need(ratios, "ratios");
+    need(stage_units, "stage_units");
+    need(words, "words");
+    MaskStream ms(ratio_vec(ratios, M * S), make_plan(plan), M, std::vector<int>(stage_units, stage_units + S), seed);
+    const bool ok = ms.stage_step_masks(t, s, words, threads);
+    if (exact_parallel) *exact_parallel = ok ? 1 : 0;
+  });
+}
+
 int pf_mask_stream_offset(int M, int S, const int* plan, const double* ratios, int n, uint64_t seed, int t, int s,
                           int m, uint64_t* offset) {
   return guard([&] {
@@ -259,7 +271,7 @@ int pf_plan_solve(int kind, int R, int C, int M, const double* w_min, const doub
     const auto plan = extract_freeze_plan(dag, prof, sol, r_max, opt.tol);
     if (ratios)
       for (int s = 1; s <= S; ++s)
-        for (int m = 1; m <= M; ++m) ratios[(s - 1) * M + (m - 1)] = plan.ratio_of(backward_action(m, s));
+        for (int m = 1; m <= M; ++m) ratios[(s - 1) * M + (m - 1)] = plan.ratio_of(freeze_node(cfg, m, s));
     if (durations)
       for (int v = 1; v + 1 < dag.node_count(); ++v) durations[v - 1] = plan.durations.at(dag.action_at(v));
     if (out5) {
@@ -289,7 +301,7 @@ int pf_plan_verify(int kind, int R, int C, int M, const double* w_min, const dou
     FreezePlan plan;
     plan.r_max = r_max;
     for (int s = 1; s <= S; ++s)
-      for (int m = 1; m <= M; ++m) plan.ratios[backward_action(m, s)] = ratios[(s - 1) * M + (m - 1)];
+      for (int m = 1; m <= M; ++m) plan.ratios[freeze_node(cfg, m, s)] = ratios[(s - 1) * M + (m - 1)];
     for (int v = 1; v + 1 < dag.node_count(); ++v) plan.durations[dag.action_at(v)] = durations[v - 1];
     plan.makespan_opt = makespan_opt;
     plan.makespan_base = longest_path_start_times(dag, prof.weights_max(dag)).makespan;
@@ -310,7 +322,7 @@ int pf_plan_weights(int kind, int R, int C, int M, const double* w_min, const do
     const auto prof = profile_from_nodes(dag, w_min, w_max);
     FreezePlan plan;
     for (int s = 1; s <= S; ++s)
-      for (int m = 1; m <= M; ++m) plan.ratios[backward_action(m, s)] = ratios[(s - 1) * M + (m - 1)];
+      for (int m = 1; m <= M; ++m) plan.ratios[freeze_node(cfg, m, s)] = ratios[(s - 1) * M + (m - 1)];
     const auto w = plan_weights(dag, prof, plan, afr_scale);
     std::copy(w.begin(), w.end(), weights);
   });
@@ -321,7 +333,9 @@ int pf_monitor_aggregate(int M, int S, int n, const int* node, const int* step, 
   return guard([&] {
     need(node, "node");
     need(ms, "sample_ms");
-    PipelineDag dag(M, S);
+    bool split = false;  // node ids past the backwards are w nodes (zbv-split dag)
+    for (int i = 0; i < n; ++i) split |= node[i] >= 2 * M * S;
+    PipelineDag dag(M, S, split);
     MonitorLog log;
     for (int i = 0; i < n; ++i)
       log.record(dag.action_at(node[i] + 1), step ? step[i] : 0, ms[i],

@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _native
 from ._device_sigs import PfModelCfg, PfStepResult, PfTrainCfg, PfTrainerInfo
-from .pipefreeze import KINDS
+from .pipefreeze import KINDS, SPLIT_KINDS
 
 
 @dataclass(frozen=True)
@@ -127,6 +127,7 @@ class Trainer:
                        shape.layers, shape.seq, shape.micro_batch, shape.rope_theta, shape.norm_eps, shape.init_std)
         c = PfTrainCfg()
         c.kind = KINDS[schedule]
+        self.kinds = 3 if c.kind in SPLIT_KINDS else 2  # action kinds per cell: f, b (, w)
         c.ranks, c.stages_per_rank, c.microbatches, c.rank = ranks, stages_per_rank, microbatches, rank
         c.phases[:] = list(phases)
         c.r_max, c.lr, c.seed = r_max, lr, seed
@@ -187,8 +188,8 @@ class Trainer:
     def get_plan(self):
         ratios = np.zeros(self.S * self.M)
         out3 = np.zeros(3)
-        wmin = np.zeros(2 * self.S * self.M)
-        wmax = np.zeros(2 * self.S * self.M)
+        wmin = np.zeros(self.kinds * self.S * self.M)
+        wmax = np.zeros(self.kinds * self.S * self.M)
         rc = self.lib.pf_trainer_get_plan(self._ctx, *(a.ctypes.data_as(ctypes.c_void_p) for a in (ratios, out3, wmin, wmax)))
         if rc == _native.PF_ERR_DOMAIN:
             return None

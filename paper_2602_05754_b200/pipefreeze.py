@@ -21,8 +21,9 @@ import numpy as np
 
 from . import _native
 
-KINDS = {"gpipe": 0, "1f1b": 1, "interleaved-1f1b": 2, "interleaved": 2, "zbv": 3}
-KIND_NAMES = {0: "gpipe", 1: "1f1b", 2: "interleaved-1f1b", 3: "zbv"}
+KINDS = {"gpipe": 0, "1f1b": 1, "interleaved-1f1b": 2, "interleaved": 2, "zbv": 3, "zbv-split": 4}
+KIND_NAMES = {0: "gpipe", 1: "1f1b", 2: "interleaved-1f1b", 3: "zbv", 4: "zbv-split"}
+SPLIT_KINDS = {4}  # backward split into b (dX) and w (dW) actions; not in the reference
 
 
 class ConfigError(ValueError):
@@ -76,12 +77,12 @@ class Phase(enum.IntEnum):
 class ActionId:
     """(kind, stage, microbatch) order as the reference's operator<=> (types.hpp:20-24)."""
 
-    kind: int  # 0 forward, 1 backward
+    kind: int  # 0 forward, 1 backward, 2 weight gradient (zbv-split only)
     stage: int
     microbatch: int
 
     def __str__(self) -> str:
-        return f"{'fb'[self.kind]}({self.microbatch},{self.stage})"
+        return f"{'fbw'[self.kind]}({self.microbatch},{self.stage})"
 
 
 def forward_action(m: int, s: int) -> ActionId:
@@ -90,6 +91,10 @@ def forward_action(m: int, s: int) -> ActionId:
 
 def backward_action(m: int, s: int) -> ActionId:
     return ActionId(1, s, m)
+
+
+def weight_action(m: int, s: int) -> ActionId:
+    return ActionId(2, s, m)
 
 
 @dataclass(frozen=True)
@@ -106,6 +111,18 @@ class PipelineConfig:
     def key(self):
         return (_kind(self.schedule_kind), self.num_ranks, self.stages_per_rank, self.num_microbatches)
 
+    @property
+    def split_weight(self) -> bool:
+        return _kind(self.schedule_kind) in SPLIT_KINDS
+
+    @property
+    def kinds(self) -> int:
+        """Action kinds per (m, s) cell: 2 (f, b) or 3 (f, b, w)."""
+        return 3 if self.split_weight else 2
+
+    def freeze_node(self, m: int, s: int) -> ActionId:
+        return weight_action(m, s) if self.split_weight else backward_action(m, s)
+
 
 @dataclass
 class RankTimeline:
@@ -118,7 +135,7 @@ class RankTimeline:
 
 def build_schedule(config: PipelineConfig) -> RankTimeline:
     k, R, C, M = config.key()
-    per = 2 * M * C
+    per = config.kinds * M * C
     acts = np.zeros(max(1, R) * per * 3 + 3, dtype=np.int32)
     lens = np.zeros(max(1, R), dtype=np.int32)
     _check(_native.host().pf_schedule_build(k, R, C, M, _p(acts), _p(lens)), "build_schedule")
@@ -140,7 +157,8 @@ def stage_to_rank(config: PipelineConfig, stage: int) -> int:
 
 
 class PipelineDag:
-    """Node ids: 0 = src, 1 + [b ? M*S : 0] + (s-1)*M + (m-1), N-1 = dst (dag.cpp:18-23)."""
+    """Node ids: 0 = src, 1 + kind*M*S + (s-1)*M + (m-1), N-1 = dst (dag.cpp:18-23; kind 2 = w
+    exists only for zbv-split)."""
 
     def __init__(self, config: PipelineConfig):
         self.config = config
@@ -157,7 +175,7 @@ class PipelineDag:
 
     @property
     def node_count(self) -> int:
-        return 2 * self.M * self.S + 2
+        return self.config.kinds * self.M * self.S + 2
 
     @property
     def source(self) -> int:
@@ -168,13 +186,13 @@ class PipelineDag:
         return self.node_count - 1
 
     def index_of(self, a: ActionId) -> int:
-        return 1 + (self.M * self.S if a.kind else 0) + (a.stage - 1) * self.M + (a.microbatch - 1)
+        return 1 + a.kind * self.M * self.S + (a.stage - 1) * self.M + (a.microbatch - 1)
 
     def action_at(self, node: int) -> ActionId:
         k = node - 1
         per = self.M * self.S
         w = k % per
-        return ActionId(1 if k >= per else 0, w // self.M + 1, w % self.M + 1)
+        return ActionId(k // per, w // self.M + 1, w % self.M + 1)
 
     def json_text(self) -> str:
         k, R, C, M = self.config.key()
@@ -292,18 +310,29 @@ def run_freezing_masks(ratios, plan: PhasePlan, M: int, S: int, n_units: int, se
 class MaskStream:
     """Random access into run_freezing_masks' single stream (t -> s -> m), by jump-ahead."""
 
-    def __init__(self, ratios, plan: PhasePlan, M: int, S: int, n_units: int, seed: int):
+    def __init__(self, ratios, plan: PhasePlan, M: int, S: int, n_units, seed: int):
+        """n_units: one count for every stage, or a list of S per-stage counts."""
         self.ratios = np.ascontiguousarray(ratios, dtype=np.float64)
-        self.plan, self.M, self.S, self.n, self.seed = plan, M, S, n_units, seed
-        self.words = words_per_mask(n_units)
+        self.plan, self.M, self.S, self.seed = plan, M, S, seed
+        self.stage_units = None if np.isscalar(n_units) else np.ascontiguousarray(n_units, dtype=np.int32)
+        self.n = int(n_units) if self.stage_units is None else None
+        self.words = words_per_mask(self.n) if self.n is not None else None
 
     def stage_step(self, t: int, s: int, threads: int = 0) -> np.ndarray:
-        out = np.zeros((self.M, max(1, self.words)), dtype=np.uint64)
+        n = self.n if self.stage_units is None else int(self.stage_units[s - 1])
+        words = words_per_mask(n)
+        out = np.zeros((self.M, max(1, words)), dtype=np.uint64)
         exact = ctypes.c_int(0)
-        _check(_native.host().pf_mask_stream_stage_step(self.M, self.S, _p(self.plan.arr()), _p(self.ratios), self.n,
-                                                        self.seed, t, s, _p(out), threads, ctypes.byref(exact)),
-               "mask_stream")
-        return out[:, : self.words]
+        lib = _native.host()
+        if self.stage_units is None:
+            rc = lib.pf_mask_stream_stage_step(self.M, self.S, _p(self.plan.arr()), _p(self.ratios), n, self.seed, t, s,
+                                               _p(out), threads, ctypes.byref(exact))
+        else:
+            rc = lib.pf_mask_stream_stage_step_units(self.M, self.S, _p(self.plan.arr()), _p(self.ratios),
+                                                     _p(self.stage_units), self.seed, t, s, _p(out), threads,
+                                                     ctypes.byref(exact))
+        _check(rc, "mask_stream")
+        return out[:, :words]
 
     def offset(self, t: int, s: int, m: int) -> int:
         out = ctypes.c_uint64(0)
@@ -327,11 +356,16 @@ class FreezePlan:
     w_max: np.ndarray = field(repr=False, default=None)
 
 
-def stage_default_bounds(M: int, S: int, fwd, bact, bparam):
-    """TimingProfile::from_stage_defaults (timing.cpp:13-27) as per-node bound arrays."""
+def stage_default_bounds(M: int, S: int, fwd, bact, bparam, split: bool = False):
+    """TimingProfile::from_stage_defaults (timing.cpp:13-27) as per-node bound arrays; split=True is
+    from_stage_defaults_split (zbv-split: b = [act, act], w = [0, param])."""
     f = np.broadcast_to(np.asarray(fwd, dtype=np.float64), (S,))
     a = np.broadcast_to(np.asarray(bact, dtype=np.float64), (S,))
     b = np.broadcast_to(np.asarray(bparam, dtype=np.float64), (S,))
+    if split:
+        wmin = np.concatenate([np.repeat(f, M), np.repeat(a, M), np.zeros(S * M)])
+        wmax = np.concatenate([np.repeat(f, M), np.repeat(a, M), np.repeat(b, M)])
+        return wmin, wmax
     wmin = np.concatenate([np.repeat(f, M), np.repeat(a, M)])
     wmax = np.concatenate([np.repeat(f, M), np.repeat(a + b, M)])
     return wmin, wmax
@@ -344,7 +378,7 @@ def solve_plan(config: PipelineConfig, w_min, w_max, r_max: float, lambda_mode: 
     wmin = np.ascontiguousarray(w_min, dtype=np.float64)
     wmax = np.ascontiguousarray(w_max, dtype=np.float64)
     ratios = np.zeros(S * M)
-    dur = np.zeros(2 * S * M)
+    dur = np.zeros(config.kinds * S * M)
     out5 = np.zeros(5)
     savg = np.zeros(S)
     _check(_native.host().pf_plan_solve(k, R, C, M, _p(wmin), _p(wmax), r_max, lambda_mode, int(budget_all),
@@ -362,7 +396,7 @@ def verify_solution(config: PipelineConfig, plan: FreezePlan) -> tuple[bool, flo
 
 
 def plan_weights(config: PipelineConfig, plan: FreezePlan, afr_scale: float = 1.0) -> np.ndarray:
-    n = 2 * config.num_microbatches * config.total_stages + 2
+    n = config.kinds * config.num_microbatches * config.total_stages + 2
     out = np.zeros(n)
     _check(_native.host().pf_plan_weights(*config.key(), _p(plan.w_min), _p(plan.w_max),
                                           _p(np.ascontiguousarray(plan.ratios)), afr_scale, _p(out)), "plan_weights")
@@ -370,12 +404,14 @@ def plan_weights(config: PipelineConfig, plan: FreezePlan, afr_scale: float = 1.
 
 
 def aggregate_monitoring(M: int, S: int, node, step, sample_ms, frozen):
+    """node = dag node id - 1; ids >= 2*M*S are w nodes of a zbv-split dag (3*M*S bounds out)."""
     node = np.ascontiguousarray(node, dtype=np.int32)
     step = np.ascontiguousarray(step, dtype=np.int32)
     ms = np.ascontiguousarray(sample_ms, dtype=np.float64)
     fz = np.ascontiguousarray(frozen, dtype=np.int32)
-    wmin = np.zeros(2 * M * S)
-    wmax = np.zeros(2 * M * S)
+    kinds = 3 if len(node) and int(node.max()) >= 2 * M * S else 2
+    wmin = np.zeros(kinds * M * S)
+    wmax = np.zeros(kinds * M * S)
     _check(_native.host().pf_monitor_aggregate(M, S, len(node), _p(node), _p(step), _p(ms), _p(fz), _p(wmin), _p(wmax)),
            "aggregate_monitoring")
     return wmin, wmax

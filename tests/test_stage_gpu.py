@@ -84,10 +84,12 @@ def test_stage_step_matches_torch_reference(cuda, override):
     tr.close()
 
 
-@pytest.mark.parametrize("stages_per_rank", [2, 4])
-def test_multi_stage_rank_matches_torch_reference(cuda, stages_per_rank):
-    """Interleaved schedule with several virtual stages on one GPU: activations and gradients
-    hand over between local stages; the update must equal the single-model reference."""
+@pytest.mark.parametrize("schedule,stages_per_rank",
+                         [("interleaved-1f1b", 2), ("interleaved-1f1b", 4), ("zbv", 2), ("zbv-split", 2)])
+def test_multi_stage_rank_matches_torch_reference(cuda, schedule, stages_per_rank):
+    """Several virtual stages on one GPU: activations and gradients hand over between local
+    stages; the update must equal the single-model reference. zbv-split runs each cell's dW as
+    a separate W action after its B (gradients kept in the slot), which must not change it."""
     import torch
 
     from gpu_util import device_view
@@ -97,7 +99,7 @@ def test_multi_stage_rank_matches_torch_reference(cuda, stages_per_rank):
 
     shape = PRESETS["tiny"]
     M, lr, S = 2, 0.5, stages_per_rank
-    tr = Trainer(shape, "interleaved-1f1b", 1, S, M, lr=lr, seed=5)
+    tr = Trainer(shape, schedule, 1, S, M, lr=lr, seed=5)
     tr.set_override(0.5)
     lays = [param_layout(shape, s, S) for s in range(1, S + 1)]
     bufs = [tr.stage_buffers(i) for i in range(S)]
@@ -213,4 +215,35 @@ def test_controller_phases_plan_and_bit_exact_masks(cuda):
     stable = results[-1]
     assert abs(stable["mean_ratio"] - p["ratios"].mean()) < 0.02
     assert stable["predicted_ms"] > 0
+    tr.close()
+
+
+def test_zbv_split_controller_plan_over_w_nodes(cuda):
+    """zbv-split through warm-up, monitoring (w nodes frozen in MonitorLower), the LP at T_m over
+    the w nodes, and the ramp: masks stay the reference stream keyed by the w cells."""
+    from paper_2602_05754_b200 import pipefreeze as pf
+    from paper_2602_05754_b200.engine import PRESETS, Trainer
+
+    shape = PRESETS["tiny"]
+    M, phases = 4, (2, 8, 10, 16)
+    tr = Trainer(shape, "zbv-split", 1, 2, M, phases=phases, r_max=0.8, lr=1e-3, seed=13)
+    plan = pf.PhasePlan(*phases)
+    units = [tr.stage_buffers(i)["n_units"] for i in range(2)]
+    for t in range(1, 13):
+        r = tr.step(t)
+        assert np.isfinite(r["loss"])
+        p = tr.get_plan()
+        if p is not None:
+            ms = pf.MaskStream(p["ratios"], plan, M, 2, units, 13)
+            for i, s in enumerate((1, 2)):
+                assert np.array_equal(tr.last_masks(i), ms.stage_step(t, s))
+    _, kinds, mbs, stages = tr.action_ms()
+    assert sorted(np.bincount(kinds).tolist()) == [2 * M] * 3  # f, b, w for both local stages
+    p = tr.get_plan()
+    n = 2 * M
+    assert len(p["w_min"]) == 3 * n
+    assert np.allclose(p["w_min"][n:2 * n], p["w_max"][n:2 * n])  # b fixed
+    assert np.all(p["w_min"][2 * n:] <= p["w_max"][2 * n:])
+    assert np.all(p["ratios"] <= 1.0) and p["ratios"].mean() <= 0.8 + 1e-6
+    assert p["makespan_opt"] <= p["makespan_base"]
     tr.close()
