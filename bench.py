@@ -202,9 +202,17 @@ def _config(args, shape) -> dict:
             "heads": shape.n_heads, "kv_heads": shape.n_kv_heads, "vocab": shape.vocab,
             "global_batch": args.microbatches * shape.micro_batch, "seq_len": shape.seq,
             "microbatches": args.microbatches, "micro_batch": shape.micro_batch, "schedule": args.schedule,
-            "parallelism": f"pp{args.gpus}", "r_max": args.r_max, "phases": list(args.phases),
+            "parallelism": f"pp{args.gpus}", "stages_per_rank": stages_per_rank(args), "r_max": args.r_max,
+            "phases": list(args.phases),
             "optimizer": args.optimizer,
             "l2": "inputs larger than L2 (>2 GB of weights and activations touched per step)"}
+
+
+def stages_per_rank(args) -> int:
+    """Virtual stages per GPU: 2 for the V-shaped zbv / zbv-split, --chunks for interleaved."""
+    if args.schedule in ("zbv", "zbv-split"):
+        return 2
+    return args.chunks if args.schedule in ("interleaved-1f1b", "interleaved") else 1
 
 
 def run_ours(args) -> None:
@@ -225,7 +233,8 @@ def run_ours(args) -> None:
     shape = PRESETS[args.model]
     M = args.microbatches
     phases = tuple(args.phases)
-    tr = Trainer(shape, args.schedule, world, 1, M, rank=rank, phases=phases, r_max=args.r_max, lr=1e-4,
+    C = stages_per_rank(args)
+    tr = Trainer(shape, args.schedule, world, C, M, rank=rank, phases=phases, r_max=args.r_max, lr=1e-4,
                  seed=args.seed, device=local, optimizer=args.optimizer, weight_decay=0.1 if args.optimizer == "adamw" else 0.0)
     lib = _native.device()
     if world > 1:
@@ -299,7 +308,7 @@ def run_ours(args) -> None:
     e2e_dev, e2e_wall, e2e_res, _ = timed_steps(t, args.steps, host=hp)
     t += args.steps
     e2e_wall = max_over_ranks(e2e_wall)
-    words = sum(((u + 63) // 64 + 1) for u in [tr.stage_buffers(0)["n_units"]]) * M
+    words = sum(((tr.stage_buffers(i)["n_units"] + 63) // 64 + 1) for i in range(tr.info["local_stages"])) * M
     h2d = 2 * M * T * 4 + words * 8
 
     peaks = load_peaks() if rank == 0 else None
@@ -357,7 +366,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="llama-1b")
-    ap.add_argument("--schedule", default="gpipe")
+    ap.add_argument("--schedule", default="gpipe",
+                    choices=["gpipe", "1f1b", "interleaved-1f1b", "zbv", "zbv-split"])
+    ap.add_argument("--chunks", type=int, default=2, help="virtual stages per GPU for interleaved-1f1b")
     ap.add_argument("--microbatches", type=int, default=8)
     ap.add_argument("--r-max", type=float, default=0.8)
     ap.add_argument("--phases", type=int, nargs=4, default=[2, 8, 10, 10000])

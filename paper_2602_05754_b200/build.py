@@ -57,7 +57,9 @@ def build_host(force: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(HOST_SRC, "*.cpp")))
     deps = srcs + glob.glob(os.path.join(HOST_SRC, "*.hpp")) + glob.glob(os.path.join(INC, "*.h"))
     if force or _newer(out, deps):
-        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra",
+        # -Bsymbolic: calls inside the library bind to its own definitions (the test oracle
+        # defines the same pipefreeze:: names)
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra", "-Wl,-Bsymbolic",
                "-I", INC, "-I", HOST_SRC, *srcs, "-o", out]
         _run(cmd)
     return out
