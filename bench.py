@@ -16,6 +16,7 @@ through the C-ABI with host (pinned) token buffers (e2e).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -105,36 +106,32 @@ def step_flops(shape, M: int, mean_ratio: float, S: int = 1) -> dict:
     return {"fwd": M * (mm + attn_f), "dx": M * (mm + attn_b), "dw": M * mm * (1.0 - mean_ratio)}
 
 
-def gemm_roofline(peaks: dict, shape, iters: int = 20) -> dict:
-    """Dominant kernel: the K1 tcgen05 GEMM at the stage's largest per-layer shape (gate|up forward),
-    timed live with CUDA events on the launching stream."""
-    import torch
-
-    from paper_2602_05754_b200 import _native
-
-    lib = _native.device()
+def gemm_roofline(peaks: dict, shape, launches: int, total_ms: float) -> dict:
+    """Dominant kernel: the K1 tcgen05 CTA-pair GEMM of the gate|up projection (the largest
+    per-layer GEMM), its launches inside the timed steps bracketed with CUDA events on the
+    trainer's stream (pf_probe_*). achieved = algorithmic FLOPs per launch / mean duration;
+    traffic = DRAM bytes per launch from the committed ncu --set full capture of this kernel."""
     T, h, N = shape.tokens, shape.hidden, 2 * shape.ffn
-    A = torch.randn(T, h, device="cuda").to(torch.bfloat16)
-    B = torch.randn(N, h, device="cuda").to(torch.bfloat16)
-    C = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
-    s = torch.cuda.Stream()
-    with torch.cuda.stream(s):
-        sp = s.cuda_stream
-        for _ in range(3):
-            _native.check(lib.pf_gemm_bf16(A.data_ptr(), 0, h, B.data_ptr(), 0, h, C.data_ptr(), N, T, N, h, 1.0, 0, 512, None, 0, sp), "gemm")
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(iters):
-            lib.pf_gemm_bf16(A.data_ptr(), 0, h, B.data_ptr(), 0, h, C.data_ptr(), N, T, N, h, 1.0, 0, 512, None, 0, sp)
-        e1.record(s)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / iters
+    ms = total_ms / max(1, launches)
     flops = 2.0 * T * N * h
     achieved = flops / (ms * 1e-3) / 1e12
-    return {"bound": "tensor", "kernel": f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, gate|up)",
-            "achieved": round(achieved, 1),
+    kernel = f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, gate|up)"
+    return {"bound": "tensor", "kernel": kernel, "achieved": round(achieved, 1),
             "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
-            "traffic": None, "avg_launch_ms": round(ms, 4), "peak_source": peaks["source"]}
+            "traffic": ncu_traffic(kernel), "avg_launch_ms": round(ms, 4), "launches_timed": launches,
+            "algorithmic_flop_per_launch": flops, "peak_source": peaks["source"]}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from profiles/roofline_traffic.json
+    (written by tools/ncu_traffic.py from an ncu --set full capture of this bench command), else None."""
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["bytes_per_launch"] if d.get("kernel") == kernel else None
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def cpu_reference_step(shape, M: int, S: int, units: int, n_params: int, ratio: float, budget_s: float = 12.0):
@@ -283,8 +280,17 @@ def run_ours(args) -> None:
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    lib.pf_probe_enable(1)  # time the dominant kernel's launches inside the timed steps
+    ncu_range = bool(os.environ.get("PF_NCU_RANGE"))  # ncu --profile-from-start off: the timed steps only
+    if ncu_range:
+        torch.cuda.profiler.start()
     with ClockSampler(local) as clk:
         dev_ms, wall_s, res, launches = timed_steps(t, args.steps)
+    if ncu_range:
+        torch.cuda.profiler.stop()
+    probe_n, probe_ms = ctypes.c_int(0), ctypes.c_double(0.0)
+    _native.check(lib.pf_probe_read(ctypes.byref(probe_n), ctypes.byref(probe_ms)), "pf_probe_read")
+    lib.pf_probe_enable(0)
     t += args.steps
     dev_ms = max_over_ranks(dev_ms)
     ms_step = dev_ms / args.steps
@@ -318,7 +324,7 @@ def run_ours(args) -> None:
         total_flops = sum(fl.values())
         batch_ms = statistics.mean(r["batch_ms"] for r in res)
         pred_ms = statistics.mean(r["predicted_ms"] for r in res)
-        roof = gemm_roofline(peaks, shape)
+        roof = gemm_roofline(peaks, shape, probe_n.value, probe_ms.value)
         try:
             units = tr.stage_buffers(0)["n_units"]
             cpu_s, cpu_info = cpu_reference_step(shape, M, world, units, tr.info["params"], mean_ratio)

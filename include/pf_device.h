@@ -170,6 +170,11 @@ int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank);
 void* pf_trainer_stream(pf_ctx* ctx);
 /* Kernels launched by this library so far (all hand-written kernels, not the ATen attention). */
 long long pf_device_launch_count(void);
+/* In-step kernel probe: while enabled (which = 1: the K1 gate|up GEMM of every layer forward),
+ * the stage brackets each launch of that kernel with CUDA events on its own stream.
+ * pf_probe_read synchronises, returns the launches seen and their summed duration, and resets. */
+int pf_probe_enable(int which);
+int pf_probe_read(int* launches, double* total_ms);
 /* Hybrid mode: the APF base set of local stage i from the last APF step (ceil(units/64) words);
  * returns PF_ERR_DOMAIN before the first APF step. */
 int pf_trainer_apf_base(pf_ctx* ctx, int local_stage, uint64_t* out);

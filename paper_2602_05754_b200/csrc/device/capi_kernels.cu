@@ -87,3 +87,57 @@ long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 }  // namespace pf
 
 extern "C" long long pf_device_launch_count(void) { return pf::launch_count(); }
+
+#include <vector>
+
+namespace pf {
+namespace {
+struct Probe {
+  int kind = PROBE_OFF;
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::size_t used = 0;         // events recorded
+};
+Probe& probe() {
+  static Probe p;
+  return p;
+}
+void probe_record(cudaStream_t s) {
+  Probe& p = probe();
+  if (p.used == p.ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    p.ev.push_back(e);
+  }
+  cudaEventRecord(p.ev[p.used++], s);
+}
+}  // namespace
+int probe_kind() { return probe().kind; }
+void probe_begin(cudaStream_t s) {
+  if (probe().kind != PROBE_OFF) probe_record(s);
+}
+void probe_end(cudaStream_t s) {
+  if (probe().kind != PROBE_OFF) probe_record(s);
+}
+}  // namespace pf
+
+extern "C" int pf_probe_enable(int which) {
+  if (which < 0 || which > 1) return PF_ERR_INVALID;
+  pf::probe().kind = which;
+  pf::probe().used = 0;
+  return PF_OK;
+}
+
+extern "C" int pf_probe_read(int* launches, double* total_ms) {
+  auto& p = pf::probe();
+  double sum = 0.0;
+  for (std::size_t i = 0; i + 1 < p.used; i += 2) {
+    if (cudaEventSynchronize(p.ev[i + 1]) != cudaSuccess) return PF_ERR_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.ev[i], p.ev[i + 1]) != cudaSuccess) return PF_ERR_CUDA;
+    sum += ms;
+  }
+  if (launches) *launches = static_cast<int>(p.used / 2);
+  if (total_ms) *total_ms = sum;
+  p.used = 0;
+  return PF_OK;
+}

@@ -39,7 +39,6 @@ namespace {
 
 constexpr int BM2 = 256;  // rows per CTA pair
 constexpr int BK = 64;
-constexpr int GROUP_M = 8;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, alternating 32-column chunks
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
@@ -61,6 +60,7 @@ struct alignas(64) Params2 {
   long long ldc;
   int M, N, K;
   int tiles_m, tiles_n;
+  int group_m;   // tile rows per raster group (B tiles are re-read once per group)
   float alpha;
   const __nv_bfloat16* R;  // EPI_ADD_BF16 residual source (defaults to C)
   long long ldr;
@@ -111,10 +111,10 @@ __device__ __forceinline__ SegIter seg_begin(const Params2& p, int cluster, int 
 }
 
 __device__ __forceinline__ void decode(const Params2& p, int t, int& tm, int& tn) {
-  const int group_size = GROUP_M * p.tiles_n;
+  const int group_size = p.group_m * p.tiles_n;
   const int g = t / group_size;
-  const int first_m = g * GROUP_M;
-  const int gm = min(p.tiles_m - first_m, GROUP_M);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.tiles_m - first_m, p.group_m);
   const int local = t - g * group_size;
   tm = first_m + local % gm;
   tn = local / gm;
@@ -553,6 +553,23 @@ int streamk_mode() { return streamk_mode_ref(); }
 
 void gemm_set_streamk(int mode) { streamk_mode_ref() = mode; }
 
+// Raster group height in 256-row tiles: consecutive work items walk G tile rows down one
+// tile column before moving right, so each B column block is fetched once per group and
+// the G row blocks of A stay hot in L2. Chosen per shape from B200 measurements
+// (profiles/r1_gemm_group_m.txt): wide forward GEMMs with short K keep all of A resident
+// (G = 16: B streamed once; lm head 1391 -> 1576 TF/s); dX GEMMs (B read MN-major) and
+// long-K shapes prefer short groups (gate|up dX 1082 -> 1270 TF/s at G = 4).
+// PF_GEMM_GROUP_M overrides.
+int group_m_for(int tiles_m, int tiles_n, int K, bool b_mn) {
+  static const int forced = [] {
+    const char* e = std::getenv("PF_GEMM_GROUP_M");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
+  if (!b_mn && tiles_n >= 48) return K <= 2048 ? std::min(tiles_m, 16) : 8;
+  return K >= 32768 ? 8 : 4;
+}
+
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
                    int epi, cudaStream_t stream) {
   constexpr int BN = 256;
@@ -576,6 +593,7 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.K = K;
   p.tiles_m = (M + BM2 - 1) / BM2;
   p.tiles_n = (N + BN - 1) / BN;
+  p.group_m = std::max(1, group_m_for(p.tiles_m, p.tiles_n, K, B.mn_major));
   p.alpha = alpha;
   const int ntiles = p.tiles_m * p.tiles_n;
   const int max_clusters = num_sms() / 2;

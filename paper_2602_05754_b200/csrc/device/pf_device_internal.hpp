@@ -69,6 +69,13 @@ void gemm_set_streamk(int mode);
 
 int num_sms();
 
+// In-step probe of one kernel (bench.py roofline: average duration of the dominant
+// kernel measured inside the timed steps, on the launching stream).
+enum ProbeKind : int { PROBE_OFF = 0, PROBE_GATE_UP_GEMM = 1 };
+int probe_kind();
+void probe_begin(cudaStream_t s);  // no-op unless the probe is enabled
+void probe_end(cudaStream_t s);
+
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).
 void count_launch();
 long long launch_count();

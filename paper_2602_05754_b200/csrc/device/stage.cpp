@@ -292,7 +292,14 @@ int Stage::forward(int slot, int microbatch, const int* tokens, const int* targe
     PF_TRY(gemm_fwd_resid(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, L.x, h, T, h,
                           cfg_.attn_dim(), s));
     PF_TRY(launch_rmsnorm_fwd(L.x2, weights_ + P.g2.offset, L.h2, L.rstd2, T, h, cfg_.norm_eps, s));
-    PF_TRY(gemm_fwd_swiglu(L.h2, h, weights_ + P.wgu.offset, h, L.gu, L.a, T, cfg_.ffn, h, s));
+    if (probe_kind() == PROBE_GATE_UP_GEMM) {  // bench.py roofline: this launch alone (unfused path)
+      probe_begin(s);
+      PF_TRY(gemm_fwd(L.h2, h, weights_ + P.wgu.offset, h, L.gu, 2 * cfg_.ffn, T, 2 * cfg_.ffn, h, EPI_STORE_BF16, s));
+      probe_end(s);
+      PF_TRY(launch_swiglu_fwd(L.gu, L.a, T, cfg_.ffn, s));
+    } else {
+      PF_TRY(gemm_fwd_swiglu(L.h2, h, weights_ + P.wgu.offset, h, L.gu, L.a, T, cfg_.ffn, h, s));
+    }
     __nv_bfloat16* next = li + 1 < nl ? sl.layers[static_cast<std::size_t>(li + 1)].x : sl.x_out;
     PF_TRY(gemm_fwd_resid(L.a, cfg_.ffn, weights_ + P.wd.offset, cfg_.ffn, next, L.x2, h, T, h, cfg_.ffn, s));
   }
