@@ -127,6 +127,8 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   cudaMalloc(&masks_dev_, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
   cudaMallocHost(&masks_host_, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
   std::memset(masks_host_, 0, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
+  cudaMallocHost(&masks_next_, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
+  std::memset(masks_next_, 0, static_cast<size_t>(std::max<long long>(words, 1)) * 8);
   cudaMallocHost(&loss_host_, 4);
   plan_ratios_.assign(static_cast<std::size_t>(S * M), 0.0);
   if (cudaStreamSynchronize(stream_) != cudaSuccess) throw std::runtime_error("trainer: setup failed");
@@ -159,6 +161,7 @@ Trainer::~Trainer() {
   cudaFree(loss_dev_);
   cudaFree(masks_dev_);
   cudaFreeHost(masks_host_);
+  cudaFreeHost(masks_next_);
   cudaFreeHost(loss_host_);
   if (apf_pinned_) cudaFreeHost(apf_pinned_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -191,6 +194,7 @@ void Trainer::set_plan(const std::vector<double>& ratios) {
   if (static_cast<int>(ratios.size()) != S * M) throw std::invalid_argument("set_plan: need M*S ratios");
   plan_ratios_ = ratios;
   plan_ready_ = true;
+  next_t_ = -1;  // prefetched masks used the old plan
 }
 
 FreezeMask Trainer::apf_base_mask(int li) const {
@@ -281,21 +285,12 @@ void Trainer::solve_plan_from_monitoring() {
   lp_solve_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepResult* out) {
-  cudaSetDevice(cfg_.device);
+// Masks of step t for every local cell into `out` (masks_host_ layout: per stage, M masks of
+// words + 1 pad word), with the frozen / total unit counts.
+void Trainer::build_masks(int t, Phase phase, bool controller, uint64_t* out, long long* frozen, long long* total) {
   const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
-  const int T = model_.tokens();
-  StepResult res;
-  Phase phase = Phase::StableFreeze;
-  const bool controller = override_ratio_ < 0.0;
-  if (controller) {
-    phase = phase_of(t, cfg_.phases);
-    if (phase == Phase::Solve && !plan_ready_) solve_plan_from_monitoring();
-  }
-  res.phase = static_cast<int>(phase);
-
-  // ---- masks for this step's cells (host, jump-ahead into the single stream)
-  const auto tm0 = std::chrono::steady_clock::now();
+  *frozen = 0;
+  *total = 0;
   std::vector<int> units_all;
   for (int s = 1; s <= S; ++s) units_all.push_back(stage_units(model_, stage_spec(model_, s, S)));
   for (std::size_t li = 0; li < stages_.size(); ++li) {
@@ -327,16 +322,42 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       }
     }
     for (int m = 0; m < M; ++m) {
-      uint64_t* dst = masks_host_ + mask_offsets_[li] + static_cast<long long>(m) * (words + 1);
+      uint64_t* dst = out + mask_offsets_[li] + static_cast<long long>(m) * (words + 1);
       std::memcpy(dst, tmp.data() + static_cast<std::size_t>(m) * static_cast<std::size_t>(words),
                   static_cast<size_t>(words) * 8);
       dst[words] = 0;
       long long pc = 0;
       for (int w = 0; w < words; ++w) pc += __builtin_popcountll(dst[w]);
-      res.frozen_units += pc;
-      res.total_units += units;
+      *frozen += pc;
+      *total += units;
     }
   }
+}
+
+int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepResult* out) {
+  cudaSetDevice(cfg_.device);
+  const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+  const int T = model_.tokens();
+  StepResult res;
+  Phase phase = Phase::StableFreeze;
+  const bool controller = override_ratio_ < 0.0;
+  if (controller) {
+    phase = phase_of(t, cfg_.phases);
+    if (phase == Phase::Solve && !plan_ready_) solve_plan_from_monitoring();
+  }
+  res.phase = static_cast<int>(phase);
+
+  // ---- masks for this step's cells (host, jump-ahead into the single stream);
+  // usually already generated while the previous step ran on the GPU
+  const auto tm0 = std::chrono::steady_clock::now();
+  if (next_t_ == t && next_override_ == override_ratio_ && next_plan_ready_ == plan_ready_) {
+    std::swap(masks_host_, masks_next_);
+    res.frozen_units = next_frozen_;
+    res.total_units = next_total_;
+  } else {
+    build_masks(t, phase, controller, masks_host_, &res.frozen_units, &res.total_units);
+  }
+  next_t_ = -1;
   res.mean_ratio = res.total_units ? static_cast<double>(res.frozen_units) / static_cast<double>(res.total_units) : 0.0;
   res.mask_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
 
@@ -471,6 +492,17 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_CUDA(cudaMemcpyAsync(apf_pinned_ + off, st->apf_eligible(), static_cast<size_t>(st->units()) * 4,
                               cudaMemcpyDeviceToHost, stream_));
       off += st->units();
+    }
+  }
+  // the next step's masks while this one runs (not in hybrid mode, whose base set comes from
+  // this step's APF result, nor across the LP solve, which changes the plan)
+  if (!cfg_.hybrid) {
+    const Phase next_phase = controller ? phase_of(t + 1, cfg_.phases) : Phase::StableFreeze;
+    if (!(controller && next_phase == Phase::Solve && !plan_ready_)) {
+      build_masks(t + 1, next_phase, controller, masks_next_, &next_frozen_, &next_total_);
+      next_t_ = t + 1;
+      next_override_ = override_ratio_;
+      next_plan_ready_ = plan_ready_;
     }
   }
   PF_CUDA(cudaStreamSynchronize(stream_));

@@ -65,7 +65,10 @@ class Trainer {
   // use device-resident synthetic tokens.
   int step(int t, const int* host_tokens, const int* host_targets, StepResult* out);
 
-  void set_override(double ratio) { override_ratio_ = ratio; }
+  void set_override(double ratio) {
+    override_ratio_ = ratio;
+    next_t_ = -1;
+  }
   void set_plan(const std::vector<double>& ratios);
   bool has_plan() const { return plan_ready_; }
   const std::vector<double>& plan_ratios() const { return plan_ratios_; }
@@ -96,6 +99,8 @@ class Trainer {
  private:
   int local_index(int stage) const;
   void solve_plan_from_monitoring();
+  void build_masks(int t, pipefreeze::Phase phase, bool controller, uint64_t* out, long long* frozen,
+                   long long* total);
   int exchange_monitoring(pipefreeze::TimingProfile* merged);
 
   void* comm_act_[2] = {nullptr, nullptr};   // ncclComm_t
@@ -125,6 +130,11 @@ class Trainer {
   float* loss_dev_ = nullptr;
   uint64_t* masks_dev_ = nullptr;
   uint64_t* masks_host_ = nullptr;  // pinned
+  uint64_t* masks_next_ = nullptr;  // pinned: step next_t_'s masks, built while the previous step ran
+  int next_t_ = -1;
+  double next_override_ = 0.0;
+  bool next_plan_ready_ = false;
+  long long next_frozen_ = 0, next_total_ = 0;
   std::vector<long long> mask_offsets_;  // words offset per local stage
   float* loss_host_ = nullptr;           // pinned
   pipefreeze::MonitorLog monitor_;
