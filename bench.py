@@ -99,9 +99,15 @@ def load_peaks() -> dict:
 def step_flops(shape, M: int, mean_ratio: float, S: int = 1) -> dict:
     """Algorithmic FLOPs of one step: matmul fwd 2TP, dX 2TP, dW (1-r) 2TP, causal attention fwd 2Tsh and bwd 5Tsh."""
     T = shape.tokens
-    P = shape.layers * shape.matmul_params_per_layer() + shape.vocab * shape.hidden
-    mm = 2 * T * P
-    attn_f = 2.0 * T * shape.seq * shape.n_heads * shape.head_dim * shape.layers  # causal: half of 4Tsh
+    if getattr(shape, "family", 0) == 1:  # ViT: patch embedding on the patch rows, head on the cls rows
+        B = shape.micro_batch
+        mm = 2 * T * shape.layers * shape.matmul_params_per_layer() + 2 * B * (shape.seq - 1) * shape.hidden * \
+            shape.patch_dim + 2 * B * shape.vocab * shape.hidden
+        attn_f = 4.0 * T * shape.seq * shape.n_heads * shape.head_dim * shape.layers  # bidirectional
+    else:
+        P = shape.layers * shape.matmul_params_per_layer() + shape.vocab * shape.hidden
+        mm = 2 * T * P
+        attn_f = 2.0 * T * shape.seq * shape.n_heads * shape.head_dim * shape.layers  # causal: half of 4Tsh
     attn_b = 2.5 * attn_f
     return {"fwd": M * (mm + attn_f), "dx": M * (mm + attn_b), "dw": M * mm * (1.0 - mean_ratio)}
 
@@ -111,11 +117,15 @@ def gemm_roofline(peaks: dict, shape, launches: int, total_ms: float) -> dict:
     per-layer GEMM), its launches inside the timed steps bracketed with CUDA events on the
     trainer's stream (pf_probe_*). achieved = algorithmic FLOPs per launch / mean duration;
     traffic = DRAM bytes per launch from the committed ncu --set full capture of this kernel."""
-    T, h, N = shape.tokens, shape.hidden, 2 * shape.ffn
-    ms = total_ms / max(1, launches)
+    vit = getattr(shape, "family", 0) == 1
+    T, h, N = shape.tokens, shape.hidden, shape.ffn if vit else 2 * shape.ffn
+    if launches <= 0 or total_ms <= 0:
+        return {"bound": "tensor", "kernel": None, "achieved": None, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": None, "traffic": None, "note": "probe saw no launches"}
+    ms = total_ms / launches
     flops = 2.0 * T * N * h
     achieved = flops / (ms * 1e-3) / 1e12
-    kernel = f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, gate|up)"
+    kernel = f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, {'fc1' if vit else 'gate|up'})"
     return {"bound": "tensor", "kernel": kernel, "achieved": round(achieved, 1),
             "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
             "traffic": ncu_traffic(kernel), "avg_launch_ms": round(ms, 4), "launches_timed": launches,

@@ -108,6 +108,9 @@ int pf_cross_entropy(void* logits, const int* targets, float* loss_sum, int T, i
 typedef struct pf_model_cfg {
   int hidden, ffn, n_heads, n_kv_heads, head_dim, vocab, layers, seq, micro_batch;
   float rope_theta, norm_eps, init_std;
+  /* family 0: LLaMA decoder (vocab = vocabulary). family 1: ViT encoder (SURVEY config C5):
+   * vocab = classes, seq = (image/patch)^2 + 1, micro_batch = images; synthetic pixels. */
+  int family, image, patch, channels;
 } pf_model_cfg;
 
 typedef struct pf_train_cfg {

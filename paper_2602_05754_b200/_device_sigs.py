@@ -11,7 +11,8 @@ c_cp = ctypes.c_char_p
 
 class PfModelCfg(ctypes.Structure):
     _fields_ = [(n, c_int) for n in ("hidden", "ffn", "n_heads", "n_kv_heads", "head_dim", "vocab", "layers", "seq",
-                                     "micro_batch")] + [("rope_theta", c_f), ("norm_eps", c_f), ("init_std", c_f)]
+                                     "micro_batch")] + [("rope_theta", c_f), ("norm_eps", c_f), ("init_std", c_f)] + \
+        [(n, c_int) for n in ("family", "image", "patch", "channels")]
 
 
 class PfTrainCfg(ctypes.Structure):

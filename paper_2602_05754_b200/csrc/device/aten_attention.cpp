@@ -23,6 +23,7 @@ struct AttnState {
   at::Tensor dq, dk, dv;
   int64_t max_q = 0, max_k = 0;
   bool cudnn = false;
+  bool causal = true;
   int rep = 1;  // K/V head expansion used for this forward (1 = native GQA)
 };
 
@@ -69,12 +70,13 @@ const char* attn_last_error() { return g_attn_err.c_str(); }
 int attn_backend_is_cudnn() { return backend(); }
 
 int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int hd, float scale, void** out,
-             long long* out_token_stride, cudaStream_t stream) {
+             long long* out_token_stride, cudaStream_t stream, bool causal) {
   try {
     c10::cuda::CUDAStreamGuard guard(wrap(stream));
     const auto v = make_views(qkv, B, S, nh, nkv, hd);
     at::Tensor o;
     st->cudnn = false;
+    st->causal = causal;
     if (backend() == 1) {
       try {
         // native GQA (nkv < nh K/V heads) when cuDNN accepts it, else expanded K/V
@@ -82,7 +84,7 @@ int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int 
         const int full_rep = nh / nkv;
         auto run = [&](int rep) {
           return at::_scaled_dot_product_cudnn_attention(v.q, expand_heads(v.k, rep), expand_heads(v.v, rep),
-                                                         std::nullopt, true, 0.0, true, false,
+                                                         std::nullopt, true, 0.0, causal, false,
                                                          static_cast<double>(scale));
         };
         decltype(run(1)) r;
@@ -111,7 +113,7 @@ int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int 
       }
     }
     if (!st->cudnn) {
-      auto r = at::_scaled_dot_product_flash_attention(v.q, v.k, v.v, 0.0, true, false, static_cast<double>(scale));
+      auto r = at::_scaled_dot_product_flash_attention(v.q, v.k, v.v, 0.0, causal, false, static_cast<double>(scale));
       o = std::get<0>(r);
       st->lse = std::get<1>(r);
       st->cum_q = std::get<2>(r);
@@ -149,13 +151,13 @@ int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int
       rep = st->rep;
       auto r = at::_scaled_dot_product_cudnn_attention_backward(
           go, v.q, expand_heads(v.k, rep), expand_heads(v.v, rep), st->out, st->lse, st->seed, st->offset,
-          at::Tensor(), st->cum_q, st->cum_k, st->max_q, st->max_k, 0.0, true, static_cast<double>(scale));
+          at::Tensor(), st->cum_q, st->cum_k, st->max_q, st->max_k, 0.0, st->causal, static_cast<double>(scale));
       dq = std::get<0>(r);
       dk = std::get<1>(r);  // nkv * rep heads; the pack kernel sums each group of rep
       dv = std::get<2>(r);
     } else {
       auto r = at::_scaled_dot_product_flash_attention_backward(go, v.q, v.k, v.v, st->out, st->lse, st->cum_q,
-                                                                st->cum_k, st->max_q, st->max_k, 0.0, true, st->seed,
+                                                                st->cum_k, st->max_q, st->max_k, 0.0, st->causal, st->seed,
                                                                 st->offset, static_cast<double>(scale));
       dq = std::get<0>(r);
       dk = std::get<1>(r);

@@ -23,8 +23,9 @@ const char* attn_last_error();
 
 // qkv: packed [B*S, (nh + 2 nkv) hd] bf16 after RoPE. *out receives the
 // attention output [B*S, nh*hd] (row stride *out_token_stride), owned by st.
+// causal = false: bidirectional (ViT encoder); the backward uses the forward's mode.
 int attn_fwd(AttnState* st, const void* qkv, int B, int S, int nh, int nkv, int hd, float scale, void** out,
-             long long* out_token_stride, cudaStream_t stream);
+             long long* out_token_stride, cudaStream_t stream, bool causal = true);
 // dout: [B*S, nh*hd] gradient of the attention output. Gradients stay owned by st.
 int attn_bwd(AttnState* st, const void* qkv, const void* dout, int B, int S, int nh, int nkv, int hd, float scale,
              AttnGrads* g, cudaStream_t stream);

@@ -160,6 +160,14 @@ int pf_trainer_create(const pf_model_cfg* m, const pf_train_cfg* c, pf_ctx** out
     mc.rope_theta = m->rope_theta;
     mc.norm_eps = m->norm_eps;
     mc.init_std = m->init_std;
+    if (m->family < 0 || m->family > 1) return PF_ERR_CONFIG;
+    mc.family = m->family;
+    if (m->family == 1) {
+      mc.image = m->image;
+      mc.patch = m->patch;
+      mc.channels = m->channels;
+      if (mc.patch <= 0 || mc.image % mc.patch || mc.channels <= 0) return PF_ERR_CONFIG;
+    }
     pf::TrainConfig tc;
     if (c->kind < 0 || c->kind > 4) return PF_ERR_CONFIG;
     tc.pipeline.schedule_kind = static_cast<pipefreeze::ScheduleKind>(c->kind);

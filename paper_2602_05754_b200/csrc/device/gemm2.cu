@@ -66,6 +66,7 @@ struct alignas(64) Params2 {
   long long ldr;
   __nv_bfloat16* aux;  // EPI_SWIGLU activation output
   long long ldaux;
+  const __nv_bfloat16* bias;  // EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (nullptr: none)
   int streamk;   // 0: one tile per work item; 1: even split of tile x k-block iterations
   float* ws;     // stream-K partials: [cluster][rank][128][BN] fp32
   int* flags;    // stream-K: [cluster][rank] == epoch once the partial is parked
@@ -411,6 +412,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
         const bool full = gcol + 32 <= p.N;
+        if (p.bias != nullptr) {  // per-column bias (ViT linear layers), same for every row
+          if (full) {
+            const uint4* b4 = reinterpret_cast<const uint4*>(p.bias + gcol);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 braw = __ldg(b4 + j);
+              const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(b2[i]);
+                v[8 * j + 2 * i] += f.x;
+                v[8 * j + 2 * i + 1] += f.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (gcol + i < p.N) v[i] += __bfloat162float(p.bias[gcol + i]);
+          }
+        }
         if constexpr (EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16) {
           __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + gcol;
           const __nv_bfloat16* rp = p.R + grow * p.ldr + gcol;
@@ -586,6 +607,8 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.ldr = C.residual ? C.ldr : C.ld;
   p.aux = static_cast<__nv_bfloat16*>(C.aux);
   p.ldaux = C.ldaux;
+  p.bias = static_cast<const __nv_bfloat16*>(C.bias);
+  if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16) return PF_ERR_INVALID;
   if (epi == EPI_SWIGLU && (N % BN != 0 || B.mn_major || !C.aux)) return PF_ERR_INVALID;
   if (epi == EPI_DSWIGLU && (N % 128 != 0 || !B.mn_major || !C.residual)) return PF_ERR_INVALID;
   p.M = M;

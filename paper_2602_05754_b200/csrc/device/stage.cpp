@@ -1,5 +1,8 @@
 #include "stage.hpp"
 
+#include "stage_ops.hpp"
+#include "vit_kernels.cuh"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -24,6 +27,10 @@ long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
   do {                                                     \
     if ((expr) != cudaSuccess) return PF_ERR_CUDA;         \
   } while (0)
+
+}  // namespace
+
+namespace ops {
 
 // CTA-pair (cta_group::2) kernel for the large K1/K2 GEMMs unless PF_GEMM_PAIR=0
 bool use_pair() {
@@ -88,6 +95,33 @@ int gemm_fwd_swiglu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* 
   return rc ? rc : launch_swiglu_fwd(gu, a, M, ffn, s);
 }
 
+int gemm_fwd_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* C,
+                  long long ldc, const __nv_bfloat16* bias, int M, int N, int K, cudaStream_t s) {
+  if (use_pair() && M >= 256 && N >= 256) {
+    GemmOut out{C, ldc};
+    out.bias = bias;
+    return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, N, K, 1.0f,
+                          EPI_STORE_BF16, s);
+  }
+  const int rc = gemm_fwd(A, lda, W, ldw, C, ldc, M, N, K, EPI_STORE_BF16, s);
+  return rc ? rc : launch_add_bias(C, ldc, bias, M, N, s);
+}
+
+int gemm_fwd_resid_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
+                        __nv_bfloat16* C, const __nv_bfloat16* R, long long ld, const __nv_bfloat16* bias, int M,
+                        int N, int K, cudaStream_t s) {
+  if (use_pair() && M >= 256 && N >= 256) {
+    GemmOut out{C, ld};
+    out.residual = R;
+    out.ldr = ld;
+    out.bias = bias;
+    return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, N, K, 1.0f, EPI_ADD_BF16,
+                          s);
+  }
+  const int rc = gemm_fwd_resid(A, lda, W, ldw, C, R, ld, M, N, K, s);
+  return rc ? rc : launch_add_bias(C, ld, bias, M, N, s);
+}
+
 int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
             int M, int N, int K, int epi, cudaStream_t s) {
   // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
@@ -110,7 +144,9 @@ int gemm_dx_dswiglu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16*
   return rc ? rc : launch_swiglu_bwd(gu, d_act, dgu, M, ffn, s);
 }
 
-}  // namespace
+}  // namespace ops
+
+using namespace ops;
 
 ParamSlice Stage::add_matrix(int rows, int cols, bool freezable) {
   ParamSlice p;
@@ -144,12 +180,45 @@ ParamSlice Stage::add_dense(long long n) {
   return p;
 }
 
-Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
-             bool split_backward)
+Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int device, bool split_backward)
     : cfg_(cfg), spec_(spec), device_(device), split_(split_backward) {
-  if (cfg.hidden % 128 || cfg.ffn % 64 || cfg.head_dim % 8 || cfg.vocab % 8 || cfg.tokens() % 128)
-    throw std::invalid_argument("stage: unsupported model shape (hidden % 128, ffn % 64, vocab % 8, T % 128)");
   cudaSetDevice(device);
+}
+
+void* Stage::alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(bytes, 256)) != cudaSuccess)
+    throw std::runtime_error("stage: cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  allocations_.push_back(p);
+  return p;
+}
+
+void Stage::allocate_parameters(uint64_t seed) {
+  master_ = alloc_f32(n_params_);
+  weights_ = alloc_bf16(n_params_);
+  grad_ = alloc_f32(n_params_);
+  stamps_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_) * 4));
+  cudaMemset(stamps_, 0, static_cast<size_t>(total_units_) * 4);
+  unit_lists_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_ + 64) * 4));
+  unit_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
+  mats_dev_ = static_cast<UnitMatrix*>(alloc(mats_.size() * sizeof(UnitMatrix)));
+  cudaMemcpy(mats_dev_, mats_.data(), mats_.size() * sizeof(UnitMatrix), cudaMemcpyHostToDevice);
+  // matrices N(0, init_std) (fixed seed per stage); families initialise their dense params
+  launch_init_normal(master_, weights_, n_unit_params_, cfg_.init_std,
+                     seed * 1000003ULL + static_cast<uint64_t>(spec_.stage), nullptr);
+  cudaMemset(grad_, 0, static_cast<size_t>(n_params_) * 4);
+}
+
+int Stage::build_unit_lists(const uint64_t* frozen_words, cudaStream_t s) {
+  return launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
+                                   unit_counts_, s);
+}
+
+LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
+                       bool split_backward)
+    : Stage(cfg, spec, device, split_backward) {
+  if (cfg.hidden % 128 || cfg.ffn % 128 || cfg.head_dim % 8 || cfg.vocab % 8 || cfg.tokens() % 128)
+    throw std::invalid_argument("stage: unsupported model shape (hidden % 128, ffn % 128, vocab % 8, T % 128)");
   const int h = cfg.hidden;
   const int nl = spec.layer_end - spec.layer_begin;
   layers_.resize(static_cast<std::size_t>(nl));
@@ -161,36 +230,17 @@ Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t 
     L.wd = add_matrix(h, cfg.ffn, true);
   }
   if (spec.last) wlm_ = add_matrix(cfg.vocab, h, true);
-  n_unit_params_ = n_params_;
-  dense_begin_ = n_params_;
+  end_unit_matrices();
   for (auto& L : layers_) {
     L.g1 = add_dense(h);
     L.g2 = add_dense(h);
   }
   if (spec.last) gf_ = add_dense(h);
   if (spec.first) emb_ = add_matrix(cfg.vocab, h, false);
-
-  auto alloc = [&](size_t bytes) -> void* {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(bytes, 256)) != cudaSuccess)
-      throw std::runtime_error("stage: cudaMalloc of " + std::to_string(bytes) + " bytes failed");
-    allocations_.push_back(p);
-    return p;
-  };
-  master_ = static_cast<float*>(alloc(static_cast<size_t>(n_params_) * 4));
-  weights_ = static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(n_params_) * 2));
-  grad_ = static_cast<float*>(alloc(static_cast<size_t>(n_params_) * 4));
-  stamps_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_) * 4));
-  cudaMemset(stamps_, 0, static_cast<size_t>(total_units_) * 4);
-  unit_lists_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_ + 64) * 4));
-  unit_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
-  mats_dev_ = static_cast<UnitMatrix*>(alloc(mats_.size() * sizeof(UnitMatrix)));
-  cudaMemcpy(mats_dev_, mats_.data(), mats_.size() * sizeof(UnitMatrix), cudaMemcpyHostToDevice);
+  allocate_parameters(seed);
   rope_ = static_cast<float2*>(alloc(static_cast<size_t>(cfg.seq) * (cfg.head_dim / 2) * sizeof(float2)));
   launch_rope_table(rope_, cfg.seq, cfg.head_dim, cfg.rope_theta, nullptr);
-
-  // init: N(0, init_std) for matrices, ones for norm gains (fixed seed per stage)
-  launch_init_normal(master_, weights_, n_unit_params_, cfg.init_std, seed * 1000003ULL + static_cast<uint64_t>(spec.stage), nullptr);
+  // ones for norm gains, N(0, init_std) for the embedding
   for (auto& L : layers_) {
     launch_fill(master_ + L.g1.offset, weights_ + L.g1.offset, h, 1.0f, nullptr);
     launch_fill(master_ + L.g2.offset, weights_ + L.g2.offset, h, 1.0f, nullptr);
@@ -199,11 +249,10 @@ Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t 
   if (spec.first)
     launch_init_normal(master_ + emb_.offset, weights_ + emb_.offset, emb_.count, cfg.init_std,
                        seed * 7919ULL + 17ULL, nullptr);
-  cudaMemset(grad_, 0, static_cast<size_t>(n_params_) * 4);
 
   const long long T = cfg.tokens();
-  auto abf = [&](long long elems) { return static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(elems) * 2)); };
-  auto af32 = [&](long long elems) { return static_cast<float*>(alloc(static_cast<size_t>(elems) * 4)); };
+  auto abf = [&](long long elems) { return alloc_bf16(elems); };
+  auto af32 = [&](long long elems) { return alloc_f32(elems); };
   slots_.resize(static_cast<std::size_t>(slots));
   for (auto& sl : slots_) {
     sl.layers.resize(static_cast<std::size_t>(nl));
@@ -241,10 +290,14 @@ Stage::Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t 
   if (cudaDeviceSynchronize() != cudaSuccess) throw std::runtime_error("stage: initialisation kernels failed");
 }
 
-Stage::~Stage() {
+LlamaStage::~LlamaStage() {
   cudaSetDevice(device_);
   for (auto& sl : slots_)
     for (auto& L : sl.layers) attn_state_free(L.attn);
+}
+
+Stage::~Stage() {
+  cudaSetDevice(device_);
   for (void* p : allocations_) cudaFree(p);
 }
 
@@ -259,7 +312,7 @@ int Stage::zero_dense_grads(cudaStream_t s) {
   return PF_OK;
 }
 
-int Stage::forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
+int LlamaStage::forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
                    float* loss_sum, cudaStream_t s) {
   if (slot < 0 || slot >= static_cast<int>(slots_.size())) return PF_ERR_INVALID;
   Slot& sl = slots_[static_cast<std::size_t>(slot)];
@@ -314,15 +367,22 @@ int Stage::forward(int slot, int microbatch, const int* tokens, const int* targe
 }
 
 int Stage::dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                       long long ldx, int stamp, cudaStream_t s) {
+                       long long ldx, int K, int stamp, cudaStream_t s) {
   const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
   GemmOut out{grad_ + w.offset, w.cols, stamps_, m.unit_offset, stamp};
   // dW[out, in] += dY^T . X over the unfrozen units; both operands MN-major (no transposes)
-  return gemm_bf16_units(GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, out, w.rows, w.cols,
-                         cfg_.tokens(), 1.0f, unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, s);
+  return gemm_bf16_units(GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, out, w.rows, w.cols, K, 1.0f,
+                         unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, s);
 }
 
-int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
+UnitGemm Stage::unit_gemm(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                          long long ldx) const {
+  const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
+  return UnitGemm{GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, grad_ + w.offset, w.cols, w.rows, w.cols,
+                  unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, m.unit_offset};
+}
+
+int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
                     __nv_bfloat16* dx_out, int stamp, cudaStream_t s) {
   if (slot < 0 || slot >= static_cast<int>(slots_.size()) || (!frozen_words && !split_)) return PF_ERR_INVALID;
   Slot& sl = slots_[static_cast<std::size_t>(slot)];
@@ -330,14 +390,13 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
   const int nl = static_cast<int>(layers_.size());
   // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units (W does it when split)
   if (!split_)
-    PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
-                                     unit_counts_, s));
+    PF_TRY(build_unit_lists(frozen_words, s));
   // split: every layer's output gradient lands in its slot buffer, the top one included
   __nv_bfloat16* top = split_ && nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
   const __nv_bfloat16* dcur = dy;
   if (spec_.last) {
     PF_TRY(gemm_dx(sl.logits, cfg_.vocab, weights_ + wlm_.offset, h, d_h_, h, T, h, cfg_.vocab, EPI_STORE_BF16, s));
-    if (!split_) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
+    if (!split_) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, T, stamp, s));
     PF_TRY(launch_rmsnorm_bwd(sl.x_out, weights_ + gf_.offset, sl.rstdf, d_h_, nullptr, top, grad_ + gf_.offset, T,
                               h, s));
     dcur = top;
@@ -389,7 +448,7 @@ int Stage::backward(int slot, const int* tokens, const uint64_t* frozen_words, c
   return PF_OK;
 }
 
-int Stage::layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
+int LlamaStage::layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
                               const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv,
                               int stamp, cudaStream_t s) {
   const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
@@ -399,22 +458,16 @@ int Stage::layer_weight_grads(const SavedLayer& L, const LayerParams& P, const _
   const __nv_bfloat16* xs[4] = {L.a, L.h2, L.attn_out, L.h1};
   const long long ldxs[4] = {ffn, h, L.attn_ld, h};
   UnitGemm items[4];
-  for (int k = 0; k < 4; ++k) {
-    const UnitMatrix& m = mats_[static_cast<std::size_t>(w[k]->unit_matrix)];
-    items[k] = UnitGemm{GemmOperand{dys[k], ldys[k], true}, GemmOperand{xs[k], ldxs[k], true},
-                        grad_ + w[k]->offset, w[k]->cols, w[k]->rows, w[k]->cols,
-                        unit_lists_ + m.unit_offset, unit_counts_ + w[k]->unit_matrix, m.units, m.unit_offset};
-  }
+  for (int k = 0; k < 4; ++k) items[k] = unit_gemm(*w[k], dys[k], ldys[k], xs[k], ldxs[k]);
   return gemm_bf16_units_grouped(items, 4, T, 1.0f, stamps_, stamp, s);
 }
 
-int Stage::backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) {
+int LlamaStage::backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) {
   if (!split_ || slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
   Slot& sl = slots_[static_cast<std::size_t>(slot)];
   const int h = cfg_.hidden;
-  PF_TRY(launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
-                                   unit_counts_, s));
-  if (spec_.last) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, stamp, s));
+  PF_TRY(build_unit_lists(frozen_words, s));
+  if (spec_.last) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, cfg_.tokens(), stamp, s));
   for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
     SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
     PF_TRY(layer_weight_grads(L, layers_[static_cast<std::size_t>(li)], L.dy, L.gu, L.dx2, L.qkv, stamp, s));
@@ -486,6 +539,20 @@ int Stage::optimizer_step(const OptimCfg& oc, int microbatches, int stamp, bool 
   return launch_adamw_dense(master_ + dense_begin_, weights_ + dense_begin_, grad_ + dense_begin_,
                             adam_m_ + dense_begin_, adam_v_ + dense_begin_, nd, inv_m, oc.lr, a.beta1, a.beta2,
                             a.one_minus_beta1, a.one_minus_beta2, oc.eps, oc.weight_decay, bc1, bc2, s);
+}
+
+}  // namespace pf
+
+namespace pf {
+
+std::unique_ptr<Stage> make_vit_stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed,
+                                      int device, bool split_backward);
+
+std::unique_ptr<Stage> make_stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed,
+                                  int device, bool split_backward) {
+  if (cfg.family == 1) return make_vit_stage(cfg, spec, slots, seed, device, split_backward);
+  if (cfg.family != 0) throw std::invalid_argument("stage: unknown model family");
+  return std::make_unique<LlamaStage>(cfg, spec, slots, seed, device, split_backward);
 }
 
 }  // namespace pf

@@ -38,8 +38,14 @@ struct ModelConfig {
   float rope_theta = 500000.f;
   float norm_eps = 1e-5f;
   float init_std = 0.02f;
+  // 0: LLaMA decoder (vocab = vocabulary). 1: ViT encoder: seq = patches + 1 (cls),
+  // vocab = classes, image / patch / channels give the patch-embedding input width.
+  int family = 0;
+  int image = 224, patch = 32, channels = 3;
 
   int tokens() const { return seq * micro_batch; }
+  int patch_dim() const { return patch * patch * channels; }
+  int patches() const { return (image / patch) * (image / patch); }
   int qkv_dim() const { return (n_heads + 2 * n_kv_heads) * head_dim; }
   int attn_dim() const { return n_heads * head_dim; }
 };
@@ -90,28 +96,30 @@ struct OptimCfg {
   double beta1 = 0.9, beta2 = 0.999;
 };
 
+// Shared by every model family: the flat parameter buffers (fp32 master, bf16 copy,
+// fp32 gradient), the 128x128 freeze-unit table, the K5 work lists, the masked K3
+// weight-gradient GEMM and the K6 optimizer (with fused K4 APF).
 class Stage {
  public:
-  // split_backward: backward() computes only input gradients (B) and keeps what
-  // backward_weight() (W) needs in the slot (zbv-split schedules).
-  Stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
-        bool split_backward = false);
-  ~Stage();
+  virtual ~Stage();
   Stage(const Stage&) = delete;
   Stage& operator=(const Stage&) = delete;
 
   // x_in: stage input activations [T, h] (ignored on the first stage, which
-  // embeds tokens). Returns a pointer to the stage output [T, h] inside the slot.
-  int forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
-              float* loss_sum, cudaStream_t s);
+  // embeds its input). Returns a pointer to the stage output [T, h] inside the slot.
+  virtual int forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
+                      float* loss_sum, cudaStream_t s) = 0;
   // frozen_words: device bitmask over this stage's units for this microbatch.
   // dy: gradient of the stage output (ignored on the last stage). dx_out
   // receives the gradient of the stage input (ignored on the first stage).
-  int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
-               __nv_bfloat16* dx_out, int stamp, cudaStream_t s);
+  virtual int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
+                       __nv_bfloat16* dx_out, int stamp, cudaStream_t s) = 0;
   // W of a split backward: the masked weight gradients of the microbatch in `slot`
   // (K5 lists + grouped K3) from the gradients its B left in the slot.
-  int backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s);
+  virtual int backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) = 0;
+  virtual const __nv_bfloat16* output(int slot) const = 0;
+  virtual long long matmul_flops_fwd() const;  // 2 * T * (matmul params of the stage)
+
   bool split_backward() const { return split_; }
   // SGD: theta -= lr * G / M (sandbox.cpp:250). AdamW: g = G / M into per-unit-step AdamW.
   // Units frozen in every microbatch of the step (stamp != this step) are not touched.
@@ -119,12 +127,10 @@ class Stage {
                      float apf_threshold, cudaStream_t s);
   int zero_dense_grads(cudaStream_t s);
 
-  const __nv_bfloat16* output(int slot) const { return slots_[slot].x_out; }
   int units() const { return total_units_; }
   int words() const { return (total_units_ + 63) / 64; }
   long long param_count() const { return n_params_; }
   long long unit_param_count() const { return n_unit_params_; }
-  long long matmul_flops_fwd() const;  // 2 * T * (matmul params of the stage)
   const std::vector<UnitMatrix>& unit_matrices() const { return mats_; }
   const ModelConfig& config() const { return cfg_; }
   const StageSpec& spec() const { return spec_; }
@@ -142,20 +148,29 @@ class Stage {
   float* apf_ema_abs() const { return apf_ema_abs_; }
   int last_unfrozen_units() const { return last_unfrozen_; }
 
- private:
+ protected:
+  Stage(const ModelConfig& cfg, const StageSpec& spec, int device, bool split_backward);
   ParamSlice add_matrix(int rows, int cols, bool freezable);
   ParamSlice add_dense(long long n);
-  int layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
-                         const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv, int stamp,
-                         cudaStream_t s);
+  // after the freezable matrices: everything registered later is dense
+  void end_unit_matrices() { n_unit_params_ = dense_begin_ = n_params_; }
+  // allocate master / weights / grad / stamps / unit lists; matrices ~ N(0, init_std)
+  void allocate_parameters(uint64_t seed);
+  void* alloc(size_t bytes);
+  __nv_bfloat16* alloc_bf16(long long elems) { return static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(elems) * 2)); }
+  float* alloc_f32(long long elems) { return static_cast<float*>(alloc(static_cast<size_t>(elems) * 4)); }
+  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units
+  int build_unit_lists(const uint64_t* frozen_words, cudaStream_t s);
+  // K3 for one matrix: G[w] (+)= dY^T . X over the unfrozen units, K = rows of dY / X
   int dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                  long long ldx, int stamp, cudaStream_t s);
+                  long long ldx, int K, int stamp, cudaStream_t s);
+  UnitGemm unit_gemm(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                     long long ldx) const;
 
   ModelConfig cfg_;
   StageSpec spec_;
   int device_;
-  std::vector<LayerParams> layers_;
-  ParamSlice emb_, gf_, wlm_;
+  bool split_ = false;
   std::vector<UnitMatrix> mats_;
   UnitMatrix* mats_dev_ = nullptr;
   long long n_params_ = 0, n_unit_params_ = 0, dense_begin_ = 0;
@@ -171,16 +186,44 @@ class Stage {
   float* adam_v_ = nullptr;
   int* unit_steps_ = nullptr;
   int dense_steps_ = 0;
-  bool split_ = false;
   int* unit_lists_ = nullptr;
   int* unit_counts_ = nullptr;
+  std::vector<void*> allocations_;
+  int last_unfrozen_ = 0;
+};
+
+// LLaMA-shaped decoder stage (RMSNorm, RoPE, GQA causal attention, SwiGLU, LM head).
+class LlamaStage final : public Stage {
+ public:
+  // split_backward: backward() computes only input gradients (B) and keeps what
+  // backward_weight() (W) needs in the slot (zbv-split schedules).
+  LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
+             bool split_backward = false);
+  ~LlamaStage() override;
+
+  int forward(int slot, int microbatch, const int* tokens, const int* targets, const __nv_bfloat16* x_in,
+              float* loss_sum, cudaStream_t s) override;
+  int backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
+               __nv_bfloat16* dx_out, int stamp, cudaStream_t s) override;
+  int backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) override;
+  const __nv_bfloat16* output(int slot) const override { return slots_[slot].x_out; }
+
+ private:
+  int layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
+                         const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv, int stamp,
+                         cudaStream_t s);
+
+  std::vector<LayerParams> layers_;
+  ParamSlice emb_, gf_, wlm_;
   float2* rope_ = nullptr;
   std::vector<Slot> slots_;
   // backward workspace
   __nv_bfloat16 *d_a_ = nullptr, *d_gu_ = nullptr, *d_h_ = nullptr, *d_x2_ = nullptr, *d_attn_ = nullptr,
                 *d_qkv_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr;
-  std::vector<void*> allocations_;
-  int last_unfrozen_ = 0;
 };
+
+// The stage of `cfg.family` (0 LLaMA decoder, 1 ViT encoder).
+std::unique_ptr<Stage> make_stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed,
+                                  int device, bool split_backward);
 
 }  // namespace pf

@@ -1,0 +1,30 @@
+// GEMM call patterns shared by the stage families (defined in stage.cpp): the
+// CTA-pair kernel for the large K1 / K2 GEMMs, the 1-CTA kernel below its tile size.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "pf_device_internal.hpp"
+
+namespace pf {
+namespace ops {
+
+bool use_pair();
+// Y[M,N] (op)= A[M,K] . W[N,K]^T, both K-major
+int gemm_fwd(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
+             int M, int N, int K, int epi, cudaStream_t s);
+// Y = R + A . W^T (residual fused in the CTA-pair epilogue)
+int gemm_fwd_resid(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* C,
+                   const __nv_bfloat16* R, long long ld, int M, int N, int K, cudaStream_t s);
+// Y = A . W^T + bias, and Y = R + A . W^T + bias (bias fused in the CTA-pair epilogue)
+int gemm_fwd_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* C,
+                  long long ldc, const __nv_bfloat16* bias, int M, int N, int K, cudaStream_t s);
+int gemm_fwd_resid_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
+                        __nv_bfloat16* C, const __nv_bfloat16* R, long long ld, const __nv_bfloat16* bias, int M,
+                        int N, int K, cudaStream_t s);
+// dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
+int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
+            int M, int N, int K, int epi, cudaStream_t s);
+
+}  // namespace ops
+}  // namespace pf

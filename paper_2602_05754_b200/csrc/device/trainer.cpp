@@ -39,11 +39,14 @@ StageSpec stage_spec(const ModelConfig& m, int s, int S) {
 
 int units_of(int rows, int cols) { return ((rows + 127) / 128) * ((cols + 127) / 128); }
 
-// Unit count of a stage without allocating it (same matrix list as Stage).
+// Unit count of a stage without allocating it (same matrix lists as LlamaStage / VitStage).
 int stage_units(const ModelConfig& m, const StageSpec& sp) {
+  const int mlp_in = m.family == 1 ? m.ffn : 2 * m.ffn;  // ViT fc1 vs LLaMA gate|up
   const int per_layer = units_of(m.qkv_dim(), m.hidden) + units_of(m.hidden, m.attn_dim()) +
-                        units_of(2 * m.ffn, m.hidden) + units_of(m.hidden, m.ffn);
-  return (sp.layer_end - sp.layer_begin) * per_layer + (sp.last ? units_of(m.vocab, m.hidden) : 0);
+                        units_of(mlp_in, m.hidden) + units_of(m.hidden, m.ffn);
+  int u = (sp.layer_end - sp.layer_begin) * per_layer + (sp.last ? units_of(m.vocab, m.hidden) : 0);
+  if (m.family == 1 && sp.first) u += units_of(m.hidden, m.patch_dim());  // patch embedding
+  return u;
 }
 
 }  // namespace
@@ -77,8 +80,7 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
     slots_.push_back(std::max(1, peak));
   }
   for (std::size_t i = 0; i < stage_ids_.size(); ++i)
-    stages_.push_back(std::make_unique<Stage>(model, stage_spec(model, stage_ids_[i], S), slots_[i], cfg.seed,
-                                              cfg.device, split));
+    stages_.push_back(make_stage(model, stage_spec(model, stage_ids_[i], S), slots_[i], cfg.seed, cfg.device, split));
   const long long T = model.tokens();
   auto act_alloc = [&]() {
     __nv_bfloat16* p = nullptr;
@@ -496,7 +498,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   }
   // the next step's masks while this one runs (not in hybrid mode, whose base set comes from
   // this step's APF result, nor across the LP solve, which changes the plan)
-  if (!cfg_.hybrid) {
+  if (!cfg_.hybrid && (!controller || t + 1 <= cfg_.phases.t_total)) {
     const Phase next_phase = controller ? phase_of(t + 1, cfg_.phases) : Phase::StableFreeze;
     if (!(controller && next_phase == Phase::Solve && !plan_ready_)) {
       build_masks(t + 1, next_phase, controller, masks_next_, &next_frozen_, &next_total_);

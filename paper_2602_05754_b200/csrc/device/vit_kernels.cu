@@ -1,0 +1,388 @@
+// K7 glue of the ViT encoder stage (ViT-L/32): LayerNorm with
+// bias, GELU (erf form), per-column bias gradients, the patch / cls / position
+// embedding, the cls-row gather for the classification head, and the synthetic
+// patch input. All HBM-bound elementwise or row/column reductions over bf16
+// activations with fp32 statistics and fp32 parameter gradients.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "kernel_util.cuh"
+#include "vit_kernels.cuh"
+
+namespace pf {
+
+namespace {
+
+// LayerNorm forward, one warp per row: mean, then variance around it (second pass
+// from L1/L2), y = (x - mean) * rstd * g + b.
+__global__ void __launch_bounds__(kBlock) layernorm_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ g,
+                                                               const __nv_bfloat16* __restrict__ b,
+                                                               __nv_bfloat16* __restrict__ y,
+                                                               float* __restrict__ mean_out,
+                                                               float* __restrict__ rstd_out, int T, int h,
+                                                               float eps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
+    const __nv_bfloat16* xr = x + static_cast<long long>(t) * h;
+    float s = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8];
+      load8(xr + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += f[i];
+    }
+    const float mu = warp_sum(s) / h;
+    float ss = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8];
+      load8(xr + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += (f[i] - mu) * (f[i] - mu);
+    }
+    const float r = rsqrtf(warp_sum(ss) / h + eps);
+    if (lane == 0) {
+      mean_out[t] = mu;
+      rstd_out[t] = r;
+    }
+    __nv_bfloat16* yr = y + static_cast<long long>(t) * h;
+    for (int c = lane * 8; c < h; c += 256) {
+      float f[8], gg[8], bb[8];
+      load8(xr + c, f);
+      load8(g + c, gg);
+      load8(b + c, bb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = (f[i] - mu) * r * gg[i] + bb[i];
+      store8(yr + c, f);
+    }
+  }
+}
+
+// dx = residual + rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)); one warp per row
+__global__ void __launch_bounds__(kBlock) layernorm_bwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ g,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               const __nv_bfloat16* __restrict__ dy,
+                                                               const __nv_bfloat16* __restrict__ residual,
+                                                               __nv_bfloat16* __restrict__ dx, int T, int h) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
+    const long long off = static_cast<long long>(t) * h;
+    const float mu = mean[t], r = rstd[t];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+      float xv[8], gv[8], dv[8];
+      load8(x + off + c, xv);
+      load8(g + c, gv);
+      load8(dy + off + c, dv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gd = gv[i] * dv[i];
+        s1 += gd;
+        s2 += gd * (xv[i] - mu) * r;
+      }
+    }
+    const float m1 = warp_sum(s1) / h, m2 = warp_sum(s2) / h;
+    for (int c = lane * 8; c < h; c += 256) {
+      float xv[8], gv[8], dv[8], out[8];
+      load8(x + off + c, xv);
+      load8(g + c, gv);
+      load8(dy + off + c, dv);
+      if (residual) load8(residual + off + c, out);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        out[i] = (residual ? out[i] : 0.f) + r * (gv[i] * dv[i] - m1 - (xv[i] - mu) * r * m2);
+      store8(dx + off + c, out);
+    }
+  }
+}
+
+// Column reductions over T rows (block = 32 column groups of 8 x 8 row lanes):
+//   dg[c] += sum_t dy[t,c] * (x[t,c] - mean[t]) * rstd[t]   (when x != nullptr)
+//   db[c] += sum_t dy[t,c]
+__global__ void __launch_bounds__(kBlock) column_reduce_kernel(const __nv_bfloat16* __restrict__ dy, long long ldy,
+                                                               const __nv_bfloat16* __restrict__ x,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               float* __restrict__ dg, float* __restrict__ db,
+                                                               int T, int n, int rows_per_block) {
+  __shared__ float pg[8][256 + 4];
+  __shared__ float pb[8][256 + 4];
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 256 + cg * 8;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(T, r0 + rows_per_block);
+  float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < n) {
+    for (int t = r0 + rl; t < r1; t += 8) {
+      float dv[8];
+      load8(dy + static_cast<long long>(t) * ldy + c, dv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ab[i] += dv[i];
+      if (x) {
+        float xv[8];
+        load8(x + static_cast<long long>(t) * n + c, xv);
+        const float mu = mean[t], r = rstd[t];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ag[i] += dv[i] * (xv[i] - mu) * r;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    pg[rl][cg * 8 + i] = ag[i];
+    pb[rl][cg * 8 + i] = ab[i];
+  }
+  __syncthreads();
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  if (col < n) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sg += pg[k][threadIdx.x];
+      sb += pb[k][threadIdx.x];
+    }
+    if (x && dg) atomicAdd(&dg[col], sg);
+    if (db) atomicAdd(&db[col], sb);
+  }
+}
+
+__device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_erf_grad(float v) {
+  return 0.5f * (1.f + erff(v * 0.70710678118654752f)) + v * 0.39894228040143268f * __expf(-0.5f * v * v);
+}
+
+__global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ pre, __nv_bfloat16* __restrict__ act, long long n8) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float f[8];
+    load8(pre + i * 8, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = gelu_erf(f[k]);
+    store8(act + i * 8, f);
+  }
+}
+
+__global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ pre, const __nv_bfloat16* __restrict__ dact,
+                                __nv_bfloat16* __restrict__ dpre, long long n8) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float p[8], d[8];
+    load8(pre + i * 8, p);
+    load8(dact + i * 8, d);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) d[k] *= gelu_erf_grad(p[k]);
+    store8(dpre + i * 8, d);
+  }
+}
+
+__global__ void add_bias_kernel(__nv_bfloat16* __restrict__ c, long long ldc, const __nv_bfloat16* __restrict__ bias,
+                                int M, int N) {
+  const int chunks = N / 8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < static_cast<long long>(M) * chunks;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / chunks;
+    const int col = static_cast<int>(i - r * chunks) * 8;
+    float v[8], b[8];
+    load8(c + r * ldc + col, v);
+    load8(bias + col, b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += b[k];
+    store8(c + r * ldc + col, v);
+  }
+}
+
+// x[b, 0] = cls + pos[0]; x[b, 1 + p] = E[b * np + p] + patch_bias + pos[1 + p]
+__global__ void vit_embed_fwd_kernel(const __nv_bfloat16* __restrict__ E, const __nv_bfloat16* __restrict__ pbias,
+                                     const __nv_bfloat16* __restrict__ cls, const __nv_bfloat16* __restrict__ pos,
+                                     __nv_bfloat16* __restrict__ x, int B, int S, int h) {
+  const int chunks = h / 8;
+  const long long total = static_cast<long long>(B) * S * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = i / chunks;
+    const int c = static_cast<int>(i - row * chunks) * 8;
+    const int b = static_cast<int>(row / S), p = static_cast<int>(row - static_cast<long long>(b) * S);
+    float v[8], q[8];
+    load8(pos + static_cast<long long>(p) * h + c, q);
+    if (p == 0) {
+      load8(cls + c, v);
+    } else {
+      float bb[8];
+      load8(E + (static_cast<long long>(b) * (S - 1) + (p - 1)) * h + c, v);
+      load8(pbias + c, bb);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] += bb[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] += q[k];
+    store8(x + row * h + c, v);
+  }
+}
+
+// Backward of vit_embed_fwd: dE rows gathered from dx, dpos[p] += sum_b dx[b, p],
+// dcls += sum_b dx[b, 0], dpatch_bias += sum_b sum_{p>0} dx[b, p].
+__global__ void vit_embed_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfloat16* __restrict__ dE,
+                                     float* __restrict__ dpos, float* __restrict__ dcls, float* __restrict__ dpbias,
+                                     int B, int S, int h) {
+  const int chunks = h / 8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       i < static_cast<long long>(S) * chunks; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int p = static_cast<int>(i / chunks);
+    const int c = static_cast<int>(i - static_cast<long long>(p) * chunks) * 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < B; ++b) {
+      const long long row = static_cast<long long>(b) * S + p;
+      float v[8];
+      load8(dx + row * h + c, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+      if (p > 0) *reinterpret_cast<uint4*>(dE + (static_cast<long long>(b) * (S - 1) + (p - 1)) * h + c) =
+          *reinterpret_cast<const uint4*>(dx + row * h + c);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dpos[static_cast<long long>(p) * h + c + k] += acc[k];
+      if (p == 0) dcls[c + k] += acc[k];
+      else atomicAdd(&dpbias[c + k], acc[k]);
+    }
+  }
+}
+
+// out[b] = x[b * S + row_in_seq]   (cls rows for the head) / scatter back into zeros
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out, int B,
+                                   int S, int h) {
+  const int chunks = h / 8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+       i < static_cast<long long>(B) * chunks; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / chunks;
+    const int c = static_cast<int>(i - b * chunks) * 8;
+    *reinterpret_cast<uint4*>(out + b * h + c) = *reinterpret_cast<const uint4*>(x + b * S * h + c);
+  }
+}
+
+__global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dx, int B,
+                                    int S, int h) {
+  const int chunks = h / 8;
+  const long long total = static_cast<long long>(B) * S * chunks;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = i / chunks;
+    const int c = static_cast<int>(i - row * chunks) * 8;
+    const long long b = row / S;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (row - b * S == 0) v = *reinterpret_cast<const uint4*>(src + b * h + c);
+    *reinterpret_cast<uint4*>(dx + row * h + c) = v;
+  }
+}
+
+// deterministic synthetic pixels in [-1, 1) (splitmix64 of the element index)
+__global__ void synthetic_patches_kernel(__nv_bfloat16* __restrict__ out, long long n, uint64_t seed) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    uint64_t z = seed + static_cast<uint64_t>(i + 1) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    out[i] = __float2bfloat16_rn(static_cast<float>(z >> 40) * 0x1.0p-23f - 1.f);
+  }
+}
+
+void column_grid(int T, int n, int* col_blocks, int* row_chunks, int* rows_per_block) {
+  *col_blocks = (n + 255) / 256;
+  int rc = std::max(1, (2 * num_sms()) / *col_blocks);
+  *rows_per_block = std::max(8, (T + rc - 1) / rc);
+  *row_chunks = (T + *rows_per_block - 1) / *rows_per_block;
+}
+
+}  // namespace
+
+int launch_layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
+                         float* mean, float* rstd, int T, int h, float eps, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  layernorm_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, b, y, mean, rstd, T, h, eps);
+  return status();
+}
+
+int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* mean, const float* rstd,
+                         const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
+                         float* db, int T, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  layernorm_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, mean, rstd, dy, residual, dx, T, h);
+  int rc = status();
+  if (rc != PF_OK || (!dg && !db)) return rc;
+  int cb, rcn, rpb;
+  column_grid(T, h, &cb, &rcn, &rpb);
+  column_reduce_kernel<<<dim3(cb, rcn), kBlock, 0, s>>>(dy, h, x, mean, rstd, dg, db, T, h, rpb);
+  return status();
+}
+
+int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, int n, cudaStream_t s) {
+  if (n % 8 || ldy % 8) return PF_ERR_INVALID;
+  int cb, rcn, rpb;
+  column_grid(T, n, &cb, &rcn, &rpb);
+  column_reduce_kernel<<<dim3(cb, rcn), kBlock, 0, s>>>(dy, ldy, nullptr, nullptr, nullptr, nullptr, db, T, n, rpb);
+  return status();
+}
+
+int launch_gelu_fwd(const __nv_bfloat16* pre, __nv_bfloat16* act, long long n, cudaStream_t s) {
+  if (n % 8) return PF_ERR_INVALID;
+  gelu_fwd_kernel<<<grid_for((n / 8 + kBlock - 1) / kBlock), kBlock, 0, s>>>(pre, act, n / 8);
+  return status();
+}
+
+int launch_gelu_bwd(const __nv_bfloat16* pre, const __nv_bfloat16* dact, __nv_bfloat16* dpre, long long n,
+                    cudaStream_t s) {
+  if (n % 8) return PF_ERR_INVALID;
+  gelu_bwd_kernel<<<grid_for((n / 8 + kBlock - 1) / kBlock), kBlock, 0, s>>>(pre, dact, dpre, n / 8);
+  return status();
+}
+
+int launch_add_bias(__nv_bfloat16* c, long long ldc, const __nv_bfloat16* bias, int M, int N, cudaStream_t s) {
+  if (N % 8 || ldc % 8) return PF_ERR_INVALID;
+  add_bias_kernel<<<grid_for((static_cast<long long>(M) * (N / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(c, ldc, bias,
+                                                                                                           M, N);
+  return status();
+}
+
+int launch_vit_embed_fwd(const __nv_bfloat16* E, const __nv_bfloat16* pbias, const __nv_bfloat16* cls,
+                         const __nv_bfloat16* pos, __nv_bfloat16* x, int B, int S, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  vit_embed_fwd_kernel<<<grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      E, pbias, cls, pos, x, B, S, h);
+  return status();
+}
+
+int launch_vit_embed_bwd(const __nv_bfloat16* dx, __nv_bfloat16* dE, float* dpos, float* dcls, float* dpbias, int B,
+                         int S, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  vit_embed_bwd_kernel<<<grid_for((static_cast<long long>(S) * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      dx, dE, dpos, dcls, dpbias, B, S, h);
+  return status();
+}
+
+int launch_gather_rows(const __nv_bfloat16* x, __nv_bfloat16* out, int B, int S, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  gather_rows_kernel<<<grid_for((static_cast<long long>(B) * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(x, out, B,
+                                                                                                              S, h);
+  return status();
+}
+
+int launch_scatter_rows(const __nv_bfloat16* src, __nv_bfloat16* dx, int B, int S, int h, cudaStream_t s) {
+  if (h % 8) return PF_ERR_INVALID;
+  scatter_rows_kernel<<<grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+      src, dx, B, S, h);
+  return status();
+}
+
+int launch_synthetic_patches(__nv_bfloat16* out, long long n, uint64_t seed, cudaStream_t s) {
+  synthetic_patches_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(out, n, seed);
+  return status();
+}
+
+}  // namespace pf

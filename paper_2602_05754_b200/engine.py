@@ -30,10 +30,18 @@ class ModelShape:
     rope_theta: float = 500000.0
     norm_eps: float = 1e-5
     init_std: float = 0.02
+    family: int = 0  # 0 LLaMA decoder, 1 ViT encoder (vocab = classes, micro_batch = images)
+    image: int = 224
+    patch: int = 32
+    channels: int = 3
 
     @property
     def tokens(self) -> int:
         return self.seq * self.micro_batch
+
+    @property
+    def patch_dim(self) -> int:
+        return self.patch * self.patch * self.channels
 
     @property
     def qkv_dim(self) -> int:
@@ -41,7 +49,8 @@ class ModelShape:
 
     def matmul_params_per_layer(self) -> int:
         h = self.hidden
-        return self.qkv_dim * h + h * self.n_heads * self.head_dim + 2 * self.ffn * h + h * self.ffn
+        mlp_in = self.ffn if self.family == 1 else 2 * self.ffn
+        return self.qkv_dim * h + h * self.n_heads * self.head_dim + mlp_in * h + h * self.ffn
 
 
 PRESETS = {
@@ -53,6 +62,10 @@ PRESETS = {
     "llama-8b": ModelShape(4096, 14336, 32, 8, 128, 128256, 32, 2048, 2),
     # LLaMA-2-13B shapes (configs[3])
     "llama-13b": ModelShape(5120, 13824, 40, 40, 128, 32000, 40, 2048, 1, rope_theta=10000.0),
+    # ViT-L/32 (configs[4], C5): 224^2 / 32^2 patches -> 49 + cls = 50 tokens, 64 images per microbatch
+    "vit-l-32": ModelShape(1024, 4096, 16, 16, 64, 1000, 24, 50, 64, norm_eps=1e-6, family=1),
+    # small ViT for parity tests: 48^2 images, 16^2 patches -> 9 + cls = 10 tokens, 64 images (T = 640)
+    "vit-tiny": ModelShape(256, 512, 4, 4, 64, 1000, 4, 10, 64, norm_eps=1e-6, family=1, image=48, patch=16),
 }
 
 
@@ -78,6 +91,29 @@ def param_layout(shape: ModelShape, s: int, S: int) -> dict:
 
     b, e = stage_layers(shape.layers, S, s)
     h = shape.hidden
+    if shape.family == 1:  # VitStage constructor order
+        if s == 1:
+            add("patch_w", h, shape.patch_dim, True)
+        for layer in range(b, e):
+            add(f"l{layer}.wqkv", 3 * h, h, True)
+            add(f"l{layer}.wo", h, h, True)
+            add(f"l{layer}.w1", shape.ffn, h, True)
+            add(f"l{layer}.w2", h, shape.ffn, True)
+        if s == S:
+            add("head", shape.vocab, h, True)
+        for layer in range(b, e):
+            for name, n in (("bqkv", 3 * h), ("bo", h), ("b1", shape.ffn), ("b2", h), ("ln1g", h), ("ln1b", h),
+                            ("ln2g", h), ("ln2b", h)):
+                add(f"l{layer}.{name}", 1, n, False)
+        if s == 1:
+            add("patch_b", 1, h, False)
+            add("cls", 1, h, False)
+            add("pos", shape.seq, h, False)
+        if s == S:
+            add("lnfg", 1, h, False)
+            add("lnfb", 1, h, False)
+            add("headb", 1, shape.vocab, False)
+        return _finish_layout(out, off)
     for layer in range(b, e):
         add(f"l{layer}.wqkv", shape.qkv_dim, h, True)
         add(f"l{layer}.wo", h, shape.n_heads * shape.head_dim, True)
@@ -92,6 +128,10 @@ def param_layout(shape: ModelShape, s: int, S: int) -> dict:
         add("gf", 1, h, False)
     if s == 1:
         add("emb", shape.vocab, h, False)
+    return _finish_layout(out, off)
+
+
+def _finish_layout(out: dict, off: int) -> dict:
     u = 0
     for ent in out["units"]:
         ent["unit_offset"] = u
@@ -124,7 +164,8 @@ class Trainer:
         self.M = microbatches
         self.S = ranks * stages_per_rank
         m = PfModelCfg(shape.hidden, shape.ffn, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.vocab,
-                       shape.layers, shape.seq, shape.micro_batch, shape.rope_theta, shape.norm_eps, shape.init_std)
+                       shape.layers, shape.seq, shape.micro_batch, shape.rope_theta, shape.norm_eps, shape.init_std,
+                       shape.family, shape.image, shape.patch, shape.channels)
         c = PfTrainCfg()
         c.kind = KINDS[schedule]
         self.kinds = 3 if c.kind in SPLIT_KINDS else 2  # action kinds per cell: f, b (, w)
