@@ -163,9 +163,14 @@ int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
 int pf_trainer_stage_buffers(pf_ctx* ctx, int local_stage, void** master, void** weights, void** grad,
                              void** stamps, long long* n_params, int* n_units);
 /* Multi-rank pipeline: `count` ncclUniqueId blobs (128 B each) created on one rank and
- * shared with all; pf_trainer_init_comm takes 4 of them (activation and gradient
- * chains, two communicators each) and must be called on every rank before step 1. */
+ * shared with all. pf_trainer_init_comm takes pf_trainer_comm_ids() of them: the world
+ * communicator (monitoring all-reduce), then one two-rank communicator per P2P link
+ * (a cross-rank (activation | gradient, src rank, dst rank) class of DAG rule-3 edges),
+ * and must be called on every rank before step 1. */
 int pf_nccl_unique_ids(void* out, int count);
+int pf_trainer_comm_ids(pf_ctx* ctx, int* count);
+/* links[3*k..3*k+2] = (kind 0 act / 1 grad, src rank, dst rank) for k < pf_trainer_comm_ids - 1 */
+int pf_trainer_links(pf_ctx* ctx, int* links);
 /* Library backend used for the attention glue: "cudnn" or "flash" (ATen). */
 const char* pf_attention_backend(void);
 int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank);

@@ -72,6 +72,8 @@ DEVICE_SIGNATURES = {
     "pf_trainer_init_comm": ([c_vp, c_vp, c_int, c_int], c_int),
     "pf_device_launch_count": ([], c_ll),
     "pf_probe_enable": ([c_int], c_int),
+    "pf_trainer_comm_ids": ([c_vp, ctypes.POINTER(c_int)], c_int),
+    "pf_trainer_links": ([c_vp, c_vp], c_int),
     "pf_probe_read": ([ctypes.POINTER(c_int), ctypes.POINTER(c_d)], c_int),
 }
 

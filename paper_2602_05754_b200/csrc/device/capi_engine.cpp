@@ -391,6 +391,27 @@ extern "C" int pf_trainer_action_starts(pf_ctx* ctx, double* start_ms) {
 
 extern "C" const char* pf_attention_backend(void) { return pf::attn_backend_is_cudnn() ? "cudnn" : "flash"; }
 
+extern "C" int pf_trainer_comm_ids(pf_ctx* ctx, int* count) {
+  return guard([&] {
+    if (!ctx || !count) return PF_ERR_INVALID;
+    *count = ctx->trainer->comm_ids_needed();
+    return PF_OK;
+  });
+}
+
+extern "C" int pf_trainer_links(pf_ctx* ctx, int* out) {
+  return guard([&] {
+    if (!ctx || !out) return PF_ERR_INVALID;
+    int k = 0;
+    for (const auto& l : ctx->trainer->links()) {
+      out[k++] = l.kind;
+      out[k++] = l.src;
+      out[k++] = l.dst;
+    }
+    return PF_OK;
+  });
+}
+
 extern "C" int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank) {
   return guard([&] { return ctx ? ctx->trainer->init_comm(ids, nranks, rank) : PF_ERR_INVALID; });
 }

@@ -63,9 +63,16 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   actions_ = timeline_.rank_order[static_cast<std::size_t>(cfg.rank)];
   for (int s = 1; s <= S; ++s)
     if (stage_to_rank(cfg.pipeline, s) == cfg.rank) stage_ids_.push_back(s);
-  if (cfg.pipeline.num_ranks > 1 && cfg.pipeline.schedule_kind != ScheduleKind::GPipe &&
-      cfg.pipeline.schedule_kind != ScheduleKind::OneFOneB)
-    throw std::invalid_argument("trainer: multi-rank transport supports gpipe and 1f1b (one stage per rank)");
+  // cross-rank edge classes of DAG rule 3 (dag.cpp:90-93): one P2P link each
+  for (int s = 1; s < S; ++s) {
+    const int a = stage_to_rank(cfg.pipeline, s), b = stage_to_rank(cfg.pipeline, s + 1);
+    if (a == b) continue;
+    for (const Link& l : {Link{0, a, b}, Link{1, b, a}}) {
+      bool seen = false;
+      for (const Link& x : links_) seen |= x.kind == l.kind && x.src == l.src && x.dst == l.dst;
+      if (!seen) links_.push_back(l);
+    }
+  }
   // in-flight microbatches per stage = slot count; a slot is held from F until the
   // action that last reads it: b, or w when the backward is split
   const bool split = splits_weight_grad(cfg.pipeline);
@@ -149,12 +156,12 @@ Trainer::~Trainer() {
   for (auto* vv : {&x_free_ev_, &out_sent_ev_, &dy_free_ev_, &dx_sent_ev_})
     for (auto& v : *vv)
       for (auto e : v) cudaEventDestroy(e);
-  for (int k = 0; k < 2; ++k) {
-    if (comm_act_[k]) ncclCommDestroy(static_cast<ncclComm_t>(comm_act_[k]));
-    if (comm_grad_[k]) ncclCommDestroy(static_cast<ncclComm_t>(comm_grad_[k]));
+  for (auto& l : links_) {
+    if (l.comm) ncclCommDestroy(static_cast<ncclComm_t>(l.comm));
+    if (l.stream) cudaStreamDestroy(l.stream);
   }
-  for (cudaStream_t s : {act_send_, act_recv_, grad_send_, grad_recv_})
-    if (s) cudaStreamDestroy(s);
+  if (world_comm_) ncclCommDestroy(static_cast<ncclComm_t>(world_comm_));
+  if (ctl_stream_) cudaStreamDestroy(ctl_stream_);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (ev_opt0_) cudaEventDestroy(ev_opt0_);
   if (ev_opt1_) cudaEventDestroy(ev_opt1_);
@@ -216,20 +223,34 @@ FreezeMask Trainer::apf_base_mask(int li) const {
 
 TimingProfile Trainer::measured_profile() const { return plan_profile_.all().empty() ? aggregate_monitoring(monitor_) : plan_profile_; }
 
+Trainer::Link* Trainer::link(int kind, int src, int dst) {
+  for (auto& l : links_)
+    if (l.kind == kind && l.src == src && l.dst == dst) return &l;
+  return nullptr;
+}
+
 int Trainer::init_comm(const void* ids, int nranks, int rank) {
-  if (nranks != cfg_.pipeline.num_ranks || rank != cfg_.rank || !ids) return PF_ERR_INVALID;
+  if (nranks != cfg_.pipeline.num_ranks || rank != cfg_.rank || !ids || distributed()) return PF_ERR_INVALID;
   cudaSetDevice(cfg_.device);
-  ncclUniqueId u[4];
-  std::memcpy(u, ids, sizeof(u));
-  ncclComm_t c[4];
-  for (int k = 0; k < 4; ++k)  // same order on every rank
-    if (ncclCommInitRank(&c[k], nranks, u[k], rank) != ncclSuccess) return PF_ERR_NCCL;
-  comm_act_[0] = c[0];
-  comm_act_[1] = c[1];
-  comm_grad_[0] = c[2];
-  comm_grad_[1] = c[3];
-  for (cudaStream_t* s : {&act_send_, &act_recv_, &grad_send_, &grad_recv_})
-    if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) return PF_ERR_CUDA;
+  const int n = comm_ids_needed();
+  std::vector<ncclUniqueId> u(static_cast<std::size_t>(n));
+  std::memcpy(u.data(), ids, static_cast<size_t>(n) * sizeof(ncclUniqueId));
+  ncclComm_t w;
+  if (ncclCommInitRank(&w, nranks, u[0], rank) != ncclSuccess) return PF_ERR_NCCL;
+  world_comm_ = w;
+  // every link this rank is an end of, initialised together (no ordering constraints)
+  if (ncclGroupStart() != ncclSuccess) return PF_ERR_NCCL;
+  for (std::size_t k = 0; k < links_.size(); ++k) {
+    Link& l = links_[k];
+    if (rank != l.src && rank != l.dst) continue;
+    ncclComm_t c;
+    if (ncclCommInitRank(&c, 2, u[k + 1], rank == l.src ? 0 : 1) != ncclSuccess) return PF_ERR_NCCL;
+    l.comm = c;
+  }
+  if (ncclGroupEnd() != ncclSuccess) return PF_ERR_NCCL;
+  for (auto& l : links_)
+    if (l.comm && cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking) != cudaSuccess) return PF_ERR_CUDA;
+  if (cudaStreamCreateWithFlags(&ctl_stream_, cudaStreamNonBlocking) != cudaSuccess) return PF_ERR_CUDA;
   for (auto* vv : {&x_free_ev_, &out_sent_ev_, &dy_free_ev_, &dx_sent_ev_}) {
     vv->resize(stage_ids_.size());
     for (std::size_t i = 0; i < stage_ids_.size(); ++i) {
@@ -256,12 +277,12 @@ int Trainer::exchange_monitoring(TimingProfile* merged) {
   if (distributed()) {
     double* dev = nullptr;
     if (cudaMalloc(&dev, host.size() * sizeof(double)) != cudaSuccess) return PF_ERR_CUDA;
-    cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, act_send_);
-    if (ncclAllReduce(dev, dev, host.size(), ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm_act_[0]),
-                      act_send_) != ncclSuccess)
+    cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, ctl_stream_);
+    if (ncclAllReduce(dev, dev, host.size(), ncclFloat64, ncclSum, static_cast<ncclComm_t>(world_comm_),
+                      ctl_stream_) != ncclSuccess)
       return PF_ERR_NCCL;
-    cudaMemcpyAsync(host.data(), dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost, act_send_);
-    cudaStreamSynchronize(act_send_);
+    cudaMemcpyAsync(host.data(), dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost, ctl_stream_);
+    cudaStreamSynchronize(ctl_stream_);
     cudaFree(dev);
   }
   TimingProfile p;
@@ -397,7 +418,8 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   if (needs_comm && !distributed()) return PF_ERR_NCCL;  // init_comm() first
   auto nccl_ok = [](ncclResult_t r) { return r == ncclSuccess ? PF_OK : PF_ERR_NCCL; };
   const int r = cfg_.rank;
-  auto comm = [](void* c) { return static_cast<ncclComm_t>(c); };
+  auto comm = [](const Link* l) { return static_cast<ncclComm_t>(l->comm); };
+  auto rank_of = [&](int s) { return stage_to_rank(cfg_.pipeline, s); };
   for (std::size_t i = 0; i < actions_.size(); ++i) {
     const ActionId a = actions_[i];
     const int li = local_index(a.stage);
@@ -412,10 +434,11 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       const bool recv_x = a.stage > 1 && local_index(a.stage - 1) < 0;
       const bool send_y = a.stage < S && local_index(a.stage + 1) < 0;
       if (recv_x) {  // f(m, s-1) output over NVLink into this slot's receive buffer
-        PF_CUDA(cudaStreamWaitEvent(act_recv_, x_free_ev_[ls][ss], 0));
-        PF_TRY(nccl_ok(ncclRecv(x_recv_[ls][ss], act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage - 1),
-                                comm(comm_act_[(r - 1) & 1]), act_recv_)));
-        PF_TRY(after(stream_, act_recv_));
+        const Link* l = link(0, rank_of(a.stage - 1), r);
+        if (!l || !l->comm) return PF_ERR_NCCL;
+        PF_CUDA(cudaStreamWaitEvent(l->stream, x_free_ev_[ls][ss], 0));
+        PF_TRY(nccl_ok(ncclRecv(x_recv_[ls][ss], act_bytes, ncclUint8, 0, comm(l), l->stream)));
+        PF_TRY(after(stream_, l->stream));
         x_in = x_recv_[ls][ss];
       } else if (a.stage > 1) {
         const int lp = local_index(a.stage - 1);
@@ -427,10 +450,11 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
       if (recv_x) PF_CUDA(cudaEventRecord(x_free_ev_[ls][ss], stream_));
       if (send_y) {  // to f(m, s+1)
-        PF_TRY(after(act_send_, stream_));
-        PF_TRY(nccl_ok(ncclSend(st.output(slot), act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage + 1),
-                                comm(comm_act_[r & 1]), act_send_)));
-        PF_CUDA(cudaEventRecord(out_sent_ev_[ls][ss], act_send_));
+        const Link* l = link(0, r, rank_of(a.stage + 1));
+        if (!l || !l->comm) return PF_ERR_NCCL;
+        PF_TRY(after(l->stream, stream_));
+        PF_TRY(nccl_ok(ncclSend(st.output(slot), act_bytes, ncclUint8, 1, comm(l), l->stream)));
+        PF_CUDA(cudaEventRecord(out_sent_ev_[ls][ss], l->stream));
       }
     } else if (a.kind == ActionKind::Weight) {  // split backward: dW of the slot's microbatch
       const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
@@ -442,10 +466,11 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       const bool send_dx = a.stage > 1 && local_index(a.stage - 1) < 0;
       const __nv_bfloat16* dy = nullptr;
       if (recv_dy) {  // b(m, s+1) input gradient
-        PF_CUDA(cudaStreamWaitEvent(grad_recv_, dy_free_ev_[ls][ss], 0));
-        PF_TRY(nccl_ok(ncclRecv(dy_recv_[ls][ss], act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage + 1),
-                                comm(comm_grad_[(r + 1) & 1]), grad_recv_)));
-        PF_TRY(after(stream_, grad_recv_));
+        const Link* l = link(1, rank_of(a.stage + 1), r);
+        if (!l || !l->comm) return PF_ERR_NCCL;
+        PF_CUDA(cudaStreamWaitEvent(l->stream, dy_free_ev_[ls][ss], 0));
+        PF_TRY(nccl_ok(ncclRecv(dy_recv_[ls][ss], act_bytes, ncclUint8, 0, comm(l), l->stream)));
+        PF_TRY(after(stream_, l->stream));
         dy = dy_recv_[ls][ss];
       } else if (a.stage < S) {
         dy = grad_bufs_[ls][ss];
@@ -465,15 +490,17 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
       if (recv_dy) PF_CUDA(cudaEventRecord(dy_free_ev_[ls][ss], stream_));
       if (send_dx) {  // to b(m, s-1)
-        PF_TRY(after(grad_send_, stream_));
-        PF_TRY(nccl_ok(ncclSend(dx, act_bytes, ncclUint8, stage_to_rank(cfg_.pipeline, a.stage - 1),
-                                comm(comm_grad_[r & 1]), grad_send_)));
-        PF_CUDA(cudaEventRecord(dx_sent_ev_[ls][ss], grad_send_));
+        const Link* l = link(1, r, rank_of(a.stage - 1));
+        if (!l || !l->comm) return PF_ERR_NCCL;
+        PF_TRY(after(l->stream, stream_));
+        PF_TRY(nccl_ok(ncclSend(dx, act_bytes, ncclUint8, 1, comm(l), l->stream)));
+        PF_CUDA(cudaEventRecord(dx_sent_ev_[ls][ss], l->stream));
       }
     }
   }
   if (distributed()) {  // the step ends when its last transfers have landed
-    for (cudaStream_t cs : {act_send_, act_recv_, grad_send_, grad_recv_}) PF_TRY(after(stream_, cs));
+    for (const Link& l : links_)
+      if (l.stream) PF_TRY(after(stream_, l.stream));
   }
   // ---- masked optimizer step: theta -= (eta / M) * sum_m U_m . g_m
   PF_CUDA(cudaEventRecord(ev_opt0_, stream_));

@@ -89,12 +89,24 @@ class Trainer {
   // this step's frozen-unit masks of local stage li: M masks of (words + 1) uint64 each
   const uint64_t* masks_host(int li) const { return masks_host_ + mask_offsets_[static_cast<std::size_t>(li)]; }
 
-  // Multi-rank P2P (NCCL over NVLink). Four communicators over the same ranks:
-  // activations r->r+1 use comm_act[r % 2], gradients r->r-1 use comm_grad[r % 2],
-  // so on every rank each communicator is driven by exactly one stream and only
-  // in one direction (sends never queue behind receives). ids: 4 x 128 bytes.
+  // Multi-rank P2P (NCCL over NVLink). One two-rank communicator and stream per link:
+  // a (kind, src rank, dst rank) class of DAG rule-3 edges that crosses ranks
+  // (activations s -> s+1, gradients s+1 -> s), so every communicator carries one
+  // direction of one edge class and no transfer queues behind another link's. This
+  // covers every placement: chains (gpipe / 1f1b), the interleaved ring (rank R-1 ->
+  // rank 0) and the ZBV V (activations flow both ways). Plus one world communicator
+  // for the monitoring all-reduce at T_m. ids: comm_ids_needed() x 128 bytes, the
+  // world id first, then one per link in links() order (same on every rank).
   int init_comm(const void* ids, int nranks, int rank);
-  bool distributed() const { return comm_act_[0] != nullptr; }
+  bool distributed() const { return world_comm_ != nullptr; }
+  struct Link {
+    int kind;      // 0 activations (forward edge), 1 gradients (backward edge)
+    int src, dst;  // ranks
+    void* comm = nullptr;  // ncclComm_t with src = comm rank 0, dst = comm rank 1
+    cudaStream_t stream = nullptr;
+  };
+  const std::vector<Link>& links() const { return links_; }
+  int comm_ids_needed() const { return 1 + static_cast<int>(links_.size()); }
 
  private:
   int local_index(int stage) const;
@@ -103,9 +115,10 @@ class Trainer {
                    long long* total);
   int exchange_monitoring(pipefreeze::TimingProfile* merged);
 
-  void* comm_act_[2] = {nullptr, nullptr};   // ncclComm_t
-  void* comm_grad_[2] = {nullptr, nullptr};  // ncclComm_t
-  cudaStream_t act_send_ = nullptr, act_recv_ = nullptr, grad_send_ = nullptr, grad_recv_ = nullptr;
+  Link* link(int kind, int src, int dst);
+  std::vector<Link> links_;
+  void* world_comm_ = nullptr;  // ncclComm_t over all ranks (monitoring all-reduce)
+  cudaStream_t ctl_stream_ = nullptr;
   std::vector<std::vector<__nv_bfloat16*>> x_recv_;   // [local stage][slot] activations from rank_of(s-1)
   std::vector<std::vector<__nv_bfloat16*>> dy_recv_;  // [local stage][slot] gradients from rank_of(s+1)
   std::vector<std::vector<__nv_bfloat16*>> dx_send_;  // [local stage][slot] gradient of the stage input

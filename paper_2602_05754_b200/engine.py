@@ -187,19 +187,30 @@ class Trainer:
     def init_comm(self) -> None:
         """Set up the NCCL P2P transport for a multi-rank pipeline (call on every rank).
 
-        Rank 0 creates the four ncclUniqueIds (activation and gradient chains, two
-        communicators each) and shares them over the default torch.distributed group."""
+        Rank 0 creates the ncclUniqueIds (the world communicator, then one two-rank
+        communicator per P2P link, see links()) and shares them over the default
+        torch.distributed group."""
         import torch.distributed as dist
 
         world, rank = dist.get_world_size(), dist.get_rank()
+        n = ctypes.c_int(0)
+        _check(self.lib.pf_trainer_comm_ids(self._ctx, ctypes.byref(n)), "comm_ids")
         obj = [None]
         if rank == 0:
-            buf = ctypes.create_string_buffer(4 * 128)
-            _check(self.lib.pf_nccl_unique_ids(buf, 4), "nccl_unique_ids")
+            buf = ctypes.create_string_buffer(n.value * 128)
+            _check(self.lib.pf_nccl_unique_ids(buf, n.value), "nccl_unique_ids")
             obj = [bytes(buf.raw)]
         dist.broadcast_object_list(obj, src=0)
-        ids = ctypes.create_string_buffer(obj[0], 4 * 128)
+        ids = ctypes.create_string_buffer(obj[0], n.value * 128)
         _check(self.lib.pf_trainer_init_comm(self._ctx, ids, world, rank), "trainer_init_comm")
+
+    def links(self) -> list[tuple[int, int, int]]:
+        """P2P links of the pipeline: (kind 0 activations / 1 gradients, src rank, dst rank)."""
+        n = ctypes.c_int(0)
+        _check(self.lib.pf_trainer_comm_ids(self._ctx, ctypes.byref(n)), "comm_ids")
+        out = np.zeros(max(1, 3 * (n.value - 1)), dtype=np.int32)
+        _check(self.lib.pf_trainer_links(self._ctx, out.ctypes.data_as(ctypes.c_void_p)), "links")
+        return [tuple(int(x) for x in out[3 * k:3 * k + 3]) for k in range(n.value - 1)]
 
     def close(self) -> None:
         if self._ctx:

@@ -156,6 +156,21 @@ def stage_to_rank(config: PipelineConfig, stage: int) -> int:
     return out.value
 
 
+def p2p_links(config: PipelineConfig) -> list[tuple[int, int, int]]:
+    """Cross-rank classes of DAG rule-3 edges (dag.cpp:90-93), one NCCL link each, in the device
+    trainer's order (trainer.cpp): for s = 1..S-1 with rank(s) != rank(s+1), the activation link
+    (0, rank(s), rank(s+1)) then the gradient link (1, rank(s+1), rank(s)), first occurrence kept."""
+    out = []
+    for s in range(1, config.total_stages):
+        a, b = stage_to_rank(config, s), stage_to_rank(config, s + 1)
+        if a == b:
+            continue
+        for link in ((0, a, b), (1, b, a)):
+            if link not in out:
+                out.append(link)
+    return out
+
+
 class PipelineDag:
     """Node ids: 0 = src, 1 + kind*M*S + (s-1)*M + (m-1), N-1 = dst (dag.cpp:18-23; kind 2 = w
     exists only for zbv-split)."""

@@ -1,14 +1,15 @@
 """Multi-rank pipeline transport logic on CPU (gloo, world size 2 and 4).
 
-The device trainer (csrc/device/trainer.cpp, Trainer::step) drives P2P with four
-communicators: activations r->r+1 on comm_act[r % 2], gradients r->r-1 on
-comm_grad[r % 2], each on its own stream, compute waiting on receive events and
-send streams waiting on compute. This test replays exactly that issue program
-(same rank action lists from libpf_host's build_schedule, same channel/peer
-rules) with one thread per stream and gloo process groups standing in for the
-NCCL communicators, and checks that it completes (no deadlock) and that every
-stage consumes the payload of the right (microbatch, stage) edge of the DAG
-(rule 3, proj/src/dag.cpp:90-93).
+The device trainer (csrc/device/trainer.cpp, Trainer::step) drives P2P over one two-rank
+communicator and stream per link: a cross-rank (activation | gradient, src rank, dst rank)
+class of DAG rule-3 edges (pipefreeze.p2p_links). Compute waits on receive events; sends
+wait on compute; neighbouring stages on the same rank hand over locally. This test replays
+exactly that issue program (same rank action lists from libpf_host's build_schedule, same
+link rules, every placement: gpipe / 1f1b chains, the interleaved ring, the ZBV V with
+activations flowing both ways, zbv-split's W actions) with one thread per link stream and a
+gloo process group per link standing in for the NCCL communicators, and checks that it
+completes (no deadlock) and that every stage consumes the payload of the right
+(microbatch, stage) edge of the DAG (rule 3, proj/src/dag.cpp:90-93).
 """
 import os
 import queue
@@ -17,7 +18,7 @@ import threading
 import pytest
 
 
-def _worker(rank, world, kind, M, port, errq):
+def _worker(rank, world, kind, C, M, port, errq):
     import torch
     import torch.distributed as dist
 
@@ -25,14 +26,14 @@ def _worker(rank, world, kind, M, port, errq):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        groups = {name: dist.new_group(list(range(world)), backend="gloo")
-                  for name in ("act0", "act1", "grad0", "grad1")}
         from paper_2602_05754_b200 import pipefreeze as pf
 
-        cfg = pf.PipelineConfig(kind, world, 1, M)
+        cfg = pf.PipelineConfig(kind, world, C, M)
+        links = pf.p2p_links(cfg)
+        groups = {l: dist.new_group([l[1], l[2]], backend="gloo") for l in links}  # collective, same order
         actions = pf.build_schedule(cfg).rank_order[rank]
-        S = world
-        stage = rank + 1
+        S = cfg.total_stages
+        rank_of = {s: pf.stage_to_rank(cfg, s) for s in range(1, S + 1)}
 
         class Stream:
             """In-order op queue on a thread (a CUDA stream stand-in)."""
@@ -63,40 +64,45 @@ def _worker(rank, world, kind, M, port, errq):
                 self.q.put(None)
                 self.t.join(timeout=60)
 
-        act_send, act_recv, grad_send, grad_recv = Stream(), Stream(), Stream(), Stream()
+        streams = {l: Stream() for l in links if rank in (l[1], l[2])}
         consumed = []
         pending_sends = []
         for a in actions:
-            m = a.microbatch
+            m, s = a.microbatch, a.stage
             if a.kind == 0:  # forward f(m, s)
-                if stage > 1:
+                if s > 1 and rank_of[s - 1] != rank:
+                    l = (0, rank_of[s - 1], rank)
                     buf = torch.zeros(2)
-                    ev = act_recv.submit(lambda b=buf: dist.recv(b, src=rank - 1, group=groups[f"act{(rank - 1) % 2}"]))
-                    assert ev.wait(60), "activation receive timed out"
-                    assert buf.tolist() == [m, stage - 1], (buf.tolist(), m, stage)
-                    consumed.append(("f", m))
-                out = torch.tensor([float(m), float(stage)])
-                if stage < S:
-                    pending_sends.append(act_send.submit(
-                        lambda t=out: dist.send(t, dst=rank + 1, group=groups[f"act{rank % 2}"])))
-            else:  # backward b(m, s)
-                if stage < S:
+                    ev = streams[l].submit(lambda b=buf, l=l: dist.recv(b, src=l[1], group=groups[l]))
+                    assert ev.wait(60), f"activation receive timed out at {a}"
+                    assert buf.tolist() == [m, s - 1], (buf.tolist(), m, s)
+                    consumed.append(("f", m, s))
+                out = torch.tensor([float(m), float(s)])
+                if s < S and rank_of[s + 1] != rank:
+                    l = (0, rank, rank_of[s + 1])
+                    pending_sends.append(streams[l].submit(lambda t=out, l=l: dist.send(t, dst=l[2], group=groups[l])))
+            elif a.kind == 1:  # backward b(m, s) (dX)
+                if s < S and rank_of[s + 1] != rank:
+                    l = (1, rank_of[s + 1], rank)
                     buf = torch.zeros(2)
-                    ev = grad_recv.submit(lambda b=buf: dist.recv(b, src=rank + 1, group=groups[f"grad{(rank + 1) % 2}"]))
-                    assert ev.wait(60), "gradient receive timed out"
-                    assert buf.tolist() == [-m, stage + 1], (buf.tolist(), m, stage)
-                    consumed.append(("b", m))
-                g = torch.tensor([-float(m), float(stage)])
-                if stage > 1:
-                    pending_sends.append(grad_send.submit(
-                        lambda t=g: dist.send(t, dst=rank - 1, group=groups[f"grad{rank % 2}"])))
+                    ev = streams[l].submit(lambda b=buf, l=l: dist.recv(b, src=l[1], group=groups[l]))
+                    assert ev.wait(60), f"gradient receive timed out at {a}"
+                    assert buf.tolist() == [-m, s + 1], (buf.tolist(), m, s)
+                    consumed.append(("b", m, s))
+                g = torch.tensor([-float(m), float(s)])
+                if s > 1 and rank_of[s - 1] != rank:
+                    l = (1, rank, rank_of[s - 1])
+                    pending_sends.append(streams[l].submit(lambda t=g, l=l: dist.send(t, dst=l[2], group=groups[l])))
+            # w(m, s): local dW only, no transfer
         for ev in pending_sends:
             assert ev.wait(60), "send never matched"
-        for s in (act_send, act_recv, grad_send, grad_recv):
-            s.close()
-        # every remote input of this stage arrived exactly once, in schedule order
-        exp = [("f", a.microbatch) for a in actions if a.kind == 0 and stage > 1] + \
-              [("b", a.microbatch) for a in actions if a.kind == 1 and stage < S]
+        for st in streams.values():
+            st.close()
+        # every remote input of this rank's stages arrived exactly once
+        exp = [("f", a.microbatch, a.stage) for a in actions
+               if a.kind == 0 and a.stage > 1 and rank_of[a.stage - 1] != rank] + \
+              [("b", a.microbatch, a.stage) for a in actions
+               if a.kind == 1 and a.stage < S and rank_of[a.stage + 1] != rank]
         assert sorted(consumed) == sorted(exp)
         dist.barrier()
         dist.destroy_process_group()
@@ -106,14 +112,17 @@ def _worker(rank, world, kind, M, port, errq):
         errq.put(f"rank {rank}: {e!r}\n{traceback.format_exc()}")
 
 
-@pytest.mark.parametrize("kind,world,M", [("1f1b", 2, 4), ("gpipe", 2, 3), ("1f1b", 4, 8), ("gpipe", 4, 2)])
-def test_p2p_issue_program_completes_and_routes(kind, world, M):
+@pytest.mark.parametrize("kind,world,C,M", [("1f1b", 2, 1, 4), ("gpipe", 2, 1, 3), ("1f1b", 4, 1, 8), ("gpipe", 4, 1, 2),
+                                            ("interleaved-1f1b", 2, 2, 4), ("interleaved-1f1b", 4, 2, 8),
+                                            ("zbv", 2, 2, 4), ("zbv", 4, 2, 8), ("zbv-split", 2, 2, 4),
+                                            ("zbv-split", 4, 2, 6)])
+def test_p2p_issue_program_completes_and_routes(kind, world, C, M):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
-    port = 29500 + hash((kind, world, M)) % 1000
-    procs = [ctx.Process(target=_worker, args=(r, world, kind, M, port, errq)) for r in range(world)]
+    port = 29500 + (abs(hash((kind, world, C, M))) % 2000)
+    procs = [ctx.Process(target=_worker, args=(r, world, kind, C, M, port, errq)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -123,3 +132,21 @@ def test_p2p_issue_program_completes_and_routes(kind, world, M):
         errs.append(errq.get())
     assert not errs, "\n".join(errs)
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+@pytest.mark.parametrize("kind,world,C", [("1f1b", 4, 1), ("interleaved-1f1b", 4, 2), ("zbv", 4, 2)])
+def test_p2p_links_cover_every_cross_rank_edge(kind, world, C):
+    from paper_2602_05754_b200 import pipefreeze as pf
+
+    cfg = pf.PipelineConfig(kind, world, C, 4)
+    links = pf.p2p_links(cfg)
+    S = cfg.total_stages
+    for s in range(1, S):
+        a, b = pf.stage_to_rank(cfg, s), pf.stage_to_rank(cfg, s + 1)
+        if a != b:
+            assert (0, a, b) in links and (1, b, a) in links
+    assert len(set(links)) == len(links)
+    if kind == "interleaved-1f1b":
+        assert (0, world - 1, 0) in links  # the ring's wrap-around edge
+    if kind == "zbv":
+        assert (0, 1, 0) in links and (0, 0, 1) in links  # the V: activations both ways

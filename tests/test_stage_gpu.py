@@ -247,3 +247,21 @@ def test_zbv_split_controller_plan_over_w_nodes(cuda):
     assert np.all(p["ratios"] <= 1.0) and p["ratios"].mean() <= 0.8 + 1e-6
     assert p["makespan_opt"] <= p["makespan_base"]
     tr.close()
+
+
+@pytest.mark.parametrize("schedule,ranks,C", [("1f1b", 4, 1), ("interleaved-1f1b", 4, 2), ("zbv", 2, 2),
+                                              ("zbv-split", 4, 2)])
+def test_trainer_p2p_links_match_host_rule(cuda, schedule, ranks, C):
+    """The device trainer's NCCL link list (one communicator per cross-rank edge class) is the one
+    the gloo replay of the issue program validated (pipefreeze.p2p_links)."""
+    from paper_2602_05754_b200 import pipefreeze as pf
+    from paper_2602_05754_b200.engine import PRESETS, Trainer
+
+    import dataclasses
+
+    cfg = pf.PipelineConfig(schedule, ranks, C, 4)
+    tr = Trainer(dataclasses.replace(PRESETS["tiny"], layers=8), schedule, ranks, C, 4, rank=1)
+    assert tr.links() == pf.p2p_links(cfg)
+    with pytest.raises(Exception):
+        tr.step(1)  # remote neighbours and no init_comm(): refused, not silently local
+    tr.close()
