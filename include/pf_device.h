@@ -44,6 +44,14 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
                      const int* unit_list, const int* unit_count, int max_units,
                      int* unit_stamp, int stamp_offset, int stamp, void* stream);
 
+/* K3 on a CTA pair (tcgen05.mma.cta_group::2, M = 256 from two units, N = 128): the same
+ * masked, unit-stamped G[M,N] (+)= dY^T . X, with dY stored [K][ldy] (logical A [M,K],
+ * MN-major) and X stored [K][ldx] (logical B [N,K], MN-major), over the padded pair list
+ * pairs[0..*pair_count) that pf_mask_to_pair_lists writes for this matrix. */
+int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                     int N, int K, const int* pairs, const int* pair_count, int* unit_stamp, int stamp_offset,
+                     int stamp, void* stream);
+
 /* K1 gate|up projection with the SwiGLU activation fused in the CTA-pair epilogue:
  * gu[T, 2*ffn] = h[T, K] . Wgu^T (bf16, Wgu rows interleave 128-blocks [gate b | up b]),
  * a[T, ffn] = silu(gate) * up from the bf16-rounded gu (== pf_swiglu_fwd(gu)). ffn % 128 == 0. */
@@ -70,13 +78,20 @@ typedef struct pf_unit_matrix {
   int unit_offset;       /* first unit id of the matrix within the stage */
   int tiles_n;           /* ceil(cols / 128) */
   int units;             /* ceil(rows/128) * tiles_n */
-  int pad_;
+  int pair_offset;       /* first entry of the matrix's K5p pair list: units + pair groups slots */
 } pf_unit_matrix;
 
 /* K5: frozen-unit bitmask (sample_mask bit order, one bit per 128x128 unit, +1
  * pad word) -> per-matrix lists of unfrozen local unit ids (lists[unit_offset..])
  * and counts[matrix]. mats is a DEVICE array of nmats entries. */
 int pf_mask_to_unit_lists(const uint64_t* frozen_words, const pf_unit_matrix* mats, int nmats, int* lists,
+                          int* counts, void* stream);
+
+/* K5p: the same mask -> per-matrix PAIR lists for pf_gemm_dw_pairs at pairs[pair_offset..]:
+ * unit rows cut into bands of 32 (more when a matrix has > 2048 band x column groups),
+ * groups (band, column) band by band, each group's unfrozen unit ids top to bottom,
+ * padded to an even count with -1; counts[matrix] = padded entry count. */
+int pf_mask_to_pair_lists(const uint64_t* frozen_words, const pf_unit_matrix* mats, int nmats, int* pairs,
                           int* counts, void* stream);
 
 /* K6 (+ fused K4): theta -= scale * G over units whose stamp == `stamp`

@@ -60,6 +60,11 @@ int pf_mask_to_unit_lists(const uint64_t* words, const pf_unit_matrix* mats, int
   return guard([&] { return pf::launch_mask_to_unit_lists(words, U(mats), nmats, lists, counts, S(stream)); });
 }
 
+int pf_mask_to_pair_lists(const uint64_t* words, const pf_unit_matrix* mats, int nmats, int* pairs, int* counts,
+                          void* stream) {
+  return guard([&] { return pf::launch_mask_to_pair_lists(words, U(mats), nmats, pairs, counts, S(stream)); });
+}
+
 int pf_masked_sgd_units(float* master, void* weights, const float* grad, const int* stamp_arr, int stamp, float scale,
                         const pf_unit_matrix* mats, int nmats, int total_units, float* ema, float* ema_abs,
                         float apf_alpha, float apf_threshold, int* eligible, void* stream) {

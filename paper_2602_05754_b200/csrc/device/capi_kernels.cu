@@ -44,6 +44,14 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
                                     static_cast<cudaStream_t>(stream)));
 }
 
+int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                     int N, int K, const int* pairs, const int* pair_count, int* unit_stamp, int stamp_offset,
+                     int stamp, void* stream) {
+  if (!dY || !X || !G) return PF_ERR_INVALID;
+  pf::DwGemm it{dY, ldy, X, ldx, G, ldg, M, N, K, pairs, pair_count, stamp_offset};
+  return record(pf::gemm_dw_pairs(&it, 1, unit_stamp, stamp, static_cast<cudaStream_t>(stream)));
+}
+
 int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw, void* gu, void* a, int T, int ffn,
                    int K, void* stream) {
   if (!h || !Wgu || !gu || !a || ffn % 128 != 0) return PF_ERR_INVALID;

@@ -76,6 +76,54 @@ __global__ void __launch_bounds__(kBlock) mask_to_lists_kernel(const uint64_t* _
   if (threadIdx.x == 0) counts[blockIdx.x] = carry;
 }
 
+// ------------------------------------------------------------------ K5p
+// One block per matrix; warp w walks groups w, w + 8, ...: a ballot over 32 row
+// blocks at a time finds the group's unfrozen units, its padded count goes to
+// shared memory, a block scan gives every group its even base, and a second
+// ballot pass writes the ids.
+__global__ void __launch_bounds__(kBlock) mask_to_pairs_kernel(const uint64_t* __restrict__ words,
+                                                               const UnitMatrix* __restrict__ mats,
+                                                               int* __restrict__ pairs, int* __restrict__ counts) {
+  const UnitMatrix m = mats[blockIdx.x];
+  __shared__ int base[kPairGroups + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tiles_n = m.tiles_n, tiles_m = m.units / m.tiles_n;
+  const int band = pair_band_rows(tiles_m, tiles_n);
+  const int groups = pair_groups(tiles_m, tiles_n);
+  auto unfrozen = [&](int mb, int nb, int mb_end) -> bool {
+    if (mb >= mb_end) return false;
+    const long long g = static_cast<long long>(m.unit_offset) + static_cast<long long>(mb) * tiles_n + nb;
+    return ((words[g >> 6] >> (g & 63)) & 1ull) == 0;
+  };
+  for (int g = warp; g < groups; g += kBlock / 32) {
+    const int b = g / tiles_n, nb = g - b * tiles_n;
+    const int mb0 = b * band, mb1 = min(tiles_m, mb0 + band);
+    int cnt = 0;
+    for (int r0 = mb0; r0 < mb1; r0 += 32) cnt += __popc(__ballot_sync(0xffffffffu, unfrozen(r0 + lane, nb, mb1)));
+    if (lane == 0) base[g + 1] = cnt + (cnt & 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    base[0] = 0;
+    for (int g = 0; g < groups; ++g) base[g + 1] += base[g];
+    counts[blockIdx.x] = base[groups];
+  }
+  __syncthreads();
+  int* out = pairs + m.pair_offset;
+  for (int g = warp; g < groups; g += kBlock / 32) {
+    const int b = g / tiles_n, nb = g - b * tiles_n;
+    const int mb0 = b * band, mb1 = min(tiles_m, mb0 + band);
+    int pos = base[g];
+    for (int r0 = mb0; r0 < mb1; r0 += 32) {
+      const bool u = unfrozen(r0 + lane, nb, mb1);
+      const uint32_t bal = __ballot_sync(0xffffffffu, u);
+      if (u) out[pos + __popc(bal & ((1u << lane) - 1u))] = (r0 + lane) * tiles_n + nb;
+      pos += __popc(bal);
+    }
+    if (lane == 0 && pos < base[g + 1]) out[pos] = -1;
+  }
+}
+
 // ------------------------------------------------------------------ K6 (+K4 fused)
 struct AdamCoef {
   float step_size;  // lr / bc1
@@ -572,6 +620,13 @@ int launch_mask_to_unit_lists(const uint64_t* words, const UnitMatrix* mats, int
                               cudaStream_t s) {
   if (nmats <= 0) return PF_OK;
   mask_to_lists_kernel<<<nmats, kBlock, 0, s>>>(words, mats, lists, counts);
+  return status();
+}
+
+int launch_mask_to_pair_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* pairs, int* counts,
+                              cudaStream_t s) {
+  if (nmats <= 0) return PF_OK;
+  mask_to_pairs_kernel<<<nmats, kBlock, 0, s>>>(words, mats, pairs, counts);
   return status();
 }
 

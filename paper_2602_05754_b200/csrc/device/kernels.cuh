@@ -15,6 +15,7 @@ struct UnitMatrix {
   int unit_offset;        // first unit id of this matrix in the stage
   int tiles_n;            // ceil(cols / 128)
   int units;              // tiles_m * tiles_n
+  int pair_offset;        // first entry of this matrix's padded pair list (K5p): units + pair_groups slots
 };
 
 constexpr int kMaxUnitMatrices = 512;
@@ -23,6 +24,26 @@ constexpr int kMaxUnitMatrices = 512;
 // (reference sample_mask bit order, proj/include/pipefreeze/freezectl.hpp:47)
 int launch_mask_to_unit_lists(const uint64_t* frozen_words, const UnitMatrix* mats_dev, int nmats,
                               int* lists, int* counts, cudaStream_t s);
+
+// ---- K5p: the same mask -> per-matrix PAIR lists for the CTA-pair dW (gemm_dw.cu).
+// Rows of units are cut into bands of pair_band_rows(); a group is (band, column).
+// Groups go band by band, columns in order inside a band, and each group lists its
+// unfrozen local unit ids (mb * tiles_n + nb) top to bottom, padded to an even count
+// with -1, at pairs[pair_offset..]; counts[matrix] = padded entry count. Pairs thus
+// share their X column block (the pair MMA's B) and a band of dY columns stays in
+// L2 while its columns are swept.
+constexpr int kPairGroups = 2048;  // (band, column) groups per matrix
+__host__ __device__ inline int pair_band_rows(int tiles_m, int tiles_n) {
+  int band = 32;
+  while (((tiles_m + band - 1) / band) * tiles_n > kPairGroups) band *= 2;
+  return band;
+}
+__host__ __device__ inline int pair_groups(int tiles_m, int tiles_n) {
+  const int band = pair_band_rows(tiles_m, tiles_n);
+  return ((tiles_m + band - 1) / band) * tiles_n;
+}
+int launch_mask_to_pair_lists(const uint64_t* frozen_words, const UnitMatrix* mats_dev, int nmats, int* pairs,
+                              int* counts, cudaStream_t s);
 
 // ---- K6: masked SGD over unit matrices, theta -= scale * G for units whose
 // stamp equals `stamp` (touched this step); optional fused APF (K4) update of

@@ -61,6 +61,23 @@ struct UnitGemm {
 int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
                             cudaStream_t stream);
 
+// K3 on a CTA pair (gemm_dw.cu): one matrix's masked dW over its padded pair list
+// (K5p output: unfrozen units column-major, each column padded to an even count with -1).
+constexpr int kMaxDwProblems = 96;  // matrices per launch (kernel parameter space <= 32 KB)
+struct DwGemm {
+  const void* dy;    // bf16 [K][M]: output-feature gradient (MN-major A)
+  long long ldy;
+  const void* x;     // bf16 [K][N]: layer input (MN-major B)
+  long long ldx;
+  float* C;          // fp32 gradient of the matrix [M][N]
+  long long ldc;
+  int M, N, K;
+  const int* pairs;       // device pair list of this matrix
+  const int* pair_count;  // device: padded entry count
+  int stamp_offset;       // first unit id of the matrix in the stage
+};
+int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
+
 // K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
                    int epi, cudaStream_t stream);

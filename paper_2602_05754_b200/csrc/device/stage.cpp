@@ -163,6 +163,8 @@ ParamSlice Stage::add_matrix(int rows, int cols, bool freezable) {
     m.unit_offset = total_units_;
     m.tiles_n = (cols + 127) / 128;
     m.units = ((rows + 127) / 128) * m.tiles_n;
+    m.pair_offset = pair_capacity_;
+    pair_capacity_ += m.units + pair_groups((rows + 127) / 128, m.tiles_n);
     total_units_ += m.units;
     p.unit_matrix = static_cast<int>(mats_.size());
     mats_.push_back(m);
@@ -199,8 +201,8 @@ void Stage::allocate_parameters(uint64_t seed) {
   grad_ = alloc_f32(n_params_);
   stamps_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_) * 4));
   cudaMemset(stamps_, 0, static_cast<size_t>(total_units_) * 4);
-  unit_lists_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_ + 64) * 4));
-  unit_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
+  pair_lists_ = static_cast<int*>(alloc(static_cast<size_t>(pair_capacity_ + 64) * 4));
+  pair_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
   mats_dev_ = static_cast<UnitMatrix*>(alloc(mats_.size() * sizeof(UnitMatrix)));
   cudaMemcpy(mats_dev_, mats_.data(), mats_.size() * sizeof(UnitMatrix), cudaMemcpyHostToDevice);
   // matrices N(0, init_std) (fixed seed per stage); families initialise their dense params
@@ -210,8 +212,8 @@ void Stage::allocate_parameters(uint64_t seed) {
 }
 
 int Stage::build_unit_lists(const uint64_t* frozen_words, cudaStream_t s) {
-  return launch_mask_to_unit_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), unit_lists_,
-                                   unit_counts_, s);
+  return launch_mask_to_pair_lists(frozen_words, mats_dev_, static_cast<int>(mats_.size()), pair_lists_,
+                                   pair_counts_, s);
 }
 
 LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
@@ -267,10 +269,8 @@ LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots,
       L.rstd1 = af32(T);
       L.rstd2 = af32(T);
       L.attn = attn_state_new();
-      if (split_) {
-        L.dy = abf(T * h);
-        L.dx2 = abf(T * h);
-      }
+      L.dy = abf(T * h);
+      L.dx2 = abf(T * h);
     }
     sl.x_out = abf(T * h);
     if (spec.last) {
@@ -280,11 +280,8 @@ LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots,
     }
   }
   d_a_ = abf(T * cfg.ffn);
-  d_gu_ = abf(T * 2 * cfg.ffn);
   d_h_ = abf(T * h);
-  d_x2_ = abf(T * h);
   d_attn_ = abf(T * cfg.attn_dim());
-  d_qkv_ = abf(T * cfg.qkv_dim());
   d_y_ = abf(T * h);
   d_tmp_ = abf(T * h);
   if (cudaDeviceSynchronize() != cudaSuccess) throw std::runtime_error("stage: initialisation kernels failed");
@@ -366,20 +363,12 @@ int LlamaStage::forward(int slot, int microbatch, const int* tokens, const int* 
   return PF_OK;
 }
 
-int Stage::dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                       long long ldx, int K, int stamp, cudaStream_t s) {
+DwGemm Stage::dw_item(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                      long long ldx, int K) const {
   const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
-  GemmOut out{grad_ + w.offset, w.cols, stamps_, m.unit_offset, stamp};
-  // dW[out, in] += dY^T . X over the unfrozen units; both operands MN-major (no transposes)
-  return gemm_bf16_units(GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, out, w.rows, w.cols, K, 1.0f,
-                         unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, s);
-}
-
-UnitGemm Stage::unit_gemm(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                          long long ldx) const {
-  const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
-  return UnitGemm{GemmOperand{dy, ldy, true}, GemmOperand{x, ldx, true}, grad_ + w.offset, w.cols, w.rows, w.cols,
-                  unit_lists_ + m.unit_offset, unit_counts_ + w.unit_matrix, m.units, m.unit_offset};
+  // dW[out, in] (+)= dY^T . X over the unfrozen units; both operands MN-major (no transposes)
+  return DwGemm{dy, ldy, x, ldx, grad_ + w.offset, w.cols, w.rows, w.cols, K,
+                pair_lists_ + m.pair_offset, pair_counts_ + w.unit_matrix, m.unit_offset};
 }
 
 int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_words, const __nv_bfloat16* dy,
@@ -388,15 +377,15 @@ int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_wor
   Slot& sl = slots_[static_cast<std::size_t>(slot)];
   const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
   const int nl = static_cast<int>(layers_.size());
-  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units (W does it when split)
+  // K5p: this microbatch's unit mask -> per-matrix pair lists of unfrozen units (W does it when split)
   if (!split_)
     PF_TRY(build_unit_lists(frozen_words, s));
-  // split: every layer's output gradient lands in its slot buffer, the top one included
-  __nv_bfloat16* top = split_ && nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
+  // every layer's output gradient lands in its slot buffer; the top layer's is the incoming
+  // gradient itself when W runs inside this action (split: copied, the buffer is reused)
+  __nv_bfloat16* top = nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
   const __nv_bfloat16* dcur = dy;
   if (spec_.last) {
     PF_TRY(gemm_dx(sl.logits, cfg_.vocab, weights_ + wlm_.offset, h, d_h_, h, T, h, cfg_.vocab, EPI_STORE_BF16, s));
-    if (!split_) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, T, stamp, s));
     PF_TRY(launch_rmsnorm_bwd(sl.x_out, weights_ + gf_.offset, sl.rstdf, d_h_, nullptr, top, grad_ + gf_.offset, T,
                               h, s));
     dcur = top;
@@ -408,10 +397,11 @@ int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_wor
   for (int li = nl - 1; li >= 0; --li) {
     SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
     const LayerParams& P = layers_[static_cast<std::size_t>(li)];
-    // split: d(gate|up) over gu and dqkv over qkv (both dead after their use here), dx2 kept
-    __nv_bfloat16* dgu = split_ ? L.gu : d_gu_;
-    __nv_bfloat16* dx2 = split_ ? L.dx2 : d_x2_;
-    __nv_bfloat16* dqkv = split_ ? L.qkv : d_qkv_;
+    L.dy_w = dcur;
+    // d(gate|up) over gu and dqkv over qkv (both dead after their use here), dx2 kept for W
+    __nv_bfloat16* dgu = L.gu;
+    __nv_bfloat16* dx2 = L.dx2;
+    __nv_bfloat16* dqkv = L.qkv;
     // MLP
     PF_TRY(gemm_dx_dswiglu(dcur, h, weights_ + P.wd.offset, ffn, L.gu, d_a_, dgu, T, ffn, h, s));
     PF_TRY(gemm_dx(dgu, 2 * ffn, weights_ + P.wgu.offset, h, d_h_, h, T, h, 2 * ffn, EPI_STORE_BF16, s));
@@ -430,50 +420,44 @@ int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_wor
     }
     PF_TRY(gemm_dx(dqkv, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
                    EPI_STORE_BF16, s));
-    // K3: the layer's four masked weight gradients in ONE grouped launch over
-    // their unfrozen units (all four dY buffers are still live here)
-    if (!split_) PF_TRY(layer_weight_grads(L, P, dcur, dgu, dx2, dqkv, stamp, s));
     __nv_bfloat16* out;
-    if (li > 0) out = split_ ? sl.layers[static_cast<std::size_t>(li - 1)].dy : (dcur == d_y_ ? d_tmp_ : d_y_);
+    if (li > 0) out = sl.layers[static_cast<std::size_t>(li - 1)].dy;
     else out = spec_.first ? d_tmp_ : dx_out;
     if (!out) return PF_ERR_INVALID;
     PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, dx2, out, grad_ + P.g1.offset, T, h, s));
-    if (split_) attn_release_keep_out(L.attn);
-    else attn_release(L.attn);
+    attn_release_keep_out(L.attn);
     dcur = out;
   }
   if (spec_.first) PF_TRY(launch_embedding_bwd(tokens, dcur, grad_ + emb_.offset, T, h, s));
   else if (nl == 0 && dx_out && dcur != dx_out)
     PF_CUDA(cudaMemcpyAsync(dx_out, dcur, static_cast<size_t>(T) * h * 2, cudaMemcpyDeviceToDevice, s));
+  // K3: all masked weight gradients of the microbatch in one launch (split: in W)
+  if (!split_) PF_TRY(weight_grads(sl, stamp, s));
   return PF_OK;
 }
 
-int LlamaStage::layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
-                              const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv,
-                              int stamp, cudaStream_t s) {
+int LlamaStage::weight_grads(Slot& sl, int stamp, cudaStream_t s) {
   const int T = cfg_.tokens(), h = cfg_.hidden, ffn = cfg_.ffn;
-  const ParamSlice* w[4] = {&P.wd, &P.wgu, &P.wo, &P.wqkv};
-  const __nv_bfloat16* dys[4] = {dy, dgu, dx2, dqkv};
-  const long long ldys[4] = {h, 2LL * ffn, h, cfg_.qkv_dim()};
-  const __nv_bfloat16* xs[4] = {L.a, L.h2, L.attn_out, L.h1};
-  const long long ldxs[4] = {ffn, h, L.attn_ld, h};
-  UnitGemm items[4];
-  for (int k = 0; k < 4; ++k) items[k] = unit_gemm(*w[k], dys[k], ldys[k], xs[k], ldxs[k]);
-  return gemm_bf16_units_grouped(items, 4, T, 1.0f, stamps_, stamp, s);
+  std::vector<DwGemm> items;
+  items.reserve(4 * layers_.size() + 1);
+  if (spec_.last) items.push_back(dw_item(wlm_, sl.logits, cfg_.vocab, sl.hf, h, T));
+  for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
+    const SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
+    const LayerParams& P = layers_[static_cast<std::size_t>(li)];
+    items.push_back(dw_item(P.wd, L.dy_w, h, L.a, ffn, T));
+    items.push_back(dw_item(P.wgu, L.gu, 2LL * ffn, L.h2, h, T));
+    items.push_back(dw_item(P.wo, L.dx2, h, L.attn_out, L.attn_ld, T));
+    items.push_back(dw_item(P.wqkv, L.qkv, cfg_.qkv_dim(), L.h1, h, T));
+  }
+  PF_TRY(run_dw(items, stamp, s));
+  for (auto& L : sl.layers) attn_release(L.attn);
+  return PF_OK;
 }
 
 int LlamaStage::backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) {
   if (!split_ || slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
-  Slot& sl = slots_[static_cast<std::size_t>(slot)];
-  const int h = cfg_.hidden;
   PF_TRY(build_unit_lists(frozen_words, s));
-  if (spec_.last) PF_TRY(dgemm_units(wlm_, sl.logits, cfg_.vocab, sl.hf, h, cfg_.tokens(), stamp, s));
-  for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
-    SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
-    PF_TRY(layer_weight_grads(L, layers_[static_cast<std::size_t>(li)], L.dy, L.gu, L.dx2, L.qkv, stamp, s));
-    attn_release(L.attn);
-  }
-  return PF_OK;
+  return weight_grads(slots_[static_cast<std::size_t>(slot)], stamp, s);
 }
 
 int Stage::optimizer_step(const OptimCfg& oc, int microbatches, int stamp, bool apf, float apf_alpha,

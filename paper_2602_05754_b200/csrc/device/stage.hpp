@@ -76,9 +76,11 @@ struct SavedLayer {  // per layer per microbatch slot
   AttnState* attn = nullptr;
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
-  // split backward only: the layer's output gradient and post-attention residual
-  // gradient, kept from B to W (dgu and dqkv are written over gu and qkv)
+  // the layer's output gradient and post-attention residual gradient, kept from B to
+  // W (dgu and dqkv are written over gu and qkv); dy_w is the output gradient W reads
+  // (dy, or the stage's incoming gradient buffer when W runs inside the same action)
   __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;
+  const __nv_bfloat16* dy_w = nullptr;
 };
 
 struct Slot {  // one in-flight microbatch
@@ -97,8 +99,9 @@ struct OptimCfg {
 };
 
 // Shared by every model family: the flat parameter buffers (fp32 master, bf16 copy,
-// fp32 gradient), the 128x128 freeze-unit table, the K5 work lists, the masked K3
-// weight-gradient GEMM and the K6 optimizer (with fused K4 APF).
+// fp32 gradient), the 128x128 freeze-unit table, the K5p pair lists, the masked K3
+// weight-gradient GEMM (CTA pair, every matrix of the microbatch in one launch) and
+// the K6 optimizer (with fused K4 APF).
 class Stage {
  public:
   virtual ~Stage();
@@ -159,13 +162,14 @@ class Stage {
   void* alloc(size_t bytes);
   __nv_bfloat16* alloc_bf16(long long elems) { return static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(elems) * 2)); }
   float* alloc_f32(long long elems) { return static_cast<float*>(alloc(static_cast<size_t>(elems) * 4)); }
-  // K5: this microbatch's unit mask -> per-matrix work lists of unfrozen units
+  // K5p: this microbatch's unit mask -> per-matrix pair lists of unfrozen units
   int build_unit_lists(const uint64_t* frozen_words, cudaStream_t s);
-  // K3 for one matrix: G[w] (+)= dY^T . X over the unfrozen units, K = rows of dY / X
-  int dgemm_units(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                  long long ldx, int K, int stamp, cudaStream_t s);
-  UnitGemm unit_gemm(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
-                     long long ldx) const;
+  // K3 work item of one matrix: G[w] (+)= dY^T . X over its unfrozen units, K = rows of dY / X
+  DwGemm dw_item(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
+                 long long ldx, int K) const;
+  int run_dw(const std::vector<DwGemm>& items, int stamp, cudaStream_t s) {
+    return gemm_dw_pairs(items.data(), static_cast<int>(items.size()), stamps_, stamp, s);
+  }
 
   ModelConfig cfg_;
   StageSpec spec_;
@@ -186,8 +190,9 @@ class Stage {
   float* adam_v_ = nullptr;
   int* unit_steps_ = nullptr;
   int dense_steps_ = 0;
-  int* unit_lists_ = nullptr;
-  int* unit_counts_ = nullptr;
+  int* pair_lists_ = nullptr;
+  int* pair_counts_ = nullptr;
+  int pair_capacity_ = 0;
   std::vector<void*> allocations_;
   int last_unfrozen_ = 0;
 };
@@ -209,17 +214,15 @@ class LlamaStage final : public Stage {
   const __nv_bfloat16* output(int slot) const override { return slots_[slot].x_out; }
 
  private:
-  int layer_weight_grads(const SavedLayer& L, const LayerParams& P, const __nv_bfloat16* dy,
-                         const __nv_bfloat16* dgu, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv, int stamp,
-                         cudaStream_t s);
+  // W: every masked weight gradient of the microbatch in `sl` in one K3 launch
+  int weight_grads(Slot& sl, int stamp, cudaStream_t s);
 
   std::vector<LayerParams> layers_;
   ParamSlice emb_, gf_, wlm_;
   float2* rope_ = nullptr;
   std::vector<Slot> slots_;
   // backward workspace
-  __nv_bfloat16 *d_a_ = nullptr, *d_gu_ = nullptr, *d_h_ = nullptr, *d_x2_ = nullptr, *d_attn_ = nullptr,
-                *d_qkv_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr;
+  __nv_bfloat16 *d_a_ = nullptr, *d_h_ = nullptr, *d_attn_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr;
 };
 
 // The stage of `cfg.family` (0 LLaMA decoder, 1 ViT encoder).

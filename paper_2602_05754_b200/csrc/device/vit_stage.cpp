@@ -44,7 +44,8 @@ struct VitSavedLayer {
   AttnState* attn = nullptr;
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
-  __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;  // split backward: kept from B to W
+  __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;  // kept from B to W
+  const __nv_bfloat16* dy_w = nullptr;          // the output gradient W reads (dy or the incoming buffer)
 };
 
 struct VitSlot {
@@ -143,10 +144,8 @@ class VitStage final : public Stage {
         L.mu2 = alloc_f32(T);
         L.r2 = alloc_f32(T);
         L.attn = attn_state_new();
-        if (split_) {
-          L.dy = alloc_bf16(T * h);
-          L.dx2 = alloc_bf16(T * h);
-        }
+        L.dy = alloc_bf16(T * h);
+        L.dx2 = alloc_bf16(T * h);
       }
       sl.x_out = alloc_bf16(T * h);
       if (spec.first) {
@@ -163,14 +162,10 @@ class VitStage final : public Stage {
       }
     }
     d_act_ = alloc_bf16(T * cfg.ffn);
-    d_pre_ = alloc_bf16(T * cfg.ffn);
     d_h_ = alloc_bf16(T * h);
-    d_x2_ = alloc_bf16(T * h);
     d_attn_ = alloc_bf16(T * h);
-    d_qkv_ = alloc_bf16(T * 3 * h);
     d_y_ = alloc_bf16(T * h);
     d_tmp_ = alloc_bf16(T * h);
-    if (spec.first) d_emb_ = alloc_bf16(static_cast<long long>(B_) * np_ * h);
     if (spec.last) {
       d_hc_ = alloc_bf16(static_cast<long long>(Mh_) * h);
       d_xc_ = alloc_bf16(static_cast<long long>(Mh_) * h);
@@ -240,11 +235,10 @@ class VitStage final : public Stage {
     const int h = cfg_.hidden, ffn = cfg_.ffn;
     const int nl = static_cast<int>(layers_.size());
     if (!split_) PF_TRY(build_unit_lists(frozen_words, s));
-    __nv_bfloat16* top = split_ && nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
+    __nv_bfloat16* top = nl > 0 ? sl.layers[static_cast<std::size_t>(nl - 1)].dy : d_y_;
     const __nv_bfloat16* dcur = dy;
     if (spec_.last) {
       PF_TRY(launch_bias_grad(sl.logits, cfg_.vocab, g(headb_), B_, cfg_.vocab, s));
-      if (!split_) PF_TRY(dgemm_units(head_, sl.logits, cfg_.vocab, sl.hc, h, B_, stamp, s));
       PF_TRY(gemm_dx(sl.logits, cfg_.vocab, w(head_), h, d_hc_, h, Mh_, h, cfg_.vocab, EPI_STORE_BF16, s));
       PF_TRY(launch_layernorm_bwd(sl.xc, w(lnfg_), sl.muc, sl.rc, d_hc_, nullptr, d_xc_, g(lnfg_), g(lnfb_), B_, h,
                                   s));
@@ -259,9 +253,10 @@ class VitStage final : public Stage {
     for (int li = nl - 1; li >= 0; --li) {
       VitSavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
       const VitLayerParams& P = layers_[static_cast<std::size_t>(li)];
-      __nv_bfloat16* dpre = split_ ? L.pre : d_pre_;  // pre is dead once GELU' is applied
-      __nv_bfloat16* dx2 = split_ ? L.dx2 : d_x2_;
-      __nv_bfloat16* dqkv = split_ ? L.qkv : d_qkv_;  // qkv is dead after the attention backward
+      L.dy_w = dcur;
+      __nv_bfloat16* dpre = L.pre;  // pre is dead once GELU' is applied
+      __nv_bfloat16* dx2 = L.dx2;
+      __nv_bfloat16* dqkv = L.qkv;  // qkv is dead after the attention backward
       // MLP
       PF_TRY(launch_bias_grad(dcur, h, g(P.b2), T_, h, s));
       PF_TRY(gemm_dx(dcur, h, w(P.w2), ffn, d_act_, ffn, T_, ffn, h, EPI_STORE_BF16, s));
@@ -282,53 +277,53 @@ class VitStage final : public Stage {
       }
       PF_TRY(launch_bias_grad(dqkv, 3LL * h, g(P.bqkv), T_, 3 * h, s));
       PF_TRY(gemm_dx(dqkv, 3LL * h, w(P.wqkv), h, d_h_, h, T_, h, 3 * h, EPI_STORE_BF16, s));
-      if (!split_) PF_TRY(layer_weight_grads(L, P, dcur, dpre, dx2, dqkv, stamp, s));
       __nv_bfloat16* out;
-      if (li > 0) out = split_ ? sl.layers[static_cast<std::size_t>(li - 1)].dy : (dcur == d_y_ ? d_tmp_ : d_y_);
+      if (li > 0) out = sl.layers[static_cast<std::size_t>(li - 1)].dy;
       else out = spec_.first ? d_tmp_ : dx_out;
       if (!out) return PF_ERR_INVALID;
       PF_TRY(launch_layernorm_bwd(L.x, w(P.ln1g), L.mu1, L.r1, d_h_, dx2, out, g(P.ln1g), g(P.ln1b), T_, h, s));
-      if (split_) attn_release_keep_out(L.attn);
-      else attn_release(L.attn);
+      attn_release_keep_out(L.attn);
       dcur = out;
     }
     if (spec_.first) {
-      __nv_bfloat16* demb = split_ ? sl.emb : d_emb_;  // patch embeddings are dead after the forward
-      PF_TRY(launch_vit_embed_bwd(dcur, demb, g(pos_), g(cls_), g(patch_b_), B_, S_, h, s));
-      if (!split_) PF_TRY(dgemm_units(patch_w_, demb, h, sl.patches, cfg_.patch_dim(), B_ * np_, stamp, s));
+      // patch embeddings are dead after the forward: their gradient overwrites them
+      PF_TRY(launch_vit_embed_bwd(dcur, sl.emb, g(pos_), g(cls_), g(patch_b_), B_, S_, h, s));
     } else if (nl == 0 && dx_out && dcur != dx_out) {
       PF_CUDA(cudaMemcpyAsync(dx_out, dcur, static_cast<size_t>(T_) * h * 2, cudaMemcpyDeviceToDevice, s));
     }
+    // K3: all masked weight gradients of the microbatch in one launch (split: in W)
+    if (!split_) PF_TRY(weight_grads(sl, stamp, s));
     return PF_OK;
   }
 
   int backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) override {
     if (!split_ || slot < 0 || slot >= static_cast<int>(slots_.size()) || !frozen_words) return PF_ERR_INVALID;
-    VitSlot& sl = slots_[static_cast<std::size_t>(slot)];
     PF_TRY(build_unit_lists(frozen_words, s));
-    if (spec_.last) PF_TRY(dgemm_units(head_, sl.logits, cfg_.vocab, sl.hc, cfg_.hidden, B_, stamp, s));
-    for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
-      VitSavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
-      PF_TRY(layer_weight_grads(L, layers_[static_cast<std::size_t>(li)], L.dy, L.pre, L.dx2, L.qkv, stamp, s));
-      attn_release(L.attn);
-    }
-    if (spec_.first)
-      PF_TRY(dgemm_units(patch_w_, sl.emb, cfg_.hidden, sl.patches, cfg_.patch_dim(), B_ * np_, stamp, s));
-    return PF_OK;
+    return weight_grads(slots_[static_cast<std::size_t>(slot)], stamp, s);
   }
 
  private:
   const __nv_bfloat16* w(const ParamSlice& p) const { return weights_ + p.offset; }
   float* g(const ParamSlice& p) const { return grad_ + p.offset; }
 
-  // K3: the layer's four masked weight gradients in one grouped launch
-  int layer_weight_grads(const VitSavedLayer& L, const VitLayerParams& P, const __nv_bfloat16* dy,
-                         const __nv_bfloat16* dpre, const __nv_bfloat16* dx2, const __nv_bfloat16* dqkv, int stamp,
-                         cudaStream_t s) {
+  // W: every masked weight gradient of the microbatch in `sl` in one K3 launch
+  int weight_grads(VitSlot& sl, int stamp, cudaStream_t s) {
     const int h = cfg_.hidden, ffn = cfg_.ffn;
-    UnitGemm items[4] = {unit_gemm(P.w2, dy, h, L.act, ffn), unit_gemm(P.w1, dpre, ffn, L.h2, h),
-                         unit_gemm(P.wo, dx2, h, L.attn_out, L.attn_ld), unit_gemm(P.wqkv, dqkv, 3LL * h, L.h1, h)};
-    return gemm_bf16_units_grouped(items, 4, T_, 1.0f, stamps_, stamp, s);
+    std::vector<DwGemm> items;
+    items.reserve(4 * layers_.size() + 2);
+    if (spec_.last) items.push_back(dw_item(head_, sl.logits, cfg_.vocab, sl.hc, h, B_));
+    for (int li = static_cast<int>(layers_.size()) - 1; li >= 0; --li) {
+      const VitSavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
+      const VitLayerParams& P = layers_[static_cast<std::size_t>(li)];
+      items.push_back(dw_item(P.w2, L.dy_w, h, L.act, ffn, T_));
+      items.push_back(dw_item(P.w1, L.pre, ffn, L.h2, h, T_));
+      items.push_back(dw_item(P.wo, L.dx2, h, L.attn_out, L.attn_ld, T_));
+      items.push_back(dw_item(P.wqkv, L.qkv, 3LL * h, L.h1, h, T_));
+    }
+    if (spec_.first) items.push_back(dw_item(patch_w_, sl.emb, h, sl.patches, cfg_.patch_dim(), B_ * np_));
+    PF_TRY(run_dw(items, stamp, s));
+    for (auto& L : sl.layers) attn_release(L.attn);
+    return PF_OK;
   }
 
   uint64_t seed_;
@@ -337,8 +332,8 @@ class VitStage final : public Stage {
   ParamSlice patch_w_, patch_b_, cls_, pos_, head_, headb_, lnfg_, lnfb_;
   float2* ident_ = nullptr;
   std::vector<VitSlot> slots_;
-  __nv_bfloat16 *d_act_ = nullptr, *d_pre_ = nullptr, *d_h_ = nullptr, *d_x2_ = nullptr, *d_attn_ = nullptr,
-                *d_qkv_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr, *d_emb_ = nullptr, *d_hc_ = nullptr,
+  __nv_bfloat16 *d_act_ = nullptr, *d_h_ = nullptr, *d_attn_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr,
+                *d_hc_ = nullptr,
                 *d_xc_ = nullptr;
 };
 

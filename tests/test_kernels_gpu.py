@@ -194,19 +194,41 @@ def test_apf_update_vs_reference_golden(cuda):
         np.testing.assert_allclose(sc.cpu().numpy(), ref_s, rtol=1e-4, atol=1e-6)
 
 
+def _pair_band(tiles_m, tiles_n):
+    """Rows of units per K5p band (kernels.cuh pair_band_rows)."""
+    band = 32
+    while -(-tiles_m // band) * tiles_n > 2048:
+        band *= 2
+    return band
+
+
 def _unit_table(shapes):
     """pf_unit_matrix table for matrices laid out back to back (64-element aligned)."""
     dt = np.dtype([("elem_offset", "<i8"), ("rows", "<i4"), ("cols", "<i4"), ("unit_offset", "<i4"),
-                   ("tiles_n", "<i4"), ("units", "<i4"), ("pad", "<i4")])
+                   ("tiles_n", "<i4"), ("units", "<i4"), ("pair_offset", "<i4")])
     tab = np.zeros(len(shapes), dtype=dt)
-    off = u = 0
+    off = u = po = 0
     for i, (r, c) in enumerate(shapes):
         tn = (c + 127) // 128
-        units = ((r + 127) // 128) * tn
-        tab[i] = (off, r, c, u, tn, units, 0)
+        tm = (r + 127) // 128
+        units = tm * tn
+        tab[i] = (off, r, c, u, tn, units, po)
         off = (off + r * c + 63) // 64 * 64
         u += units
+        po += units + -(-tm // _pair_band(tm, tn)) * tn
     return tab, off, u
+
+
+def pair_list_ref(frozen, tiles_m, tiles_n):
+    """K5p restated: (band, column) groups band by band, unfrozen local unit ids top to bottom,
+    each group padded to an even count with -1."""
+    band = _pair_band(tiles_m, tiles_n)
+    out = []
+    for b0 in range(0, tiles_m, band):
+        for nb in range(tiles_n):
+            grp = [mb * tiles_n + nb for mb in range(b0, min(tiles_m, b0 + band)) if not frozen[mb * tiles_n + nb]]
+            out += grp + ([-1] if len(grp) % 2 else [])
+    return out
 
 
 def test_mask_to_unit_lists_matches_numpy(cuda):
@@ -230,6 +252,34 @@ def test_mask_to_unit_lists_matches_numpy(cuda):
         expect = [j for j in range(n) if not frozen[lo + j]]
         assert counts[i].item() == len(expect)
         assert L[lo:lo + len(expect)].tolist() == expect
+
+
+@pytest.mark.parametrize("ratio", [0.0, 0.55, 0.8, 1.0])
+def test_mask_to_pair_lists_matches_numpy(cuda, ratio):
+    """K5p: banded, column-grouped, even-padded pair lists; a 1002-row matrix spans 32 bands
+    (the LM head shape) and a 64-column one exercises many groups per band."""
+    import torch
+
+    from paper_2602_05754_b200 import pipefreeze as pf
+
+    tab, _, U = _unit_table([(384, 256), (256, 640), (1000, 128), (128, 128), (128256, 256), (2048, 8192)])
+    words = pf.sample_masks(7, U, [ratio])[0]
+    w = np.concatenate([words, np.zeros(1, dtype=np.uint64)])
+    wd = torch.tensor(w.view(np.int64), device=cuda)
+    td = torch.tensor(tab.view(np.uint8), device=cuda)
+    cap = int(tab["pair_offset"][-1]) + int(tab["units"][-1]) * 2 + 64
+    pairs = torch.full((cap,), -7, dtype=torch.int32, device=cuda)
+    counts = torch.zeros(len(tab), dtype=torch.int32, device=cuda)
+    chk(lib().pf_mask_to_pair_lists(wd.data_ptr(), td.data_ptr(), len(tab), pairs.data_ptr(), counts.data_ptr(),
+                                    sp()))
+    torch.cuda.synchronize()
+    frozen = pf.unpack_mask(words, U)
+    P = pairs.cpu().numpy()
+    for i, ent in enumerate(tab):
+        lo, n, tn, po = int(ent["unit_offset"]), int(ent["units"]), int(ent["tiles_n"]), int(ent["pair_offset"])
+        expect = pair_list_ref(frozen[lo:lo + n], n // tn, tn)
+        assert counts[i].item() == len(expect) and len(expect) % 2 == 0
+        assert P[po:po + len(expect)].tolist() == expect
 
 
 def test_masked_sgd_units_and_fused_apf(cuda):
