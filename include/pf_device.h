@@ -47,7 +47,7 @@ int pf_gemm_dw_units(const void* A, int a_mn_major, long long lda, const void* B
 /* K3 on a CTA pair (tcgen05.mma.cta_group::2, M = 256 from two units, N = 128): the same
  * masked, unit-stamped G[M,N] (+)= dY^T . X, with dY stored [K][ldy] (logical A [M,K],
  * MN-major) and X stored [K][ldx] (logical B [N,K], MN-major), over the padded pair list
- * pairs[0..*pair_count) that pf_mask_to_pair_lists writes for this matrix. */
+ * pairs[0..*pair_count) that pf_mask_to_pair_lists writes for this matrix (8-byte aligned). */
 int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
                      int N, int K, const int* pairs, const int* pair_count, int* unit_stamp, int stamp_offset,
                      int stamp, void* stream);
@@ -78,7 +78,7 @@ typedef struct pf_unit_matrix {
   int unit_offset;       /* first unit id of the matrix within the stage */
   int tiles_n;           /* ceil(cols / 128) */
   int units;             /* ceil(rows/128) * tiles_n */
-  int pair_offset;       /* first entry of the matrix's K5p pair list: units + pair groups slots */
+  int pair_offset;       /* first entry (even) of the matrix's K5p pair list: units + pair groups slots */
 } pf_unit_matrix;
 
 /* K5: frozen-unit bitmask (sample_mask bit order, one bit per 128x128 unit, +1

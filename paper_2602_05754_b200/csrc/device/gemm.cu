@@ -61,44 +61,54 @@ struct alignas(64) Problem {
   const int* count;  // list mode: device-resident count
   int stamp_offset;  // first global unit id of this matrix (EPI_ACC_F32)
   int num_tiles;     // plain mode
+  int num_kb;        // k-blocks of this problem (list mode: K differs per matrix)
 };
 
+// MAXP = 1 for one plain GEMM; kMaxDwProblems for the batched masked dW (list mode), whose
+// parameter block holds every matrix of a microbatch (<= 32 KB of kernel parameters).
+template <int MAXP>
 struct GemmParams {
-  Problem prob[kMaxGemmProblems];
+  Problem prob[MAXP];
   int nprob;
-  int K;
   float alpha;
   int list_mode;
   int* unit_stamp;  // EPI_ACC_F32 first-touch stamps
   int stamp;
 };
 
-struct TileMap {
-  int prefix[kMaxGemmProblems + 1];
-  int total;
-};
-
-__device__ __forceinline__ TileMap tile_map(const GemmParams& p) {
-  TileMap m;
-  m.prefix[0] = 0;
-  for (int i = 0; i < kMaxGemmProblems; ++i) {
-    const int n = i < p.nprob ? (p.list_mode ? *p.prob[i].count : p.prob[i].num_tiles) : 0;
-    m.prefix[i + 1] = m.prefix[i] + n;
+// prefix[i] = first tile of problem i (shared memory, filled once per CTA)
+template <int MAXP>
+__device__ __forceinline__ int find_prob(const int* prefix, int nprob, int t) {
+  if constexpr (MAXP == 1) {
+    return 0;
+  } else {
+    int lo = 0, hi = nprob - 1;
+    while (lo < hi) {  // last problem with prefix <= t
+      const int mid = (lo + hi + 1) >> 1;
+      if (prefix[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
   }
-  m.total = m.prefix[kMaxGemmProblems];
-  return m;
 }
 
-__device__ __forceinline__ void decode_tile(const GemmParams& p, const TileMap& tm, int t, int& pi, int& mb,
-                                            int& nb) {
-  pi = 0;
-  while (pi + 1 < p.nprob && t >= tm.prefix[pi + 1]) ++pi;
+// unit entry of tile t (list mode) or -1 (plain mode / past the end)
+template <int MAXP>
+__device__ __forceinline__ int tile_unit(const GemmParams<MAXP>& p, const int* prefix, int total, int t) {
+  if (!p.list_mode || t >= total) return -1;
+  const int pi = find_prob<MAXP>(prefix, p.nprob, t);
+  return __ldg(p.prob[pi].list + (t - prefix[pi]));
+}
+
+template <int MAXP>
+__device__ __forceinline__ void decode_tile(const GemmParams<MAXP>& p, const int* prefix, int t, int unit, int& pi,
+                                            int& mb, int& nb) {
+  pi = find_prob<MAXP>(prefix, p.nprob, t);
   const Problem& pr = p.prob[pi];
-  const int lt = t - tm.prefix[pi];
+  const int lt = t - prefix[pi];
   if (p.list_mode) {
-    const int u = pr.list[lt];
-    mb = u / pr.tiles_n;
-    nb = u - mb * pr.tiles_n;
+    mb = unit / pr.tiles_n;
+    nb = unit - mb * pr.tiles_n;
     return;
   }
   const int group_size = GROUP_M * pr.tiles_n;
@@ -110,8 +120,8 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, const TileMap& 
   nb = local / gm;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams p) {
+template <int BN, bool A_MN, bool B_MN, int EPI, int MAXP>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_constant__ GemmParams<MAXP> p) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
@@ -130,9 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
 
-  const TileMap tm = tile_map(p);
-  const int ntiles = tm.total;
-  const int num_kb = (p.K + BK - 1) / BK;
+  __shared__ int prefix[MAXP + 1];
+  if (threadIdx.x < p.nprob)
+    prefix[threadIdx.x + 1] = p.list_mode ? __ldcg(p.prob[threadIdx.x].count) : p.prob[threadIdx.x].num_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -153,21 +163,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
     tmem_relinquish();
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    prefix[0] = 0;
+    for (int i = 0; i < p.nprob; ++i) prefix[i + 1] += prefix[i];
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int ntiles = prefix[p.nprob];
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
       int stage = 0;
       uint32_t phase = 0;
+      // list mode: the next tile's unit id is loaded one tile ahead, off the TMA issue path
+      int nxt = tile_unit(p, prefix, ntiles, blockIdx.x);
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int pi, mb, nb;
-        decode_tile(p, tm, t, pi, mb, nb);
+        decode_tile(p, prefix, t, nxt, pi, mb, nb);
+        nxt = tile_unit(p, prefix, ntiles, t + gridDim.x);
         const CUtensorMap* ta = &p.prob[pi].ta;
         const CUtensorMap* tb = &p.prob[pi].tb;
+        const int num_kb = p.prob[pi].num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
@@ -202,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
       int abuf = 0;
       uint32_t aphase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int num_kb = p.prob[find_prob<MAXP>(prefix, p.nprob, t)].num_kb;
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int pi, mb, nb;
-      decode_tile(p, tm, t, pi, mb, nb);
+      decode_tile(p, prefix, t, tile_unit(p, prefix, ntiles, t), pi, mb, nb);
       const Problem& pr = p.prob[pi];
       bool first_touch = false;
       int unit = 0;
@@ -377,10 +398,10 @@ int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols,
   return r == CUDA_SUCCESS ? PF_OK : PF_ERR_INVALID;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
-int launch(const GemmParams& p, int grid_limit, cudaStream_t stream) {
+template <int BN, bool A_MN, bool B_MN, int EPI, int MAXP = 1>
+int launch(const GemmParams<MAXP>& p, int grid_limit, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = gemm_tcgen05_kernel<BN, A_MN, B_MN, EPI, MAXP>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
@@ -395,7 +416,7 @@ int launch(const GemmParams& p, int grid_limit, cudaStream_t stream) {
 }
 
 template <int BN>
-int dispatch(bool a_mn, bool b_mn, const GemmParams& p, int epi, int grid_limit, cudaStream_t s) {
+int dispatch(bool a_mn, bool b_mn, const GemmParams<1>& p, int epi, int grid_limit, cudaStream_t s) {
   const int key = (a_mn ? 1 : 0) | (b_mn ? 2 : 0);
 #define PF_GEMM_CASE(AM, BMN, E) \
   if (key == ((AM) | ((BMN) << 1)) && epi == (E)) return launch<BN, (AM) != 0, (BMN) != 0, (E)>(p, grid_limit, s);
@@ -424,6 +445,7 @@ int fill_problem(Problem& pr, const GemmOperand& A, const GemmOperand& B, int M,
   pr.tiles_m = (M + BM - 1) / BM;
   pr.tiles_n = (N + block_n - 1) / block_n;
   pr.num_tiles = pr.tiles_m * pr.tiles_n;
+  pr.num_kb = (K + BK - 1) / BK;
   return PF_OK;
 }
 
@@ -450,9 +472,8 @@ int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int 
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
   if (block_n != 128 && block_n != 256) return PF_ERR_INVALID;
   if (epi == EPI_ACC_F32 && (C.unit_stamp == nullptr || block_n != 128)) return PF_ERR_INVALID;
-  GemmParams p{};
+  GemmParams<1> p{};
   p.nprob = 1;
-  p.K = K;
   p.alpha = alpha;
   p.list_mode = 0;
   p.unit_stamp = C.unit_stamp;
@@ -466,38 +487,46 @@ int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int 
                         : dispatch<128>(A.mn_major, B.mn_major, p, epi, pr.num_tiles, stream);
 }
 
-int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
-                            cudaStream_t stream) {
-  if (n <= 0 || n > kMaxGemmProblems || K <= 0 || (K % 8) != 0 || unit_stamp == nullptr) return PF_ERR_INVALID;
-  GemmParams p{};
-  p.nprob = n;
-  p.K = K;
-  p.alpha = alpha;
-  p.list_mode = 1;
-  p.unit_stamp = unit_stamp;
-  p.stamp = stamp;
-  int max_units = 0;
-  const bool a_mn = items[0].A.mn_major, b_mn = items[0].B.mn_major;
-  for (int i = 0; i < n; ++i) {
-    const UnitGemm& it = items[i];
-    if (it.A.mn_major != a_mn || it.B.mn_major != b_mn || !it.unit_list || !it.unit_count) return PF_ERR_INVALID;
-    Problem& pr = p.prob[i];
-    if (int rc = fill_problem(pr, it.A, it.B, it.M, it.N, K, 128)) return rc;
-    pr.C = it.C;
-    pr.ldc = it.ldc;
-    pr.list = it.unit_list;
-    pr.count = it.unit_count;
-    pr.stamp_offset = it.stamp_offset;
-    max_units += it.max_units;
+int gemm_dw_units(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream) {
+  if (n < 0 || unit_stamp == nullptr) return PF_ERR_INVALID;
+  for (int base = 0; base < n; base += kMaxDwProblems) {
+    const int cnt = std::min(kMaxDwProblems, n - base);
+    GemmParams<kMaxDwProblems> p{};
+    p.nprob = cnt;
+    p.alpha = 1.0f;
+    p.list_mode = 1;
+    p.unit_stamp = unit_stamp;
+    p.stamp = stamp;
+    long long max_units = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const DwGemm& it = items[base + i];
+      if (it.M <= 0 || it.N <= 0 || it.K <= 0 || (it.K % 8) != 0 || !it.list || !it.count || !it.C)
+        return PF_ERR_INVALID;
+      Problem& pr = p.prob[i];
+      if (int rc = fill_problem(pr, GemmOperand{it.dy, it.ldy, true}, GemmOperand{it.x, it.ldx, true}, it.M, it.N,
+                                it.K, 128))
+        return rc;
+      pr.C = it.C;
+      pr.ldc = it.ldc;
+      pr.list = it.list;
+      pr.count = it.count;
+      pr.stamp_offset = it.stamp_offset;
+      max_units += pr.num_tiles;
+    }
+    if (int rc = launch<128, true, true, EPI_ACC_F32, kMaxDwProblems>(
+            p, static_cast<int>(std::min<long long>(max_units, num_sms())), stream))
+      return rc;
   }
-  return dispatch<128>(a_mn, b_mn, p, EPI_ACC_F32, max_units, stream);
+  return PF_OK;
 }
 
 int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,
                     const int* unit_list, const int* unit_count, int max_units, cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return PF_ERR_INVALID;
-  UnitGemm it{A, B, C.ptr, C.ld, M, N, unit_list, unit_count, max_units, C.stamp_offset};
-  return gemm_bf16_units_grouped(&it, 1, K, alpha, C.unit_stamp, C.stamp, stream);
+  (void)max_units;
+  if (M <= 0 || N <= 0 || !A.mn_major || !B.mn_major || alpha != 1.0f) return PF_ERR_INVALID;
+  DwGemm it{A.ptr, A.ld, B.ptr, B.ld, static_cast<float*>(C.ptr), C.ld, M, N, K, unit_list, unit_count,
+            C.stamp_offset};
+  return gemm_dw_units(&it, 1, C.unit_stamp, C.stamp, stream);
 }
 
 }  // namespace pf

@@ -139,12 +139,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
+      // the next item's pair entries are loaded one item ahead, off the TMA issue path
+      auto load_pair = [&](int t) -> int2 {
+        if (t >= total) return make_int2(0, 0);
+        const int pi = find_problem(tab.prefix, p.nprob, t);
+        const int li = t - tab.prefix[pi];
+        return __ldg(reinterpret_cast<const int2*>(p.prob[pi].pairs) + li);
+      };
+      int2 nxt = load_pair(cluster);
       for (int t = cluster; t < total; t += nclusters) {
         const int pi = find_problem(tab.prefix, p.nprob, t);
         const DwProblem& pr = p.prob[pi];
-        const int li = t - tab.prefix[pi];
-        const int u0 = __ldg(pr.pairs + 2 * li);
-        const int u1 = __ldg(pr.pairs + 2 * li + 1);
+        const int u0 = nxt.x, u1 = nxt.y;
+        nxt = load_pair(t + nclusters);
         const int mine = (rank == 0 || u1 < 0) ? u0 : u1;
         const int mb = mine / pr.tiles_n;
         const int nb = u0 - (u0 / pr.tiles_n) * pr.tiles_n;
@@ -322,15 +329,15 @@ int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaSt
     long long max_pairs = 0;
     for (int i = 0; i < cnt; ++i) {
       const DwGemm& it = items[base + i];
-      if (it.M <= 0 || it.N <= 0 || it.K <= 0 || (it.K % 8) != 0 || !it.pairs || !it.pair_count || !it.C)
+      if (it.M <= 0 || it.N <= 0 || it.K <= 0 || (it.K % 8) != 0 || !it.list || !it.count || !it.C)
         return PF_ERR_INVALID;
       DwProblem& pr = p.prob[i];
       if (int rc = tma_desc_bf16_2d(&pr.ta, it.dy, it.K, it.M, it.ldy, 64, 64)) return rc;
       if (int rc = tma_desc_bf16_2d(&pr.tb, it.x, it.K, it.N, it.ldx, 64, 64)) return rc;
       pr.C = it.C;
       pr.ldc = it.ldc;
-      pr.pairs = it.pairs;
-      pr.count = it.pair_count;
+      pr.pairs = it.list;
+      pr.count = it.count;
       pr.M = it.M;
       pr.N = it.N;
       pr.K = it.K;

@@ -15,7 +15,7 @@ struct UnitMatrix {
   int unit_offset;        // first unit id of this matrix in the stage
   int tiles_n;            // ceil(cols / 128)
   int units;              // tiles_m * tiles_n
-  int pair_offset;        // first entry of this matrix's padded pair list (K5p): units + pair_groups slots
+  int pair_offset;        // first entry (even) of this matrix's padded pair list (K5p): units + pair_groups slots
 };
 
 constexpr int kMaxUnitMatrices = 512;

@@ -39,30 +39,14 @@ struct GemmOut {
 int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,
               float alpha, int epi, int block_n, cudaStream_t stream);
 
-// Masked weight-gradient GEMM over a device-resident list of 128x128 units.
+// Masked weight-gradient GEMM over a device-resident list of 128x128 units
+// (dY and X MN-major, alpha = 1; one matrix of gemm_dw_units).
 int gemm_bf16_units(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N,
                     int K, float alpha, const int* unit_list, const int* unit_count,
                     int max_units, cudaStream_t stream);
 
-// Grouped masked dW: up to kMaxGemmProblems weight matrices (same K = tokens,
-// same operand majorness) in one persistent launch over their unit lists.
-constexpr int kMaxGemmProblems = 4;
-struct UnitGemm {
-  GemmOperand A;  // dY  (logical [M = out, K = T])
-  GemmOperand B;  // X   (logical [N = in,  K = T])
-  void* C;        // fp32 gradient of the matrix
-  long long ldc;
-  int M, N;
-  const int* unit_list;
-  const int* unit_count;
-  int max_units;
-  int stamp_offset;
-};
-int gemm_bf16_units_grouped(const UnitGemm* items, int n, int K, float alpha, int* unit_stamp, int stamp,
-                            cudaStream_t stream);
-
-// K3 on a CTA pair (gemm_dw.cu): one matrix's masked dW over its padded pair list
-// (K5p output: unfrozen units column-major, each column padded to an even count with -1).
+// K3, batched: the masked dW of many matrices (every matrix of a microbatch) in one
+// persistent launch. One work item per matrix: G (+)= dY^T . X over its unfrozen units.
 constexpr int kMaxDwProblems = 96;  // matrices per launch (kernel parameter space <= 32 KB)
 struct DwGemm {
   const void* dy;    // bf16 [K][M]: output-feature gradient (MN-major A)
@@ -72,10 +56,13 @@ struct DwGemm {
   float* C;          // fp32 gradient of the matrix [M][N]
   long long ldc;
   int M, N, K;
-  const int* pairs;       // device pair list of this matrix
-  const int* pair_count;  // device: padded entry count
-  int stamp_offset;       // first unit id of the matrix in the stage
+  const int* list;   // device work list of this matrix (K5 unit list / K5p pair list)
+  const int* count;  // device: entry count
+  int stamp_offset;  // first unit id of the matrix in the stage
 };
+// 1-CTA 128 x 128 tiles over K5 unit lists (gemm.cu) -- the default
+int gemm_dw_units(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
+// CTA-pair 256 x 128 tiles over K5p pair lists (gemm_dw.cu; PF_DW_PAIR=1)
 int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
 
 // K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.

@@ -162,13 +162,15 @@ class Stage {
   void* alloc(size_t bytes);
   __nv_bfloat16* alloc_bf16(long long elems) { return static_cast<__nv_bfloat16*>(alloc(static_cast<size_t>(elems) * 2)); }
   float* alloc_f32(long long elems) { return static_cast<float*>(alloc(static_cast<size_t>(elems) * 4)); }
-  // K5p: this microbatch's unit mask -> per-matrix pair lists of unfrozen units
+  // K5 (K5p with the CTA-pair dW): this microbatch's unit mask -> per-matrix work lists
   int build_unit_lists(const uint64_t* frozen_words, cudaStream_t s);
   // K3 work item of one matrix: G[w] (+)= dY^T . X over its unfrozen units, K = rows of dY / X
   DwGemm dw_item(const ParamSlice& w, const __nv_bfloat16* dy, long long ldy, const __nv_bfloat16* x,
                  long long ldx, int K) const;
+  // K3 over every item in one launch
   int run_dw(const std::vector<DwGemm>& items, int stamp, cudaStream_t s) {
-    return gemm_dw_pairs(items.data(), static_cast<int>(items.size()), stamps_, stamp, s);
+    return dw_pair_ ? gemm_dw_pairs(items.data(), static_cast<int>(items.size()), stamps_, stamp, s)
+                    : gemm_dw_units(items.data(), static_cast<int>(items.size()), stamps_, stamp, s);
   }
 
   ModelConfig cfg_;
@@ -190,8 +192,11 @@ class Stage {
   float* adam_v_ = nullptr;
   int* unit_steps_ = nullptr;
   int dense_steps_ = 0;
-  int* pair_lists_ = nullptr;
-  int* pair_counts_ = nullptr;
+  // K3 variant: 1-CTA 128 x 128 units over K5 lists (default), or CTA-pair 256 x 128 over
+  // K5p pair lists (PF_DW_PAIR=1; measured slower on B200, profiles/r1_dw_bench.txt)
+  bool dw_pair_ = false;
+  int* unit_lists_ = nullptr;  // K5 (row-major) or K5p (pair) lists
+  int* unit_counts_ = nullptr;
   int pair_capacity_ = 0;
   std::vector<void*> allocations_;
   int last_unfrozen_ = 0;

@@ -216,6 +216,7 @@ def _unit_table(shapes):
         off = (off + r * c + 63) // 64 * 64
         u += units
         po += units + -(-tm // _pair_band(tm, tn)) * tn
+        po += po & 1
     return tab, off, u
 
 
