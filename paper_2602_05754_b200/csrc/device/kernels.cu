@@ -400,6 +400,171 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16
   }
 }
 
+// Row-in-registers RMSNorm for h = 256 * CH (the LLaMA widths): one warp per row, lane
+// holds columns lane*8 + 256 j (16-byte loads), so x is read from HBM exactly once.
+template <int CH>
+__global__ void __launch_bounds__(kBlock) rmsnorm_fwd_reg_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                 const __nv_bfloat16* __restrict__ g,
+                                                                 __nv_bfloat16* __restrict__ y,
+                                                                 float* __restrict__ rstd, int T, float eps) {
+  constexpr int H = 256 * CH;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nw) {
+    const __nv_bfloat16* xr = x + static_cast<long long>(t) * H + lane * 8;
+    uint4 xv[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + 256 * j));
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&xv[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(b[i]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+    }
+    ss = warp_sum(ss);
+    const float r = rsqrtf(ss / H + eps);
+    if (lane == 0) rstd[t] = r;
+    __nv_bfloat16* yr = y + static_cast<long long>(t) * H + lane * 8;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      float f[8], gg[8];
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&xv[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 v = __bfloat1622float2(b[i]);
+        f[2 * i] = v.x;
+        f[2 * i + 1] = v.y;
+      }
+      load8(g + lane * 8 + 256 * j, gg);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = f[i] * r * gg[i];
+      store8(yr + 256 * j, f);
+    }
+  }
+}
+
+// Fused RMSNorm backward for h = 256 * CH: dx = residual + rstd * g * dy - rstd^3 * x * mean(g * dy * x)
+// and dg[c] += sum_t dy[t,c] * x[t,c] * rstd[t] in ONE pass over x and dy (was two kernels).
+// One warp per row; rows are held in registers (CH <= 8). A warp's dg partial lives in
+// registers (CH <= 4) or in its shared-memory slice; the block's slices are summed and
+// added to dg with one float4 atomic per 4 columns (148 blocks: ~77k vector atomics).
+template <int CH>
+__host__ __device__ constexpr int norm_bwd_threads() { return 256; }
+
+template <int CH>
+__global__ void __launch_bounds__(norm_bwd_threads<CH>(), 1) rmsnorm_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ residual, __nv_bfloat16* __restrict__ dx,
+    float* __restrict__ dg, int T) {
+  constexpr int H = 256 * CH;
+  constexpr int NT = norm_bwd_threads<CH>();
+  constexpr int NW = NT / 32;
+  constexpr bool ACC_REG = CH <= 4;  // dg partial in registers (else in the warp's smem slice)
+  constexpr bool HOLD = CH <= 8;     // x and dy kept in registers between the two passes (else re-read)
+  extern __shared__ float slices[];  // [NW][H]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* mine = slices + warp * H + lane * 8;
+  float acc[ACC_REG ? CH * 8 : 1];
+  if constexpr (ACC_REG) {
+#pragma unroll
+    for (int i = 0; i < CH * 8; ++i) acc[i] = 0.f;
+  } else {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      reinterpret_cast<float4*>(mine + 256 * j)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(mine + 256 * j)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {
+    const long long off = static_cast<long long>(t) * H + lane * 8;
+    uint4 xv[HOLD ? CH : 1], dv[HOLD ? CH : 1];
+    if constexpr (HOLD) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j) xv[j] = __ldcs(reinterpret_cast<const uint4*>(x + off + 256 * j));
+    }
+    const float r = rstd[t];
+    float dot = 0.f;
+#pragma unroll(HOLD ? CH : 4)
+    for (int j = 0; j < CH; ++j) {
+      float gv[8];
+      load8(g + lane * 8 + 256 * j, gv);
+      uint4 xj;
+      if constexpr (HOLD) xj = xv[j];
+      else xj = *reinterpret_cast<const uint4*>(x + off + 256 * j);
+      const uint4 dj = *reinterpret_cast<const uint4*>(dy + off + 256 * j);
+      if constexpr (HOLD) dv[j] = dj;
+      const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&xj);
+      const __nv_bfloat162* db = reinterpret_cast<const __nv_bfloat162*>(&dj);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 xf = __bfloat1622float2(xb[i]), df = __bfloat1622float2(db[i]);
+        dot += gv[2 * i] * df.x * xf.x + gv[2 * i + 1] * df.y * xf.y;
+      }
+    }
+    dot = warp_sum(dot);
+    const float k = dot * r * r * r / H;
+#pragma unroll(HOLD ? CH : 4)
+    for (int j = 0; j < CH; ++j) {
+      float gv[8], out[8];
+      load8(g + lane * 8 + 256 * j, gv);
+      if (residual) load8(residual + off + 256 * j, out);
+      uint4 xj, dj;
+      if constexpr (HOLD) {
+        xj = xv[j];
+        dj = dv[j];
+      } else {
+        xj = __ldcs(reinterpret_cast<const uint4*>(x + off + 256 * j));
+        dj = __ldcs(reinterpret_cast<const uint4*>(dy + off + 256 * j));
+      }
+      const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&xj);
+      const __nv_bfloat162* db = reinterpret_cast<const __nv_bfloat162*>(&dj);
+      float c[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 xf = __bfloat1622float2(xb[i]), df = __bfloat1622float2(db[i]);
+        out[2 * i] = (residual ? out[2 * i] : 0.f) + r * gv[2 * i] * df.x - k * xf.x;
+        out[2 * i + 1] = (residual ? out[2 * i + 1] : 0.f) + r * gv[2 * i + 1] * df.y - k * xf.y;
+        c[2 * i] = df.x * xf.x * r;
+        c[2 * i + 1] = df.y * xf.y * r;
+      }
+      store8(dx + off + 256 * j, out);
+      if constexpr (ACC_REG) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[8 * j + i] += c[i];
+      } else {
+        float4* m4 = reinterpret_cast<float4*>(mine + 256 * j);
+        const float4 a = m4[0], b = m4[1];
+        m4[0] = make_float4(a.x + c[0], a.y + c[1], a.z + c[2], a.w + c[3]);
+        m4[1] = make_float4(b.x + c[4], b.y + c[5], b.z + c[6], b.w + c[7]);
+      }
+    }
+  }
+  if (dg == nullptr) return;
+  if constexpr (ACC_REG) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      reinterpret_cast<float4*>(mine + 256 * j)[0] = make_float4(acc[8 * j], acc[8 * j + 1], acc[8 * j + 2], acc[8 * j + 3]);
+      reinterpret_cast<float4*>(mine + 256 * j)[1] =
+          make_float4(acc[8 * j + 4], acc[8 * j + 5], acc[8 * j + 6], acc[8 * j + 7]);
+    }
+  }
+  __syncthreads();
+  // block partial (slices summed in warp order) -> dg with one vector atomic per 4 columns
+  for (int c = threadIdx.x * 4; c < H; c += NT * 4) {
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float4 v = *reinterpret_cast<const float4*>(slices + w * H + c);
+      sum = make_float4(sum.x + v.x, sum.y + v.y, sum.z + v.z, sum.w + v.w);
+    }
+    atomicAdd(reinterpret_cast<float4*>(dg + c), sum);
+  }
+}
+
 // rotate-half RoPE on the q and k heads of the packed qkv activation, in place.
 // grid.y = token; each thread rotates 8 consecutive pairs (16-byte loads).
 __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int seq, int nh,
@@ -698,13 +863,53 @@ int launch_embedding_bwd(const int* tok, const __nv_bfloat16* dout, float* g, in
 int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, float* rstd, int T, int h,
                        float eps, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  rmsnorm_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, y, rstd, T, h, eps);
+  const int grid = grid_for((T + 7) / 8);
+  switch (h) {
+    case 256: rmsnorm_fwd_reg_kernel<1><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 512: rmsnorm_fwd_reg_kernel<2><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 1024: rmsnorm_fwd_reg_kernel<4><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 2048: rmsnorm_fwd_reg_kernel<8><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 4096: rmsnorm_fwd_reg_kernel<16><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 5120: rmsnorm_fwd_reg_kernel<20><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    default: break;
+  }
+  rmsnorm_fwd_kernel<<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, h, eps);
   return status();
 }
+
+namespace {
+template <int CH>
+int launch_rmsnorm_bwd_fused(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd,
+                             const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
+                             int T, cudaStream_t s) {
+  constexpr int H = 256 * CH;
+  constexpr int NT = norm_bwd_threads<CH>();
+  constexpr int smem = (NT / 32) * H * 4;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(rmsnorm_bwd_fused_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return PF_ERR_CUDA;
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(num_sms(), (T + NT / 32 - 1) / (NT / 32)));
+  rmsnorm_bwd_fused_kernel<CH><<<grid, NT, smem, s>>>(x, g, rstd, dy, residual, dx, dg, T);
+  return status();
+}
+}  // namespace
 
 int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
                        const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
+  switch (h) {
+    case 256: return launch_rmsnorm_bwd_fused<1>(x, g, rstd, dy, residual, dx, dg, T, s);
+    case 512: return launch_rmsnorm_bwd_fused<2>(x, g, rstd, dy, residual, dx, dg, T, s);
+    case 1024: return launch_rmsnorm_bwd_fused<4>(x, g, rstd, dy, residual, dx, dg, T, s);
+    case 2048: return launch_rmsnorm_bwd_fused<8>(x, g, rstd, dy, residual, dx, dg, T, s);
+    case 4096: return launch_rmsnorm_bwd_fused<16>(x, g, rstd, dy, residual, dx, dg, T, s);
+    case 5120: return launch_rmsnorm_bwd_fused<20>(x, g, rstd, dy, residual, dx, dg, T, s);
+    default: break;
+  }
   rmsnorm_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, rstd, dy, residual, dx, T, h);
   int rc = status();
   if (rc != PF_OK || dg == nullptr) return rc;
@@ -749,7 +954,7 @@ int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfl
 
 int launch_cross_entropy(__nv_bfloat16* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
                          float loss_scale, cudaStream_t s) {
-  if (V % 8) return PF_ERR_INVALID;
+  if (V % 8 || T <= 0) return PF_ERR_INVALID;
   cross_entropy_kernel<<<T, kBlock, 0, s>>>(logits, targets, loss_sum, V, grad_scale, loss_scale);
   return status();
 }

@@ -33,10 +33,12 @@ def bf(x):
     return x.to(torch.bfloat16)
 
 
-def test_rmsnorm_fwd_bwd(cuda):
+@pytest.mark.parametrize("T,h", [(256, 1024), (512, 2048), (136, 256), (200, 4096), (72, 5120), (64, 768)])
+def test_rmsnorm_fwd_bwd(cuda, T, h):
+    """Register-row forward and the fused backward (dx + dg in one pass, deterministic dg) for the
+    LLaMA widths; h = 768 takes the generic kernels."""
     import torch
 
-    T, h = 256, 1024
     g = torch.Generator().manual_seed(1)
     x = bf(torch.randn(T, h, generator=g)).cuda()
     w = bf(1 + 0.1 * torch.randn(h, generator=g)).cuda()
@@ -59,6 +61,15 @@ def test_rmsnorm_fwd_bwd(cuda):
     exp = xf.grad + res.float()
     assert (dx.float() - exp).abs().max().item() < 2e-2 * exp.abs().max().item()
     assert torch.allclose(dg, wf.grad, rtol=1e-3, atol=1e-3 * wf.grad.abs().max().item())
+    # dg accumulates into its buffer; dx does not depend on residual being absent
+    dg2 = torch.zeros(h, device=cuda)
+    dx2 = torch.empty_like(x)
+    for _ in range(2):
+        chk(lib().pf_rmsnorm_bwd(x.data_ptr(), w.data_ptr(), rstd.data_ptr(), dy.data_ptr(), None, dx2.data_ptr(),
+                                 dg2.data_ptr(), T, h, sp()))
+    torch.cuda.synchronize()
+    assert torch.allclose(dg2, 2 * dg, rtol=1e-5, atol=1e-5 * dg.abs().max().item())
+    assert torch.allclose(dx2.float(), xf.grad, rtol=2e-2, atol=2e-2 * xf.grad.abs().max().item())
 
 
 def test_swiglu_fwd_bwd(cuda):
@@ -151,7 +162,7 @@ def test_rope_matches_reference(cuda):
     assert (qkv.float().view_as(ref) - ref).abs().max().item() < 2e-2
 
 
-@pytest.mark.parametrize("V", [4096, 1024, 1000, 128256])
+@pytest.mark.parametrize("V", [4096, 1024, 1000, 128256, 32000, 8, 65544])
 def test_cross_entropy_fused(cuda, V):
     import torch
     import torch.nn.functional as F

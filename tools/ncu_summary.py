@@ -20,13 +20,18 @@ def short(name: str) -> str:
     if m:
         bn, bmn, epi = m.groups()
         return f"gemm_tcgen05_pair<256x{bn},{'dX K2' if bmn in ('true', '1') else 'fwd K1'},epi={epi}>"
-    m = re.search(r"gemm_tcgen05_kernel<(\d+), (\d), (\d), (\d)>", name)
+    m = re.search(r"gemm_tcgen05_kernel<(\d+), (\d), (\d), (\d)(?:, (\d+))?>", name)
     if m:
-        bn, amn, bmn, epi = m.groups()
+        bn, amn, bmn, epi, maxp = m.groups()
+        if maxp and maxp != "1":
+            return f"gemm_tcgen05<BN={bn},dW K3 (masked units, all matrices of a microbatch)>"
         role = {("0", "0"): "fwd K1", ("0", "1"): "dX K2", ("1", "1"): "dW K3 (masked units)"}.get((amn, bmn), "gemm")
         return f"gemm_tcgen05<BN={bn},{role},epi={epi}>"
     name = re.sub(r"\(.*", "", name)
-    name = re.sub(r"<.*>", "<>", name)
+    name = re.sub(r"^void ", "", name)
+    name = re.sub(r"<(\d+(?:, \d+)*)>$", r"<\1>", name)  # keep numeric template args (tile / row widths)
+    if not re.search(r"<\d+(?:, \d+)*>$", name):
+        name = re.sub(r"<.*>", "<>", name)
     return name.replace("void ", "").replace("pf::(anonymous namespace)::", "").replace("pf::<unnamed>::", "")
 
 
