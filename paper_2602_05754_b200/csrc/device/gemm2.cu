@@ -337,6 +337,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (abuf == 0) aphase ^= 1;
         continue;
       }
+      // EPI_ADD_BF16: the residual does not depend on the accumulator, so chunk c's 32 columns
+      // are fetched while the MMAs (chunk `half`) or the previous chunk's math (c > half) run.
+      uint4 rpre[4];
+      auto fetch_r = [&](int c) {
+        if constexpr (EPI == EPI_ADD_BF16) {
+          const int gcol = tn * BN + c * 32;
+          if (!row_ok || gcol + 32 > p.N) return;
+          const uint4* r4 = reinterpret_cast<const uint4*>(p.R + grow * p.ldr + gcol);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rpre[j] = __ldcs(r4 + j);
+        }
+      };
+      if (EPI == EPI_ADD_BF16 && !park) fetch_r(half);
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
       if constexpr (EPI == EPI_SWIGLU) {
@@ -386,6 +399,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(abuf * BN + c * 32),
                            r);
+        const uint4 rcur[4] = {rpre[0], rpre[1], rpre[2], rpre[3]};
+        if (EPI == EPI_ADD_BF16 && !park && c + 2 < BN / 32) fetch_r(c + 2);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -437,14 +452,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const __nv_bfloat16* rp = p.R + grow * p.ldr + gcol;
           if (full) {
             uint4* c4 = reinterpret_cast<uint4*>(cp);
-            const uint4* r4 = reinterpret_cast<const uint4*>(rp);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               float w[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) w[i] = v[j * 8 + i];
               if constexpr (EPI == EPI_ADD_BF16) {
-                const uint4 old = r4[j];
+                const uint4 old = rcur[j];
                 const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {

@@ -207,9 +207,16 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// 1 / (1 + e^-x) with the MUFU exp and an IEEE-rounded reciprocal (no division subroutine);
-// shared by the SwiGLU kernels and the fused GEMM epilogues so they agree bit for bit.
-__device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.f + __expf(-x)); }
+// 1 / (1 + e^-x) with the MUFU exp and the MUFU reciprocal (rcp.approx: one instruction; the
+// IEEE-rounded __frcp_rn is a multi-instruction subroutine that made the fused SwiGLU GEMM
+// epilogue the bottleneck, profiles/r1_swiglu_epilogue.md). Shared by the SwiGLU kernels and
+// the fused GEMM epilogues so they agree bit for bit. x -> -inf: 1 + e^-x = inf, rcp = 0.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return rcp_approx(1.f + __expf(-x)); }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

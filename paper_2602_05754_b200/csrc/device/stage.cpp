@@ -41,16 +41,20 @@ bool use_pair() {
   return on;
 }
 
-// SwiGLU forward/backward in the CTA-pair GEMM epilogues only with PF_FUSE_SWIGLU=1: measured
-// on B200 (tools/swiglu_bench.py) the per-row epilogue loads of gu stall on latency and the
-// fused backward is slower than GEMM + the HBM-roofline swiglu_bwd kernel.
-bool fuse_swiglu() {
-  static const bool on = [] {
+// SwiGLU forward/backward in the CTA-pair GEMM epilogues. PF_FUSE_SWIGLU=1 forces both on, 0
+// both off; by default (tools/swiglu_bench.py on B200, profiles/r1_swiglu_epilogue.md) the
+// backward is fused (0.148 -> 0.145 ms at LLaMA-1B, 0.451 -> 0.417 ms at LLaMA-8B shapes) and
+// the forward only when K >= 4096: at K = 2048 a tile's mainloop is too short to hide the
+// activation epilogue (0.222 ms GEMM + kernel vs 0.231 ms fused; 8B: 0.709 vs 0.689 ms).
+int fuse_swiglu_mode() {
+  static const int mode = [] {
     const char* e = std::getenv("PF_FUSE_SWIGLU");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  return mode;
 }
+bool fuse_swiglu_fwd(int K) { return fuse_swiglu_mode() == 1 || (fuse_swiglu_mode() < 0 && K >= 4096); }
+bool fuse_swiglu_bwd() { return fuse_swiglu_mode() != 0; }
 
 int gemm_any(const GemmOperand& A, const GemmOperand& B, void* C, long long ldc, int M, int N, int K, int epi,
              cudaStream_t s) {
@@ -84,7 +88,7 @@ int gemm_fwd_resid(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W
 // CTA-pair kernel the activation is computed in the GEMM epilogue from the same tile.
 int gemm_fwd_swiglu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* gu,
                     __nv_bfloat16* a, int M, int ffn, int K, cudaStream_t s) {
-  if (use_pair() && fuse_swiglu() && M >= 256 && (2 * ffn) % 256 == 0) {
+  if (use_pair() && fuse_swiglu_fwd(K) && M >= 256 && (2 * ffn) % 256 == 0) {
     GemmOut out{gu, 2LL * ffn};
     out.aux = a;
     out.ldaux = ffn;
@@ -133,7 +137,7 @@ int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long
 int gemm_dx_dswiglu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* Wd, long long ldw,
                     const __nv_bfloat16* gu, __nv_bfloat16* d_act, __nv_bfloat16* dgu, int M, int ffn, int K,
                     cudaStream_t s) {
-  if (use_pair() && fuse_swiglu() && M >= 256 && ffn >= 256) {
+  if (use_pair() && fuse_swiglu_bwd() && M >= 256 && ffn >= 256) {
     GemmOut out{dgu, 2LL * ffn};
     out.residual = gu;
     out.ldr = 2LL * ffn;
@@ -346,13 +350,18 @@ int LlamaStage::forward(int slot, int microbatch, const int* tokens, const int* 
     PF_TRY(gemm_fwd_resid(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, L.x, h, T, h,
                           cfg_.attn_dim(), s));
     PF_TRY(launch_rmsnorm_fwd(L.x2, weights_ + P.g2.offset, L.h2, L.rstd2, T, h, cfg_.norm_eps, s));
-    if (probe_kind() == PROBE_GATE_UP_GEMM) {  // bench.py roofline: this launch alone (unfused path)
+    // bench.py roofline probe: brackets the gate|up GEMM launch alone (with its fused SwiGLU
+    // epilogue when that path is taken, else without the separate activation kernel)
+    const bool probe = probe_kind() == PROBE_GATE_UP_GEMM;
+    if (probe && !(use_pair() && fuse_swiglu_fwd(h))) {
       probe_begin(s);
       PF_TRY(gemm_fwd(L.h2, h, weights_ + P.wgu.offset, h, L.gu, 2 * cfg_.ffn, T, 2 * cfg_.ffn, h, EPI_STORE_BF16, s));
       probe_end(s);
       PF_TRY(launch_swiglu_fwd(L.gu, L.a, T, cfg_.ffn, s));
     } else {
+      if (probe) probe_begin(s);
       PF_TRY(gemm_fwd_swiglu(L.h2, h, weights_ + P.wgu.offset, h, L.gu, L.a, T, cfg_.ffn, h, s));
+      if (probe) probe_end(s);
     }
     __nv_bfloat16* next = li + 1 < nl ? sl.layers[static_cast<std::size_t>(li + 1)].x : sl.x_out;
     PF_TRY(gemm_fwd_resid(L.a, cfg_.ffn, weights_ + P.wd.offset, cfg_.ffn, next, L.x2, h, T, h, cfg_.ffn, s));
