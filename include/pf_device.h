@@ -64,7 +64,9 @@ int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw,
 int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw, const void* gu, void* dgu, int T,
                     int ffn, int K, void* stream);
 
-/* Stream-K split of the CTA-pair GEMM: -1 auto, 0 off (default), 1 force. */
+/* Stream-K split of the CTA-pair GEMM: 0 off (default), 1 split every tile, 2 data-parallel
+ * full waves + the last wave split over all CTA pairs, -1 auto (mode 2 when the last wave would
+ * leave > 8% of the CTA pairs idle). */
 int pf_gemm_set_streamk(int mode);
 
 int pf_device_sm_count(void);

@@ -73,7 +73,7 @@ int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw
 }
 
 int pf_gemm_set_streamk(int mode) {
-  if (mode < -1 || mode > 1) return PF_ERR_INVALID;
+  if (mode < -1 || mode > 2) return PF_ERR_INVALID;
   pf::gemm_set_streamk(mode);
   return PF_OK;
 }

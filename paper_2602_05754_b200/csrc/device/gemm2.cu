@@ -15,11 +15,16 @@
 // leader's tmem-empty barrier through shared::cluster addresses).
 //
 // Stream-K: when the tile count leaves the last wave of clusters mostly idle
-// (the N = hidden GEMMs of a LLaMA layer: 128 tiles on 74 clusters), the
-// tile x k-block iteration space is split evenly over the clusters. A tile is
-// then cut at most once: the cluster whose range STARTS inside it computes the
-// tail first and parks the fp32 partial in a workspace; the cluster whose range
-// ENDS inside it computes the head last, adds the parked partial and writes C.
+// (the N = hidden GEMMs of a LLaMA layer: 128 tiles on 74 clusters), the full
+// waves run data-parallel (one whole tile per work item) and only the tiles of
+// the last, partial wave are split: their tile x k-block iterations are divided
+// evenly over ALL clusters (mode 2, "DP + stream-K tail"; mode 1 splits every
+// tile that way). A cluster whose range STARTS inside a tile computes that
+// piece first and parks the fp32 partial in its workspace slot; the cluster
+// whose range holds the tile's first k-block computes the head last, waits for
+// the parked pieces of every later cluster that covers the tile, adds them and
+// writes C. Only a cluster's first piece can start mid-tile, so one slot per
+// cluster suffices.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -67,7 +72,9 @@ struct alignas(64) Params2 {
   __nv_bfloat16* aux;  // EPI_SWIGLU activation output
   long long ldaux;
   const __nv_bfloat16* bias;  // EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (nullptr: none)
-  int streamk;   // 0: one tile per work item; 1: even split of tile x k-block iterations
+  int streamk;   // 0: one tile per work item; 1/2: stream-K (2: data-parallel full waves first)
+  int dp_tiles;  // stream-K: tiles [0, dp_tiles) run whole, round-robin over the clusters
+  long long sk_q;  // stream-K: iterations of the split region per cluster
   float* ws;     // stream-K partials: [cluster][rank][128][BN] fp32
   int* flags;    // stream-K: [cluster][rank] == epoch once the partial is parked
   int epoch;
@@ -92,21 +99,29 @@ __device__ __forceinline__ bool next_seg(const Params2& p, int cluster, int nclu
     it.t += nclusters;
     return true;
   }
-  if (it.next >= it.end) return false;
-  s.tile = static_cast<int>(it.next / num_kb);
-  s.kb0 = static_cast<int>(it.next - static_cast<long long>(s.tile) * num_kb);
-  s.kb1 = static_cast<int>(std::min<long long>(num_kb, s.kb0 + (it.end - it.next)));
-  it.next += s.kb1 - s.kb0;
+  // split pieces first (a head's parked pieces are the FIRST pieces of the next clusters, so
+  // they are ready when it needs them, and its fixup epilogue overlaps a whole tile's MMAs),
+  // then the data-parallel tiles
+  if (it.next < it.end) {
+    s.tile = static_cast<int>(it.next / num_kb);
+    s.kb0 = static_cast<int>(it.next - static_cast<long long>(s.tile) * num_kb);
+    s.kb1 = static_cast<int>(std::min<long long>(num_kb, s.kb0 + (it.end - it.next)));
+    it.next += s.kb1 - s.kb0;
+    return true;
+  }
+  if (it.t >= p.dp_tiles) return false;
+  s = Seg{it.t, 0, num_kb};
+  it.t += nclusters;
   return true;
 }
 
 __device__ __forceinline__ SegIter seg_begin(const Params2& p, int cluster, int nclusters, int num_kb) {
   SegIter it{0, 0, cluster};
   if (p.streamk) {
+    const long long base = static_cast<long long>(p.dp_tiles) * num_kb;
     const long long total = static_cast<long long>(p.tiles_m) * p.tiles_n * num_kb;
-    const long long q = (total + nclusters - 1) / nclusters;
-    it.next = std::min<long long>(total, static_cast<long long>(cluster) * q);
-    it.end = std::min<long long>(total, it.next + q);
+    it.next = std::min<long long>(total, base + static_cast<long long>(cluster) * p.sk_q);
+    it.end = std::min<long long>(total, it.next + p.sk_q);
   }
   return it;
 }
@@ -262,20 +277,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
       int tm, tn;
       decode(p, sg.tile, tm, tn);
-      // stream-K roles: a tail (kb0 > 0) parks its partial in this cluster's slot; a head
-      // (kb1 < num_kb) adds the partial parked by the next cluster, whose range starts
-      // with this tile's tail, then writes C.
+      // stream-K roles: a piece that starts mid-tile (kb0 > 0) parks its partial in this
+      // cluster's slot; a head (kb1 < num_kb) adds the pieces parked by clusters
+      // cluster+1 .. last_slot (the owner of the tile's last k-block), then writes C.
       const bool park = sg.kb0 > 0;
       const bool fixup = sg.kb0 == 0 && sg.kb1 < num_kb;
-      const int slot = park ? cluster : cluster + 1;
-      float* ws_rows = p.streamk ? p.ws + (static_cast<long long>(slot) * 2 + rank) * 128 * BN : nullptr;
+      int last_slot = cluster;
       if (fixup) {
+        const long long last_it = static_cast<long long>(sg.tile) * num_kb + num_kb - 1 -
+                                  static_cast<long long>(p.dp_tiles) * num_kb;
+        last_slot = static_cast<int>(last_it / p.sk_q);
         if (threadIdx.x == 64) {
-          const int* f = p.flags + slot * 2 + rank;
-          while (ld_acquire(f) != p.epoch) __nanosleep(64);
+          for (int sl = cluster + 1; sl <= last_slot; ++sl) {
+            const int* f = p.flags + sl * 2 + rank;
+            while (ld_acquire(f) != p.epoch) __nanosleep(64);
+          }
         }
         named_bar_sync(1, kEpiThreads);
       }
+      auto ws_of = [&](int sl) { return p.ws + (static_cast<long long>(sl) * 2 + rank) * 128 * BN; };
       const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
       const bool row_ok = grow < p.M;
       if constexpr (EPI == EPI_DSWIGLU) {
@@ -292,8 +312,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint4* u4 = reinterpret_cast<const uint4*>(p.R + gc + 128);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            gb[j] = __ldcs(g4 + j);
-            ub[j] = __ldcs(u4 + j);
+            gb[j] = ldg_nc_l2_256(g4 + j);
+            ub[j] = ldg_nc_l2_256(u4 + j);
           }
         };
         fetch(half);
@@ -406,20 +426,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if (park) {  // raw fp32 partial, row-major within the slot
-          float4* w = reinterpret_cast<float4*>(ws_rows + static_cast<long long>(row) * BN + c * 32);
+          float4* w = reinterpret_cast<float4*>(ws_of(cluster) + static_cast<long long>(row) * BN + c * 32);
 #pragma unroll
           for (int j = 0; j < 8; ++j) w[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           continue;
         }
         if (fixup) {
-          const float4* w = reinterpret_cast<const float4*>(ws_rows + static_cast<long long>(row) * BN + c * 32);
+          for (int sl = cluster + 1; sl <= last_slot; ++sl) {
+            const float4* w = reinterpret_cast<const float4*>(ws_of(sl) + static_cast<long long>(row) * BN + c * 32);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 o = __ldcg(w + j);
-            v[4 * j] += o.x;
-            v[4 * j + 1] += o.y;
-            v[4 * j + 2] += o.z;
-            v[4 * j + 3] += o.w;
+            for (int j = 0; j < 8; ++j) {
+              const float4 o = __ldcg(w + j);
+              v[4 * j] += o.x;
+              v[4 * j + 1] += o.y;
+              v[4 * j + 2] += o.z;
+              v[4 * j + 3] += o.w;
+            }
           }
         }
         const int gcol = tn * BN + c * 32;
@@ -497,7 +519,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (threadIdx.x == 64) {
           __threadfence();
-          st_release(p.flags + slot * 2 + rank, p.epoch);
+          st_release(p.flags + cluster * 2 + rank, p.epoch);
         }
       }
       abuf ^= 1;
@@ -553,7 +575,9 @@ int launch2(Params2 p, int clusters, cudaStream_t stream) {
       return PF_ERR_CUDA;
     attr_set = true;
   }
-  clusters = std::min(clusters, max_active_clusters<BN, B_MN, EPI>());
+  const int active = max_active_clusters<BN, B_MN, EPI>();
+  if (p.streamk && clusters > active) return PF_ERR_INVALID;  // ranges were cut for `clusters`
+  clusters = std::min(clusters, active);
   if (clusters <= 0) return PF_OK;
   kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
   count_launch();
@@ -574,11 +598,13 @@ StreamKState& sk_state() {
 }
 
 int& streamk_mode_ref() {
-  // Default off: measured on B200 (profiles/r1_gemm_bench_streamk.txt) the split tiles'
-  // fixup waits and lost L2 locality cost more than the idle last wave they recover.
+  // 0 off (default), 1 every tile split, 2 data-parallel full waves + split last wave, -1 auto
+  // (mode 2 where the last wave would leave > 8% of the CTA pairs idle). Both split forms
+  // measured slower than whole tiles on B200 for every LLaMA shape, including the 1.73-wave
+  // N = 2048 GEMMs they target (profiles/r1_gemm_bench_streamk.txt).
   static int mode = [] {
     const char* e = std::getenv("PF_GEMM_STREAMK");
-    return e ? std::atoi(e) : 0;  // -1 auto, 0 off, 1 force
+    return e ? std::atoi(e) : 0;
   }();
   return mode;
 }
@@ -640,12 +666,15 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   const int waves = (ntiles + max_clusters - 1) / max_clusters;
   const double eff = static_cast<double>(ntiles) / (static_cast<double>(waves) * max_clusters);
   const int mode = streamk_mode();
-  // Clusters at different k offsets share little L2; keep stream-K to operands that fit in L2.
-  const bool fits_l2 = (static_cast<long long>(M) + N) * K * 2 <= (48LL << 20);
-  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && ntiles > max_clusters && num_kb >= 8 && (mode == 1 || (mode < 0 && eff < 0.92 && fits_l2));
+  const int active = std::min(max_clusters, max_active_clusters<BN, false, EPI_STORE_BF16>());
+  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && ntiles > active && num_kb >= 8 &&
+                  (mode == 1 || mode == 2 || (mode < 0 && eff < 0.92));
   if (sk) {
     StreamKState& st = sk_state();
-    clusters = max_clusters;
+    clusters = active;
+    p.dp_tiles = mode == 1 ? 0 : (ntiles / clusters) * clusters;
+    const long long split = static_cast<long long>(ntiles - p.dp_tiles) * num_kb;
+    p.sk_q = (split + clusters - 1) / clusters;
     if (st.slots < clusters + 1) {
       if (st.ws) cudaFree(st.ws);
       if (st.flags) cudaFree(st.flags);
@@ -655,7 +684,7 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
       cudaMemset(st.flags, 0, static_cast<size_t>(clusters + 1) * 2 * sizeof(int));
       st.slots = clusters + 1;
     }
-    p.streamk = 1;
+    p.streamk = mode == 1 ? 1 : 2;
     p.ws = st.ws;
     p.flags = st.flags;
     p.epoch = ++st.epoch;

@@ -218,6 +218,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 __device__ __forceinline__ float sigmoid_fast(float x) { return rcp_approx(1.f + __expf(-x)); }
 
+// 16-byte global load through the non-coherent path with a 256-byte L2 fetch: the row-per-thread
+// epilogue reads 64 contiguous bytes per row as 4 such loads, so the first brings the whole
+// line into L1 / L2 and the next three hit. Only for data this kernel does not write before
+// reading it.
+__device__ __forceinline__ uint4 ldg_nc_l2_256(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

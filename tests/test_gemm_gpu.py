@@ -176,13 +176,16 @@ def test_gemm_cta_pair(cuda, b_mn, epi, M, N, K):
     assert (C.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-2
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("b_mn", [0, 1])
 @pytest.mark.parametrize("epi", [0, 1, 3])
-@pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512)])
-def test_gemm_cta_pair_stream_k(cuda, b_mn, epi, M, N, K):
-    """Forced stream-K (split tiles, parked fp32 partials) on tile counts just above the 74 clusters."""
+@pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512), (4096, 2048, 8192)])
+def test_gemm_cta_pair_stream_k(cuda, mode, b_mn, epi, M, N, K):
+    """Forced stream-K on tile counts just above the 74 clusters: mode 1 splits every tile, mode 2
+    runs the full waves data-parallel and splits the last wave's tiles over all clusters (a tile
+    then spans up to three clusters: its head adds every parked piece)."""
     lib, nat = _lib()
-    nat.check(lib.pf_gemm_set_streamk(1), "pf_gemm_set_streamk")
+    nat.check(lib.pf_gemm_set_streamk(mode), "pf_gemm_set_streamk")
     try:
         _stream_k_case(cuda, b_mn, epi, M, N, K)
     finally:
