@@ -85,12 +85,23 @@ const char* pf_device_last_error(void) { return g_last_error.c_str(); }
 }  // extern "C"
 
 #include <atomic>
+#include <cstdlib>
 
 namespace pf {
 namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Off by default: on one B200 (bench.py, alternating runs) PDL moved the stable-freeze step by
+// +0.3..0.6% (noise level) and slowed the no-freeze step by 3%; back-to-back small kernels gain
+// (rmsnorm_fwd 8.2 -> 5.5 us per launch, tools/gap_bench.py). PF_PDL=1 turns it on.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 }  // namespace pf
 

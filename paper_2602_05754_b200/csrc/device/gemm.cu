@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <mutex>
 
+#include "kernel_util.cuh"
 #include "ptx.cuh"
 #include "pf_device_internal.hpp"
 
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
   const uint32_t lane = threadIdx.x & 31;
 
   __shared__ int prefix[MAXP + 1];
+  pdl_wait();  // the unit counts (and operands) come from the preceding kernels
   if (threadIdx.x < p.nprob)
     prefix[threadIdx.x + 1] = p.list_mode ? __ldcg(p.prob[threadIdx.x].count) : p.prob[threadIdx.x].num_tiles;
 
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
           }
         }
       }
+      pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -410,7 +413,7 @@ int launch(const GemmParams<MAXP>& p, int grid_limit, cudaStream_t stream) {
   }
   const int grid = std::min(grid_limit, num_sms());
   if (grid <= 0) return PF_OK;
-  kern<<<grid, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
+  launch_k(kern, dim3(grid), dim3(kThreads), Cfg::SMEM_BYTES, stream, p);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
 }

@@ -33,6 +33,7 @@
 #include <cstdlib>
 
 #include "pf_device_internal.hpp"
+#include "kernel_util.cuh"
 #include "ptx.cuh"
 
 namespace pf {
@@ -194,6 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();  // barrier inits and TMEM allocation visible to both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // setup above overlapped the preceding kernel; operands are its outputs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -226,6 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -579,7 +582,7 @@ int launch2(Params2 p, int clusters, cudaStream_t stream) {
   if (p.streamk && clusters > active) return PF_ERR_INVALID;  // ranges were cut for `clusters`
   clusters = std::min(clusters, active);
   if (clusters <= 0) return PF_OK;
-  kern<<<2 * clusters, kThreads, Cfg::SMEM_BYTES, stream>>>(p);
+  launch_k(kern, dim3(2 * clusters), dim3(kThreads), Cfg::SMEM_BYTES, stream, p);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;
 }

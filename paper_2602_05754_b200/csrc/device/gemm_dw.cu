@@ -31,6 +31,7 @@
 
 #include "kernels.cuh"
 #include "pf_device_internal.hpp"
+#include "kernel_util.cuh"
 #include "ptx.cuh"
 
 namespace pf {
@@ -106,6 +107,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
 
+  pdl_wait();  // the pair counts and operands come from the preceding kernels
   // pair counts of every problem -> prefix table (identical in both CTAs)
   if (threadIdx.x < p.nprob) tab.prefix[threadIdx.x + 1] = __ldcg(p.prob[threadIdx.x].count) >> 1;
   if (threadIdx.x == 0) {
@@ -170,6 +172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
       }
+      pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -348,7 +351,7 @@ int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaSt
     }
     const int clusters = static_cast<int>(std::min<long long>(max_pairs, max_dw_clusters()));
     if (clusters <= 0) continue;
-    gemm_dw_pair_kernel<<<2 * clusters, kThreads, SMEM_BYTES, stream>>>(p);
+    launch_k(gemm_dw_pair_kernel, dim3(2 * clusters), dim3(kThreads), SMEM_BYTES, stream, p);
     count_launch();
     if (cudaPeekAtLastError() != cudaSuccess) return PF_ERR_CUDA;
   }

@@ -19,6 +19,24 @@ inline int grid_for(long long work_items, int per_sm = 8) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+// Kernel launch with the PDL attribute (see pdl_enabled); arguments convert to the kernel's
+// parameter types as with <<<>>>.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline int status() {
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? PF_OK : PF_ERR_CUDA;

@@ -35,6 +35,7 @@ __device__ __forceinline__ const UnitMatrix& find_matrix(const UnitMatrix* mats,
 __global__ void __launch_bounds__(kBlock) mask_to_lists_kernel(const uint64_t* __restrict__ words,
                                                                const UnitMatrix* __restrict__ mats,
                                                                int* __restrict__ lists, int* __restrict__ counts) {
+  pdl_begin();
   const UnitMatrix m = mats[blockIdx.x];
   __shared__ int warp_tot[kBlock / 32];
   __shared__ int carry;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kBlock) mask_to_lists_kernel(const uint64_t* _
 __global__ void __launch_bounds__(kBlock) mask_to_pairs_kernel(const uint64_t* __restrict__ words,
                                                                const UnitMatrix* __restrict__ mats,
                                                                int* __restrict__ pairs, int* __restrict__ counts) {
+  pdl_begin();
   const UnitMatrix m = mats[blockIdx.x];
   __shared__ int base[kPairGroups + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -164,6 +166,7 @@ __device__ __forceinline__ float4 adamw4(const OptimArgs& a, const AdamCoef& c, 
 }
 
 __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArgs a) {
+  pdl_begin();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int red[kBlock / 32];
   const bool apf = a.apf_ema != nullptr;
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kBlock) masked_sgd_units_kernel(const OptimArg
 
 __global__ void sgd_dense_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
                                  const float* __restrict__ g, long long n4, float scale) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const float4 gv = reinterpret_cast<const float4*>(g)[i];
@@ -261,6 +265,7 @@ __global__ void sgd_dense_kernel(float* __restrict__ master, __nv_bfloat16* __re
 __global__ void apf_update_kernel(float* __restrict__ ema, float* __restrict__ ema_abs,
                                   const float* __restrict__ delta, float* __restrict__ score, long long n,
                                   float alpha) {
+  pdl_begin();
   const float be = 1.0f - alpha;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -276,6 +281,7 @@ __global__ void apf_update_kernel(float* __restrict__ ema, float* __restrict__ e
 // ------------------------------------------------------------------ K7 glue
 __global__ void embedding_fwd_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
                                      __nv_bfloat16* __restrict__ out, int T, int h) {
+  pdl_begin();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp; t < T; t += nw) {
@@ -287,6 +293,7 @@ __global__ void embedding_fwd_kernel(const int* __restrict__ tok, const __nv_bfl
 
 __global__ void embedding_bwd_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ gtable, int T, int h) {
+  pdl_begin();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp; t < T; t += nw) {
@@ -304,6 +311,7 @@ __global__ void embedding_bwd_kernel(const int* __restrict__ tok, const __nv_bfl
 __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                                    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int T, int h,
                                    float eps) {
+  pdl_begin();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = warp; t < T; t += nw) {
@@ -336,6 +344,7 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_dg_kernel(const __nv_bfloat16*
                                                             const float* __restrict__ rstd,
                                                             const __nv_bfloat16* __restrict__ dy,
                                                             float* __restrict__ dg, int T, int h, int rows_per_block) {
+  pdl_begin();
   __shared__ float part[8][256 + 4];
   const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int c = blockIdx.x * 256 + cg * 8;
@@ -372,6 +381,7 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_bwd_kernel(const __nv_bfloat16
                                                              const __nv_bfloat16* __restrict__ dy,
                                                              const __nv_bfloat16* __restrict__ residual,
                                                              __nv_bfloat16* __restrict__ dx, int T, int h) {
+  pdl_begin();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
     const long long off = static_cast<long long>(t) * h;
@@ -407,6 +417,7 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_fwd_reg_kernel(const __nv_bflo
                                                                  const __nv_bfloat16* __restrict__ g,
                                                                  __nv_bfloat16* __restrict__ y,
                                                                  float* __restrict__ rstd, int T, float eps) {
+  pdl_begin();
   constexpr int H = 256 * CH;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -460,6 +471,7 @@ __global__ void __launch_bounds__(norm_bwd_threads<CH>(), 1) rmsnorm_bwd_fused_k
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ residual, __nv_bfloat16* __restrict__ dx,
     float* __restrict__ dg, int T) {
+  pdl_begin();
   constexpr int H = 256 * CH;
   constexpr int NT = norm_bwd_threads<CH>();
   constexpr int NW = NT / 32;
@@ -569,6 +581,7 @@ __global__ void __launch_bounds__(norm_bwd_threads<CH>(), 1) rmsnorm_bwd_fused_k
 // grid.y = token; each thread rotates 8 consecutive pairs (16-byte loads).
 __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int seq, int nh,
                                 int nkv, int hd) {
+  pdl_begin();
   const int half = hd / 2, chunks = half / 8;
   const int t = blockIdx.y;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -593,6 +606,7 @@ __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* _
 // are summed onto their KV head) -> inverse RoPE -> packed dqkv [T, (nh+2nkv) hd].
 __global__ void rope_bwd_pack_kernel(const AttnGradView g, __nv_bfloat16* __restrict__ dqkv,
                                      const float2* __restrict__ cs, int seq, int nh, int nkv, int hd) {
+  pdl_begin();
   const int half = hd / 2, chunks = half / 8;
   const int heads = nh + 2 * nkv;
   const int t = blockIdx.y;
@@ -649,6 +663,7 @@ __device__ __forceinline__ int gate_col(int j) { return ((j >> 7) << 8) + (j & 1
 // grid.y = token, x covers the row in 8-element chunks (no 64-bit index division)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int T,
                                   int ffn) {
+  pdl_begin();
   {
     const long long t = blockIdx.y;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -665,6 +680,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
                                   __nv_bfloat16* __restrict__ dgu, int T, int ffn) {
+  pdl_begin();
   {
     const long long t = blockIdx.y;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -691,6 +707,7 @@ __global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __
                                                                const int* __restrict__ targets,
                                                                float* __restrict__ loss_sum, int V,
                                                                float grad_scale, float loss_scale) {
+  pdl_begin();
   const long long t = blockIdx.x;
   __nv_bfloat16* row = logits + t * V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -743,6 +760,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 __global__ void init_normal_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w, long long n,
                                    float stddev, uint64_t seed) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const uint64_t r = mix64(seed + 0x9e3779b97f4a7c15ULL * static_cast<uint64_t>(i + 1));
@@ -755,6 +773,7 @@ __global__ void init_normal_kernel(float* __restrict__ master, __nv_bfloat16* __
 }
 
 __global__ void fill_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w, long long n, float v) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     master[i] = v;
@@ -763,6 +782,7 @@ __global__ void fill_kernel(float* __restrict__ master, __nv_bfloat16* __restric
 }
 
 __global__ void rope_table_kernel(float2* cs, int seq, int hd, float theta) {
+  pdl_begin();
   const int half = hd / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < seq * half; i += gridDim.x * blockDim.x) {
     const int p = i / half, j = i % half;
@@ -773,6 +793,7 @@ __global__ void rope_table_kernel(float2* cs, int seq, int hd, float theta) {
 }
 
 __global__ void random_tokens_kernel(int* tok, long long n, int vocab, uint64_t seed) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     tok[i] = static_cast<int>(mix64(seed + 0x9e3779b97f4a7c15ULL * static_cast<uint64_t>(i + 1)) %
@@ -784,33 +805,34 @@ __global__ void random_tokens_kernel(int* tok, long long n, int vocab, uint64_t 
 int launch_mask_to_unit_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* lists, int* counts,
                               cudaStream_t s) {
   if (nmats <= 0) return PF_OK;
-  mask_to_lists_kernel<<<nmats, kBlock, 0, s>>>(words, mats, lists, counts);
+  launch_k(mask_to_lists_kernel, dim3(nmats), dim3(kBlock), 0, s, words, mats, lists, counts);
   return status();
 }
 
 int launch_mask_to_pair_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* pairs, int* counts,
                               cudaStream_t s) {
   if (nmats <= 0) return PF_OK;
-  mask_to_pairs_kernel<<<nmats, kBlock, 0, s>>>(words, mats, pairs, counts);
+  launch_k(mask_to_pairs_kernel, dim3(nmats), dim3(kBlock), 0, s, words, mats, pairs, counts);
   return status();
 }
 
 int launch_masked_sgd_units(const OptimArgs& a, cudaStream_t s) {
   if (a.total_units <= 0) return PF_OK;
-  masked_sgd_units_kernel<<<grid_for(a.total_units, 8), kBlock, 0, s>>>(a);
+  launch_k(masked_sgd_units_kernel, dim3(grid_for(a.total_units, 8)), dim3(kBlock), 0, s, a);
   return status();
 }
 
 int launch_sgd_dense(float* master, __nv_bfloat16* w, const float* g, long long n, float scale, cudaStream_t s) {
   if (n <= 0) return PF_OK;
   if (n % 4) return PF_ERR_INVALID;
-  sgd_dense_kernel<<<grid_for((n / 4 + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, g, n / 4, scale);
+  launch_k(sgd_dense_kernel, dim3(grid_for((n / 4 + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, master, w, g, n / 4, scale);
   return status();
 }
 
 __global__ void adamw_dense_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w,
                                    const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                                    long long n, const OptimArgs a, const AdamCoef c) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float th = master[i], mi = m[i], vi = v[i];
@@ -836,27 +858,27 @@ int launch_adamw_dense(float* master, __nv_bfloat16* w, const float* g, float* m
   a.eps = eps;
   a.weight_decay = weight_decay;
   const AdamCoef c{static_cast<float>(lr / bc1), static_cast<float>(1.0 / std::sqrt(bc2)), 1.f - lr * weight_decay};
-  adamw_dense_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, g, m, v, n, a, c);
+  launch_k(adamw_dense_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, master, w, g, m, v, n, a, c);
   return status();
 }
 
 int launch_apf_update(float* ema, float* ema_abs, const float* delta, float* score, long long n, float alpha,
                       cudaStream_t s) {
   if (n <= 0) return PF_OK;
-  apf_update_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(ema, ema_abs, delta, score, n, alpha);
+  launch_k(apf_update_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, ema, ema_abs, delta, score, n, alpha);
   return status();
 }
 
 int launch_embedding_fwd(const int* tok, const __nv_bfloat16* table, __nv_bfloat16* out, int T, int h,
                          cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  embedding_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(tok, table, out, T, h);
+  launch_k(embedding_fwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, tok, table, out, T, h);
   return status();
 }
 
 int launch_embedding_bwd(const int* tok, const __nv_bfloat16* dout, float* g, int T, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  embedding_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(tok, dout, g, T, h);
+  launch_k(embedding_bwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, tok, dout, g, T, h);
   return status();
 }
 
@@ -865,15 +887,15 @@ int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bflo
   if (h % 8) return PF_ERR_INVALID;
   const int grid = grid_for((T + 7) / 8);
   switch (h) {
-    case 256: rmsnorm_fwd_reg_kernel<1><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
-    case 512: rmsnorm_fwd_reg_kernel<2><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
-    case 1024: rmsnorm_fwd_reg_kernel<4><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
-    case 2048: rmsnorm_fwd_reg_kernel<8><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
-    case 4096: rmsnorm_fwd_reg_kernel<16><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
-    case 5120: rmsnorm_fwd_reg_kernel<20><<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, eps); return status();
+    case 256: launch_k(rmsnorm_fwd_reg_kernel<1>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
+    case 512: launch_k(rmsnorm_fwd_reg_kernel<2>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
+    case 1024: launch_k(rmsnorm_fwd_reg_kernel<4>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
+    case 2048: launch_k(rmsnorm_fwd_reg_kernel<8>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
+    case 4096: launch_k(rmsnorm_fwd_reg_kernel<16>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
+    case 5120: launch_k(rmsnorm_fwd_reg_kernel<20>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps); return status();
     default: break;
   }
-  rmsnorm_fwd_kernel<<<grid, kBlock, 0, s>>>(x, g, y, rstd, T, h, eps);
+  launch_k(rmsnorm_fwd_kernel, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, h, eps);
   return status();
 }
 
@@ -893,7 +915,7 @@ int launch_rmsnorm_bwd_fused(const __nv_bfloat16* x, const __nv_bfloat16* g, con
     attr = true;
   }
   const int grid = std::max(1, std::min(num_sms(), (T + NT / 32 - 1) / (NT / 32)));
-  rmsnorm_bwd_fused_kernel<CH><<<grid, NT, smem, s>>>(x, g, rstd, dy, residual, dx, dg, T);
+  launch_k(rmsnorm_bwd_fused_kernel<CH>, dim3(grid), dim3(NT), smem, s, x, g, rstd, dy, residual, dx, dg, T);
   return status();
 }
 }  // namespace
@@ -910,7 +932,7 @@ int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const flo
     case 5120: return launch_rmsnorm_bwd_fused<20>(x, g, rstd, dy, residual, dx, dg, T, s);
     default: break;
   }
-  rmsnorm_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, rstd, dy, residual, dx, T, h);
+  launch_k(rmsnorm_bwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, x, g, rstd, dy, residual, dx, T, h);
   int rc = status();
   if (rc != PF_OK || dg == nullptr) return rc;
   // column blocks x row chunks so the grid covers ~2 waves
@@ -918,7 +940,7 @@ int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const flo
   int row_chunks = std::max(1, (2 * num_sms()) / col_blocks);
   const int rows_per_block = std::max(8, (T + row_chunks - 1) / row_chunks);
   row_chunks = (T + rows_per_block - 1) / rows_per_block;
-  rmsnorm_dg_kernel<<<dim3(col_blocks, row_chunks), kBlock, 0, s>>>(x, rstd, dy, dg, T, h, rows_per_block);
+  launch_k(rmsnorm_dg_kernel, dim3(dim3(col_blocks, row_chunks)), dim3(kBlock), 0, s, x, rstd, dy, dg, T, h, rows_per_block);
   return status();
 }
 
@@ -926,7 +948,7 @@ int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh
   if (hd % 16) return PF_ERR_INVALID;
   const int work = (nh + nkv) * (hd / 16);
   const int threads = std::min(kBlock, (work + 31) / 32 * 32);
-  rope_fwd_kernel<<<dim3((work + threads - 1) / threads, T), threads, 0, s>>>(qkv, cs, seq, nh, nkv, hd);
+  launch_k(rope_fwd_kernel, dim3(dim3((work + threads - 1) / threads, T)), dim3(threads), 0, s, qkv, cs, seq, nh, nkv, hd);
   return status();
 }
 
@@ -935,50 +957,50 @@ int launch_rope_bwd_pack(const AttnGradView& g, __nv_bfloat16* dqkv, const float
   if (hd % 16 || g.rep < 1) return PF_ERR_INVALID;
   const int work = (nh + 2 * nkv) * (hd / 16);
   const int threads = std::min(kBlock, (work + 31) / 32 * 32);
-  rope_bwd_pack_kernel<<<dim3((work + threads - 1) / threads, T), threads, 0, s>>>(g, dqkv, cs, seq, nh, nkv, hd);
+  launch_k(rope_bwd_pack_kernel, dim3(dim3((work + threads - 1) / threads, T)), dim3(threads), 0, s, g, dqkv, cs, seq, nh, nkv, hd);
   return status();
 }
 
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s) {
   if (ffn % 128) return PF_ERR_INVALID;
-  swiglu_fwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, a, T, ffn);
+  launch_k(swiglu_fwd_kernel, dim3(dim3((ffn / 8 + kBlock - 1) / kBlock, T)), dim3(kBlock), 0, s, gu, a, T, ffn);
   return status();
 }
 
 int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
                       cudaStream_t s) {
   if (ffn % 128) return PF_ERR_INVALID;
-  swiglu_bwd_kernel<<<dim3((ffn / 8 + kBlock - 1) / kBlock, T), kBlock, 0, s>>>(gu, da, dgu, T, ffn);
+  launch_k(swiglu_bwd_kernel, dim3(dim3((ffn / 8 + kBlock - 1) / kBlock, T)), dim3(kBlock), 0, s, gu, da, dgu, T, ffn);
   return status();
 }
 
 int launch_cross_entropy(__nv_bfloat16* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
                          float loss_scale, cudaStream_t s) {
   if (V % 8 || T <= 0) return PF_ERR_INVALID;
-  cross_entropy_kernel<<<T, kBlock, 0, s>>>(logits, targets, loss_sum, V, grad_scale, loss_scale);
+  launch_k(cross_entropy_kernel, dim3(T), dim3(kBlock), 0, s, logits, targets, loss_sum, V, grad_scale, loss_scale);
   return status();
 }
 
 int launch_init_normal(float* master, __nv_bfloat16* w, long long n, float stddev, uint64_t seed, cudaStream_t s) {
   if (n <= 0) return PF_OK;
-  init_normal_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, n, stddev, seed);
+  launch_k(init_normal_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, master, w, n, stddev, seed);
   return status();
 }
 
 int launch_fill(float* master, __nv_bfloat16* w, long long n, float v, cudaStream_t s) {
   if (n <= 0) return PF_OK;
-  fill_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(master, w, n, v);
+  launch_k(fill_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, master, w, n, v);
   return status();
 }
 
 int launch_rope_table(float2* cs, int seq, int hd, float theta, cudaStream_t s) {
-  rope_table_kernel<<<grid_for((static_cast<long long>(seq) * hd / 2 + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+  launch_k(rope_table_kernel, dim3(grid_for((static_cast<long long>(seq) * hd / 2 + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, 
       cs, seq, hd, theta);
   return status();
 }
 
 int launch_random_tokens(int* tok, long long n, int vocab, uint64_t seed, cudaStream_t s) {
-  random_tokens_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(tok, n, vocab, seed);
+  launch_k(random_tokens_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, tok, n, vocab, seed);
   return status();
 }
 

@@ -81,6 +81,14 @@ int probe_kind();
 void probe_begin(cudaStream_t s);  // no-op unless the probe is enabled
 void probe_end(cudaStream_t s);
 
+// Programmatic dependent launch (PDL): every kernel of this library is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, waits (griddepcontrol.wait) for the
+// previous kernel's completion and memory before touching global memory, and lets the next
+// kernel launch early (griddepcontrol.launch_dependents), so a kernel's launch and prologue
+// overlap its predecessor's tail. Off unless PF_PDL=1 (measured: capi_kernels.cu). The
+// kernels always execute griddepcontrol.wait / launch_dependents (no-ops without the attribute).
+bool pdl_enabled();
+
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).
 void count_launch();
 long long launch_count();

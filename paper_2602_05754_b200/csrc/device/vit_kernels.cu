@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "kernel_util.cuh"
+#include "ptx.cuh"
 #include "vit_kernels.cuh"
 
 namespace pf {
@@ -25,6 +26,7 @@ __global__ void __launch_bounds__(kBlock) layernorm_fwd_kernel(const __nv_bfloat
                                                                float* __restrict__ mean_out,
                                                                float* __restrict__ rstd_out, int T, int h,
                                                                float eps) {
+  pdl_begin();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
     const __nv_bfloat16* xr = x + static_cast<long long>(t) * h;
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(kBlock) layernorm_bwd_kernel(const __nv_bfloat
                                                                const __nv_bfloat16* __restrict__ dy,
                                                                const __nv_bfloat16* __restrict__ residual,
                                                                __nv_bfloat16* __restrict__ dx, int T, int h) {
+  pdl_begin();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = blockIdx.x * (kBlock / 32) + warp; t < T; t += gridDim.x * (kBlock / 32)) {
     const long long off = static_cast<long long>(t) * h;
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(kBlock) column_reduce_kernel(const __nv_bfloat
                                                                const float* __restrict__ rstd,
                                                                float* __restrict__ dg, float* __restrict__ db,
                                                                int T, int n, int rows_per_block) {
+  pdl_begin();
   __shared__ float pg[8][256 + 4];
   __shared__ float pb[8][256 + 4];
   const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
@@ -158,6 +162,7 @@ __device__ __forceinline__ float gelu_erf_grad(float v) {
 }
 
 __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ pre, __nv_bfloat16* __restrict__ act, long long n8) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float f[8];
@@ -170,6 +175,7 @@ __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ pre, __nv_bflo
 
 __global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ pre, const __nv_bfloat16* __restrict__ dact,
                                 __nv_bfloat16* __restrict__ dpre, long long n8) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float p[8], d[8];
@@ -183,6 +189,7 @@ __global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ pre, const __n
 
 __global__ void add_bias_kernel(__nv_bfloat16* __restrict__ c, long long ldc, const __nv_bfloat16* __restrict__ bias,
                                 int M, int N) {
+  pdl_begin();
   const int chunks = N / 8;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < static_cast<long long>(M) * chunks;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -201,6 +208,7 @@ __global__ void add_bias_kernel(__nv_bfloat16* __restrict__ c, long long ldc, co
 __global__ void vit_embed_fwd_kernel(const __nv_bfloat16* __restrict__ E, const __nv_bfloat16* __restrict__ pbias,
                                      const __nv_bfloat16* __restrict__ cls, const __nv_bfloat16* __restrict__ pos,
                                      __nv_bfloat16* __restrict__ x, int B, int S, int h) {
+  pdl_begin();
   const int chunks = h / 8;
   const long long total = static_cast<long long>(B) * S * chunks;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -230,6 +238,7 @@ __global__ void vit_embed_fwd_kernel(const __nv_bfloat16* __restrict__ E, const 
 __global__ void vit_embed_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_bfloat16* __restrict__ dE,
                                      float* __restrict__ dpos, float* __restrict__ dcls, float* __restrict__ dpbias,
                                      int B, int S, int h) {
+  pdl_begin();
   const int chunks = h / 8;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
        i < static_cast<long long>(S) * chunks; i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -257,6 +266,7 @@ __global__ void vit_embed_bwd_kernel(const __nv_bfloat16* __restrict__ dx, __nv_
 // out[b] = x[b * S + row_in_seq]   (cls rows for the head) / scatter back into zeros
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out, int B,
                                    int S, int h) {
+  pdl_begin();
   const int chunks = h / 8;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
        i < static_cast<long long>(B) * chunks; i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -268,6 +278,7 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfl
 
 __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dx, int B,
                                     int S, int h) {
+  pdl_begin();
   const int chunks = h / 8;
   const long long total = static_cast<long long>(B) * S * chunks;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -283,6 +294,7 @@ __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ src, __nv_
 
 // deterministic synthetic pixels in [-1, 1) (splitmix64 of the element index)
 __global__ void synthetic_patches_kernel(__nv_bfloat16* __restrict__ out, long long n, uint64_t seed) {
+  pdl_begin();
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     uint64_t z = seed + static_cast<uint64_t>(i + 1) * 0x9e3779b97f4a7c15ULL;
@@ -305,7 +317,7 @@ void column_grid(int T, int n, int* col_blocks, int* row_chunks, int* rows_per_b
 int launch_layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
                          float* mean, float* rstd, int T, int h, float eps, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  layernorm_fwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, b, y, mean, rstd, T, h, eps);
+  launch_k(layernorm_fwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, h, eps);
   return status();
 }
 
@@ -313,12 +325,12 @@ int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const f
                          const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
                          float* db, int T, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  layernorm_bwd_kernel<<<grid_for((T + 7) / 8), kBlock, 0, s>>>(x, g, mean, rstd, dy, residual, dx, T, h);
+  launch_k(layernorm_bwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, x, g, mean, rstd, dy, residual, dx, T, h);
   int rc = status();
   if (rc != PF_OK || (!dg && !db)) return rc;
   int cb, rcn, rpb;
   column_grid(T, h, &cb, &rcn, &rpb);
-  column_reduce_kernel<<<dim3(cb, rcn), kBlock, 0, s>>>(dy, h, x, mean, rstd, dg, db, T, h, rpb);
+  launch_k(column_reduce_kernel, dim3(dim3(cb, rcn)), dim3(kBlock), 0, s, dy, h, x, mean, rstd, dg, db, T, h, rpb);
   return status();
 }
 
@@ -326,26 +338,26 @@ int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, i
   if (n % 8 || ldy % 8) return PF_ERR_INVALID;
   int cb, rcn, rpb;
   column_grid(T, n, &cb, &rcn, &rpb);
-  column_reduce_kernel<<<dim3(cb, rcn), kBlock, 0, s>>>(dy, ldy, nullptr, nullptr, nullptr, nullptr, db, T, n, rpb);
+  launch_k(column_reduce_kernel, dim3(dim3(cb, rcn)), dim3(kBlock), 0, s, dy, ldy, nullptr, nullptr, nullptr, nullptr, db, T, n, rpb);
   return status();
 }
 
 int launch_gelu_fwd(const __nv_bfloat16* pre, __nv_bfloat16* act, long long n, cudaStream_t s) {
   if (n % 8) return PF_ERR_INVALID;
-  gelu_fwd_kernel<<<grid_for((n / 8 + kBlock - 1) / kBlock), kBlock, 0, s>>>(pre, act, n / 8);
+  launch_k(gelu_fwd_kernel, dim3(grid_for((n / 8 + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, pre, act, n / 8);
   return status();
 }
 
 int launch_gelu_bwd(const __nv_bfloat16* pre, const __nv_bfloat16* dact, __nv_bfloat16* dpre, long long n,
                     cudaStream_t s) {
   if (n % 8) return PF_ERR_INVALID;
-  gelu_bwd_kernel<<<grid_for((n / 8 + kBlock - 1) / kBlock), kBlock, 0, s>>>(pre, dact, dpre, n / 8);
+  launch_k(gelu_bwd_kernel, dim3(grid_for((n / 8 + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, pre, dact, dpre, n / 8);
   return status();
 }
 
 int launch_add_bias(__nv_bfloat16* c, long long ldc, const __nv_bfloat16* bias, int M, int N, cudaStream_t s) {
   if (N % 8 || ldc % 8) return PF_ERR_INVALID;
-  add_bias_kernel<<<grid_for((static_cast<long long>(M) * (N / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(c, ldc, bias,
+  launch_k(add_bias_kernel, dim3(grid_for((static_cast<long long>(M) * (N / 8) + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, c, ldc, bias,
                                                                                                            M, N);
   return status();
 }
@@ -353,7 +365,7 @@ int launch_add_bias(__nv_bfloat16* c, long long ldc, const __nv_bfloat16* bias, 
 int launch_vit_embed_fwd(const __nv_bfloat16* E, const __nv_bfloat16* pbias, const __nv_bfloat16* cls,
                          const __nv_bfloat16* pos, __nv_bfloat16* x, int B, int S, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  vit_embed_fwd_kernel<<<grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+  launch_k(vit_embed_fwd_kernel, dim3(grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, 
       E, pbias, cls, pos, x, B, S, h);
   return status();
 }
@@ -361,27 +373,27 @@ int launch_vit_embed_fwd(const __nv_bfloat16* E, const __nv_bfloat16* pbias, con
 int launch_vit_embed_bwd(const __nv_bfloat16* dx, __nv_bfloat16* dE, float* dpos, float* dcls, float* dpbias, int B,
                          int S, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  vit_embed_bwd_kernel<<<grid_for((static_cast<long long>(S) * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+  launch_k(vit_embed_bwd_kernel, dim3(grid_for((static_cast<long long>(S) * (h / 8) + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, 
       dx, dE, dpos, dcls, dpbias, B, S, h);
   return status();
 }
 
 int launch_gather_rows(const __nv_bfloat16* x, __nv_bfloat16* out, int B, int S, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  gather_rows_kernel<<<grid_for((static_cast<long long>(B) * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(x, out, B,
+  launch_k(gather_rows_kernel, dim3(grid_for((static_cast<long long>(B) * (h / 8) + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, x, out, B,
                                                                                                               S, h);
   return status();
 }
 
 int launch_scatter_rows(const __nv_bfloat16* src, __nv_bfloat16* dx, int B, int S, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  scatter_rows_kernel<<<grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+  launch_k(scatter_rows_kernel, dim3(grid_for((static_cast<long long>(B) * S * (h / 8) + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, 
       src, dx, B, S, h);
   return status();
 }
 
 int launch_synthetic_patches(__nv_bfloat16* out, long long n, uint64_t seed, cudaStream_t s) {
-  synthetic_patches_kernel<<<grid_for((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(out, n, seed);
+  launch_k(synthetic_patches_kernel, dim3(grid_for((n + kBlock - 1) / kBlock)), dim3(kBlock), 0, s, out, n, seed);
   return status();
 }
 
