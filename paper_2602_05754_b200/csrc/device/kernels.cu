@@ -702,28 +702,60 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
   }
 }
 
-// one block per row: online max/sum-exp, then dlogits in place
-__global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __restrict__ logits,
-                                                               const int* __restrict__ targets,
-                                                               float* __restrict__ loss_sum, int V,
-                                                               float grad_scale, float loss_scale) {
+// One block per row: online max/sum-exp, then dlogits in place. Large vocabularies use
+// 512-thread blocks, 2 per SM: ~300 rows in flight (76 MB at V = 128256) stay in L2, so the
+// second pass over a row hits L2 instead of HBM (with 8 x 256-thread blocks per SM, 1184 rows
+// = 303 MB were in flight and the row was read from HBM twice). Four 16-byte loads per
+// thread are issued before their max/exp work.
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 2 : 1) cross_entropy_kernel(__nv_bfloat16* __restrict__ logits,
+                                                                             const int* __restrict__ targets,
+                                                                             float* __restrict__ loss_sum, int V,
+                                                                             float grad_scale, float loss_scale) {
   pdl_begin();
   const long long t = blockIdx.x;
   __nv_bfloat16* row = logits + t * V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ float sm[kBlock / 32], ss[kBlock / 32];
+  __shared__ float sm[NT / 32], ss[NT / 32];
   float mx = -INFINITY, sum = 0.f;
-  for (int c = threadIdx.x * 8; c < V; c += kBlock * 8) {
-    float f[8];
-    load8(row + c, f);
-    float lm = f[0];
+  constexpr int U = 4;
+  for (int c0 = threadIdx.x * 8; c0 < V; c0 += NT * 8 * U) {
+    uint4 raw[U];
 #pragma unroll
-    for (int i = 1; i < 8; ++i) lm = fmaxf(lm, f[i]);
-    const float nm = fmaxf(mx, lm);
-    sum *= __expf(mx - nm);
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * NT * 8;
+      raw[u] = c < V ? *reinterpret_cast<const uint4*>(row + c)
+                     : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);  // bf16 -inf
+    }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sum += __expf(f[i] - nm);
-    mx = nm;
+    for (int u = 0; u < U; ++u) {
+      float f[8];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 v2 = __bfloat1622float2(h[i]);
+        f[2 * i] = v2.x;
+        f[2 * i + 1] = v2.y;
+      }
+      float lm = f[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) lm = fmaxf(lm, f[i]);
+      if (lm == -INFINITY) continue;  // padding chunk past the row end
+      const float nm = fmaxf(mx, lm);
+      // e^(x - m) = 2^(x log2e - m log2e): one FFMA + one MUFU.EX2 per logit
+      const float nml = nm * kLog2e;
+      sum *= ex2_approx(fmaf(mx, kLog2e, -nml));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += ex2_approx(fmaf(f[i], kLog2e, -nml));
+      mx = nm;
+    }
   }
   // combine (max, sum) across the block
   float wm = warp_max(mx);
@@ -735,18 +767,19 @@ __global__ void __launch_bounds__(kBlock) cross_entropy_kernel(__nv_bfloat16* __
   }
   __syncthreads();
   float bm = -INFINITY;
-  for (int w = 0; w < kBlock / 32; ++w) bm = fmaxf(bm, sm[w]);
+  for (int w = 0; w < NT / 32; ++w) bm = fmaxf(bm, sm[w]);
   float bs = 0.f;
-  for (int w = 0; w < kBlock / 32; ++w) bs += sm[w] == -INFINITY ? 0.f : ss[w] * __expf(sm[w] - bm);
+  for (int w = 0; w < NT / 32; ++w) bs += sm[w] == -INFINITY ? 0.f : ss[w] * __expf(sm[w] - bm);
   const float lse = bm + __logf(bs);
   const int tgt = targets[t];
   const float xt = __bfloat162float(row[tgt]);
   __syncthreads();
-  for (int c = threadIdx.x * 8; c < V; c += kBlock * 8) {
+  const float lsel = lse * kLog2e;
+  for (int c = threadIdx.x * 8; c < V; c += NT * 8) {
     float f[8];
     load8(row + c, f);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = (__expf(f[i] - lse) - (c + i == tgt ? 1.f : 0.f)) * grad_scale;
+    for (int i = 0; i < 8; ++i) f[i] = (ex2_approx(fmaf(f[i], kLog2e, -lsel)) - (c + i == tgt ? 1.f : 0.f)) * grad_scale;
     store8(row + c, f);
   }
   if (threadIdx.x == 0) atomicAdd(loss_sum, (lse - xt) * loss_scale);
@@ -977,7 +1010,12 @@ int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfl
 int launch_cross_entropy(__nv_bfloat16* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
                          float loss_scale, cudaStream_t s) {
   if (V % 8 || T <= 0) return PF_ERR_INVALID;
-  launch_k(cross_entropy_kernel, dim3(T), dim3(kBlock), 0, s, logits, targets, loss_sum, V, grad_scale, loss_scale);
+  if (V >= 16384)
+    launch_k(cross_entropy_kernel<512>, dim3(T), dim3(512), 0, s, logits, targets, loss_sum, V, grad_scale,
+             loss_scale);
+  else
+    launch_k(cross_entropy_kernel<kBlock>, dim3(T), dim3(kBlock), 0, s, logits, targets, loss_sum, V, grad_scale,
+             loss_scale);
   return status();
 }
 
