@@ -125,7 +125,7 @@ def gemm_roofline(peaks: dict, shape, launches: int, total_ms: float) -> dict:
     ms = total_ms / launches
     flops = 2.0 * T * N * h
     achieved = flops / (ms * 1e-3) / 1e12
-    fused = not vit and os.environ.get("PF_FUSE_SWIGLU", "") != "0" and (h >= 4096 or os.environ.get("PF_FUSE_SWIGLU") == "1")
+    fused = not vit and os.environ.get("PF_FUSE_SWIGLU", "") != "0"
     kernel = f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, {'fc1' if vit else 'gate|up'}" + \
         (", SwiGLU fused in the epilogue)" if fused else ")")
     # the kernel is timed inside the long timed steps, so the roofline is the SUSTAINED bf16 peak

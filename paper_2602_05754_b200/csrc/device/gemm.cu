@@ -387,7 +387,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // Row-major bf16 matrix [rows][cols] with row stride ld (elements); box
 // {box_cols (inner), box_rows}.
 int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
-              int box_rows) {
+              int box_rows, CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto encode = get_encode();
   if (!encode) return PF_ERR_CUDA;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -395,7 +395,7 @@ int make_tmap(CUtensorMap* map, const void* ptr, long long rows, long long cols,
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   // invalid geometry (row stride not a multiple of 16 B, misaligned base, ...)
   return r == CUDA_SUCCESS ? PF_OK : PF_ERR_INVALID;
@@ -457,6 +457,11 @@ int fill_problem(Problem& pr, const GemmOperand& A, const GemmOperand& B, int M,
 int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
                      int box_rows) {
   return make_tmap(map, ptr, rows, cols, ld, box_cols, box_rows);
+}
+
+int tma_desc_bf16_2d_sw64(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
+                          int box_cols, int box_rows) {
+  return make_tmap(map, ptr, rows, cols, ld, box_cols, box_rows, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 int num_sms() {

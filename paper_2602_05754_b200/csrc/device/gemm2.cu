@@ -40,6 +40,8 @@ namespace pf {
 
 int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
                      int box_rows);
+int tma_desc_bf16_2d_sw64(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
+                          int box_cols, int box_rows);
 
 namespace {
 
@@ -49,19 +51,28 @@ constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, alternating 32
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = 64 + kEpiThreads;
 
-template <int BN>
+template <int BN, int EPI = EPI_STORE_BF16>
 struct Cfg2 {
-  static constexpr int STAGES = 6;
+  // The SwiGLU epilogues give one ring stage to two epilogue buffers staged through TMA:
+  // EPI_DSWIGLU gate|up of one 32-column chunk (in by TMA, overwritten by d(gate)|d(up), out by
+  // TMA: 16 KB); EPI_SWIGLU gate|up|act of one chunk (out by TMA: 24 KB).
+  static constexpr bool TMA_EPI = EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU;
+  static constexpr int STAGES = TMA_EPI ? 5 : 6;
   static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's half of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_BUF = EPI == EPI_SWIGLU ? 3 * 8192 : 2 * 8192;
+  static constexpr int EPI_BYTES = TMA_EPI ? 2 * EPI_BUF : 0;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
 struct alignas(64) Params2 {
   CUtensorMap ta;
   CUtensorMap tb;
+  // SwiGLU epilogues, 128-row x 32-column boxes, SWIZZLE_64B:
+  CUtensorMap tgu;   // EPI_DSWIGLU: gate|up in (R); EPI_SWIGLU: gate|up out (C)
+  CUtensorMap tdgu;  // EPI_DSWIGLU: d(gate|up) out (C); EPI_SWIGLU: act out (aux)
   void* C;
   long long ldc;
   int M, N, K;
@@ -149,7 +160,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 template <int BN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_tcgen05_pair_kernel(const __grid_constant__ Params2 p) {
-  using Cfg = Cfg2<BN>;
+  using Cfg = Cfg2<BN, EPI>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM2, BN, false, B_MN);
 
@@ -158,11 +169,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;  // EPI_DSWIGLU buffers (1024-aligned)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sE + Cfg::EPI_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* ebar = tempty_bar + 2;  // EPI_DSWIGLU: epilogue buffer k loaded
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -180,12 +193,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 2 * kEpiThreads);
+      mbar_init(&ebar[b], 1);
     }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
+    if constexpr (Cfg::TMA_EPI) {
+      tma_prefetch(&p.tgu);
+      tma_prefetch(&p.tdgu);
+    }
   }
   if (warp == 1) {
     tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
@@ -275,6 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
     int abuf = 0;
     uint32_t aphase = 0;
+    uint32_t ephase = 0;  // EPI_DSWIGLU: bit k = parity of epilogue buffer k's barrier
     SegIter it = seg_begin(p, cluster, nclusters, num_kb);
     Seg sg;
     while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
@@ -302,56 +321,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const long long grow = static_cast<long long>(tm) * BM2 + rank * 128 + row;
       const bool row_ok = grow < p.M;
       if constexpr (EPI == EPI_DSWIGLU) {
-        // acc = d(act) for activation columns [tn*BN, tn*BN + BN); gate/up of those columns sit
-        // in gu at (j / 128) * 256 + j % 128 (+128). They do not depend on the accumulator, so
-        // chunk 0 is fetched while the MMAs still run and chunk c+1 while chunk c computes.
-        // Same arithmetic as swiglu_bwd_kernel on the bf16-rounded d(act). No stream-K.
-        uint4 gb[4], ub[4];
-        auto fetch = [&](int c) {
-          const int gcol = tn * BN + c * 32;
-          if (!row_ok || gcol >= p.N) return;
-          const long long gc = grow * p.ldr + ((gcol >> 7) << 8) + (gcol & 127);
-          const uint4* g4 = reinterpret_cast<const uint4*>(p.R + gc);
-          const uint4* u4 = reinterpret_cast<const uint4*>(p.R + gc + 128);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            gb[j] = ldg_nc_l2_256(g4 + j);
-            ub[j] = ldg_nc_l2_256(u4 + j);
-          }
+        // acc = d(act) for activation columns [tn*BN, tn*BN + BN) of this CTA's 128 rows. For
+        // each 32-column chunk c, TMA brings gate|up (two 128 x 32 boxes at gu columns
+        // (j / 128) * 256 + j % 128 and +128, SWIZZLE_64B) into buffer c & 1; every thread
+        // rewrites its row's 16 columns in place with d(gate)|d(up) (same arithmetic as
+        // swiglu_bwd_kernel on the bf16-rounded d(act)) and one thread stores the boxes by TMA,
+        // then refills the buffer with chunk c + 2. The loads of chunks 0 and 1 are issued
+        // before the accumulator is ready. No stream-K.
+        const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
+        const bool elected = threadIdx.x == 64;
+        auto gate_col = [&](int c) {
+          const int j = tn * BN + c * 32;
+          return ((j >> 7) << 8) + (j & 127);
         };
-        fetch(half);
+        auto load_chunk = [&](int c) {  // elected thread
+          uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
+          bulk_wait_read0();  // the buffer's last TMA store has read it
+          mbar_arrive_expect_tx(&ebar[c & 1], Cfg::EPI_BUF);
+          tma_load_2d(buf, &p.tgu, &ebar[c & 1], gate_col(c), y0);
+          tma_load_2d(buf + Cfg::EPI_BUF / 2, &p.tgu, &ebar[c & 1], gate_col(c) + 128, y0);
+        };
+        if (elected) {
+          load_chunk(0);
+          load_chunk(1);
+        }
         mbar_wait(&tfull_bar[abuf], aphase);
         tc_fence_after();
 #pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                 static_cast<uint32_t>(abuf * BN + c * 32),
+        for (int c = 0; c < BN / 32; ++c) {
+          const int k = c & 1;
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(abuf * BN + c * 32 + half * 16),
                              r);
-          const uint4 gcur[4] = {gb[0], gb[1], gb[2], gb[3]};
-          const uint4 ucur[4] = {ub[0], ub[1], ub[2], ub[3]};
-          if (c + 2 < BN / 32) fetch(c + 2);
+          mbar_wait(&ebar[k], (ephase >> k) & 1u);
+          ephase ^= 1u << k;
           tmem_ld_wait();
-          const int gcol = tn * BN + c * 32;
-          if (!row_ok || gcol >= p.N) continue;
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + ((gcol >> 7) << 8) + (gcol & 127);
+          uint8_t* buf = sE + k * Cfg::EPI_BUF;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gcur[j]);
-            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&ucur[j]);
+          for (int s2 = 0; s2 < 2; ++s2) {
+            // 16-byte chunk (2 half + s2) of this row's 64 bytes, SWIZZLE_64B: chunk ^ ((row / 2) % 4)
+            const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
+            uint4* gp = reinterpret_cast<uint4*>(buf + off);
+            uint4* up = reinterpret_cast<uint4*>(buf + Cfg::EPI_BUF / 2 + off);
+            const uint4 graw = *gp, uraw = *up;
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&graw);
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uraw);
             uint32_t dgw[4], duw[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const float2 g = __bfloat1622float2(g2[i]);
               const float2 u = __bfloat1622float2(u2[i]);
-              const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * j + 2 * i]),
-                                                                        p.alpha * __uint_as_float(r[8 * j + 2 * i + 1])));
+              const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * s2 + 2 * i]),
+                                                                        p.alpha * __uint_as_float(r[8 * s2 + 2 * i + 1])));
               const float s0 = sigmoid_fast(g.x), s1 = sigmoid_fast(g.y);
               duw[i] = pack_bf16x2(d.x * (g.x * s0), d.y * (g.y * s1));
               dgw[i] = pack_bf16x2(d.x * u.x * s0 * (1.f + g.x * (1.f - s0)), d.y * u.y * s1 * (1.f + g.y * (1.f - s1)));
             }
-            reinterpret_cast<uint4*>(dst)[j] = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
-            reinterpret_cast<uint4*>(dst + 128)[j] = make_uint4(duw[0], duw[1], duw[2], duw[3]);
+            *gp = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
+            *up = make_uint4(duw[0], duw[1], duw[2], duw[3]);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiThreads);
+          if (elected) {
+            tma_store_2d(&p.tdgu, buf, gate_col(c), y0);
+            tma_store_2d(&p.tdgu, buf + Cfg::EPI_BUF / 2, gate_col(c) + 128, y0);
+            bulk_commit();
+            if (c + 2 < BN / 32) load_chunk(c + 2);
           }
         }
         tc_fence_before();
@@ -377,37 +413,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if constexpr (EPI == EPI_SWIGLU) {
         // columns [0, BN/2) of the tile are gate j, [BN/2, BN) up j (host: N % BN == 0, no stream-K);
-        // the activation uses the bf16-rounded gate/up exactly as swiglu_fwd_kernel does.
+        // the activation uses the bf16-rounded gate/up exactly as swiglu_fwd_kernel does. Each
+        // 32-column chunk c of gate, up and act is written to buffer c & 1 (three 128 x 32
+        // SWIZZLE_64B boxes) and stored by TMA, so HBM sees whole lines.
+        const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
+        const bool elected = threadIdx.x == 64;
 #pragma unroll 1
-        for (int c = half; c < BN / 64; c += 2) {
-          uint32_t rg[32], ru[32];
-          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(abuf * BN);
-          tmem_ld_32x32b_x32(tbase + c * 32, rg);
-          tmem_ld_32x32b_x32(tbase + BN / 2 + c * 32, ru);
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t rg[16], ru[16];
+          const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(abuf * BN + c * 32 + half * 16);
+          tmem_ld_32x32b_x16(tbase, rg);
+          tmem_ld_32x32b_x16(tbase + BN / 2, ru);
+          uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
+          if (elected) bulk_wait_read1();  // the store of chunk c - 2 (this buffer) has read it
+          named_bar_sync(1, kEpiThreads);
           tmem_ld_wait();
-          if (!row_ok) continue;
-          __nv_bfloat16* gp = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + tn * BN + c * 32;
-          __nv_bfloat16* ap = p.aux + grow * p.ldaux + tn * (BN / 2) + c * 32;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
             uint32_t gw[4], uw[4], aw[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const __nv_bfloat162 g2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(rg[8 * j + 2 * i]),
-                                                              p.alpha * __uint_as_float(rg[8 * j + 2 * i + 1]));
-              const __nv_bfloat162 u2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(ru[8 * j + 2 * i]),
-                                                              p.alpha * __uint_as_float(ru[8 * j + 2 * i + 1]));
+              const __nv_bfloat162 g2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(rg[8 * s2 + 2 * i]),
+                                                              p.alpha * __uint_as_float(rg[8 * s2 + 2 * i + 1]));
+              const __nv_bfloat162 u2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(ru[8 * s2 + 2 * i]),
+                                                              p.alpha * __uint_as_float(ru[8 * s2 + 2 * i + 1]));
               const float2 g = __bfloat1622float2(g2);
               const float2 u = __bfloat1622float2(u2);
-              const float a0 = g.x * sigmoid_fast(g.x) * u.x;
-              const float a1 = g.y * sigmoid_fast(g.y) * u.y;
               gw[i] = *reinterpret_cast<const uint32_t*>(&g2);
               uw[i] = *reinterpret_cast<const uint32_t*>(&u2);
-              aw[i] = pack_bf16x2(a0, a1);
+              aw[i] = pack_bf16x2(g.x * sigmoid_fast(g.x) * u.x, g.y * sigmoid_fast(g.y) * u.y);
             }
-            reinterpret_cast<uint4*>(gp)[j] = make_uint4(gw[0], gw[1], gw[2], gw[3]);
-            reinterpret_cast<uint4*>(gp + BN / 2)[j] = make_uint4(uw[0], uw[1], uw[2], uw[3]);
-            reinterpret_cast<uint4*>(ap)[j] = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+            *reinterpret_cast<uint4*>(buf + off) = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+            *reinterpret_cast<uint4*>(buf + 8192 + off) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+            *reinterpret_cast<uint4*>(buf + 16384 + off) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiThreads);
+          if (elected) {
+            tma_store_2d(&p.tgu, buf, tn * BN + c * 32, y0);
+            tma_store_2d(&p.tgu, buf + 8192, tn * BN + BN / 2 + c * 32, y0);
+            tma_store_2d(&p.tdgu, buf + 16384, tn * (BN / 2) + c * 32, y0);
+            bulk_commit();
           }
         }
         tc_fence_before();
@@ -528,6 +576,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       abuf ^= 1;
       if (abuf == 0) aphase ^= 1;
     }
+    if (Cfg::TMA_EPI && threadIdx.x == 64) bulk_wait0();  // the last TMA stores have landed
   }
 
   tc_fence_before();
@@ -542,7 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // grid must never exceed what the GPU can hold at once).
 template <int BN, bool B_MN, int EPI>
 int max_active_clusters() {
-  using Cfg = Cfg2<BN>;
+  using Cfg = Cfg2<BN, EPI>;
   static int n = -1;
   if (n < 0) {
     auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
@@ -570,7 +619,7 @@ int max_active_clusters() {
 
 template <int BN, bool B_MN, int EPI>
 int launch2(Params2 p, int clusters, cudaStream_t stream) {
-  using Cfg = Cfg2<BN>;
+  using Cfg = Cfg2<BN, EPI>;
   auto kern = gemm_tcgen05_pair_kernel<BN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -652,8 +701,18 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.ldaux = C.ldaux;
   p.bias = static_cast<const __nv_bfloat16*>(C.bias);
   if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16) return PF_ERR_INVALID;
-  if (epi == EPI_SWIGLU && (N % BN != 0 || B.mn_major || !C.aux)) return PF_ERR_INVALID;
-  if (epi == EPI_DSWIGLU && (N % 128 != 0 || !B.mn_major || !C.residual)) return PF_ERR_INVALID;
+  if (epi == EPI_SWIGLU) {
+    if (N % BN != 0 || B.mn_major || !C.aux) return PF_ERR_INVALID;
+    // gate|up [M][N] and act [M][N/2] out by TMA, 32-column x 128-row boxes
+    if ((rc = tma_desc_bf16_2d_sw64(&p.tgu, C.ptr, M, N, C.ld, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.tdgu, C.aux, M, N / 2, C.ldaux, 32, 128))) return rc;
+  }
+  if (epi == EPI_DSWIGLU) {
+    if (N % 128 != 0 || !B.mn_major || !C.residual) return PF_ERR_INVALID;
+    // gate|up in and d(gate|up) out by TMA: [M][2N] bf16, 32-column x 128-row boxes
+    if ((rc = tma_desc_bf16_2d_sw64(&p.tgu, C.residual, M, 2LL * N, C.ldr, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.tdgu, C.ptr, M, 2LL * N, C.ld, 32, 128))) return rc;
+  }
   p.M = M;
   p.N = N;
   p.K = K;

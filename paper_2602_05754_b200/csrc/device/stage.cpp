@@ -41,20 +41,19 @@ bool use_pair() {
   return on;
 }
 
-// SwiGLU forward/backward in the CTA-pair GEMM epilogues. PF_FUSE_SWIGLU=1 forces both on, 0
-// both off; by default (tools/swiglu_bench.py on B200, profiles/r1_swiglu_epilogue.md) the
-// backward is fused (0.148 -> 0.145 ms at LLaMA-1B, 0.451 -> 0.417 ms at LLaMA-8B shapes) and
-// the forward only when K >= 4096: at K = 2048 a tile's mainloop is too short to hide the
-// activation epilogue (0.222 ms GEMM + kernel vs 0.231 ms fused; 8B: 0.709 vs 0.689 ms).
-int fuse_swiglu_mode() {
-  static const int mode = [] {
+// SwiGLU forward/backward in the CTA-pair GEMM epilogues (default), staged through shared
+// memory and TMA stores (profiles/r1_swiglu_epilogue.md): at LLaMA-1B shapes forward 0.212 ms
+// GEMM + kernel -> 0.188 ms fused, backward 0.144 -> 0.121 ms; LLaMA-8B 0.677 -> 0.636 and
+// 0.423 -> 0.371 ms. PF_FUSE_SWIGLU=0 runs GEMM + the standalone kernels.
+bool fuse_swiglu() {
+  static const bool on = [] {
     const char* e = std::getenv("PF_FUSE_SWIGLU");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
+    return !(e && e[0] == '0');
   }();
-  return mode;
+  return on;
 }
-bool fuse_swiglu_fwd(int K) { return fuse_swiglu_mode() == 1 || (fuse_swiglu_mode() < 0 && K >= 4096); }
-bool fuse_swiglu_bwd() { return fuse_swiglu_mode() != 0; }
+bool fuse_swiglu_fwd(int /*K*/) { return fuse_swiglu(); }
+bool fuse_swiglu_bwd() { return fuse_swiglu(); }
 
 int gemm_any(const GemmOperand& A, const GemmOperand& B, void* C, long long ldc, int M, int N, int K, int epi,
              cudaStream_t s) {
