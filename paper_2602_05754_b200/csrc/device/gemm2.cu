@@ -56,13 +56,15 @@ struct Cfg2 {
   // The SwiGLU epilogues give one ring stage to two epilogue buffers staged through TMA:
   // EPI_DSWIGLU gate|up of one 32-column chunk (in by TMA, overwritten by d(gate)|d(up), out by
   // TMA: 16 KB); EPI_SWIGLU gate|up|act of one chunk (out by TMA: 24 KB).
+  // EPI_STORE_BF16 / EPI_ADD_BF16: two 8 KB buffers (one 128 x 32 box of C, R read in place).
   static constexpr bool TMA_EPI = EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU;
+  static constexpr bool TMA_PLAIN = EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16;
   static constexpr int STAGES = TMA_EPI ? 5 : 6;
   static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's half of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BUF = EPI == EPI_SWIGLU ? 3 * 8192 : 2 * 8192;
-  static constexpr int EPI_BYTES = TMA_EPI ? 2 * EPI_BUF : 0;
+  static constexpr int EPI_BUF = EPI == EPI_SWIGLU ? 3 * 8192 : (EPI == EPI_DSWIGLU ? 2 * 8192 : 8192);
+  static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? 2 * EPI_BUF : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
@@ -70,9 +72,14 @@ struct Cfg2 {
 struct alignas(64) Params2 {
   CUtensorMap ta;
   CUtensorMap tb;
-  // SwiGLU epilogues, 128-row x 32-column boxes, SWIZZLE_64B:
-  CUtensorMap tgu;   // EPI_DSWIGLU: gate|up in (R); EPI_SWIGLU: gate|up out (C)
-  CUtensorMap tdgu;  // EPI_DSWIGLU: d(gate|up) out (C); EPI_SWIGLU: act out (aux)
+  // TMA-staged epilogues, 128-row x 32-column boxes, SWIZZLE_64B:
+  //   EPI_DSWIGLU  te_in = gate|up (R)         te_out = d(gate|up) (C)
+  //   EPI_SWIGLU   te_in = gate|up out (C)     te_out = act (aux)
+  //   EPI_ADD_BF16 te_in = residual (R)        te_out = C
+  //   EPI_STORE_BF16                           te_out = C
+  CUtensorMap te_in;
+  CUtensorMap te_out;
+  int tma_epi;  // EPI_STORE_BF16 / EPI_ADD_BF16: 1 = staged through TMA (no bias, no stream-K)
   void* C;
   long long ldc;
   int M, N, K;
@@ -200,9 +207,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
-    if constexpr (Cfg::TMA_EPI) {
-      tma_prefetch(&p.tgu);
-      tma_prefetch(&p.tdgu);
+    if (Cfg::TMA_EPI || (Cfg::TMA_PLAIN && p.tma_epi)) {
+      tma_prefetch(&p.te_in);
+      tma_prefetch(&p.te_out);
     }
   }
   if (warp == 1) {
@@ -338,8 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
           bulk_wait_read0();  // the buffer's last TMA store has read it
           mbar_arrive_expect_tx(&ebar[c & 1], Cfg::EPI_BUF);
-          tma_load_2d(buf, &p.tgu, &ebar[c & 1], gate_col(c), y0);
-          tma_load_2d(buf + Cfg::EPI_BUF / 2, &p.tgu, &ebar[c & 1], gate_col(c) + 128, y0);
+          tma_load_2d(buf, &p.te_in, &ebar[c & 1], gate_col(c), y0);
+          tma_load_2d(buf + Cfg::EPI_BUF / 2, &p.te_in, &ebar[c & 1], gate_col(c) + 128, y0);
         };
         if (elected) {
           load_chunk(0);
@@ -384,8 +391,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
           if (elected) {
-            tma_store_2d(&p.tdgu, buf, gate_col(c), y0);
-            tma_store_2d(&p.tdgu, buf + Cfg::EPI_BUF / 2, gate_col(c) + 128, y0);
+            tma_store_2d(&p.te_out, buf, gate_col(c), y0);
+            tma_store_2d(&p.te_out, buf + Cfg::EPI_BUF / 2, gate_col(c) + 128, y0);
             bulk_commit();
             if (c + 2 < BN / 32) load_chunk(c + 2);
           }
@@ -395,6 +402,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
         continue;
+      }
+      if constexpr (Cfg::TMA_PLAIN) {
+        if (p.tma_epi) {
+          // C = bf16(alpha * acc (+ R)) staged per 32-column chunk: R (EPI_ADD_BF16) arrives by TMA
+          // into buffer c & 1 (chunks 0 and 1 while the MMAs run), every thread writes its row's 16
+          // columns in place, one thread stores the box by TMA and refills the buffer with R of
+          // chunk c + 2 once the store has read it.
+          const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
+          const bool elected = threadIdx.x == 64;
+          auto load_r = [&](int c) {  // elected thread
+            uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
+            bulk_wait_read0();
+            mbar_arrive_expect_tx(&ebar[c & 1], Cfg::EPI_BUF);
+            tma_load_2d(buf, &p.te_in, &ebar[c & 1], tn * BN + c * 32, y0);
+          };
+          if (EPI == EPI_ADD_BF16 && elected) {
+            load_r(0);
+            load_r(1);
+          }
+          mbar_wait(&tfull_bar[abuf], aphase);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            const int k = c & 1;
+            uint32_t r[16];
+            tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(abuf * BN + c * 32 + half * 16),
+                               r);
+            uint8_t* buf = sE + k * Cfg::EPI_BUF;
+            if constexpr (EPI == EPI_ADD_BF16) {
+              mbar_wait(&ebar[k], (ephase >> k) & 1u);
+              ephase ^= 1u << k;
+            } else {
+              if (elected) bulk_wait_read1();  // the store of chunk c - 2 (this buffer) has read it
+              named_bar_sync(1, kEpiThreads);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+              const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
+              uint4* cp4 = reinterpret_cast<uint4*>(buf + off);
+              float w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = p.alpha * __uint_as_float(r[8 * s2 + i]);
+              if constexpr (EPI == EPI_ADD_BF16) {
+                const uint4 old = *cp4;
+                const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(o[i]);
+                  w[2 * i] += f.x;
+                  w[2 * i + 1] += f.y;
+                }
+              }
+              *cp4 = make_uint4(pack_bf16x2(w[0], w[1]), pack_bf16x2(w[2], w[3]), pack_bf16x2(w[4], w[5]),
+                                pack_bf16x2(w[6], w[7]));
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, kEpiThreads);
+            if (elected) {
+              tma_store_2d(&p.te_out, buf, tn * BN + c * 32, y0);
+              bulk_commit();
+              if (EPI == EPI_ADD_BF16 && c + 2 < BN / 32) load_r(c + 2);
+            }
+          }
+          tc_fence_before();
+          mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+          abuf ^= 1;
+          if (abuf == 0) aphase ^= 1;
+          continue;
+        }
       }
       // EPI_ADD_BF16: the residual does not depend on the accumulator, so chunk c's 32 columns
       // are fetched while the MMAs (chunk `half`) or the previous chunk's math (c > half) run.
@@ -452,9 +530,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
           if (elected) {
-            tma_store_2d(&p.tgu, buf, tn * BN + c * 32, y0);
-            tma_store_2d(&p.tgu, buf + 8192, tn * BN + BN / 2 + c * 32, y0);
-            tma_store_2d(&p.tdgu, buf + 16384, tn * (BN / 2) + c * 32, y0);
+            tma_store_2d(&p.te_in, buf, tn * BN + c * 32, y0);
+            tma_store_2d(&p.te_in, buf + 8192, tn * BN + BN / 2 + c * 32, y0);
+            tma_store_2d(&p.te_out, buf + 16384, tn * (BN / 2) + c * 32, y0);
             bulk_commit();
           }
         }
@@ -576,7 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       abuf ^= 1;
       if (abuf == 0) aphase ^= 1;
     }
-    if (Cfg::TMA_EPI && threadIdx.x == 64) bulk_wait0();  // the last TMA stores have landed
+    if ((Cfg::TMA_EPI || Cfg::TMA_PLAIN) && threadIdx.x == 64) bulk_wait0();  // the last TMA stores have landed
   }
 
   tc_fence_before();
@@ -662,6 +740,15 @@ int& streamk_mode_ref() {
 }
 int streamk_mode() { return streamk_mode_ref(); }
 
+// K1/K2 plain epilogues through shared memory + TMA stores (PF_GEMM_TMA_EPI=0: row-per-thread stores)
+bool tma_plain_epi() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_GEMM_TMA_EPI");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 void gemm_set_streamk(int mode) { streamk_mode_ref() = mode; }
@@ -704,14 +791,14 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   if (epi == EPI_SWIGLU) {
     if (N % BN != 0 || B.mn_major || !C.aux) return PF_ERR_INVALID;
     // gate|up [M][N] and act [M][N/2] out by TMA, 32-column x 128-row boxes
-    if ((rc = tma_desc_bf16_2d_sw64(&p.tgu, C.ptr, M, N, C.ld, 32, 128))) return rc;
-    if ((rc = tma_desc_bf16_2d_sw64(&p.tdgu, C.aux, M, N / 2, C.ldaux, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.ptr, M, N, C.ld, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.aux, M, N / 2, C.ldaux, 32, 128))) return rc;
   }
   if (epi == EPI_DSWIGLU) {
     if (N % 128 != 0 || !B.mn_major || !C.residual) return PF_ERR_INVALID;
     // gate|up in and d(gate|up) out by TMA: [M][2N] bf16, 32-column x 128-row boxes
-    if ((rc = tma_desc_bf16_2d_sw64(&p.tgu, C.residual, M, 2LL * N, C.ldr, 32, 128))) return rc;
-    if ((rc = tma_desc_bf16_2d_sw64(&p.tdgu, C.ptr, M, 2LL * N, C.ld, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.residual, M, 2LL * N, C.ldr, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, 2LL * N, C.ld, 32, 128))) return rc;
   }
   p.M = M;
   p.N = N;
@@ -750,6 +837,11 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     p.ws = st.ws;
     p.flags = st.flags;
     p.epoch = ++st.epoch;
+  }
+  if ((epi == EPI_STORE_BF16 || epi == EPI_ADD_BF16) && !p.bias && !p.streamk && N % 32 == 0 && tma_plain_epi()) {
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
+    if (epi == EPI_ADD_BF16 && (rc = tma_desc_bf16_2d_sw64(&p.te_in, p.R, M, N, p.ldr, 32, 128))) return rc;
+    p.tma_epi = 1;
   }
   const bool bmn = B.mn_major;
   switch (epi) {
