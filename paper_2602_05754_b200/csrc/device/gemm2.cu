@@ -79,7 +79,7 @@ struct alignas(64) Params2 {
   //   EPI_STORE_BF16                           te_out = C
   CUtensorMap te_in;
   CUtensorMap te_out;
-  int tma_epi;  // EPI_STORE_BF16 / EPI_ADD_BF16: 1 = staged through TMA (no bias, no stream-K)
+  int tma_epi;  // EPI_STORE_BF16 / EPI_ADD_BF16: 1 = staged through TMA (no stream-K, N % 32 == 0)
   void* C;
   long long ldc;
   int M, N, K;
@@ -446,6 +446,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               float w[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) w[i] = p.alpha * __uint_as_float(r[8 * s2 + i]);
+              if (p.bias != nullptr) {  // per-column bias (ViT linear layers); N % 32 == 0 on this path
+                const uint4 braw = __ldg(reinterpret_cast<const uint4*>(p.bias + tn * BN + c * 32 + half * 16 + 8 * s2));
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(b2[i]);
+                  w[2 * i] += f.x;
+                  w[2 * i + 1] += f.y;
+                }
+              }
               if constexpr (EPI == EPI_ADD_BF16) {
                 const uint4 old = *cp4;
                 const __nv_bfloat162* o = reinterpret_cast<const __nv_bfloat162*>(&old);
@@ -838,7 +848,7 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     p.flags = st.flags;
     p.epoch = ++st.epoch;
   }
-  if ((epi == EPI_STORE_BF16 || epi == EPI_ADD_BF16) && !p.bias && !p.streamk && N % 32 == 0 && tma_plain_epi()) {
+  if ((epi == EPI_STORE_BF16 || epi == EPI_ADD_BF16) && !p.streamk && N % 32 == 0 && tma_plain_epi()) {
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
     if (epi == EPI_ADD_BF16 && (rc = tma_desc_bf16_2d_sw64(&p.te_in, p.R, M, N, p.ldr, 32, 128))) return rc;
     p.tma_epi = 1;
