@@ -125,9 +125,9 @@ def gemm_roofline(peaks: dict, shape, launches: int, total_ms: float) -> dict:
     ms = total_ms / launches
     flops = 2.0 * T * N * h
     achieved = flops / (ms * 1e-3) / 1e12
-    fused = not vit and os.environ.get("PF_FUSE_SWIGLU", "") != "0"
+    fused = os.environ.get("PF_FUSE_SWIGLU", "") != "0"
     kernel = f"gemm_tcgen05_pair (cta_group::2) fwd {T}x{N}x{h} (K1, {'fc1' if vit else 'gate|up'}" + \
-        (", SwiGLU fused in the epilogue)" if fused else ")")
+        ((", bias + GELU" if vit else ", SwiGLU") + " fused in the epilogue)" if fused else ")")
     # the kernel is timed inside the long timed steps, so the roofline is the SUSTAINED bf16 peak
     # (cuBLAS back to back, power-capped clocks); the burst figure is reported beside it
     sus, burst = peaks["bf16_tflops_sustained"], peaks["bf16_tflops"]

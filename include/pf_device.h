@@ -64,6 +64,18 @@ int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw,
 int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw, const void* gu, void* dgu, int T,
                     int ffn, int K, void* stream);
 
+/* ViT MLP with GELU (erf form) fused in the CTA-pair epilogue, staged through TMA:
+ * pf_gemm_gelu:  pre[T, ffn] = bf16(x[T, K] . W1[ffn, K]^T + bias), act = gelu(pre) (== GEMM with bias
+ *                + pf_gelu_fwd); pf_gemm_dgelu: d_act = dY[T, K] . W2[K, ffn] (W2 stored [K][ffn], read
+ *                MN-major) rounded to bf16, dpre = d_act * gelu'(pre) (== GEMM + pf_gelu_bwd); dpre may
+ *                alias pre. ffn % 32 == 0. */
+int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream);              /* act = gelu(pre), n % 8 == 0 */
+int pf_gelu_bwd(const void* pre, const void* dact, void* dpre, long long n, void* stream); /* dpre = dact * gelu'(pre) */
+int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, const void* bias, void* pre, void* act,
+                 int T, int ffn, int K, void* stream);
+int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre, int T,
+                  int ffn, int K, void* stream);
+
 /* Stream-K split of the CTA-pair GEMM: 0 off (default), 1 split every tile, 2 data-parallel
  * full waves + the last wave split over all CTA pairs, -1 auto (mode 2 when the last wave would
  * leave > 8% of the CTA pairs idle). */

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "vit_kernels.cuh"
 #include "pf_device.h"
 #include "trainer.hpp"
 
@@ -119,6 +120,20 @@ int pf_swiglu_fwd(const void* gu, void* a, int T, int ffn, void* stream) {
   return guard([&] {
     return pf::launch_swiglu_fwd(static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(a), T, ffn,
                                  S(stream));
+  });
+}
+
+int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream) {
+  return guard([&] {
+    return pf::launch_gelu_fwd(static_cast<const __nv_bfloat16*>(pre), static_cast<__nv_bfloat16*>(act), n,
+                               S(stream));
+  });
+}
+
+int pf_gelu_bwd(const void* pre, const void* dact, void* dpre, long long n, void* stream) {
+  return guard([&] {
+    return pf::launch_gelu_bwd(static_cast<const __nv_bfloat16*>(pre), static_cast<const __nv_bfloat16*>(dact),
+                               static_cast<__nv_bfloat16*>(dpre), n, S(stream));
   });
 }
 

@@ -72,6 +72,27 @@ int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw
                                    1.0f, pf::EPI_DSWIGLU, static_cast<cudaStream_t>(stream)));
 }
 
+int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, const void* bias, void* pre, void* act,
+                 int T, int ffn, int K, void* stream) {
+  if (!x || !W1 || !pre || !act || ffn % 32 != 0) return PF_ERR_INVALID;
+  pf::GemmOut c{pre, ffn};
+  c.aux = act;
+  c.ldaux = ffn;
+  c.bias = bias;
+  return record(pf::gemm_bf16_pair(pf::GemmOperand{x, ldx, false}, pf::GemmOperand{W1, ldw, false}, c, T, ffn, K,
+                                   1.0f, pf::EPI_GELU, static_cast<cudaStream_t>(stream)));
+}
+
+int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre, int T,
+                  int ffn, int K, void* stream) {
+  if (!dY || !W2 || !pre || !dpre || ffn % 32 != 0) return PF_ERR_INVALID;
+  pf::GemmOut c{dpre, ffn};
+  c.residual = pre;
+  c.ldr = ffn;
+  return record(pf::gemm_bf16_pair(pf::GemmOperand{dY, ldy, false}, pf::GemmOperand{W2, ldw, true}, c, T, ffn, K,
+                                   1.0f, pf::EPI_DGELU, static_cast<cudaStream_t>(stream)));
+}
+
 int pf_gemm_set_streamk(int mode) {
   if (mode < -1 || mode > 2) return PF_ERR_INVALID;
   pf::gemm_set_streamk(mode);

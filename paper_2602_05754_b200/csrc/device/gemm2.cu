@@ -57,13 +57,14 @@ struct Cfg2 {
   // EPI_DSWIGLU gate|up of one 32-column chunk (in by TMA, overwritten by d(gate)|d(up), out by
   // TMA: 16 KB); EPI_SWIGLU gate|up|act of one chunk (out by TMA: 24 KB).
   // EPI_STORE_BF16 / EPI_ADD_BF16: two 8 KB buffers (one 128 x 32 box of C, R read in place).
-  static constexpr bool TMA_EPI = EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU;
+  static constexpr bool TMA_EPI = EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU || EPI == EPI_GELU || EPI == EPI_DGELU;
   static constexpr bool TMA_PLAIN = EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16;
   static constexpr int STAGES = TMA_EPI ? 5 : 6;
   static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's half of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BUF = EPI == EPI_SWIGLU ? 3 * 8192 : (EPI == EPI_DSWIGLU ? 2 * 8192 : 8192);
+  static constexpr int EPI_BUF =
+      EPI == EPI_SWIGLU ? 3 * 8192 : ((EPI == EPI_DSWIGLU || EPI == EPI_GELU) ? 2 * 8192 : 8192);
   static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? 2 * EPI_BUF : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
@@ -75,6 +76,8 @@ struct alignas(64) Params2 {
   // TMA-staged epilogues, 128-row x 32-column boxes, SWIZZLE_64B:
   //   EPI_DSWIGLU  te_in = gate|up (R)         te_out = d(gate|up) (C)
   //   EPI_SWIGLU   te_in = gate|up out (C)     te_out = act (aux)
+  //   EPI_GELU     te_in = pre out (C)         te_out = act (aux)
+  //   EPI_DGELU    te_in = pre (R)             te_out = d(pre) (C)
   //   EPI_ADD_BF16 te_in = residual (R)        te_out = C
   //   EPI_STORE_BF16                           te_out = C
   CUtensorMap te_in;
@@ -499,6 +502,106 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (EPI == EPI_ADD_BF16 && !park) fetch_r(half);
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
+      if constexpr (EPI == EPI_GELU || EPI == EPI_DGELU) {
+        // ViT MLP, per 32-column chunk staged in buffer c & 1 (128 x 32 SWIZZLE_64B boxes):
+        //   EPI_GELU:  pre = bf16(alpha acc + bias), act = gelu(pre); both boxes stored by TMA
+        //              (= GEMM with bias followed by gelu_fwd_kernel, bit for bit)
+        //   EPI_DGELU: pre arrives by TMA (chunks 0 and 1 while the MMAs run), is overwritten in
+        //              place by d(pre) = bf16(alpha acc) * gelu'(pre), stored by TMA, and the buffer
+        //              is refilled with chunk c + 2 (= GEMM then gelu_bwd_kernel, bit for bit)
+        const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
+        const bool elected = threadIdx.x == 64;
+        auto load_pre = [&](int c) {  // EPI_DGELU, elected thread
+          uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
+          bulk_wait_read0();
+          mbar_arrive_expect_tx(&ebar[c & 1], Cfg::EPI_BUF);
+          tma_load_2d(buf, &p.te_in, &ebar[c & 1], tn * BN + c * 32, y0);
+        };
+        if (EPI == EPI_DGELU && elected) {
+          load_pre(0);
+          load_pre(1);
+        }
+        mbar_wait(&tfull_bar[abuf], aphase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int k = c & 1;
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                 static_cast<uint32_t>(abuf * BN + c * 32 + half * 16),
+                             r);
+          uint8_t* buf = sE + k * Cfg::EPI_BUF;
+          if constexpr (EPI == EPI_DGELU) {
+            mbar_wait(&ebar[k], (ephase >> k) & 1u);
+            ephase ^= 1u << k;
+          } else {
+            if (elected) bulk_wait_read1();  // the stores of chunk c - 2 (this buffer) have read it
+            named_bar_sync(1, kEpiThreads);
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
+            uint4* pp = reinterpret_cast<uint4*>(buf + off);
+            if constexpr (EPI == EPI_GELU) {
+              float w[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) w[i] = p.alpha * __uint_as_float(r[8 * s2 + i]);
+              if (p.bias != nullptr) {
+                const uint4 braw =
+                    __ldg(reinterpret_cast<const uint4*>(p.bias + tn * BN + c * 32 + half * 16 + 8 * s2));
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(b2[i]);
+                  w[2 * i] += f.x;
+                  w[2 * i + 1] += f.y;
+                }
+              }
+              uint32_t pw[4], aw[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const __nv_bfloat162 pb = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+                const float2 pf = __bfloat1622float2(pb);
+                pw[i] = *reinterpret_cast<const uint32_t*>(&pb);
+                aw[i] = pack_bf16x2(gelu_erf(pf.x), gelu_erf(pf.y));
+              }
+              *pp = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+              *reinterpret_cast<uint4*>(buf + 8192 + off) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+            } else {
+              const uint4 praw = *pp;
+              const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&praw);
+              uint32_t dw[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 pf = __bfloat1622float2(p2[i]);
+                const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * s2 + 2 * i]),
+                                                                          p.alpha * __uint_as_float(r[8 * s2 + 2 * i + 1])));
+                dw[i] = pack_bf16x2(d.x * gelu_erf_grad(pf.x), d.y * gelu_erf_grad(pf.y));
+              }
+              *pp = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiThreads);
+          if (elected) {
+            if constexpr (EPI == EPI_GELU) {
+              tma_store_2d(&p.te_in, buf, tn * BN + c * 32, y0);
+              tma_store_2d(&p.te_out, buf + 8192, tn * BN + c * 32, y0);
+              bulk_commit();
+            } else {
+              tma_store_2d(&p.te_out, buf, tn * BN + c * 32, y0);
+              bulk_commit();
+              if (c + 2 < BN / 32) load_pre(c + 2);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+        continue;
+      }
       if constexpr (EPI == EPI_SWIGLU) {
         // columns [0, BN/2) of the tile are gate j, [BN/2, BN) up j (host: N % BN == 0, no stream-K);
         // the activation uses the bf16-rounded gate/up exactly as swiglu_fwd_kernel does. Each
@@ -797,7 +900,17 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.aux = static_cast<__nv_bfloat16*>(C.aux);
   p.ldaux = C.ldaux;
   p.bias = static_cast<const __nv_bfloat16*>(C.bias);
-  if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16) return PF_ERR_INVALID;
+  if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16 && epi != EPI_GELU) return PF_ERR_INVALID;
+  if (epi == EPI_GELU) {  // pre [M][N] and act [M][N] out by TMA
+    if (N % 32 != 0 || B.mn_major || !C.aux) return PF_ERR_INVALID;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.ptr, M, N, C.ld, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.aux, M, N, C.ldaux, 32, 128))) return rc;
+  }
+  if (epi == EPI_DGELU) {  // pre [M][N] in, d(pre) [M][N] out by TMA (may be the same buffer)
+    if (N % 32 != 0 || !B.mn_major || !C.residual || C.bias) return PF_ERR_INVALID;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.residual, M, N, C.ldr, 32, 128))) return rc;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
+  }
   if (epi == EPI_SWIGLU) {
     if (N % BN != 0 || B.mn_major || !C.aux) return PF_ERR_INVALID;
     // gate|up [M][N] and act [M][N/2] out by TMA, 32-column x 128-row boxes
@@ -826,7 +939,7 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   const double eff = static_cast<double>(ntiles) / (static_cast<double>(waves) * max_clusters);
   const int mode = streamk_mode();
   const int active = std::min(max_clusters, max_active_clusters<BN, false, EPI_STORE_BF16>());
-  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && ntiles > active && num_kb >= 8 &&
+  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && epi != EPI_GELU && epi != EPI_DGELU && ntiles > active && num_kb >= 8 &&
                   (mode == 1 || mode == 2 || (mode < 0 && eff < 0.92));
   if (sk) {
     StreamKState& st = sk_state();
@@ -868,6 +981,10 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
       return launch2<BN, false, EPI_SWIGLU>(p, clusters, stream);
     case EPI_DSWIGLU:
       return launch2<BN, true, EPI_DSWIGLU>(p, clusters, stream);
+    case EPI_GELU:
+      return launch2<BN, false, EPI_GELU>(p, clusters, stream);
+    case EPI_DGELU:
+      return launch2<BN, true, EPI_DGELU>(p, clusters, stream);
     default: return PF_ERR_INVALID;
   }
 }

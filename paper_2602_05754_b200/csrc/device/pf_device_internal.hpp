@@ -15,6 +15,8 @@ enum GemmEpilogue : int {
   EPI_STORE_F32 = 3,   // C = alpha * acc (fp32)
   EPI_SWIGLU = 4,      // CTA pair only: C = bf16(gate|up), aux = silu(gate) * up (interleaved 128-blocks)
   EPI_DSWIGLU = 5,     // CTA pair only: acc = d(act) [M][ffn]; residual = gu; C = d(gate|up), same layout as gu
+  EPI_GELU = 6,        // CTA pair only: C = pre = bf16(acc + bias), aux = gelu(pre)      (ViT fc1)
+  EPI_DGELU = 7,       // CTA pair only: acc = d(act); residual = pre; C = d(act) * gelu'(pre) (ViT fc2 dX)
 };
 
 struct GemmOperand {

@@ -268,6 +268,13 @@ __device__ __forceinline__ uint4 ldg_nc_l2_256(const void* p) {
   return v;
 }
 
+// GELU (erf form) and its derivative; shared by the ViT GELU kernels and the fused GEMM
+// epilogues so they agree bit for bit.
+__device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_erf_grad(float v) {
+  return 0.5f * (1.f + erff(v * 0.70710678118654752f)) + v * 0.39894228040143268f * __expf(-0.5f * v * v);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -10,6 +10,8 @@ namespace pf {
 namespace ops {
 
 bool use_pair();
+// SwiGLU / GELU fused in the CTA-pair GEMM epilogues (PF_FUSE_SWIGLU=0 turns both off)
+bool fuse_swiglu();
 // Y[M,N] (op)= A[M,K] . W[N,K]^T, both K-major
 int gemm_fwd(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
              int M, int N, int K, int epi, cudaStream_t s);
@@ -22,6 +24,14 @@ int gemm_fwd_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W,
 int gemm_fwd_resid_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
                         __nv_bfloat16* C, const __nv_bfloat16* R, long long ld, const __nv_bfloat16* bias, int M,
                         int N, int K, cudaStream_t s);
+// ViT MLP: pre = A . W1^T + bias and act = gelu(pre) (GELU fused in the CTA-pair epilogue);
+// dpre = (dY . W2) * gelu'(pre), dpre may alias pre (d_act scratch only on the unfused path)
+int gemm_fwd_bias_gelu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
+                       const __nv_bfloat16* bias, __nv_bfloat16* pre, __nv_bfloat16* act, int M, int N, int K,
+                       cudaStream_t s);
+int gemm_dx_dgelu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw,
+                  const __nv_bfloat16* pre, __nv_bfloat16* d_act, __nv_bfloat16* dpre, int M, int N, int K,
+                  cudaStream_t s);
 // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
 int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,
             int M, int N, int K, int epi, cudaStream_t s);

@@ -156,10 +156,6 @@ __global__ void __launch_bounds__(kBlock) column_reduce_kernel(const __nv_bfloat
   }
 }
 
-__device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
-__device__ __forceinline__ float gelu_erf_grad(float v) {
-  return 0.5f * (1.f + erff(v * 0.70710678118654752f)) + v * 0.39894228040143268f * __expf(-0.5f * v * v);
-}
 
 __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ pre, __nv_bfloat16* __restrict__ act, long long n8) {
   pdl_begin();

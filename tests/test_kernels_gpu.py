@@ -117,6 +117,54 @@ def test_gemm_swiglu_epilogue_matches_unfused(cuda):
     assert torch.equal(a, a_ref)
 
 
+@pytest.mark.parametrize("T,ffn,D", [(512, 768, 256), (3200, 4096, 1024)])
+def test_gemm_gelu_epilogues_match_unfused(cuda, T, ffn, D):
+    """ViT MLP: GELU fused in the pair-GEMM epilogues == GEMM then gelu_fwd / gelu_bwd, bit for bit
+    (zero bias, so the unfused GEMM rounds the same value); with a bias, vs torch fp32; dpre in place."""
+    import torch
+
+    g = torch.Generator().manual_seed(T + ffn + D)
+    x = bf(torch.randn(T, D, generator=g)).cuda()
+    w1 = bf(torch.randn(ffn, D, generator=g) * 0.1).cuda()
+    w2 = bf(torch.randn(D, ffn, generator=g) * 0.1).cuda()  # fc2 weight [out=D][in=ffn]
+    dy = bf(torch.randn(T, D, generator=g)).cuda()
+    zero = torch.zeros(ffn, dtype=torch.bfloat16, device=cuda)
+    pre = torch.empty(T, ffn, dtype=torch.bfloat16, device=cuda)
+    act = torch.empty_like(pre)
+    chk(lib().pf_gemm_gelu(x.data_ptr(), D, w1.data_ptr(), D, zero.data_ptr(), pre.data_ptr(), act.data_ptr(), T, ffn,
+                           D, sp()))
+    pre_ref = torch.empty_like(pre)
+    chk(lib().pf_gemm_bf16(x.data_ptr(), 0, D, w1.data_ptr(), 0, D, pre_ref.data_ptr(), ffn, T, ffn, D, 1.0, 0, 512,
+                           None, 0, sp()))
+    act_ref = torch.empty_like(pre)
+    chk(lib().pf_gelu_fwd(pre_ref.data_ptr(), act_ref.data_ptr(), T * ffn, sp()))
+    torch.cuda.synchronize()
+    assert torch.equal(pre, pre_ref) and torch.equal(act, act_ref)
+    # bias: fp32 reference
+    b = bf(torch.randn(ffn, generator=g)).cuda()
+    chk(lib().pf_gemm_gelu(x.data_ptr(), D, w1.data_ptr(), D, b.data_ptr(), pre.data_ptr(), act.data_ptr(), T, ffn, D,
+                           sp()))
+    torch.cuda.synchronize()
+    p32 = x.float() @ w1.float().t() + b.float()
+    assert (pre.float() - p32).abs().max().item() <= 2e-2 * p32.abs().max().item()
+    a32 = torch.nn.functional.gelu(pre.float())
+    assert (act.float() - a32).abs().max().item() <= 2e-2 * a32.abs().max().item()
+    # backward: dpre = bf16(dy . W2) * gelu'(pre); out of place, then in place over a copy of pre
+    dpre = torch.empty_like(pre)
+    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, pre.data_ptr(), dpre.data_ptr(), T, ffn, D, sp()))
+    da = torch.empty_like(pre)
+    chk(lib().pf_gemm_bf16(dy.data_ptr(), 0, D, w2.data_ptr(), 1, ffn, da.data_ptr(), ffn, T, ffn, D, 1.0, 0, 512,
+                           None, 0, sp()))
+    dpre_ref = torch.empty_like(pre)
+    chk(lib().pf_gelu_bwd(pre.data_ptr(), da.data_ptr(), dpre_ref.data_ptr(), T * ffn, sp()))
+    inplace = pre.clone()
+    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, inplace.data_ptr(), inplace.data_ptr(), T, ffn, D,
+                            sp()))
+    torch.cuda.synchronize()
+    assert torch.equal(dpre, dpre_ref)
+    assert torch.equal(inplace, dpre_ref)
+
+
 @pytest.mark.parametrize("T,ffn,D", [(512, 768, 256), (4096, 2048, 1024)])
 def test_gemm_dswiglu_epilogue_matches_unfused(cuda, T, ffn, D):
     """Pair-GEMM SwiGLU-backward epilogue == GEMM (bf16 d_act) followed by swiglu_bwd, bit for bit
