@@ -52,6 +52,13 @@ int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx
                      int N, int K, const int* pairs, const int* pair_count, int* unit_stamp, int stamp_offset,
                      int stamp, void* stream);
 
+/* K3 over ROW PAIRS (default K3 of the stage engine): the same masked, unit-stamped dW, each
+ * CTA computing two unfrozen units of one unit row with one 128 x 256 MMA per K step, over the
+ * int2 entries {u0, u1 or -1} that pf_mask_to_rowpair_lists writes for this matrix. */
+int pf_gemm_dw_rowpairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                        int N, int K, const int* entries, const int* entry_count, int* unit_stamp, int stamp_offset,
+                        int stamp, void* stream);
+
 /* K1 gate|up projection with the SwiGLU activation fused in the CTA-pair epilogue:
  * gu[T, 2*ffn] = h[T, K] . Wgu^T (bf16, Wgu rows interleave 128-blocks [gate b | up b]),
  * a[T, ffn] = silu(gate) * up from the bf16-rounded gu (== pf_swiglu_fwd(gu)). ffn % 128 == 0. */
@@ -92,7 +99,7 @@ typedef struct pf_unit_matrix {
   int unit_offset;       /* first unit id of the matrix within the stage */
   int tiles_n;           /* ceil(cols / 128) */
   int units;             /* ceil(rows/128) * tiles_n */
-  int pair_offset;       /* first entry (even) of the matrix's K5p pair list: units + pair groups slots */
+  int pair_offset;       /* first int (even) of the matrix's K5p / K5r list: units + max(groups, rows) slots */
 } pf_unit_matrix;
 
 /* K5: frozen-unit bitmask (sample_mask bit order, one bit per 128x128 unit, +1
@@ -100,6 +107,12 @@ typedef struct pf_unit_matrix {
  * and counts[matrix]. mats is a DEVICE array of nmats entries. */
 int pf_mask_to_unit_lists(const uint64_t* frozen_words, const pf_unit_matrix* mats, int nmats, int* lists,
                           int* counts, void* stream);
+
+/* K5r: the same mask -> per-matrix ROW-PAIR lists for pf_gemm_dw_rowpairs at lists[pair_offset..]:
+ * int2 entries {u0, u1} of unfrozen units of one unit row in row-major order, a row with an odd
+ * count ending {u, -1}; counts[matrix] = entries. */
+int pf_mask_to_rowpair_lists(const uint64_t* frozen_words, const pf_unit_matrix* mats, int nmats, int* lists,
+                             int* counts, void* stream);
 
 /* K5p: the same mask -> per-matrix PAIR lists for pf_gemm_dw_pairs at pairs[pair_offset..]:
  * unit rows cut into bands of 32 (more when a matrix has > 2048 band x column groups),

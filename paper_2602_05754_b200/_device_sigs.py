@@ -39,6 +39,7 @@ DEVICE_SIGNATURES = {
     "pf_engine_last_error": ([], c_cp),
     "pf_mask_to_unit_lists": ([c_vp, c_vp, c_int, c_vp, c_vp, c_vp], c_int),
     "pf_mask_to_pair_lists": ([c_vp, c_vp, c_int, c_vp, c_vp, c_vp], c_int),
+    "pf_mask_to_rowpair_lists": ([c_vp, c_vp, c_int, c_vp, c_vp, c_vp], c_int),
     "pf_masked_sgd_units": ([c_vp, c_vp, c_vp, c_vp, c_int, c_f, c_vp, c_int, c_int, c_vp, c_vp, c_f, c_f, c_vp,
                              c_vp], c_int),
     "pf_sgd_dense": ([c_vp, c_vp, c_vp, c_ll, c_f, c_vp], c_int),

@@ -61,6 +61,11 @@ int pf_mask_to_unit_lists(const uint64_t* words, const pf_unit_matrix* mats, int
   return guard([&] { return pf::launch_mask_to_unit_lists(words, U(mats), nmats, lists, counts, S(stream)); });
 }
 
+int pf_mask_to_rowpair_lists(const uint64_t* words, const pf_unit_matrix* mats, int nmats, int* lists, int* counts,
+                             void* stream) {
+  return guard([&] { return pf::launch_mask_to_rowpair_lists(words, U(mats), nmats, lists, counts, S(stream)); });
+}
+
 int pf_mask_to_pair_lists(const uint64_t* words, const pf_unit_matrix* mats, int nmats, int* pairs, int* counts,
                           void* stream) {
   return guard([&] { return pf::launch_mask_to_pair_lists(words, U(mats), nmats, pairs, counts, S(stream)); });

@@ -52,6 +52,14 @@ int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx
   return record(pf::gemm_dw_pairs(&it, 1, unit_stamp, stamp, static_cast<cudaStream_t>(stream)));
 }
 
+int pf_gemm_dw_rowpairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                        int N, int K, const int* entries, const int* entry_count, int* unit_stamp, int stamp_offset,
+                        int stamp, void* stream) {
+  if (!dY || !X || !G) return PF_ERR_INVALID;
+  pf::DwGemm it{dY, ldy, X, ldx, G, ldg, M, N, K, entries, entry_count, stamp_offset};
+  return record(pf::gemm_dw_rowpairs(&it, 1, unit_stamp, stamp, static_cast<cudaStream_t>(stream)));
+}
+
 int pf_gemm_swiglu(const void* h, long long ldh, const void* Wgu, long long ldw, void* gu, void* a, int T, int ffn,
                    int K, void* stream) {
   if (!h || !Wgu || !gu || !a || ffn % 128 != 0) return PF_ERR_INVALID;

@@ -126,6 +126,53 @@ __global__ void __launch_bounds__(kBlock) mask_to_pairs_kernel(const uint64_t* _
   }
 }
 
+// ------------------------------------------------------------------ K5r
+// One block per matrix; warp w walks unit rows w, w + 8, ...: a ballot over 32 column
+// blocks at a time finds the row's unfrozen units, which are paired in order (a row with
+// an odd count ends with {u, -1}). Pass 1 counts entries per row into shared memory, a
+// block scan gives each row its base, pass 2 writes the entries.
+constexpr int kRowPairRows = 4096;
+__global__ void __launch_bounds__(kBlock) mask_to_rowpairs_kernel(const uint64_t* __restrict__ words,
+                                                                  const UnitMatrix* __restrict__ mats,
+                                                                  int* __restrict__ lists, int* __restrict__ counts) {
+  pdl_begin();
+  const UnitMatrix m = mats[blockIdx.x];
+  __shared__ int base[kRowPairRows + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tiles_n = m.tiles_n, tiles_m = m.units / m.tiles_n;
+  auto unfrozen = [&](int mb, int nb) -> bool {
+    if (nb >= tiles_n) return false;
+    const long long g = static_cast<long long>(m.unit_offset) + static_cast<long long>(mb) * tiles_n + nb;
+    return ((words[g >> 6] >> (g & 63)) & 1ull) == 0;
+  };
+  for (int mb = warp; mb < tiles_m; mb += kBlock / 32) {
+    int cnt = 0;
+    for (int n0 = 0; n0 < tiles_n; n0 += 32) cnt += __popc(__ballot_sync(0xffffffffu, unfrozen(mb, n0 + lane)));
+    if (lane == 0) base[mb + 1] = (cnt + 1) >> 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    base[0] = 0;
+    for (int mb = 0; mb < tiles_m; ++mb) base[mb + 1] += base[mb];
+    counts[blockIdx.x] = base[tiles_m];
+  }
+  __syncthreads();
+  int* out = lists + m.pair_offset;
+  for (int mb = warp; mb < tiles_m; mb += kBlock / 32) {
+    int pos = 0;  // unfrozen units of this row seen so far
+    for (int n0 = 0; n0 < tiles_n; n0 += 32) {
+      const bool u = unfrozen(mb, n0 + lane);
+      const uint32_t bal = __ballot_sync(0xffffffffu, u);
+      if (u) {
+        const int k = pos + __popc(bal & ((1u << lane) - 1u));
+        out[2 * (base[mb] + (k >> 1)) + (k & 1)] = mb * tiles_n + n0 + lane;
+      }
+      pos += __popc(bal);
+    }
+    if (lane == 0 && (pos & 1)) out[2 * (base[mb] + (pos >> 1)) + 1] = -1;
+  }
+}
+
 // ------------------------------------------------------------------ K6 (+K4 fused)
 struct AdamCoef {
   float step_size;  // lr / bc1
@@ -846,6 +893,13 @@ int launch_mask_to_pair_lists(const uint64_t* words, const UnitMatrix* mats, int
                               cudaStream_t s) {
   if (nmats <= 0) return PF_OK;
   launch_k(mask_to_pairs_kernel, dim3(nmats), dim3(kBlock), 0, s, words, mats, pairs, counts);
+  return status();
+}
+
+int launch_mask_to_rowpair_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* lists, int* counts,
+                                 cudaStream_t s) {
+  if (nmats <= 0) return PF_OK;
+  launch_k(mask_to_rowpairs_kernel, dim3(nmats), dim3(kBlock), 0, s, words, mats, lists, counts);
   return status();
 }
 

@@ -45,6 +45,17 @@ __host__ __device__ inline int pair_groups(int tiles_m, int tiles_n) {
 int launch_mask_to_pair_lists(const uint64_t* frozen_words, const UnitMatrix* mats_dev, int nmats, int* pairs,
                               int* counts, cudaStream_t s);
 
+// ---- K5r: the same mask -> per-matrix ROW-PAIR lists for gemm_dw_rowpairs (gemm_dw_rows.cu):
+// entries {u0, u1} of two unfrozen units of one unit row, in row-major order, a row with an
+// odd count ending {u, -1}; int2 entries at lists[pair_offset..] (ceil(count_r / 2) per row,
+// at most units + tiles_m ints); counts[matrix] = entries. tiles_m <= 4096.
+int launch_mask_to_rowpair_lists(const uint64_t* frozen_words, const UnitMatrix* mats_dev, int nmats, int* lists,
+                                 int* counts, cudaStream_t s);
+__host__ __device__ inline int pair_list_capacity(int tiles_m, int tiles_n) {
+  const int extra = pair_groups(tiles_m, tiles_n) > tiles_m ? pair_groups(tiles_m, tiles_n) : tiles_m;
+  return ((tiles_m * tiles_n + extra + 1) / 2) * 2;  // even: int2-aligned lists
+}
+
 // ---- K6: masked SGD over unit matrices, theta -= scale * G for units whose
 // stamp equals `stamp` (touched this step); optional fused APF (K4) update of
 // E / E_abs with delta = -scale * G (0 for untouched units) and a per-unit

@@ -66,6 +66,8 @@ struct DwGemm {
 int gemm_dw_units(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
 // CTA-pair 256 x 128 tiles over K5p pair lists (gemm_dw.cu; PF_DW_PAIR=1)
 int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
+// 1-CTA 128 x 256 tiles over K5r row-pair lists: two units of one row per MMA (gemm_dw_rows.cu)
+int gemm_dw_rowpairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
 
 // K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,

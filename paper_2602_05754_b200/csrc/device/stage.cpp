@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <string>
 
 namespace pf {
 
@@ -195,8 +196,7 @@ ParamSlice Stage::add_matrix(int rows, int cols, bool freezable) {
     m.tiles_n = (cols + 127) / 128;
     m.units = ((rows + 127) / 128) * m.tiles_n;
     m.pair_offset = pair_capacity_;
-    pair_capacity_ += m.units + pair_groups((rows + 127) / 128, m.tiles_n);
-    pair_capacity_ += pair_capacity_ & 1;  // each list starts 8-byte aligned (int2 pair loads)
+    pair_capacity_ += pair_list_capacity((rows + 127) / 128, m.tiles_n);  // even: lists stay int2-aligned
     total_units_ += m.units;
     p.unit_matrix = static_cast<int>(mats_.size());
     mats_.push_back(m);
@@ -233,9 +233,12 @@ void Stage::allocate_parameters(uint64_t seed) {
   grad_ = alloc_f32(n_params_);
   stamps_ = static_cast<int*>(alloc(static_cast<size_t>(total_units_) * 4));
   cudaMemset(stamps_, 0, static_cast<size_t>(total_units_) * 4);
-  const char* e = std::getenv("PF_DW_PAIR");
-  dw_pair_ = e && std::atoi(e) != 0;
-  unit_lists_ = static_cast<int*>(alloc(static_cast<size_t>((dw_pair_ ? pair_capacity_ : total_units_) + 64) * 4));
+  if (const char* e = std::getenv("PF_DW_KERNEL")) {
+    const std::string k(e);
+    dw_kernel_ = k == "units" ? DW_UNITS : k == "pairs" ? DW_CTA_PAIRS : DW_ROWPAIRS;
+  }
+  unit_lists_ = static_cast<int*>(
+      alloc(static_cast<size_t>((dw_kernel_ == DW_UNITS ? total_units_ : pair_capacity_) + 64) * 4));
   unit_counts_ = static_cast<int*>(alloc(static_cast<size_t>(mats_.size() + 1) * 4));
   mats_dev_ = static_cast<UnitMatrix*>(alloc(mats_.size() * sizeof(UnitMatrix)));
   cudaMemcpy(mats_dev_, mats_.data(), mats_.size() * sizeof(UnitMatrix), cudaMemcpyHostToDevice);
@@ -247,8 +250,11 @@ void Stage::allocate_parameters(uint64_t seed) {
 
 int Stage::build_unit_lists(const uint64_t* frozen_words, cudaStream_t s) {
   const int n = static_cast<int>(mats_.size());
-  return dw_pair_ ? launch_mask_to_pair_lists(frozen_words, mats_dev_, n, unit_lists_, unit_counts_, s)
-                  : launch_mask_to_unit_lists(frozen_words, mats_dev_, n, unit_lists_, unit_counts_, s);
+  switch (dw_kernel_) {
+    case DW_ROWPAIRS: return launch_mask_to_rowpair_lists(frozen_words, mats_dev_, n, unit_lists_, unit_counts_, s);
+    case DW_CTA_PAIRS: return launch_mask_to_pair_lists(frozen_words, mats_dev_, n, unit_lists_, unit_counts_, s);
+    default: return launch_mask_to_unit_lists(frozen_words, mats_dev_, n, unit_lists_, unit_counts_, s);
+  }
 }
 
 LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed, int device,
@@ -408,7 +414,7 @@ DwGemm Stage::dw_item(const ParamSlice& w, const __nv_bfloat16* dy, long long ld
   const UnitMatrix& m = mats_[static_cast<std::size_t>(w.unit_matrix)];
   // dW[out, in] (+)= dY^T . X over the unfrozen units; both operands MN-major (no transposes)
   return DwGemm{dy, ldy, x, ldx, grad_ + w.offset, w.cols, w.rows, w.cols, K,
-                unit_lists_ + (dw_pair_ ? m.pair_offset : m.unit_offset), unit_counts_ + w.unit_matrix,
+                unit_lists_ + (dw_kernel_ == DW_UNITS ? m.unit_offset : m.pair_offset), unit_counts_ + w.unit_matrix,
                 m.unit_offset};
 }
 

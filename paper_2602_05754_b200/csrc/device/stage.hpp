@@ -169,8 +169,12 @@ class Stage {
                  long long ldx, int K) const;
   // K3 over every item in one launch
   int run_dw(const std::vector<DwGemm>& items, int stamp, cudaStream_t s) {
-    return dw_pair_ ? gemm_dw_pairs(items.data(), static_cast<int>(items.size()), stamps_, stamp, s)
-                    : gemm_dw_units(items.data(), static_cast<int>(items.size()), stamps_, stamp, s);
+    const int n = static_cast<int>(items.size());
+    switch (dw_kernel_) {
+      case DW_ROWPAIRS: return gemm_dw_rowpairs(items.data(), n, stamps_, stamp, s);
+      case DW_CTA_PAIRS: return gemm_dw_pairs(items.data(), n, stamps_, stamp, s);
+      default: return gemm_dw_units(items.data(), n, stamps_, stamp, s);
+    }
   }
 
   ModelConfig cfg_;
@@ -192,10 +196,12 @@ class Stage {
   float* adam_v_ = nullptr;
   int* unit_steps_ = nullptr;
   int dense_steps_ = 0;
-  // K3 variant: 1-CTA 128 x 128 units over K5 lists (default), or CTA-pair 256 x 128 over
-  // K5p pair lists (PF_DW_PAIR=1; measured slower on B200, profiles/r1_dw_bench.txt)
-  bool dw_pair_ = false;
-  int* unit_lists_ = nullptr;  // K5 (row-major) or K5p (pair) lists
+  // K3 variant (PF_DW_KERNEL=units|pairs|rows): 1-CTA 128 x 256 tiles over K5r row pairs
+  // (default), 1-CTA 128 x 128 units over K5 lists, or CTA-pair 256 x 128 tiles over K5p
+  // column pairs (profiles/r1_dw_bench.txt)
+  enum DwKernel { DW_UNITS = 0, DW_CTA_PAIRS = 1, DW_ROWPAIRS = 2 };
+  int dw_kernel_ = DW_ROWPAIRS;
+  int* unit_lists_ = nullptr;  // K5 / K5p / K5r lists
   int* unit_counts_ = nullptr;
   int pair_capacity_ = 0;
   std::vector<void*> allocations_;

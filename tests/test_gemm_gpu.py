@@ -107,6 +107,52 @@ def test_gemm_dw_unit_list_accumulates(cuda):
         assert st[u] == (42 if u in {0, 5, 6, 11, 1, 2} else 0)
 
 
+@pytest.mark.parametrize("T,O,I", [(512, 384, 512), (320, 1000, 392), (1024, 4608, 384), (256, 256, 4608)])
+def test_gemm_dw_rowpairs_accumulates(cuda, T, O, I):
+    """Row-pair dW (128 x 256 MMA over two units of one row, a single 128 x 128 for an odd row):
+    first touch stores, later microbatches accumulate, untouched units keep stale data; O = 1000
+    has a partial row block, I = 392 a partial column block."""
+    import numpy as np
+    import torch
+
+    from test_kernels_gpu import rowpair_list_ref
+
+    lib, nat = _lib()
+    tm, tn = -(-O // 128), -(-I // 128)
+    U = tm * tn
+    g = torch.Generator(device="cpu").manual_seed(T + O + I + 1)
+    rng = np.random.default_rng(O + 1)
+    G = torch.full((O, I), 7.0, dtype=torch.float32, device=cuda)
+    stamps = torch.zeros(U, dtype=torch.int32, device=cuda)
+    expect = torch.full((O, I), 7.0, dtype=torch.float64)
+    stream = torch.cuda.current_stream().cuda_stream
+    seen = set()
+    for frac in (0.3, 0.55, 0.9, 0.0):
+        frozen = rng.random(U) < frac
+        ents = rowpair_list_ref(frozen, tm, tn)
+        units = [u for u in ents if u >= 0]
+        dY = torch.randn(T, O, generator=g).to(torch.bfloat16).cuda()
+        X = torch.randn(T, I, generator=g).to(torch.bfloat16).cuda()
+        el = torch.tensor(ents + [0, 0], dtype=torch.int32, device=cuda)
+        cnt = torch.tensor([len(ents) // 2], dtype=torch.int32, device=cuda)
+        rc = lib.pf_gemm_dw_rowpairs(dY.data_ptr(), dY.stride(0), X.data_ptr(), X.stride(0), G.data_ptr(),
+                                     G.stride(0), O, I, T, el.data_ptr(), cnt.data_ptr(), stamps.data_ptr(), 0, 42,
+                                     stream)
+        nat.check(rc, "pf_gemm_dw_rowpairs")
+        full = dY.double().cpu().t() @ X.double().cpu()
+        for u in units:
+            r, c = divmod(u, tn)
+            rs, cs = slice(r * 128, min(O, r * 128 + 128)), slice(c * 128, min(I, c * 128 + 128))
+            expect[rs, cs] = expect[rs, cs] + full[rs, cs] if u in seen else full[rs, cs]
+        seen |= set(units)
+    torch.cuda.synchronize()
+    err = (G.double().cpu() - expect).abs().max().item()
+    assert err <= 1e-3 * expect.abs().max().item()
+    st = stamps.cpu().tolist()
+    for u in range(U):
+        assert st[u] == (42 if u in seen else 0)
+
+
 @pytest.mark.parametrize("T,O,I", [(512, 384, 512), (320, 1000, 256), (1024, 4608, 384)])
 def test_gemm_dw_pairs_accumulates(cuda, T, O, I):
     """CTA-pair dW over K5p pair lists: first touch stores, later microbatches accumulate,

@@ -274,9 +274,19 @@ def _unit_table(shapes):
         tab[i] = (off, r, c, u, tn, units, po)
         off = (off + r * c + 63) // 64 * 64
         u += units
-        po += units + -(-tm // _pair_band(tm, tn)) * tn
-        po += po & 1
+        po += ((units + max(-(-tm // _pair_band(tm, tn)) * tn, tm) + 1) // 2) * 2  # pair_list_capacity
     return tab, off, u
+
+
+def rowpair_list_ref(frozen, tiles_m, tiles_n):
+    """K5r restated: per unit row, its unfrozen local unit ids paired in order, an odd row ending (u, -1)."""
+    out = []
+    for mb in range(tiles_m):
+        row = [mb * tiles_n + nb for nb in range(tiles_n) if not frozen[mb * tiles_n + nb]]
+        if len(row) % 2:
+            row.append(-1)
+        out += row
+    return out
 
 
 def pair_list_ref(frozen, tiles_m, tiles_n):
@@ -340,6 +350,35 @@ def test_mask_to_pair_lists_matches_numpy(cuda, ratio):
         expect = pair_list_ref(frozen[lo:lo + n], n // tn, tn)
         assert counts[i].item() == len(expect) and len(expect) % 2 == 0
         assert P[po:po + len(expect)].tolist() == expect
+
+
+@pytest.mark.parametrize("ratio", [0.0, 0.55, 0.8, 1.0])
+def test_mask_to_rowpair_lists_matches_numpy(cuda, ratio):
+    """K5r: row-major pairs of unfrozen units of one unit row; 64 and 112 column blocks span
+    several ballots; the LM-head shape has 1002 rows."""
+    import torch
+
+    from paper_2602_05754_b200 import pipefreeze as pf
+
+    tab, _, U = _unit_table([(384, 256), (256, 640), (1000, 128), (128, 128), (128256, 256), (2048, 8192),
+                             (4096, 14336)])
+    words = pf.sample_masks(11, U, [ratio])[0]
+    w = np.concatenate([words, np.zeros(1, dtype=np.uint64)])
+    wd = torch.tensor(w.view(np.int64), device=cuda)
+    td = torch.tensor(tab.view(np.uint8), device=cuda)
+    cap = int(tab["pair_offset"][-1]) + int(tab["units"][-1]) * 2 + 64
+    lists = torch.full((cap,), -7, dtype=torch.int32, device=cuda)
+    counts = torch.zeros(len(tab), dtype=torch.int32, device=cuda)
+    chk(lib().pf_mask_to_rowpair_lists(wd.data_ptr(), td.data_ptr(), len(tab), lists.data_ptr(), counts.data_ptr(),
+                                       sp()))
+    torch.cuda.synchronize()
+    frozen = pf.unpack_mask(words, U)
+    L = lists.cpu().numpy()
+    for i, ent in enumerate(tab):
+        lo, n, tn, po = int(ent["unit_offset"]), int(ent["units"]), int(ent["tiles_n"]), int(ent["pair_offset"])
+        expect = rowpair_list_ref(frozen[lo:lo + n], n // tn, tn)
+        assert counts[i].item() * 2 == len(expect)
+        assert L[po:po + len(expect)].tolist() == expect
 
 
 def test_masked_sgd_units_and_fused_apf(cuda):

@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2602_05754_b200 import _native  # noqa: E402
-from test_kernels_gpu import pair_list_ref  # noqa: E402
+from test_kernels_gpu import pair_list_ref, rowpair_list_ref  # noqa: E402
 
 lib = _native.device()
 
@@ -26,6 +26,7 @@ def bench(name, T, O, I, frac, iters=20):
     frozen[rng.permutation(U)[:int(frac * U)]] = True
     units = [u for u in range(U) if not frozen[u]]
     plist = pair_list_ref(frozen, tm, tn)
+    rlist = rowpair_list_ref(frozen, tm, tn)
     dY = torch.randn(T, O, device="cuda").to(torch.bfloat16)
     X = torch.randn(T, I, device="cuda").to(torch.bfloat16)
     G = torch.zeros(O, I, device="cuda")
@@ -34,6 +35,8 @@ def bench(name, T, O, I, frac, iters=20):
     uc = torch.tensor([len(units)], dtype=torch.int32, device="cuda")
     pl = torch.tensor(plist + [0], dtype=torch.int32, device="cuda")
     pc = torch.tensor([len(plist)], dtype=torch.int32, device="cuda")
+    rl = torch.tensor(rlist + [0, 0], dtype=torch.int32, device="cuda")
+    rc_ = torch.tensor([len(rlist) // 2], dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
 
@@ -45,8 +48,12 @@ def bench(name, T, O, I, frac, iters=20):
         return lib.pf_gemm_dw_pairs(dY.data_ptr(), dY.stride(0), X.data_ptr(), X.stride(0), G.data_ptr(), G.stride(0),
                                     O, I, T, pl.data_ptr(), pc.data_ptr(), st.data_ptr(), 0, k, s)
 
+    def rows(k):
+        return lib.pf_gemm_dw_rowpairs(dY.data_ptr(), dY.stride(0), X.data_ptr(), X.stride(0), G.data_ptr(),
+                                       G.stride(0), O, I, T, rl.data_ptr(), rc_.data_ptr(), st.data_ptr(), 0, k, s)
+
     out = []
-    for fn in (old, new):
+    for fn in (old, new, rows):
         for k in range(3):
             assert fn(k + 1) == 0
         tot = 0.0
@@ -62,8 +69,8 @@ def bench(name, T, O, I, frac, iters=20):
         out.append((2.0 * len(units) * 128 * 128 * T / (ms * 1e-3) / 1e12, ms))
     pad = sum(1 for u in plist if u < 0)
     print(f"{name:10s} {O}x{I} T={T} units {len(units)}/{U} pad {pad} | 1-CTA {out[0][0]:7.1f} TF/s "
-          f"({out[0][1]:.3f} ms) | pair {out[1][0]:7.1f} TF/s ({out[1][1]:.3f} ms) | x{out[0][1] / out[1][1]:.2f}",
-          flush=True)
+          f"({out[0][1]:.3f} ms) | CTA pair {out[1][0]:7.1f} TF/s ({out[1][1]:.3f} ms) | row pair {out[2][0]:7.1f} "
+          f"TF/s ({out[2][1]:.3f} ms)", flush=True)
 
 
 if __name__ == "__main__":
