@@ -127,49 +127,80 @@ __global__ void __launch_bounds__(kBlock) mask_to_pairs_kernel(const uint64_t* _
 }
 
 // ------------------------------------------------------------------ K5r
-// One block per matrix; warp w walks unit rows w, w + 8, ...: a ballot over 32 column
-// blocks at a time finds the row's unfrozen units, which are paired in order (a row with
-// an odd count ends with {u, -1}). Pass 1 counts entries per row into shared memory, a
-// block scan gives each row its base, pass 2 writes the entries.
+// One block of 1024 threads per matrix, one thread per unit row: the row's frozen bits are
+// read 64 at a time (two words and a funnel shift), the unfrozen count goes to shared memory,
+// a block scan gives each row its entry base, and the thread then walks its row's unfrozen
+// units in order writing pairs (a row with an odd count ends with {u, -1}).
 constexpr int kRowPairRows = 4096;
-__global__ void __launch_bounds__(kBlock) mask_to_rowpairs_kernel(const uint64_t* __restrict__ words,
-                                                                  const UnitMatrix* __restrict__ mats,
-                                                                  int* __restrict__ lists, int* __restrict__ counts) {
+constexpr int kRowPairThreads = 1024;
+__device__ __forceinline__ uint64_t bits64(const uint64_t* __restrict__ words, long long start) {
+  const uint64_t w0 = words[start >> 6];
+  const int sh = static_cast<int>(start & 63);
+  return sh ? (w0 >> sh) | (words[(start >> 6) + 1] << (64 - sh)) : w0;  // buffer padded by one word
+}
+__global__ void __launch_bounds__(kRowPairThreads) mask_to_rowpairs_kernel(const uint64_t* __restrict__ words,
+                                                                           const UnitMatrix* __restrict__ mats,
+                                                                           int* __restrict__ lists,
+                                                                           int* __restrict__ counts) {
   pdl_begin();
   const UnitMatrix m = mats[blockIdx.x];
   __shared__ int base[kRowPairRows + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int warp_tot[kRowPairThreads / 32];
   const int tiles_n = m.tiles_n, tiles_m = m.units / m.tiles_n;
-  auto unfrozen = [&](int mb, int nb) -> bool {
-    if (nb >= tiles_n) return false;
-    const long long g = static_cast<long long>(m.unit_offset) + static_cast<long long>(mb) * tiles_n + nb;
-    return ((words[g >> 6] >> (g & 63)) & 1ull) == 0;
+  auto row_unfrozen = [&](int mb, int c0) -> uint64_t {  // unfrozen mask of columns [c0, c0 + 64)
+    const uint64_t f = bits64(words, static_cast<long long>(m.unit_offset) + static_cast<long long>(mb) * tiles_n + c0);
+    const int valid = tiles_n - c0;
+    return ~f & (valid >= 64 ? ~0ull : ((1ull << valid) - 1ull));
   };
-  for (int mb = warp; mb < tiles_m; mb += kBlock / 32) {
+  for (int mb = threadIdx.x; mb < tiles_m; mb += kRowPairThreads) {
     int cnt = 0;
-    for (int n0 = 0; n0 < tiles_n; n0 += 32) cnt += __popc(__ballot_sync(0xffffffffu, unfrozen(mb, n0 + lane)));
-    if (lane == 0) base[mb + 1] = (cnt + 1) >> 1;
+    for (int c0 = 0; c0 < tiles_n; c0 += 64) cnt += __popcll(row_unfrozen(mb, c0));
+    base[mb + 1] = (cnt + 1) >> 1;
   }
   __syncthreads();
+  // block-wide exclusive scan of base[1..tiles_m] (chunks of kRowPairThreads rows)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int carry = 0;
+  for (int r0 = 0; r0 < tiles_m; r0 += kRowPairThreads) {
+    const int r = r0 + threadIdx.x;
+    const int v = r < tiles_m ? base[r + 1] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += warp_tot[w];
+    int blk = 0;
+    for (int w = 0; w < kRowPairThreads / 32; ++w) blk += warp_tot[w];
+    __syncthreads();
+    if (r < tiles_m) base[r + 1] = carry + wbase + incl;
+    carry += blk;
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     base[0] = 0;
-    for (int mb = 0; mb < tiles_m; ++mb) base[mb + 1] += base[mb];
     counts[blockIdx.x] = base[tiles_m];
   }
   __syncthreads();
-  int* out = lists + m.pair_offset;
-  for (int mb = warp; mb < tiles_m; mb += kBlock / 32) {
-    int pos = 0;  // unfrozen units of this row seen so far
-    for (int n0 = 0; n0 < tiles_n; n0 += 32) {
-      const bool u = unfrozen(mb, n0 + lane);
-      const uint32_t bal = __ballot_sync(0xffffffffu, u);
-      if (u) {
-        const int k = pos + __popc(bal & ((1u << lane) - 1u));
-        out[2 * (base[mb] + (k >> 1)) + (k & 1)] = mb * tiles_n + n0 + lane;
+  int2* out = reinterpret_cast<int2*>(lists + m.pair_offset);
+  for (int mb = threadIdx.x; mb < tiles_m; mb += kRowPairThreads) {
+    int e = base[mb], pending = -1;
+    for (int c0 = 0; c0 < tiles_n; c0 += 64) {
+      for (uint64_t b = row_unfrozen(mb, c0); b; b &= b - 1) {
+        const int u = mb * tiles_n + c0 + __ffsll(static_cast<long long>(b)) - 1;
+        if (pending < 0) {
+          pending = u;
+        } else {
+          out[e++] = make_int2(pending, u);
+          pending = -1;
+        }
       }
-      pos += __popc(bal);
     }
-    if (lane == 0 && (pos & 1)) out[2 * (base[mb] + (pos >> 1)) + 1] = -1;
+    if (pending >= 0) out[e] = make_int2(pending, -1);
   }
 }
 
@@ -899,7 +930,7 @@ int launch_mask_to_pair_lists(const uint64_t* words, const UnitMatrix* mats, int
 int launch_mask_to_rowpair_lists(const uint64_t* words, const UnitMatrix* mats, int nmats, int* lists, int* counts,
                                  cudaStream_t s) {
   if (nmats <= 0) return PF_OK;
-  launch_k(mask_to_rowpairs_kernel, dim3(nmats), dim3(kBlock), 0, s, words, mats, lists, counts);
+  launch_k(mask_to_rowpairs_kernel, dim3(nmats), dim3(kRowPairThreads), 0, s, words, mats, lists, counts);
   return status();
 }
 
