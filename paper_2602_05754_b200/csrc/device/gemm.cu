@@ -479,6 +479,9 @@ int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int 
               int epi, int block_n, cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0) return PF_ERR_INVALID;
   if (block_n != 128 && block_n != 256) return PF_ERR_INVALID;
+  // the epilogue moves 16-byte vectors: output rows must be 16-byte aligned
+  const int esz = (epi == EPI_STORE_F32 || epi == EPI_ACC_F32) ? 4 : 2;
+  if ((C.ld * esz) % 16 != 0 || reinterpret_cast<uintptr_t>(C.ptr) % 16 != 0) return PF_ERR_INVALID;
   if (epi == EPI_ACC_F32 && (C.unit_stamp == nullptr || block_n != 128)) return PF_ERR_INVALID;
   GemmParams<1> p{};
   p.nprob = 1;

@@ -887,6 +887,11 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
                    int epi, cudaStream_t stream) {
   constexpr int BN = 256;
   if (M <= 0 || N <= 0 || K <= 0 || (K % 8) != 0 || A.mn_major) return PF_ERR_INVALID;
+  // the epilogues move 16-byte vectors: output and residual rows must be 16-byte aligned
+  const int esz = epi == EPI_STORE_F32 ? 4 : 2;
+  if ((C.ld * esz) % 16 != 0 || reinterpret_cast<uintptr_t>(C.ptr) % 16 != 0 ||
+      (C.residual && ((C.ldr * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(C.residual) % 16 != 0)))
+    return PF_ERR_INVALID;
   Params2 p{};
   int rc = tma_desc_bf16_2d(&p.ta, A.ptr, M, K, A.ld, 64, 128);
   if (rc) return rc;
@@ -962,9 +967,9 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     p.epoch = ++st.epoch;
   }
   if ((epi == EPI_STORE_BF16 || epi == EPI_ADD_BF16) && !p.streamk && N % 32 == 0 && tma_plain_epi()) {
-    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
-    if (epi == EPI_ADD_BF16 && (rc = tma_desc_bf16_2d_sw64(&p.te_in, p.R, M, N, p.ldr, 32, 128))) return rc;
-    p.tma_epi = 1;
+    // TMA needs 16-byte aligned bases and row strides; otherwise the row-per-thread epilogue runs
+    p.tma_epi = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128) == PF_OK &&
+                (epi != EPI_ADD_BF16 || tma_desc_bf16_2d_sw64(&p.te_in, p.R, M, N, p.ldr, 32, 128) == PF_OK);
   }
   const bool bmn = B.mn_major;
   switch (epi) {

@@ -198,6 +198,33 @@ def test_gemm_dw_pairs_accumulates(cuda, T, O, I):
         assert st[u] == (42 if u in seen else 0)
 
 
+@pytest.mark.parametrize("pad", [0, 4, 8])
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_cta_pair_strided_c(cuda, pad, epi):
+    """C with row stride N + pad through the TMA-staged epilogue (pad 0, 8) equals the fp32 reference
+    and leaves the padding columns alone; rows that are not 16-byte aligned (pad 4) are rejected
+    with PF_ERR_INVALID before any launch."""
+    import torch
+
+    lib, nat = _lib()
+    M, N, K = 512, 768, 256
+    g = torch.Generator(device="cpu").manual_seed(pad * 10 + epi)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16).cuda()
+    base = torch.randn(M, N + pad, generator=g).to(torch.bfloat16).cuda()
+    C = base.clone()
+    rc = lib.pf_gemm_bf16(A.data_ptr(), 0, K, B.data_ptr(), 0, K, C.data_ptr(), N + pad, M, N, K, 1.0, epi, 512,
+                          None, 0, torch.cuda.current_stream().cuda_stream)
+    if pad % 8:
+        assert rc == 4  # PF_ERR_INVALID
+        return
+    nat.check(rc, "pf_gemm_bf16")
+    torch.cuda.synchronize()
+    ref = _ref(A, 0, B, 0) + (base[:, :N].float() if epi == 1 else 0)
+    assert (C[:, :N].float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-2
+    assert torch.equal(C[:, N:], base[:, N:])  # padding columns untouched
+
+
 @pytest.mark.parametrize("b_mn", [0, 1])
 @pytest.mark.parametrize("epi", [0, 1, 3])
 @pytest.mark.parametrize("M,N,K", [(256, 512, 320), (512, 768, 1024), (296, 392, 200), (1024, 2048, 512)])
