@@ -104,6 +104,141 @@ __global__ void __launch_bounds__(kBlock) layernorm_bwd_kernel(const __nv_bfloat
   }
 }
 
+// Row-in-registers LayerNorm for h = 256 * CH: one warp per row, lane holds columns
+// lane*8 + 256 j; mean and variance from the registers, x read from HBM once.
+template <int CH>
+__global__ void __launch_bounds__(kBlock) layernorm_fwd_reg_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const __nv_bfloat16* __restrict__ g,
+                                                                   const __nv_bfloat16* __restrict__ b,
+                                                                   __nv_bfloat16* __restrict__ y,
+                                                                   float* __restrict__ mean_out,
+                                                                   float* __restrict__ rstd_out, int T, float eps) {
+  pdl_begin();
+  constexpr int H = 256 * CH;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nw) {
+    const long long off = static_cast<long long>(t) * H + lane * 8;
+    float f[CH][8];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) load8(x + off + 256 * j, f[j]);
+    float sm = 0.f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sm += f[j][i];
+    const float mu = warp_sum(sm) / H;
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += (f[j][i] - mu) * (f[j][i] - mu);
+    const float r = rsqrtf(warp_sum(ss) / H + eps);
+    if (lane == 0) {
+      mean_out[t] = mu;
+      rstd_out[t] = r;
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      float gg[8], bb[8], o[8];
+      load8(g + lane * 8 + 256 * j, gg);
+      load8(b + lane * 8 + 256 * j, bb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (f[j][i] - mu) * r * gg[i] + bb[i];
+      store8(y + off + 256 * j, o);
+    }
+  }
+}
+
+// Fused LayerNorm backward for h = 256 * CH, one pass over x and dy:
+//   dx = residual + rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat))
+//   dg += sum_t dy * xhat,  db += sum_t dy,  dsum += sum_t dx   (dsum: the bias gradient of the
+//   linear layer whose output gradient dx is; nullptr skips it)
+// Per-lane register partials, summed over the block's warps in shared memory, added to the
+// fp32 gradients with float4 atomics (one per 4 columns per block).
+template <int CH>
+__global__ void __launch_bounds__(kBlock, 1) layernorm_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ residual,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ dg, float* __restrict__ db, float* __restrict__ dsum, int T) {
+  pdl_begin();
+  constexpr int H = 256 * CH;
+  constexpr int NW = kBlock / 32;
+  extern __shared__ float red[];  // [3][NW][H]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float ag[CH * 8], ab[CH * 8], as[CH * 8];
+#pragma unroll
+  for (int i = 0; i < CH * 8; ++i) ag[i] = ab[i] = as[i] = 0.f;
+  for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {
+    const long long off = static_cast<long long>(t) * H + lane * 8;
+    const float mu = mean[t], r = rstd[t];
+    float xv[CH][8], dv[CH][8];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      load8(x + off + 256 * j, xv[j]);
+      load8(dy + off + 256 * j, dv[j]);
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      float gv[8];
+      load8(g + lane * 8 + 256 * j, gv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float gd = gv[i] * dv[j][i];
+        s1 += gd;
+        s2 += gd * (xv[j][i] - mu) * r;
+      }
+    }
+    const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      float gv[8], out[8];
+      load8(g + lane * 8 + 256 * j, gv);
+      if (residual) load8(residual + off + 256 * j, out);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (xv[j][i] - mu) * r;
+        out[i] = (residual ? out[i] : 0.f) + r * (gv[i] * dv[j][i] - m1 - xh * m2);
+        ag[8 * j + i] += dv[j][i] * xh;
+        ab[8 * j + i] += dv[j][i];
+      }
+      store8(dx + off + 256 * j, out);
+      if (dsum) {  // the bias gradient sums the stored (bf16-rounded) dx, as a column reduction of dx would
+#pragma unroll
+        for (int i = 0; i < 8; ++i) as[8 * j + i] += __bfloat162float(__float2bfloat16_rn(out[i]));
+      }
+    }
+  }
+  auto park = [&](const float (&acc)[CH * 8], int a) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      float* slot = red + (a * NW + warp) * H + lane * 8 + 256 * j;
+      reinterpret_cast<float4*>(slot)[0] = make_float4(acc[8 * j], acc[8 * j + 1], acc[8 * j + 2], acc[8 * j + 3]);
+      reinterpret_cast<float4*>(slot)[1] =
+          make_float4(acc[8 * j + 4], acc[8 * j + 5], acc[8 * j + 6], acc[8 * j + 7]);
+    }
+  };
+  auto flush = [&](float* outp, int a) {
+    for (int c = threadIdx.x * 4; c < H; c += kBlock * 4) {
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const float4 v = *reinterpret_cast<const float4*>(red + (a * NW + w) * H + c);
+        sum = make_float4(sum.x + v.x, sum.y + v.y, sum.z + v.z, sum.w + v.w);
+      }
+      atomicAdd(reinterpret_cast<float4*>(outp + c), sum);
+    }
+  };
+  if (dg) park(ag, 0);
+  if (db) park(ab, 1);
+  if (dsum) park(as, 2);
+  __syncthreads();
+  if (dg) flush(dg, 0);
+  if (db) flush(db, 1);
+  if (dsum) flush(dsum, 2);
+}
+
 // Column reductions over T rows (block = 32 column groups of 8 x 8 row lanes):
 //   dg[c] += sum_t dy[t,c] * (x[t,c] - mean[t]) * rstd[t]   (when x != nullptr)
 //   db[c] += sum_t dy[t,c]
@@ -313,21 +448,57 @@ void column_grid(int T, int n, int* col_blocks, int* row_chunks, int* rows_per_b
 int launch_layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
                          float* mean, float* rstd, int T, int h, float eps, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
-  launch_k(layernorm_fwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, h, eps);
+  const dim3 grid(grid_for((T + 7) / 8));
+  switch (h) {
+    case 256: launch_k(layernorm_fwd_reg_kernel<1>, grid, dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, eps); return status();
+    case 512: launch_k(layernorm_fwd_reg_kernel<2>, grid, dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, eps); return status();
+    case 1024: launch_k(layernorm_fwd_reg_kernel<4>, grid, dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, eps); return status();
+    default: break;
+  }
+  launch_k(layernorm_fwd_kernel, grid, dim3(kBlock), 0, s, x, g, b, y, mean, rstd, T, h, eps);
   return status();
 }
 
+namespace {
+template <int CH>
+int launch_layernorm_bwd_fused(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* mean, const float* rstd,
+                               const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
+                               float* db, float* dsum, int T, cudaStream_t s) {
+  constexpr int smem = 3 * (kBlock / 32) * 256 * CH * 4;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(layernorm_bwd_fused_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return PF_ERR_CUDA;
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(num_sms(), (T + 7) / 8));
+  launch_k(layernorm_bwd_fused_kernel<CH>, dim3(grid), dim3(kBlock), smem, s, x, g, mean, rstd, dy, residual, dx, dg,
+           db, dsum, T);
+  return status();
+}
+}  // namespace
+
 int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* mean, const float* rstd,
                          const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
-                         float* db, int T, int h, cudaStream_t s) {
+                         float* db, float* dsum, int T, int h, cudaStream_t s) {
   if (h % 8) return PF_ERR_INVALID;
+  switch (h) {
+    case 256: return launch_layernorm_bwd_fused<1>(x, g, mean, rstd, dy, residual, dx, dg, db, dsum, T, s);
+    case 512: return launch_layernorm_bwd_fused<2>(x, g, mean, rstd, dy, residual, dx, dg, db, dsum, T, s);
+    case 1024: return launch_layernorm_bwd_fused<4>(x, g, mean, rstd, dy, residual, dx, dg, db, dsum, T, s);
+    default: break;
+  }
   launch_k(layernorm_bwd_kernel, dim3(grid_for((T + 7) / 8)), dim3(kBlock), 0, s, x, g, mean, rstd, dy, residual, dx, T, h);
   int rc = status();
-  if (rc != PF_OK || (!dg && !db)) return rc;
-  int cb, rcn, rpb;
-  column_grid(T, h, &cb, &rcn, &rpb);
-  launch_k(column_reduce_kernel, dim3(dim3(cb, rcn)), dim3(kBlock), 0, s, dy, h, x, mean, rstd, dg, db, T, h, rpb);
-  return status();
+  if (rc == PF_OK && (dg || db)) {
+    int cb, rcn, rpb;
+    column_grid(T, h, &cb, &rcn, &rpb);
+    launch_k(column_reduce_kernel, dim3(dim3(cb, rcn)), dim3(kBlock), 0, s, dy, h, x, mean, rstd, dg, db, T, h, rpb);
+    rc = status();
+  }
+  if (rc == PF_OK && dsum) rc = launch_bias_grad(dx, h, dsum, T, h, s);
+  return rc;
 }
 
 int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, int n, cudaStream_t s) {

@@ -12,9 +12,11 @@ namespace pf {
 int launch_layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const __nv_bfloat16* b, __nv_bfloat16* y,
                          float* mean, float* rstd, int T, int h, float eps, cudaStream_t s);
 // dx = residual + LayerNorm backward; dg += sum dy * xhat, db += sum dy (either may be nullptr)
+// dsum (may be nullptr): += column sums of the bf16 dx (the bias gradient of the linear layer
+// whose output gradient dx is), computed in the same pass on the fused path (h = 256, 512, 1024)
 int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* mean, const float* rstd,
                          const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
-                         float* db, int T, int h, cudaStream_t s);
+                         float* db, float* dsum, int T, int h, cudaStream_t s);
 // db[c] += sum_t dy[t, c] (bias gradient of a linear layer)
 int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, int n, cudaStream_t s);
 // act = GELU(pre) (erf form); dpre = dact * GELU'(pre)

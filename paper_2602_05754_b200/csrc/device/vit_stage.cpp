@@ -249,7 +249,7 @@ class VitStage final : public Stage {
     if (spec_.last) {
       PF_TRY(launch_bias_grad(sl.logits, cfg_.vocab, g(headb_), B_, cfg_.vocab, s));
       PF_TRY(gemm_dx(sl.logits, cfg_.vocab, w(head_), h, d_hc_, h, Mh_, h, cfg_.vocab, EPI_STORE_BF16, s));
-      PF_TRY(launch_layernorm_bwd(sl.xc, w(lnfg_), sl.muc, sl.rc, d_hc_, nullptr, d_xc_, g(lnfg_), g(lnfb_), B_, h,
+      PF_TRY(launch_layernorm_bwd(sl.xc, w(lnfg_), sl.muc, sl.rc, d_hc_, nullptr, d_xc_, g(lnfg_), g(lnfb_), nullptr, B_, h,
                                   s));
       PF_TRY(launch_scatter_rows(d_xc_, top, B_, S_, h, s));
       dcur = top;
@@ -267,13 +267,16 @@ class VitStage final : public Stage {
       __nv_bfloat16* dx2 = L.dx2;
       __nv_bfloat16* dqkv = L.qkv;  // qkv is dead after the attention backward
       // MLP
-      PF_TRY(launch_bias_grad(dcur, h, g(P.b2), T_, h, s));
+      // b2's gradient: the column sums of this layer's output gradient (the layer above's
+      // LayerNorm-1 backward produced them in the same pass, except for the top layer)
+      if (li == nl - 1) PF_TRY(launch_bias_grad(dcur, h, g(P.b2), T_, h, s));
       PF_TRY(gemm_dx_dgelu(dcur, h, w(P.w2), ffn, L.pre, d_act_, dpre, T_, ffn, h, s));
       PF_TRY(launch_bias_grad(dpre, ffn, g(P.b1), T_, ffn, s));
       PF_TRY(gemm_dx(dpre, ffn, w(P.w1), h, d_h_, h, T_, h, ffn, EPI_STORE_BF16, s));
-      PF_TRY(launch_layernorm_bwd(L.x2, w(P.ln2g), L.mu2, L.r2, d_h_, dcur, dx2, g(P.ln2g), g(P.ln2b), T_, h, s));
+      // LayerNorm-2 backward; bo's gradient (column sums of dx2) in the same pass
+      PF_TRY(launch_layernorm_bwd(L.x2, w(P.ln2g), L.mu2, L.r2, d_h_, dcur, dx2, g(P.ln2g), g(P.ln2b), g(P.bo), T_, h,
+                                  s));
       // attention
-      PF_TRY(launch_bias_grad(dx2, h, g(P.bo), T_, h, s));
       PF_TRY(gemm_dx(dx2, h, w(P.wo), h, d_attn_, h, T_, h, h, EPI_STORE_BF16, s));
       AttnGrads ag{};
       PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ag, s));
@@ -289,7 +292,11 @@ class VitStage final : public Stage {
       if (li > 0) out = sl.layers[static_cast<std::size_t>(li - 1)].dy;
       else out = spec_.first ? d_tmp_ : dx_out;
       if (!out) return PF_ERR_INVALID;
-      PF_TRY(launch_layernorm_bwd(L.x, w(P.ln1g), L.mu1, L.r1, d_h_, dx2, out, g(P.ln1g), g(P.ln1b), T_, h, s));
+      // LayerNorm-1 backward; its output is the layer below's output gradient, whose column sums
+      // are that layer's b2 gradient
+      float* b2_below = li > 0 ? g(layers_[static_cast<std::size_t>(li - 1)].b2) : nullptr;
+      PF_TRY(launch_layernorm_bwd(L.x, w(P.ln1g), L.mu1, L.r1, d_h_, dx2, out, g(P.ln1g), g(P.ln1b), b2_below, T_, h,
+                                  s));
       attn_release_keep_out(L.attn);
       dcur = out;
     }
