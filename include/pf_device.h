@@ -80,8 +80,8 @@ int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream);         
 int pf_gelu_bwd(const void* pre, const void* dact, void* dpre, long long n, void* stream); /* dpre = dact * gelu'(pre) */
 int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, const void* bias, void* pre, void* act,
                  int T, int ffn, int K, void* stream);
-int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre, int T,
-                  int ffn, int K, void* stream);
+int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre,
+                  float* db, int T, int ffn, int K, void* stream);  /* db (nullable): += column sums of dpre */
 
 /* Stream-K split of the CTA-pair GEMM: 0 off (default), 1 split every tile, 2 data-parallel
  * full waves + the last wave split over all CTA pairs, -1 auto (mode 2 when the last wave would

@@ -91,12 +91,13 @@ int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, co
                                    1.0f, pf::EPI_GELU, static_cast<cudaStream_t>(stream)));
 }
 
-int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre, int T,
-                  int ffn, int K, void* stream) {
+int pf_gemm_dgelu(const void* dY, long long ldy, const void* W2, long long ldw, const void* pre, void* dpre,
+                  float* db, int T, int ffn, int K, void* stream) {
   if (!dY || !W2 || !pre || !dpre || ffn % 32 != 0) return PF_ERR_INVALID;
   pf::GemmOut c{dpre, ffn};
   c.residual = pre;
   c.ldr = ffn;
+  c.colsum = db;
   return record(pf::gemm_bf16_pair(pf::GemmOperand{dY, ldy, false}, pf::GemmOperand{W2, ldw, true}, c, T, ffn, K,
                                    1.0f, pf::EPI_DGELU, static_cast<cudaStream_t>(stream)));
 }

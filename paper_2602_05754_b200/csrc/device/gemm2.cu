@@ -94,6 +94,7 @@ struct alignas(64) Params2 {
   __nv_bfloat16* aux;  // EPI_SWIGLU activation output
   long long ldaux;
   const __nv_bfloat16* bias;  // EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (nullptr: none)
+  float* colsum;              // EPI_DGELU: += column sums of d(pre) (the fc1 bias gradient; nullptr: none)
   int streamk;   // 0: one tile per work item; 1/2: stream-K (2: data-parallel full waves first)
   int dp_tiles;  // stream-K: tiles [0, dp_tiles) run whole, round-robin over the clusters
   long long sk_q;  // stream-K: iterations of the split region per cluster
@@ -584,6 +585,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
+          if (EPI == EPI_DGELU && p.colsum != nullptr) {
+            // column sums of the chunk's 128 x 32 d(pre) box: warp w (0..7) owns columns 4w..4w+3,
+            // lane l rows l, l+32, l+64, l+96; one atomic per column per CTA and chunk. Rows past M
+            // were loaded as zeros (TMA fill), so they add nothing.
+            const int wq = warp - 2;
+            float cs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+              const int rw = static_cast<int>(lane) + 32 * rr;
+              const int col0 = 4 * wq;  // 4 consecutive columns = 8 bytes inside one 16-byte chunk
+              const int off = rw * 64 + (((col0 >> 3) ^ ((rw >> 1) & 3)) << 4) + (col0 & 7) * 2;
+              const uint2 v = *reinterpret_cast<const uint2*>(buf + off);
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+              cs[0] += a.x;
+              cs[1] += a.y;
+              cs[2] += b.x;
+              cs[3] += b.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cs[i] = warp_sum_f(cs[i]);
+            const int gcol = tn * BN + c * 32 + 4 * wq;
+            const float mine = lane == 0 ? cs[0] : lane == 1 ? cs[1] : lane == 2 ? cs[2] : cs[3];
+            if (lane < 4 && gcol + static_cast<int>(lane) < p.N) atomicAdd(p.colsum + gcol + lane, mine);
+            named_bar_sync(1, kEpiThreads);  // the buffer is refilled below only after every warp read it
+          }
           if (elected) {
             if constexpr (EPI == EPI_GELU) {
               tma_store_2d(&p.te_in, buf, tn * BN + c * 32, y0);
@@ -911,6 +938,8 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.ptr, M, N, C.ld, 32, 128))) return rc;
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.aux, M, N, C.ldaux, 32, 128))) return rc;
   }
+  p.colsum = C.colsum;
+  if (C.colsum && epi != EPI_DGELU) return PF_ERR_INVALID;
   if (epi == EPI_DGELU) {  // pre [M][N] in, d(pre) [M][N] out by TMA (may be the same buffer)
     if (N % 32 != 0 || !B.mn_major || !C.residual || C.bias) return PF_ERR_INVALID;
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.residual, M, N, C.ldr, 32, 128))) return rc;

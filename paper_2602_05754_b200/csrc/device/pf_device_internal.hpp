@@ -36,6 +36,7 @@ struct GemmOut {
   void* aux = nullptr;  // EPI_SWIGLU: [M][N/2] bf16 activation
   long long ldaux = 0;
   const void* bias = nullptr;  // CTA-pair EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (bf16 [N])
+  float* colsum = nullptr;     // CTA-pair EPI_DGELU: += column sums of the bf16 output (a bias gradient)
 };
 
 int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,

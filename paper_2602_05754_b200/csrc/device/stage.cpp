@@ -163,17 +163,20 @@ int gemm_fwd_bias_gelu(const __nv_bfloat16* A, long long lda, const __nv_bfloat1
 }
 
 int gemm_dx_dgelu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw,
-                  const __nv_bfloat16* pre, __nv_bfloat16* d_act, __nv_bfloat16* dpre, int M, int N, int K,
+                  const __nv_bfloat16* pre, __nv_bfloat16* d_act, __nv_bfloat16* dpre, float* db, int M, int N, int K,
                   cudaStream_t s) {
   if (use_pair() && fuse_swiglu() && M >= 256 && N >= 256 && N % 32 == 0) {
     GemmOut out{dpre, N};
     out.residual = pre;
     out.ldr = N;
+    out.colsum = db;
     return gemm_bf16_pair(GemmOperand{dY, ldy, false}, GemmOperand{W, ldw, true}, out, M, N, K, 1.0f, EPI_DGELU,
                           s);
   }
-  const int rc = gemm_dx(dY, ldy, W, ldw, d_act, N, M, N, K, EPI_STORE_BF16, s);
-  return rc ? rc : launch_gelu_bwd(pre, d_act, dpre, static_cast<long long>(M) * N, s);
+  int rc = gemm_dx(dY, ldy, W, ldw, d_act, N, M, N, K, EPI_STORE_BF16, s);
+  if (!rc) rc = launch_gelu_bwd(pre, d_act, dpre, static_cast<long long>(M) * N, s);
+  if (!rc && db) rc = launch_bias_grad(dpre, N, db, M, N, s);
+  return rc;
 }
 
 }  // namespace ops

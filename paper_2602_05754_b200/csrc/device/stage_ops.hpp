@@ -29,8 +29,9 @@ int gemm_fwd_resid_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat
 int gemm_fwd_bias_gelu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
                        const __nv_bfloat16* bias, __nv_bfloat16* pre, __nv_bfloat16* act, int M, int N, int K,
                        cudaStream_t s);
+// db (may be nullptr) += column sums of dpre (the fc1 bias gradient), in the epilogue when fused
 int gemm_dx_dgelu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw,
-                  const __nv_bfloat16* pre, __nv_bfloat16* d_act, __nv_bfloat16* dpre, int M, int N, int K,
+                  const __nv_bfloat16* pre, __nv_bfloat16* d_act, __nv_bfloat16* dpre, float* db, int M, int N, int K,
                   cudaStream_t s);
 // dX[M=T, N=in] = dY[T, K=out] . W[out, in]   (W read MN-major, no transpose)
 int gemm_dx(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16* W, long long ldw, void* C, long long ldc,

@@ -270,8 +270,8 @@ class VitStage final : public Stage {
       // b2's gradient: the column sums of this layer's output gradient (the layer above's
       // LayerNorm-1 backward produced them in the same pass, except for the top layer)
       if (li == nl - 1) PF_TRY(launch_bias_grad(dcur, h, g(P.b2), T_, h, s));
-      PF_TRY(gemm_dx_dgelu(dcur, h, w(P.w2), ffn, L.pre, d_act_, dpre, T_, ffn, h, s));
-      PF_TRY(launch_bias_grad(dpre, ffn, g(P.b1), T_, ffn, s));
+      // fc2 dX with GELU' and b1's gradient (column sums of dpre) in the epilogue
+      PF_TRY(gemm_dx_dgelu(dcur, h, w(P.w2), ffn, L.pre, d_act_, dpre, g(P.b1), T_, ffn, h, s));
       PF_TRY(gemm_dx(dpre, ffn, w(P.w1), h, d_h_, h, T_, h, ffn, EPI_STORE_BF16, s));
       // LayerNorm-2 backward; bo's gradient (column sums of dx2) in the same pass
       PF_TRY(launch_layernorm_bwd(L.x2, w(P.ln2g), L.mu2, L.r2, d_h_, dcur, dx2, g(P.ln2g), g(P.ln2b), g(P.bo), T_, h,

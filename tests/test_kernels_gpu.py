@@ -151,18 +151,22 @@ def test_gemm_gelu_epilogues_match_unfused(cuda, T, ffn, D):
     assert (act.float() - a32).abs().max().item() <= 2e-2 * a32.abs().max().item()
     # backward: dpre = bf16(dy . W2) * gelu'(pre); out of place, then in place over a copy of pre
     dpre = torch.empty_like(pre)
-    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, pre.data_ptr(), dpre.data_ptr(), T, ffn, D, sp()))
+    db = torch.full((ffn,), 0.5, device=cuda)
+    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, pre.data_ptr(), dpre.data_ptr(), db.data_ptr(), T,
+                            ffn, D, sp()))
     da = torch.empty_like(pre)
     chk(lib().pf_gemm_bf16(dy.data_ptr(), 0, D, w2.data_ptr(), 1, ffn, da.data_ptr(), ffn, T, ffn, D, 1.0, 0, 512,
                            None, 0, sp()))
     dpre_ref = torch.empty_like(pre)
     chk(lib().pf_gelu_bwd(pre.data_ptr(), da.data_ptr(), dpre_ref.data_ptr(), T * ffn, sp()))
     inplace = pre.clone()
-    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, inplace.data_ptr(), inplace.data_ptr(), T, ffn, D,
-                            sp()))
+    chk(lib().pf_gemm_dgelu(dy.data_ptr(), D, w2.data_ptr(), ffn, inplace.data_ptr(), inplace.data_ptr(), None, T, ffn,
+                            D, sp()))
     torch.cuda.synchronize()
     assert torch.equal(dpre, dpre_ref)
     assert torch.equal(inplace, dpre_ref)
+    colsum = dpre_ref.float().sum(0) + 0.5  # db accumulates into its buffer
+    assert torch.allclose(db, colsum, rtol=1e-4, atol=1e-3 * colsum.abs().max().item())
 
 
 @pytest.mark.parametrize("T,ffn,D", [(512, 768, 256), (4096, 2048, 1024)])
