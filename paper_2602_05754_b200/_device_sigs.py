@@ -51,6 +51,7 @@ DEVICE_SIGNATURES = {
     "pf_gemm_set_streamk": ([c_int], c_int),
     "pf_gelu_fwd": ([c_vp, c_vp, c_ll, c_vp], c_int),
     "pf_gelu_bwd": ([c_vp, c_vp, c_vp, c_ll, c_vp], c_int),
+    "pf_gemm_rope": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_gemm_gelu": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp], c_int),
     "pf_gemm_dgelu": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_vp], c_int),
     "pf_gemm_dswiglu": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_vp, c_int, c_int, c_int, c_vp], c_int),

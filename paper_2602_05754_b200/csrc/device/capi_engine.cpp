@@ -7,6 +7,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "pf_device_internal.hpp"
 #include "vit_kernels.cuh"
 #include "pf_device.h"
 #include "trainer.hpp"
@@ -156,6 +157,28 @@ int pf_rope_fwd(void* qkv, int T, int seq, int nh, int nkv, int hd, float theta,
       return PF_ERR_CUDA;
     int rc = pf::launch_rope_table(cs, seq, hd, theta, S(stream));
     if (rc == PF_OK) rc = pf::launch_rope_fwd(static_cast<__nv_bfloat16*>(qkv), cs, T, seq, nh, nkv, hd, S(stream));
+    cudaFreeAsync(cs, S(stream));
+    return rc;
+  });
+}
+
+int pf_gemm_rope(const void* h, long long ldh, const void* Wqkv, long long ldw, void* qkv, int T, int seq, int nh,
+                 int nkv, int hd, int K, float theta, void* stream) {
+  return guard([&] {
+    if (!h || !Wqkv || !qkv || hd != 64) return static_cast<int>(PF_ERR_INVALID);
+    float2* cs = nullptr;
+    if (cudaMallocAsync(&cs, static_cast<size_t>(seq) * (hd / 2) * sizeof(float2), S(stream)) != cudaSuccess)
+      return static_cast<int>(PF_ERR_CUDA);
+    int rc = pf::launch_rope_table(cs, seq, hd, theta, S(stream));
+    const int N = (nh + 2 * nkv) * hd;
+    if (rc == PF_OK) {
+      pf::GemmOut out{qkv, N};
+      out.rope = cs;
+      out.rope_seq = seq;
+      out.rope_cols = (nh + nkv) * hd;
+      rc = pf::gemm_bf16_pair(pf::GemmOperand{h, ldh, false}, pf::GemmOperand{Wqkv, ldw, false}, out, T, N, K, 1.0f,
+                              pf::EPI_ROPE, S(stream));
+    }
     cudaFreeAsync(cs, S(stream));
     return rc;
   });

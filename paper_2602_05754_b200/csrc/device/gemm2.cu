@@ -57,14 +57,15 @@ struct Cfg2 {
   // EPI_DSWIGLU gate|up of one 32-column chunk (in by TMA, overwritten by d(gate)|d(up), out by
   // TMA: 16 KB); EPI_SWIGLU gate|up|act of one chunk (out by TMA: 24 KB).
   // EPI_STORE_BF16 / EPI_ADD_BF16: two 8 KB buffers (one 128 x 32 box of C, R read in place).
-  static constexpr bool TMA_EPI = EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU || EPI == EPI_GELU || EPI == EPI_DGELU;
+  static constexpr bool TMA_EPI =
+      EPI == EPI_DSWIGLU || EPI == EPI_SWIGLU || EPI == EPI_GELU || EPI == EPI_DGELU || EPI == EPI_ROPE;
   static constexpr bool TMA_PLAIN = EPI == EPI_STORE_BF16 || EPI == EPI_ADD_BF16;
   static constexpr int STAGES = TMA_EPI ? 5 : 6;
   static constexpr int A_BYTES = 128 * BK * 2;       // this CTA's half of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BUF =
-      EPI == EPI_SWIGLU ? 3 * 8192 : ((EPI == EPI_DSWIGLU || EPI == EPI_GELU) ? 2 * 8192 : 8192);
+      EPI == EPI_SWIGLU ? 3 * 8192 : ((EPI == EPI_DSWIGLU || EPI == EPI_GELU || EPI == EPI_ROPE) ? 2 * 8192 : 8192);
   static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? 2 * EPI_BUF : 0;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
@@ -95,6 +96,8 @@ struct alignas(64) Params2 {
   long long ldaux;
   const __nv_bfloat16* bias;  // EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (nullptr: none)
   float* colsum;              // EPI_DGELU: += column sums of d(pre) (the fc1 bias gradient; nullptr: none)
+  const float2* rope;         // EPI_ROPE: (cos, sin) [seq][32]
+  int rope_seq, rope_cols;
   int streamk;   // 0: one tile per work item; 1/2: stream-K (2: data-parallel full waves first)
   int dp_tiles;  // stream-K: tiles [0, dp_tiles) run whole, round-robin over the clusters
   long long sk_q;  // stream-K: iterations of the split region per cluster
@@ -503,6 +506,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (EPI == EPI_ADD_BF16 && !park) fetch_r(half);
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
+      if constexpr (EPI == EPI_ROPE) {
+        // qkv projection with rotate-half RoPE (head_dim 64): per head of the tile, the thread of
+        // (row, half) holds j in [16 half, 16 half + 16) and its partner j + 32, rotates them with
+        // the (cos, sin) of the row's position (q and k heads only) and writes the two 128 x 32
+        // boxes of the head into buffer hh & 1, stored by TMA (= GEMM then rope_fwd_kernel).
+        const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
+        const bool elected = threadIdx.x == 64;
+        const float2* cs = p.rope + static_cast<long long>(grow % p.rope_seq) * 32 + half * 16;
+#pragma unroll 1
+        for (int hh = 0; hh < BN / 64; ++hh) {
+          uint32_t ra[16], rb[16];
+          const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                              static_cast<uint32_t>(abuf * BN + hh * 64 + half * 16);
+          uint8_t* buf = sE + (hh & 1) * Cfg::EPI_BUF;
+          if (hh == 0) {
+            mbar_wait(&tfull_bar[abuf], aphase);
+            tc_fence_after();
+          }
+          tmem_ld_32x32b_x16(tb, ra);
+          tmem_ld_32x32b_x16(tb + 32, rb);
+          if (elected) bulk_wait_read1();  // the stores of head hh - 2 (this buffer) have read it
+          named_bar_sync(1, kEpiThreads);
+          tmem_ld_wait();
+          const bool rot = tn * BN + hh * 64 < p.rope_cols;
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) {
+            const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
+            uint32_t aw[4], bw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const __nv_bfloat162 a2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(ra[8 * s2 + 2 * i]),
+                                                              p.alpha * __uint_as_float(ra[8 * s2 + 2 * i + 1]));
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(p.alpha * __uint_as_float(rb[8 * s2 + 2 * i]),
+                                                              p.alpha * __uint_as_float(rb[8 * s2 + 2 * i + 1]));
+              if (rot) {
+                const float2 a = __bfloat1622float2(a2), b = __bfloat1622float2(b2);
+                float oa0, ob0, oa1, ob1;
+                rope_rotate(a.x, b.x, __ldg(cs + 8 * s2 + 2 * i), oa0, ob0);
+                rope_rotate(a.y, b.y, __ldg(cs + 8 * s2 + 2 * i + 1), oa1, ob1);
+                aw[i] = pack_bf16x2(oa0, oa1);
+                bw[i] = pack_bf16x2(ob0, ob1);
+              } else {
+                aw[i] = *reinterpret_cast<const uint32_t*>(&a2);
+                bw[i] = *reinterpret_cast<const uint32_t*>(&b2);
+              }
+            }
+            *reinterpret_cast<uint4*>(buf + off) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
+            *reinterpret_cast<uint4*>(buf + 8192 + off) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, kEpiThreads);
+          if (elected) {
+            tma_store_2d(&p.te_out, buf, tn * BN + hh * 64, y0);
+            tma_store_2d(&p.te_out, buf + 8192, tn * BN + hh * 64 + 32, y0);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+        continue;
+      }
       if constexpr (EPI == EPI_GELU || EPI == EPI_DGELU) {
         // ViT MLP, per 32-column chunk staged in buffer c & 1 (128 x 32 SWIZZLE_64B boxes):
         //   EPI_GELU:  pre = bf16(alpha acc + bias), act = gelu(pre); both boxes stored by TMA
@@ -933,6 +999,13 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.ldaux = C.ldaux;
   p.bias = static_cast<const __nv_bfloat16*>(C.bias);
   if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16 && epi != EPI_GELU) return PF_ERR_INVALID;
+  if (epi == EPI_ROPE) {  // qkv [M][N] out by TMA, q/k heads of 64 columns rotated
+    if (N % BN != 0 || B.mn_major || !C.rope || C.rope_seq <= 0 || C.rope_cols % 64 != 0) return PF_ERR_INVALID;
+    if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
+    p.rope = static_cast<const float2*>(C.rope);
+    p.rope_seq = C.rope_seq;
+    p.rope_cols = C.rope_cols;
+  }
   if (epi == EPI_GELU) {  // pre [M][N] and act [M][N] out by TMA
     if (N % 32 != 0 || B.mn_major || !C.aux) return PF_ERR_INVALID;
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_in, C.ptr, M, N, C.ld, 32, 128))) return rc;
@@ -973,7 +1046,8 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   const double eff = static_cast<double>(ntiles) / (static_cast<double>(waves) * max_clusters);
   const int mode = streamk_mode();
   const int active = std::min(max_clusters, max_active_clusters<BN, false, EPI_STORE_BF16>());
-  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && epi != EPI_GELU && epi != EPI_DGELU && ntiles > active && num_kb >= 8 &&
+  const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && epi != EPI_GELU && epi != EPI_DGELU && epi != EPI_ROPE &&
+                  ntiles > active && num_kb >= 8 &&
                   (mode == 1 || mode == 2 || (mode < 0 && eff < 0.92));
   if (sk) {
     StreamKState& st = sk_state();
@@ -1017,6 +1091,8 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
       return launch2<BN, true, EPI_DSWIGLU>(p, clusters, stream);
     case EPI_GELU:
       return launch2<BN, false, EPI_GELU>(p, clusters, stream);
+    case EPI_ROPE:
+      return launch2<BN, false, EPI_ROPE>(p, clusters, stream);
     case EPI_DGELU:
       return launch2<BN, true, EPI_DGELU>(p, clusters, stream);
     default: return PF_ERR_INVALID;

@@ -671,11 +671,7 @@ __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* _
   load8(p + j, a);
   load8(p + j + half, b);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float2 cc = c[i];
-    oa[i] = a[i] * cc.x - b[i] * cc.y;
-    ob[i] = b[i] * cc.x + a[i] * cc.y;
-  }
+  for (int i = 0; i < 8; ++i) rope_rotate(a[i], b[i], c[i], oa[i], ob[i]);
   store8(p + j, oa);
   store8(p + j + half, ob);
 }

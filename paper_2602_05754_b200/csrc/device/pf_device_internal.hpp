@@ -17,6 +17,7 @@ enum GemmEpilogue : int {
   EPI_DSWIGLU = 5,     // CTA pair only: acc = d(act) [M][ffn]; residual = gu; C = d(gate|up), same layout as gu
   EPI_GELU = 6,        // CTA pair only: C = pre = bf16(acc + bias), aux = gelu(pre)      (ViT fc1)
   EPI_DGELU = 7,       // CTA pair only: acc = d(act); residual = pre; C = d(act) * gelu'(pre) (ViT fc2 dX)
+  EPI_ROPE = 8,        // CTA pair only: C = qkv with rotate-half RoPE on the q and k heads (head_dim 64)
 };
 
 struct GemmOperand {
@@ -37,6 +38,9 @@ struct GemmOut {
   long long ldaux = 0;
   const void* bias = nullptr;  // CTA-pair EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (bf16 [N])
   float* colsum = nullptr;     // CTA-pair EPI_DGELU: += column sums of the bf16 output (a bias gradient)
+  const void* rope = nullptr;  // CTA-pair EPI_ROPE: float2 (cos, sin) table [seq][32]
+  int rope_seq = 0;            // EPI_ROPE: positions per sequence (row t is position t % seq)
+  int rope_cols = 0;           // EPI_ROPE: columns [0, rope_cols) are q and k heads (rotated)
 };
 
 int gemm_bf16(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K,

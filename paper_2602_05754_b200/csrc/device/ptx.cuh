@@ -274,6 +274,13 @@ __device__ __forceinline__ uint4 ldg_nc_l2_256(const void* p) {
   return v;
 }
 
+// Rotate-half RoPE of one (x_j, x_{j+hd/2}) pair with (cos, sin): rounded products, no FMA
+// contraction, so rope_fwd_kernel and the fused qkv epilogue agree bit for bit.
+__device__ __forceinline__ void rope_rotate(float a, float b, float2 cs, float& oa, float& ob) {
+  oa = __fsub_rn(__fmul_rn(a, cs.x), __fmul_rn(b, cs.y));
+  ob = __fadd_rn(__fmul_rn(b, cs.x), __fmul_rn(a, cs.y));
+}
+
 // GELU (erf form) and its derivative; shared by the ViT GELU kernels and the fused GEMM
 // epilogues so they agree bit for bit.
 __device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }

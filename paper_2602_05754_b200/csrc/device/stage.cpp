@@ -148,6 +148,24 @@ int gemm_dx_dswiglu(const __nv_bfloat16* dY, long long ldy, const __nv_bfloat16*
   return rc ? rc : launch_swiglu_bwd(gu, d_act, dgu, M, ffn, s);
 }
 
+int gemm_fwd_rope(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* qkv,
+                  const float2* rope, int M, int seq, int nh, int nkv, int hd, int K, cudaStream_t s) {
+  static const bool fuse = [] {
+    const char* e = std::getenv("PF_FUSE_ROPE");
+    return !(e && e[0] == '0');
+  }();
+  const int N = (nh + 2 * nkv) * hd;
+  if (use_pair() && fuse_swiglu() && fuse && hd == 64 && M >= 256 && N % 256 == 0) {
+    GemmOut out{qkv, N};
+    out.rope = rope;
+    out.rope_seq = seq;
+    out.rope_cols = (nh + nkv) * hd;
+    return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, N, K, 1.0f, EPI_ROPE, s);
+  }
+  const int rc = gemm_fwd(A, lda, W, ldw, qkv, N, M, N, K, EPI_STORE_BF16, s);
+  return rc ? rc : launch_rope_fwd(qkv, rope, M, seq, nh, nkv, hd, s);
+}
+
 int gemm_fwd_bias_gelu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
                        const __nv_bfloat16* bias, __nv_bfloat16* pre, __nv_bfloat16* act, int M, int N, int K,
                        cudaStream_t s) {
@@ -374,9 +392,8 @@ int LlamaStage::forward(int slot, int microbatch, const int* tokens, const int* 
     SavedLayer& L = sl.layers[static_cast<std::size_t>(li)];
     const LayerParams& P = layers_[static_cast<std::size_t>(li)];
     PF_TRY(launch_rmsnorm_fwd(L.x, weights_ + P.g1.offset, L.h1, L.rstd1, T, h, cfg_.norm_eps, s));
-    PF_TRY(gemm_fwd(L.h1, h, weights_ + P.wqkv.offset, h, L.qkv, cfg_.qkv_dim(), T, cfg_.qkv_dim(), h,
-                    EPI_STORE_BF16, s));
-    PF_TRY(launch_rope_fwd(L.qkv, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
+    PF_TRY(gemm_fwd_rope(L.h1, h, weights_ + P.wqkv.offset, h, L.qkv, rope_, T, cfg_.seq, cfg_.n_heads,
+                         cfg_.n_kv_heads, cfg_.head_dim, h, s));
     void* ao = nullptr;
     long long ald = 0;
     PF_TRY(attn_fwd(L.attn, L.qkv, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, scale,

@@ -24,6 +24,10 @@ int gemm_fwd_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W,
 int gemm_fwd_resid_bias(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,
                         __nv_bfloat16* C, const __nv_bfloat16* R, long long ld, const __nv_bfloat16* bias, int M,
                         int N, int K, cudaStream_t s);
+// qkv = A . Wqkv^T with rotate-half RoPE on the q and k heads (fused in the CTA-pair epilogue when
+// head_dim == 64, else GEMM + rope_fwd_kernel)
+int gemm_fwd_rope(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw, __nv_bfloat16* qkv,
+                  const float2* rope, int M, int seq, int nh, int nkv, int hd, int K, cudaStream_t s);
 // ViT MLP: pre = A . W1^T + bias and act = gelu(pre) (GELU fused in the CTA-pair epilogue);
 // dpre = (dY . W2) * gelu'(pre), dpre may alias pre (d_act scratch only on the unfused path)
 int gemm_fwd_bias_gelu(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W, long long ldw,

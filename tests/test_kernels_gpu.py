@@ -117,6 +117,31 @@ def test_gemm_swiglu_epilogue_matches_unfused(cuda):
     assert torch.equal(a, a_ref)
 
 
+@pytest.mark.parametrize("T,S,nh,nkv,D", [(4096, 2048, 32, 8, 2048), (512, 128, 4, 4, 256), (300, 100, 6, 1, 256)])
+def test_gemm_rope_epilogue_matches_unfused(cuda, T, S, nh, nkv, D):
+    """qkv projection with RoPE fused in the pair-GEMM epilogue == GEMM then rope_fwd, bit for bit
+    (GQA widths; T = 300 leaves a partial row tile, S = 100 several sequences per microbatch)."""
+    import torch
+
+    hd = 64
+    N = (nh + 2 * nkv) * hd
+    g = torch.Generator().manual_seed(T + nh)
+    x = bf(torch.randn(T, D, generator=g)).cuda()
+    w = bf(torch.randn(N, D, generator=g) * 0.1).cuda()
+    qkv = torch.empty(T, N, dtype=torch.bfloat16, device=cuda)
+    rc = lib().pf_gemm_rope(x.data_ptr(), D, w.data_ptr(), D, qkv.data_ptr(), T, S, nh, nkv, hd, D, 500000.0, sp())
+    if N % 256:
+        assert rc == 4  # the fused epilogue needs whole 256-column tiles (the stage then runs GEMM + rope)
+        return
+    chk(rc)
+    ref = torch.empty_like(qkv)
+    chk(lib().pf_gemm_bf16(x.data_ptr(), 0, D, w.data_ptr(), 0, D, ref.data_ptr(), N, T, N, D, 1.0, 0, 512, None, 0,
+                           sp()))
+    chk(lib().pf_rope_fwd(ref.data_ptr(), T, S, nh, nkv, hd, 500000.0, sp()))
+    torch.cuda.synchronize()
+    assert torch.equal(qkv, ref)
+
+
 @pytest.mark.parametrize("T,ffn,D", [(512, 768, 256), (3200, 4096, 1024)])
 def test_gemm_gelu_epilogues_match_unfused(cuda, T, ffn, D):
     """ViT MLP: GELU fused in the pair-GEMM epilogues == GEMM then gelu_fwd / gelu_bwd, bit for bit
