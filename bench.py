@@ -178,7 +178,7 @@ def run_reference(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    shape = PRESETS[args.model]
+    shape = model_shape(args)
     M = args.microbatches
     S = args.gpus
     units = _units_for(shape, S)
@@ -204,6 +204,17 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def model_shape(args):
+    """The preset of --model, with --layers overriding the layer count (a per-rank slice of a
+    pipeline that does not fit one GPU, e.g. LLaMA-13B's 5 layers per rank at PP=8)."""
+    import dataclasses
+
+    from paper_2602_05754_b200.engine import PRESETS
+
+    shape = PRESETS[args.model]
+    return dataclasses.replace(shape, layers=args.layers) if args.layers else shape
+
+
 def _units_for(shape, S: int) -> int:
     from paper_2602_05754_b200.engine import param_layout
 
@@ -213,6 +224,8 @@ def _units_for(shape, S: int) -> int:
 def _config(args, shape) -> dict:
     cfg_idx = {"llama-1b": 1, "llama-8b": 2, "llama-13b": 3, "vit-l-32": 4}.get(args.model)
     tag = f"BASELINE configs[{cfg_idx}] shapes" if cfg_idx is not None else "test shapes"
+    if getattr(args, "layers", 0):
+        tag += f", {args.layers}-layer slice"
     return {"workload": f"{args.model}-shaped {args.schedule} PP={args.gpus} ({tag})",
             "model": args.model, "hidden": shape.hidden, "layers": shape.layers, "ffn": shape.ffn,
             "heads": shape.n_heads, "kv_heads": shape.n_kv_heads, "vocab": shape.vocab,
@@ -246,7 +259,7 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl")
-    shape = PRESETS[args.model]
+    shape = model_shape(args)
     M = args.microbatches
     phases = tuple(args.phases)
     C = stages_per_rank(args)
@@ -395,6 +408,8 @@ def main() -> None:
                     choices=["gpipe", "1f1b", "interleaved-1f1b", "zbv", "zbv-split"])
     ap.add_argument("--chunks", type=int, default=2, help="virtual stages per GPU for interleaved-1f1b")
     ap.add_argument("--microbatches", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=0,
+                    help="override the preset's layer count (a per-rank slice of a larger pipeline)")
     ap.add_argument("--r-max", type=float, default=0.8)
     ap.add_argument("--phases", type=int, nargs=4, default=[2, 8, 10, 10000])
     ap.add_argument("--seed", type=int, default=42)
