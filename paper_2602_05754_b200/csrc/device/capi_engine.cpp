@@ -184,6 +184,23 @@ int pf_gemm_rope(const void* h, long long ldh, const void* Wqkv, long long ldw, 
   });
 }
 
+int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, int nh, int hd, float scale,
+                    void* stream) {
+  return guard([&] {
+    return pf::launch_vit_attn_fwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out), lse, B,
+                                   seq, nh, hd, scale, S(stream));
+  });
+}
+
+int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B,
+                    int seq, int nh, int hd, float scale, void* stream) {
+  return guard([&] {
+    return pf::launch_vit_attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(out),
+                                   static_cast<const __nv_bfloat16*>(dout), lse, static_cast<__nv_bfloat16*>(dqkv), B,
+                                   seq, nh, hd, scale, S(stream));
+  });
+}
+
 int pf_cross_entropy(void* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,
                      float loss_scale, void* stream) {
   return guard([&] {

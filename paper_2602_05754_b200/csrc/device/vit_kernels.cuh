@@ -18,6 +18,14 @@ int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const f
                          const __nv_bfloat16* dy, const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg,
                          float* db, float* dsum, int T, int h, cudaStream_t s);
 // db[c] += sum_t dy[t, c] (bias gradient of a linear layer)
+// Bidirectional attention for S <= 64, head_dim 64 (vit_attention.cu): qkv packed [B S, 3 nh 64],
+// out [B S, nh 64], lse fp32 [B][nh][S]; the backward writes dq|dk|dv packed into dqkv (may alias qkv).
+int launch_vit_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int nh, int hd,
+                        float scale, cudaStream_t s);
+int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                        const float* lse, __nv_bfloat16* dqkv, int B, int S, int nh, int hd, float scale,
+                        cudaStream_t s);
+
 int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, int n, cudaStream_t s);
 // act = GELU(pre) (erf form); dpre = dact * GELU'(pre)
 int launch_gelu_fwd(const __nv_bfloat16* pre, __nv_bfloat16* act, long long n, cudaStream_t s);

@@ -15,6 +15,8 @@
 #include "stage.hpp"
 #include "stage_ops.hpp"
 #include "vit_kernels.cuh"
+#include <string>
+#include <cstdlib>
 
 namespace pf {
 
@@ -44,6 +46,8 @@ struct VitSavedLayer {
   AttnState* attn = nullptr;
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
+  __nv_bfloat16* ao = nullptr;  // short-sequence attention output [T, h] (vit_attention.cu)
+  float* lse = nullptr;         // and its row log-sum-exp [B][nh][S]
   __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;  // kept from B to W
   const __nv_bfloat16* dy_w = nullptr;          // the output gradient W reads (dy or the incoming buffer)
 };
@@ -70,6 +74,10 @@ class VitStage final : public Stage {
     S_ = cfg.seq;
     np_ = S_ - 1;
     T_ = cfg.tokens();
+    // short sequences (ViT-L/32: 50 tokens) use the per-(image, head) kernel; PF_VIT_ATTN=cudnn
+    // (or S > 64, head_dim != 64) takes the generic fused attention
+    const char* ae = std::getenv("PF_VIT_ATTN");
+    own_attn_ = S_ <= 64 && cfg.head_dim == 64 && !(ae && std::string(ae) == "cudnn");
     Mh_ = (B_ + 127) / 128 * 128;
     const int nl = spec.layer_end - spec.layer_begin;
     layers_.resize(static_cast<std::size_t>(nl));
@@ -144,6 +152,10 @@ class VitStage final : public Stage {
         L.mu2 = alloc_f32(T);
         L.r2 = alloc_f32(T);
         L.attn = attn_state_new();
+        if (own_attn_) {
+          L.ao = alloc_bf16(T * h);
+          L.lse = alloc_f32(static_cast<long long>(B_) * cfg.n_heads * S_);
+        }
         L.dy = alloc_bf16(T * h);
         L.dx2 = alloc_bf16(T * h);
       }
@@ -203,11 +215,17 @@ class VitStage final : public Stage {
       const VitLayerParams& P = layers_[static_cast<std::size_t>(li)];
       PF_TRY(launch_layernorm_fwd(L.x, w(P.ln1g), w(P.ln1b), L.h1, L.mu1, L.r1, T_, h, cfg_.norm_eps, s));
       PF_TRY(gemm_fwd_bias(L.h1, h, w(P.wqkv), h, L.qkv, 3LL * h, w(P.bqkv), T_, 3 * h, h, s));
-      void* ao = nullptr;
-      long long ald = 0;
-      PF_TRY(attn_fwd(L.attn, L.qkv, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ao, &ald, s, false));
-      L.attn_out = static_cast<const __nv_bfloat16*>(ao);
-      L.attn_ld = ald;
+      if (own_attn_) {
+        PF_TRY(launch_vit_attn_fwd(L.qkv, L.ao, L.lse, B_, S_, cfg_.n_heads, cfg_.head_dim, scale, s));
+        L.attn_out = L.ao;
+        L.attn_ld = h;
+      } else {
+        void* ao = nullptr;
+        long long ald = 0;
+        PF_TRY(attn_fwd(L.attn, L.qkv, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ao, &ald, s, false));
+        L.attn_out = static_cast<const __nv_bfloat16*>(ao);
+        L.attn_ld = ald;
+      }
       PF_TRY(gemm_fwd_resid_bias(L.attn_out, L.attn_ld, w(P.wo), h, L.x2, L.x, h, w(P.bo), T_, h, h, s));
       PF_TRY(launch_layernorm_fwd(L.x2, w(P.ln2g), w(P.ln2b), L.h2, L.mu2, L.r2, T_, h, cfg_.norm_eps, s));
       // MLP up-projection with bias and GELU fused in the epilogue; the bench.py roofline probe
@@ -278,9 +296,11 @@ class VitStage final : public Stage {
                                   s));
       // attention
       PF_TRY(gemm_dx(dx2, h, w(P.wo), h, d_attn_, h, T_, h, h, EPI_STORE_BF16, s));
-      AttnGrads ag{};
-      PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ag, s));
-      {
+      if (own_attn_) {  // dq|dk|dv straight into the packed dqkv (over qkv)
+        PF_TRY(launch_vit_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, dqkv, B_, S_, cfg_.n_heads, cfg_.head_dim, scale, s));
+      } else {
+        AttnGrads ag{};
+        PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ag, s));
         AttnGradView gv{static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
                         static_cast<const __nv_bfloat16*>(ag.dv), ag.q_b, ag.q_t, ag.q_h, ag.k_b, ag.k_t, ag.k_h,
                         ag.v_b, ag.v_t, ag.v_h, ag.rep};
@@ -343,6 +363,7 @@ class VitStage final : public Stage {
 
   uint64_t seed_;
   int B_ = 0, S_ = 0, np_ = 0, T_ = 0, Mh_ = 0;
+  bool own_attn_ = false;
   std::vector<VitLayerParams> layers_;
   ParamSlice patch_w_, patch_b_, cls_, pos_, head_, headb_, lnfg_, lnfb_;
   float2* ident_ = nullptr;

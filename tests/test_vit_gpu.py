@@ -108,3 +108,44 @@ def test_vit_controller_plan_and_training(cuda):
     assert p is not None and p["ratios"].mean() <= 0.8 + 1e-6
     assert np.mean(losses[-3:]) < np.mean(losses[:3])
     tr.close()
+
+
+@pytest.mark.parametrize("B,S,nh", [(4, 50, 16), (3, 64, 2), (5, 10, 4), (2, 1, 3)])
+def test_short_sequence_attention_vs_torch(cuda, B, S, nh):
+    """Per-(image, head) attention kernels vs torch fp32 softmax attention: O, LSE and the packed
+    dq|dk|dv (also written in place over qkv)."""
+    import math
+
+    import torch
+
+    from paper_2602_05754_b200 import _native
+
+    lib = _native.device()
+    hd = 64
+    g = torch.Generator().manual_seed(B * 100 + S)
+    qkv = torch.randn(B * S, 3 * nh * hd, generator=g).to(torch.bfloat16).cuda()
+    dout = torch.randn(B * S, nh * hd, generator=g).to(torch.bfloat16).cuda()
+    out = torch.empty(B * S, nh * hd, dtype=torch.bfloat16, device=cuda)
+    lse = torch.empty(B * nh * S, device=cuda)
+    scale = 1.0 / math.sqrt(hd)
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.pf_vit_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), B, S, nh, hd, scale, st), "fwd")
+    dqkv = torch.empty_like(qkv)
+    _native.check(lib.pf_vit_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
+                                      B, S, nh, hd, scale, st), "bwd")
+    inplace = qkv.clone()
+    _native.check(lib.pf_vit_attn_bwd(inplace.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                      inplace.data_ptr(), B, S, nh, hd, scale, st), "bwd in place")
+    torch.cuda.synchronize()
+    x = qkv.float().view(B, S, 3, nh, hd).permute(2, 0, 3, 1, 4)  # [3, B, nh, S, hd]
+    q, k, v = (t.clone().requires_grad_(True) for t in x)
+    sc = q @ k.transpose(-1, -2) * scale
+    ref_lse = torch.logsumexp(sc, -1)
+    o = torch.softmax(sc, -1) @ v
+    o.backward(dout.float().view(B, S, nh, hd).permute(0, 2, 1, 3))
+    o_ref = o.permute(0, 2, 1, 3).reshape(B * S, nh * hd)
+    assert (out.float() - o_ref).abs().max().item() <= 2e-2 * o_ref.abs().max().item()
+    assert torch.allclose(lse.view(B, nh, S), ref_lse, atol=2e-2, rtol=1e-2)
+    grads = torch.stack([q.grad, k.grad, v.grad]).permute(1, 3, 0, 2, 4).reshape(B * S, 3 * nh * hd)
+    assert (dqkv.float() - grads).abs().max().item() <= 3e-2 * grads.abs().max().item()
+    assert torch.equal(inplace, dqkv)
