@@ -513,7 +513,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // boxes of the head into buffer hh & 1, stored by TMA (= GEMM then rope_fwd_kernel).
         const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
         const bool elected = threadIdx.x == 64;
-        const float2* cs = p.rope + static_cast<long long>(grow % p.rope_seq) * 32 + half * 16;
+        // (cos, sin) of this row's position for j in [16 half, 16 half + 16): the same for every
+        // head of the tile, loaded once (as float4 pairs) while the MMAs still run
+        float2 csr[16];
+        {
+          const float4* c4 = reinterpret_cast<const float4*>(p.rope + static_cast<long long>(grow % p.rope_seq) * 32 +
+                                                             half * 16);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 v = __ldg(c4 + i);
+            csr[2 * i] = make_float2(v.x, v.y);
+            csr[2 * i + 1] = make_float2(v.z, v.w);
+          }
+        }
 #pragma unroll 1
         for (int hh = 0; hh < BN / 64; ++hh) {
           uint32_t ra[16], rb[16];
@@ -543,8 +555,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (rot) {
                 const float2 a = __bfloat1622float2(a2), b = __bfloat1622float2(b2);
                 float oa0, ob0, oa1, ob1;
-                rope_rotate(a.x, b.x, __ldg(cs + 8 * s2 + 2 * i), oa0, ob0);
-                rope_rotate(a.y, b.y, __ldg(cs + 8 * s2 + 2 * i + 1), oa1, ob1);
+                rope_rotate(a.x, b.x, csr[8 * s2 + 2 * i], oa0, ob0);
+                rope_rotate(a.y, b.y, csr[8 * s2 + 2 * i + 1], oa1, ob1);
                 aw[i] = pack_bf16x2(oa0, oa1);
                 bw[i] = pack_bf16x2(ob0, ob1);
               } else {
