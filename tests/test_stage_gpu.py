@@ -16,10 +16,13 @@ def _expand_unit_mask(frozen_bits: np.ndarray, ent: dict) -> np.ndarray:
     return np.kron(upd, np.ones((128, 128), dtype=np.float32))[:r, :c]
 
 
-@pytest.mark.parametrize("override", [0.0, 0.5])
-def test_stage_step_matches_torch_reference(cuda, override):
+@pytest.mark.parametrize("override,dw", [(0.0, "rows"), (0.5, "rows"), (0.5, "units"), (0.5, "pairs")])
+def test_stage_step_matches_torch_reference(cuda, override, dw, monkeypatch):
+    """One stage step vs an fp32 torch restatement on the same bf16 weights and masks, with each
+    masked-dW kernel (row pairs: the default; 1-CTA units; CTA-pair column pairs)."""
     import torch
 
+    monkeypatch.setenv("PF_DW_KERNEL", dw)
     from gpu_util import device_view
     from llama_ref import stage_loss, unflatten
     from paper_2602_05754_b200 import pipefreeze as pf
