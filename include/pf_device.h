@@ -78,10 +78,11 @@ int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw
  *                alias pre. ffn % 32 == 0. */
 /* Bidirectional attention for S <= 64 and head_dim 64 (ViT-L/32), one CTA per (image, head):
  * qkv packed [B S, 3 nh 64], out [B S, nh 64], lse fp32 [B][nh][S]; the backward writes dq|dk|dv
- * into a packed dqkv (may alias qkv). */
+ * into a packed dqkv (may alias qkv) and, when dbias != NULL, adds the qkv bias gradient (the column sums
+ * of the bf16 dq|dk|dv, fp32 [3 nh 64]) into dbias. */
 int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int nh, int hd, float scale, void* stream);
-int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B, int S,
-                    int nh, int hd, float scale, void* stream);
+int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, float* dbias,
+                    int B, int S, int nh, int hd, float scale, void* stream);
 int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream);              /* act = gelu(pre), n % 8 == 0 */
 int pf_gelu_bwd(const void* pre, const void* dact, void* dpre, long long n, void* stream); /* dpre = dact * gelu'(pre) */
 int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, const void* bias, void* pre, void* act,

@@ -192,12 +192,12 @@ int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, int 
   });
 }
 
-int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B,
-                    int seq, int nh, int hd, float scale, void* stream) {
+int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, float* dbias,
+                    int B, int seq, int nh, int hd, float scale, void* stream) {
   return guard([&] {
     return pf::launch_vit_attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(out),
-                                   static_cast<const __nv_bfloat16*>(dout), lse, static_cast<__nv_bfloat16*>(dqkv), B,
-                                   seq, nh, hd, scale, S(stream));
+                                   static_cast<const __nv_bfloat16*>(dout), lse, static_cast<__nv_bfloat16*>(dqkv),
+                                   dbias, B, seq, nh, hd, scale, S(stream));
   });
 }
 

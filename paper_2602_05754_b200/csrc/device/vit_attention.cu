@@ -198,9 +198,10 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
                                                                 const __nv_bfloat16* __restrict__ out,
                                                                 const __nv_bfloat16* __restrict__ dout,
                                                                 const float* __restrict__ lse, __nv_bfloat16* dqkv,
-                                                                int S, int nh, float scale) {
+                                                                float* __restrict__ dbias, int S, int nh,
+                                                                float scale) {
   pdl_begin();
-  extern __shared__ __align__(16) uint8_t attn_smem[];  // 6 tiles of 64 x 72 bf16 (55 KB) + D
+  extern __shared__ __align__(16) uint8_t attn_smem[];  // 6 tiles of 64 x 72 bf16 (55 KB) + D + bias sums
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(attn_smem);
   __nv_bfloat16* Ks = Qs + kS * kLd;
   __nv_bfloat16* Vs = Ks + kS * kLd;
@@ -208,6 +209,28 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
   __nv_bfloat16* Ps = dOs + kS * kLd;
   __nv_bfloat16* dSs = Ps + kS * kLd;
   float* Dsum = reinterpret_cast<float*>(dSs + kS * kLd);
+  float* bsum = Dsum + kS;  // [4 warps][3 x 64]: per-warp column sums of the bf16 dq | dk | dv rows
+  // column sums over this warp's 16 rows of one 16 x 64 C-fragment block (values rounded to bf16,
+  // as a column reduction of the stored gradient would see them) -> bsum[warp][base + col]
+  auto colsum16 = [&](const float (&v)[8][4], int base, float mul, bool ok0, bool ok1) {
+    const int lane_ = threadIdx.x & 31;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      float c0 = (ok0 ? __bfloat162float(__float2bfloat16_rn(v[dt][0] * mul)) : 0.f) +
+                 (ok1 ? __bfloat162float(__float2bfloat16_rn(v[dt][2] * mul)) : 0.f);
+      float c1 = (ok0 ? __bfloat162float(__float2bfloat16_rn(v[dt][1] * mul)) : 0.f) +
+                 (ok1 ? __bfloat162float(__float2bfloat16_rn(v[dt][3] * mul)) : 0.f);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {  // sum over the 8 row groups (lanes with the same lane % 4)
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      }
+      if (lane_ < 4) {
+        bsum[(threadIdx.x >> 5) * 192 + base + dt * 8 + 2 * lane_] = c0;
+        bsum[(threadIdx.x >> 5) * 192 + base + dt * 8 + 2 * lane_ + 1] = c1;
+      }
+    }
+  };
   const int b = blockIdx.x / nh, h = blockIdx.x - b * nh;
   const long long row0 = static_cast<long long>(b) * S, ld = 3LL * nh * kD, ldo = static_cast<long long>(nh) * kD;
   load_tile(Qs, qkv, row0, ld, h * kD, S);
@@ -294,6 +317,7 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
         mma16816(dq[dt + 1], a0, a1, a2, a3, bb[2], bb[3]);
       }
     }
+    if (dbias) colsum16(dq, 0, scale, q0 < S, q1 < S);
     __syncthreads();  // every warp's P / dS rows are in shared memory; Q, K, V, dO reads are done
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
@@ -328,6 +352,16 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
       }
     }
     const int k0 = r0 + g, k1 = r0 + g + 8;
+    if (dbias) {
+      colsum16(dk, 64, scale, k0 < S, k1 < S);
+      colsum16(dv, 128, 1.f, k0 < S, k1 < S);
+      __syncthreads();
+      // bqkv gradient: q | k | v columns of head h sit at h*64, (nh + h)*64, (2 nh + h)*64
+      for (int c = threadIdx.x; c < 192; c += kThreads) {
+        const float v = bsum[c] + bsum[192 + c] + bsum[384 + c] + bsum[576 + c];
+        atomicAdd(dbias + (c / 64) * nh * kD + h * kD + (c % 64), v);
+      }
+    }
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
       const int ck = (nh + h) * kD + dt * 8 + c2, cv = (2 * nh + h) * kD + dt * 8 + c2;
@@ -353,17 +387,17 @@ int launch_vit_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse
 }
 
 int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
-                        const float* lse, __nv_bfloat16* dqkv, int B, int S, int nh, int hd, float scale,
+                        const float* lse, __nv_bfloat16* dqkv, float* dbias, int B, int S, int nh, int hd, float scale,
                         cudaStream_t s) {
   if (S < 1 || S > kS || hd != kD || B < 1 || nh < 1) return PF_ERR_INVALID;
-  constexpr int smem = 6 * kS * kLd * 2 + kS * 4;
+  constexpr int smem = 6 * kS * kLd * 2 + kS * 4 + 4 * 192 * 4;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(vit_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return PF_ERR_CUDA;
     attr = true;
   }
-  launch_k(vit_attn_bwd_kernel, dim3(B * nh), dim3(kThreads), smem, s, qkv, out, dout, lse, dqkv, S, nh, scale);
+  launch_k(vit_attn_bwd_kernel, dim3(B * nh), dim3(kThreads), smem, s, qkv, out, dout, lse, dqkv, dbias, S, nh, scale);
   return status();
 }
 

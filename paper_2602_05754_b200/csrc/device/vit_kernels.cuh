@@ -22,8 +22,9 @@ int launch_layernorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const f
 // out [B S, nh 64], lse fp32 [B][nh][S]; the backward writes dq|dk|dv packed into dqkv (may alias qkv).
 int launch_vit_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int nh, int hd,
                         float scale, cudaStream_t s);
+// dbias (nullable): += column sums of the packed dq|dk|dv (the qkv bias gradient), from the same CTAs
 int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
-                        const float* lse, __nv_bfloat16* dqkv, int B, int S, int nh, int hd, float scale,
+                        const float* lse, __nv_bfloat16* dqkv, float* dbias, int B, int S, int nh, int hd, float scale,
                         cudaStream_t s);
 
 int launch_bias_grad(const __nv_bfloat16* dy, long long ldy, float* db, int T, int n, cudaStream_t s);

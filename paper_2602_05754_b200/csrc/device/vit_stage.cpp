@@ -296,8 +296,9 @@ class VitStage final : public Stage {
                                   s));
       // attention
       PF_TRY(gemm_dx(dx2, h, w(P.wo), h, d_attn_, h, T_, h, h, EPI_STORE_BF16, s));
-      if (own_attn_) {  // dq|dk|dv straight into the packed dqkv (over qkv)
-        PF_TRY(launch_vit_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, dqkv, B_, S_, cfg_.n_heads, cfg_.head_dim, scale, s));
+      if (own_attn_) {  // dq|dk|dv straight into the packed dqkv (over qkv), bqkv's gradient alongside
+        PF_TRY(launch_vit_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, dqkv, g(P.bqkv), B_, S_, cfg_.n_heads,
+                                   cfg_.head_dim, scale, s));
       } else {
         AttnGrads ag{};
         PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ag, s));
@@ -306,7 +307,7 @@ class VitStage final : public Stage {
                         ag.v_b, ag.v_t, ag.v_h, ag.rep};
         PF_TRY(launch_rope_bwd_pack(gv, dqkv, ident_, T_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, s));
       }
-      PF_TRY(launch_bias_grad(dqkv, 3LL * h, g(P.bqkv), T_, 3 * h, s));
+      if (!own_attn_) PF_TRY(launch_bias_grad(dqkv, 3LL * h, g(P.bqkv), T_, 3 * h, s));
       PF_TRY(gemm_dx(dqkv, 3LL * h, w(P.wqkv), h, d_h_, h, T_, h, 3 * h, EPI_STORE_BF16, s));
       __nv_bfloat16* out;
       if (li > 0) out = sl.layers[static_cast<std::size_t>(li - 1)].dy;

@@ -132,10 +132,11 @@ def test_short_sequence_attention_vs_torch(cuda, B, S, nh):
     _native.check(lib.pf_vit_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), B, S, nh, hd, scale, st), "fwd")
     dqkv = torch.empty_like(qkv)
     _native.check(lib.pf_vit_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
-                                      B, S, nh, hd, scale, st), "bwd")
+                                      None, B, S, nh, hd, scale, st), "bwd")
     inplace = qkv.clone()
+    dbias = torch.full((3 * nh * hd,), 0.5, device=cuda)  # accumulated into, like the stage's grad buffer
     _native.check(lib.pf_vit_attn_bwd(inplace.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
-                                      inplace.data_ptr(), B, S, nh, hd, scale, st), "bwd in place")
+                                      inplace.data_ptr(), dbias.data_ptr(), B, S, nh, hd, scale, st), "bwd in place")
     torch.cuda.synchronize()
     x = qkv.float().view(B, S, 3, nh, hd).permute(2, 0, 3, 1, 4)  # [3, B, nh, S, hd]
     q, k, v = (t.clone().requires_grad_(True) for t in x)
@@ -149,3 +150,6 @@ def test_short_sequence_attention_vs_torch(cuda, B, S, nh):
     grads = torch.stack([q.grad, k.grad, v.grad]).permute(1, 3, 0, 2, 4).reshape(B * S, 3 * nh * hd)
     assert (dqkv.float() - grads).abs().max().item() <= 3e-2 * grads.abs().max().item()
     assert torch.equal(inplace, dqkv)
+    # fused bias gradient = column sums of the stored bf16 dqkv (fp32 atomics: order-dependent rounding only)
+    db_ref = dqkv.float().sum(0) + 0.5
+    assert torch.allclose(dbias, db_ref, atol=1e-3, rtol=1e-4)
