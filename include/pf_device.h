@@ -83,6 +83,14 @@ int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw
 int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int nh, int hd, float scale, void* stream);
 int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, float* dbias,
                     int B, int S, int nh, int hd, float scale, void* stream);
+/* LayerNorm over rows of h (ViT): y = (x - mean) * rstd * g + b, mean / rstd fp32 per row saved for the
+ * backward; pf_layernorm_bwd: dx = residual (nullable) + LayerNorm backward of dy, dg / db += column sums
+ * of dy * xhat / dy, dsum += column sums of the bf16 dx (the upstream linear layer's bias gradient);
+ * dg, db, dsum nullable. One pass for h = 256, 512, 1024. */
+int pf_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd, int T, int h,
+                     float eps, void* stream);
+int pf_layernorm_bwd(const void* x, const void* g, const float* mean, const float* rstd, const void* dy,
+                     const void* residual, void* dx, float* dg, float* db, float* dsum, int T, int h, void* stream);
 int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream);              /* act = gelu(pre), n % 8 == 0 */
 int pf_gelu_bwd(const void* pre, const void* dact, void* dpre, long long n, void* stream); /* dpre = dact * gelu'(pre) */
 int pf_gemm_gelu(const void* x, long long ldx, const void* W1, long long ldw, const void* bias, void* pre, void* act,

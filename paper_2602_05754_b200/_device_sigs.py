@@ -51,6 +51,8 @@ DEVICE_SIGNATURES = {
     "pf_gemm_set_streamk": ([c_int], c_int),
     "pf_vit_attn_fwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_vit_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
+    "pf_layernorm_fwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f, c_vp], c_int),
+    "pf_layernorm_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_vp], c_int),
     "pf_gelu_fwd": ([c_vp, c_vp, c_ll, c_vp], c_int),
     "pf_gelu_bwd": ([c_vp, c_vp, c_vp, c_ll, c_vp], c_int),
     "pf_gemm_rope": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_int, c_int, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),

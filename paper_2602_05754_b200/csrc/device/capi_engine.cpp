@@ -129,6 +129,25 @@ int pf_swiglu_fwd(const void* gu, void* a, int T, int ffn, void* stream) {
   });
 }
 
+int pf_layernorm_fwd(const void* x, const void* g, const void* b, void* y, float* mean, float* rstd, int T, int h,
+                     float eps, void* stream) {
+  return guard([&] {
+    return pf::launch_layernorm_fwd(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(g),
+                                    static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), mean, rstd,
+                                    T, h, eps, S(stream));
+  });
+}
+
+int pf_layernorm_bwd(const void* x, const void* g, const float* mean, const float* rstd, const void* dy,
+                     const void* residual, void* dx, float* dg, float* db, float* dsum, int T, int h, void* stream) {
+  return guard([&] {
+    return pf::launch_layernorm_bwd(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(g), mean,
+                                    rstd, static_cast<const __nv_bfloat16*>(dy),
+                                    static_cast<const __nv_bfloat16*>(residual), static_cast<__nv_bfloat16*>(dx), dg,
+                                    db, dsum, T, h, S(stream));
+  });
+}
+
 int pf_gelu_fwd(const void* pre, void* act, long long n, void* stream) {
   return guard([&] {
     return pf::launch_gelu_fwd(static_cast<const __nv_bfloat16*>(pre), static_cast<__nv_bfloat16*>(act), n,

@@ -571,10 +571,13 @@ __global__ void __launch_bounds__(norm_bwd_threads<CH>(), 1) rmsnorm_bwd_fused_k
   }
   for (int t = blockIdx.x * NW + warp; t < T; t += gridDim.x * NW) {
     const long long off = static_cast<long long>(t) * H + lane * 8;
-    uint4 xv[HOLD ? CH : 1], dv[HOLD ? CH : 1];
-    if constexpr (HOLD) {
+    uint4 xv[HOLD ? CH : 1], dv[HOLD ? CH : 1], rv[HOLD ? CH : 1];
+    if constexpr (HOLD) {  // the residual rides with x: one memory round trip per row
 #pragma unroll
-      for (int j = 0; j < CH; ++j) xv[j] = __ldcs(reinterpret_cast<const uint4*>(x + off + 256 * j));
+      for (int j = 0; j < CH; ++j) {
+        xv[j] = __ldcs(reinterpret_cast<const uint4*>(x + off + 256 * j));
+        if (residual) rv[j] = __ldcs(reinterpret_cast<const uint4*>(residual + off + 256 * j));
+      }
     }
     const float r = rstd[t];
     float dot = 0.f;
@@ -601,7 +604,19 @@ __global__ void __launch_bounds__(norm_bwd_threads<CH>(), 1) rmsnorm_bwd_fused_k
     for (int j = 0; j < CH; ++j) {
       float gv[8], out[8];
       load8(g + lane * 8 + 256 * j, gv);
-      if (residual) load8(residual + off + 256 * j, out);
+      if (residual) {
+        if constexpr (HOLD) {
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv[j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 t2 = __bfloat1622float2(r2[i]);
+            out[2 * i] = t2.x;
+            out[2 * i + 1] = t2.y;
+          }
+        } else {
+          load8(residual + off + 256 * j, out);
+        }
+      }
       uint4 xj, dj;
       if constexpr (HOLD) {
         xj = xv[j];

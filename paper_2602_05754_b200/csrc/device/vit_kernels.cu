@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kBlock) layernorm_fwd_reg_kernel(const __nv_bf
 //   dx = residual + rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat))
 //   dg += sum_t dy * xhat,  db += sum_t dy,  dsum += sum_t dx   (dsum: the bias gradient of the
 //   linear layer whose output gradient dx is; nullptr skips it)
-// Per-lane register partials, summed over the block's warps in shared memory, added to the
+// x, dy and the residual of a row are loaded together (one memory round trip per row). Per-lane
+// register partials, summed over the block's warps in shared memory, added to the
 // fp32 gradients with float4 atomics (one per 4 columns per block).
 template <int CH>
 __global__ void __launch_bounds__(kBlock, 1) layernorm_bwd_fused_kernel(
@@ -173,10 +174,12 @@ __global__ void __launch_bounds__(kBlock, 1) layernorm_bwd_fused_kernel(
     const long long off = static_cast<long long>(t) * H + lane * 8;
     const float mu = mean[t], r = rstd[t];
     float xv[CH][8], dv[CH][8];
+    uint4 rr[CH];
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       load8(x + off + 256 * j, xv[j]);
       load8(dy + off + 256 * j, dv[j]);
+      if (residual) rr[j] = *reinterpret_cast<const uint4*>(residual + off + 256 * j);
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -195,7 +198,15 @@ __global__ void __launch_bounds__(kBlock, 1) layernorm_bwd_fused_kernel(
     for (int j = 0; j < CH; ++j) {
       float gv[8], out[8];
       load8(g + lane * 8 + 256 * j, gv);
-      if (residual) load8(residual + off + 256 * j, out);
+      if (residual) {
+        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rr[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 t2 = __bfloat1622float2(r2[i]);
+          out[2 * i] = t2.x;
+          out[2 * i + 1] = t2.y;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float xh = (xv[j][i] - mu) * r;

@@ -153,3 +153,46 @@ def test_short_sequence_attention_vs_torch(cuda, B, S, nh):
     # fused bias gradient = column sums of the stored bf16 dqkv (fp32 atomics: order-dependent rounding only)
     db_ref = dqkv.float().sum(0) + 0.5
     assert torch.allclose(dbias, db_ref, atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T,h", [(3200, 1024), (777, 512), (129, 256), (300, 768)])
+def test_layernorm_fwd_bwd_vs_torch(cuda, T, h):
+    """pf_layernorm_fwd / pf_layernorm_bwd against torch fp32 (the fused one-pass backward for
+    h = 256 * {1, 2, 4}, the two-kernel path for h = 768), with residual, dg, db and dsum."""
+    import torch
+
+    from paper_2602_05754_b200 import _native
+
+    lib = _native.device()
+    gen = torch.Generator().manual_seed(T + h)
+    x = torch.randn(T, h, generator=gen).to(torch.bfloat16).cuda()
+    g = (1 + 0.1 * torch.randn(h, generator=gen)).to(torch.bfloat16).cuda()
+    b = (0.1 * torch.randn(h, generator=gen)).to(torch.bfloat16).cuda()
+    dy = torch.randn(T, h, generator=gen).to(torch.bfloat16).cuda()
+    res = torch.randn(T, h, generator=gen).to(torch.bfloat16).cuda()
+    y = torch.empty_like(x)
+    mean = torch.empty(T, device=cuda)
+    rstd = torch.empty(T, device=cuda)
+    dx = torch.empty_like(x)
+    dg, db, dsum = (torch.full((h,), 0.25, device=cuda) for _ in range(3))
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.pf_layernorm_fwd(x.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), mean.data_ptr(),
+                                       rstd.data_ptr(), T, h, 1e-6, st), "ln fwd")
+    _native.check(lib.pf_layernorm_bwd(x.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(),
+                                       res.data_ptr(), dx.data_ptr(), dg.data_ptr(), db.data_ptr(), dsum.data_ptr(),
+                                       T, h, st), "ln bwd")
+    torch.cuda.synchronize()
+    xf = x.float().requires_grad_(True)
+    gf = g.float().requires_grad_(True)
+    bf = b.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xf, (h,), gf, bf, eps=1e-6)
+    yr.backward(dy.float())
+    assert (y.float() - yr).abs().max().item() <= 2e-2 * yr.abs().max().item()
+    assert torch.allclose(mean, x.float().mean(1), atol=1e-4)
+    ref_dx = xf.grad + res.float()
+    assert (dx.float() - ref_dx).abs().max().item() <= 1e-2 * ref_dx.abs().max().item()
+    assert torch.allclose(dg - 0.25, gf.grad, atol=2e-2 * gf.grad.abs().max().item())
+    assert torch.allclose(db - 0.25, bf.grad, atol=1e-3 * bf.grad.abs().max().item() + 1e-3)
+    # dsum sums the stored bf16 dx (fp32 atomics: order-dependent rounding only)
+    assert torch.allclose(dsum - 0.25, dx.float().sum(0), atol=1e-3 * T ** 0.5, rtol=1e-4)

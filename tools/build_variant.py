@@ -1,5 +1,6 @@
-"""Build libpf_device.so variants that differ in compile-time defines of ONE translation unit, for
-same-box A/B runs: python tools/build_variant.py NAME SRC.cu -DX=1 ...  ->  variants/NAME/libpf_device.so
+"""Build libpf_device.so variants that differ in compile-time defines (or the source) of ONE translation
+unit, for same-box A/B runs: python tools/build_variant.py NAME SRC.cu|PATH/SRC.cu -DX=1 ...
+->  variants/NAME/libpf_device.so
 (on the box: cp variants/NAME/libpf_device.so paper_2602_05754_b200/lib/ before the run)."""
 import glob
 import os
@@ -16,7 +17,8 @@ def main():
     B.build_device()
     out_dir = os.path.join(ROOT, "variants", name)
     os.makedirs(out_dir, exist_ok=True)
-    srcp = os.path.join(B.DEV_SRC, src)
+    srcp = src if os.sep in src else os.path.join(B.DEV_SRC, src)  # a path: an alternative copy of a device TU
+    src = os.path.basename(srcp)
     obj = os.path.join(out_dir, src + ".o")
     subprocess.run([B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler",
                     "-fPIC", "-I", B.INC, "-I", B.DEV_SRC, "-I", B.HOST_SRC, *defs, "-c", srcp, "-o", obj], check=True)
