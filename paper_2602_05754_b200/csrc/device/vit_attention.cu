@@ -75,16 +75,21 @@ __device__ __forceinline__ void load_b_kn(uint32_t (&b)[4], const __nv_bfloat16*
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) { return pack_bf16x2(lo, hi); }
 
-// rows [0, S) of a head's 64 columns at `col` of a [*, ld] bf16 matrix -> smem tile (zero-padded)
+// rows [0, S) of a head's 64 columns at `col` of a [*, ld] bf16 matrix -> smem tile (zero-padded),
+// by cp.async: every tile load of a CTA is in flight at once (cp_async_wait_all before use)
 __device__ __forceinline__ void load_tile(__nv_bfloat16* t, const __nv_bfloat16* g, long long row0, long long ld,
                                           int col, int S) {
+#pragma unroll
   for (int i = threadIdx.x; i < kS * (kD / 8); i += kThreads) {
     const int r = i >> 3, c = (i & 7) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < S) v = *reinterpret_cast<const uint4*>(g + (row0 + r) * ld + col + c);
-    *reinterpret_cast<uint4*>(t + r * kLd + c) = v;
+    const bool ok = r < S;
+    const __nv_bfloat16* src = g + (row0 + (ok ? r : 0)) * ld + col + c;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(t + r * kLd + c)), "l"(src),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
   }
 }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // S = scale * Q K^T for the warp's 16 query rows (8 key tiles of 8), keys >= S masked to -inf
 __device__ __forceinline__ void scores(float (&s)[8][4], const __nv_bfloat16* Qs, const __nv_bfloat16* Ks, int r0,
@@ -125,6 +130,7 @@ __global__ void __launch_bounds__(kThreads) vit_attn_fwd_kernel(const __nv_bfloa
   load_tile(Qs, qkv, row0, ld, h * kD, S);
   load_tile(Ks, qkv, row0, ld, (nh + h) * kD, S);
   load_tile(Vs, qkv, row0, ld, (2 * nh + h) * kD, S);
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r0 = warp * 16;
   if (r0 >= S) return;
@@ -256,6 +262,7 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if ((threadIdx.x & 1) == 0) Dsum[q] = acc;
   }
+  cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r0 = warp * 16;
   const int g = lane >> 2, c2 = (lane & 3) * 2;
@@ -357,9 +364,15 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
       colsum16(dv, 128, 1.f, k0 < S, k1 < S);
       __syncthreads();
       // bqkv gradient: q | k | v columns of head h sit at h*64, (nh + h)*64, (2 nh + h)*64
-      for (int c = threadIdx.x; c < 192; c += kThreads) {
-        const float v = bsum[c] + bsum[192 + c] + bsum[384 + c] + bsum[576 + c];
-        atomicAdd(dbias + (c / 64) * nh * kD + h * kD + (c % 64), v);
+      if (threadIdx.x < 48) {  // one float4 atomic per 4 columns
+        const int c = threadIdx.x * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float4 t = *reinterpret_cast<const float4*>(bsum + w * 192 + c);
+          v = make_float4(v.x + t.x, v.y + t.y, v.z + t.z, v.w + t.w);
+        }
+        atomicAdd(reinterpret_cast<float4*>(dbias + (c / 64) * nh * kD + h * kD + (c % 64)), v);
       }
     }
 #pragma unroll
@@ -390,6 +403,7 @@ int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, cons
                         const float* lse, __nv_bfloat16* dqkv, float* dbias, int B, int S, int nh, int hd, float scale,
                         cudaStream_t s) {
   if (S < 1 || S > kS || hd != kD || B < 1 || nh < 1) return PF_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(dbias) % 16) return PF_ERR_INVALID;  // float4 atomics
   constexpr int smem = 6 * kS * kLd * 2 + kS * 4 + 4 * 192 * 4;
   static bool attr = false;
   if (!attr) {
