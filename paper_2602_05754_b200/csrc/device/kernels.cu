@@ -501,9 +501,12 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_fwd_reg_kernel(const __nv_bflo
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nw) {
     const __nv_bfloat16* xr = x + static_cast<long long>(t) * H + lane * 8;
-    uint4 xv[CH];
+    uint4 xv[CH], gv[CH];  // g rides with x: its loads do not wait behind the row reduction
 #pragma unroll
-    for (int j = 0; j < CH; ++j) xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + 256 * j));
+    for (int j = 0; j < CH; ++j) {
+      xv[j] = __ldcs(reinterpret_cast<const uint4*>(xr + 256 * j));
+      gv[j] = *reinterpret_cast<const uint4*>(g + lane * 8 + 256 * j);
+    }
     float ss = 0.f;
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
@@ -528,7 +531,13 @@ __global__ void __launch_bounds__(kBlock) rmsnorm_fwd_reg_kernel(const __nv_bflo
         f[2 * i] = v.x;
         f[2 * i + 1] = v.y;
       }
-      load8(g + lane * 8 + 256 * j, gg);
+      const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 v = __bfloat1622float2(gb[i]);
+        gg[2 * i] = v.x;
+        gg[2 * i + 1] = v.y;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) f[i] = f[i] * r * gg[i];
       store8(yr + 256 * j, f);

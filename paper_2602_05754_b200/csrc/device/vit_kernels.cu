@@ -120,8 +120,13 @@ __global__ void __launch_bounds__(kBlock) layernorm_fwd_reg_kernel(const __nv_bf
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nw) {
     const long long off = static_cast<long long>(t) * H + lane * 8;
     float f[CH][8];
+    uint4 gr[CH], br[CH];  // g and b ride with x: their loads do not wait behind the row reductions
 #pragma unroll
-    for (int j = 0; j < CH; ++j) load8(x + off + 256 * j, f[j]);
+    for (int j = 0; j < CH; ++j) {
+      load8(x + off + 256 * j, f[j]);
+      gr[j] = *reinterpret_cast<const uint4*>(g + lane * 8 + 256 * j);
+      br[j] = *reinterpret_cast<const uint4*>(b + lane * 8 + 256 * j);
+    }
     float sm = 0.f;
 #pragma unroll
     for (int j = 0; j < CH; ++j)
@@ -141,8 +146,16 @@ __global__ void __launch_bounds__(kBlock) layernorm_fwd_reg_kernel(const __nv_bf
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
       float gg[8], bb[8], o[8];
-      load8(g + lane * 8 + 256 * j, gg);
-      load8(b + lane * 8 + 256 * j, bb);
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr[j]);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&br[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 gf = __bfloat1622float2(g2[i]), bf = __bfloat1622float2(b2[i]);
+        gg[2 * i] = gf.x;
+        gg[2 * i + 1] = gf.y;
+        bb[2 * i] = bf.x;
+        bb[2 * i + 1] = bf.y;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) o[i] = (f[j][i] - mu) * r * gg[i] + bb[i];
       store8(y + off + 256 * j, o);

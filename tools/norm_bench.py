@@ -1,4 +1,4 @@
-"""RMSNorm backward (dx with residual + dg) at LLaMA shapes through the C ABI: CUDA events, L2 flushed."""
+"""RMSNorm backward (dx with residual + dg) and forward at LLaMA shapes through the C ABI: CUDA events, L2 flushed."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -25,3 +25,14 @@ for T, h in [(4096, 2048), (4096, 4096)]:
         if k >= 3: tot += e0.elapsed_time(e1)
     us = tot / 20 * 1e3
     print(f"rmsnorm_bwd T={T} h={h}: {us:.1f} us, {4 * T * h * 2 / us / 1e3:.0f} GB/s (x, dy, residual in; dx out)")
+    y = torch.empty_like(x)
+    tot = 0.0
+    for k in range(23):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        assert lib.pf_rmsnorm_fwd(x.data_ptr(), g.data_ptr(), y.data_ptr(), rstd.data_ptr(), T, h, 1e-5, s) == 0
+        e1.record(); torch.cuda.synchronize()
+        if k >= 3: tot += e0.elapsed_time(e1)
+    us = tot / 20 * 1e3
+    print(f"rmsnorm_fwd T={T} h={h}: {us:.1f} us, {2 * T * h * 2 / us / 1e3:.0f} GB/s (x in; y out)")
