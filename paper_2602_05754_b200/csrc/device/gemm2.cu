@@ -1059,7 +1059,7 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   const int mode = streamk_mode();
   const int active = std::min(max_clusters, max_active_clusters<BN, false, EPI_STORE_BF16>());
   const bool sk = epi != EPI_SWIGLU && epi != EPI_DSWIGLU && epi != EPI_GELU && epi != EPI_DGELU && epi != EPI_ROPE &&
-                  ntiles > active && num_kb >= 8 &&
+                  (ntiles > active || mode == 1) && num_kb >= 8 &&
                   (mode == 1 || mode == 2 || (mode < 0 && eff < 0.92));
   if (sk) {
     StreamKState& st = sk_state();

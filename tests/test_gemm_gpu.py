@@ -252,9 +252,11 @@ def test_gemm_cta_pair(cuda, b_mn, epi, M, N, K):
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("b_mn", [0, 1])
 @pytest.mark.parametrize("epi", [0, 1, 3])
-@pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512), (4096, 2048, 8192)])
+@pytest.mark.parametrize("M,N,K", [(4096, 2048, 1024), (2048, 2560, 832), (4352, 2304, 512), (4096, 2048, 8192),
+                                   (3200, 1024, 1024), (3200, 1024, 4096)])
 def test_gemm_cta_pair_stream_k(cuda, mode, b_mn, epi, M, N, K):
-    """Forced stream-K on tile counts just above the 74 clusters: mode 1 splits every tile, mode 2
+    """Forced stream-K on tile counts just above the 74 clusters (and, mode 1 only, the 52-tile ViT
+    N = 1024 shapes below one wave): mode 1 splits every tile, mode 2
     runs the full waves data-parallel and splits the last wave's tiles over all clusters (a tile
     then spans up to three clusters: its head adds every parked piece)."""
     lib, nat = _lib()
