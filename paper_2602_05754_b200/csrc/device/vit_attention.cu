@@ -200,14 +200,14 @@ __global__ void __launch_bounds__(kThreads) vit_attn_fwd_kernel(const __nv_bfloa
   }
 }
 
-__global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloat16* qkv,
+__global__ void __launch_bounds__(kThreads, 4) vit_attn_bwd_kernel(const __nv_bfloat16* qkv,
                                                                 const __nv_bfloat16* __restrict__ out,
                                                                 const __nv_bfloat16* __restrict__ dout,
                                                                 const float* __restrict__ lse, __nv_bfloat16* dqkv,
                                                                 float* __restrict__ dbias, int S, int nh,
                                                                 float scale) {
   pdl_begin();
-  extern __shared__ __align__(16) uint8_t attn_smem[];  // 6 tiles of 64 x 72 bf16 (55 KB) + D + bias sums
+  extern __shared__ __align__(16) uint8_t attn_smem[];  // 6 tiles of 64 x 72 bf16 (55 KB) + D: 4 CTAs per SM
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(attn_smem);
   __nv_bfloat16* Ks = Qs + kS * kLd;
   __nv_bfloat16* Vs = Ks + kS * kLd;
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
   __nv_bfloat16* Ps = dOs + kS * kLd;
   __nv_bfloat16* dSs = Ps + kS * kLd;
   float* Dsum = reinterpret_cast<float*>(dSs + kS * kLd);
-  float* bsum = Dsum + kS;  // [4 warps][3 x 64]: per-warp column sums of the bf16 dq | dk | dv rows
   // column sums over this warp's 16 rows of one 16 x 64 C-fragment block (values rounded to bf16,
-  // as a column reduction of the stored gradient would see them) -> bsum[warp][base + col]
-  auto colsum16 = [&](const float (&v)[8][4], int base, float mul, bool ok0, bool ok1) {
+  // as a column reduction of the stored gradient would see them) -> dst[col] (float2 atomics into
+  // global memory when `atomic`, else plain shared-memory stores)
+  auto colsum16 = [&](const float (&v)[8][4], float mul, bool ok0, bool ok1, float* dst, bool atomic) {
     const int lane_ = threadIdx.x & 31;
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
@@ -232,8 +232,12 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
         c1 += __shfl_xor_sync(0xffffffffu, c1, o);
       }
       if (lane_ < 4) {
-        bsum[(threadIdx.x >> 5) * 192 + base + dt * 8 + 2 * lane_] = c0;
-        bsum[(threadIdx.x >> 5) * 192 + base + dt * 8 + 2 * lane_ + 1] = c1;
+        if (atomic) {
+          atomicAdd(reinterpret_cast<float2*>(dst + dt * 8 + 2 * lane_), make_float2(c0, c1));
+        } else {
+          dst[dt * 8 + 2 * lane_] = c0;
+          dst[dt * 8 + 2 * lane_ + 1] = c1;
+        }
       }
     }
   };
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
         mma16816(dq[dt + 1], a0, a1, a2, a3, bb[2], bb[3]);
       }
     }
-    if (dbias) colsum16(dq, 0, scale, q0 < S, q1 < S);
+    if (dbias) colsum16(dq, scale, q0 < S, q1 < S, dbias + h * kD, true);  // the q block of bqkv
     __syncthreads();  // every warp's P / dS rows are in shared memory; Q, K, V, dO reads are done
 #pragma unroll
     for (int dt = 0; dt < 8; ++dt) {
@@ -360,19 +364,20 @@ __global__ void __launch_bounds__(kThreads) vit_attn_bwd_kernel(const __nv_bfloa
     }
     const int k0 = r0 + g, k1 = r0 + g + 8;
     if (dbias) {
-      colsum16(dk, 64, scale, k0 < S, k1 < S);
-      colsum16(dv, 128, 1.f, k0 < S, k1 < S);
+      __syncthreads();  // every warp's P / dS / Q / dO reads are done: the P tile holds the k | v sums
+      float* bsum = reinterpret_cast<float*>(Ps);  // [4 warps][128]
+      colsum16(dk, scale, k0 < S, k1 < S, bsum + warp * 128, false);
+      colsum16(dv, 1.f, k0 < S, k1 < S, bsum + warp * 128 + 64, false);
       __syncthreads();
-      // bqkv gradient: q | k | v columns of head h sit at h*64, (nh + h)*64, (2 nh + h)*64
-      if (threadIdx.x < 48) {  // one float4 atomic per 4 columns
+      if (threadIdx.x < 32) {  // one float4 atomic per 4 columns: k at (nh + h) * 64, v at (2 nh + h) * 64
         const int c = threadIdx.x * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const float4 t = *reinterpret_cast<const float4*>(bsum + w * 192 + c);
+          const float4 t = *reinterpret_cast<const float4*>(bsum + w * 128 + c);
           v = make_float4(v.x + t.x, v.y + t.y, v.z + t.z, v.w + t.w);
         }
-        atomicAdd(reinterpret_cast<float4*>(dbias + (c / 64) * nh * kD + h * kD + (c % 64)), v);
+        atomicAdd(reinterpret_cast<float4*>(dbias + (c < 64 ? nh : 2 * nh) * kD + h * kD + (c & 63)), v);
       }
     }
 #pragma unroll
@@ -404,7 +409,7 @@ int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, cons
                         cudaStream_t s) {
   if (S < 1 || S > kS || hd != kD || B < 1 || nh < 1) return PF_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(dbias) % 16) return PF_ERR_INVALID;  // float4 atomics
-  constexpr int smem = 6 * kS * kLd * 2 + kS * 4 + 4 * 192 * 4;
+  constexpr int smem = 6 * kS * kLd * 2 + kS * 4;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(vit_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
