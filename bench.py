@@ -386,7 +386,7 @@ def run_ours(args) -> None:
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
-            "attention_backend": lib.pf_attention_backend().decode(),
+            "attention_backend": attention_backend(shape, lib),
             "loss": {"first": round(ctl[0]["loss"], 4), "last": round(res[-1]["loss"], 4)},
         }
         print(json.dumps(line), flush=True)
@@ -395,6 +395,16 @@ def run_ours(args) -> None:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def attention_backend(shape, lib) -> str:
+    """Which attention the step ran: ViT with S <= 64 and head_dim 64 uses the hand-written
+    short-sequence kernel (vit_attention.cu) unless PF_VIT_ATTN=cudnn; everything else the
+    library fused attention pf_attention_backend() names."""
+    if getattr(shape, "family", 0) == 1 and shape.seq <= 64 and shape.head_dim == 64 and \
+            os.environ.get("PF_VIT_ATTN") != "cudnn":
+        return "vit_attn (own mma.sync kernel, S <= 64)"
+    return lib.pf_attention_backend().decode()
 
 
 def main() -> None:
