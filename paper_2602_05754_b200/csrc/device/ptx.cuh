@@ -282,10 +282,31 @@ __device__ __forceinline__ void rope_rotate(float a, float b, float2 cs, float& 
 }
 
 // GELU (erf form) and its derivative; shared by the ViT GELU kernels and the fused GEMM
-// epilogues so they agree bit for bit.
-__device__ __forceinline__ float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
+// epilogues so they agree bit for bit. Phi(v) = 0.5 (1 + erf(v / sqrt 2)) comes from
+// Abramowitz & Stegun 7.1.26 on |z|, z = v / sqrt 2: 0.5 erfc(|z|) = 0.5 t P(t) e^{-z^2},
+// t = 1 / (1 + 0.3275911 |z|), |erf error| <= 1.5e-7; one MUFU reciprocal and one MUFU exp,
+// and e^{-z^2} = e^{-v^2/2} is the Gaussian density term gelu' needs. Taking 1 - q only for
+// v >= 0 avoids the cancellation of 1 + erf(z) for negative v (over every bf16 input the
+// bf16-rounded GELU differs from the fp64 one in 0.43% of values, libm erff: 0.51%). erff was
+// a ~30-instruction branchy routine that made the GELU epilogues the bottleneck of the fused
+// ViT MLP GEMMs (tools/gelu_bench.py).
+__device__ __forceinline__ float gelu_phi(float v, float& e) {
+  const float a = fabsf(v) * 0.70710678118654752f;
+  const float t = rcp_approx(fmaf(0.3275911f, a, 1.f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f), -0.284496736f), 0.254829592f);
+  e = __expf(-(a * a));
+  const float q = 0.5f * poly * e;
+  return v >= 0.f ? 1.f - q : q;
+}
+__device__ __forceinline__ float gelu_erf(float v) {
+  float e;
+  return v * gelu_phi(v, e);
+}
 __device__ __forceinline__ float gelu_erf_grad(float v) {
-  return 0.5f * (1.f + erff(v * 0.70710678118654752f)) + v * 0.39894228040143268f * __expf(-0.5f * v * v);
+  float e;
+  const float ph = gelu_phi(v, e);
+  return ph + v * 0.39894228040143268f * e;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
