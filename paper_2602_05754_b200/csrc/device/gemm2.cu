@@ -67,8 +67,10 @@ struct Cfg2 {
   static constexpr int EPI_BUF =
       EPI == EPI_SWIGLU ? 3 * 8192 : ((EPI == EPI_DSWIGLU || EPI == EPI_GELU || EPI == EPI_ROPE) ? 2 * 8192 : 8192);
   static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? 2 * EPI_BUF : 0;
+  // EPI_DGELU column sums: [2 accumulator buffers][4 row quarters][BN] fp32
+  static constexpr int CS_BYTES = EPI == EPI_DGELU ? 2 * 4 * BN * 4 : 0;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + CS_BYTES + 256;
 };
 
 struct alignas(64) Params2 {
@@ -184,7 +186,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
   uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;  // EPI_DSWIGLU buffers (1024-aligned)
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sE + Cfg::EPI_BYTES);
+  float* csum = reinterpret_cast<float*>(sE + Cfg::EPI_BYTES);  // EPI_DGELU column sums
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sE + Cfg::EPI_BYTES + Cfg::CS_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -656,7 +659,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float2 pf = __bfloat1622float2(p2[i]);
                 const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * s2 + 2 * i]),
                                                                           p.alpha * __uint_as_float(r[8 * s2 + 2 * i + 1])));
-                dw[i] = pack_bf16x2(d.x * gelu_erf_grad(pf.x), d.y * gelu_erf_grad(pf.y));
+                const __nv_bfloat162 o = __floats2bfloat162_rn(d.x * gelu_erf_grad(pf.x), d.y * gelu_erf_grad(pf.y));
+                dw[i] = *reinterpret_cast<const uint32_t*>(&o);
+                const float2 of = __bfloat1622float2(o);  // the stored (bf16) d(pre) feeds the bias gradient
+                r[8 * s2 + 2 * i] = __float_as_uint(of.x);
+                r[8 * s2 + 2 * i + 1] = __float_as_uint(of.y);
               }
               *pp = make_uint4(dw[0], dw[1], dw[2], dw[3]);
             }
@@ -664,30 +671,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
           if (EPI == EPI_DGELU && p.colsum != nullptr) {
-            // column sums of the chunk's 128 x 32 d(pre) box: warp w (0..7) owns columns 4w..4w+3,
-            // lane l rows l, l+32, l+64, l+96; one atomic per column per CTA and chunk. Rows past M
-            // were loaded as zeros (TMA fill), so they add nothing.
-            const int wq = warp - 2;
-            float cs[4] = {0.f, 0.f, 0.f, 0.f};
+            // column sums over this warp's 32 rows of its 16 columns, from registers (r holds the
+            // bf16-rounded d(pre)): a butterfly reduce-scatter, 16 shuffles; lane l ends with the sum
+            // of column (l >> 1) & 15 (lanes l, l ^ 1 agree). Rows past M are TMA zero-fill: 0.
+            float v[16];
 #pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              const int rw = static_cast<int>(lane) + 32 * rr;
-              const int col0 = 4 * wq;  // 4 consecutive columns = 8 bytes inside one 16-byte chunk
-              const int off = rw * 64 + (((col0 >> 3) ^ ((rw >> 1) & 3)) << 4) + (col0 & 7) * 2;
-              const uint2 v = *reinterpret_cast<const uint2*>(buf + off);
-              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
-              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
-              cs[0] += a.x;
-              cs[1] += a.y;
-              cs[2] += b.x;
-              cs[3] += b.y;
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) cs[i] = warp_sum_f(cs[i]);
-            const int gcol = tn * BN + c * 32 + 4 * wq;
-            const float mine = lane == 0 ? cs[0] : lane == 1 ? cs[1] : lane == 2 ? cs[2] : cs[3];
-            if (lane < 4 && gcol + static_cast<int>(lane) < p.N) atomicAdd(p.colsum + gcol + lane, mine);
-            named_bar_sync(1, kEpiThreads);  // the buffer is refilled below only after every warp read it
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+            // round (W values move, lane bit B, partner lane ^ 2^B): keep the half selected by bit B
+#define PF_CS_ROUND(W, B)                                              \
+  {                                                                    \
+    const bool up = (lane >> (B)) & 1u;                                \
+    _Pragma("unroll") for (int j = 0; j < (W); ++j) {                  \
+      const float send = up ? v[j] : v[j + (W)];                       \
+      const float keep = up ? v[j + (W)] : v[j];                       \
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << (B));      \
+    }                                                                  \
+  }
+            PF_CS_ROUND(8, 4)
+            PF_CS_ROUND(4, 3)
+            PF_CS_ROUND(2, 2)
+            PF_CS_ROUND(1, 1)
+#undef PF_CS_ROUND
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            if ((lane & 1u) == 0)
+              csum[(abuf * 4 + q) * BN + c * 32 + half * 16 + static_cast<int>((lane >> 1) & 15u)] = v[0];
           }
           if (elected) {
             if constexpr (EPI == EPI_GELU) {
@@ -699,6 +706,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               bulk_commit();
               if (c + 2 < BN / 32) load_pre(c + 2);
             }
+          }
+        }
+        if (EPI == EPI_DGELU && p.colsum != nullptr) {
+          // one atomic per column per CTA and tile (csum is double-buffered by accumulator buffer:
+          // the next tile's writes go to the other half, and the one after follows 8 named barriers)
+          named_bar_sync(1, kEpiThreads);
+          for (int cc = threadIdx.x - 64; cc < BN; cc += kEpiThreads) {
+            const float* cs = csum + abuf * 4 * BN + cc;
+            const int gcol = tn * BN + cc;
+            if (gcol < p.N) atomicAdd(p.colsum + gcol, cs[0] + cs[BN] + cs[2 * BN] + cs[3 * BN]);
           }
         }
         tc_fence_before();
