@@ -4,7 +4,7 @@
 // At S <= 64 a head's Q, K, V (and O, dO) are 8 KB tiles: the whole problem of one
 // (image, head) fits in shared memory, S = QK^T is one 64 x 64 tile and no online
 // softmax is needed. The op is HBM-bound (forward: read Q, K, V, write O, 4 x 6.5 MB per
-// layer and microbatch; backward: read Q, K, V, O, dO, write dQ, dK, dV), so the 64 x 64 x 64
+// layer and microbatch; backward: read Q, K, V, dO, write dQ, dK, dV), so the 64 x 64 x 64
 // products run on warp-level MMAs (mma.sync m16n8k16, bf16 in, fp32 accumulate) straight
 // from shared memory; a 128-row tcgen05 tile would be half padding here. The generic fused
 // attention (cuDNN) spent 18.5 us forward and 62 us backward per layer on this shape.
@@ -214,7 +214,6 @@ __global__ void __launch_bounds__(kThreads, 4) vit_attn_bwd_kernel(const __nv_bf
   __nv_bfloat16* dOs = Vs + kS * kLd;
   __nv_bfloat16* Ps = dOs + kS * kLd;
   __nv_bfloat16* dSs = Ps + kS * kLd;
-  float* Dsum = reinterpret_cast<float*>(dSs + kS * kLd);
   // column sums over this warp's 16 rows of one 16 x 64 C-fragment block (values rounded to bf16,
   // as a column reduction of the stored gradient would see them) -> dst[col] (float2 atomics into
   // global memory when `atomic`, else plain shared-memory stores)
@@ -243,29 +242,11 @@ __global__ void __launch_bounds__(kThreads, 4) vit_attn_bwd_kernel(const __nv_bf
   };
   const int b = blockIdx.x / nh, h = blockIdx.x - b * nh;
   const long long row0 = static_cast<long long>(b) * S, ld = 3LL * nh * kD, ldo = static_cast<long long>(nh) * kD;
+  (void)out;  // the flash-attention signature keeps O; D = rowsum(dO * O) is taken as rowsum(P * dP) below
   load_tile(Qs, qkv, row0, ld, h * kD, S);
   load_tile(Ks, qkv, row0, ld, (nh + h) * kD, S);
   load_tile(Vs, qkv, row0, ld, (2 * nh + h) * kD, S);
   load_tile(dOs, dout, row0, ldo, h * kD, S);
-  // D[q] = sum_d dO[q, d] O[q, d] (O read straight from global, one row per thread pair)
-  for (int q = threadIdx.x >> 1; q < kS; q += kThreads / 2) {
-    float acc = 0.f;
-    if (q < S) {
-      const int half = threadIdx.x & 1;
-      const __nv_bfloat16* orow = out + (row0 + q) * ldo + h * kD + half * 32;
-      const __nv_bfloat16* drow = dout + (row0 + q) * ldo + h * kD + half * 32;
-#pragma unroll
-      for (int c = 0; c < 32; c += 8) {
-        float fo[8], fd[8];
-        load8(orow + c, fo);
-        load8(drow + c, fd);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc += fo[i] * fd[i];
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if ((threadIdx.x & 1) == 0) Dsum[q] = acc;
-  }
   cp_async_wait_all();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, r0 = warp * 16;
@@ -277,7 +258,6 @@ __global__ void __launch_bounds__(kThreads, 4) vit_attn_bwd_kernel(const __nv_bf
     const int q0 = r0 + g, q1 = r0 + g + 8;
     const float* l = lse + (static_cast<long long>(b) * nh + h) * S;
     const float l0 = q0 < S ? l[q0] : 0.f, l1 = q1 < S ? l[q1] : 0.f;
-    const float d0 = Dsum[q0], d1 = Dsum[q1];
     float dp[8][4];
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt)
@@ -295,11 +275,27 @@ __global__ void __launch_bounds__(kThreads, 4) vit_attn_bwd_kernel(const __nv_bf
         mma16816(dp[nt + 1], a[0], a[1], a[2], a[3], bb[2], bb[3]);
       }
     }
+    // P, and D[q] = sum_k P[q, k] dP[q, k] (= sum_d dO[q, d] O[q, d]: the whole key range of
+    // a row is in this warp's fragments, so D needs no pass over O); a row lives in a lane quad
+    float d0 = 0.f, d1 = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
       // padded query rows get P = 0 (their lse is 0 and scores -inf only for padded keys, so zero them)
-      const float p0 = q0 < S ? __expf(s[nt][0] - l0) : 0.f, p1 = q0 < S ? __expf(s[nt][1] - l0) : 0.f;
-      const float p2 = q1 < S ? __expf(s[nt][2] - l1) : 0.f, p3 = q1 < S ? __expf(s[nt][3] - l1) : 0.f;
+      s[nt][0] = q0 < S ? __expf(s[nt][0] - l0) : 0.f;
+      s[nt][1] = q0 < S ? __expf(s[nt][1] - l0) : 0.f;
+      s[nt][2] = q1 < S ? __expf(s[nt][2] - l1) : 0.f;
+      s[nt][3] = q1 < S ? __expf(s[nt][3] - l1) : 0.f;
+      d0 += s[nt][0] * dp[nt][0] + s[nt][1] * dp[nt][1];
+      d1 += s[nt][2] * dp[nt][2] + s[nt][3] * dp[nt][3];
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = s[nt][0], p1 = s[nt][1], p2 = s[nt][2], p3 = s[nt][3];
       s[nt][0] = p0 * (dp[nt][0] - d0);  // dS
       s[nt][1] = p1 * (dp[nt][1] - d0);
       s[nt][2] = p2 * (dp[nt][2] - d1);
@@ -409,7 +405,7 @@ int launch_vit_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, cons
                         cudaStream_t s) {
   if (S < 1 || S > kS || hd != kD || B < 1 || nh < 1) return PF_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(dbias) % 16) return PF_ERR_INVALID;  // float4 atomics
-  constexpr int smem = 6 * kS * kLd * 2 + kS * 4;
+  constexpr int smem = 6 * kS * kLd * 2;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(vit_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

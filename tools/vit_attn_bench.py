@@ -44,8 +44,8 @@ def main():
     fused = timed(lambda: lib.pf_vit_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                                               dqkv.data_ptr(), db.data_ptr(), B, S, nh, hd, sc, st))
     colsum = timed(lambda: db.add_(dqkv.float().sum(0)))
-    # bytes: qkv + out + dout read, dqkv written (bf16), lse read
-    nbytes = B * S * (3 * nh * hd * 2 * 2 + nh * hd * 2 * 2) + B * nh * S * 4
+    # bytes: qkv + dout read, dqkv written (bf16), lse read (D comes from P and dP: O is not read)
+    nbytes = B * S * (3 * nh * hd * 2 * 2 + nh * hd * 2) + B * nh * S * 4
     print(f"B={B} S={S} nh={nh}: fwd {fwd * 1e3:.1f} us | bwd {plain * 1e3:.1f} us "
           f"({nbytes / (plain * 1e-3) / 1e9:.0f} GB/s) | bwd + fused bias grad {fused * 1e3:.1f} us | "
           f"torch column sum {colsum * 1e3:.1f} us")
