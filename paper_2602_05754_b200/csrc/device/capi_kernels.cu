@@ -122,15 +122,20 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-// Off by default: on one B200 (bench.py, alternating runs) PDL moved the stable-freeze step by
-// +0.3..0.6% (noise level) and slowed the no-freeze step by 3%; back-to-back small kernels gain
-// (rmsnorm_fwd 8.2 -> 5.5 us per launch, tools/gap_bench.py). PF_PDL=1 turns it on.
+// Per model family (set_pdl_default, from make_stage): on one B200 (bench.py, alternating runs)
+// PDL moves the LLaMA-1B stable-freeze step by +0.3..0.6% (noise level) and slows its no-freeze
+// step by 2-3%, so LLaMA stages keep it off; the ViT-L/32 step, thousands of small kernels,
+// gains 7.5% (399k -> 429k tok/s), so ViT stages turn it on. PF_PDL=1 / PF_PDL=0 override both.
+namespace {
+std::atomic<int> g_pdl_default{0};
+}
+void set_pdl_default(bool on) { g_pdl_default.store(on ? 1 : 0, std::memory_order_relaxed); }
 bool pdl_enabled() {
-  static const bool on = [] {
+  static const int env = [] {
     const char* e = std::getenv("PF_PDL");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  return env >= 0 ? env == 1 : g_pdl_default.load(std::memory_order_relaxed) != 0;
 }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 }  // namespace pf

@@ -94,9 +94,11 @@ void probe_end(cudaStream_t s);
 // cudaLaunchAttributeProgrammaticStreamSerialization, waits (griddepcontrol.wait) for the
 // previous kernel's completion and memory before touching global memory, and lets the next
 // kernel launch early (griddepcontrol.launch_dependents), so a kernel's launch and prologue
-// overlap its predecessor's tail. Off unless PF_PDL=1 (measured: capi_kernels.cu). The
-// kernels always execute griddepcontrol.wait / launch_dependents (no-ops without the attribute).
+// overlap its predecessor's tail. Default per model family (set_pdl_default: ViT on, LLaMA
+// off; measured: capi_kernels.cu), PF_PDL=0|1 overrides. The kernels always execute
+// griddepcontrol.wait / launch_dependents (no-ops without the attribute).
 bool pdl_enabled();
+void set_pdl_default(bool on);
 
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).
 void count_launch();

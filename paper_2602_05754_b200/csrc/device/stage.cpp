@@ -601,6 +601,7 @@ std::unique_ptr<Stage> make_vit_stage(const ModelConfig& cfg, const StageSpec& s
 
 std::unique_ptr<Stage> make_stage(const ModelConfig& cfg, const StageSpec& spec, int slots, uint64_t seed,
                                   int device, bool split_backward) {
+  set_pdl_default(cfg.family == 1);  // PDL pays on the ViT step's many small kernels only
   if (cfg.family == 1) return make_vit_stage(cfg, spec, slots, seed, device, split_backward);
   if (cfg.family != 0) throw std::invalid_argument("stage: unknown model family");
   return std::make_unique<LlamaStage>(cfg, spec, slots, seed, device, split_backward);
