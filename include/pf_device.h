@@ -210,6 +210,14 @@ int pf_trainer_destroy(pf_ctx* ctx);
  * int32 or NULL (device-resident synthetic tokens). */
 int pf_trainer_step(pf_ctx* ctx, int t, const int32_t* host_tokens, const int32_t* host_targets,
                     pf_step_result* out);
+/* One step with CALLER-OWNED host frozen-unit masks: host_masks holds, per local
+ * stage in order, M masks of ceil(units/64) uint64 words in FreezeMask::test bit order
+ * (reference proj/include/pipefreeze/freezectl.hpp:41-59: unit u = bit u%64 of word u/64); bits
+ * past the last unit are ignored. They replace the controller's masks for this step (no
+ * monitoring sample is recorded); the words are copied to HBM before the step's first action.
+ * Reference caller: cmd_simulate's run_freezing_masks -> MaskHistory (tools/pipefreeze.cpp:85-171). */
+int pf_trainer_step_masks(pf_ctx* ctx, int t, const int32_t* host_tokens, const int32_t* host_targets,
+                          const uint64_t* host_masks, pf_step_result* out);
 /* ratio < 0: the phase controller + LP plan; ratio in [0,1]: every cell frozen at `ratio`. */
 int pf_trainer_set_override(pf_ctx* ctx, double ratio);
 int pf_trainer_set_plan(pf_ctx* ctx, const double* ratios /* (s-1)*M + (m-1) */);

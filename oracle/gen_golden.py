@@ -3,7 +3,9 @@
 Run in the build container (needs /root/reference for the fixtures and
 oracle/_ref/libpfref.so from `make -C oracle`):
 
-    python oracle/gen_golden.py
+    python oracle/gen_golden.py            # everything but the two below
+    python oracle/gen_golden.py artifacts  # tests/golden/artifacts.json
+    python oracle/gen_golden.py lp_big     # tests/golden/lp_big.json (reference simplex, ~7 min)
 
 Every number here comes from the reference's own functions (oracle/ref_harness.cpp).
 Floats that must match bit-exactly are stored as float.hex() strings.
@@ -178,6 +180,36 @@ def gen_lp(fx):
     dump("lp.json", rows)
 
 
+BIG_LP_CASES = [
+    # (kind, R, C, M): 258-node and 514-node-class DAGs the dense simplex still finishes (90-190 s each);
+    # embedding-heavy first stage, LM-head-heavy last stage (the heterogeneous rows of gen_lp, scaled up)
+    ("1f1b", 8, 1, 16), ("interleaved-1f1b", 8, 2, 8), ("1f1b", 4, 1, 32),
+]
+
+
+def _het(S):
+    fw = [12.0] + [10.0] * (S - 2) + [16.0]
+    ba = [13.0] + [10.0] * (S - 2) + [18.0]
+    bp = [15.0] + [12.0] * (S - 2) + [20.0]
+    return fw, ba, bp
+
+
+def gen_lp_big():
+    """tests/golden/lp_big.json: reference solves of 258-node pipelines (slow: ~7 min in total)."""
+    import time
+
+    rows = []
+    for kind, R, C, M in BIG_LP_CASES:
+        fw, ba, bp = _het(R * C)
+        w0 = time.time()
+        p = ref.plan(kind, R, C, M, fw, ba, bp, 0.8, 0, 0)
+        rows.append({"name": f"{kind}_r{R}c{C}m{M}_big", "kind": kind, "R": R, "C": C, "M": M, "fwd": fw, "bact": ba,
+                     "bparam": bp, "r_max": 0.8, "lambda_mode": 0, "budget_all": 0,
+                     **{k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in p.items()},
+                     "wall_s": time.time() - w0})
+    dump("lp_big.json", rows)
+
+
 def gen_monitor():
     out = []
     for M, S, fw, ba, bp, plan, sigma, seed in [(2, 2, [1.0, 2.0], [1.0, 1.5], [1.0, 2.5], [160, 200, 250, 400], 0.0, 13),
@@ -201,7 +233,7 @@ def gen_sgd():
     dump("sgd.json", out)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     fx = fixtures()
     dump("fixtures.json", fx)
     gen_rng()
@@ -238,3 +270,6 @@ def gen_artifacts(fx):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "artifacts":
     gen_artifacts(fixtures())
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lp_big":
+    gen_lp_big()

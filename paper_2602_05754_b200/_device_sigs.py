@@ -65,6 +65,7 @@ DEVICE_SIGNATURES = {
     "pf_trainer_create": ([ctypes.POINTER(PfModelCfg), ctypes.POINTER(PfTrainCfg), ctypes.POINTER(c_vp)], c_int),
     "pf_trainer_destroy": ([c_vp], c_int),
     "pf_trainer_step": ([c_vp, c_int, c_vp, c_vp, ctypes.POINTER(PfStepResult)], c_int),
+    "pf_trainer_step_masks": ([c_vp, c_int, c_vp, c_vp, c_vp, ctypes.POINTER(PfStepResult)], c_int),
     "pf_trainer_set_override": ([c_vp, c_d], c_int),
     "pf_trainer_set_plan": ([c_vp, c_vp], c_int),
     "pf_trainer_get_plan": ([c_vp, c_vp, c_vp, c_vp, c_vp], c_int),

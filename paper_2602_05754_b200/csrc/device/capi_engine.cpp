@@ -297,10 +297,15 @@ int pf_trainer_destroy(pf_ctx* ctx) {
 }
 
 int pf_trainer_step(pf_ctx* ctx, int t, const int32_t* tok, const int32_t* tgt, pf_step_result* out) {
+  return pf_trainer_step_masks(ctx, t, tok, tgt, nullptr, out);
+}
+
+int pf_trainer_step_masks(pf_ctx* ctx, int t, const int32_t* tok, const int32_t* tgt, const uint64_t* masks,
+                          pf_step_result* out) {
   return guard([&] {
     if (!ctx) return PF_ERR_INVALID;
     pf::StepResult r;
-    const int rc = ctx->trainer->step(t, tok, tgt, &r);
+    const int rc = ctx->trainer->step(t, tok, tgt, &r, masks);
     if (rc == PF_OK && out) {
       out->loss = r.loss;
       out->batch_ms = r.batch_ms;

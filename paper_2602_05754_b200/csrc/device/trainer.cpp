@@ -203,8 +203,35 @@ void Trainer::set_plan(const std::vector<double>& ratios) {
   if (static_cast<int>(ratios.size()) != S * M) throw std::invalid_argument("set_plan: need M*S ratios");
   plan_ratios_ = ratios;
   plan_ready_ = true;
+  mask_stream_.reset();
   next_t_ = -1;  // prefetched masks used the old plan
 }
+
+int Trainer::mask_words(int li) const { return stages_[static_cast<std::size_t>(li)]->words(); }
+
+const MaskStream& Trainer::mask_stream() {
+  if (!mask_stream_) {
+    const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
+    std::vector<int> units_all;
+    for (int s = 1; s <= S; ++s) units_all.push_back(stage_units(model_, stage_spec(model_, s, S)));
+    mask_stream_ = std::make_unique<MaskStream>(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
+  }
+  return *mask_stream_;
+}
+
+namespace {
+// splitmix64 finaliser over non-overlapping (t, s, m) fields: per-cell seeds of the
+// override / hybrid masks without int overflow or collisions across stages
+uint64_t cell_seed(uint64_t seed, uint64_t salt, int t, int s, int m) {
+  uint64_t z = seed ^ salt;
+  z += (static_cast<uint64_t>(static_cast<uint32_t>(t)) << 32) ^ (static_cast<uint64_t>(s & 0xFFFF) << 16) ^
+       static_cast<uint64_t>(m & 0xFFFF);
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+}  // namespace
 
 FreezeMask Trainer::apf_base_mask(int li) const {
   const Stage& st = *stages_[static_cast<std::size_t>(li)];
@@ -305,6 +332,7 @@ void Trainer::solve_plan_from_monitoring() {
     for (int m = 1; m <= M; ++m)
       plan_ratios_[static_cast<std::size_t>((s - 1) * M + (m - 1))] = plan_.ratio_of(freeze_node(cfg_.pipeline, m, s));
   plan_ready_ = true;
+  mask_stream_.reset();
   lp_solve_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -314,8 +342,7 @@ void Trainer::build_masks(int t, Phase phase, bool controller, uint64_t* out, lo
   const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
   *frozen = 0;
   *total = 0;
-  std::vector<int> units_all;
-  for (int s = 1; s <= S; ++s) units_all.push_back(stage_units(model_, stage_spec(model_, s, S)));
+  (void)S;
   for (std::size_t li = 0; li < stages_.size(); ++li) {
     const int s = stage_ids_[li];
     const int units = stages_[li]->units();
@@ -325,20 +352,19 @@ void Trainer::build_masks(int t, Phase phase, bool controller, uint64_t* out, lo
                              (phase == Phase::ProgressiveFreeze || phase == Phase::StableFreeze);
     if (hybrid_cell) {
       // Alg. 2: grow / shrink the APF base set to the cell's exact TimelyFreeze count
-      MaskStream ms(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
+      const MaskStream& ms = mask_stream();
       const FreezeMask base = apf_base_mask(static_cast<int>(li));
       for (int m = 1; m <= M; ++m) {
-        Rng rng(cfg_.seed ^ (0x2545f4914f6cdd1dULL * static_cast<uint64_t>((t * 4096 + s) * 4096 + m)));
+        Rng rng(cell_seed(cfg_.seed, 0x2545f4914f6cdd1dULL, t, s, m));
         const auto mk = reconcile_mask(base, ms.cell_count(t, s, m), rng);
         std::memcpy(tmp.data() + static_cast<std::size_t>(m - 1) * static_cast<std::size_t>(words), mk.words().data(),
                     static_cast<size_t>(words) * 8);
       }
     } else if (controller) {
-      MaskStream ms(plan_ratios_, cfg_.phases, M, units_all, cfg_.seed);
-      ms.stage_step_masks(t, s, tmp.data(), cfg_.mask_threads);
+      mask_stream().stage_step_masks(t, s, tmp.data(), cfg_.mask_threads);
     } else {
       for (int m = 1; m <= M; ++m) {
-        Rng rng(cfg_.seed ^ (0x51ed270b27f2e6a1ULL * static_cast<uint64_t>(t * 4096 + s * 64 + m)));
+        Rng rng(cell_seed(cfg_.seed, 0x51ed270b27f2e6a1ULL, t, s, m));
         const auto mk = sample_mask(units, override_ratio_, rng);
         std::memcpy(tmp.data() + static_cast<std::size_t>(m - 1) * static_cast<std::size_t>(words), mk.words().data(),
                     static_cast<size_t>(words) * 8);
@@ -357,13 +383,15 @@ void Trainer::build_masks(int t, Phase phase, bool controller, uint64_t* out, lo
   }
 }
 
-int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepResult* out) {
+int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepResult* out,
+                  const uint64_t* host_masks) {
   cudaSetDevice(cfg_.device);
   const int S = cfg_.pipeline.total_stages(), M = cfg_.pipeline.num_microbatches;
   const int T = model_.tokens();
   StepResult res;
   Phase phase = Phase::StableFreeze;
-  const bool controller = override_ratio_ < 0.0;
+  const bool controller = override_ratio_ < 0.0 && !host_masks;
+  const int stamp = ++stamp_;
   if (controller) {
     phase = phase_of(t, cfg_.phases);
     if (phase == Phase::Solve && !plan_ready_) solve_plan_from_monitoring();
@@ -373,7 +401,23 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   // ---- masks for this step's cells (host, jump-ahead into the single stream);
   // usually already generated while the previous step ran on the GPU
   const auto tm0 = std::chrono::steady_clock::now();
-  if (next_t_ == t && next_override_ == override_ratio_ && next_plan_ready_ == plan_ready_) {
+  if (host_masks) {  // caller-owned masks (reference plan / mask history replay)
+    res.frozen_units = res.total_units = 0;
+    long long src = 0;
+    for (std::size_t li = 0; li < stages_.size(); ++li) {
+      const int words = stages_[li]->words();
+      const int units = stages_[li]->units();
+      for (int m = 0; m < M; ++m) {
+        uint64_t* dst = masks_host_ + mask_offsets_[li] + static_cast<long long>(m) * (words + 1);
+        std::memcpy(dst, host_masks + src, static_cast<size_t>(words) * 8);
+        if (units % 64) dst[words - 1] &= (1ULL << (units % 64)) - 1;  // bits past the last unit are not units
+        dst[words] = 0;
+        src += words;
+        for (int w = 0; w < words; ++w) res.frozen_units += __builtin_popcountll(dst[w]);
+        res.total_units += units;
+      }
+    }
+  } else if (next_t_ == t && next_override_ == override_ratio_ && next_plan_ready_ == plan_ready_) {
     std::swap(masks_host_, masks_next_);
     res.frozen_units = next_frozen_;
     res.total_units = next_total_;
@@ -459,7 +503,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
     } else if (a.kind == ActionKind::Weight) {  // split backward: dW of the slot's microbatch
       const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
       PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
-      PF_TRY(st.backward_weight(slot, mw, t, stream_));
+      PF_TRY(st.backward_weight(slot, mw, stamp, stream_));
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
     } else {
       const bool recv_dy = a.stage < S && local_index(a.stage + 1) < 0;
@@ -486,7 +530,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       }
       const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
       PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
-      PF_TRY(st.backward(slot, tok, mw, dy, dx, t, stream_));
+      PF_TRY(st.backward(slot, tok, mw, dy, dx, stamp, stream_));
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
       if (recv_dy) PF_CUDA(cudaEventRecord(dy_free_ev_[ls][ss], stream_));
       if (send_dx) {  // to b(m, s-1)
@@ -508,7 +552,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   OptimCfg oc = cfg_.optim;
   oc.lr = static_cast<float>(cfg_.lr);
   for (auto& st : stages_)
-    PF_TRY(st->optimizer_step(oc, M, t, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
+    PF_TRY(st->optimizer_step(oc, M, stamp, apf_step, cfg_.apf_alpha, cfg_.apf_threshold, stream_));
   PF_CUDA(cudaEventRecord(ev_opt1_, stream_));
   PF_CUDA(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, stream_));
   if (apf_step && cfg_.hybrid) {  // per-unit APF eligibility counts for the next steps' base sets
@@ -525,7 +569,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   }
   // the next step's masks while this one runs (not in hybrid mode, whose base set comes from
   // this step's APF result, nor across the LP solve, which changes the plan)
-  if (!cfg_.hybrid && (!controller || t + 1 <= cfg_.phases.t_total)) {
+  if (!host_masks && !cfg_.hybrid && (!controller || t + 1 <= cfg_.phases.t_total)) {
     const Phase next_phase = controller ? phase_of(t + 1, cfg_.phases) : Phase::StableFreeze;
     if (!(controller && next_phase == Phase::Solve && !plan_ready_)) {
       build_masks(t + 1, next_phase, controller, masks_next_, &next_frozen_, &next_total_);
@@ -579,7 +623,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
                                 (cfg_.phases.t_freeze - cfg_.phases.t_monitor));
     if (!controller || phase == Phase::ProgressiveFreeze || phase == Phase::StableFreeze) {
       FreezePlan p = plan_;
-      if (!controller)
+      if (!controller && !host_masks)
         for (auto& [k, r] : p.ratios) r = override_ratio_;
       res.predicted_ms = longest_path_start_times(*dag_, plan_weights(*dag_, plan_profile_, p, scale)).makespan;
     }

@@ -62,13 +62,20 @@ class Trainer {
   ~Trainer();
 
   // host_tokens / host_targets: [M][T] int32 (pinned or pageable) or null to
-  // use device-resident synthetic tokens.
-  int step(int t, const int* host_tokens, const int* host_targets, StepResult* out);
+  // use device-resident synthetic tokens. host_masks: caller-owned frozen-unit
+  // masks for every local cell (per local stage, M masks of ceil(units/64) words,
+  // FreezeMask::test bit order) instead of the controller's; null = controller.
+  int step(int t, const int* host_tokens, const int* host_targets, StepResult* out,
+           const uint64_t* host_masks = nullptr);
+  // device gradient stamp of the last step (internal counter, 1 for the first step)
+  int stamp() const { return stamp_; }
 
   void set_override(double ratio) {
     override_ratio_ = ratio;
     next_t_ = -1;
   }
+  // words of local stage li's masks (ceil(units / 64))
+  int mask_words(int li) const;
   void set_plan(const std::vector<double>& ratios);
   bool has_plan() const { return plan_ready_; }
   const std::vector<double>& plan_ratios() const { return plan_ratios_; }
@@ -110,6 +117,7 @@ class Trainer {
 
  private:
   int local_index(int stage) const;
+  const pipefreeze::MaskStream& mask_stream();
   void solve_plan_from_monitoring();
   void build_masks(int t, pipefreeze::Phase phase, bool controller, uint64_t* out, long long* frozen,
                    long long* total);
@@ -162,6 +170,13 @@ class Trainer {
   bool apf_base_ready_ = false;
   int* apf_pinned_ = nullptr;
   double lp_solve_ms_ = 0.0;
+  // Gradient stamps (Stage::unit_stamp): an internal counter that starts at 1 and rises by
+  // one every step, independent of the caller's t, so a unit's first dW of a step always
+  // overwrites G (which is never memset) and a repeated t cannot accumulate old gradients.
+  int stamp_ = 0;
+  // The reference mask stream of the current plan. Kept across steps so its step-prefix cache
+  // grows incrementally (O(1) amortised per step, not O(t)); rebuilt when the plan changes.
+  std::unique_ptr<pipefreeze::MaskStream> mask_stream_;
 };
 
 }  // namespace pf

@@ -223,11 +223,33 @@ class Trainer:
         except Exception:
             pass
 
-    def step(self, t: int, tokens: np.ndarray | None = None, targets: np.ndarray | None = None) -> dict:
+    def _host_ids(self, a: np.ndarray | None, what: str):
+        """[M, T] int32 C-contiguous (the C side copies M*T*4 bytes); keeps the array alive."""
+        if a is None:
+            return None, None
+        if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous):
+            a = np.ascontiguousarray(a, dtype=np.int32)
+        if a.size != self.M * self.shape.tokens:
+            raise ValueError(f"{what}: need {self.M} x {self.shape.tokens} ids, got shape {a.shape}")
+        return a, a.ctypes.data_as(ctypes.c_void_p)
+
+    def step(self, t: int, tokens: np.ndarray | None = None, targets: np.ndarray | None = None,
+             masks: np.ndarray | None = None) -> dict:
+        """One training step. masks: caller-owned frozen-unit masks of every local cell (per local
+        stage, M masks of ceil(units/64) uint64 words, FreezeMask::test bit order) instead of the
+        controller's (pf_trainer_step_masks)."""
         r = PfStepResult()
-        tp = tokens.ctypes.data_as(ctypes.c_void_p) if tokens is not None else None
-        gp = targets.ctypes.data_as(ctypes.c_void_p) if targets is not None else None
-        _check(self.lib.pf_trainer_step(self._ctx, t, tp, gp, ctypes.byref(r)), f"trainer_step(t={t})")
+        tokens, tp = self._host_ids(tokens, "tokens")
+        targets, gp = self._host_ids(targets, "targets")
+        if masks is None:
+            _check(self.lib.pf_trainer_step(self._ctx, t, tp, gp, ctypes.byref(r)), f"trainer_step(t={t})")
+        else:
+            need = sum(self.M * ((self.stage_buffers(i)["n_units"] + 63) // 64) for i in range(self.info["local_stages"]))
+            mk = np.ascontiguousarray(masks, dtype=np.uint64)
+            if mk.size != need:
+                raise ValueError(f"masks: need {need} words, got {mk.size}")
+            _check(self.lib.pf_trainer_step_masks(self._ctx, t, tp, gp, mk.ctypes.data_as(ctypes.c_void_p),
+                                                  ctypes.byref(r)), f"trainer_step_masks(t={t})")
         return {k: getattr(r, k) for k, _ in PfStepResult._fields_}
 
     def set_override(self, ratio: float | None) -> None:
