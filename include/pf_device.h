@@ -158,7 +158,7 @@ int pf_swiglu_fwd(const void* gu, void* a, int T, int ffn, void* stream);
 int pf_swiglu_bwd(const void* gu, const void* da, void* dgu, int T, int ffn, void* stream);
 int pf_rope_fwd(void* qkv, int T, int seq, int nh, int nkv, int hd, float theta, void* stream);
 /* qkv[T, (nh + 2 nkv) hd] = h[T, K] . Wqkv^T with the rotate-half RoPE of the q and k heads fused in
- * the CTA-pair epilogue (== pf_gemm_bf16 then pf_rope_fwd, bit for bit); hd == 64. */
+ * the CTA-pair epilogue (== pf_gemm_bf16 then pf_rope_fwd, bit for bit); hd == 64 or 128. */
 int pf_gemm_rope(const void* h, long long ldh, const void* Wqkv, long long ldw, void* qkv, int T, int seq, int nh,
                  int nkv, int hd, int K, float theta, void* stream);
 int pf_cross_entropy(void* logits, const int* targets, float* loss_sum, int T, int V, float grad_scale,

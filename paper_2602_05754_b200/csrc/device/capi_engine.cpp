@@ -184,7 +184,7 @@ int pf_rope_fwd(void* qkv, int T, int seq, int nh, int nkv, int hd, float theta,
 int pf_gemm_rope(const void* h, long long ldh, const void* Wqkv, long long ldw, void* qkv, int T, int seq, int nh,
                  int nkv, int hd, int K, float theta, void* stream) {
   return guard([&] {
-    if (!h || !Wqkv || !qkv || hd != 64) return static_cast<int>(PF_ERR_INVALID);
+    if (!h || !Wqkv || !qkv || (hd != 64 && hd != 128)) return static_cast<int>(PF_ERR_INVALID);
     float2* cs = nullptr;
     if (cudaMallocAsync(&cs, static_cast<size_t>(seq) * (hd / 2) * sizeof(float2), S(stream)) != cudaSuccess)
       return static_cast<int>(PF_ERR_CUDA);
@@ -194,6 +194,7 @@ int pf_gemm_rope(const void* h, long long ldh, const void* Wqkv, long long ldw, 
       pf::GemmOut out{qkv, N};
       out.rope = cs;
       out.rope_seq = seq;
+      out.rope_hd = hd;
       out.rope_cols = (nh + nkv) * hd;
       rc = pf::gemm_bf16_pair(pf::GemmOperand{h, ldh, false}, pf::GemmOperand{Wqkv, ldw, false}, out, T, N, K, 1.0f,
                               pf::EPI_ROPE, S(stream));

@@ -99,7 +99,7 @@ struct alignas(64) Params2 {
   const __nv_bfloat16* bias;  // EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (nullptr: none)
   float* colsum;              // EPI_DGELU: += column sums of d(pre) (the fc1 bias gradient; nullptr: none)
   const float2* rope;         // EPI_ROPE: (cos, sin) [seq][32]
-  int rope_seq, rope_cols;
+  int rope_seq, rope_cols, rope_hd;
   int streamk;   // 0: one tile per work item; 1/2: stream-K (2: data-parallel full waves first)
   int dp_tiles;  // stream-K: tiles [0, dp_tiles) run whole, round-robin over the clusters
   long long sk_q;  // stream-K: iterations of the split region per cluster
@@ -510,41 +510,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[abuf], aphase);
       tc_fence_after();
       if constexpr (EPI == EPI_ROPE) {
-        // qkv projection with rotate-half RoPE (head_dim 64): per head of the tile, the thread of
-        // (row, half) holds j in [16 half, 16 half + 16) and its partner j + 32, rotates them with
-        // the (cos, sin) of the row's position (q and k heads only) and writes the two 128 x 32
-        // boxes of the head into buffer hh & 1, stored by TMA (= GEMM then rope_fwd_kernel).
+        // qkv projection with rotate-half RoPE (head_dim 64 or 128). The tile is walked in BN / 64
+        // pieces of two 128 x 32 boxes: a = columns [ca, ca + 32) of a head and its rotation
+        // partner b = a + hd / 2 (hd 64: one head per piece, ca = 0; hd 128: piece c of a head,
+        // ca = 32 c). The thread of (row, half) holds j in [ca + 16 half, ca + 16 half + 16) and
+        // j + hd / 2, rotates them with the (cos, sin) of the row's position (q and k heads only)
+        // and writes the two boxes into buffer pp & 1, stored by TMA (= GEMM then rope_fwd_kernel).
         const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
         const bool elected = threadIdx.x == 64;
-        // (cos, sin) of this row's position for j in [16 half, 16 half + 16): the same for every
-        // head of the tile, loaded once (as float4 pairs) while the MMAs still run
-        float2 csr[16];
-        {
-          const float4* c4 = reinterpret_cast<const float4*>(p.rope + static_cast<long long>(grow % p.rope_seq) * 32 +
-                                                             half * 16);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 v = __ldg(c4 + i);
-            csr[2 * i] = make_float2(v.x, v.y);
-            csr[2 * i + 1] = make_float2(v.z, v.w);
-          }
-        }
+        const int hd = p.rope_hd;
+        const float2* cs_row = p.rope + static_cast<long long>(grow % p.rope_seq) * (hd / 2);
 #pragma unroll 1
-        for (int hh = 0; hh < BN / 64; ++hh) {
+        for (int pp = 0; pp < BN / 64; ++pp) {
+          // columns of box a within the tile, the head's first column, j of this thread's first value
+          const int head0 = hd == 64 ? pp * 64 : (pp >> 1) * 128;
+          const int ca = hd == 64 ? 0 : (pp & 1) * 32;
+          const int acol = head0 + ca, bcol = acol + hd / 2;
           uint32_t ra[16], rb[16];
-          const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                              static_cast<uint32_t>(abuf * BN + hh * 64 + half * 16);
-          uint8_t* buf = sE + (hh & 1) * Cfg::EPI_BUF;
-          if (hh == 0) {
+          const uint32_t tb = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(abuf * BN);
+          uint8_t* buf = sE + (pp & 1) * Cfg::EPI_BUF;
+          if (pp == 0) {
             mbar_wait(&tfull_bar[abuf], aphase);
             tc_fence_after();
           }
-          tmem_ld_32x32b_x16(tb, ra);
-          tmem_ld_32x32b_x16(tb + 32, rb);
-          if (elected) bulk_wait_read1();  // the stores of head hh - 2 (this buffer) have read it
+          tmem_ld_32x32b_x16(tb + static_cast<uint32_t>(acol + half * 16), ra);
+          tmem_ld_32x32b_x16(tb + static_cast<uint32_t>(bcol + half * 16), rb);
+          // (cos, sin) of j in [ca + 16 half, ca + 16 half + 16) at this row's position (L1-resident)
+          float2 csr[16];
+          {
+            const float4* c4 = reinterpret_cast<const float4*>(cs_row + ca + half * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 v = __ldg(c4 + i);
+              csr[2 * i] = make_float2(v.x, v.y);
+              csr[2 * i + 1] = make_float2(v.z, v.w);
+            }
+          }
+          if (elected) bulk_wait_read1();  // the stores of piece pp - 2 (this buffer) have read it
           named_bar_sync(1, kEpiThreads);
           tmem_ld_wait();
-          const bool rot = tn * BN + hh * 64 < p.rope_cols;
+          const bool rot = tn * BN + head0 < p.rope_cols;
 #pragma unroll
           for (int s2 = 0; s2 < 2; ++s2) {
             const int off = row * 64 + (((2 * half + s2) ^ ((row >> 1) & 3)) << 4);
@@ -573,8 +578,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, kEpiThreads);
           if (elected) {
-            tma_store_2d(&p.te_out, buf, tn * BN + hh * 64, y0);
-            tma_store_2d(&p.te_out, buf + 8192, tn * BN + hh * 64 + 32, y0);
+            tma_store_2d(&p.te_out, buf, tn * BN + acol, y0);
+            tma_store_2d(&p.te_out, buf + 8192, tn * BN + bcol, y0);
             bulk_commit();
           }
         }
@@ -1028,8 +1033,11 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
   p.ldaux = C.ldaux;
   p.bias = static_cast<const __nv_bfloat16*>(C.bias);
   if (p.bias && epi != EPI_STORE_BF16 && epi != EPI_ADD_BF16 && epi != EPI_GELU) return PF_ERR_INVALID;
-  if (epi == EPI_ROPE) {  // qkv [M][N] out by TMA, q/k heads of 64 columns rotated
-    if (N % BN != 0 || B.mn_major || !C.rope || C.rope_seq <= 0 || C.rope_cols % 64 != 0) return PF_ERR_INVALID;
+  if (epi == EPI_ROPE) {  // qkv [M][N] out by TMA, q/k heads of 64 or 128 columns rotated
+    if (N % BN != 0 || B.mn_major || !C.rope || C.rope_seq <= 0 || (C.rope_hd != 64 && C.rope_hd != 128) ||
+        C.rope_cols % C.rope_hd != 0)
+      return PF_ERR_INVALID;
+    p.rope_hd = C.rope_hd;
     if ((rc = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128))) return rc;
     p.rope = static_cast<const float2*>(C.rope);
     p.rope_seq = C.rope_seq;

@@ -38,7 +38,8 @@ struct GemmOut {
   long long ldaux = 0;
   const void* bias = nullptr;  // CTA-pair EPI_STORE_BF16 / EPI_ADD_BF16: + bias[col] (bf16 [N])
   float* colsum = nullptr;     // CTA-pair EPI_DGELU: += column sums of the bf16 output (a bias gradient)
-  const void* rope = nullptr;  // CTA-pair EPI_ROPE: float2 (cos, sin) table [seq][32]
+  const void* rope = nullptr;  // CTA-pair EPI_ROPE: float2 (cos, sin) table [seq][rope_hd / 2]
+  int rope_hd = 64;            // EPI_ROPE: head_dim, 64 or 128
   int rope_seq = 0;            // EPI_ROPE: positions per sequence (row t is position t % seq)
   int rope_cols = 0;           // EPI_ROPE: columns [0, rope_cols) are q and k heads (rotated)
 };

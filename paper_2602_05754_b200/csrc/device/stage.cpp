@@ -155,10 +155,11 @@ int gemm_fwd_rope(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* W,
     return !(e && e[0] == '0');
   }();
   const int N = (nh + 2 * nkv) * hd;
-  if (use_pair() && fuse_swiglu() && fuse && hd == 64 && M >= 256 && N % 256 == 0) {
+  if (use_pair() && fuse_swiglu() && fuse && (hd == 64 || hd == 128) && M >= 256 && N % 256 == 0) {
     GemmOut out{qkv, N};
     out.rope = rope;
     out.rope_seq = seq;
+    out.rope_hd = hd;
     out.rope_cols = (nh + nkv) * hd;
     return gemm_bf16_pair(GemmOperand{A, lda, false}, GemmOperand{W, ldw, false}, out, M, N, K, 1.0f, EPI_ROPE, s);
   }

@@ -391,7 +391,7 @@ int pf_apf_update_host(int n, double alpha, double* ema, double* ema_abs, const 
     need(ema, "ema");
     need(ema_abs, "ema_abs");
     need(delta, "delta");
-    ApfState st{std::vector<double>(ema, ema + n), std::vector<double>(ema_abs, ema_abs + n), alpha};
+    ApfState st{Vector(ema, ema + n), Vector(ema_abs, ema_abs + n), alpha};
     if (!(alpha > 0.0 && alpha < 1.0)) throw config_error("apf alpha must lie in (0, 1)");
     const auto sc = apf_update(st, std::vector<double>(delta, delta + n));
     std::copy(st.ema.begin(), st.ema.end(), ema);

@@ -150,10 +150,10 @@ int autofreeze_select(const std::vector<double>& scores, int prefix, double perc
 
 ApfState ApfState::zeros(std::size_t n, double alpha) {
   if (!(alpha > 0.0 && alpha < 1.0)) throw config_error("apf alpha must lie in (0, 1)");
-  return ApfState{std::vector<double>(n, 0.0), std::vector<double>(n, 0.0), alpha};
+  return ApfState{Vector(n, 0.0), Vector(n, 0.0), alpha};
 }
 
-std::vector<double> apf_update(ApfState& st, const std::vector<double>& delta) {
+Vector apf_update(ApfState& st, const std::vector<double>& delta) {
   if (delta.size() != st.ema.size()) throw std::domain_error("apf update dimension mismatch");
   const double a = st.alpha, b = 1.0 - st.alpha;
   std::vector<double> score(delta.size());

@@ -67,15 +67,42 @@ FreezeMask reconcile_mask(const FreezeMask& base, int target_count, Rng& rng);
 double autofreeze_score(double norm_prev, double norm_cur);
 int autofreeze_select(const std::vector<double>& scores, int frozen_prefix_len, double percentile);
 
+// Dense fp64 vector of the APF state: a std::vector<double> that also takes the element-access
+// spelling of the reference's Eigen::VectorXd (v(i), Constant, Zero), so the reference's call
+// sites and its own unit suite (tests/test_freezectl.cpp, built by oracle/Makefile product-check)
+// compile unchanged against this header; Eigen is not installed here.
+struct Vector : std::vector<double> {
+  using std::vector<double>::vector;
+  Vector() = default;
+  Vector(const std::vector<double>& v) : std::vector<double>(v) {}  // NOLINT: implicit, like the reference
+  double& operator()(std::size_t i) { return (*this)[i]; }
+  double operator()(std::size_t i) const { return (*this)[i]; }
+  static Vector Constant(std::size_t n, double v) { return Vector(n, v); }
+  static Vector Zero(std::size_t n) { return Vector(n, 0.0); }
+  // comma initialiser: v << a, b, c;
+  struct CommaInit {
+    Vector& v;
+    std::size_t i;
+    CommaInit& operator,(double x) {
+      v.at(i++) = x;
+      return *this;
+    }
+  };
+  CommaInit operator<<(double x) {
+    at(0) = x;
+    return CommaInit{*this, 1};
+  }
+};
+
 struct ApfState {
-  std::vector<double> ema;      // E
-  std::vector<double> ema_abs;  // E_abs
+  Vector ema;      // E
+  Vector ema_abs;  // E_abs
   double alpha{0.9};
 
   static ApfState zeros(std::size_t n, double alpha = 0.9);
 };
 
-std::vector<double> apf_update(ApfState& state, const std::vector<double>& delta);
+Vector apf_update(ApfState& state, const std::vector<double>& delta);
 std::vector<int> apf_eligible(const std::vector<double>& scores, double threshold);
 
 struct MaskRecord {

@@ -117,13 +117,15 @@ def test_gemm_swiglu_epilogue_matches_unfused(cuda):
     assert torch.equal(a, a_ref)
 
 
-@pytest.mark.parametrize("T,S,nh,nkv,D", [(4096, 2048, 32, 8, 2048), (512, 128, 4, 4, 256), (300, 100, 6, 1, 256)])
-def test_gemm_rope_epilogue_matches_unfused(cuda, T, S, nh, nkv, D):
+@pytest.mark.parametrize("T,S,nh,nkv,D,hd", [(4096, 2048, 32, 8, 2048, 64), (512, 128, 4, 4, 256, 64),
+                                             (300, 100, 6, 1, 256, 64), (4096, 2048, 32, 8, 4096, 128),
+                                             (2048, 2048, 40, 40, 5120, 128), (384, 128, 2, 1, 256, 128)])
+def test_gemm_rope_epilogue_matches_unfused(cuda, T, S, nh, nkv, D, hd):
     """qkv projection with RoPE fused in the pair-GEMM epilogue == GEMM then rope_fwd, bit for bit
-    (GQA widths; T = 300 leaves a partial row tile, S = 100 several sequences per microbatch)."""
+    (GQA widths; T = 300 leaves a partial row tile, S = 100 several sequences per microbatch;
+    head_dim 128 at the LLaMA-8B (32/8) and LLaMA-13B (40/40 MHA) shapes)."""
     import torch
 
-    hd = 64
     N = (nh + 2 * nkv) * hd
     g = torch.Generator().manual_seed(T + nh)
     x = bf(torch.randn(T, D, generator=g)).cuda()
@@ -222,21 +224,26 @@ def test_gemm_dswiglu_epilogue_matches_unfused(cuda, T, ffn, D):
     assert (dgus[1].float() - dgu_ref.float()).abs().max().item() <= 1e-2 * dgu_ref.float().abs().max().item()
 
 
-def test_rope_matches_reference(cuda):
+@pytest.mark.parametrize("B,S,nh,nkv,hd,theta", [(2, 64, 4, 2, 64, 500000.0), (2, 2048, 32, 8, 128, 500000.0),
+                                                 (1, 2048, 40, 40, 128, 10000.0)])
+def test_rope_matches_reference(cuda, B, S, nh, nkv, hd, theta):
+    """rope_fwd vs the fp32 rotate-half restatement, head_dim 64 and 128 (LLaMA-8B / 13B shapes)."""
     import torch
 
     from llama_ref import rope
 
-    B, S, nh, nkv, hd = 2, 64, 4, 2, 64
     T = B * S
     W = (nh + 2 * nkv) * hd
     g = torch.Generator().manual_seed(3)
     qkv = bf(torch.randn(T, W, generator=g)).cuda()
     ref = qkv.float().view(B, S, nh + 2 * nkv, hd).clone()
-    ref[:, :, : nh + nkv] = rope(ref[:, :, : nh + nkv], S, 500000.0)
-    chk(lib().pf_rope_fwd(qkv.data_ptr(), T, S, nh, nkv, hd, 500000.0, sp()))
+    ref[:, :, : nh + nkv] = rope(ref[:, :, : nh + nkv], S, theta)
+    chk(lib().pf_rope_fwd(qkv.data_ptr(), T, S, nh, nkv, hd, theta, sp()))
     torch.cuda.synchronize()
-    assert (qkv.float().view_as(ref) - ref).abs().max().item() < 2e-2
+    got = qkv.float().view_as(ref)
+    # bf16 output: one rounding of the fp32 rotation (|x| <~ 5 -> ulp <= 2^-5)
+    assert (got - ref).abs().max().item() < 2e-2
+    assert torch.equal(got[:, :, nh + nkv:], ref[:, :, nh + nkv:])  # v heads untouched
 
 
 @pytest.mark.parametrize("V", [4096, 1024, 1000, 128256, 32000, 8, 65544])

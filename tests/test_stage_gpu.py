@@ -57,7 +57,7 @@ def test_stage_step_matches_torch_reference(cuda, override, dw, monkeypatch):
         for v in params.values():
             v.grad = None
         loss = stage_loss(params, shape, range(shape.layers), torch.tensor(tokens[m], device=cuda).long(),
-                          torch.tensor(targets[m], device=cuda).long(), True, True)
+                          torch.tensor(targets[m], device=cuda).long(), True, True, faithful=True)
         loss.backward()
         losses.append(loss.item())
         for ent in lay["units"]:
@@ -127,7 +127,7 @@ def test_multi_stage_rank_matches_torch_reference(cuda, schedule, stages_per_ran
         for v in params.values():
             v.grad = None
         loss = stage_loss(params, shape, range(shape.layers), torch.tensor(tokens[m], device=cuda).long(),
-                          torch.tensor(targets[m], device=cuda).long(), True, True)
+                          torch.tensor(targets[m], device=cuda).long(), True, True, faithful=True)
         loss.backward()
         losses.append(loss.item())
         for i in range(S):
