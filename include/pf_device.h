@@ -225,7 +225,8 @@ int pf_trainer_set_plan(pf_ctx* ctx, const double* ratios /* (s-1)*M + (m-1) */)
  * w_min / w_max: one entry per action node in ActionId order (2*S*M, or 3*S*M for zbv-split). */
 int pf_trainer_get_plan(pf_ctx* ctx, double* ratios, double* out3, double* w_min, double* w_max);
 int pf_trainer_action_ms(pf_ctx* ctx, double* ms, int* kinds, int* microbatches, int* stages);
-/* start of each action of the last step relative to the rank's first action (ms, CUDA events) */
+/* start of each action of the last step relative to the step origin: a CUDA event recorded when
+ * pf_trainer_step began enqueueing (ranks that barrier right before the call share one time axis) */
 int pf_trainer_action_starts(pf_ctx* ctx, double* start_ms);
 int pf_trainer_get_info(pf_ctx* ctx, pf_trainer_info* info);
 /* Raw buffers of local stage i (tests): fp32 master / grad, bf16 weights, unit stamps, device unit table. */

@@ -38,6 +38,12 @@ const char* pf_last_error(void);
 int pf_schedule_build(int kind, int R, int C, int M, int* actions, int* lens);
 /* stage_to_rank (schedule.hpp:30) */
 int pf_stage_to_rank(int kind, int R, int C, int M, int stage, int* rank);
+/* The issue program of one rank (addition; the reference has no transport): its actions in
+ * schedule order (build_schedule) with the P2P transfers of the cross-rank DAG rule-3 edges
+ * (proj/src/dag.cpp:90-93) around each. ops: rows of 5 ints (kind, microbatch, stage,
+ * recv_from rank or -1, send_to rank or -1); *n = rows (at most 3*M*C). The device trainer walks
+ * exactly this program (trainer.cpp); tests/test_pipeline_p2p_gloo.py replays it over gloo. */
+int pf_issue_program(int kind, int R, int C, int M, int rank, int* ops, int* n);
 
 /* build_dag + topological_order + dag_to_json_text (dag.hpp:69, :45, :84).
  * edges: insertion order (from, to) pairs; json may be NULL. */

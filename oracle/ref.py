@@ -31,6 +31,11 @@ def lib() -> ctypes.CDLL:
             raise FileNotFoundError(f"{LIB_PATH} not built (make -C oracle)")
         L = ctypes.CDLL(LIB_PATH)
         L.ref_last_error.restype = ctypes.c_char_p
+        L.ref_param_pass.restype = ctypes.c_double
+        L.ref_param_pass.argtypes = [ctypes.c_long, ctypes.c_long, ctypes.c_long, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_int, ctypes.c_long, ctypes.c_double]
+        L.ref_controller_step.restype = ctypes.c_double
+        L.ref_controller_step.argtypes = [ctypes.c_int] * 5 + [ctypes.c_double, ctypes.c_uint64, ctypes.c_void_p]
         L.ref_cpu_step.restype = ctypes.c_double
         L.ref_cpu_step.argtypes = [ctypes.c_int] * 5 + [ctypes.c_long, ctypes.c_double, ctypes.c_uint64]
         _lib = L
@@ -201,6 +206,20 @@ def masked_sgd(diag, theta0, eta, M, steps, sigma, policy, param, seed):
     _chk(lib().ref_masked_sgd(d, _p(dg), _p(t0), ctypes.c_double(eta), M, steps, ctypes.c_double(sigma), policy,
                               ctypes.c_double(param), ctypes.c_uint64(seed), _p(th), _p(gs)))
     return th, gs
+
+
+def param_pass_seconds(begin, end, block, masks, per_unit, lr=0.01) -> float:
+    """ref_param_pass: elements [begin, end) of the reference per-parameter step (apf_update +
+    masked accumulation + SGD) over the M x words masks."""
+    m = np.ascontiguousarray(masks, dtype=np.uint64)
+    return lib().ref_param_pass(begin, end, block, m.shape[0], _p(m), m.shape[1], per_unit, lr)
+
+
+def controller_step(kind, R, C, M, n_units, ratio, seed=42):
+    """ref_controller_step: schedule + DAG + longest path + S*M sample_mask; (seconds, stage-1 masks)."""
+    out = np.zeros((M, (n_units + 63) // 64), dtype=np.uint64)
+    secs = lib().ref_controller_step(KIND[kind], R, C, M, n_units, ratio, seed, _p(out))
+    return secs, out
 
 
 def cpu_step_seconds(kind, R, C, M, n_units, n_params, ratio, seed=42) -> float:

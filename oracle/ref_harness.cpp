@@ -438,4 +438,99 @@ double ref_cpu_step(int kind, int R, int C, int M, int n_units, long n_params, d
   return secs;
 }
 
+// One worker's share of the reference's per-parameter step (bench.py --impl reference and the
+// cpu_baseline leg shard a stage's parameters element-wise over worker processes):
+// elements [begin, end), in blocks of `block` elements, each block through
+//   * apf_update (freezectl.cpp:147-156) on the block's APF state (E, E_abs);
+//   * the masked accumulation total = sum_m U_m (.) g over the M microbatch masks and the SGD
+//     update theta -= (lr / M) total of run_masked_sgd (sandbox.cpp:232-250), unit of element i =
+//     i / per_unit (ref_cpu_step's contiguous-unit mapping), FreezeMask::test on the reference's
+//     masks (`masks`: M x words uint64, FreezeMask bit order).
+// The blocks reuse one set of block-sized buffers (the arithmetic per element is the reference's;
+// the full stage state would not fit host memory at 8B parameters). Returns the seconds of the
+// timed loop (buffer setup excluded).
+double ref_param_pass(long begin, long end, long block, int M, const uint64_t* masks, int words, long per_unit,
+                      double lr) {
+  double secs = -1.0;
+  guard([&] {
+    const long n = std::max<long>(1, std::min(block, end - begin));
+    auto st = ApfState::zeros(n, 0.9);
+    Eigen::VectorXd delta(n), theta(n), total(n), g(n), upd(n);
+    Rng rng(static_cast<uint64_t>(begin) + 1);
+    for (long i = 0; i < n; ++i) {
+      delta(i) = 1e-3 * (rng.unit() - 0.5);
+      theta(i) = rng.unit();
+      g(i) = rng.unit() - 0.5;
+    }
+    std::vector<FreezeMask> mk;
+    mk.reserve(static_cast<size_t>(M));
+    const int n_units = words * 64;
+    for (int m = 0; m < M; ++m) {
+      FreezeMask f(n_units);
+      for (int u = 0; u < n_units; ++u)
+        if ((masks[static_cast<size_t>(m) * words + u / 64] >> (u % 64)) & 1ULL) f.set(u);
+      mk.push_back(std::move(f));
+    }
+    volatile double sink = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long b0 = begin; b0 < end; b0 += block) {
+      const long len = std::min(block, end - b0);
+      const auto scores = apf_update(st, delta);
+      sink = sink + scores(0);
+      for (long i = 0; i < len; ++i) total(i) = 0.0;
+      for (int m = 0; m < M; ++m) {
+        // U_m: the 0/1 update mask of this block's elements (what MaskPolicy::draw_update_mask
+        // hands run_masked_sgd), then the reference's total += U_m .* g (sandbox.cpp:243)
+        const auto& f = mk[static_cast<size_t>(m)];
+        for (long i = 0; i < len;) {
+          const long u = std::min<long>(n_units - 1, (b0 + i) / per_unit);
+          const long stop = u == n_units - 1 ? len : std::min(len, (u + 1) * per_unit - b0);
+          const double keep = f.test(static_cast<int>(u)) ? 0.0 : 1.0;
+          for (; i < stop; ++i) upd(i) = keep;
+        }
+        // (written out as the single fused pass Eigen's expression templates evaluate it to; the
+        // test-only Eigen shim is eager and would add a temporary per microbatch)
+        for (long i = 0; i < len; ++i) total(i) += upd(i) * g(i);
+      }
+      const double sc = lr / M;
+      for (long i = 0; i < len; ++i) theta(i) -= sc * total(i);
+      sink = sink + theta(0);
+    }
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    (void)sink;
+  });
+  return secs;
+}
+
+// The reference's per-step controller work for a stage: build_schedule + build_dag +
+// longest_path_start_times, then the step's S*M exact-count masks over n_units
+// (run_freezing_masks' per-cell sample_mask, freezectl.cpp:185-211). masks_out (M x words of
+// stage 1, may be NULL) receives the first stage's masks. Returns seconds.
+double ref_controller_step(int kind, int R, int C, int M, int n_units, double ratio, uint64_t seed,
+                           uint64_t* masks_out) {
+  double secs = -1.0;
+  guard([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto pc = cfg(kind, R, C, M);
+    const int S = pc.total_stages();
+    const auto dag = build_dag(build_schedule(pc));
+    std::vector<double> w(dag.node_count(), 1.0);
+    w[dag.source()] = 0.0;
+    w[dag.destination()] = 0.0;
+    volatile double ms = longest_path_start_times(dag, w).makespan;
+    (void)ms;
+    Rng rng(seed);
+    const int words = (n_units + 63) / 64;
+    for (int s = 1; s <= S; ++s)
+      for (int m = 1; m <= M; ++m) {
+        const auto mk = sample_mask(n_units, ratio, rng);
+        if (masks_out && s == 1)
+          for (int u = 0; u < n_units; ++u)
+            if (mk.test(u)) masks_out[static_cast<size_t>(m - 1) * words + u / 64] |= 1ULL << (u % 64);
+      }
+    secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  return secs;
+}
+
 }  // extern "C"

@@ -11,6 +11,7 @@ HOST_SIGNATURES = {
     "pf_last_error": ([], c_cp),
     "pf_schedule_build": ([c_int, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "pf_stage_to_rank": ([c_int, c_int, c_int, c_int, c_int, c_vp], c_int),
+    "pf_issue_program": ([c_int, c_int, c_int, c_int, c_int, c_vp, c_vp], c_int),
     "pf_dag_build": ([c_int, c_int, c_int, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_int], c_int),
     "pf_longest_path": ([c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp], c_int),
     "pf_critical_path": ([c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp], c_int),

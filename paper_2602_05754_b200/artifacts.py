@@ -95,13 +95,31 @@ def gantt(config: pf.PipelineConfig, weights) -> dict:
     return {"blocks": blocks, "makespan_ms": float(st.makespan), "num_ranks": config.num_ranks}
 
 
-def measured_gantt(trainer, rank: int = 0) -> dict:
-    """Timeline of the trainer's last step in the same schema, from its CUDA-event action times
-    (start/end relative to the rank's first action)."""
+def measured_gantt(trainer, rank: int | None = None, group=None) -> dict:
+    """Timeline of the trainer's last step in the reference's gantt schema (gantt.cpp:12-48), from
+    the CUDA-event action times (start/end relative to the step's origin event).
+
+    Multi-rank (torch.distributed initialised): every rank's blocks are gathered (a collective:
+    call it on every rank) and num_ranks is the world size. The ranks share one time axis when
+    they barriered right before the step (pf_trainer_step records the origin event first); the
+    makespan is the latest end over all ranks."""
+    import torch.distributed as dist
+
     start, end, kinds, mbs, stages = trainer.action_times()
-    blocks = [{"end_ms": float(e), "kind": "fbw"[int(k)], "microbatch": int(m), "rank": rank, "stage": int(s),
+    multi = dist.is_available() and dist.is_initialized()
+    if rank is None:
+        rank = dist.get_rank(group) if multi else 0
+    blocks = [{"end_ms": float(e), "kind": "fbw"[int(k)], "microbatch": int(m), "rank": int(rank), "stage": int(s),
                "start_ms": float(b)} for b, e, k, m, s in zip(start, end, kinds, mbs, stages)]
-    return {"blocks": blocks, "makespan_ms": float(max(end) if len(end) else 0.0), "num_ranks": 1}
+    world = 1
+    if multi:
+        world = dist.get_world_size(group)
+        parts = [None] * world
+        dist.all_gather_object(parts, blocks, group=group)
+        blocks = [b for part in parts for b in part]
+    blocks.sort(key=lambda b: (b["rank"], b["start_ms"]))
+    return {"blocks": blocks, "makespan_ms": float(max((b["end_ms"] for b in blocks), default=0.0)),
+            "num_ranks": world}
 
 
 def gantt_to_json(doc: dict) -> str:

@@ -60,7 +60,9 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   const int M = cfg.pipeline.num_microbatches;
   if (cfg.rank < 0 || cfg.rank >= cfg.pipeline.num_ranks) throw std::invalid_argument("trainer: rank out of range");
   if (model.layers < S) throw std::invalid_argument("trainer: fewer layers than pipeline stages");
-  actions_ = timeline_.rank_order[static_cast<std::size_t>(cfg.rank)];
+  // the rank's issue program (libpf_host): actions in schedule order + their cross-rank P2P
+  program_ = issue_program(cfg.pipeline, cfg.rank);
+  for (const auto& op : program_) actions_.push_back(op.action);
   for (int s = 1; s <= S; ++s)
     if (stage_to_rank(cfg.pipeline, s) == cfg.rank) stage_ids_.push_back(s);
   // cross-rank edge classes of DAG rule 3 (dag.cpp:90-93): one P2P link each
@@ -121,6 +123,7 @@ Trainer::Trainer(const ModelConfig& model, const TrainConfig& cfg) : model_(mode
   ev_.resize(2 * actions_.size());
   for (auto& e : ev_) cudaEventCreate(&e);
   cudaEventCreate(&ev_opt0_);
+  cudaEventCreate(&ev_origin_);
   cudaEventCreate(&ev_opt1_);
   cudaMalloc(&tokens_dev_, static_cast<size_t>(M) * T * 4);
   cudaMalloc(&targets_dev_, static_cast<size_t>(M) * T * 4);
@@ -164,6 +167,7 @@ Trainer::~Trainer() {
   if (ctl_stream_) cudaStreamDestroy(ctl_stream_);
   for (auto& e : ev_) cudaEventDestroy(e);
   if (ev_opt0_) cudaEventDestroy(ev_opt0_);
+  if (ev_origin_) cudaEventDestroy(ev_origin_);
   if (ev_opt1_) cudaEventDestroy(ev_opt1_);
   cudaFree(tokens_dev_);
   cudaFree(targets_dev_);
@@ -428,6 +432,9 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   res.mean_ratio = res.total_units ? static_cast<double>(res.frozen_units) / static_cast<double>(res.total_units) : 0.0;
   res.mask_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tm0).count();
 
+  // step origin: action start times are relative to this event, recorded before the step's
+  // first enqueue (a caller that barriers all ranks right before step() gets one time axis)
+  PF_CUDA(cudaEventRecord(ev_origin_, stream_));
   PF_CUDA(cudaMemcpyAsync(masks_dev_, masks_host_, static_cast<size_t>(mask_offsets_.back()) * 8,
                           cudaMemcpyHostToDevice, stream_));
   if (host_tokens)
@@ -463,7 +470,6 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   auto nccl_ok = [](ncclResult_t r) { return r == ncclSuccess ? PF_OK : PF_ERR_NCCL; };
   const int r = cfg_.rank;
   auto comm = [](const Link* l) { return static_cast<ncclComm_t>(l->comm); };
-  auto rank_of = [&](int s) { return stage_to_rank(cfg_.pipeline, s); };
   for (std::size_t i = 0; i < actions_.size(); ++i) {
     const ActionId a = actions_[i];
     const int li = local_index(a.stage);
@@ -473,12 +479,13 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
     const auto ss = static_cast<std::size_t>(slot);
     const int* tok = tokens_dev_ + static_cast<long long>(a.microbatch - 1) * T;
     const int* tgt = targets_dev_ + static_cast<long long>(a.microbatch - 1) * T;
+    const IssueOp& op = program_[i];
     if (a.kind == ActionKind::Forward) {
       const __nv_bfloat16* x_in = nullptr;
-      const bool recv_x = a.stage > 1 && local_index(a.stage - 1) < 0;
-      const bool send_y = a.stage < S && local_index(a.stage + 1) < 0;
+      const bool recv_x = op.recv_from >= 0;
+      const bool send_y = op.send_to >= 0;
       if (recv_x) {  // f(m, s-1) output over NVLink into this slot's receive buffer
-        const Link* l = link(0, rank_of(a.stage - 1), r);
+        const Link* l = link(0, op.recv_from, r);
         if (!l || !l->comm) return PF_ERR_NCCL;
         PF_CUDA(cudaStreamWaitEvent(l->stream, x_free_ev_[ls][ss], 0));
         PF_TRY(nccl_ok(ncclRecv(x_recv_[ls][ss], act_bytes, ncclUint8, 0, comm(l), l->stream)));
@@ -494,7 +501,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
       if (recv_x) PF_CUDA(cudaEventRecord(x_free_ev_[ls][ss], stream_));
       if (send_y) {  // to f(m, s+1)
-        const Link* l = link(0, r, rank_of(a.stage + 1));
+        const Link* l = link(0, r, op.send_to);
         if (!l || !l->comm) return PF_ERR_NCCL;
         PF_TRY(after(l->stream, stream_));
         PF_TRY(nccl_ok(ncclSend(st.output(slot), act_bytes, ncclUint8, 1, comm(l), l->stream)));
@@ -506,11 +513,11 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_TRY(st.backward_weight(slot, mw, stamp, stream_));
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
     } else {
-      const bool recv_dy = a.stage < S && local_index(a.stage + 1) < 0;
-      const bool send_dx = a.stage > 1 && local_index(a.stage - 1) < 0;
+      const bool recv_dy = op.recv_from >= 0;
+      const bool send_dx = op.send_to >= 0;
       const __nv_bfloat16* dy = nullptr;
       if (recv_dy) {  // b(m, s+1) input gradient
-        const Link* l = link(1, rank_of(a.stage + 1), r);
+        const Link* l = link(1, op.recv_from, r);
         if (!l || !l->comm) return PF_ERR_NCCL;
         PF_CUDA(cudaStreamWaitEvent(l->stream, dy_free_ev_[ls][ss], 0));
         PF_TRY(nccl_ok(ncclRecv(dy_recv_[ls][ss], act_bytes, ncclUint8, 0, comm(l), l->stream)));
@@ -534,7 +541,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
       if (recv_dy) PF_CUDA(cudaEventRecord(dy_free_ev_[ls][ss], stream_));
       if (send_dx) {  // to b(m, s-1)
-        const Link* l = link(1, r, rank_of(a.stage - 1));
+        const Link* l = link(1, r, op.send_to);
         if (!l || !l->comm) return PF_ERR_NCCL;
         PF_TRY(after(l->stream, stream_));
         PF_TRY(nccl_ok(ncclSend(dx, act_bytes, ncclUint8, 1, comm(l), l->stream)));
@@ -593,7 +600,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
   for (std::size_t i = 0; i < actions_.size(); ++i) {
     float ms = 0.f, st = 0.f;
     cudaEventElapsedTime(&ms, ev_[2 * i], ev_[2 * i + 1]);
-    cudaEventElapsedTime(&st, ev_[0], ev_[2 * i]);
+    cudaEventElapsedTime(&st, ev_origin_, ev_[2 * i]);
     action_ms_[i] = ms;
     action_start_ms_[i] = st;
   }

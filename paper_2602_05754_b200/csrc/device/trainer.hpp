@@ -81,7 +81,8 @@ class Trainer {
   const std::vector<double>& plan_ratios() const { return plan_ratios_; }
   const pipefreeze::FreezePlan& plan() const { return plan_; }
   const std::vector<double>& action_ms() const { return action_ms_; }
-  // start of each action relative to the rank's first action of the last step (CUDA events)
+  // start of each action of the last step relative to the step's origin event, recorded when
+  // step() began enqueueing (CUDA events)
   const std::vector<double>& action_start_ms() const { return action_start_ms_; }
   const std::vector<pipefreeze::ActionId>& actions() const { return actions_; }
   std::vector<Stage*> local_stages();
@@ -138,14 +139,15 @@ class Trainer {
   TrainConfig cfg_;
   pipefreeze::RankTimeline timeline_;
   std::unique_ptr<pipefreeze::PipelineDag> dag_;
-  std::vector<pipefreeze::ActionId> actions_;
+  std::vector<pipefreeze::IssueOp> program_;   // this rank's issue program (host layer)
+  std::vector<pipefreeze::ActionId> actions_;  // program_'s actions
   std::vector<int> stage_ids_;                  // local stages (1-based)
   std::vector<std::unique_ptr<Stage>> stages_;  // parallel to stage_ids_
   std::vector<int> slots_;                      // per local stage
   std::vector<std::vector<__nv_bfloat16*>> grad_bufs_;  // [local stage][slot]: dL/d(stage output)
   cudaStream_t stream_ = nullptr;
   std::vector<cudaEvent_t> ev_;
-  cudaEvent_t ev_opt0_ = nullptr, ev_opt1_ = nullptr;
+  cudaEvent_t ev_opt0_ = nullptr, ev_opt1_ = nullptr, ev_origin_ = nullptr;
   int* tokens_dev_ = nullptr;
   int* targets_dev_ = nullptr;
   float* loss_dev_ = nullptr;

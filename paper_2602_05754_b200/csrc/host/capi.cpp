@@ -105,6 +105,24 @@ int pf_stage_to_rank(int kind, int R, int C, int M, int stage, int* rank) {
   });
 }
 
+int pf_issue_program(int kind, int R, int C, int M, int rank, int* ops, int* n) {
+  return guard([&] {
+    need(ops, "ops");
+    need(n, "n");
+    const auto prog = issue_program(make_cfg(kind, R, C, M), rank);
+    int i = 0;
+    for (const auto& op : prog) {
+      ops[5 * i] = static_cast<int>(op.action.kind);
+      ops[5 * i + 1] = op.action.microbatch;
+      ops[5 * i + 2] = op.action.stage;
+      ops[5 * i + 3] = op.recv_from;
+      ops[5 * i + 4] = op.send_to;
+      ++i;
+    }
+    *n = i;
+  });
+}
+
 int pf_dag_build(int kind, int R, int C, int M, int* edges, int edge_cap, int* n_edges, int* topo, char* json,
                  int json_cap) {
   return guard([&] {

@@ -156,6 +156,21 @@ def stage_to_rank(config: PipelineConfig, stage: int) -> int:
     return out.value
 
 
+def issue_program(config: PipelineConfig, rank: int) -> list[tuple[ActionId, int, int]]:
+    """The rank's issue program (libpf_host issue_program, the one trainer.cpp walks): its actions
+    in schedule order, each with the rank to receive from before it and the rank to send to after
+    it (-1: none) for the cross-rank DAG rule-3 edges (dag.cpp:90-93)."""
+    cap = config.kinds * config.num_microbatches * config.stages_per_rank
+    ops = np.zeros(5 * cap, dtype=np.int32)
+    n = ctypes.c_int(0)
+    _check(_native.host().pf_issue_program(*config.key(), rank, _p(ops), ctypes.byref(n)), "issue_program")
+    out = []
+    for i in range(n.value):
+        k, m, s, rf, st = (int(x) for x in ops[5 * i:5 * i + 5])
+        out.append((ActionId(k, s, m), rf, st))
+    return out
+
+
 def p2p_links(config: PipelineConfig) -> list[tuple[int, int, int]]:
     """Cross-rank classes of DAG rule-3 edges (dag.cpp:90-93), one NCCL link each, in the device
     trainer's order (trainer.cpp): for s = 1..S-1 with rank(s) != rank(s+1), the activation link

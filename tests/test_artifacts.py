@@ -93,3 +93,61 @@ def test_bad_plan_json_raises_config_error():
     with pytest.raises(pf.ConfigError):
         art.plan_from_json(json.dumps({"makespan_opt": 1, "makespan_base": 1, "makespan_floor": 1,
                                        "ratios": [{"m": 3, "s": 1, "r": 0.5}]}), 2, 1)
+
+
+def _gantt_worker(rank, world, kind, C, M, port, errq, outq):
+    import torch.distributed as dist
+
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cfg = pf.PipelineConfig(kind, world, C, M)
+        dag = pf.build_dag(cfg)
+        rng = np.random.default_rng(5)
+        w = rng.uniform(0.5, 2.0, size=dag.node_count)
+        w[0] = w[-1] = 0.0
+        st = pf.longest_path_start_times(dag, w)
+
+        class FakeTrainer:  # this rank's CUDA-event action times = the DAG schedule of w
+            def action_times(self):
+                acts = [a for a, _, _ in pf.issue_program(cfg, rank)]
+                v = np.array([dag.index_of(a) for a in acts])
+                return (st.start[v], st.start[v] + w[v], np.array([a.kind for a in acts]),
+                        np.array([a.microbatch for a in acts]), np.array([a.stage for a in acts]))
+
+        doc = art.measured_gantt(FakeTrainer())
+        if rank == 0:
+            outq.put((doc, art.gantt(cfg, w)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        errq.put(f"rank {rank}: {e!r}\n{traceback.format_exc()}")
+
+
+@pytest.mark.parametrize("kind,world,C,M", [("1f1b", 2, 1, 4), ("interleaved-1f1b", 2, 2, 4)])
+def test_measured_gantt_gathers_every_rank(kind, world, C, M):
+    """Multi-rank measured Gantt (gantt.cpp:12-48 schema): blocks of every rank gathered over the
+    process group, num_ranks = world size; with action times equal to the DAG schedule it is the
+    reference's build_gantt of the same weights, block for block."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    errq, outq = ctx.Queue(), ctx.Queue()
+    port = 31000 + (abs(hash((kind, world, C, M))) % 2000)
+    procs = [ctx.Process(target=_gantt_worker, args=(r, world, kind, C, M, port, errq, outq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    doc, ref = outq.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, "\n".join(errs)
+    assert doc["num_ranks"] == world
+    key = lambda b: (b["rank"], b["start_ms"], b["stage"], b["microbatch"], b["kind"])  # noqa: E731
+    assert sorted(doc["blocks"], key=key) == sorted(ref["blocks"], key=key)
+    assert doc["makespan_ms"] == ref["makespan_ms"]

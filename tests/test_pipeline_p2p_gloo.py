@@ -4,8 +4,8 @@ The device trainer (csrc/device/trainer.cpp, Trainer::step) drives P2P over one 
 communicator and stream per link: a cross-rank (activation | gradient, src rank, dst rank)
 class of DAG rule-3 edges (pipefreeze.p2p_links). Compute waits on receive events; sends
 wait on compute; neighbouring stages on the same rank hand over locally. This test replays
-exactly that issue program (same rank action lists from libpf_host's build_schedule, same
-link rules, every placement: gpipe / 1f1b chains, the interleaved ring, the ZBV V with
+the product's own issue program (pipefreeze.issue_program = libpf_host issue_program, the
+list Trainer::step walks), with the same link rules, over every placement: gpipe / 1f1b chains, the interleaved ring, the ZBV V with
 activations flowing both ways, zbv-split's W actions) with one thread per link stream and a
 gloo process group per link standing in for the NCCL communicators, and checks that it
 completes (no deadlock) and that every stage consumes the payload of the right
@@ -67,33 +67,25 @@ def _worker(rank, world, kind, C, M, port, errq):
         streams = {l: Stream() for l in links if rank in (l[1], l[2])}
         consumed = []
         pending_sends = []
-        for a in actions:
+        # the product's issue program (libpf_host issue_program, the list trainer.cpp walks)
+        for a, recv_from, send_to in pf.issue_program(cfg, rank):
             m, s = a.microbatch, a.stage
-            if a.kind == 0:  # forward f(m, s)
-                if s > 1 and rank_of[s - 1] != rank:
-                    l = (0, rank_of[s - 1], rank)
-                    buf = torch.zeros(2)
-                    ev = streams[l].submit(lambda b=buf, l=l: dist.recv(b, src=l[1], group=groups[l]))
-                    assert ev.wait(60), f"activation receive timed out at {a}"
-                    assert buf.tolist() == [m, s - 1], (buf.tolist(), m, s)
-                    consumed.append(("f", m, s))
-                out = torch.tensor([float(m), float(s)])
-                if s < S and rank_of[s + 1] != rank:
-                    l = (0, rank, rank_of[s + 1])
-                    pending_sends.append(streams[l].submit(lambda t=out, l=l: dist.send(t, dst=l[2], group=groups[l])))
-            elif a.kind == 1:  # backward b(m, s) (dX)
-                if s < S and rank_of[s + 1] != rank:
-                    l = (1, rank_of[s + 1], rank)
-                    buf = torch.zeros(2)
-                    ev = streams[l].submit(lambda b=buf, l=l: dist.recv(b, src=l[1], group=groups[l]))
-                    assert ev.wait(60), f"gradient receive timed out at {a}"
-                    assert buf.tolist() == [-m, s + 1], (buf.tolist(), m, s)
-                    consumed.append(("b", m, s))
-                g = torch.tensor([-float(m), float(s)])
-                if s > 1 and rank_of[s - 1] != rank:
-                    l = (1, rank, rank_of[s - 1])
-                    pending_sends.append(streams[l].submit(lambda t=g, l=l: dist.send(t, dst=l[2], group=groups[l])))
-            # w(m, s): local dW only, no transfer
+            if a.kind == 2:
+                assert recv_from == -1 and send_to == -1  # w(m, s): local dW only
+                continue
+            edge = a.kind  # 0: activations of f, 1: gradients of b
+            if recv_from >= 0:
+                l = (edge, recv_from, rank)
+                buf = torch.zeros(2)
+                ev = streams[l].submit(lambda b=buf, l=l: dist.recv(b, src=l[1], group=groups[l]))
+                assert ev.wait(60), f"receive timed out at {a}"
+                want = [m, s - 1] if edge == 0 else [-m, s + 1]
+                assert buf.tolist() == want, (buf.tolist(), a)
+                consumed.append(("fb"[edge], m, s))
+            if send_to >= 0:
+                l = (edge, rank, send_to)
+                out = torch.tensor([float(m), float(s)]) if edge == 0 else torch.tensor([-float(m), float(s)])
+                pending_sends.append(streams[l].submit(lambda t=out, l=l: dist.send(t, dst=l[2], group=groups[l])))
         for ev in pending_sends:
             assert ev.wait(60), "send never matched"
         for st in streams.values():
