@@ -115,6 +115,16 @@ int pf_simulate_monitoring(int M, int S, const double* fwd, const double* bact,
 int pf_masked_sgd_host(int d, const double* diag, const double* theta0, double eta, int M, int steps,
                        double sigma, int policy, double param, uint64_t seed, double* theta_out,
                        double* grad_sq_out);
+/* run_masked_sgd with MaskPolicy::plan_driven (sandbox.cpp:97-115, per-coordinate Bernoulli of the
+ * AFR of the coordinate's stage block at :158): ratios[(s-1)*M + (m-1)] = the plan's b(m,s) ratio,
+ * phases = {T_w, T_m, T_f, T_total}, step < 0 = t_total. */
+int pf_masked_sgd_plan_host(int d, const double* diag, const double* theta0, double eta, int M, int steps,
+                            double sigma, int S, const double* ratios, const int* phases, int step, uint64_t seed,
+                            double* theta_out, double* grad_sq_out);
+/* AutoFreeze baseline (freezectl.hpp; freezectl.cpp:116-136): relative layer-norm change score and
+ * the nearest-rank percentile prefix selection. */
+int pf_autofreeze_score(double norm_prev, double norm_cur, double* out);
+int pf_autofreeze_select(const double* scores, int n, int frozen_prefix_len, double percentile, int* out);
 
 /* apf_update (freezectl.hpp:88) in fp64 on the host. */
 int pf_apf_update_host(int n, double alpha, double* ema, double* ema_abs, const double* delta,

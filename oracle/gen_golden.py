@@ -230,7 +230,25 @@ def gen_sgd():
         th, gs = ref.masked_sgd(diag, theta0, eta, M, steps, sigma, policy, param, seed)
         out.append({"d": d, "M": M, "steps": steps, "eta": eta, "sigma": sigma, "policy": policy, "param": param,
                     "seed": seed, "diag": hx(diag), "theta0": hx(theta0), "theta": hx(th), "grad_sq": hx(gs)})
-    dump("sgd.json", out)
+    # MaskPolicy::plan_driven (sandbox.cpp:97-115): the reference's own LP plan of two fixtures,
+    # AFR at a ramp step and at t_total
+    fx = fixtures()
+    plan_rows = []
+    for name, d, steps, eta, sigma, step, seed in [("gpipe_s2m2", 40, 12, 0.05, 0.1, 15, 3),
+                                                   ("default_1f1b_s4m8", 64, 8, 0.02, 0.0, -1, 21)]:
+        f = fx[name]
+        pl = f["pipeline"]
+        R, C, M = pl["num_ranks"], pl["stages_per_rank"], pl["num_microbatches"]
+        t = f["timing"]["per_stage"]
+        pr = ref.plan(pl["schedule"], R, C, M, t["forward_ms"], t["backward_act_ms"], t["backward_param_ms"], f["r_max"])
+        phases = [2, 8, 10, 20]
+        diag = np.linspace(0.5, 2.0, d)
+        theta0 = np.linspace(-1.0, 1.0, d)
+        th, gs = ref.masked_sgd_plan(diag, theta0, eta, M, steps, sigma, R * C, pr["ratios"], phases, step, seed)
+        plan_rows.append({"fixture": name, "d": d, "M": M, "S": R * C, "steps": steps, "eta": eta, "sigma": sigma,
+                          "ratios": hx(pr["ratios"]), "phases": phases, "step": step, "seed": seed, "diag": hx(diag),
+                          "theta0": hx(theta0), "theta": hx(th), "grad_sq": hx(gs)})
+    dump("sgd.json", {"runs": out, "plan_driven": plan_rows})
 
 
 if __name__ == "__main__" and len(sys.argv) == 1:

@@ -208,6 +208,33 @@ def masked_sgd(diag, theta0, eta, M, steps, sigma, policy, param, seed):
     return th, gs
 
 
+def masked_sgd_plan(diag, theta0, eta, M, steps, sigma, S, ratios, phases, step, seed):
+    """run_masked_sgd with MaskPolicy::plan_driven (sandbox.cpp:97-115)."""
+    d = len(diag)
+    dg = np.ascontiguousarray(diag, dtype=np.float64)
+    t0 = np.ascontiguousarray(theta0, dtype=np.float64)
+    r = np.ascontiguousarray(ratios, dtype=np.float64)
+    ph = np.ascontiguousarray(phases, dtype=np.int32)
+    th = np.zeros(d)
+    gs = np.zeros(steps)
+    _chk(lib().ref_masked_sgd_plan(d, _p(dg), _p(t0), ctypes.c_double(eta), M, steps, ctypes.c_double(sigma), S,
+                                   _p(r), _p(ph), step, ctypes.c_uint64(seed), _p(th), _p(gs)))
+    return th, gs
+
+
+def autofreeze_score(prev: float, cur: float) -> float:
+    f = lib().ref_autofreeze_score
+    f.restype, f.argtypes = ctypes.c_double, [ctypes.c_double, ctypes.c_double]
+    return f(prev, cur)
+
+
+def autofreeze_select(scores, prefix: int, pct: float) -> int:
+    sc = np.ascontiguousarray(scores, dtype=np.float64)
+    out = ctypes.c_int(0)
+    _chk(lib().ref_autofreeze_select(_p(sc), len(sc), prefix, ctypes.c_double(pct), ctypes.byref(out)))
+    return out.value
+
+
 def param_pass_seconds(begin, end, block, masks, per_unit, lr=0.01) -> float:
     """ref_param_pass: elements [begin, end) of the reference per-parameter step (apf_update +
     masked accumulation + SGD) over the M x words masks."""

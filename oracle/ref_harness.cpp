@@ -344,6 +344,38 @@ int ref_masked_sgd(int d, const double* diag, const double* theta0, double eta, 
   });
 }
 
+// run_masked_sgd with MaskPolicy::plan_driven (sandbox.cpp:97-115; Bernoulli draws at :158): the
+// plan's backward ratios[(s-1)*M + (m-1)], the AFR at `step` (< 0: t_total) of `phases`.
+int ref_masked_sgd_plan(int d, const double* diag, const double* theta0, double eta, int M, int steps, double sigma,
+                        int S, const double* ratios, const int* phases, int step, uint64_t seed, double* theta_out,
+                        double* gradsq_out) {
+  return guard([&] {
+    Eigen::VectorXd dg(d), t0(d);
+    for (int j = 0; j < d; ++j) {
+      dg(j) = diag[j];
+      t0(j) = theta0[j];
+    }
+    const auto obj = SyntheticObjective::quadratic(dg, sigma);
+    FreezePlan plan;
+    for (int s = 1; s <= S; ++s)
+      for (int m = 1; m <= M; ++m) plan.ratios[backward_action(m, s)] = ratios[(s - 1) * M + (m - 1)];
+    const PhasePlan ph{phases[0], phases[1], phases[2], phases[3]};
+    const auto pol = MaskPolicy::plan_driven(plan, ph, M, S, step < 0 ? std::nullopt : std::optional<int>(step));
+    SgdHyper h;
+    h.eta = eta;
+    h.microbatches = M;
+    h.total_steps = steps;
+    const auto run = run_masked_sgd(obj, pol, h, t0, seed);
+    for (int j = 0; j < d; ++j) theta_out[j] = run.theta_final(j);
+    for (int t = 0; t < static_cast<int>(run.grad_sq_norms.size()); ++t) gradsq_out[t] = run.grad_sq_norms[t];
+  });
+}
+
+double ref_autofreeze_score(double prev, double cur) { return autofreeze_score(prev, cur); }
+int ref_autofreeze_select(const double* scores, int n, int prefix, double pct, int* out) {
+  return guard([&] { *out = autofreeze_select(std::vector<double>(scores, scores + n), prefix, pct); });
+}
+
 namespace {
 int copy_text(const std::string& s, char* out, int cap) {
   if (!out || cap <= 0) return static_cast<int>(s.size()) + 1;

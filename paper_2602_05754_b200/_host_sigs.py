@@ -32,6 +32,10 @@ HOST_SIGNATURES = {
     "pf_simulate_monitoring": ([c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_d, c_u64, c_vp, c_vp], c_int),
     "pf_apf_update_host": ([c_int, c_d, c_vp, c_vp, c_vp, c_vp], c_int),
     "pf_masked_sgd_host": ([c_int, c_vp, c_vp, c_d, c_int, c_int, c_d, c_int, c_d, c_u64, c_vp, c_vp], c_int),
+    "pf_autofreeze_score": ([c_d, c_d, c_vp], c_int),
+    "pf_autofreeze_select": ([c_vp, c_int, c_int, c_d, c_vp], c_int),
+    "pf_masked_sgd_plan_host": ([c_int, c_vp, c_vp, c_d, c_int, c_int, c_d, c_int, c_vp, c_vp, c_int, c_u64, c_vp,
+                                 c_vp], c_int),
 }
 
 

@@ -404,6 +404,45 @@ int pf_masked_sgd_host(int d, const double* diag, const double* theta0, double e
   });
 }
 
+int pf_masked_sgd_plan_host(int d, const double* diag, const double* theta0, double eta, int M, int steps,
+                            double sigma, int S, const double* ratios, const int* phases, int step, uint64_t seed,
+                            double* theta_out, double* grad_sq_out) {
+  return guard([&] {
+    need(diag, "diag");
+    need(theta0, "theta0");
+    need(ratios, "ratios");
+    need(phases, "phases");
+    const auto obj = SyntheticObjective::quadratic(Vec(diag, diag + d), sigma);
+    FreezePlan plan;
+    for (int s = 1; s <= S; ++s)
+      for (int m = 1; m <= M; ++m) plan.ratios[backward_action(m, s)] = ratios[(s - 1) * M + (m - 1)];
+    const PhasePlan ph{phases[0], phases[1], phases[2], phases[3]};
+    const auto pol = MaskPolicy::plan_driven(plan, ph, M, S, step < 0 ? std::nullopt : std::optional<int>(step));
+    SgdHyper h;
+    h.eta = eta;
+    h.microbatches = M;
+    h.total_steps = steps;
+    const auto run = run_masked_sgd(obj, pol, h, Vec(theta0, theta0 + d), seed);
+    if (theta_out) std::copy(run.theta_final.begin(), run.theta_final.end(), theta_out);
+    if (grad_sq_out) std::copy(run.grad_sq_norms.begin(), run.grad_sq_norms.end(), grad_sq_out);
+  });
+}
+
+int pf_autofreeze_score(double norm_prev, double norm_cur, double* out) {
+  return guard([&] {
+    need(out, "out");
+    *out = autofreeze_score(norm_prev, norm_cur);
+  });
+}
+
+int pf_autofreeze_select(const double* scores, int n, int frozen_prefix_len, double percentile, int* out) {
+  return guard([&] {
+    need(scores, "scores");
+    need(out, "out");
+    *out = autofreeze_select(std::vector<double>(scores, scores + n), frozen_prefix_len, percentile);
+  });
+}
+
 int pf_apf_update_host(int n, double alpha, double* ema, double* ema_abs, const double* delta, double* scores) {
   return guard([&] {
     need(ema, "ema");

@@ -470,6 +470,38 @@ def run_masked_sgd_quadratic(diag, theta0, eta: float, microbatches: int, steps:
     return th, gs
 
 
+def run_masked_sgd_plan_quadratic(diag, theta0, eta: float, microbatches: int, steps: int, sigma: float, S: int,
+                                  ratios, phases, step: int, seed: int):
+    """run_masked_sgd with MaskPolicy::plan_driven (sandbox.cpp:97-115,158) on a diagonal quadratic:
+    coordinate j belongs to stage block min(S-1, j*S/d) and is frozen in microbatch m with
+    probability AFR(step, phases, ratio of b(m, s)). ratios[(s-1)*M + (m-1)]; step < 0 = t_total."""
+    dg = np.ascontiguousarray(diag, dtype=np.float64)
+    t0 = np.ascontiguousarray(theta0, dtype=np.float64)
+    r = np.ascontiguousarray(ratios, dtype=np.float64)
+    ph = np.ascontiguousarray(phases, dtype=np.int32)
+    th = np.zeros_like(t0)
+    gs = np.zeros(steps)
+    _check(_native.host().pf_masked_sgd_plan_host(len(dg), _p(dg), _p(t0), eta, microbatches, steps, sigma, S, _p(r),
+                                                  _p(ph), step, seed, _p(th), _p(gs)), "run_masked_sgd(plan_driven)")
+    return th, gs
+
+
+def autofreeze_score(norm_prev: float, norm_cur: float) -> float:
+    """AutoFreeze layer score (freezectl.cpp:116-122)."""
+    out = ctypes.c_double(0)
+    _check(_native.host().pf_autofreeze_score(norm_prev, norm_cur, ctypes.byref(out)), "autofreeze_score")
+    return out.value
+
+
+def autofreeze_select(scores, frozen_prefix_len: int, percentile: float) -> int:
+    """AutoFreeze prefix selection by nearest-rank percentile (freezectl.cpp:124-136)."""
+    sc = np.ascontiguousarray(scores, dtype=np.float64)
+    out = ctypes.c_int(0)
+    _check(_native.host().pf_autofreeze_select(_p(sc), len(sc), frozen_prefix_len, percentile, ctypes.byref(out)),
+           "autofreeze_select")
+    return out.value
+
+
 def apf_update_host(ema: np.ndarray, ema_abs: np.ndarray, delta, alpha: float = 0.9) -> np.ndarray:
     d = np.ascontiguousarray(delta, dtype=np.float64)
     sc = np.zeros_like(d)

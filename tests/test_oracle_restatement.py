@@ -84,7 +84,7 @@ def test_apf_restatement():
 
 def test_masked_sgd_restatement_matches_reference_trajectory():
     """Replay run_masked_sgd's exact-count policy with the restated primitives (sandbox.cpp:222-253)."""
-    for case in gold("sgd.json"):
+    for case in gold("sgd.json")["runs"]:
         if case["policy"] != 2:
             continue
         d, M = case["d"], case["M"]
