@@ -1,17 +1,24 @@
 """Benchmark: TimelyFreeze pipeline training step on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model llama-1b]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model llama-8b]
 
-Workload (BASELINE.json configs[1], the single-GPU-sized config): LLaMA-3.2-1B-shaped
-decoder, GPipe, PP = N (N=1: one stage holds all 16 layers), M = 8 microbatches of
-2 x 2048 tokens, synthetic uniform tokens and N(0, 0.02) random-init weights.
+Workload (BASELINE.json configs[2], the north-star configuration): LLaMA-3-8B-shaped decoder
+(h 4096, 32 layers, GQA 32/8, head_dim 128, vocab 128256), 1F1B, PP = N, M = 32 microbatches of
+2 x 2048 tokens, synthetic uniform tokens and N(0, 0.02) random-init weights. N = 1: one stage holds
+all 32 layers (the whole model fits one B200's HBM). --gpus N > 1 without a launcher spawns the N
+ranks itself (torch.distributed.run on 127.0.0.1).
 
-Procedure (ours): run the Alg. 1 controller untimed through warm-up, the two
-monitoring halves (CUDA-event action times), the LP solve at T_m and the AFR ramp,
-then W stable-phase warm-up steps, then K timed stable-phase steps (device time,
-CUDA events on the trainer's stream, max over ranks). The same K steps are timed
-with every unit unfrozen (no-freeze) for the speed-up, and once more end-to-end
-through the C-ABI with host (pinned) token buffers (e2e).
+Procedure (ours): run the Alg. 1 controller untimed through warm-up, the two monitoring halves
+(CUDA-event action times), the LP solve at T_m and the AFR ramp, then W stable-phase warm-up
+steps, then K timed stable-phase steps (device time, CUDA events on the trainer's stream, max over
+ranks). The same steps are timed with every unit unfrozen (no-freeze) for the speed-up, and K
+more end-to-end through the C-ABI with pinned host token buffers and the loss read back (e2e).
+
+Reference arm (--impl reference) and cpu_baseline: the reference's own CPU implementation of the
+path (oracle/_ref, the unmodified reference compiled here) at the FULL parameter count of the
+workload, sharded element-wise over every host core: per step the controller work (schedule +
+DAG + longest path + the step's S*M exact-count masks) and the per-parameter pass (apf_update +
+the masked accumulation and SGD update of run_masked_sgd). Only steps actually timed are reported.
 """
 from __future__ import annotations
 
@@ -151,56 +158,126 @@ def ncu_traffic(kernel: str):
         return None
 
 
-def cpu_reference_step(shape, M: int, S: int, units: int, n_params: int, ratio: float, budget_s: float = 12.0):
-    """Reference CPU path (oracle/_ref: the unmodified reference compiled here) for one step of this
-    workload: schedule + DAG + longest path, S*M exact-count masks over the stage units, apf_update and
-    the masked SGD update over the stage parameters. The per-parameter part runs on a bounded sample
-    and is scaled linearly to the full parameter count."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import ref  # noqa: E402  (oracle: reference arm / cpu_baseline only)
+# ---------------------------------------------------------------- reference CPU path (oracle/_ref)
+# Only the reference arm and the cpu_baseline leg import oracle/ (the checker), never the product.
+_RW_MASKS = None
 
-    if not ref.available():
-        raise RuntimeError("oracle/_ref/libpfref.so is not built")
-    d1, d2 = 2_000_000, 8_000_000
-    t1 = min(ref.cpu_step_seconds("gpipe", S, 1, M, units, d1, ratio) for _ in range(2))
-    t2 = min(ref.cpu_step_seconds("gpipe", S, 1, M, units, d2, ratio) for _ in range(2))
-    per_param = max(0.0, (t2 - t1) / (d2 - d1))
-    fixed = max(0.0, t1 - per_param * d1)
-    est = fixed + per_param * n_params
-    return est, {"fixed_s": fixed, "per_param_ns": per_param * 1e9, "sample_params": [d1, d2],
-                 "sample": f"reference step (schedule+DAG+longest path, {S * M} sample_mask over {units} units, "
-                           f"apf_update + masked SGD) on {d1:,} and {d2:,} params, scaled linearly to {n_params:,} params"}
+
+def _ref_worker_init(masks):
+    global _RW_MASKS
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    _RW_MASKS = masks
+
+
+def _ref_worker_pass(job):
+    import ref  # noqa: E402  (oracle, reference arm / cpu_baseline only)
+
+    begin, end, block, per_unit = job
+    return ref.param_pass_seconds(begin, end, block, _RW_MASKS, per_unit)
+
+
+class ReferenceCpuStep:
+    """One step of this workload through the reference's CPU implementation (oracle/_ref), at the
+    full parameter count, on `workers` processes (element-wise shards of the parameters):
+
+      controller (main process): build_schedule + build_dag + longest_path_start_times and the
+        step's S*M exact-count masks over the stage's units (run_freezing_masks, freezectl.cpp:185-211);
+      per-parameter pass (workers): apf_update (freezectl.cpp:147-156) and the masked accumulation
+        sum_m U_m (.) g + SGD update (run_masked_sgd, sandbox.cpp:232-250) over every parameter.
+
+    Step time = controller + the slowest worker's pass (wall clock around both)."""
+
+    BLOCK = 1 << 16
+
+    def __init__(self, kind: str, R: int, C: int, M: int, n_units: int, n_params: int, ratio: float,
+                 workers: int | None = None):
+        import multiprocessing as mp
+
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import ref  # noqa: E402  (oracle, reference arm / cpu_baseline only)
+
+        if not ref.available():
+            raise RuntimeError("oracle/_ref/libpfref.so is not built")
+        self.ref = ref
+        self.kind, self.R, self.C, self.M = kind, R, C, M
+        self.n_units, self.n_params, self.ratio = n_units, n_params, ratio
+        self.workers = workers or os.cpu_count() or 1
+        _, masks = ref.controller_step(kind, R, C, M, n_units, ratio)
+        per_unit = max(1, n_params // max(1, n_units))
+        bounds = [n_params * i // self.workers for i in range(self.workers + 1)]
+        self.jobs = [(bounds[i], bounds[i + 1], self.BLOCK, per_unit) for i in range(self.workers)]
+        self.pool = mp.get_context("spawn").Pool(self.workers, initializer=_ref_worker_init, initargs=(masks,))
+        self.seed = 42
+
+    def step(self) -> dict:
+        w0 = time.perf_counter()
+        self.seed += 1
+        ctl_s, _ = self.ref.controller_step(self.kind, self.R, self.C, self.M, self.n_units, self.ratio, self.seed)
+        secs = self.pool.map(_ref_worker_pass, self.jobs, chunksize=1)
+        wall = time.perf_counter() - w0
+        return {"wall_s": wall, "controller_s": ctl_s, "param_pass_s": max(secs)}
+
+    def describe(self) -> str:
+        S = self.R * self.C
+        return (f"reference CPU step at full size: controller (schedule + DAG + longest path + {S * self.M} "
+                f"sample_mask over {self.n_units:,} units) + apf_update and masked SGD over all "
+                f"{self.n_params:,} parameters at frozen ratio {self.ratio:.3f}, {self.workers} worker processes "
+                f"(element-wise shards, {self.BLOCK}-element blocks)")
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def _workload_params(shape, S: int) -> tuple[int, int]:
+    """(parameters of the whole job, freeze units of stage 1): the same counts both arms report."""
+    from paper_2602_05754_b200.engine import param_layout
+
+    n_params = sum(param_layout(shape, s, S)["n_params"] for s in range(1, S + 1))
+    return n_params, param_layout(shape, 1, S)["n_units"]
 
 
 def run_reference(args) -> None:
-    from paper_2602_05754_b200.engine import PRESETS
-
     rank, world, _ = dist_env()
     if rank != 0:
         return
     shape = model_shape(args)
     M = args.microbatches
-    S = args.gpus
-    units = _units_for(shape, S)
-    n_params = shape.layers * shape.matmul_params_per_layer() // S + shape.vocab * shape.hidden
-    step_s, info = cpu_reference_step(shape, M, S, units, n_params, 0.8 * 0.8)
-    timed = []
-    for _ in range(args.warmup):
-        cpu_reference_step(shape, M, S, units, n_params, 0.64)
-    for _ in range(args.steps):
-        s, _ = cpu_reference_step(shape, M, S, units, n_params, 0.64)
-        timed.append(s)
-    step_s = statistics.mean(timed) if timed else step_s
+    C = stages_per_rank(args)
+    S = args.gpus * C
+    n_params, units = _workload_params(shape, S)
+    ratio = args.r_max  # the LP's stable-phase mean freeze ratio is r_max on these workloads
+    cpu = ReferenceCpuStep(args.schedule, args.gpus, C, M, units, n_params, ratio)
+    budget = float(os.environ.get("PF_REF_BUDGET_S", "150"))
+    try:
+        warm = min(args.warmup, 1)
+        for _ in range(warm):
+            cpu.step()
+        timed = []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            timed.append(cpu.step())
+            if time.perf_counter() - t0 > budget:
+                break
+    finally:
+        cpu.close()
+    step_s = statistics.mean(r["wall_s"] for r in timed)
     tokens = M * shape.tokens
     value = tokens / step_s
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(args, shape),
-            "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": 1, "kind": "reference",
-                             "sample": info["sample"]},
+            "steps": len(timed), "steps_requested": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+            "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config(args, shape),
+            "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cpu.workers, "kind": "reference",
+                             "sample": cpu.describe()},
             "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "the reference has no transformer math; its step is the CPU stand-in (controller masks, APF, masked SGD)"}
+            "n_params": n_params, "nproc": os.cpu_count(),
+            "step_breakdown_s": {"controller": round(statistics.mean(r["controller_s"] for r in timed), 4),
+                                 "param_pass": round(statistics.mean(r["param_pass_s"] for r in timed), 3)},
+            "timed_budget_s": budget,
+            "note": ("the reference has no transformer math; its step is the CPU path of the freeze controller, "
+                     "APF metric and masked update at the workload's parameter count. Steps stop early (reported "
+                     "'steps') once the timed steps exceed timed_budget_s.")}
     print(json.dumps(line), flush=True)
 
 
@@ -244,6 +321,108 @@ def stages_per_rank(args) -> int:
     return args.chunks if args.schedule in ("interleaved-1f1b", "interleaved") else 1
 
 
+def _dev_view(ptr: int, n: int, dtype):
+    """Zero-copy torch view of a device buffer returned by the C-ABI."""
+    import torch
+
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<i2"}[dtype]
+    obj = type("Cai", (), {})()
+    obj.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+    t = torch.as_tensor(obj, device="cuda")
+    return t.view(torch.bfloat16) if dtype is torch.bfloat16 else t
+
+
+def pp_consistency_check(world: int, rank: int, local: int) -> dict:
+    """Before timing: one step of a tiny LLaMA pipeline split over the job's ranks (PP = N, NCCL P2P)
+    against the same model as ONE stage on this GPU, on identical weights and tokens, nothing frozen.
+    The PP = 1 copy is assembled from every rank's stage parameters (all-gathered), so both compute
+    the same function; the per-parameter update must agree (max relative difference over ranks).
+    At N = 1 the split is 2 local stages on this GPU (same mapping code, no NCCL)."""
+    import dataclasses
+
+    import numpy as np
+    import torch
+
+    from paper_2602_05754_b200.engine import PRESETS, Trainer, param_layout
+
+    split = max(2, world)
+    shape = dataclasses.replace(PRESETS["tiny"], layers=max(4, split))
+    M, lr = 4, 0.5
+    if world > 1:
+        import torch.distributed as dist
+
+        trA = Trainer(shape, "1f1b", world, 1, M, rank=rank, lr=lr, seed=3, device=local)
+        trA.init_comm()
+        stages = [rank + 1]
+    else:
+        trA = Trainer(shape, "interleaved-1f1b", 1, 2, M, rank=0, lr=lr, seed=3, device=local)
+        stages = [1, 2]
+    trB = Trainer(shape, "1f1b", 1, 1, M, rank=0, lr=lr, seed=3, device=local)
+    trA.set_override(0.0)
+    trB.set_override(0.0)
+    layB = param_layout(shape, 1, 1)
+    offB = {e["name"]: e for e in layB["units"] + layB["dense"]}
+    bufB = trB.stage_buffers(0)
+    mB = _dev_view(bufB["master"], bufB["n_params"], torch.float32)
+    wB = _dev_view(bufB["weights"], bufB["n_params"], torch.bfloat16)
+
+    def stage_master(i):
+        b = trA.stage_buffers(i)
+        return _dev_view(b["master"], b["n_params"], torch.float32)
+
+    # every stage's master parameters, gathered to every rank
+    mine = {s: stage_master(i).clone() for i, s in enumerate(stages)}
+    if world > 1:
+        n_max = max(param_layout(shape, s, split)["n_params"] for s in range(1, split + 1))
+        pad = torch.zeros(n_max, device="cuda")
+        pad[: mine[rank + 1].numel()] = mine[rank + 1]
+        parts = [torch.zeros_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        allm = {s + 1: parts[s] for s in range(world)}
+    else:
+        allm = mine
+    before = {}
+    for s in range(1, split + 1):
+        lay = param_layout(shape, s, split)
+        for e in lay["units"] + lay["dense"]:
+            n = e["rows"] * e["cols"]
+            dst = offB[e["name"]]["offset"]
+            mB[dst:dst + n] = allm[s][e["offset"]:e["offset"] + n]
+            wB[dst:dst + n] = mB[dst:dst + n].bfloat16()
+            if s in stages:
+                before[e["name"]] = (s, e)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(123)
+    tok = rng.integers(0, shape.vocab, size=(M, shape.tokens), dtype=np.int32)
+    tgt = rng.integers(0, shape.vocab, size=(M, shape.tokens), dtype=np.int32)
+    thetaB0 = mB.clone()
+    thetaA0 = {s: stage_master(i).clone() for i, s in enumerate(stages)}
+    rA = trA.step(1, tok, tgt)
+    rB = trB.step(1, tok, tgt)
+    torch.cuda.synchronize()
+    worst, bitwise = 0.0, True
+    for name, (s, e) in before.items():
+        i = stages.index(s)
+        n = e["rows"] * e["cols"]
+        dA = stage_master(i)[e["offset"]:e["offset"] + n] - thetaA0[s][e["offset"]:e["offset"] + n]
+        o = offB[name]["offset"]
+        dB = mB[o:o + n] - thetaB0[o:o + n]
+        bitwise &= bool(torch.equal(dA, dB))
+        den = dB.norm().item()
+        if den > 0:
+            worst = max(worst, (dA - dB).norm().item() / den)
+    if world > 1:
+        t = torch.tensor([worst, 0.0 if bitwise else 1.0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        worst, bitwise = t[0].item(), t[1].item() == 0.0
+    trA.close()
+    trB.close()
+    return {"what": f"tiny LLaMA ({shape.layers} layers, M={M}) split over {split} stages "
+                    f"({'NCCL P2P over ' + str(world) + ' ranks' if world > 1 else '2 local stages, 1 GPU'}) vs 1 stage",
+            "max_rel_update_diff": worst, "bitwise_equal": bitwise, "ok": worst <= 1e-2,
+            "loss_pp1": round(rB["loss"], 6)}
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -258,7 +437,11 @@ def run_ours(args) -> None:
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL init logging (communicator ranks / transports) for the run's record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl")
+    pp_check = pp_consistency_check(world, rank, local)
     shape = model_shape(args)
     M = args.microbatches
     phases = tuple(args.phases)
@@ -328,20 +511,24 @@ def run_ours(args) -> None:
     ms_step = dev_ms / args.steps
     value = tokens_per_step / (ms_step * 1e-3)
 
-    # ---- no-freeze comparison (same steps, every unit updated)
+    # ---- no-freeze comparison (every unit updated; a shorter run: it is the speed-up's denominator)
+    nf_steps = min(args.steps, 8)
     tr.set_override(0.0)
-    for i in range(max(1, args.warmup // 2)):
+    for i in range(2):
         tr.step(t + i)
-    t += max(1, args.warmup // 2)
-    nf_ms, _, nf_res, _ = timed_steps(t, args.steps)
-    t += args.steps
-    nf_ms = max_over_ranks(nf_ms) / args.steps
+    t += 2
+    nf_ms, _, nf_res, _ = timed_steps(t, nf_steps)
+    t += nf_steps
+    nf_ms = max_over_ranks(nf_ms) / nf_steps
     tr.set_override(None)
 
-    # ---- e2e through the C-ABI with host (pinned) token buffers; loss read back each step
+    # ---- e2e through the C-ABI with host (pinned) token buffers; loss read back each step. The
+    # host tokens are drawn from one seeded stream, identical on every rank (the first stage's
+    # tokens and the last stage's targets then belong to the same microbatches).
     T = shape.tokens
-    host_tok = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32).pin_memory()
-    host_tgt = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32).pin_memory()
+    g = torch.Generator().manual_seed(args.seed)
+    host_tok = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32, generator=g).pin_memory()
+    host_tgt = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32, generator=g).pin_memory()
     hp = (host_tok.numpy(), host_tgt.numpy())
     e2e_dev, e2e_wall, e2e_res, _ = timed_steps(t, args.steps, host=hp)
     t += args.steps
@@ -357,19 +544,28 @@ def run_ours(args) -> None:
         batch_ms = statistics.mean(r["batch_ms"] for r in res)
         pred_ms = statistics.mean(r["predicted_ms"] for r in res)
         roof = gemm_roofline(peaks, shape, probe_n.value, probe_ms.value)
-        try:
-            units = tr.stage_buffers(0)["n_units"]
-            cpu_s, cpu_info = cpu_reference_step(shape, M, world, units, tr.info["params"], mean_ratio)
-            cpu = {"value": round(tokens_per_step / cpu_s, 2), "unit": "tokens/s", "cores": 1, "kind": "reference",
-                   "sample": cpu_info["sample"]}
-        except Exception as e:  # pragma: no cover - oracle missing on the box
-            cpu = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+        cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": "reference", "sample": "not run (N > 1)"}
+        if world == 1 and not os.environ.get("PF_SKIP_CPU_BASELINE"):
+            # the reference's CPU path on this host's cores, one full-size step (after the timed region)
+            n_params, units = _workload_params(shape, world * C)
+            try:
+                ref_step = ReferenceCpuStep(args.schedule, world, C, M, units, n_params, mean_ratio)
+                try:
+                    r = ref_step.step()
+                finally:
+                    ref_step.close()
+                cpu = {"value": round(tokens_per_step / r["wall_s"], 2), "unit": "tokens/s", "cores": ref_step.workers,
+                       "kind": "reference", "sample": ref_step.describe() + " (1 step)",
+                       "ms_per_step": round(r["wall_s"] * 1e3, 1)}
+            except Exception as e:  # pragma: no cover - oracle missing on the box
+                cpu["sample"] = f"unavailable: {e}"
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, N(0,0.02) random-init weights)",
             "config": _config(args, shape),
-            "nofreeze": {"value": round(tokens_per_step / (nf_ms * 1e-3), 1), "ms_per_step": round(nf_ms, 3)},
+            "nofreeze": {"value": round(tokens_per_step / (nf_ms * 1e-3), 1), "ms_per_step": round(nf_ms, 3),
+                         "steps": nf_steps},
             "freeze_speedup": round(nf_ms / ms_step, 4),
             "batch_vs_lp": {"batch_ms": round(batch_ms, 3), "lp_makespan_ms": round(pred_ms, 3),
                             "ratio": round(batch_ms / pred_ms, 4) if pred_ms else None,
@@ -388,6 +584,8 @@ def run_ours(args) -> None:
             "gpu_launches": int(launches),
             "attention_backend": attention_backend(shape, lib),
             "loss": {"first": round(ctl[0]["loss"], 4), "last": round(res[-1]["loss"], 4)},
+            "n_params": tr.info["params"] if world == 1 else None,
+            "pp_check": pp_check,
         }
         print(json.dumps(line), flush=True)
     tr.close()
@@ -413,21 +611,28 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--model", default="llama-1b")
-    ap.add_argument("--schedule", default="gpipe",
+    ap.add_argument("--model", default="llama-8b")
+    ap.add_argument("--schedule", default="1f1b",
                     choices=["gpipe", "1f1b", "interleaved-1f1b", "zbv", "zbv-split"])
     ap.add_argument("--chunks", type=int, default=2, help="virtual stages per GPU for interleaved-1f1b")
-    ap.add_argument("--microbatches", type=int, default=8)
+    ap.add_argument("--microbatches", type=int, default=32)
     ap.add_argument("--layers", type=int, default=0,
                     help="override the preset's layer count (a per-rank slice of a larger pipeline)")
     ap.add_argument("--r-max", type=float, default=0.8)
-    ap.add_argument("--phases", type=int, nargs=4, default=[2, 8, 10, 10000])
+    ap.add_argument("--phases", type=int, nargs=4, default=[1, 7, 8, 10000],
+                    help="T_w T_m T_f T_total: warm-up 1, monitoring 2-6 (3 unfrozen + 2 frozen samples), LP at 7")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--optimizer", choices=["sgd", "adamw"], default="sgd",
                     help="sgd = the reference's masked update (sandbox.cpp:250); adamw = the paper's optimizer")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no launcher: spawn one rank per GPU on this node (same command line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("MASTER_PORT", "29531"),
+               os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:
