@@ -80,6 +80,15 @@ int pf_gemm_dswiglu(const void* dY, long long ldy, const void* Wd, long long ldw
  * qkv packed [B S, 3 nh 64], out [B S, nh 64], lse fp32 [B][nh][S]; the backward writes dq|dk|dv
  * into a packed dqkv (may alias qkv) and, when dbias != NULL, adds the qkv bias gradient (the column sums
  * of the bf16 dq|dk|dv, fp32 [3 nh 64]) into dbias. */
+/* K7 attention of the LLaMA stages (flash_attn.cu; tcgen05 MMAs into TMEM fed by TMA): causal (or
+ * bidirectional) multi-head attention with native GQA over the packed qkv [B*S, (nh + 2 nkv) hd] bf16
+ * (after RoPE); S % 128 == 0, hd 64 or 128. out [B*S, nh*hd] bf16, lse [B, nh, S] fp32 (log2 domain).
+ * The backward writes dq|dk|dv packed into dqkv [B*S, (nh + 2 nkv) hd] (may be qkv itself); with
+ * rope_theta > 0 the rotate-half RoPE backward is applied to dq and dk (inputs were rotated). */
+int pf_flash_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int nh, int nkv, int hd, float scale,
+                      int causal, void* stream);
+int pf_flash_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B, int S,
+                      int nh, int nkv, int hd, float scale, int causal, float rope_theta, void* stream);
 int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int nh, int hd, float scale, void* stream);
 int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, float* dbias,
                     int B, int S, int nh, int hd, float scale, void* stream);
@@ -241,7 +250,8 @@ int pf_nccl_unique_ids(void* out, int count);
 int pf_trainer_comm_ids(pf_ctx* ctx, int* count);
 /* links[3*k..3*k+2] = (kind 0 act / 1 grad, src rank, dst rank) for k < pf_trainer_comm_ids - 1 */
 int pf_trainer_links(pf_ctx* ctx, int* links);
-/* Library backend used for the attention glue: "cudnn" or "flash" (ATen). */
+/* The attention implementation of the LLaMA stages (always this library's own flash_attn.cu kernels;
+ * ViT stages with seq <= 64 use vit_attention.cu). */
 const char* pf_attention_backend(void);
 int pf_trainer_init_comm(pf_ctx* ctx, const void* ids, int nranks, int rank);
 /* The cudaStream_t the trainer enqueues its step on (for device-side timing by the caller). */

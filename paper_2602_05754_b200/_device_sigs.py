@@ -49,6 +49,9 @@ DEVICE_SIGNATURES = {
     "pf_swiglu_fwd": ([c_vp, c_vp, c_int, c_int, c_vp], c_int),
     "pf_gemm_swiglu": ([c_vp, c_ll, c_vp, c_ll, c_vp, c_vp, c_int, c_int, c_int, c_vp], c_int),
     "pf_gemm_set_streamk": ([c_int], c_int),
+    "pf_flash_attn_fwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_f, c_int, c_vp], c_int),
+    "pf_flash_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_f, c_int, c_f, c_vp],
+                          c_int),
     "pf_vit_attn_fwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_vit_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_layernorm_fwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f, c_vp], c_int),

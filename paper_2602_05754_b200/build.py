@@ -30,13 +30,6 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
-def _torch_paths():
-    import torch  # noqa: F401  (only for include / lib paths of ATen, used by attention glue)
-
-    tdir = os.path.dirname(os.path.abspath(sys.modules["torch"].__file__))
-    return [os.path.join(tdir, "include"), os.path.join(tdir, "include", "torch", "csrc", "api", "include")], os.path.join(tdir, "lib")
-
-
 def _newer(target: str, sources: list[str]) -> bool:
     if not os.path.exists(target):
         return True
@@ -65,16 +58,26 @@ def build_host(force: bool = False) -> str:
     return out
 
 
+def _nccl_flags() -> list[str]:
+    """Link NCCL: the system library when its headers and .so are installed (this image), else the
+    nvidia-nccl wheel bundled with the Python environment."""
+    import glob as _g
+
+    if _g.glob("/usr/lib/x86_64-linux-gnu/libnccl.so*") or _g.glob("/usr/local/cuda/lib64/libnccl.so*"):
+        return ["-lnccl"]
+    for d in _g.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia", "nccl", "lib")):
+        return [f"-L{d}", "-Xlinker", f"-rpath={d}", "-l:libnccl.so.2"]
+    return ["-lnccl"]
+
+
 def build_device(force: bool = False) -> str:
     os.makedirs(LIB, exist_ok=True)
     os.makedirs(OBJ, exist_ok=True)
     out = os.path.join(LIB, "libpf_device.so")
-    tinc, tlib = _torch_paths()
     cu = sorted(glob.glob(os.path.join(DEV_SRC, "*.cu")))
     cpp = sorted(glob.glob(os.path.join(DEV_SRC, "*.cpp")))
     headers = glob.glob(os.path.join(DEV_SRC, "*.cuh")) + glob.glob(os.path.join(DEV_SRC, "*.hpp")) + glob.glob(os.path.join(INC, "*.h"))
     common = ["-I", INC, "-I", DEV_SRC, "-I", HOST_SRC]
-    tflags = [f"-I{p}" for p in tinc] + ["-D_GLIBCXX_USE_CXX11_ABI=1"]
     jobs = []
     objs = []
     for src in cu + cpp:
@@ -82,22 +85,20 @@ def build_device(force: bool = False) -> str:
         objs.append(obj)
         if not (force or _newer(obj, [src] + headers)):
             continue
-        uses_torch = os.path.basename(src).startswith("aten_")
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-                   "-Xcompiler", "-fPIC", *common, *(tflags if uses_torch else []), "-c", src, "-o", obj]
+                   "-Xcompiler", "-fPIC", *common, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", *common, f"-I{CUDA_HOME}/include",
-                   *(tflags if uses_torch else []), "-c", src, "-o", obj]
+                   "-c", src, "-o", obj]
         jobs.append(cmd)
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
             list(ex.map(_run, jobs))
     if force or jobs or _newer(out, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out,
-               f"-L{tlib}", f"-Xlinker", f"-rpath={tlib}",
-               "-lc10", "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart",
-               f"-L{LIB}", "-lpf_host", "-Xlinker", "-rpath=$ORIGIN", "-lnccl"]
+        # no libtorch: the device library needs only the CUDA runtime / driver, NCCL and libpf_host
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", out, "-lcudart",
+               f"-L{LIB}", "-lpf_host", "-Xlinker", "-rpath=$ORIGIN", *_nccl_flags()]
         _run(cmd)
     return out
 

@@ -26,7 +26,7 @@ int guard(F&& f) {
     const int rc = f();
     if (rc == PF_ERR_CUDA) {
       const cudaError_t e = cudaGetLastError();
-      g_err = std::string("cuda: ") + cudaGetErrorString(e) + " / " + pf::attn_last_error();
+      g_err = std::string("cuda: ") + cudaGetErrorString(e);
     }
     return rc;
   } catch (const pipefreeze::config_error& e) {
@@ -218,6 +218,44 @@ int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const fl
     return pf::launch_vit_attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(out),
                                    static_cast<const __nv_bfloat16*>(dout), lse, static_cast<__nv_bfloat16*>(dqkv),
                                    dbias, B, seq, nh, hd, scale, S(stream));
+  });
+}
+
+int pf_flash_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, int nh, int nkv, int hd, float scale,
+                      int causal, void* stream) {
+  return guard([&] {
+    return pf::launch_flash_attn_fwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out),
+                                     static_cast<long long>(nh) * hd, lse, B, seq, nh, nkv, hd, scale, causal != 0,
+                                     S(stream));
+  });
+}
+
+int pf_flash_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B, int seq,
+                      int nh, int nkv, int hd, float scale, int causal, float rope_theta, void* stream) {
+  return guard([&] {
+    const long long T = static_cast<long long>(B) * seq;
+    float* D = nullptr;
+    float* acc = nullptr;
+    float2* cs = nullptr;
+    int rc = PF_OK;
+    if (cudaMallocAsync(&D, static_cast<size_t>(T) * nh * 4, S(stream)) != cudaSuccess ||
+        cudaMallocAsync(&acc, static_cast<size_t>(T) * nh * hd * 4, S(stream)) != cudaSuccess)
+      rc = PF_ERR_CUDA;
+    if (rc == PF_OK && rope_theta > 0.f) {
+      if (cudaMallocAsync(&cs, static_cast<size_t>(seq) * (hd / 2) * sizeof(float2), S(stream)) != cudaSuccess)
+        rc = PF_ERR_CUDA;
+      else
+        rc = pf::launch_rope_table(cs, seq, hd, rope_theta, S(stream));
+    }
+    if (rc == PF_OK)
+      rc = pf::launch_flash_attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(out),
+                                     static_cast<const __nv_bfloat16*>(dout), lse, D, acc,
+                                     static_cast<__nv_bfloat16*>(dqkv), cs, B, seq, nh, nkv, hd, scale, causal != 0,
+                                     S(stream));
+    if (D) cudaFreeAsync(D, S(stream));
+    if (acc) cudaFreeAsync(acc, S(stream));
+    if (cs) cudaFreeAsync(cs, S(stream));
+    return rc;
   });
 }
 
@@ -479,7 +517,9 @@ extern "C" int pf_trainer_action_starts(pf_ctx* ctx, double* start_ms) {
   });
 }
 
-extern "C" const char* pf_attention_backend(void) { return pf::attn_backend_is_cudnn() ? "cudnn" : "flash"; }
+extern "C" const char* pf_attention_backend(void) {
+  return "flash_attn.cu (hand-written tcgen05/TMEM/TMA flash attention, sm_100a)";
+}
 
 extern "C" int pf_trainer_comm_ids(pf_ctx* ctx, int* count) {
   return guard([&] {

@@ -1,0 +1,722 @@
+// K7 attention: causal (LLaMA) or bidirectional multi-head attention with native GQA, hand-written
+// for sm_100a. Replaces the library fused attention the stage used before (the reference has no
+// attention at all: its cost sits inside the forward / backward_act stand-ins,
+// proj/src/timing.cpp:21-23, the part of the backward freezing can never shrink).
+//
+// Layout (stage.cpp): qkv [T, (nh + 2 nkv) hd] bf16 after RoPE, T = B * S tokens, a head's 128-row
+// tile of q / k / v is read straight out of it by TMA (box 64 x 128, SWIZZLE_128B; a tile is hd/64
+// such 16 KB regions). S % 128 == 0, hd in {64, 128}.
+//
+// Forward (flash_fwd_kernel, one CTA per (sequence, head, 128-query block), heaviest causal blocks
+// first; 6 warps):
+//   warp 0      TMA: Q once, then K_j and V_j into a ring of 128-row tiles
+//   warp 1      TMEM allocation + the MMA issuer (one thread):
+//                 S_j = Q K_j^T   tcgen05.mma, A and B from shared memory -> TMEM (two S buffers)
+//                 O  += P_j V_j   A = P_j from TMEM (bf16, written over S_j), B = V_j -> TMEM O
+//               S_{j+1} is issued before waiting for P_j, so the tensor pipe computes the next
+//               scores while the softmax warps exponentiate the current ones.
+//   warps 2-5   softmax, one thread per query row: tcgen05.ld of the S row, row max, lazy rescale of
+//               O in TMEM only when the max grows by more than 2^8 (FA4-style), P = 2^(s - m) as
+//               bf16 back into TMEM; epilogue O / l -> bf16 [T, nh*hd], LSE (log2 domain) [B, nh, S].
+//
+// Backward (flash_bwd_kernel, one CTA per (sequence, kv head, 128-key block): it loops over the
+// rep = nh / nkv query heads of the group and the query blocks the keys see, so K_j / V_j stay in
+// shared memory and dK / dV accumulate in TMEM):
+//   S^T  = K_j Q_i^T, dP^T = V_j dO_i^T                       (TMEM, lane = key row)
+//   P^T  = 2^(S^T * c - LSE_i), dS^T = P^T (dP^T - D_i)      (softmax warps; bf16 into TMEM over
+//                                                              S^T / dP^T and dS^T into shared memory)
+//   dV  += P^T dO_i,  dK += dS^T Q_i                          (A from TMEM)
+//   dQ_i = dS K_j                                             (A = dS^T in shared memory read MN-major)
+// dQ_i is drained from TMEM by the softmax warps into an fp32 accumulator (red.global.add.v4.f32);
+// flash_bwd_dq_kernel then scales it, applies the RoPE backward and writes bf16 dq into the packed
+// dqkv. dK (scaled, RoPE backward) and dV are written by the CTA that owns the key block, in place
+// over qkv's k / v columns of that block (no other CTA reads them). flash_bwd_pre_kernel computes
+// D = rowsum(dO * O) and zeroes the dQ accumulator.
+// The same shared-memory tile serves as a K-major operand (rows = M/N, columns = K) and as an
+// MN-major one (rows = K): SWIZZLE_128B 64-column regions are both layouts' canonical form.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernel_util.cuh"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace pf {
+
+int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                     int box_rows);
+
+namespace {
+
+constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold: unnormalised P stays <= 2^8
+constexpr int kAttnThreads = 192;
+
+struct FwdParams {
+  CUtensorMap tqkv;  // qkv [T, W], box {64, 128}
+  __nv_bfloat16* out;
+  long long ldo;
+  float* lse;  // [B, nh, S]: m + log2(l) of the log2-scaled scores
+  int B, S, nh, nkv, rep, nqb, causal;
+  float scale_log2;
+};
+
+struct BwdParams {
+  CUtensorMap tqkv;  // qkv [T, W], box {64, 128}
+  CUtensorMap tdo;   // dO [T, nh*hd], box {64, 128}
+  const float* lse;  // [B, nh, S]
+  const float* D;    // [B, nh, S]
+  float* dq_acc;     // [T, nh*hd] fp32
+  __nv_bfloat16* dqkv;
+  long long ldq;  // row stride of qkv / dqkv (W)
+  const float2* rope;  // (cos, sin) [S][hd/2] or null
+  int B, S, nh, nkv, rep, nqb, causal;
+  float scale_log2, scale;
+};
+
+template <int HD>
+struct AttnCfg {
+  static constexpr int TILE = 128 * HD * 2;  // one 128-row tile, HD/64 regions of 16 KB
+  static constexpr int FWD_STAGES = HD == 128 ? 4 : 6;
+  static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 256;
+  // bwd: K, V, two {Q, dO, lse, D} stages, dS^T (128 x 128 bf16)
+  static constexpr int BWD_QDO = 2 * TILE + 1024;
+  static constexpr int BWD_SMEM_NOPAD = 2 * TILE + 2 * BWD_QDO + 32768 + 256;
+  static constexpr int BWD_SMEM = BWD_SMEM_NOPAD + 1024 <= 232448 ? BWD_SMEM_NOPAD + 1024 : BWD_SMEM_NOPAD;
+};
+
+// K-major SW128 operand of a 128-row tile: k-step kk (16 elements) of the hd dimension
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
+  return sdesc_sw128(base + static_cast<uint32_t>((kk >> 2) * 16384 + (kk & 3) * 32), 16, 1024);
+}
+// MN-major SW128 operand of a 128-row tile whose rows are the K dimension: k-step kk (16 rows)
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
+  return sdesc_sw128(base + static_cast<uint32_t>(kk * 2048), 16384, 1024);
+}
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~static_cast<uintptr_t>(1023));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid_constant__ FwdParams p) {
+  using Cfg = AttnCfg<HD>;
+  constexpr int TILE = Cfg::TILE;
+  constexpr int ST = Cfg::FWD_STAGES;
+  constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false, false);
+  constexpr uint32_t IDESC_O = idesc_bf16_f32(128, HD, false, true);
+  constexpr uint32_t O_COL = 256;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + TILE;
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(sKV + ST * TILE);
+  uint64_t* kv_full = q_full + 1;
+  uint64_t* kv_empty = kv_full + ST;
+  uint64_t* s_full = kv_empty + ST;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_bar = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nbh = p.B * p.nh;
+  const int bh = blockIdx.x % nbh;
+  const int qb = p.causal ? p.nqb - 1 - static_cast<int>(blockIdx.x) / nbh : static_cast<int>(blockIdx.x) / nbh;
+  const int b = bh / p.nh, h = bh % p.nh, g = h / p.rep;
+  const int nblk = p.causal ? qb + 1 : p.nqb;
+  const int row0 = b * p.S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+    }
+    mbar_init(o_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch(&p.tqkv);
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(q_full, TILE);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) tma_load_2d(sQ + c * 16384, &p.tqkv, q_full, h * HD + c * 64, row0 + qb * 128);
+      for (int u = 0; u < 2 * nblk; ++u) {
+        const int st = u % ST;
+        mbar_wait(&kv_empty[st], ((u / ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], TILE);
+        const int col = ((u & 1) ? (p.nh + p.nkv + g) : (p.nh + g)) * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_2d(sKV + st * TILE + c * 16384, &p.tqkv, &kv_full[st], col + c * 64, row0 + (u >> 1) * 128);
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sQ);
+      auto issue_s = [&](int j) {
+        const int u = 2 * j, st = u % ST;
+        mbar_wait(&kv_full[st], (u / ST) & 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(sKV + st * TILE);
+        const uint32_t d = tmem + static_cast<uint32_t>((j & 1) * 128);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) umma_bf16(d, kmajor_desc(qa, k), kmajor_desc(kb, k), IDESC_S, k > 0 ? 1u : 0u);
+        umma_commit(&kv_empty[st]);
+        umma_commit(&s_full[j & 1]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) issue_s(j + 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const int u = 2 * j + 1, st = u % ST;
+        mbar_wait(&kv_full[st], (u / ST) & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(sKV + st * TILE);
+        const uint32_t pa = tmem + static_cast<uint32_t>((j & 1) * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16_ts(tmem + O_COL, pa + static_cast<uint32_t>(k * 8), mnmajor_desc(vb, k), IDESC_O,
+                       (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&kv_empty[st]);
+        umma_commit(o_bar);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const int qpos = qb * 128 + r;
+    float m_used = 0.f, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sa = tmem + lane_off + static_cast<uint32_t>((j & 1) * 128);
+      uint32_t sr[128];
+      tmem_ld_32x32b_x32(sa, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld_32x32b_x32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld_32x32b_x32(sa + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+      tmem_ld_32x32b_x32(sa + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+      tmem_ld_wait();
+      const bool diag = p.causal && j == qb;
+      float s[128];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        s[i] = __uint_as_float(sr[i]) * p.scale_log2;
+        if (diag && i > r) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      if (j == 0) {
+        m_used = mx;
+      } else if (mx > m_used + kRescaleLog2) {
+        // O and l were accumulated against m_used: rescale once PV_{j-1} has landed in TMEM
+        mbar_wait(o_bar, (j - 1) & 1);
+        tc_fence_after();
+        const float a = ex2_approx(m_used - mx);
+        l *= a;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+          tmem_st_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
+        }
+        tmem_st_wait();
+        m_used = mx;
+      }
+      uint32_t pk[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float p0 = ex2_approx(s[2 * i] - m_used), p1 = ex2_approx(s[2 * i + 1] - m_used);
+        l += p0 + p1;
+        pk[i] = pack_bf16x2(p0, p1);
+      }
+      tmem_st_32x32b_x32(sa, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tmem_st_32x32b_x32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[j & 1]);
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(o_bar, (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + qpos) * p.ldo + h * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
+      tmem_ld_wait();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+        w.y = pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+        w.z = pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+        w.w = pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+        dst[v] = w;
+      }
+    }
+    p.lse[(static_cast<long long>(b) * p.nh + h) * p.S + qpos] = m_used + __log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// D[b, h, s] = sum_d dO * O (fp32 from the bf16 tensors); zero the dQ accumulator. One warp per
+// (token, head).
+template <int HD>
+__global__ void flash_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
+                                     float* __restrict__ D, float* __restrict__ dq_acc, int T, int S, int nh) {
+  pdl_begin();
+  const long long nw = static_cast<long long>(T) * nh;
+  const int lane = threadIdx.x & 31;
+  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < nw;
+       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
+    const long long t = w / nh;
+    const int h = static_cast<int>(w % nh);
+    const long long off = t * nh * HD + h * HD + lane * (HD / 32);
+    float acc = 0.f;
+    if constexpr (HD == 128) {
+      const uint2 o = *reinterpret_cast<const uint2*>(out + off);
+      const uint2 d = *reinterpret_cast<const uint2*>(dout + off);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&d);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 a = __bfloat1622float2(o2[i]), c = __bfloat1622float2(d2[i]);
+        acc = fmaf(a.x, c.x, fmaf(a.y, c.y, acc));
+      }
+      *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(out + off));
+      const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
+      acc = fmaf(a.x, c.x, a.y * c.y);
+      *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const int b = static_cast<int>(t / S), s = static_cast<int>(t % S);
+      D[(static_cast<long long>(b) * nh + h) * S + s] = acc;
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid_constant__ BwdParams p) {
+  using Cfg = AttnCfg<HD>;
+  constexpr int TILE = Cfg::TILE;
+  constexpr uint32_t IDESC_SS = idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
+  constexpr uint32_t IDESC_TS = idesc_bf16_f32(128, HD, false, true);    // dV, dK: A in TMEM, B MN-major
+  constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, HD, true, true);     // dQ: A (dS) and B (K) MN-major
+  constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + TILE;
+  uint8_t* sQD = smem + 2 * TILE;  // 2 stages of {Q, dO, lse[128], D[128]}
+  uint8_t* sDS = sQD + 2 * Cfg::BWD_QDO;
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sDS + 32768);
+  uint64_t* qdo_full = kv_full + 1;
+  uint64_t* qdo_empty = qdo_full + 2;
+  uint64_t* s_full = qdo_empty + 2;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* dq_full = p_full + 1;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* dkv_full = dq_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nbg = p.B * p.nkv;
+  const int bg = blockIdx.x % nbg;
+  const int j = p.causal ? static_cast<int>(blockIdx.x) / nbg : static_cast<int>(blockIdx.x) / nbg;
+  const int b = bg / p.nkv, g = bg % p.nkv;
+  const int row0 = b * p.S;
+  const int i0 = p.causal ? j : 0;
+  const int nq = p.nqb - i0;
+  const int niter = p.rep * nq;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qdo_full[s], 1);
+      mbar_init(&qdo_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 128);
+    mbar_init(dkv_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tqkv);
+    tma_prefetch(&p.tdo);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(kv_full, 2 * TILE);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_2d(sK + c * 16384, &p.tqkv, kv_full, (p.nh + g) * HD + c * 64, row0 + j * 128);
+        tma_load_2d(sV + c * 16384, &p.tqkv, kv_full, (p.nh + p.nkv + g) * HD + c * 64, row0 + j * 128);
+      }
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1;
+        const int h = g * p.rep + it / nq, i = i0 + it % nq;
+        mbar_wait(&qdo_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], Cfg::BWD_QDO);
+        uint8_t* base = sQD + st * Cfg::BWD_QDO;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_2d(base + c * 16384, &p.tqkv, &qdo_full[st], h * HD + c * 64, row0 + i * 128);
+          tma_load_2d(base + TILE + c * 16384, &p.tdo, &qdo_full[st], h * HD + c * 64, row0 + i * 128);
+        }
+        const long long li = (static_cast<long long>(b) * p.nh + h) * p.S + i * 128;
+        bulk_load_1d(base + 2 * TILE, p.lse + li, 512, &qdo_full[st]);
+        bulk_load_1d(base + 2 * TILE + 512, p.D + li, 512, &qdo_full[st]);
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), dsa = smem_u32(sDS);
+      for (int it = 0; it < niter; ++it) {
+        const int st = it & 1;
+        mbar_wait(&qdo_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sQD + st * Cfg::BWD_QDO);
+        const uint32_t da = qa + TILE;
+        // S^T = K_j Q_i^T (over P^T of the previous iteration: its dV MMA was issued before)
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16(tmem + S_COL, kmajor_desc(ka, k), kmajor_desc(qa, k), IDESC_SS, k > 0 ? 1u : 0u);
+        if (it > 0) {  // dQ_{it-1} (in the dP columns) has been drained
+          mbar_wait(dq_empty, (it - 1) & 1);
+          tc_fence_after();
+        }
+        // dP^T = V_j dO_i^T
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16(tmem + DP_COL, kmajor_desc(va, k), kmajor_desc(da, k), IDESC_SS, k > 0 ? 1u : 0u);
+        umma_commit(s_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+        // dV += P^T dO_i, dK += dS^T Q_i (A from TMEM, 16 queries per k-step)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16_ts(tmem + DV_COL, tmem + S_COL + k * 8, mnmajor_desc(da, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16_ts(tmem + DK_COL, tmem + DP_COL + k * 8, mnmajor_desc(qa, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
+        // dQ_i = dS K_j into the dP columns (after dK read dS^T there: in issue order)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          umma_bf16(tmem + DP_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka, k), IDESC_DQ, k > 0 ? 1u : 0u);
+        umma_commit(&qdo_empty[st]);
+        umma_commit(dq_full);
+      }
+      umma_commit(dkv_full);
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax / dQ drain / dK dV
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // key row of S^T; query row of dQ
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    uint8_t* ds_row = sDS + r * 128;
+    for (int it = 0; it < niter; ++it) {
+      const int st = it & 1;
+      const int h = g * p.rep + it / nq, i = i0 + it % nq;
+      mbar_wait(&qdo_full[st], (it >> 1) & 1);  // lse / D of this query block are in shared memory
+      const float* sL = reinterpret_cast<const float*>(sQD + st * Cfg::BWD_QDO + 2 * TILE);
+      const float* sDv = sL + 128;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      const bool diag = p.causal && i == j;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sr[32], dr[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + S_COL + c * 32, sr);
+        tmem_ld_32x32b_x32(tmem + lane_off + DP_COL + c * 32, dr);
+        tmem_ld_wait();
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          float pp[2], dd[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = c * 32 + t + e;
+            float pv = ex2_approx(__uint_as_float(sr[t + e]) * p.scale_log2 - sL[q]);
+            if (diag && q < r) pv = 0.f;  // key r is after query q
+            pp[e] = pv;
+            dd[e] = pv * (__uint_as_float(dr[t + e]) - sDv[q]);
+          }
+          pk[t >> 1] = pack_bf16x2(pp[0], pp[1]);
+          dk[t >> 1] = pack_bf16x2(dd[0], dd[1]);
+        }
+        tmem_st_32x32b_x16(tmem + lane_off + S_COL + c * 16, pk);
+        tmem_st_32x32b_x16(tmem + lane_off + DP_COL + c * 16, dk);
+        // dS^T row r, queries [32c, 32c + 32): region c/2, 16-byte units (c%2)*4 .. +4, SW128
+        uint8_t* reg = ds_row + (c >> 1) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int unit = ((c & 1) * 4 + u) ^ (r & 7);
+          *reinterpret_cast<uint4*>(reg + unit * 16) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      // dQ_i drain: row r = query (i*128 + r) of head h
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128 + r) * (p.nh * HD) + h * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + DP_COL + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          red_add_v4(dst + c * 32 + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                     __uint_as_float(v[e + 3]));
+      }
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+    }
+    // ---------------------------------------------------------------- dK, dV of key block j
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const int pos = j * 128 + r;
+    __nv_bfloat16* row = p.dqkv + static_cast<long long>(row0 + pos) * p.ldq;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem + lane_off + DV_COL + c * 32, v);
+      tmem_ld_wait();
+      uint4* dv = reinterpret_cast<uint4*>(row + (p.nh + p.nkv + g) * HD + c * 32);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        dv[u] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * u]), __uint_as_float(v[8 * u + 1])),
+                           pack_bf16x2(__uint_as_float(v[8 * u + 2]), __uint_as_float(v[8 * u + 3])),
+                           pack_bf16x2(__uint_as_float(v[8 * u + 4]), __uint_as_float(v[8 * u + 5])),
+                           pack_bf16x2(__uint_as_float(v[8 * u + 6]), __uint_as_float(v[8 * u + 7])));
+    }
+    // dK: pairs (d, d + HD/2) for the RoPE backward, 32 columns of each half at a time
+    const float2* cs = p.rope ? p.rope + static_cast<long long>(pos) * (HD / 2) : nullptr;
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) {
+      uint32_t a[32], bb[32];
+      tmem_ld_32x32b_x32(tmem + lane_off + DK_COL + c * 32, a);
+      tmem_ld_32x32b_x32(tmem + lane_off + DK_COL + HD / 2 + c * 32, bb);
+      tmem_ld_wait();
+      float fa[32], fb[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float ga = __uint_as_float(a[e]) * p.scale, gb = __uint_as_float(bb[e]) * p.scale;
+        if (cs) {
+          const float2 t = cs[c * 32 + e];
+          fa[e] = ga * t.x + gb * t.y;
+          fb[e] = gb * t.x - ga * t.y;
+        } else {
+          fa[e] = ga;
+          fb[e] = gb;
+        }
+      }
+      uint4* ka = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + c * 32);
+      uint4* kb = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + HD / 2 + c * 32);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ka[u] = make_uint4(pack_bf16x2(fa[8 * u], fa[8 * u + 1]), pack_bf16x2(fa[8 * u + 2], fa[8 * u + 3]),
+                           pack_bf16x2(fa[8 * u + 4], fa[8 * u + 5]), pack_bf16x2(fa[8 * u + 6], fa[8 * u + 7]));
+        kb[u] = make_uint4(pack_bf16x2(fb[8 * u], fb[8 * u + 1]), pack_bf16x2(fb[8 * u + 2], fb[8 * u + 3]),
+                           pack_bf16x2(fb[8 * u + 4], fb[8 * u + 5]), pack_bf16x2(fb[8 * u + 6], fb[8 * u + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// dq = scale * dQ_acc with the RoPE backward, bf16 into dqkv's q columns. One thread per
+// (token, head, pair d < HD/2).
+template <int HD>
+__global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ldq,
+                                    const float2* __restrict__ rope, int T, int S, int nh, float scale) {
+  pdl_begin();
+  constexpr int HALF = HD / 2;
+  const long long n = static_cast<long long>(T) * nh * (HALF / 4);
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int d4 = static_cast<int>(idx % (HALF / 4)) * 4;
+    const long long th = idx / (HALF / 4);
+    const long long t = th / nh;
+    const int h = static_cast<int>(th % nh);
+    const float* src = dq_acc + t * nh * HD + h * HD;
+    const float4 a = *reinterpret_cast<const float4*>(src + d4);
+    const float4 c = *reinterpret_cast<const float4*>(src + HALF + d4);
+    float ga[4] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale};
+    float gb[4] = {c.x * scale, c.y * scale, c.z * scale, c.w * scale};
+    float oa[4], ob[4];
+    const float2* cs = rope ? rope + static_cast<long long>(t % S) * HALF + d4 : nullptr;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (cs) {
+        const float2 r = cs[e];
+        oa[e] = ga[e] * r.x + gb[e] * r.y;
+        ob[e] = gb[e] * r.x - ga[e] * r.y;
+      } else {
+        oa[e] = ga[e];
+        ob[e] = gb[e];
+      }
+    }
+    __nv_bfloat16* dst = dqkv + t * ldq + h * HD;
+    *reinterpret_cast<uint2*>(dst + d4) = make_uint2(pack_bf16x2(oa[0], oa[1]), pack_bf16x2(oa[2], oa[3]));
+    *reinterpret_cast<uint2*>(dst + HALF + d4) = make_uint2(pack_bf16x2(ob[0], ob[1]), pack_bf16x2(ob[2], ob[3]));
+  }
+}
+
+template <int HD>
+int fwd_impl(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S, int nh, int nkv,
+             float scale, bool causal, cudaStream_t s) {
+  using Cfg = AttnCfg<HD>;
+  FwdParams p{};
+  const long long W = static_cast<long long>(nh + 2 * nkv) * HD;
+  const long long T = static_cast<long long>(B) * S;
+  if (tma_desc_bf16_2d(&p.tqkv, qkv, T, W, W, 64, 128)) return PF_ERR_INVALID;
+  p.out = out;
+  p.ldo = ldo;
+  p.lse = lse;
+  p.B = B;
+  p.S = S;
+  p.nh = nh;
+  p.nkv = nkv;
+  p.rep = nh / nkv;
+  p.nqb = S / 128;
+  p.causal = causal ? 1 : 0;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  auto kern = flash_fwd_kernel<HD>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::FWD_SMEM) != cudaSuccess)
+      return PF_ERR_CUDA;
+    attr = true;
+  }
+  launch_k(kern, dim3(B * nh * p.nqb), dim3(kAttnThreads), Cfg::FWD_SMEM, s, p);
+  return status();
+}
+
+template <int HD>
+int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse,
+             float* D, float* dq_acc, __nv_bfloat16* dqkv, const float2* rope, int B, int S, int nh, int nkv,
+             float scale, bool causal, cudaStream_t s) {
+  using Cfg = AttnCfg<HD>;
+  const int T = B * S;
+  launch_k(flash_bwd_pre_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh / 8)), dim3(256), 0, s, out, dout, D,
+           dq_acc, T, S, nh);
+  int rc = status();
+  if (rc) return rc;
+  BwdParams p{};
+  const long long W = static_cast<long long>(nh + 2 * nkv) * HD;
+  if (tma_desc_bf16_2d(&p.tqkv, qkv, T, W, W, 64, 128)) return PF_ERR_INVALID;
+  if (tma_desc_bf16_2d(&p.tdo, dout, T, static_cast<long long>(nh) * HD, static_cast<long long>(nh) * HD, 64, 128))
+    return PF_ERR_INVALID;
+  p.lse = lse;
+  p.D = D;
+  p.dq_acc = dq_acc;
+  p.dqkv = dqkv;
+  p.ldq = W;
+  p.rope = rope;
+  p.B = B;
+  p.S = S;
+  p.nh = nh;
+  p.nkv = nkv;
+  p.rep = nh / nkv;
+  p.nqb = S / 128;
+  p.causal = causal ? 1 : 0;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.scale = scale;
+  auto kern = flash_bwd_kernel<HD>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BWD_SMEM) != cudaSuccess)
+      return PF_ERR_CUDA;
+    attr = true;
+  }
+  launch_k(kern, dim3(B * nkv * p.nqb), dim3(kAttnThreads), Cfg::BWD_SMEM, s, p);
+  if ((rc = status())) return rc;
+  launch_k(flash_bwd_dq_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh * HD / 8 / 256 + 1)), dim3(256), 0, s,
+           dq_acc, dqkv, W, rope, T, S, nh, scale);
+  return status();
+}
+
+bool shape_ok(int B, int S, int nh, int nkv, int hd) {
+  return B > 0 && S > 0 && S % 128 == 0 && nkv > 0 && nh % nkv == 0 && (hd == 64 || hd == 128);
+}
+
+}  // namespace
+
+int launch_flash_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S,
+                          int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s) {
+  if (!shape_ok(B, S, nh, nkv, hd) || ldo % 8) return PF_ERR_INVALID;
+  return hd == 128 ? fwd_impl<128>(qkv, out, ldo, lse, B, S, nh, nkv, scale, causal, s)
+                   : fwd_impl<64>(qkv, out, ldo, lse, B, S, nh, nkv, scale, causal, s);
+}
+
+int launch_flash_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                          const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, const float2* rope, int B,
+                          int S, int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s) {
+  if (!shape_ok(B, S, nh, nkv, hd)) return PF_ERR_INVALID;
+  return hd == 128 ? bwd_impl<128>(qkv, out, dout, lse, D, dq_acc, dqkv, rope, B, S, nh, nkv, scale, causal, s)
+                   : bwd_impl<64>(qkv, out, dout, lse, D, dq_acc, dqkv, rope, B, S, nh, nkv, scale, causal, s);
+}
+
+}  // namespace pf

@@ -700,57 +700,6 @@ __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* _
   store8(p + j + half, ob);
 }
 
-// Attention gradients (any [B,H,S,D] strides; K/V gradients of `rep` expanded heads
-// are summed onto their KV head) -> inverse RoPE -> packed dqkv [T, (nh+2nkv) hd].
-__global__ void rope_bwd_pack_kernel(const AttnGradView g, __nv_bfloat16* __restrict__ dqkv,
-                                     const float2* __restrict__ cs, int seq, int nh, int nkv, int hd) {
-  pdl_begin();
-  const int half = hd / 2, chunks = half / 8;
-  const int heads = nh + 2 * nkv;
-  const int t = blockIdx.y;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= heads * chunks) return;
-  const int head = idx / chunks, j = (idx - head * chunks) * 8;
-  const int bi = t / seq, si = t - bi * seq;
-  float a[8], b[8];
-  if (head < nh) {
-    const __nv_bfloat16* src = g.dq + bi * g.q_b + si * g.q_t + head * g.q_h;
-    load8(src + j, a);
-    load8(src + j + half, b);
-  } else {
-    const bool is_k = head < nh + nkv;
-    const int kv = is_k ? head - nh : head - nh - nkv;
-    const __nv_bfloat16* base = is_k ? g.dk : g.dv;
-    const long long sb = is_k ? g.k_b : g.v_b, st = is_k ? g.k_t : g.v_t, sh = is_k ? g.k_h : g.v_h;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
-    for (int r = 0; r < g.rep; ++r) {
-      const __nv_bfloat16* src = base + bi * sb + si * st + static_cast<long long>(kv * g.rep + r) * sh;
-      float x[8], y[8];
-      load8(src + j, x);
-      load8(src + j + half, y);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        a[i] += x[i];
-        b[i] += y[i];
-      }
-    }
-  }
-  if (head < nh + nkv) {  // inverse rotation (transpose of the forward rotation)
-    const float2* c = cs + static_cast<long long>(t % seq) * half + j;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float2 cc = c[i];
-      const float x = a[i], y = b[i];
-      a[i] = x * cc.x + y * cc.y;
-      b[i] = y * cc.x - x * cc.y;
-    }
-  }
-  __nv_bfloat16* d = dqkv + static_cast<long long>(t) * heads * hd + static_cast<long long>(head) * hd;
-  store8(d + j, a);
-  store8(d + j + half, b);
-}
-
 __device__ __forceinline__ float sigmoidf_(float x) { return sigmoid_fast(x); }
 
 // gate|up rows are interleaved in 128-blocks (kGuBlock): gu column of gate j is
@@ -1090,14 +1039,6 @@ int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh
   return status();
 }
 
-int launch_rope_bwd_pack(const AttnGradView& g, __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh,
-                         int nkv, int hd, cudaStream_t s) {
-  if (hd % 16 || g.rep < 1) return PF_ERR_INVALID;
-  const int work = (nh + 2 * nkv) * (hd / 16);
-  const int threads = std::min(kBlock, (work + 31) / 32 * 32);
-  launch_k(rope_bwd_pack_kernel, dim3(dim3((work + threads - 1) / threads, T)), dim3(threads), 0, s, g, dqkv, cs, seq, nh, nkv, hd);
-  return status();
-}
 
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s) {
   if (ffn % 128) return PF_ERR_INVALID;

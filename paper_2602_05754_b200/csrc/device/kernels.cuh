@@ -112,15 +112,16 @@ int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bflo
 int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const float* rstd, const __nv_bfloat16* dy,
                        const __nv_bfloat16* residual, __nv_bfloat16* dx, float* dg, int T, int h, cudaStream_t s);
 int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh, int nkv, int hd, cudaStream_t s);
-// attention input gradients as strided [B, H, S, D] views (element strides)
-struct AttnGradView {
-  const __nv_bfloat16 *dq, *dk, *dv;
-  long long q_b, q_t, q_h, k_b, k_t, k_h, v_b, v_t, v_h;
-  int rep;  // dk/dv carry nkv * rep heads; each group of rep is summed (GQA with expanded K/V)
-};
-// dq, dk, dv -> rotated back (inverse RoPE on q, k) and packed into dqkv [T, (nh+2nkv)hd]
-int launch_rope_bwd_pack(const AttnGradView& g, __nv_bfloat16* dqkv, const float2* cs, int T, int seq, int nh,
-                         int nkv, int hd, cudaStream_t s);
+// K7 attention (flash_attn.cu): tcgen05 flash attention over the packed qkv [B*S, (nh + 2 nkv) hd]
+// (after RoPE), S % 128 == 0, hd in {64, 128}, native GQA. Forward: out [B*S, nh*hd] (row stride
+// ldo), lse [B, nh, S] (log2 domain). Backward: dout [B*S, nh*hd] contiguous; D [B, nh, S] and
+// dq_acc [B*S, nh*hd] fp32 are scratch; dq|dk|dv are written packed into dqkv (may be qkv itself),
+// with the RoPE backward on dq and dk when rope ((cos, sin) [S][hd/2]) is not null.
+int launch_flash_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S,
+                          int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s);
+int launch_flash_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
+                          const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, const float2* rope, int B,
+                          int S, int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s);
 int launch_swiglu_fwd(const __nv_bfloat16* gu, __nv_bfloat16* a, int T, int ffn, cudaStream_t s);
 int launch_swiglu_bwd(const __nv_bfloat16* gu, const __nv_bfloat16* da, __nv_bfloat16* dgu, int T, int ffn,
                       cudaStream_t s);

@@ -331,7 +331,8 @@ LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots,
       L.a = abf(T * cfg.ffn);
       L.rstd1 = af32(T);
       L.rstd2 = af32(T);
-      L.attn = attn_state_new();
+      L.ao = abf(T * cfg.attn_dim());
+      L.lse = af32(static_cast<long long>(cfg.micro_batch) * cfg.n_heads * cfg.seq);
       L.dy = abf(T * h);
       L.dx2 = abf(T * h);
     }
@@ -345,16 +346,14 @@ LlamaStage::LlamaStage(const ModelConfig& cfg, const StageSpec& spec, int slots,
   d_a_ = abf(T * cfg.ffn);
   d_h_ = abf(T * h);
   d_attn_ = abf(T * cfg.attn_dim());
+  attn_D_ = af32(static_cast<long long>(cfg.micro_batch) * cfg.n_heads * cfg.seq);
+  dq_acc_ = af32(T * cfg.attn_dim());
   d_y_ = abf(T * h);
   d_tmp_ = abf(T * h);
   if (cudaDeviceSynchronize() != cudaSuccess) throw std::runtime_error("stage: initialisation kernels failed");
 }
 
-LlamaStage::~LlamaStage() {
-  cudaSetDevice(device_);
-  for (auto& sl : slots_)
-    for (auto& L : sl.layers) attn_state_free(L.attn);
-}
+LlamaStage::~LlamaStage() { cudaSetDevice(device_); }
 
 Stage::~Stage() {
   cudaSetDevice(device_);
@@ -395,12 +394,10 @@ int LlamaStage::forward(int slot, int microbatch, const int* tokens, const int* 
     PF_TRY(launch_rmsnorm_fwd(L.x, weights_ + P.g1.offset, L.h1, L.rstd1, T, h, cfg_.norm_eps, s));
     PF_TRY(gemm_fwd_rope(L.h1, h, weights_ + P.wqkv.offset, h, L.qkv, rope_, T, cfg_.seq, cfg_.n_heads,
                          cfg_.n_kv_heads, cfg_.head_dim, h, s));
-    void* ao = nullptr;
-    long long ald = 0;
-    PF_TRY(attn_fwd(L.attn, L.qkv, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, scale,
-                    &ao, &ald, s));
-    L.attn_out = static_cast<const __nv_bfloat16*>(ao);
-    L.attn_ld = ald;
+    PF_TRY(launch_flash_attn_fwd(L.qkv, L.ao, cfg_.attn_dim(), L.lse, cfg_.micro_batch, cfg_.seq, cfg_.n_heads,
+                                 cfg_.n_kv_heads, cfg_.head_dim, scale, true, s));
+    L.attn_out = L.ao;
+    L.attn_ld = cfg_.attn_dim();
     PF_TRY(gemm_fwd_resid(L.attn_out, L.attn_ld, weights_ + P.wo.offset, cfg_.attn_dim(), L.x2, L.x, h, T, h,
                           cfg_.attn_dim(), s));
     PF_TRY(launch_rmsnorm_fwd(L.x2, weights_ + P.g2.offset, L.h2, L.rstd2, T, h, cfg_.norm_eps, s));
@@ -477,15 +474,11 @@ int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_wor
     // attention
     PF_TRY(gemm_dx(dx2, h, weights_ + P.wo.offset, cfg_.attn_dim(), d_attn_, cfg_.attn_dim(), T, cfg_.attn_dim(), h,
                    EPI_STORE_BF16, s));
-    AttnGrads ag{};
-    PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, cfg_.micro_batch, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
-                    1.0f / std::sqrt(static_cast<float>(cfg_.head_dim)), &ag, s));
-    {
-      AttnGradView gv{static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
-                      static_cast<const __nv_bfloat16*>(ag.dv), ag.q_b, ag.q_t, ag.q_h, ag.k_b, ag.k_t, ag.k_h,
-                      ag.v_b, ag.v_t, ag.v_h, ag.rep};
-      PF_TRY(launch_rope_bwd_pack(gv, dqkv, rope_, T, cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim, s));
-    }
+    // dq|dk|dv with the RoPE backward, packed over qkv (the key block's owner writes dk / dv in
+    // place once it no longer reads k / v; dq follows from the fp32 accumulator)
+    PF_TRY(launch_flash_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, attn_D_, dq_acc_, dqkv, rope_, cfg_.micro_batch,
+                                 cfg_.seq, cfg_.n_heads, cfg_.n_kv_heads, cfg_.head_dim,
+                                 1.0f / std::sqrt(static_cast<float>(cfg_.head_dim)), true, s));
     PF_TRY(gemm_dx(dqkv, cfg_.qkv_dim(), weights_ + P.wqkv.offset, h, d_h_, h, T, h, cfg_.qkv_dim(),
                    EPI_STORE_BF16, s));
     __nv_bfloat16* out;
@@ -493,7 +486,6 @@ int LlamaStage::backward(int slot, const int* tokens, const uint64_t* frozen_wor
     else out = spec_.first ? d_tmp_ : dx_out;
     if (!out) return PF_ERR_INVALID;
     PF_TRY(launch_rmsnorm_bwd(L.x, weights_ + P.g1.offset, L.rstd1, d_h_, dx2, out, grad_ + P.g1.offset, T, h, s));
-    attn_release_keep_out(L.attn);
     dcur = out;
   }
   if (spec_.first) PF_TRY(launch_embedding_bwd(tokens, dcur, grad_ + emb_.offset, T, h, s));
@@ -517,9 +509,7 @@ int LlamaStage::weight_grads(Slot& sl, int stamp, cudaStream_t s) {
     items.push_back(dw_item(P.wo, L.dx2, h, L.attn_out, L.attn_ld, T));
     items.push_back(dw_item(P.wqkv, L.qkv, cfg_.qkv_dim(), L.h1, h, T));
   }
-  PF_TRY(run_dw(items, stamp, s));
-  for (auto& L : sl.layers) attn_release(L.attn);
-  return PF_OK;
+  return run_dw(items, stamp, s);
 }
 
 int LlamaStage::backward_weight(int slot, const uint64_t* frozen_words, int stamp, cudaStream_t s) {

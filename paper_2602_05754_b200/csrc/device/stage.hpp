@@ -19,7 +19,6 @@
 #include <memory>
 #include <vector>
 
-#include "attention.hpp"
 #include "kernels.cuh"
 #include "pf_device_internal.hpp"
 
@@ -73,7 +72,8 @@ struct SavedLayer {  // per layer per microbatch slot
   __nv_bfloat16 *x = nullptr, *h1 = nullptr, *qkv = nullptr, *x2 = nullptr, *h2 = nullptr, *gu = nullptr,
                 *a = nullptr;
   float *rstd1 = nullptr, *rstd2 = nullptr;
-  AttnState* attn = nullptr;
+  __nv_bfloat16* ao = nullptr;  // attention output [T, nh*hd] (kept for dWo)
+  float* lse = nullptr;         // attention log-sum-exp [B, nh, S] (log2 domain)
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
   // the layer's output gradient and post-attention residual gradient, kept from B to
@@ -234,6 +234,8 @@ class LlamaStage final : public Stage {
   std::vector<Slot> slots_;
   // backward workspace
   __nv_bfloat16 *d_a_ = nullptr, *d_h_ = nullptr, *d_attn_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr;
+  float* attn_D_ = nullptr;   // attention backward: rowsum(dO * O) [B, nh, S]
+  float* dq_acc_ = nullptr;   // attention backward: fp32 dQ accumulator [T, nh*hd]
 };
 
 // The stage of `cfg.family` (0 LLaMA decoder, 1 ViT encoder).

@@ -43,10 +43,9 @@ struct VitSavedLayer {
   __nv_bfloat16 *x = nullptr, *h1 = nullptr, *qkv = nullptr, *x2 = nullptr, *h2 = nullptr, *pre = nullptr,
                 *act = nullptr;
   float *mu1 = nullptr, *r1 = nullptr, *mu2 = nullptr, *r2 = nullptr;
-  AttnState* attn = nullptr;
   const __nv_bfloat16* attn_out = nullptr;
   long long attn_ld = 0;
-  __nv_bfloat16* ao = nullptr;  // short-sequence attention output [T, h] (vit_attention.cu)
+  __nv_bfloat16* ao = nullptr;  // attention output [T, h]
   float* lse = nullptr;         // and its row log-sum-exp [B][nh][S]
   __nv_bfloat16 *dy = nullptr, *dx2 = nullptr;  // kept from B to W
   const __nv_bfloat16* dy_w = nullptr;          // the output gradient W reads (dy or the incoming buffer)
@@ -74,10 +73,11 @@ class VitStage final : public Stage {
     S_ = cfg.seq;
     np_ = S_ - 1;
     T_ = cfg.tokens();
-    // short sequences (ViT-L/32: 50 tokens) use the per-(image, head) kernel; PF_VIT_ATTN=cudnn
-    // (or S > 64, head_dim != 64) takes the generic fused attention
-    const char* ae = std::getenv("PF_VIT_ATTN");
-    own_attn_ = S_ <= 64 && cfg.head_dim == 64 && !(ae && std::string(ae) == "cudnn");
+    // short sequences (ViT-L/32: 50 tokens) use the per-(image, head) kernel (vit_attention.cu);
+    // sequences of whole 128-token blocks the bidirectional tcgen05 flash attention (flash_attn.cu)
+    own_attn_ = S_ <= 64 && cfg.head_dim == 64;
+    if (!own_attn_ && (S_ % 128 != 0 || (cfg.head_dim != 64 && cfg.head_dim != 128)))
+      throw std::invalid_argument("vit stage: attention needs seq <= 64 with head_dim 64, or seq % 128 == 0");
     Mh_ = (B_ + 127) / 128 * 128;
     const int nl = spec.layer_end - spec.layer_begin;
     layers_.resize(static_cast<std::size_t>(nl));
@@ -130,10 +130,6 @@ class VitStage final : public Stage {
       fill(lnfb_, 0.f);
       fill(headb_, 0.f);
     }
-    // RoPE-free attention: the pack kernel runs with an identity rotation table
-    std::vector<float2> ident(static_cast<std::size_t>(S_) * (cfg.head_dim / 2), make_float2(1.f, 0.f));
-    ident_ = static_cast<float2*>(alloc(ident.size() * sizeof(float2)));
-    cudaMemcpy(ident_, ident.data(), ident.size() * sizeof(float2), cudaMemcpyHostToDevice);
 
     const long long T = T_;
     slots_.resize(static_cast<std::size_t>(slots));
@@ -151,11 +147,8 @@ class VitStage final : public Stage {
         L.r1 = alloc_f32(T);
         L.mu2 = alloc_f32(T);
         L.r2 = alloc_f32(T);
-        L.attn = attn_state_new();
-        if (own_attn_) {
-          L.ao = alloc_bf16(T * h);
-          L.lse = alloc_f32(static_cast<long long>(B_) * cfg.n_heads * S_);
-        }
+        L.ao = alloc_bf16(T * h);
+        L.lse = alloc_f32(static_cast<long long>(B_) * cfg.n_heads * S_);
         L.dy = alloc_bf16(T * h);
         L.dx2 = alloc_bf16(T * h);
       }
@@ -176,6 +169,10 @@ class VitStage final : public Stage {
     d_act_ = alloc_bf16(T * cfg.ffn);
     d_h_ = alloc_bf16(T * h);
     d_attn_ = alloc_bf16(T * h);
+    if (!own_attn_) {
+      attn_D_ = alloc_f32(static_cast<long long>(B_) * cfg.n_heads * S_);
+      dq_acc_ = alloc_f32(T * h);
+    }
     d_y_ = alloc_bf16(T * h);
     d_tmp_ = alloc_bf16(T * h);
     if (spec.last) {
@@ -185,11 +182,7 @@ class VitStage final : public Stage {
     if (cudaDeviceSynchronize() != cudaSuccess) throw std::runtime_error("vit stage: initialisation failed");
   }
 
-  ~VitStage() override {
-    cudaSetDevice(device_);
-    for (auto& sl : slots_)
-      for (auto& L : sl.layers) attn_state_free(L.attn);
-  }
+  ~VitStage() override { cudaSetDevice(device_); }
 
   const __nv_bfloat16* output(int slot) const override { return slots_[static_cast<std::size_t>(slot)].x_out; }
 
@@ -220,11 +213,10 @@ class VitStage final : public Stage {
         L.attn_out = L.ao;
         L.attn_ld = h;
       } else {
-        void* ao = nullptr;
-        long long ald = 0;
-        PF_TRY(attn_fwd(L.attn, L.qkv, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ao, &ald, s, false));
-        L.attn_out = static_cast<const __nv_bfloat16*>(ao);
-        L.attn_ld = ald;
+        PF_TRY(launch_flash_attn_fwd(L.qkv, L.ao, h, L.lse, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale,
+                                     false, s));
+        L.attn_out = L.ao;
+        L.attn_ld = h;
       }
       PF_TRY(gemm_fwd_resid_bias(L.attn_out, L.attn_ld, w(P.wo), h, L.x2, L.x, h, w(P.bo), T_, h, h, s));
       PF_TRY(launch_layernorm_fwd(L.x2, w(P.ln2g), w(P.ln2b), L.h2, L.mu2, L.r2, T_, h, cfg_.norm_eps, s));
@@ -299,13 +291,9 @@ class VitStage final : public Stage {
       if (own_attn_) {  // dq|dk|dv straight into the packed dqkv (over qkv), bqkv's gradient alongside
         PF_TRY(launch_vit_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, dqkv, g(P.bqkv), B_, S_, cfg_.n_heads,
                                    cfg_.head_dim, scale, s));
-      } else {
-        AttnGrads ag{};
-        PF_TRY(attn_bwd(L.attn, L.qkv, d_attn_, B_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, &ag, s));
-        AttnGradView gv{static_cast<const __nv_bfloat16*>(ag.dq), static_cast<const __nv_bfloat16*>(ag.dk),
-                        static_cast<const __nv_bfloat16*>(ag.dv), ag.q_b, ag.q_t, ag.q_h, ag.k_b, ag.k_t, ag.k_h,
-                        ag.v_b, ag.v_t, ag.v_h, ag.rep};
-        PF_TRY(launch_rope_bwd_pack(gv, dqkv, ident_, T_, S_, cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, s));
+      } else {  // no RoPE in the ViT: dq|dk|dv packed over qkv as they are
+        PF_TRY(launch_flash_attn_bwd(L.qkv, L.ao, d_attn_, L.lse, attn_D_, dq_acc_, dqkv, nullptr, B_, S_,
+                                     cfg_.n_heads, cfg_.n_heads, cfg_.head_dim, scale, false, s));
       }
       if (!own_attn_) PF_TRY(launch_bias_grad(dqkv, 3LL * h, g(P.bqkv), T_, 3 * h, s));
       PF_TRY(gemm_dx(dqkv, 3LL * h, w(P.wqkv), h, d_h_, h, T_, h, 3 * h, EPI_STORE_BF16, s));
@@ -318,7 +306,6 @@ class VitStage final : public Stage {
       float* b2_below = li > 0 ? g(layers_[static_cast<std::size_t>(li - 1)].b2) : nullptr;
       PF_TRY(launch_layernorm_bwd(L.x, w(P.ln1g), L.mu1, L.r1, d_h_, dx2, out, g(P.ln1g), g(P.ln1b), b2_below, T_, h,
                                   s));
-      attn_release_keep_out(L.attn);
       dcur = out;
     }
     if (spec_.first) {
@@ -358,7 +345,6 @@ class VitStage final : public Stage {
     }
     if (spec_.first) items.push_back(dw_item(patch_w_, sl.emb, h, sl.patches, cfg_.patch_dim(), B_ * np_));
     PF_TRY(run_dw(items, stamp, s));
-    for (auto& L : sl.layers) attn_release(L.attn);
     return PF_OK;
   }
 
@@ -367,7 +353,8 @@ class VitStage final : public Stage {
   bool own_attn_ = false;
   std::vector<VitLayerParams> layers_;
   ParamSlice patch_w_, patch_b_, cls_, pos_, head_, headb_, lnfg_, lnfb_;
-  float2* ident_ = nullptr;
+  float* attn_D_ = nullptr;  // flash attention backward scratch (seq % 128 == 0 shapes)
+  float* dq_acc_ = nullptr;
   std::vector<VitSlot> slots_;
   __nv_bfloat16 *d_act_ = nullptr, *d_h_ = nullptr, *d_attn_ = nullptr, *d_y_ = nullptr, *d_tmp_ = nullptr,
                 *d_hc_ = nullptr,
