@@ -89,6 +89,9 @@ int pf_flash_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int 
                       int causal, void* stream);
 int pf_flash_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B, int S,
                       int nh, int nkv, int hd, float scale, int causal, float rope_theta, void* stream);
+/* Development aid: with PF_ATTN_PROF=1 in the environment the attention kernels accumulate the first
+ * CTA's per-role cycle counts (waits, compute) into 32 counters; this copies them out and resets. */
+int pf_flash_attn_prof(unsigned long long* out32);
 int pf_vit_attn_fwd(const void* qkv, void* out, float* lse, int B, int S, int nh, int hd, float scale, void* stream);
 int pf_vit_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, float* dbias,
                     int B, int S, int nh, int hd, float scale, void* stream);

@@ -52,6 +52,7 @@ DEVICE_SIGNATURES = {
     "pf_flash_attn_fwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_f, c_int, c_vp], c_int),
     "pf_flash_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_f, c_int, c_f, c_vp],
                           c_int),
+    "pf_flash_attn_prof": ([c_vp], c_int),
     "pf_vit_attn_fwd": ([c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_vit_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_int, c_int, c_f, c_vp], c_int),
     "pf_layernorm_fwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_int, c_f, c_vp], c_int),

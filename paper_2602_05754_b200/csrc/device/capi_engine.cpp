@@ -230,6 +230,10 @@ int pf_flash_attn_fwd(const void* qkv, void* out, float* lse, int B, int seq, in
   });
 }
 
+int pf_flash_attn_prof(unsigned long long* out32) {
+  return guard([&] { return pf::flash_attn_prof_read(out32); });
+}
+
 int pf_flash_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv, int B, int seq,
                       int nh, int nkv, int hd, float scale, int causal, float rope_theta, void* stream) {
   return guard([&] {

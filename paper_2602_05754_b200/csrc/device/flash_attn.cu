@@ -39,6 +39,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernel_util.cuh"
 #include "kernels.cuh"
@@ -51,15 +52,27 @@ int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long lon
 
 namespace {
 
+// Optional cycle accounting of the first CTA's roles (PF_ATTN_PROF=1; tools/attn_bench.py --prof)
+__device__ unsigned long long g_attn_prof[32];
+struct ProfClock {
+  bool on;
+  __device__ __forceinline__ long long now() const { return on ? clock64() : 0; }
+  __device__ __forceinline__ void add(int slot, long long t0) const {
+    if (on) g_attn_prof[slot] += static_cast<unsigned long long>(clock64() - t0);
+  }
+};
+
 constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold: unnormalised P stays <= 2^8
-constexpr int kAttnThreads = 192;
+constexpr int kSoftWarps = 16;        // softmax warps: 4 per TMEM lane quarter, one 32-column slice each
+constexpr int kSoftThreads = 32 * kSoftWarps;
+constexpr int kAttnThreads = 64 + kSoftThreads;
 
 struct FwdParams {
   CUtensorMap tqkv;  // qkv [T, W], box {64, 128}
   __nv_bfloat16* out;
   long long ldo;
   float* lse;  // [B, nh, S]: m + log2(l) of the log2-scaled scores
-  int B, S, nh, nkv, rep, nqb, causal;
+  int B, S, nh, nkv, rep, nqb, causal, prof;
   float scale_log2;
 };
 
@@ -72,7 +85,7 @@ struct BwdParams {
   __nv_bfloat16* dqkv;
   long long ldq;  // row stride of qkv / dqkv (W)
   const float2* rope;  // (cos, sin) [S][hd/2] or null
-  int B, S, nh, nkv, rep, nqb, causal;
+  int B, S, nh, nkv, rep, nqb, causal, prof;
   float scale_log2, scale;
 };
 
@@ -80,24 +93,47 @@ template <int HD>
 struct AttnCfg {
   static constexpr int TILE = 128 * HD * 2;  // one 128-row tile, HD/64 regions of 16 KB
   static constexpr int FWD_STAGES = HD == 128 ? 4 : 6;
-  static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 256;
+  static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 4096 + 256;
   // bwd: K, V, two {Q, dO, lse, D} stages, dS^T (128 x 128 bf16)
   static constexpr int BWD_QDO = 2 * TILE + 1024;
   static constexpr int BWD_SMEM_NOPAD = 2 * TILE + 2 * BWD_QDO + 32768 + 256;
   static constexpr int BWD_SMEM = BWD_SMEM_NOPAD + 1024 <= 232448 ? BWD_SMEM_NOPAD + 1024 : BWD_SMEM_NOPAD;
 };
 
-// K-major SW128 operand of a 128-row tile: k-step kk (16 elements) of the hd dimension
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
-  return sdesc_sw128(base + static_cast<uint32_t>((kk >> 2) * 16384 + (kk & 3) * 32), 16, 1024);
+// SW128 operand descriptors of a 128-row tile. The MMA issuer builds one base descriptor per tile
+// and steps it by constants (the start-address field is the descriptor's low 14 bits, addr >> 4):
+// a per-MMA sdesc_sw128 was a ~150-cycle dependent chain on the single issuing thread, longer than
+// the 64-cycle 128 x 128 x 16 MMA itself (tools/probes/umma_probe.cu).
+//   K-major (rows = M/N, columns = K): k-step kk (16 elements) of the hd dimension
+//   MN-major (rows = K):               k-step kk (16 rows)
+__device__ __forceinline__ uint64_t kmajor_base(uint32_t addr) { return sdesc_sw128(addr, 16, 1024); }
+__device__ __forceinline__ uint64_t mnmajor_base(uint32_t addr) { return sdesc_sw128(addr, 16384, 1024); }
+__device__ __forceinline__ uint64_t kmajor_desc(uint64_t base, int kk) {
+  return base + static_cast<uint64_t>(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
 }
-// MN-major SW128 operand of a 128-row tile whose rows are the K dimension: k-step kk (16 rows)
-__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
-  return sdesc_sw128(base + static_cast<uint32_t>(kk * 2048), 16384, 1024);
-}
+__device__ __forceinline__ uint64_t mnmajor_desc(uint64_t base, int kk) { return base + static_cast<uint64_t>(kk * 128); }
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~static_cast<uintptr_t>(1023));
+}
+
+// TMEM load / store of N consecutive 32-bit columns of this warp's lane quarter (N = 16 or 32)
+template <int N>
+__device__ __forceinline__ void tld(uint32_t taddr, uint32_t* r) {
+  if constexpr (N == 32) tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+  else tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+}
+template <int N>
+__device__ __forceinline__ void tst(uint32_t taddr, const uint32_t* r) {
+  if constexpr (N == 32) tmem_st_32x32b_x32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(r));
+  else tmem_st_32x32b_x16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+}
+
+// exponentials of a softmax slice: 3 of every 8 on the FMA pipe (ex2_poly), the rest on the MUFU
+template <int I>
+__device__ __forceinline__ float ex2_mixed(float x) {
+  if constexpr ((I & 7) >= 5) return ex2_poly(x);
+  else return ex2_approx(x);
 }
 
 template <int HD>
@@ -108,12 +144,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
   constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false, false);
   constexpr uint32_t IDESC_O = idesc_bf16_f32(128, HD, false, true);
   constexpr uint32_t O_COL = 256;
+  constexpr int OC = HD / 4;  // O columns per softmax warp
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + TILE;
-  uint64_t* q_full = reinterpret_cast<uint64_t*>(sKV + ST * TILE);
+  float* red = reinterpret_cast<float*>(sKV + ST * TILE);  // [2][4 slices][128 rows] partial maxima, then sums
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(red + 2 * 4 * 128);
   uint64_t* kv_full = q_full + 1;
   uint64_t* kv_empty = kv_full + ST;
   uint64_t* s_full = kv_empty + ST;
@@ -121,7 +159,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
   uint64_t* o_bar = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 1);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
   const int nbh = p.B * p.nh;
   const int bh = blockIdx.x % nbh;
@@ -129,6 +167,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
   const int b = bh / p.nh, h = bh % p.nh, g = h / p.rep;
   const int nblk = p.causal ? qb + 1 : p.nqb;
   const int row0 = b * p.S;
+  const ProfClock pc{p.prof != 0 && blockIdx.x == 0};
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -138,7 +177,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 128);
+      mbar_init(&p_full[s], kSoftThreads);
     }
     mbar_init(o_bar, 1);
     fence_barrier_init();
@@ -152,7 +191,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = warp_uniform(*tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -162,7 +201,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
       for (int c = 0; c < HD / 64; ++c) tma_load_2d(sQ + c * 16384, &p.tqkv, q_full, h * HD + c * 64, row0 + qb * 128);
       for (int u = 0; u < 2 * nblk; ++u) {
         const int st = u % ST;
+        const long long t0 = pc.now();
         mbar_wait(&kv_empty[st], ((u / ST) & 1) ^ 1);
+        pc.add(6, t0);
         mbar_arrive_expect_tx(&kv_full[st], TILE);
         const int col = ((u & 1) ? (p.nh + p.nkv + g) : (p.nh + g)) * HD;
 #pragma unroll
@@ -172,160 +213,188 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
       pdl_trigger();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- MMA issuer
+    {
+      // ---------------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
+      const ProfClock pm{pc.on && lane == 0};
       mbar_wait(q_full, 0);
       tc_fence_after();
-      const uint32_t qa = smem_u32(sQ);
+      const uint64_t qa = kmajor_base(smem_u32(sQ));
+      const long long tm0 = pm.now();
       auto issue_s = [&](int j) {
         const int u = 2 * j, st = u % ST;
+        const long long t0 = pm.now();
         mbar_wait(&kv_full[st], (u / ST) & 1);
+        pm.add(1, t0);
         tc_fence_after();
-        const uint32_t kb = smem_u32(sKV + st * TILE);
+        const uint64_t kb = kmajor_base(smem_u32(sKV + st * TILE));
         const uint32_t d = tmem + static_cast<uint32_t>((j & 1) * 128);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) umma_bf16(d, kmajor_desc(qa, k), kmajor_desc(kb, k), IDESC_S, k > 0 ? 1u : 0u);
-        umma_commit(&kv_empty[st]);
-        umma_commit(&s_full[j & 1]);
+        for (int k = 0; k < HD / 16; ++k) umma_bf16_w(d, kmajor_desc(qa, k), kmajor_desc(kb, k), IDESC_S, k > 0 ? 1u : 0u);
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(&s_full[j & 1]);
       };
       issue_s(0);
       for (int j = 0; j < nblk; ++j) {
         if (j + 1 < nblk) issue_s(j + 1);
+        long long t0 = pm.now();
         mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        pm.add(0, t0);
         tc_fence_after();
         const int u = 2 * j + 1, st = u % ST;
+        t0 = pm.now();
         mbar_wait(&kv_full[st], (u / ST) & 1);
+        pm.add(1, t0);
         tc_fence_after();
-        const uint32_t vb = smem_u32(sKV + st * TILE);
+        const uint64_t vb = mnmajor_base(smem_u32(sKV + st * TILE));
         const uint32_t pa = tmem + static_cast<uint32_t>((j & 1) * 128);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16_ts(tmem + O_COL, pa + static_cast<uint32_t>(k * 8), mnmajor_desc(vb, k), IDESC_O,
+          umma_bf16_ts_w(tmem + O_COL, pa + static_cast<uint32_t>(k * 8), mnmajor_desc(vb, k), IDESC_O,
                        (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&kv_empty[st]);
-        umma_commit(o_bar);
+        umma_commit_w(&kv_empty[st]);
+        umma_commit_w(o_bar);
       }
+      pm.add(2, tm0);
     }
   } else {
     // ------------------------------------------------------------------ softmax
+    // 16 warps: 4 per TMEM lane quarter (query rows 32 q4 .. 32 q4 + 31), each owning a 32-column
+    // slice of the scores (and OC columns of O); row statistics are combined through shared memory
+    // with one named barrier per quarter and block.
     const int q4 = warp & 3;
+    const int slice = (warp - 2) >> 2;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t bar_id = 1 + q4;
     const int qpos = qb * 128 + r;
-    float m_used = 0.f, l = 0.f;
+    const float c = p.scale_log2;
+    const ProfClock sp{pc.on && threadIdx.x == 64};
+    const long long ts0 = sp.now();
+    float m_used = 0.f, l = 0.f;  // running max (scaled, log2) and this slice's partial row sum
     for (int j = 0; j < nblk; ++j) {
+      const long long t0 = sp.now();
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      sp.add(3, t0);
+      const long long tc0 = sp.now();
       tc_fence_after();
       const uint32_t sa = tmem + lane_off + static_cast<uint32_t>((j & 1) * 128);
-      uint32_t sr[128];
-      tmem_ld_32x32b_x32(sa, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld_32x32b_x32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld_32x32b_x32(sa + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-      tmem_ld_32x32b_x32(sa + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+      uint32_t sr[32];
+      tld<32>(sa + slice * 32, sr);
       tmem_ld_wait();
-      const bool diag = p.causal && j == qb;
-      float s[128];
-      float mx = -INFINITY;
+      float sv[32];
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        s[i] = __uint_as_float(sr[i]) * p.scale_log2;
-        if (diag && i > r) s[i] = -INFINITY;
-        mx = fmaxf(mx, s[i]);
+      for (int i = 0; i < 32; ++i) sv[i] = __uint_as_float(sr[i]);
+      if (p.causal && j == qb) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (slice * 32 + i > r) sv[i] = -INFINITY;
       }
+      float mx[4] = {sv[0], sv[1], sv[2], sv[3]};
+#pragma unroll
+      for (int i = 4; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], sv[i]);
+      float* rb = red + (j & 1) * 512;
+      rb[slice * 128 + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const long long tb0 = sp.now();
+      named_bar_sync(bar_id, 128);  // every slice's maximum is in; every S read of the quarter is done
+      sp.add(4, tb0);
+      const float mrow =
+          fmaxf(fmaxf(rb[r], rb[128 + r]), fmaxf(rb[256 + r], rb[384 + r])) * c;
       if (j == 0) {
-        m_used = mx;
-      } else if (mx > m_used + kRescaleLog2) {
+        m_used = mrow;
+      } else if (mrow > m_used + kRescaleLog2) {
         // O and l were accumulated against m_used: rescale once PV_{j-1} has landed in TMEM
         mbar_wait(o_bar, (j - 1) & 1);
         tc_fence_after();
-        const float a = ex2_approx(m_used - mx);
+        const float a = ex2_approx(m_used - mrow);
         l *= a;
+        uint32_t o[OC];
+        tld<OC>(tmem + lane_off + O_COL + slice * OC, o);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
-          tmem_st_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
-        }
-        tmem_st_wait();
-        m_used = mx;
+        for (int i = 0; i < OC; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+        tst<OC>(tmem + lane_off + O_COL + slice * OC, o);
+        m_used = mrow;
       }
-      uint32_t pk[64];
+      const float nm = -m_used;
+      uint32_t pk[16];
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = ex2_approx(s[2 * i] - m_used), p1 = ex2_approx(s[2 * i + 1] - m_used);
-        l += p0 + p1;
+      for (int i = 0; i < 16; ++i) {
+        float p0, p1;
+        // compile-time pattern of which exponentials go to the FMA pipe
+        switch (i & 3) {
+          case 0: p0 = ex2_mixed<0>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<1>(fmaf(sv[2 * i + 1], c, nm)); break;
+          case 1: p0 = ex2_mixed<2>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<3>(fmaf(sv[2 * i + 1], c, nm)); break;
+          case 2: p0 = ex2_mixed<4>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<5>(fmaf(sv[2 * i + 1], c, nm)); break;
+          default: p0 = ex2_mixed<6>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<7>(fmaf(sv[2 * i + 1], c, nm)); break;
+        }
+        ls[i & 3] += p0 + p1;
         pk[i] = pack_bf16x2(p0, p1);
       }
-      tmem_st_32x32b_x32(sa, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      tmem_st_32x32b_x32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      tst<16>(sa + slice * 16, pk);  // P over S (every S read of this quarter finished at the barrier)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[j & 1]);
+      sp.add(7, tc0);
     }
+    sp.add(5, ts0);
     // ---------------------------------------------------------------- epilogue
+    float* rs = red + (nblk & 1) * 512;  // the buffer block nblk - 1 did not use
+    rs[slice * 128 + r] = l;
+    named_bar_sync(bar_id, 128);
+    const float lrow = (rs[r] + rs[128 + r]) + (rs[256 + r] + rs[384 + r]);
     mbar_wait(o_bar, (nblk - 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + qpos) * p.ldo + h * HD;
+    const float inv = 1.f / lrow;
+    __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + qpos) * p.ldo + h * HD + slice * OC;
+    uint32_t o[OC];
+    tld<OC>(tmem + lane_off + O_COL + slice * OC, o);
+    tmem_ld_wait();
+    uint4* dst = reinterpret_cast<uint4*>(orow);
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tmem + lane_off + O_COL + c * 32, o);
-      tmem_ld_wait();
-      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 w;
-        w.x = pack_bf16x2(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-        w.y = pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-        w.z = pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-        w.w = pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-        dst[v] = w;
-      }
+    for (int v = 0; v < OC / 8; ++v) {
+      uint4 w;
+      w.x = pack_bf16x2(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+      w.y = pack_bf16x2(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+      w.z = pack_bf16x2(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+      w.w = pack_bf16x2(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+      dst[v] = w;
     }
-    p.lse[(static_cast<long long>(b) * p.nh + h) * p.S + qpos] = m_used + __log2f(l);
+    if (slice == 0) p.lse[(static_cast<long long>(b) * p.nh + h) * p.S + qpos] = m_used + __log2f(lrow);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// D[b, h, s] = sum_d dO * O (fp32 from the bf16 tensors); zero the dQ accumulator. One warp per
-// (token, head).
+// D[b, h, s] = sum_d dO * O (fp32 from the bf16 tensors); zero the dQ accumulator. HD/8 threads per
+// (token, head), 16-byte loads and stores.
 template <int HD>
 __global__ void flash_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
                                      float* __restrict__ D, float* __restrict__ dq_acc, int T, int S, int nh) {
   pdl_begin();
-  const long long nw = static_cast<long long>(T) * nh;
-  const int lane = threadIdx.x & 31;
-  for (long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; w < nw;
-       w += (static_cast<long long>(gridDim.x) * blockDim.x) >> 5) {
-    const long long t = w / nh;
-    const int h = static_cast<int>(w % nh);
-    const long long off = t * nh * HD + h * HD + lane * (HD / 32);
+  constexpr int TPR = HD / 8;  // threads per row
+  const long long n = static_cast<long long>(T) * nh * TPR;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long w = idx / TPR;  // (token, head)
+    const int part = static_cast<int>(idx % TPR);
+    const long long off = w * HD + part * 8;
+    float o[8], d[8];
+    load8(out + off, o);
+    load8(dout + off, d);
     float acc = 0.f;
-    if constexpr (HD == 128) {
-      const uint2 o = *reinterpret_cast<const uint2*>(out + off);
-      const uint2 d = *reinterpret_cast<const uint2*>(dout + off);
-      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
-      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&d);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float2 a = __bfloat1622float2(o2[i]), c = __bfloat1622float2(d2[i]);
-        acc = fmaf(a.x, c.x, fmaf(a.y, c.y, acc));
-      }
-      *reinterpret_cast<float4*>(dq_acc + off) = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(out + off));
-      const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
-      acc = fmaf(a.x, c.x, a.y * c.y);
-      *reinterpret_cast<float2*>(dq_acc + off) = make_float2(0.f, 0.f);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
+    for (int e = 0; e < 8; ++e) acc = fmaf(o[e], d[e], acc);
+    float4* z = reinterpret_cast<float4*>(dq_acc + off);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int o2 = TPR / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2, TPR);
+    if (part == 0) {
+      const long long t = w / nh;
+      const int h = static_cast<int>(w % nh);
       const int b = static_cast<int>(t / S), s = static_cast<int>(t % S);
       D[(static_cast<long long>(b) * nh + h) * S + s] = acc;
     }
@@ -339,10 +408,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
   constexpr uint32_t IDESC_SS = idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
   constexpr uint32_t IDESC_TS = idesc_bf16_f32(128, HD, false, true);    // dV, dK: A in TMEM, B MN-major
   constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, HD, true, true);     // dQ: A (dS) and B (K) MN-major
+  // TMEM: S^T | dP^T | dV | dK (| dQ when it fits: head_dim 64); at head_dim 128 dQ reuses the dP^T
+  // columns (its MMA follows dK's read of dS^T there in issue order)
+  constexpr bool DQ_OWN = HD == 64;
   constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + HD;
+  constexpr uint32_t DQ_COL = DQ_OWN ? 256 + 2 * HD : DP_COL;
+  constexpr int QC = HD / 4;  // dQ columns per softmax warp
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  if constexpr (Cfg::BWD_SMEM == Cfg::BWD_SMEM_NOPAD) {
+    if (smem != smem_raw) __trap();  // no room to realign: dynamic shared memory must start 1 KB aligned
+  }
   uint8_t* sK = smem;
   uint8_t* sV = smem + TILE;
   uint8_t* sQD = smem + 2 * TILE;  // 2 stages of {Q, dO, lse[128], D[128]}
@@ -357,16 +434,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
   uint64_t* dkv_full = dq_empty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_full + 1);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
   const int nbg = p.B * p.nkv;
   const int bg = blockIdx.x % nbg;
-  const int j = p.causal ? static_cast<int>(blockIdx.x) / nbg : static_cast<int>(blockIdx.x) / nbg;
+  const int j = static_cast<int>(blockIdx.x) / nbg;  // causal: key block 0 (the most query blocks) first
   const int b = bg / p.nkv, g = bg % p.nkv;
   const int row0 = b * p.S;
   const int i0 = p.causal ? j : 0;
   const int nq = p.nqb - i0;
   const int niter = p.rep * nq;
+  const ProfClock pc{p.prof != 0 && blockIdx.x == 0};
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -375,9 +453,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
       mbar_init(&qdo_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, kSoftThreads);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(dq_empty, kSoftThreads);
     mbar_init(dkv_full, 1);
     fence_barrier_init();
   }
@@ -393,7 +471,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = warp_uniform(*tmem_slot);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -422,147 +500,182 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
       pdl_trigger();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------------- MMA issuer
+    {
+      // ---------------------------------------------------------------- MMA issuer (whole warp, one elected lane issues)
+      const ProfClock pm{pc.on && lane == 0};
       mbar_wait(kv_full, 0);
       tc_fence_after();
-      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), dsa = smem_u32(sDS);
+      const uint64_t ka = kmajor_base(smem_u32(sK)), va = kmajor_base(smem_u32(sV));
+      const uint64_t ka_mn = mnmajor_base(smem_u32(sK)), dsa = mnmajor_base(smem_u32(sDS));
+      const long long tm0 = pm.now();
       for (int it = 0; it < niter; ++it) {
         const int st = it & 1;
+        long long t0 = pm.now();
         mbar_wait(&qdo_full[st], (it >> 1) & 1);
+        pm.add(8, t0);
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQD + st * Cfg::BWD_QDO);
-        const uint32_t da = qa + TILE;
+        const uint32_t qaddr = smem_u32(sQD + st * Cfg::BWD_QDO);
+        const uint64_t qa = kmajor_base(qaddr), da = kmajor_base(qaddr + TILE);
+        const uint64_t qa_mn = mnmajor_base(qaddr), da_mn = mnmajor_base(qaddr + TILE);
         // S^T = K_j Q_i^T (over P^T of the previous iteration: its dV MMA was issued before)
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + S_COL, kmajor_desc(ka, k), kmajor_desc(qa, k), IDESC_SS, k > 0 ? 1u : 0u);
-        if (it > 0) {  // dQ_{it-1} (in the dP columns) has been drained
+          umma_bf16_w(tmem + S_COL, kmajor_desc(ka, k), kmajor_desc(qa, k), IDESC_SS, k > 0 ? 1u : 0u);
+        if (!DQ_OWN && it > 0) {  // dQ_{it-1} (in the dP columns) has been drained
+          t0 = pm.now();
           mbar_wait(dq_empty, (it - 1) & 1);
+          pm.add(9, t0);
           tc_fence_after();
         }
         // dP^T = V_j dO_i^T
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + DP_COL, kmajor_desc(va, k), kmajor_desc(da, k), IDESC_SS, k > 0 ? 1u : 0u);
-        umma_commit(s_full);
+          umma_bf16_w(tmem + DP_COL, kmajor_desc(va, k), kmajor_desc(da, k), IDESC_SS, k > 0 ? 1u : 0u);
+        umma_commit_w(s_full);
+        t0 = pm.now();
         mbar_wait(p_full, it & 1);
+        pm.add(10, t0);
         tc_fence_after();
         // dV += P^T dO_i, dK += dS^T Q_i (A from TMEM, 16 queries per k-step)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16_ts(tmem + DV_COL, tmem + S_COL + k * 8, mnmajor_desc(da, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts_w(tmem + DV_COL, tmem + S_COL + k * 8, mnmajor_desc(da_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16_ts(tmem + DK_COL, tmem + DP_COL + k * 8, mnmajor_desc(qa, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
-        // dQ_i = dS K_j into the dP columns (after dK read dS^T there: in issue order)
+          umma_bf16_ts_w(tmem + DK_COL, tmem + DP_COL + k * 8, mnmajor_desc(qa_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
+        if (DQ_OWN && it > 0) {  // dQ_{it-1} has been drained from its own columns
+          mbar_wait(dq_empty, (it - 1) & 1);
+          tc_fence_after();
+        }
+        // dQ_i = dS K_j
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16(tmem + DP_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka, k), IDESC_DQ, k > 0 ? 1u : 0u);
-        umma_commit(&qdo_empty[st]);
-        umma_commit(dq_full);
+          umma_bf16_w(tmem + DQ_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka_mn, k), IDESC_DQ, k > 0 ? 1u : 0u);
+        umma_commit_w(&qdo_empty[st]);
+        umma_commit_w(dq_full);
       }
-      umma_commit(dkv_full);
+      pm.add(11, tm0);
+      umma_commit_w(dkv_full);
     }
   } else {
     // ------------------------------------------------------------------ softmax / dQ drain / dK dV
+    // 16 warps: 4 per TMEM lane quarter, each owning 32 query columns of S^T / dP^T, QC columns of
+    // the dQ drain and a share of the final dK / dV rows.
     const int q4 = warp & 3;
+    const int slice = (warp - 2) >> 2;
     const int r = q4 * 32 + lane;  // key row of S^T; query row of dQ
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    uint8_t* ds_row = sDS + r * 128;
+    const uint32_t bar_id = 1 + q4;
+    const float c = p.scale_log2;
+    uint8_t* ds_reg = sDS + (slice >> 1) * 16384 + r * 128;
+    const ProfClock sp{pc.on && threadIdx.x == 64};
+    const long long ts0 = sp.now();
     for (int it = 0; it < niter; ++it) {
       const int st = it & 1;
       const int h = g * p.rep + it / nq, i = i0 + it % nq;
       mbar_wait(&qdo_full[st], (it >> 1) & 1);  // lse / D of this query block are in shared memory
-      const float* sL = reinterpret_cast<const float*>(sQD + st * Cfg::BWD_QDO + 2 * TILE);
-      const float* sDv = sL + 128;
+      const float4* sL = reinterpret_cast<const float4*>(sQD + st * Cfg::BWD_QDO + 2 * TILE) + slice * 8;
+      const float4* sDv = sL + 32;
+      long long t0 = sp.now();
       mbar_wait(s_full, it & 1);
+      sp.add(12, t0);
+      const long long tc0 = sp.now();
       tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tld<32>(tmem + lane_off + S_COL + slice * 32, sr);
+      tld<32>(tmem + lane_off + DP_COL + slice * 32, dr);
+      tmem_ld_wait();
+      t0 = sp.now();
+      named_bar_sync(bar_id, 128);  // every S^T / dP^T read of the quarter is done before P / dS go over them
+      sp.add(17, t0);
       const bool diag = p.causal && i == j;
+      uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sr[32], dr[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + S_COL + c * 32, sr);
-        tmem_ld_32x32b_x32(tmem + lane_off + DP_COL + c * 32, dr);
-        tmem_ld_wait();
-        uint32_t pk[16], dk[16];
+      for (int v = 0; v < 8; ++v) {
+        const float4 L = sL[v], Dd = sDv[v];
+        const float lq[4] = {L.x, L.y, L.z, L.w}, dq[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
+        float pp[4], dd[4];
 #pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          float pp[2], dd[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int q = c * 32 + t + e;
-            float pv = ex2_approx(__uint_as_float(sr[t + e]) * p.scale_log2 - sL[q]);
-            if (diag && q < r) pv = 0.f;  // key r is after query q
-            pp[e] = pv;
-            dd[e] = pv * (__uint_as_float(dr[t + e]) - sDv[q]);
-          }
-          pk[t >> 1] = pack_bf16x2(pp[0], pp[1]);
-          dk[t >> 1] = pack_bf16x2(dd[0], dd[1]);
+        for (int e = 0; e < 4; ++e) {
+          const int t = 4 * v + e;
+          float pv = (e == 3) ? ex2_poly(fmaf(__uint_as_float(sr[t]), c, -lq[e]))
+                              : ex2_approx(fmaf(__uint_as_float(sr[t]), c, -lq[e]));
+          if (diag && slice * 32 + t < r) pv = 0.f;  // key r is after query (slice*32 + t)
+          pp[e] = pv;
+          dd[e] = pv * (__uint_as_float(dr[t]) - dq[e]);
         }
-        tmem_st_32x32b_x16(tmem + lane_off + S_COL + c * 16, pk);
-        tmem_st_32x32b_x16(tmem + lane_off + DP_COL + c * 16, dk);
-        // dS^T row r, queries [32c, 32c + 32): region c/2, 16-byte units (c%2)*4 .. +4, SW128
-        uint8_t* reg = ds_row + (c >> 1) * 16384;
+        pk[2 * v] = pack_bf16x2(pp[0], pp[1]);
+        pk[2 * v + 1] = pack_bf16x2(pp[2], pp[3]);
+        dk[2 * v] = pack_bf16x2(dd[0], dd[1]);
+        dk[2 * v + 1] = pack_bf16x2(dd[2], dd[3]);
+      }
+      tst<16>(tmem + lane_off + S_COL + slice * 16, pk);
+      tst<16>(tmem + lane_off + DP_COL + slice * 16, dk);
+      // dS^T row r, queries [32 slice, 32 slice + 32): region slice/2, 16-byte units (slice%2)*4 .. +4
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int unit = ((c & 1) * 4 + u) ^ (r & 7);
-          *reinterpret_cast<uint4*>(reg + unit * 16) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
-        }
+      for (int u = 0; u < 4; ++u) {
+        const int unit = ((slice & 1) * 4 + u) ^ (r & 7);
+        *reinterpret_cast<uint4*>(ds_reg + unit * 16) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
       }
       tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
-      // dQ_i drain: row r = query (i*128 + r) of head h
+      sp.add(14, tc0);
+      // dQ_i drain: row r = query (i*128 + r) of head h, this warp's QC columns
+      t0 = sp.now();
       mbar_wait(dq_full, it & 1);
+      sp.add(13, t0);
+      const long long td0 = sp.now();
       tc_fence_after();
-      float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128 + r) * (p.nh * HD) + h * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + DP_COL + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; e += 4)
-          red_add_v4(dst + c * 32 + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                     __uint_as_float(v[e + 3]));
-      }
+      uint32_t v[QC];
+      tld<QC>(tmem + lane_off + DQ_COL + slice * QC, v);
+      tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_empty);
+      float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128 + r) * (p.nh * HD) + h * HD + slice * QC;
+#pragma unroll
+      for (int e = 0; e < QC; e += 4)
+        red_add_v4(dst + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                   __uint_as_float(v[e + 3]));
+      sp.add(15, td0);
     }
+    sp.add(16, ts0);
     // ---------------------------------------------------------------- dK, dV of key block j
     mbar_wait(dkv_full, 0);
     tc_fence_after();
     const int pos = j * 128 + r;
     __nv_bfloat16* row = p.dqkv + static_cast<long long>(row0 + pos) * p.ldq;
+    if (slice >= 2) {  // dV: slices 2, 3 take HD/2 columns each
+      constexpr int VC = HD / 2;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tmem + lane_off + DV_COL + c * 32, v);
+      for (int c0 = 0; c0 < VC; c0 += 32) {
+        const int col = (slice - 2) * VC + c0;
+        uint32_t w[32];
+        tld<32>(tmem + lane_off + DV_COL + col, w);
+        tmem_ld_wait();
+        uint4* dv = reinterpret_cast<uint4*>(row + (p.nh + p.nkv + g) * HD + col);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          dv[u] = make_uint4(pack_bf16x2(__uint_as_float(w[8 * u]), __uint_as_float(w[8 * u + 1])),
+                             pack_bf16x2(__uint_as_float(w[8 * u + 2]), __uint_as_float(w[8 * u + 3])),
+                             pack_bf16x2(__uint_as_float(w[8 * u + 4]), __uint_as_float(w[8 * u + 5])),
+                             pack_bf16x2(__uint_as_float(w[8 * u + 6]), __uint_as_float(w[8 * u + 7])));
+      }
+    } else {  // dK: slices 0, 1 take HD/4 columns of the first half each and their RoPE partners
+      constexpr int KC = HD / 4;
+      const int col = slice * KC;
+      uint32_t a[KC], bb[KC];
+      tld<KC>(tmem + lane_off + DK_COL + col, a);
+      tld<KC>(tmem + lane_off + DK_COL + HD / 2 + col, bb);
       tmem_ld_wait();
-      uint4* dv = reinterpret_cast<uint4*>(row + (p.nh + p.nkv + g) * HD + c * 32);
+      const float2* cs = p.rope ? p.rope + static_cast<long long>(pos) * (HD / 2) + col : nullptr;
+      float fa[KC], fb[KC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        dv[u] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * u]), __uint_as_float(v[8 * u + 1])),
-                           pack_bf16x2(__uint_as_float(v[8 * u + 2]), __uint_as_float(v[8 * u + 3])),
-                           pack_bf16x2(__uint_as_float(v[8 * u + 4]), __uint_as_float(v[8 * u + 5])),
-                           pack_bf16x2(__uint_as_float(v[8 * u + 6]), __uint_as_float(v[8 * u + 7])));
-    }
-    // dK: pairs (d, d + HD/2) for the RoPE backward, 32 columns of each half at a time
-    const float2* cs = p.rope ? p.rope + static_cast<long long>(pos) * (HD / 2) : nullptr;
-#pragma unroll
-    for (int c = 0; c < HD / 64; ++c) {
-      uint32_t a[32], bb[32];
-      tmem_ld_32x32b_x32(tmem + lane_off + DK_COL + c * 32, a);
-      tmem_ld_32x32b_x32(tmem + lane_off + DK_COL + HD / 2 + c * 32, bb);
-      tmem_ld_wait();
-      float fa[32], fb[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
+      for (int e = 0; e < KC; ++e) {
         const float ga = __uint_as_float(a[e]) * p.scale, gb = __uint_as_float(bb[e]) * p.scale;
         if (cs) {
-          const float2 t = cs[c * 32 + e];
+          const float2 t = cs[e];
           fa[e] = ga * t.x + gb * t.y;
           fb[e] = gb * t.x - ga * t.y;
         } else {
@@ -570,10 +683,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
           fb[e] = gb;
         }
       }
-      uint4* ka = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + c * 32);
-      uint4* kb = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + HD / 2 + c * 32);
+      uint4* ka = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + col);
+      uint4* kb = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + HD / 2 + col);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < KC / 8; ++u) {
         ka[u] = make_uint4(pack_bf16x2(fa[8 * u], fa[8 * u + 1]), pack_bf16x2(fa[8 * u + 2], fa[8 * u + 3]),
                            pack_bf16x2(fa[8 * u + 4], fa[8 * u + 5]), pack_bf16x2(fa[8 * u + 6], fa[8 * u + 7]));
         kb[u] = make_uint4(pack_bf16x2(fb[8 * u], fb[8 * u + 1]), pack_bf16x2(fb[8 * u + 2], fb[8 * u + 3]),
@@ -624,6 +737,14 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloa
   }
 }
 
+int attn_prof_enabled() {
+  static const int on = [] {
+    const char* e = std::getenv("PF_ATTN_PROF");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return on;
+}
+
 template <int HD>
 int fwd_impl(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S, int nh, int nkv,
              float scale, bool causal, cudaStream_t s) {
@@ -642,6 +763,7 @@ int fwd_impl(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float*
   p.rep = nh / nkv;
   p.nqb = S / 128;
   p.causal = causal ? 1 : 0;
+  p.prof = attn_prof_enabled();
   p.scale_log2 = scale * 1.4426950408889634f;
   auto kern = flash_fwd_kernel<HD>;
   static bool attr = false;
@@ -660,8 +782,8 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
              float scale, bool causal, cudaStream_t s) {
   using Cfg = AttnCfg<HD>;
   const int T = B * S;
-  launch_k(flash_bwd_pre_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh / 8)), dim3(256), 0, s, out, dout, D,
-           dq_acc, T, S, nh);
+  launch_k(flash_bwd_pre_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh * (HD / 8) / 256 + 1)), dim3(256), 0, s,
+           out, dout, D, dq_acc, T, S, nh);
   int rc = status();
   if (rc) return rc;
   BwdParams p{};
@@ -682,6 +804,7 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
   p.rep = nh / nkv;
   p.nqb = S / 128;
   p.causal = causal ? 1 : 0;
+  p.prof = attn_prof_enabled();
   p.scale_log2 = scale * 1.4426950408889634f;
   p.scale = scale;
   auto kern = flash_bwd_kernel<HD>;
@@ -703,6 +826,13 @@ bool shape_ok(int B, int S, int nh, int nkv, int hd) {
 }
 
 }  // namespace
+
+// cycle accounting of the first CTA (PF_ATTN_PROF=1): copy out and reset
+int flash_attn_prof_read(unsigned long long* out32) {
+  if (cudaMemcpyFromSymbol(out32, g_attn_prof, 32 * sizeof(unsigned long long)) != cudaSuccess) return PF_ERR_CUDA;
+  static const unsigned long long zeros[32] = {};
+  return cudaMemcpyToSymbol(g_attn_prof, zeros, sizeof(zeros)) == cudaSuccess ? PF_OK : PF_ERR_CUDA;
+}
 
 int launch_flash_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S,
                           int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s) {

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));  // uniform: MMA issue stays on the uniform datapath
   const uint32_t lane = threadIdx.x & 31;
 
   __shared__ int prefix[MAXP + 1];
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
   const int ntiles = prefix[p.nprob];
 
   if (warp == 0) {
@@ -218,14 +218,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
       pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
       int stage = 0;
       uint32_t phase = 0;
       int abuf = 0;
       uint32_t aphase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int num_kb = p.prob[find_prob<MAXP>(prefix, p.nprob, t)].num_kb;
+        const int num_kb = static_cast<int>(warp_uniform(p.prob[find_prob<MAXP>(prefix, p.nprob, t)].num_kb));
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
@@ -242,15 +242,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tcgen05_kernel(const __grid_
                                         : sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_w(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          umma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[abuf]);
+        umma_commit_w(&tfull_bar[abuf]);
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }

@@ -194,7 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* ebar = tempty_bar + 2;  // EPI_DSWIGLU: epilogue buffer k loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2);
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));  // uniform: MMA issue stays on the uniform datapath
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -229,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync_all();  // barrier inits and TMEM allocation visible to both CTAs
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
   pdl_wait();  // setup above overlapped the preceding kernel; operands are its outputs
 
   if (warp == 0) {
@@ -266,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {  // whole warp: one elected lane issues (umma_*_w)
       // ---------------------------------------------------------- MMA issuer (leader CTA)
       int stage = 0;
       uint32_t phase = 0;
@@ -288,15 +288,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t adesc = sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb != sg.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair_w(d_tmem, adesc, bdesc, IDESC, (kb != sg.kb0 || k != 0) ? 1u : 0u);
           }
-          umma_commit_pair_multicast(&empty_bar[stage], 0x3);
+          umma_commit_pair_multicast_w(&empty_bar[stage], 0x3);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair_multicast(&tfull_bar[abuf], 0x3);
+        umma_commit_pair_multicast_w(&tfull_bar[abuf], 0x3);
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }

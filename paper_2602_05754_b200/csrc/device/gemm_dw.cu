@@ -100,7 +100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   __shared__ DwShared tab;
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));  // uniform: MMA issue stays on the uniform datapath
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -133,7 +133,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync_all();  // barrier inits, TMEM allocation and the table visible
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
   const int total = tab.prefix[p.nprob];
 
   if (warp == 0) {
@@ -175,15 +175,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       pdl_trigger();  // every load issued: the next kernel may launch (it waits for our completion)
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
-      // ---------------------------------------------------------- MMA issuer (leader CTA)
+    if (leader) {
+      // ---------------------------------------------------------- MMA issuer (leader CTA; whole warp, one elected lane issues)
       int stage = 0;
       uint32_t phase = 0;
       int abuf = 0;
       uint32_t aphase = 0;
       for (int t = cluster; t < total; t += nclusters) {
         const int pi = find_problem(tab.prefix, p.nprob, t);
-        const int num_kb = (p.prob[pi].K + BK - 1) / BK;
+        const int num_kb = static_cast<int>(warp_uniform((p.prob[pi].K + BK - 1) / BK));
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * 128);
@@ -197,15 +197,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // MN-major: advance 16 token rows = 2 swizzle atoms of 8 rows x 128 B
             const uint64_t adesc = sdesc_sw128(a_base + k * 2048, 8192, 1024);
             const uint64_t bdesc = sdesc_sw128(b_base + k * 2048, 8192, 1024);
-            umma_bf16_pair(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_pair_w(d_tmem, adesc, bdesc, IDESC, (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit_pair_multicast(&empty_bar[stage], 0x3);
+          umma_commit_pair_multicast_w(&empty_bar[stage], 0x3);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair_multicast(&tfull_bar[abuf], 0x3);
+        umma_commit_pair_multicast_w(&tfull_bar[abuf], 0x3);
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }

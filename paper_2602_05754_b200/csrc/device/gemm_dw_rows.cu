@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dw_rowpair_kernel(const __gr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   __shared__ int prefix[kMaxDwProblems + 1];
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));  // uniform: MMA issue stays on the uniform datapath
   const uint32_t lane = threadIdx.x & 31;
 
   pdl_wait();  // entry counts and operands come from the preceding kernels
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dw_rowpair_kernel(const __gr
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
   const int total = prefix[p.nprob];
 
   auto entry = [&](int t, int& pi) -> int2 {
@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dw_rowpair_kernel(const __gr
       pdl_trigger();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------------------ MMA issuer (whole warp, one elected lane issues)
       int stage = 0;
       uint32_t phase = 0;
       int abuf = 0;
@@ -169,8 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dw_rowpair_kernel(const __gr
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int pi;
         const int2 e = entry(t, pi);
-        const uint32_t idesc = e.y >= 0 ? IDESC_PAIR : IDESC_ONE;
-        const int num_kb = (p.prob[pi].K + BK - 1) / BK;
+        const uint32_t idesc = warp_uniform(e.y >= 0 ? IDESC_PAIR : IDESC_ONE);
+        const int num_kb = static_cast<int>(warp_uniform((p.prob[pi].K + BK - 1) / BK));
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * 256);
@@ -184,15 +184,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dw_rowpair_kernel(const __gr
             // MN-major: 16 token rows = 2 swizzle atoms of 8 rows x 128 B; 64-column chunks 8 KB apart
             const uint64_t adesc = sdesc_sw128(a_base + k * 2048, 8192, 1024);
             const uint64_t bdesc = sdesc_sw128(b_base + k * 2048, 8192, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16_w(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          umma_commit_w(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[abuf]);
+        umma_commit_w(&tfull_bar[abuf]);
         abuf ^= 1;
         if (abuf == 0) aphase ^= 1;
       }

@@ -119,6 +119,8 @@ int launch_rope_fwd(__nv_bfloat16* qkv, const float2* cs, int T, int seq, int nh
 // with the RoPE backward on dq and dk when rope ((cos, sin) [S][hd/2]) is not null.
 int launch_flash_attn_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float* lse, int B, int S,
                           int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s);
+// development aid (PF_ATTN_PROF=1): per-role cycle counters of the first CTA, copied out and reset
+int flash_attn_prof_read(unsigned long long* out32);
 int launch_flash_attn_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout,
                           const float* lse, float* D, float* dq_acc, __nv_bfloat16* dqkv, const float2* rope, int B,
                           int S, int nh, int nkv, int hd, float scale, bool causal, cudaStream_t s);

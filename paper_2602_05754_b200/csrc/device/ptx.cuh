@@ -193,6 +193,47 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
+// Warp-collective MMA issue: every lane of the warp executes these with the same (warp-uniform)
+// operands and one elected lane issues the instruction. Called from uniform control flow, the
+// descriptors stay in uniform registers; issuing from an `if (lane == 0)` branch instead makes the
+// compiler wrap every MMA in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop (~170 cycles per MMA on the
+// issuing thread, measured: tools/probes/umma_probe.cu).
+__device__ __forceinline__ void umma_bf16_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// the same value in every lane (lets the compiler treat it as warp-uniform)
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 // 1-D bulk copy global -> shared (bytes % 16 == 0, 16-byte aligned), completion on an mbarrier.
 __device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -210,6 +251,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA / integer pipes instead of the MUFU (the softmax kernels run part of their
+// exponentials here so the two pipes share the load, FA4-style): x = n + f with n = round(x) from
+// the 1.5 * 2^23 magic-number addition, 2^f on [-1/2, 1/2] by a degree-3 polynomial (max relative
+// error 2.2e-4; the result feeds bf16 operands, whose half-ulp is 2e-3), n added to the exponent
+// field. x is clamped to >= -125 (the exponent field stays normal: -inf -> 2^-125).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float j = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(j, 12582912.f));
+  float p = fmaf(0.05286731571f, f, 0.24215213954f);
+  p = fmaf(p, f, 0.69358682632f);
+  p = fmaf(p, f, 0.99996274710f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
 // Shared-memory matrix descriptor (sm_100 "version 1"), SWIZZLE_128B layout.
@@ -293,6 +349,31 @@ __device__ __forceinline__ void umma_commit_pair_multicast(uint64_t* bar, uint16
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// Warp-collective forms of the CTA-pair MMA and commit (see umma_bf16_w): every lane executes them
+// with the same operands, one elected lane issues.
+__device__ __forceinline__ void umma_bf16_pair_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_multicast_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
       "h"(mask)
       : "memory");
 }
