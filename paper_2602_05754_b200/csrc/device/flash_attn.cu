@@ -49,6 +49,8 @@ namespace pf {
 
 int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
                      int box_rows);
+int tma_desc_f32_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                    int box_rows);
 
 namespace {
 
@@ -66,6 +68,8 @@ constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold: unnormalised 
 constexpr int kSoftWarps = 16;        // softmax warps: 4 per TMEM lane quarter, one 32-column slice each
 constexpr int kSoftThreads = 32 * kSoftWarps;
 constexpr int kAttnThreads = 64 + kSoftThreads;
+constexpr int kDrainWarps = 4;  // backward: one dQ-drain warp per TMEM lane quarter
+constexpr int kBwdThreads = kAttnThreads + 32 * kDrainWarps;
 
 struct FwdParams {
   CUtensorMap tqkv;  // qkv [T, W], box {64, 128}
@@ -79,6 +83,7 @@ struct FwdParams {
 struct BwdParams {
   CUtensorMap tqkv;  // qkv [T, W], box {64, 128}
   CUtensorMap tdo;   // dO [T, nh*hd], box {64, 128}
+  CUtensorMap tdq;   // dQ accumulator fp32 [T, nh*hd], box {32, 32}, SWIZZLE_128B (TMA reduce-add)
   const float* lse;  // [B, nh, S]
   const float* D;    // [B, nh, S]
   float* dq_acc;     // [T, nh*hd] fp32
@@ -96,7 +101,10 @@ struct AttnCfg {
   static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 4096 + 256;
   // bwd: K, V, two {Q, dO, lse, D} stages, dS^T (128 x 128 bf16)
   static constexpr int BWD_QDO = 2 * TILE + 1024;
-  static constexpr int BWD_SMEM_NOPAD = 2 * TILE + 2 * BWD_QDO + 32768 + 256;
+  // dQ staging for the TMA reduce-add: the dS^T buffer itself at head_dim 128 (dQ_i is drained after
+  // its MMA read dS^T and before the next softmax writes it), its own 32 KB at head_dim 64
+  static constexpr int BWD_STAGE = HD == 64 ? 32768 : 0;
+  static constexpr int BWD_SMEM_NOPAD = 2 * TILE + 2 * BWD_QDO + 32768 + BWD_STAGE + 256;
   static constexpr int BWD_SMEM = BWD_SMEM_NOPAD + 1024 <= 232448 ? BWD_SMEM_NOPAD + 1024 : BWD_SMEM_NOPAD;
 };
 
@@ -126,7 +134,8 @@ __device__ __forceinline__ void tld(uint32_t taddr, uint32_t* r) {
 template <int N>
 __device__ __forceinline__ void tst(uint32_t taddr, const uint32_t* r) {
   if constexpr (N == 32) tmem_st_32x32b_x32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(r));
-  else tmem_st_32x32b_x16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+  else if constexpr (N == 16) tmem_st_32x32b_x16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+  else tmem_st_32x32b_x8(taddr, *reinterpret_cast<const uint32_t(*)[8]>(r));
 }
 
 // exponentials of a softmax slice: 3 of every 8 on the FMA pipe (ex2_poly), the rest on the MUFU
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
   const int b = bh / p.nh, h = bh % p.nh, g = h / p.rep;
   const int nblk = p.causal ? qb + 1 : p.nqb;
   const int row0 = b * p.S;
-  const ProfClock pc{p.prof != 0 && blockIdx.x == 0};
+  const ProfClock pc{(p.prof & 1) != 0 && blockIdx.x == 0};
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -401,13 +410,45 @@ __global__ void flash_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, cons
   }
 }
 
+// P^T and dS^T of 16 queries of a key row (backward softmax): P = 2^(S c - LSE_q), dS = P (dP - D_q), both
+// packed to bf16 pairs; LSE / D come from shared memory (lse_s, d_s: 32-bit shared addresses of query q0);
+// MASK zeroes queries before the key (the diagonal block of a causal pass)
+template <bool MASK>
+__device__ __forceinline__ void bwd_half(const uint32_t* sr, const uint32_t* dr, uint32_t lse_s, uint32_t d_s, float c,
+                                         int q0, int r, uint32_t (&pk)[8], uint32_t (&dk)[8]) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const float4 L = lds_v4(lse_s + 16 * v), Dd = lds_v4(d_s + 16 * v);
+    const float lq[4] = {L.x, L.y, L.z, L.w}, dq[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
+    float pp[4], dd[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int t = 4 * v + e;
+      float pv = ex2_approx(fmaf(__uint_as_float(sr[t]), c, -lq[e]));
+      if (MASK && q0 + t < r) pv = 0.f;  // key r is after query q0 + t
+      pp[e] = pv;
+      dd[e] = pv * (__uint_as_float(dr[t]) - dq[e]);
+    }
+    pk[2 * v] = pack_bf16x2(pp[0], pp[1]);
+    pk[2 * v + 1] = pack_bf16x2(pp[2], pp[3]);
+    dk[2 * v] = pack_bf16x2(dd[0], dd[1]);
+    dk[2 * v + 1] = pack_bf16x2(dd[2], dd[3]);
+  }
+}
+
 template <int HD>
-__global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid_constant__ BwdParams p) {
+__global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_constant__ BwdParams p) {
   using Cfg = AttnCfg<HD>;
   constexpr int TILE = Cfg::TILE;
   constexpr uint32_t IDESC_SS = idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
-  constexpr uint32_t IDESC_TS = idesc_bf16_f32(128, HD, false, true);    // dV, dK: A in TMEM, B MN-major
+  constexpr uint32_t IDESC_TS = idesc_bf16_f32(128, HD, false, true);    // dV: A = P^T in TMEM; dK: A = dS^T in smem
+                                                                         // (K-major); B MN-major
   constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, HD, true, true);     // dQ: A (dS) and B (K) MN-major
+  // head_dim 128: dQ^T = K^T dS^T instead (M = hd, N = queries; A = K_j and B = dS^T, both MN-major),
+  // so a TMEM lane holds one hd column of dQ for all 128 queries and a warp's fp32 reductions into the
+  // accumulator are 32 consecutive floats (one 128-byte line) per instruction
+  constexpr bool DQ_T = HD == 128;
+  constexpr uint32_t IDESC_DQT = idesc_bf16_f32(HD, 128, true, true);
   // TMEM: S^T | dP^T | dV | dK (| dQ when it fits: head_dim 64); at head_dim 128 dQ reuses the dP^T
   // columns (its MMA follows dK's read of dS^T there in issue order)
   constexpr bool DQ_OWN = HD == 64;
@@ -424,7 +465,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
   uint8_t* sV = smem + TILE;
   uint8_t* sQD = smem + 2 * TILE;  // 2 stages of {Q, dO, lse[128], D[128]}
   uint8_t* sDS = sQD + 2 * Cfg::BWD_QDO;
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sDS + 32768);
+  uint8_t* sStage = HD == 64 ? sDS + 32768 : sDS;  // dQ staging: 128 rows x 64 fp32
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(sDS + 32768 + Cfg::BWD_STAGE);
   uint64_t* qdo_full = kv_full + 1;
   uint64_t* qdo_empty = qdo_full + 2;
   uint64_t* s_full = qdo_empty + 2;
@@ -444,7 +486,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
   const int i0 = p.causal ? j : 0;
   const int nq = p.nqb - i0;
   const int niter = p.rep * nq;
-  const ProfClock pc{p.prof != 0 && blockIdx.x == 0};
+  const ProfClock pc{(p.prof & 1) != 0 && blockIdx.x == 0};
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -455,13 +497,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
     mbar_init(s_full, 1);
     mbar_init(p_full, kSoftThreads);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, kSoftThreads);
+    mbar_init(dq_empty, 32 * kDrainWarps);
     mbar_init(dkv_full, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tqkv);
     tma_prefetch(&p.tdo);
+    tma_prefetch(&p.tdq);
   }
   if (warp == 1) {
     tmem_alloc(tmem_slot, 512);
@@ -507,6 +550,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
       tc_fence_after();
       const uint64_t ka = kmajor_base(smem_u32(sK)), va = kmajor_base(smem_u32(sV));
       const uint64_t ka_mn = mnmajor_base(smem_u32(sK)), dsa = mnmajor_base(smem_u32(sDS));
+      const uint64_t dsa_k = kmajor_base(smem_u32(sDS));  // dS^T rows = keys (M), queries = K
       const long long tm0 = pm.now();
       for (int it = 0; it < niter; ++it) {
         const int st = it & 1;
@@ -542,7 +586,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
           umma_bf16_ts_w(tmem + DV_COL, tmem + S_COL + k * 8, mnmajor_desc(da_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16_ts_w(tmem + DK_COL, tmem + DP_COL + k * 8, mnmajor_desc(qa_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_w(tmem + DK_COL, kmajor_desc(dsa_k, k), mnmajor_desc(qa_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
         if (DQ_OWN && it > 0) {  // dQ_{it-1} has been drained from its own columns
           mbar_wait(dq_empty, (it - 1) & 1);
           tc_fence_after();
@@ -550,95 +594,153 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
         // dQ_i = dS K_j
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          umma_bf16_w(tmem + DQ_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka_mn, k), IDESC_DQ, k > 0 ? 1u : 0u);
+          if constexpr (DQ_T)
+            umma_bf16_w(tmem + DQ_COL, mnmajor_desc(ka_mn, k), mnmajor_desc(dsa, k), IDESC_DQT, k > 0 ? 1u : 0u);
+          else
+            umma_bf16_w(tmem + DQ_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka_mn, k), IDESC_DQ, k > 0 ? 1u : 0u);
         umma_commit_w(&qdo_empty[st]);
         umma_commit_w(dq_full);
       }
       pm.add(11, tm0);
       umma_commit_w(dkv_full);
     }
+  } else if (warp >= 2 + kSoftWarps) {
+    // ------------------------------------------------------------------ dQ drain (4 warps)
+    // one warp per TMEM lane quarter: rows = queries of block i; tcgen05.ld of dQ_i, the columns
+    // handed back (dq_empty) before the fp32 reductions into the accumulator, which overlap the next
+    // iteration's S^T / dP^T MMAs and softmax
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const ProfClock sp{pc.on && warp == 2 + kSoftWarps + 2 && lane == 0};
+    int h = g * p.rep, i = i0;
+    for (int it = 0; it < niter; ++it) {
+      if (it > 0 && ++i == p.nqb) {
+        i = i0;
+        ++h;
+      }
+      long long t0 = sp.now();
+      mbar_wait(dq_full, it & 1);
+      sp.add(13, t0);
+      const long long td0 = sp.now();
+      tc_fence_after();
+      if constexpr (DQ_T) {
+        // lane = hd column d of dQ^T; 32 queries per TMEM load, each a coalesced 128-byte reduction
+        const int d = q4 * 32 + lane;
+        float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128) * (p.nh * HD) + h * HD + d;
+        const long long ld = static_cast<long long>(p.nh) * HD;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t v[32];
+          tld<32>(tmem + lane_off + DQ_COL + c0, v);
+          tmem_ld_wait();
+          if (c0 == 96) {
+            tc_fence_before();
+            mbar_arrive(dq_empty);
+            sp.add(22, td0);
+          }
+          if (p.prof & 2) continue;  // development: PF_ATTN_PROF=3 drops the dQ reductions (timing only)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) red_add_f32(dst + (c0 + e) * ld, __uint_as_float(v[e]));
+        }
+        sp.add(15, td0);
+        continue;
+      }
+      // 64 columns at a time: TMEM -> this warp's 32 staged rows as two 32 x 32 fp32 SWIZZLE_128B boxes
+      // (16-byte chunk c of row l at c ^ (l % 8): 4-way instead of 32-way bank conflicts) -> TMA
+      // reduce-add of each box into the accumulator
+      uint8_t* stage = sStage + q4 * 8192;
+#pragma unroll
+      for (int c0 = 0; c0 < HD; c0 += 64) {
+        uint32_t v[64];
+        tld<32>(tmem + lane_off + DQ_COL + c0, v);
+        tld<32>(tmem + lane_off + DQ_COL + c0 + 32, v + 32);
+        tmem_ld_wait();
+        if (c0 > 0) {  // the previous boxes' reduces have finished reading the staging rows
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx) {
+          uint8_t* srow = stage + bx * 4096 + lane * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(srow + ((ch ^ (lane & 7)) << 4)) =
+                make_uint4(v[bx * 32 + 4 * ch], v[bx * 32 + 4 * ch + 1], v[bx * 32 + 4 * ch + 2], v[bx * 32 + 4 * ch + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&p.tdq, stage, h * HD + c0, row0 + i * 128 + q4 * 32);
+          tma_reduce_add_2d(&p.tdq, stage + 4096, h * HD + c0 + 32, row0 + i * 128 + q4 * 32);
+          bulk_commit();
+        }
+      }
+      if (lane == 0) bulk_wait_read0();  // staging free for the next softmax (head_dim 128: it is dS^T)
+      __syncwarp();
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+      sp.add(22, td0);
+      sp.add(15, td0);
+    }
+    if (lane == 0) bulk_wait0();  // every reduce-add has landed before the CTA retires
   } else {
-    // ------------------------------------------------------------------ softmax / dQ drain / dK dV
-    // 16 warps: 4 per TMEM lane quarter, each owning 32 query columns of S^T / dP^T, QC columns of
-    // the dQ drain and a share of the final dK / dV rows.
+    // ------------------------------------------------------------------ softmax, then dK dV
+    // 16 warps: 4 per TMEM lane quarter, each owning 32 query columns of S^T / dP^T and a share of
+    // the final dK / dV rows.
     const int q4 = warp & 3;
     const int slice = (warp - 2) >> 2;
-    const int r = q4 * 32 + lane;  // key row of S^T; query row of dQ
+    const int r = q4 * 32 + lane;  // key row of S^T
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const uint32_t bar_id = 1 + q4;
     const float c = p.scale_log2;
-    uint8_t* ds_reg = sDS + (slice >> 1) * 16384 + r * 128;
+    const uint32_t ds_row = smem_u32(sDS + (slice >> 1) * 16384 + r * 128);
     const ProfClock sp{pc.on && threadIdx.x == 64};
     const long long ts0 = sp.now();
-    for (int it = 0; it < niter; ++it) {
+    int i = i0;
+    for (int it = 0; it < niter; ++it, i = (i + 1 == p.nqb) ? i0 : i + 1) {
       const int st = it & 1;
-      const int h = g * p.rep + it / nq, i = i0 + it % nq;
       mbar_wait(&qdo_full[st], (it >> 1) & 1);  // lse / D of this query block are in shared memory
-      const float4* sL = reinterpret_cast<const float4*>(sQD + st * Cfg::BWD_QDO + 2 * TILE) + slice * 8;
-      const float4* sDv = sL + 32;
+      // lse[128] then D[128] of this query block, this slice's 32 queries
+      const uint32_t lse_s = smem_u32(sQD + st * Cfg::BWD_QDO + 2 * TILE) + slice * 128;
       long long t0 = sp.now();
       mbar_wait(s_full, it & 1);
       sp.add(12, t0);
       const long long tc0 = sp.now();
       tc_fence_after();
-      uint32_t sr[32], dr[32];
+      uint32_t sr[32];
       tld<32>(tmem + lane_off + S_COL + slice * 32, sr);
-      tld<32>(tmem + lane_off + DP_COL + slice * 32, dr);
       tmem_ld_wait();
+      sp.add(18, tc0);
       t0 = sp.now();
-      named_bar_sync(bar_id, 128);  // every S^T / dP^T read of the quarter is done before P / dS go over them
+      named_bar_sync(bar_id, 128);  // every S^T read of the quarter is done before P^T goes over it
       sp.add(17, t0);
       const bool diag = p.causal && i == j;
-      uint32_t pk[16], dk[16];
+      const long long tt0 = sp.now();
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const float4 L = sL[v], Dd = sDv[v];
-        const float lq[4] = {L.x, L.y, L.z, L.w}, dq[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
-        float pp[4], dd[4];
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t dr[16], pk[8], dk[8];
+        tld<16>(tmem + lane_off + DP_COL + slice * 32 + hf * 16, dr);
+        tmem_ld_wait();
+        if (diag) bwd_half<true>(sr + hf * 16, dr, lse_s + hf * 64, lse_s + 512 + hf * 64, c, slice * 32 + hf * 16, r, pk, dk);
+        else bwd_half<false>(sr + hf * 16, dr, lse_s + hf * 64, lse_s + 512 + hf * 64, c, slice * 32 + hf * 16, r, pk, dk);
+        tst<8>(tmem + lane_off + S_COL + slice * 16 + hf * 8, pk);
+        // dS^T row r, queries [32 slice + 16 hf, +16): region slice/2, 16-byte units (slice%2)*4 + 2 hf .. +2, SW128
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int t = 4 * v + e;
-          float pv = (e == 3) ? ex2_poly(fmaf(__uint_as_float(sr[t]), c, -lq[e]))
-                              : ex2_approx(fmaf(__uint_as_float(sr[t]), c, -lq[e]));
-          if (diag && slice * 32 + t < r) pv = 0.f;  // key r is after query (slice*32 + t)
-          pp[e] = pv;
-          dd[e] = pv * (__uint_as_float(dr[t]) - dq[e]);
+        for (int u = 0; u < 2; ++u) {
+          const int unit = ((slice & 1) * 4 + hf * 2 + u) ^ (r & 7);
+          sts_v4(ds_row + unit * 16, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
         }
-        pk[2 * v] = pack_bf16x2(pp[0], pp[1]);
-        pk[2 * v + 1] = pack_bf16x2(pp[2], pp[3]);
-        dk[2 * v] = pack_bf16x2(dd[0], dd[1]);
-        dk[2 * v + 1] = pack_bf16x2(dd[2], dd[3]);
       }
-      tst<16>(tmem + lane_off + S_COL + slice * 16, pk);
-      tst<16>(tmem + lane_off + DP_COL + slice * 16, dk);
-      // dS^T row r, queries [32 slice, 32 slice + 32): region slice/2, 16-byte units (slice%2)*4 .. +4
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int unit = ((slice & 1) * 4 + u) ^ (r & 7);
-        *reinterpret_cast<uint4*>(ds_reg + unit * 16) = make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
-      }
+      sp.add(19, tt0);
+      sp.add(20, tt0);
+      const long long tw0 = sp.now();
       tmem_st_wait();
+      sp.add(21, tw0);
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
       sp.add(14, tc0);
-      // dQ_i drain: row r = query (i*128 + r) of head h, this warp's QC columns
-      t0 = sp.now();
-      mbar_wait(dq_full, it & 1);
-      sp.add(13, t0);
-      const long long td0 = sp.now();
-      tc_fence_after();
-      uint32_t v[QC];
-      tld<QC>(tmem + lane_off + DQ_COL + slice * QC, v);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(dq_empty);
-      float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128 + r) * (p.nh * HD) + h * HD + slice * QC;
-#pragma unroll
-      for (int e = 0; e < QC; e += 4)
-        red_add_v4(dst + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                   __uint_as_float(v[e + 3]));
-      sp.add(15, td0);
     }
     sp.add(16, ts0);
     // ---------------------------------------------------------------- dK, dV of key block j
@@ -664,33 +766,36 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_kernel(const __grid
       }
     } else {  // dK: slices 0, 1 take HD/4 columns of the first half each and their RoPE partners
       constexpr int KC = HD / 4;
-      const int col = slice * KC;
-      uint32_t a[KC], bb[KC];
-      tld<KC>(tmem + lane_off + DK_COL + col, a);
-      tld<KC>(tmem + lane_off + DK_COL + HD / 2 + col, bb);
-      tmem_ld_wait();
-      const float2* cs = p.rope ? p.rope + static_cast<long long>(pos) * (HD / 2) + col : nullptr;
-      float fa[KC], fb[KC];
 #pragma unroll
-      for (int e = 0; e < KC; ++e) {
-        const float ga = __uint_as_float(a[e]) * p.scale, gb = __uint_as_float(bb[e]) * p.scale;
-        if (cs) {
-          const float2 t = cs[e];
-          fa[e] = ga * t.x + gb * t.y;
-          fb[e] = gb * t.x - ga * t.y;
-        } else {
-          fa[e] = ga;
-          fb[e] = gb;
+      for (int c16 = 0; c16 < KC; c16 += 16) {
+        const int col = slice * KC + c16;
+        uint32_t a[16], bb[16];
+        tld<16>(tmem + lane_off + DK_COL + col, a);
+        tld<16>(tmem + lane_off + DK_COL + HD / 2 + col, bb);
+        tmem_ld_wait();
+        const float2* cs = p.rope ? p.rope + static_cast<long long>(pos) * (HD / 2) + col : nullptr;
+        float fa[16], fb[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float ga = __uint_as_float(a[e]) * p.scale, gb = __uint_as_float(bb[e]) * p.scale;
+          if (cs) {
+            const float2 t = cs[e];
+            fa[e] = ga * t.x + gb * t.y;
+            fb[e] = gb * t.x - ga * t.y;
+          } else {
+            fa[e] = ga;
+            fb[e] = gb;
+          }
         }
-      }
-      uint4* ka = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + col);
-      uint4* kb = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + HD / 2 + col);
+        uint4* ka = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + col);
+        uint4* kb = reinterpret_cast<uint4*>(row + (p.nh + g) * HD + HD / 2 + col);
 #pragma unroll
-      for (int u = 0; u < KC / 8; ++u) {
-        ka[u] = make_uint4(pack_bf16x2(fa[8 * u], fa[8 * u + 1]), pack_bf16x2(fa[8 * u + 2], fa[8 * u + 3]),
-                           pack_bf16x2(fa[8 * u + 4], fa[8 * u + 5]), pack_bf16x2(fa[8 * u + 6], fa[8 * u + 7]));
-        kb[u] = make_uint4(pack_bf16x2(fb[8 * u], fb[8 * u + 1]), pack_bf16x2(fb[8 * u + 2], fb[8 * u + 3]),
-                           pack_bf16x2(fb[8 * u + 4], fb[8 * u + 5]), pack_bf16x2(fb[8 * u + 6], fb[8 * u + 7]));
+        for (int u = 0; u < 2; ++u) {
+          ka[u] = make_uint4(pack_bf16x2(fa[8 * u], fa[8 * u + 1]), pack_bf16x2(fa[8 * u + 2], fa[8 * u + 3]),
+                             pack_bf16x2(fa[8 * u + 4], fa[8 * u + 5]), pack_bf16x2(fa[8 * u + 6], fa[8 * u + 7]));
+          kb[u] = make_uint4(pack_bf16x2(fb[8 * u], fb[8 * u + 1]), pack_bf16x2(fb[8 * u + 2], fb[8 * u + 3]),
+                             pack_bf16x2(fb[8 * u + 4], fb[8 * u + 5]), pack_bf16x2(fb[8 * u + 6], fb[8 * u + 7]));
+        }
       }
     }
   }
@@ -740,7 +845,7 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloa
 int attn_prof_enabled() {
   static const int on = [] {
     const char* e = std::getenv("PF_ATTN_PROF");
-    return e && e[0] == '1' ? 1 : 0;
+    return e ? std::atoi(e) : 0;
   }();
   return on;
 }
@@ -791,6 +896,8 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
   if (tma_desc_bf16_2d(&p.tqkv, qkv, T, W, W, 64, 128)) return PF_ERR_INVALID;
   if (tma_desc_bf16_2d(&p.tdo, dout, T, static_cast<long long>(nh) * HD, static_cast<long long>(nh) * HD, 64, 128))
     return PF_ERR_INVALID;
+  if (tma_desc_f32_2d(&p.tdq, dq_acc, T, static_cast<long long>(nh) * HD, static_cast<long long>(nh) * HD, 32, 32))
+    return PF_ERR_INVALID;
   p.lse = lse;
   p.D = D;
   p.dq_acc = dq_acc;
@@ -814,7 +921,7 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
       return PF_ERR_CUDA;
     attr = true;
   }
-  launch_k(kern, dim3(B * nkv * p.nqb), dim3(kAttnThreads), Cfg::BWD_SMEM, s, p);
+  launch_k(kern, dim3(B * nkv * p.nqb), dim3(kBwdThreads), Cfg::BWD_SMEM, s, p);
   if ((rc = status())) return rc;
   launch_k(flash_bwd_dq_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh * HD / 8 / 256 + 1)), dim3(256), 0, s,
            dq_acc, dqkv, W, rope, T, S, nh, scale);

@@ -459,6 +459,22 @@ int tma_desc_bf16_2d(CUtensorMap* map, const void* ptr, long long rows, long lon
   return make_tmap(map, ptr, rows, cols, ld, box_cols, box_rows);
 }
 
+// fp32 row-major [rows][cols], row stride ld (elements), SWIZZLE_128B: box_cols * 4 <= 128 (TMA
+// reduce-add targets)
+int tma_desc_f32_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_cols,
+                    int box_rows) {
+  auto encode = get_encode();
+  if (!encode) return PF_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PF_OK : PF_ERR_INVALID;
+}
+
 int tma_desc_bf16_2d_sw64(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
                           int box_cols, int box_rows) {
   return make_tmap(map, ptr, rows, cols, ld, box_cols, box_rows, CU_TENSOR_MAP_SWIZZLE_64B);

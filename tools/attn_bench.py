@@ -49,7 +49,7 @@ def main():
                                             dqkv.data_ptr(), B, S, nh, nkv, hd, scale, 1, 500000.0, st)
         assert fwd() == 0 and bwd() == 0
         f_ms, b_ms = timeit(fwd, a.iters), timeit(bwd, a.iters)
-        if os.environ.get("PF_ATTN_PROF") == "1":
+        if os.environ.get("PF_ATTN_PROF", "0") in ("1", "3"):
             import ctypes
 
             import numpy as np
@@ -65,7 +65,8 @@ def main():
             torch.cuda.synchronize()
             lib.pf_flash_attn_prof(buf.ctypes.data_as(ctypes.c_void_p))
             print(f"{name} bwd CTA0 cycles: mma wait_qdo {buf[8]} wait_dqempty {buf[9]} wait_p {buf[10]} total {buf[11]} | "
-                  f"softmax wait_s {buf[12]} bar {buf[17]} compute {buf[14]} wait_dq {buf[13]} drain {buf[15]} total {buf[16]}")
+                  f"softmax wait_s {buf[12]} bar {buf[17]} compute {buf[14]} (tld {buf[18]} bar+math {buf[19]} tst {buf[20]} "
+                  f"st_wait {buf[21]}) wait_dq {buf[13]} drain {buf[15]} (tld {buf[22]}) total {buf[16]}")
         flops_f = 4.0 * B * S * S * nh * hd / 2  # causal
         line = f"{name:9s} ours: fwd {f_ms * 1e3:7.1f} us ({flops_f / f_ms / 1e9:6.1f} TF/s)  bwd {b_ms * 1e3:7.1f} us " \
                f"({2.5 * flops_f / b_ms / 1e9:6.1f} TF/s)"
