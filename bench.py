@@ -37,6 +37,14 @@ sys.path.insert(0, ROOT)
 METRIC = "tokens/sec per PP step at 1/2/4/8 B200 vs no-freeze; batch time vs LP makespan"
 
 
+_T0 = time.perf_counter()
+
+
+def progress(msg: str) -> None:
+    """Phase marks on stderr (the JSON line stays the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -441,7 +449,9 @@ def run_ours(args) -> None:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl")
+    progress("pp consistency check")
     pp_check = pp_consistency_check(world, rank, local)
+    progress(f"pp check done: {pp_check['max_rel_update_diff']:.2e}")
     shape = model_shape(args)
     M = args.microbatches
     phases = tuple(args.phases)
@@ -457,8 +467,10 @@ def run_ours(args) -> None:
     # ---- controller: warm-up, monitoring, LP solve, ramp (untimed)
     t = 0
     ctl = []
+    progress("trainer ready; controller steps")
     for t in range(1, phases[2] + 1):
         ctl.append(tr.step(t))
+        progress(f"controller step {t}: loss {ctl[-1]['loss']:.4f} batch {ctl[-1]['batch_ms']:.1f} ms")
     plan = tr.get_plan()
 
     def timed_steps(start_t: int, k: int, host=None):
@@ -495,6 +507,7 @@ def run_ours(args) -> None:
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    progress("timed freeze steps")
     lib.pf_probe_enable(1)  # time the dominant kernel's launches inside the timed steps
     ncu_range = bool(os.environ.get("PF_NCU_RANGE"))  # ncu --profile-from-start off: the timed steps only
     if ncu_range:
@@ -513,6 +526,7 @@ def run_ours(args) -> None:
 
     # ---- no-freeze comparison (every unit updated; a shorter run: it is the speed-up's denominator)
     nf_steps = min(args.steps, 8)
+    progress(f"freeze {ms_step:.1f} ms/step; no-freeze steps")
     tr.set_override(0.0)
     for i in range(2):
         tr.step(t + i)
@@ -530,7 +544,9 @@ def run_ours(args) -> None:
     host_tok = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32, generator=g).pin_memory()
     host_tgt = torch.randint(0, shape.vocab, (M, T), dtype=torch.int32, generator=g).pin_memory()
     hp = (host_tok.numpy(), host_tgt.numpy())
+    progress(f"no-freeze {nf_ms:.1f} ms/step; e2e steps")
     e2e_dev, e2e_wall, e2e_res, _ = timed_steps(t, args.steps, host=hp)
+    progress("e2e done")
     t += args.steps
     e2e_wall = max_over_ranks(e2e_wall)
     words = sum(((tr.stage_buffers(i)["n_units"] + 63) // 64 + 1) for i in range(tr.info["local_stages"])) * M
@@ -548,6 +564,7 @@ def run_ours(args) -> None:
         if world == 1 and not os.environ.get("PF_SKIP_CPU_BASELINE"):
             # the reference's CPU path on this host's cores, one full-size step (after the timed region)
             n_params, units = _workload_params(shape, world * C)
+            progress("cpu_baseline: one reference CPU step")
             try:
                 ref_step = ReferenceCpuStep(args.schedule, world, C, M, units, n_params, mean_ratio)
                 try:

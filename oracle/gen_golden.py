@@ -291,3 +291,30 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "artifacts":
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lp_big":
     gen_lp_big()
+
+
+def gen_boundary(fx):
+    """Device-boundary case (tests/test_boundary_gpu.py): the reference's plan.json for the C1
+    fixture, whose stage-2 row (8 ratios) is injected with pf_trainer_set_plan into a 1-stage,
+    8-microbatch trainer of the tiny preset (160 units); the expected masks are the reference's
+    run_freezing_masks words for that single stage (freezectl.cpp:185-211) over t = 1..T."""
+    f = fx["default_1f1b_s4m8"]
+    pl = f["pipeline"]
+    R, C, M = pl["num_ranks"], pl["stages_per_rank"], pl["num_microbatches"]
+    t = f["timing"]["per_stage"]
+    plan_txt, _ = ref.plan_json(pl["schedule"], R, C, M, t["forward_ms"], t["backward_act_ms"],
+                                t["backward_param_ms"], f["r_max"])
+    doc = json.loads(plan_txt)
+    ratios = np.zeros(M)
+    for e in doc["ratios"]:
+        if e["s"] == 2:
+            ratios[e["m"] - 1] = e["r"]
+    phases, n, seed, T = [1, 3, 4, 9], 160, 17, 9
+    _, _, words = ref.freezing_masks(M, 1, phases, ratios, n, seed, 1, T)
+    dump("boundary.json", {"fixture": "default_1f1b_s4m8", "plan_json": plan_txt, "stage": 2, "M": M,
+                           "phases": phases, "n_units": n, "seed": seed, "steps": T,
+                           "words": [[str(int(x)) for x in row] for row in words]})
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "boundary":
+    gen_boundary(fixtures())
