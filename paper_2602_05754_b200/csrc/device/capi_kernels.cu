@@ -115,6 +115,8 @@ const char* pf_device_last_error(void) { return g_last_error.c_str(); }
 }  // extern "C"
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 
 namespace pf {
@@ -138,6 +140,24 @@ bool pdl_enabled() {
   return env >= 0 ? env == 1 : g_pdl_default.load(std::memory_order_relaxed) != 0;
 }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+bool trace_launches() {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_TRACE_LAUNCH");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+void trace_launch(const void* func, dim3 grid, cudaStream_t s) {
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, func) != cudaSuccess || !name) name = "?";
+  std::fprintf(stderr, "[pf launch %lld] %s grid (%u,%u,%u) ...", launch_count(), name, grid.x, grid.y, grid.z);
+  std::fflush(stderr);
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = cudaStreamSynchronize(s);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::fprintf(stderr, " %s %.3f ms\n", cudaGetErrorString(e), ms);
+  std::fflush(stderr);
+}
 }  // namespace pf
 
 extern "C" long long pf_device_launch_count(void) { return pf::launch_count(); }

@@ -310,11 +310,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
           fmaxf(fmaxf(rb[r], rb[128 + r]), fmaxf(rb[256 + r], rb[384 + r])) * c;
       if (j == 0) {
         m_used = mrow;
-      } else if (mrow > m_used + kRescaleLog2) {
-        // O and l were accumulated against m_used: rescale once PV_{j-1} has landed in TMEM
+      } else if (__any_sync(0xffffffffu, mrow > m_used + kRescaleLog2)) {
+        // O and l were accumulated against m_used: rescale once PV_{j-1} has landed in TMEM. The
+        // decision is warp-uniform (tcgen05.ld / st are warp-collective: a lane-divergent TMEM access
+        // hangs the warp); every lane moves to max(m_used, mrow), a factor of 1 where its max did not
+        // grow. The quarter's 4 slice warps see the same rows, so they take the same branch.
         mbar_wait(o_bar, (j - 1) & 1);
         tc_fence_after();
-        const float a = ex2_approx(m_used - mrow);
+        const float mn = fmaxf(m_used, mrow);
+        const float a = ex2_approx(m_used - mn);
         l *= a;
         uint32_t o[OC];
         tld<OC>(tmem + lane_off + O_COL + slice * OC, o);
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
 #pragma unroll
         for (int i = 0; i < OC; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
         tst<OC>(tmem + lane_off + O_COL + slice * OC, o);
-        m_used = mrow;
+        m_used = mn;
       }
       const float nm = -m_used;
       uint32_t pk[16];

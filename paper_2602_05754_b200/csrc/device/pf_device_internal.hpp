@@ -101,6 +101,12 @@ void probe_end(cudaStream_t s);
 bool pdl_enabled();
 void set_pdl_default(bool on);
 
+// PF_TRACE_LAUNCH=1 (debugging a hung step): every launch_k prints the kernel's name and grid to
+// stderr, synchronises its stream and prints the elapsed time, so the last line names a kernel
+// that never finished.
+bool trace_launches();
+void trace_launch(const void* func, dim3 grid, cudaStream_t s);
+
 // Number of kernels this library has launched (evidence for bench.py gpu_launches).
 void count_launch();
 long long launch_count();

@@ -5,6 +5,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#ifdef PF_MBAR_WATCHDOG
+#include <cstdio>
+#endif
 
 namespace pf {
 
@@ -43,6 +46,30 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef PF_MBAR_WATCHDOG
+// Debug builds (tools/build_variant.py ... -DPF_MBAR_WATCHDOG): a wait that spins for ~2^31 cycles
+// prints the CTA, thread, barrier offset and parity, then traps (a hung pipeline names its barrier).
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 31)) {
+      extern __shared__ uint8_t pf_wd_smem[];
+      printf("[mbar watchdog] block %d thread %d bar smem+%d parity %u\n", static_cast<int>(blockIdx.x),
+             static_cast<int>(threadIdx.x), static_cast<int>(smem_u32(bar) - smem_u32(pf_wd_smem)), parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -54,6 +81,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {

@@ -158,3 +158,40 @@ def test_flash_attention_rejects_unsupported_shapes(cuda):
     assert lib().pf_flash_attn_fwd(buf.data_ptr(), buf.data_ptr(), lse.data_ptr(), 1, 100, 2, 2, 64, 0.1, 1, sp()) == 4
     assert lib().pf_flash_attn_fwd(buf.data_ptr(), buf.data_ptr(), lse.data_ptr(), 1, 128, 2, 2, 96, 0.1, 1, sp()) == 4
     assert lib().pf_flash_attn_fwd(buf.data_ptr(), buf.data_ptr(), lse.data_ptr(), 1, 128, 3, 2, 64, 0.1, 1, sp()) == 4
+
+
+@pytest.mark.parametrize("hd,causal", [(128, True), (64, True), (128, False)])
+def test_flash_forward_lane_divergent_rescale(cuda, hd, causal):
+    """Rows of one warp whose running max grows past the lazy-rescale threshold at different key
+    blocks (alternating query rows see a +-12 log2-unit spike in key block 1): the O rescale must
+    be warp-uniform (tcgen05.ld / st are warp-collective; a lane-divergent TMEM access hung the
+    LLaMA-8B step). Forward output and LSE vs fp32."""
+    import torch
+    import torch.nn.functional as F
+
+    B, S, nh, nkv = 1, 512, 4, 2
+    T, W = B * S, (nh + 2 * nkv) * hd
+    g = torch.Generator(device="cpu").manual_seed(77)
+    x = torch.randn(T, nh + 2 * nkv, hd, generator=g) * 0.5
+    sign = torch.where(torch.arange(S) % 2 == 0, 1.0, -1.0)
+    x[:, :nh, 0] = 5.0 * sign[:, None]           # q: +-5 along dim 0, alternating rows
+    x[128:256, nh:nh + nkv, 0] = 2.2 * hd ** 0.5  # k: spike along dim 0 in key block 1
+    qkv = x.reshape(T, W).bfloat16().cuda()
+    out = torch.empty(T, nh * hd, dtype=torch.bfloat16, device=cuda)
+    lse = torch.empty(B, nh, S, dtype=torch.float32, device=cuda)
+    scale = hd ** -0.5
+    chk(lib().pf_flash_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), B, S, nh, nkv, hd, scale, int(causal),
+                                sp()), "fwd")
+    torch.cuda.synchronize()
+    xf = qkv.float().view(B, S, nh + 2 * nkv, hd)
+    q, k, v = xf[:, :, :nh], xf[:, :, nh:nh + nkv], xf[:, :, nh + nkv:]
+    rep = nh // nkv
+    ke, ve = k.repeat_interleave(rep, 2), v.repeat_interleave(rep, 2)
+    ref = F.scaled_dot_product_attention(q.transpose(1, 2), ke.transpose(1, 2), ve.transpose(1, 2), is_causal=causal,
+                                         scale=scale).transpose(1, 2).reshape(T, nh * hd)
+    assert _rel(out, ref) <= 1e-2, _rel(out, ref)
+    s = torch.einsum("bqhd,bkhd->bhqk", q, ke) * scale
+    if causal:
+        s = s.masked_fill(torch.ones(S, S, dtype=torch.bool, device=cuda).triu(1), float("-inf"))
+    lse_ref = torch.logsumexp(s, -1) / np.log(2.0)
+    assert (lse - lse_ref).abs().max().item() <= 1e-3 * max(1.0, lse_ref.abs().max().item())

@@ -23,11 +23,9 @@ def main():
     subprocess.run([B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler",
                     "-fPIC", "-I", B.INC, "-I", B.DEV_SRC, "-I", B.HOST_SRC, *defs, "-c", srcp, "-o", obj], check=True)
     objs = [o for o in glob.glob(os.path.join(B.OBJ, "*.o")) if os.path.basename(o) != src + ".o"] + [obj]
-    _, tlib = B._torch_paths()
     subprocess.run([B.NVCC, *B.ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o",
-                    os.path.join(out_dir, "libpf_device.so"), f"-L{tlib}", "-Xlinker", f"-rpath={tlib}", "-lc10",
-                    "-lc10_cuda", "-ltorch_cpu", "-ltorch_cuda", "-lcudart", f"-L{B.LIB}", "-lpf_host", "-Xlinker",
-                    "-rpath=$ORIGIN", "-lnccl"], check=True)
+                    os.path.join(out_dir, "libpf_device.so"), "-lcudart", f"-L{B.LIB}", "-lpf_host", "-Xlinker",
+                    "-rpath=$ORIGIN/../../paper_2602_05754_b200/lib", *B._nccl_flags()], check=True)
     os.remove(obj)
     print(os.path.join(out_dir, "libpf_device.so"))
 
