@@ -60,6 +60,19 @@ class _FlashRefAttention(torch.autograd.Function):
         return dq, dk, dv
 
 
+class _RoundFwdBF16(torch.autograd.Function):
+    """bf16 rounding of the value only: the gradient passes through in fp32 (the device rounds it
+    later, at an upstream storage point)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        return x.bfloat16().float()
+
+    @staticmethod
+    def backward(ctx, g):
+        return g
+
+
 def _q(x, faithful: bool):
     return _RoundBF16.apply(x) if faithful else x
 
@@ -121,7 +134,10 @@ def stage_loss(params: dict, shape, layers: range, tokens: torch.Tensor, targets
         q = qkv[:, : nh * hd].view(B, S, nh, hd)
         k = qkv[:, nh * hd:(nh + nkv) * hd].view(B, S, nkv, hd)
         v = qkv[:, (nh + nkv) * hd:].view(B, S, nkv, hd)
-        q, k = Q(rope(q, S, shape.rope_theta)), Q(rope(k, S, shape.rope_theta))
+        # the device rotates the bf16 q / k in fp32 and rounds the result (qkv GEMM epilogue); its
+        # backward rotates the fp32 dq / dk accumulators and rounds once, into dqkv (flash_attn.cu)
+        Qf = (lambda t: _RoundFwdBF16.apply(t)) if faithful else (lambda t: t)  # noqa: E731
+        q, k = Qf(rope(q, S, shape.rope_theta)), Qf(rope(k, S, shape.rope_theta))
         rep = nh // nkv
         k = k.repeat_interleave(rep, dim=2)
         v = v.repeat_interleave(rep, dim=2)
