@@ -33,10 +33,11 @@ def bf(x):
     return x.to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("T,h", [(256, 1024), (512, 2048), (136, 256), (200, 4096), (72, 5120), (64, 768)])
+@pytest.mark.parametrize("T,h", [(256, 1024), (512, 2048), (136, 256), (200, 4096), (201, 4096), (72, 5120), (73, 5120), (64, 768)])
 def test_rmsnorm_fwd_bwd(cuda, T, h):
-    """Register-row forward and the fused backward (dx + dg in one pass, deterministic dg) for the
-    LLaMA widths; h = 768 takes the generic kernels."""
+    """Register-row forward and the fused backward (dx + dg in one pass) for the LLaMA widths
+    (h = 4096 / 5120: the row-block kernels, odd T covers their tail rows); h = 768 takes the
+    generic kernels."""
     import torch
 
     g = torch.Generator().manual_seed(1)

@@ -6,7 +6,8 @@ from paper_2602_05754_b200 import _native  # noqa: E402
 lib = _native.device()
 s = torch.cuda.current_stream().cuda_stream
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
-for T, h in [(4096, 2048), (4096, 4096)]:
+for T, h, rows in [(4096, 2048, "1"), (4096, 4096, "0"), (4096, 4096, "1"), (2048, 5120, "1")]:
+    os.environ["PF_NORM_ROWS"] = rows  # 0: warp-per-row kernels at h = 4096 (A/B)
     x = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     dy = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     res = torch.randn(T, h, device="cuda").to(torch.bfloat16)
@@ -24,7 +25,7 @@ for T, h in [(4096, 2048), (4096, 4096)]:
         e1.record(); torch.cuda.synchronize()
         if k >= 3: tot += e0.elapsed_time(e1)
     us = tot / 20 * 1e3
-    print(f"rmsnorm_bwd T={T} h={h}: {us:.1f} us, {4 * T * h * 2 / us / 1e3:.0f} GB/s (x, dy, residual in; dx out)")
+    print(f"rmsnorm_bwd T={T} h={h} rows={rows}: {us:.1f} us, {4 * T * h * 2 / us / 1e3:.0f} GB/s (x, dy, residual in; dx out)")
     y = torch.empty_like(x)
     tot = 0.0
     for k in range(23):
@@ -35,4 +36,4 @@ for T, h in [(4096, 2048), (4096, 4096)]:
         e1.record(); torch.cuda.synchronize()
         if k >= 3: tot += e0.elapsed_time(e1)
     us = tot / 20 * 1e3
-    print(f"rmsnorm_fwd T={T} h={h}: {us:.1f} us, {2 * T * h * 2 / us / 1e3:.0f} GB/s (x in; y out)")
+    print(f"rmsnorm_fwd T={T} h={h} rows={rows}: {us:.1f} us, {2 * T * h * 2 / us / 1e3:.0f} GB/s (x in; y out)")
