@@ -20,8 +20,9 @@
 //               bf16 back into TMEM; epilogue O / l -> bf16 [T, nh*hd], LSE (log2 domain) [B, nh, S].
 //
 // Backward (flash_bwd_kernel, one CTA per (sequence, kv head, 128-key block): it loops over the
-// rep = nh / nkv query heads of the group and the query blocks the keys see, so K_j / V_j stay in
-// shared memory and dK / dV accumulate in TMEM):
+// query blocks the keys see and, inside, the rep = nh / nkv query heads of the group, so K_j / V_j
+// stay in shared memory and dK / dV accumulate in TMEM; query-block-major, the CTAs of different key
+// blocks that run in lockstep reduce into different dQ rows at any time):
 //   S^T  = K_j Q_i^T, dP^T = V_j dO_i^T                       (TMEM, lane = key row)
 //   P^T  = 2^(S^T * c - LSE_i), dS^T = P^T (dP^T - D_i)      (softmax warps; bf16 into TMEM over
 //                                                              S^T / dP^T and dS^T into shared memory)
@@ -138,12 +139,6 @@ __device__ __forceinline__ void tst(uint32_t taddr, const uint32_t* r) {
   else tmem_st_32x32b_x8(taddr, *reinterpret_cast<const uint32_t(*)[8]>(r));
 }
 
-// exponentials of a softmax slice: 3 of every 8 on the FMA pipe (ex2_poly), the rest on the MUFU
-template <int I>
-__device__ __forceinline__ float ex2_mixed(float x) {
-  if constexpr ((I & 7) >= 5) return ex2_poly(x);
-  else return ex2_approx(x);
-}
 
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid_constant__ FwdParams p) {
@@ -298,11 +293,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
         for (int i = 0; i < 32; ++i)
           if (slice * 32 + i > r) sv[i] = -INFINITY;
       }
-      float mx[4] = {sv[0], sv[1], sv[2], sv[3]};
+      // row maximum of the slice: 3-input maxima in 4 independent chains
+      float mx[4] = {max3f(sv[0], sv[1], sv[2]), max3f(sv[3], sv[4], sv[5]), max3f(sv[6], sv[7], sv[8]),
+                     max3f(sv[9], sv[10], sv[11])};
 #pragma unroll
-      for (int i = 4; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], sv[i]);
+      for (int i = 12; i < 28; i += 8) {
+        mx[0] = max3f(mx[0], sv[i], sv[i + 1]);
+        mx[1] = max3f(mx[1], sv[i + 2], sv[i + 3]);
+        mx[2] = max3f(mx[2], sv[i + 4], sv[i + 5]);
+        mx[3] = max3f(mx[3], sv[i + 6], sv[i + 7]);
+      }
       float* rb = red + (j & 1) * 512;
-      rb[slice * 128 + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      rb[slice * 128 + r] = fmaxf(max3f(mx[0], mx[1], sv[28]), max3f(mx[2], mx[3], fmaxf(sv[29], fmaxf(sv[30], sv[31]))));
       const long long tb0 = sp.now();
       named_bar_sync(bar_id, 128);  // every slice's maximum is in; every S read of the quarter is done
       sp.add(4, tb0);
@@ -330,21 +332,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
       }
       const float nm = -m_used;
       uint32_t pk[16];
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      // x = s c - m on packed pairs (FFMA2); 2^x for 6 of the 16 pairs on the FMA pipe (ex2_poly2,
+      // FA4-style MUFU offload), the rest on the MUFU; row sums in two packed accumulators (FADD2)
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        float p0, p1;
-        // compile-time pattern of which exponentials go to the FMA pipe
-        switch (i & 3) {
-          case 0: p0 = ex2_mixed<0>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<1>(fmaf(sv[2 * i + 1], c, nm)); break;
-          case 1: p0 = ex2_mixed<2>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<3>(fmaf(sv[2 * i + 1], c, nm)); break;
-          case 2: p0 = ex2_mixed<4>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<5>(fmaf(sv[2 * i + 1], c, nm)); break;
-          default: p0 = ex2_mixed<6>(fmaf(sv[2 * i], c, nm)); p1 = ex2_mixed<7>(fmaf(sv[2 * i + 1], c, nm)); break;
-        }
-        ls[i & 3] += p0 + p1;
-        pk[i] = pack_bf16x2(p0, p1);
+        const float2 x = fma2(make_float2(sv[2 * i], sv[2 * i + 1]), make_float2(c, c), make_float2(nm, nm));
+        float2 e;
+        if ((i % 8) == 2 || (i % 8) == 5 || (i % 8) == 7) e = ex2_poly2(x);
+        else e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        ls2[i & 1] = add2(ls2[i & 1], e);
+        pk[i] = pack_bf16x2(e.x, e.y);
       }
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      l += (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
       tst<16>(sa + slice * 16, pk);  // P over S (every S read of this quarter finished at the barrier)
       tmem_st_wait();
       tc_fence_before();
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
       }
       for (int it = 0; it < niter; ++it) {
         const int st = it & 1;
-        const int h = g * p.rep + it / nq, i = i0 + it % nq;
+        const int h = g * p.rep + it % p.rep, i = i0 + it / p.rep;
         mbar_wait(&qdo_empty[st], ((it >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qdo_full[st], Cfg::BWD_QDO);
         uint8_t* base = sQD + st * Cfg::BWD_QDO;
@@ -617,21 +617,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const ProfClock sp{pc.on && warp == 2 + kSoftWarps + 2 && lane == 0};
-    int h = g * p.rep, i = i0;
     for (int it = 0; it < niter; ++it) {
-      if (it > 0 && ++i == p.nqb) {
-        i = i0;
-        ++h;
-      }
+      const int h = g * p.rep + it % p.rep, i = i0 + it / p.rep;
       long long t0 = sp.now();
       mbar_wait(dq_full, it & 1);
       sp.add(13, t0);
       const long long td0 = sp.now();
       tc_fence_after();
       if constexpr (DQ_T) {
-        // lane = hd column d of dQ^T; 32 queries per TMEM load, each a coalesced 128-byte reduction
-        const int d = q4 * 32 + lane;
-        float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128) * (p.nh * HD) + h * HD + d;
+        // lane = hd column d of dQ^T, 32 queries per TMEM load. A 4 x 4 transpose inside each lane quad
+        // (two xor-shuffle stages) gives lane 4a + b the 4 consecutive columns 4a .. 4a + 3 of query
+        // 4c + b, so a warp's reduction is one red.global.add.v4.f32 per 4 queries (4 x 128 B lines)
+        // instead of one scalar red per query: a quarter of the L2 reduction operations
+        const int a4 = lane >> 2, b4 = lane & 3;
+        float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128) * (p.nh * HD) + h * HD + q4 * 32 + 4 * a4;
         const long long ld = static_cast<long long>(p.nh) * HD;
 #pragma unroll
         for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -645,7 +644,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
           }
           if (p.prof & 2) continue;  // development: PF_ATTN_PROF=3 drops the dQ reductions (timing only)
 #pragma unroll
-          for (int e = 0; e < 32; ++e) red_add_f32(dst + (c0 + e) * ld, __uint_as_float(v[e]));
+          for (int c = 0; c < 8; ++c) {
+            float x0 = __uint_as_float(v[4 * c]), x1 = __uint_as_float(v[4 * c + 1]);
+            float x2 = __uint_as_float(v[4 * c + 2]), x3 = __uint_as_float(v[4 * c + 3]);
+            {  // 2 x 2 blocks across lanes b, b ^ 2
+              const bool up = (b4 & 2) != 0;
+              const float r0 = __shfl_xor_sync(0xffffffffu, up ? x0 : x2, 2);
+              const float r1 = __shfl_xor_sync(0xffffffffu, up ? x1 : x3, 2);
+              if (up) {
+                x0 = r0;
+                x1 = r1;
+              } else {
+                x2 = r0;
+                x3 = r1;
+              }
+            }
+            {  // within the 2 x 2 blocks, lanes b, b ^ 1
+              const bool up = (b4 & 1) != 0;
+              const float r0 = __shfl_xor_sync(0xffffffffu, up ? x0 : x1, 1);
+              const float r1 = __shfl_xor_sync(0xffffffffu, up ? x2 : x3, 1);
+              if (up) {
+                x0 = r0;
+                x2 = r1;
+              } else {
+                x1 = r0;
+                x3 = r1;
+              }
+            }
+            red_add_v4(dst + (c0 + 4 * c + b4) * ld, x0, x1, x2, x3);
+          }
         }
         sp.add(15, td0);
         continue;
@@ -701,8 +728,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
     const uint32_t ds_row = smem_u32(sDS + (slice >> 1) * 16384 + r * 128);
     const ProfClock sp{pc.on && threadIdx.x == 64};
     const long long ts0 = sp.now();
-    int i = i0;
-    for (int it = 0; it < niter; ++it, i = (i + 1 == p.nqb) ? i0 : i + 1) {
+    for (int it = 0; it < niter; ++it) {
+      const int i = i0 + it / p.rep;
       const int st = it & 1;
       mbar_wait(&qdo_full[st], (it >> 1) & 1);  // lse / D of this query block are in shared memory
       // lse[128] then D[128] of this query block, this slice's 32 queries
