@@ -423,20 +423,25 @@ __device__ __forceinline__ void bwd_half(const uint32_t* sr, const uint32_t* dr,
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     const float4 L = lds_v4(lse_s + 16 * v), Dd = lds_v4(d_s + 16 * v);
-    const float lq[4] = {L.x, L.y, L.z, L.w}, dq[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
-    float pp[4], dd[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int t = 4 * v + e;
-      float pv = ex2_approx(fmaf(__uint_as_float(sr[t]), c, -lq[e]));
-      if (MASK && q0 + t < r) pv = 0.f;  // key r is after query q0 + t
-      pp[e] = pv;
-      dd[e] = pv * (__uint_as_float(dr[t]) - dq[e]);
+    for (int h2 = 0; h2 < 2; ++h2) {
+      // one pair of queries t, t + 1: packed fp32 (FFMA2 / FADD2 / FMUL2); the exponentials of
+      // 3 pairs in 8 on the FMA pipe (ex2_poly2), the rest on the MUFU
+      const int t = 4 * v + 2 * h2;
+      const float2 lq = h2 ? make_float2(-L.z, -L.w) : make_float2(-L.x, -L.y);
+      const float2 nd = h2 ? make_float2(-Dd.z, -Dd.w) : make_float2(-Dd.x, -Dd.y);
+      const float2 x = fma2(make_float2(__uint_as_float(sr[t]), __uint_as_float(sr[t + 1])), make_float2(c, c), lq);
+      float2 pv;
+      if ((v * 2 + h2) % 8 == 2 || (v * 2 + h2) % 8 == 5 || (v * 2 + h2) % 8 == 7) pv = ex2_poly2(x);
+      else pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+      if (MASK) {  // key r is after query q0 + t
+        if (q0 + t < r) pv.x = 0.f;
+        if (q0 + t + 1 < r) pv.y = 0.f;
+      }
+      const float2 dd = mul2(pv, add2(make_float2(__uint_as_float(dr[t]), __uint_as_float(dr[t + 1])), nd));
+      pk[2 * v + h2] = pack_bf16x2(pv.x, pv.y);
+      dk[2 * v + h2] = pack_bf16x2(dd.x, dd.y);
     }
-    pk[2 * v] = pack_bf16x2(pp[0], pp[1]);
-    pk[2 * v + 1] = pack_bf16x2(pp[2], pp[3]);
-    dk[2 * v] = pack_bf16x2(dd[0], dd[1]);
-    dk[2 * v + 1] = pack_bf16x2(dd[2], dd[3]);
   }
 }
 
