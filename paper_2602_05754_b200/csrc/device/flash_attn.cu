@@ -69,6 +69,7 @@ constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold: unnormalised 
 constexpr int kSoftWarps = 16;        // softmax warps: 4 per TMEM lane quarter, one 32-column slice each
 constexpr int kSoftThreads = 32 * kSoftWarps;
 constexpr int kAttnThreads = 64 + kSoftThreads;
+constexpr int kFwd2Threads = 64 + 512;  // two-tile forward: TMA, MMA, 8 softmax warps per tile
 constexpr int kDrainWarps = 4;  // backward: one dQ-drain warp per TMEM lane quarter
 constexpr int kBwdThreads = kAttnThreads + 32 * kDrainWarps;
 
@@ -100,6 +101,8 @@ struct AttnCfg {
   static constexpr int TILE = 128 * HD * 2;  // one 128-row tile, HD/64 regions of 16 KB
   static constexpr int FWD_STAGES = HD == 128 ? 4 : 6;
   static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 4096 + 256;
+  static constexpr int FWD2_STAGES = HD == 128 ? 4 : 6;
+  static constexpr int FWD2_SMEM = 1024 + TILE * (2 + FWD2_STAGES) + 4096 + 256;
   // bwd: K, V, two {Q, dO, lse, D} stages, dS^T (128 x 128 bf16)
   static constexpr int BWD_QDO = 2 * TILE + 1024;
   // dQ staging for the TMA reduce-add: the dS^T buffer itself at head_dim 128 (dQ_i is drained after
@@ -375,6 +378,274 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_fwd_kernel(const __grid
       dst[v] = w;
     }
     if (slice == 0) p.lse[(static_cast<long long>(b) * p.nh + h) * p.S + qpos] = m_used + __log2f(lrow);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// Forward, two query tiles per CTA (flash_fwd2_kernel; FA4-style ping-pong): the CTA owns query
+// blocks 2p (tile A) and 2p + 1 (tile B) of one (sequence, head) and streams K_j / V_j once for both.
+// TMEM holds one S and one O per tile (S_A | S_B | O_A | O_B = 512 columns), so while the softmax
+// warps of one tile exponentiate S_t(j), the tensor pipe runs the other tile's P.V and next Q.K^T:
+//   S_A(0) S_B(0) | PV_A(0) S_A(1) | PV_B(0) S_B(1) | PV_A(1) S_A(2) | ...
+// Softmax: 8 warps per tile, 2 per TMEM lane quarter, each owning a 64-column half of the tile's
+// scores (two TMEM loads, one wait) and HD/2 columns of its O; row maxima and sums are combined
+// through shared memory with one 64-thread named barrier per quarter and block. Same arithmetic as
+// flash_fwd_kernel (packed fp32, lazy warp-uniform O rescale, 3/8 of the exponentials on the FMA
+// pipe). S_t(j+1) is issued after PV_t(j) (one S buffer per tile), so a tile's softmax waits one
+// P.V + Q.K^T; the other tile's fills the pipe meanwhile. LLaMA shapes (tools/attn_bench.py):
+// 8B 94 -> 89 us, 13B 69 -> 64 us, 1B 83 -> 70 us vs the one-tile kernel (PF_ATTN_FWD=1).
+template <int HD>
+__global__ void __launch_bounds__(kFwd2Threads, 1) flash_fwd2_kernel(const __grid_constant__ FwdParams p) {
+  using Cfg = AttnCfg<HD>;
+  constexpr int TILE = Cfg::TILE;
+  constexpr int ST = Cfg::FWD2_STAGES;
+  constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false, false);
+  constexpr uint32_t IDESC_O = idesc_bf16_f32(128, HD, false, true);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;  // tile A, tile B
+  uint8_t* sKV = smem + 2 * TILE;
+  float* red = reinterpret_cast<float*>(sKV + ST * TILE);  // [tile][2 bufs][2 halves][128 rows]
+  uint64_t* q_full = reinterpret_cast<uint64_t*>(red + 2 * 2 * 2 * 128);
+  uint64_t* kv_full = q_full + 1;
+  uint64_t* kv_empty = kv_full + ST;
+  uint64_t* s_full = kv_empty + ST;  // [tile]
+  uint64_t* p_full = s_full + 2;     // [tile]
+  uint64_t* o_bar = p_full + 2;      // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
+  const int lane = threadIdx.x & 31;
+  const int nbh = p.B * p.nh;
+  const int npair = (p.nqb + 1) >> 1;
+  const int bh = blockIdx.x % nbh;
+  const int pr = p.causal ? npair - 1 - static_cast<int>(blockIdx.x) / nbh : static_cast<int>(blockIdx.x) / nbh;
+  const int b = bh / p.nh, h = bh % p.nh, g = h / p.rep;
+  const int qbA = 2 * pr, qbB = 2 * pr + 1;
+  const bool hasB = qbB < p.nqb;
+  const int nA = p.causal ? qbA + 1 : p.nqb;
+  const int nB = hasB ? (p.causal ? qbB + 1 : p.nqb) : 0;
+  const int nmax = nA > nB ? nA : nB;
+  const int row0 = b * p.S;
+  const ProfClock pc{(p.prof & 1) != 0 && blockIdx.x == 0};
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 256);
+      mbar_init(&o_bar[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch(&p.tqkv);
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = warp_uniform(*tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(q_full, hasB ? 2 * TILE : TILE);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_2d(sQ + c * 16384, &p.tqkv, q_full, h * HD + c * 64, row0 + qbA * 128);
+        if (hasB) tma_load_2d(sQ + TILE + c * 16384, &p.tqkv, q_full, h * HD + c * 64, row0 + qbB * 128);
+      }
+      for (int u = 0; u < 2 * nmax; ++u) {
+        const int st = u % ST;
+        mbar_wait(&kv_empty[st], ((u / ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], TILE);
+        const int col = ((u & 1) ? (p.nh + p.nkv + g) : (p.nh + g)) * HD;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_2d(sKV + st * TILE + c * 16384, &p.tqkv, &kv_full[st], col + c * 64, row0 + (u >> 1) * 128);
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (warp-collective issue)
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint64_t qa0 = kmajor_base(smem_u32(sQ)), qa1 = kmajor_base(smem_u32(sQ + TILE));
+    auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T; K_j's stage is released by the last tile reading it
+      const int u = 2 * j, st = u % ST;
+      mbar_wait(&kv_full[st], (u / ST) & 1);
+      tc_fence_after();
+      const uint64_t kb = kmajor_base(smem_u32(sKV + st * TILE));
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_bf16_w(tmem + static_cast<uint32_t>(t * 128), kmajor_desc(t ? qa1 : qa0, k), kmajor_desc(kb, k), IDESC_S,
+                    k > 0 ? 1u : 0u);
+      umma_commit_w(&s_full[t]);
+      if (t == 1 || j >= nB) umma_commit_w(&kv_empty[st]);
+    };
+    const ProfClock pm{pc.on && lane == 0};
+    const long long tm0 = pm.now();
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P from TMEM over S_t
+      const long long t0 = pm.now();
+      mbar_wait(&p_full[t], j & 1);
+      pm.add(0, t0);
+      tc_fence_after();
+      const int u = 2 * j + 1, st = u % ST;
+      mbar_wait(&kv_full[st], (u / ST) & 1);
+      tc_fence_after();
+      const uint64_t vb = mnmajor_base(smem_u32(sKV + st * TILE));
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        umma_bf16_ts_w(tmem + 256 + static_cast<uint32_t>(t * 128), tmem + static_cast<uint32_t>(t * 128 + k * 8),
+                       mnmajor_desc(vb, k), IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
+      umma_commit_w(&o_bar[t]);
+      if (t == 1 || j >= nB) umma_commit_w(&kv_empty[st]);
+    };
+    if (nA > 0) issue_s(0, 0);
+    if (nB > 0) issue_s(1, 0);
+    for (int j = 0; j < nmax; ++j) {
+      if (j < nA) {
+        issue_pv(0, j);
+        if (j + 1 < nA) issue_s(0, j + 1);
+      }
+      if (j < nB) {
+        issue_pv(1, j);
+        if (j + 1 < nB) issue_s(1, j + 1);
+      }
+    }
+    pm.add(2, tm0);
+  } else {
+    // ------------------------------------------------------------------ softmax (8 warps per tile)
+    const int q4 = warp & 3;
+    const int sw = (warp - 2) >> 2;  // 0..3
+    const int t = sw >> 1;           // tile
+    const int e = sw & 1;            // 64-column half of the scores, HD/2 columns of O
+    const int n_t = t ? nB : nA;
+    const int qb = t ? qbB : qbA;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const uint32_t bar_id = 1 + t * 4 + q4;
+    const uint32_t s_col = tmem + lane_off + static_cast<uint32_t>(t * 128);
+    const uint32_t o_col = tmem + lane_off + static_cast<uint32_t>(256 + t * 128 + e * (HD / 2));
+    const float c = p.scale_log2;
+    float* redt = red + t * 512;
+    float m_used = 0.f, l = 0.f;
+    const ProfClock sp{pc.on && threadIdx.x == 64};
+    const long long ts0 = sp.now();
+    for (int j = 0; j < n_t; ++j) {
+      long long t0 = sp.now();
+      mbar_wait(&s_full[t], j & 1);
+      sp.add(3, t0);
+      t0 = sp.now();
+      tc_fence_after();
+      const bool diag = p.causal && j == qb;
+      // this warp's 64 scores of the row: two loads, one wait; partial maximum
+      uint32_t v[64];
+      tld<32>(s_col + e * 64, v);
+      tld<32>(s_col + e * 64 + 32, v + 32);
+      tmem_ld_wait();
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (e * 64 + i > r) v[i] = __float_as_uint(-INFINITY);
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8) {
+        mx[0] = max3f(mx[0], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        mx[1] = max3f(mx[1], __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        mx[2] = max3f(mx[2], __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+        mx[3] = max3f(mx[3], __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+      }
+      float* rb = redt + (j & 1) * 256;
+      rb[e * 128 + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      named_bar_sync(bar_id, 64);  // both halves' maxima are in; both halves' S reads are done
+      const float mrow = fmaxf(rb[r], rb[128 + r]) * c;
+      sp.add(4, t0);
+      t0 = sp.now();
+      if (j == 0) {
+        m_used = mrow;
+      } else if (__any_sync(0xffffffffu, mrow > m_used + kRescaleLog2)) {
+        mbar_wait(&o_bar[t], (j - 1) & 1);
+        tc_fence_after();
+        const float mn = fmaxf(m_used, mrow);
+        const float a = ex2_approx(m_used - mn);
+        l *= a;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD / 2; c0 += 16) {
+          uint32_t o[16];
+          tld<16>(o_col + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+          tst<16>(o_col + c0, o);
+        }
+        m_used = mn;
+      }
+      const float nm = -m_used;
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int q = hf * 32 + 2 * i;
+          const float2 x = fma2(make_float2(__uint_as_float(v[q]), __uint_as_float(v[q + 1])), make_float2(c, c),
+                                make_float2(nm, nm));
+          float2 ev;
+          if ((i % 8) == 2 || (i % 8) == 5 || (i % 8) == 7) ev = ex2_poly2(x);
+          else ev = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          ls2[i & 1] = add2(ls2[i & 1], ev);
+          pk[i] = pack_bf16x2(ev.x, ev.y);
+        }
+        tst<16>(s_col + e * 32 + hf * 16, pk);  // P (bf16 pairs) over S, after the barrier
+      }
+      l += (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+      sp.add(7, t0);
+    }
+    sp.add(5, ts0);
+    if (n_t > 0) {
+      // ---------------------------------------------------------------- epilogue of tile t: O / l, LSE
+      float* rs = redt + (n_t & 1) * 256;  // the buffer block n_t - 1 did not use
+      rs[e * 128 + r] = l;
+      named_bar_sync(bar_id, 64);
+      const float lrow = rs[r] + rs[128 + r];
+      mbar_wait(&o_bar[t], (n_t - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / lrow;
+      const int qpos = qb * 128 + r;
+      __nv_bfloat16* orow = p.out + static_cast<long long>(row0 + qpos) * p.ldo + h * HD + e * (HD / 2);
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD / 2; c0 += 16) {
+        uint32_t o[16];
+        tld<16>(o_col + c0, o);
+        tmem_ld_wait();
+        uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+        for (int vv = 0; vv < 2; ++vv) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(o[8 * vv + 0]) * inv, __uint_as_float(o[8 * vv + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(o[8 * vv + 2]) * inv, __uint_as_float(o[8 * vv + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(o[8 * vv + 4]) * inv, __uint_as_float(o[8 * vv + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(o[8 * vv + 6]) * inv, __uint_as_float(o[8 * vv + 7]) * inv);
+          dst[vv] = w;
+        }
+      }
+      if (e == 0) p.lse[(static_cast<long long>(b) * p.nh + h) * p.S + qpos] = m_used + __log2f(lrow);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -878,6 +1149,15 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloa
   }
 }
 
+// PF_ATTN_FWD=1: the one-tile forward (flash_fwd_kernel) instead of the two-tile ping-pong (A/B)
+bool fwd_one_tile() {
+  static const bool one = [] {
+    const char* e = std::getenv("PF_ATTN_FWD");
+    return e && e[0] == '1';
+  }();
+  return one;
+}
+
 int attn_prof_enabled() {
   static const int on = [] {
     const char* e = std::getenv("PF_ATTN_PROF");
@@ -906,14 +1186,19 @@ int fwd_impl(const __nv_bfloat16* qkv, __nv_bfloat16* out, long long ldo, float*
   p.causal = causal ? 1 : 0;
   p.prof = attn_prof_enabled();
   p.scale_log2 = scale * 1.4426950408889634f;
-  auto kern = flash_fwd_kernel<HD>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::FWD_SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(flash_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::FWD_SMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(flash_fwd2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::FWD2_SMEM) !=
+            cudaSuccess)
       return PF_ERR_CUDA;
     attr = true;
   }
-  launch_k(kern, dim3(B * nh * p.nqb), dim3(kAttnThreads), Cfg::FWD_SMEM, s, p);
+  if (fwd_one_tile())
+    launch_k(flash_fwd_kernel<HD>, dim3(B * nh * p.nqb), dim3(kAttnThreads), Cfg::FWD_SMEM, s, p);
+  else
+    launch_k(flash_fwd2_kernel<HD>, dim3(B * nh * ((p.nqb + 1) / 2)), dim3(kFwd2Threads), Cfg::FWD2_SMEM, s, p);
   return status();
 }
 
