@@ -101,6 +101,7 @@ struct AttnCfg {
   static constexpr int TILE = 128 * HD * 2;  // one 128-row tile, HD/64 regions of 16 KB
   static constexpr int FWD_STAGES = HD == 128 ? 4 : 6;
   static constexpr int FWD_SMEM = 1024 + TILE * (1 + FWD_STAGES) + 4096 + 256;
+  static constexpr int BWDQ_SMEM = 1024 + TILE * 6 + 1024 + 256;  // Q, dO, 2 x {K, V}, lse / D, barriers
   static constexpr int FWD2_STAGES = HD == 128 ? 4 : 6;
   static constexpr int FWD2_SMEM = 1024 + TILE * (2 + FWD2_STAGES) + 4096 + 256;
   // bwd: K, V, two {Q, dO, lse, D} stages, dS^T (128 x 128 bf16)
@@ -671,9 +672,11 @@ __global__ void flash_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, cons
     float acc = 0.f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc = fmaf(o[e], d[e], acc);
-    float4* z = reinterpret_cast<float4*>(dq_acc + off);
-    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dq_acc) {  // the fused dQ path accumulates into it (the separate dQ kernel stores it whole)
+      float4* z = reinterpret_cast<float4*>(dq_acc + off);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 #pragma unroll
     for (int o2 = TPR / 2; o2 > 0; o2 >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2, TPR);
     if (part == 0) {
@@ -716,8 +719,8 @@ __device__ __forceinline__ void bwd_half(const uint32_t* sr, const uint32_t* dr,
   }
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_constant__ BwdParams p) {
+template <int HD, bool SEP>
+__global__ void __launch_bounds__(SEP ? kAttnThreads : kBwdThreads, 1) flash_bwd_kernel(const __grid_constant__ BwdParams p) {
   using Cfg = AttnCfg<HD>;
   constexpr int TILE = Cfg::TILE;
   constexpr uint32_t IDESC_SS = idesc_bf16_f32(128, 128, false, false);  // S^T, dP^T
@@ -845,7 +848,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16_w(tmem + S_COL, kmajor_desc(ka, k), kmajor_desc(qa, k), IDESC_SS, k > 0 ? 1u : 0u);
-        if (!DQ_OWN && it > 0) {  // dQ_{it-1} (in the dP columns) has been drained
+        if (!SEP && !DQ_OWN && it > 0) {  // dQ_{it-1} (in the dP columns) has been drained
           t0 = pm.now();
           mbar_wait(dq_empty, (it - 1) & 1);
           pm.add(9, t0);
@@ -867,24 +870,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           umma_bf16_w(tmem + DK_COL, kmajor_desc(dsa_k, k), mnmajor_desc(qa_mn, k), IDESC_TS, (it > 0 || k > 0) ? 1u : 0u);
-        if (DQ_OWN && it > 0) {  // dQ_{it-1} has been drained from its own columns
-          mbar_wait(dq_empty, (it - 1) & 1);
-          tc_fence_after();
-        }
-        // dQ_i = dS K_j
+        if constexpr (!SEP) {
+          if (DQ_OWN && it > 0) {  // dQ_{it-1} has been drained from its own columns
+            mbar_wait(dq_empty, (it - 1) & 1);
+            tc_fence_after();
+          }
+          // dQ_i = dS K_j
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if constexpr (DQ_T)
-            umma_bf16_w(tmem + DQ_COL, mnmajor_desc(ka_mn, k), mnmajor_desc(dsa, k), IDESC_DQT, k > 0 ? 1u : 0u);
-          else
-            umma_bf16_w(tmem + DQ_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka_mn, k), IDESC_DQ, k > 0 ? 1u : 0u);
+          for (int k = 0; k < 8; ++k)
+            if constexpr (DQ_T)
+              umma_bf16_w(tmem + DQ_COL, mnmajor_desc(ka_mn, k), mnmajor_desc(dsa, k), IDESC_DQT, k > 0 ? 1u : 0u);
+            else
+              umma_bf16_w(tmem + DQ_COL, mnmajor_desc(dsa, k), mnmajor_desc(ka_mn, k), IDESC_DQ, k > 0 ? 1u : 0u);
+        }
         umma_commit_w(&qdo_empty[st]);
-        umma_commit_w(dq_full);
+        if constexpr (!SEP) umma_commit_w(dq_full);
       }
       pm.add(11, tm0);
       umma_commit_w(dkv_full);
     }
-  } else if (warp >= 2 + kSoftWarps) {
+  } else if (!SEP && warp >= 2 + kSoftWarps) {
     // ------------------------------------------------------------------ dQ drain (4 warps)
     // one warp per TMEM lane quarter: rows = queries of block i; tcgen05.ld of dQ_i, the columns
     // handed back (dq_empty) before the fp32 reductions into the accumulator, which overlap the next
@@ -1113,6 +1118,205 @@ __global__ void __launch_bounds__(kBwdThreads, 1) flash_bwd_kernel(const __grid_
 
 // dq = scale * dQ_acc with the RoPE backward, bf16 into dqkv's q columns. One thread per
 // (token, head, pair d < HD/2).
+// dQ without atomics (flash_bwd_q_kernel, PF_ATTN_BWD=2; run before the dK / dV kernel, which then
+// has no dQ work): one CTA per (sequence, head, 128-query block) loops over the key blocks the queries see,
+// recomputing S = Q K_j^T and dP = dO V_j^T (TMEM: S in two buffers | dP | dQ), P = 2^(S c - LSE),
+// dS = P (dP - D) as bf16 over S, and dQ += dS K_j with A = dS from TMEM. dQ stays in TMEM for the
+// whole loop and leaves once, unscaled fp32, into dq_acc (plain stores: the CTA owns its rows);
+// flash_bwd_dq_kernel scales it, applies the RoPE backward and writes dq into dqkv after the dK / dV
+// kernel has consumed q. S(j + 2) reuses S(j)'s buffer after dQ(j) read dS(j); dP(j + 1) follows
+// the softmax's read of dP(j). The softmax warps (4 per TMEM lane quarter, lane = query row, 32
+// key columns each) write dS over the first 16 of their own 32 S columns: no cross-warp hazard.
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __grid_constant__ BwdParams p) {
+  using Cfg = AttnCfg<HD>;
+  constexpr int TILE = Cfg::TILE;
+  constexpr uint32_t IDESC_SS = idesc_bf16_f32(128, 128, false, false);  // S, dP: A (Q, dO) and B (K, V) K-major
+  constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, HD, false, true);    // dQ: A = dS in TMEM, B = K_j MN-major
+  constexpr uint32_t DP_COL = 256, DQ_COL = 384;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sDO = smem + TILE;
+  uint8_t* sKV = smem + 2 * TILE;  // 2 stages of {K_j, V_j}
+  float* sLD = reinterpret_cast<float*>(sKV + 4 * TILE);  // lse[128], D[128]
+  uint64_t* qd_full = reinterpret_cast<uint64_t*>(sLD + 256);
+  uint64_t* kv_full = qd_full + 1;   // [2]
+  uint64_t* kv_empty = kv_full + 2;  // [2]
+  uint64_t* s_full = kv_empty + 2;   // [2] per S buffer
+  uint64_t* dp_full = s_full + 2;
+  uint64_t* p_full = dp_full + 1;
+  uint64_t* dq_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
+  const int lane = threadIdx.x & 31;
+  const int nbh = p.B * p.nh;
+  const int bh = blockIdx.x % nbh;
+  const int i = p.causal ? p.nqb - 1 - static_cast<int>(blockIdx.x) / nbh : static_cast<int>(blockIdx.x) / nbh;
+  const int b = bh / p.nh, h = bh % p.nh, g = h / p.rep;
+  const int nblk = p.causal ? i + 1 : p.nqb;
+  const int row0 = b * p.S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qd_full, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init(&kv_full[s2], 1);
+      mbar_init(&kv_empty[s2], 1);
+      mbar_init(&s_full[s2], 1);
+    }
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, kSoftThreads);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tqkv);
+    tma_prefetch(&p.tdo);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = warp_uniform(*tmem_slot);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(qd_full, 2 * TILE + 1024);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_2d(sQ + c * 16384, &p.tqkv, qd_full, h * HD + c * 64, row0 + i * 128);
+        tma_load_2d(sDO + c * 16384, &p.tdo, qd_full, h * HD + c * 64, row0 + i * 128);
+      }
+      const long long li = (static_cast<long long>(b) * p.nh + h) * p.S + i * 128;
+      bulk_load_1d(sLD, p.lse + li, 512, qd_full);
+      bulk_load_1d(sLD + 128, p.D + li, 512, qd_full);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * TILE);
+        uint8_t* base = sKV + st * 2 * TILE;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_2d(base + c * 16384, &p.tqkv, &kv_full[st], (p.nh + g) * HD + c * 64, row0 + j * 128);
+          tma_load_2d(base + TILE + c * 16384, &p.tqkv, &kv_full[st], (p.nh + p.nkv + g) * HD + c * 64,
+                      row0 + j * 128);
+        }
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (warp-collective issue)
+    mbar_wait(qd_full, 0);
+    tc_fence_after();
+    const uint64_t qa = kmajor_base(smem_u32(sQ)), da = kmajor_base(smem_u32(sDO));
+    auto issue_s = [&](int j) {
+      const int st = j & 1;
+      mbar_wait(&kv_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t kb = kmajor_base(smem_u32(sKV + st * 2 * TILE));
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_bf16_w(tmem + static_cast<uint32_t>(st * 128), kmajor_desc(qa, k), kmajor_desc(kb, k), IDESC_SS,
+                    k > 0 ? 1u : 0u);
+      umma_commit_w(&s_full[st]);
+    };
+    auto issue_dp = [&](int j) {
+      const int st = j & 1;
+      mbar_wait(&kv_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t vb = kmajor_base(smem_u32(sKV + st * 2 * TILE + TILE));
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_bf16_w(tmem + DP_COL, kmajor_desc(da, k), kmajor_desc(vb, k), IDESC_SS, k > 0 ? 1u : 0u);
+      umma_commit_w(dp_full);
+    };
+    issue_s(0);
+    issue_dp(0);
+    if (nblk > 1) issue_s(1);
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j & 1;
+      mbar_wait(p_full, j & 1);  // dS(j) is in TMEM over S(j); dP(j) has been read
+      tc_fence_after();
+      // dQ += dS(j) K_j: 16 keys per k-step, key slice kk / 2's first 16 columns of S(j)
+      const uint64_t kb_mn = mnmajor_base(smem_u32(sKV + st * 2 * TILE));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_bf16_ts_w(tmem + DQ_COL, tmem + static_cast<uint32_t>(st * 128 + (kk >> 1) * 32 + (kk & 1) * 8),
+                       mnmajor_desc(kb_mn, kk), IDESC_DQ, (j > 0 || kk > 0) ? 1u : 0u);
+      umma_commit_w(&kv_empty[st]);  // K_j, V_j: dP(j) and dQ(j) were their last readers
+      if (j + 1 < nblk) issue_dp(j + 1);
+      if (j + 2 < nblk) issue_s(j + 2);
+    }
+    umma_commit_w(dq_done);
+  } else {
+    // ------------------------------------------------------------------ softmax (16 warps)
+    const int q4 = warp & 3;
+    const int slice = (warp - 2) >> 2;
+    const int r = q4 * 32 + lane;  // query row
+    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    const float c = p.scale_log2;
+    mbar_wait(qd_full, 0);
+    const float2 nl = make_float2(-sLD[r], -sLD[r]);
+    const float2 nd = make_float2(-sLD[128 + r], -sLD[128 + r]);
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tld<32>(tmem + lane_off + static_cast<uint32_t>(st * 128 + slice * 32), sr);
+      tld<32>(tmem + lane_off + DP_COL + static_cast<uint32_t>(slice * 32), dr);
+      tmem_ld_wait();
+      const bool diag = p.causal && j == i;
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
+                              make_float2(c, c), nl);
+        float2 pv;
+        if ((e % 8) == 2 || (e % 8) == 5 || (e % 8) == 7) pv = ex2_poly2(x);
+        else pv = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        if (diag) {  // key after query
+          if (slice * 32 + 2 * e > r) pv.x = 0.f;
+          if (slice * 32 + 2 * e + 1 > r) pv.y = 0.f;
+        }
+        const float2 ds = mul2(pv, add2(make_float2(__uint_as_float(dr[2 * e]), __uint_as_float(dr[2 * e + 1])), nd));
+        pk[e] = pack_bf16x2(ds.x, ds.y);
+      }
+      tst<16>(tmem + lane_off + static_cast<uint32_t>(st * 128 + slice * 32), pk);  // dS over this slice's S
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    // ---------------------------------------------------------------- dQ (unscaled fp32) -> dq_acc
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    constexpr int QC = HD / 4;
+    float* dst = p.dq_acc + static_cast<long long>(row0 + i * 128 + r) * (p.nh * HD) + h * HD + slice * QC;
+#pragma unroll
+    for (int c0 = 0; c0 < QC; c0 += 16) {
+      uint32_t v[16];
+      tld<16>(tmem + lane_off + DQ_COL + static_cast<uint32_t>(slice * QC + c0), v);
+      tmem_ld_wait();
+      float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        d4[u] = make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]), __uint_as_float(v[4 * u + 2]),
+                            __uint_as_float(v[4 * u + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 template <int HD>
 __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, long long ldq,
                                     const float2* __restrict__ rope, int T, int S, int nh, float scale) {
@@ -1147,6 +1351,19 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloa
     *reinterpret_cast<uint2*>(dst + d4) = make_uint2(pack_bf16x2(oa[0], oa[1]), pack_bf16x2(oa[2], oa[3]));
     *reinterpret_cast<uint2*>(dst + HALF + d4) = make_uint2(pack_bf16x2(ob[0], ob[1]), pack_bf16x2(ob[2], ob[3]));
   }
+}
+
+// PF_ATTN_BWD=2: the separate dQ kernel (flash_bwd_q_kernel, no fp32 atomics) + the dK / dV kernel
+// without dQ, instead of the default dK / dV / dQ kernel with fp32 reductions. Measured slower at the
+// LLaMA shapes (8B: 149 + 185 us + 35 us of pre / convert vs 335-340 us; both kernels ~40% tensor
+// active: S / dP -> softmax -> MMA stays serial in each), kept for A/B
+// (profiles/r2_attention_experiments.md).
+bool bwd_fused_dq() {
+  static const bool fused = [] {
+    const char* e = std::getenv("PF_ATTN_BWD");
+    return !(e && e[0] == '2');
+  }();
+  return fused;
 }
 
 // PF_ATTN_FWD=1: the one-tile forward (flash_fwd_kernel) instead of the two-tile ping-pong (A/B)
@@ -1208,8 +1425,9 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
              float scale, bool causal, cudaStream_t s) {
   using Cfg = AttnCfg<HD>;
   const int T = B * S;
+  const bool sep = !bwd_fused_dq();
   launch_k(flash_bwd_pre_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh * (HD / 8) / 256 + 1)), dim3(256), 0, s,
-           out, dout, D, dq_acc, T, S, nh);
+           out, dout, D, sep ? nullptr : dq_acc, T, S, nh);
   int rc = status();
   if (rc) return rc;
   BwdParams p{};
@@ -1235,14 +1453,25 @@ int bwd_impl(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bflo
   p.prof = attn_prof_enabled();
   p.scale_log2 = scale * 1.4426950408889634f;
   p.scale = scale;
-  auto kern = flash_bwd_kernel<HD>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BWD_SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(flash_bwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::BWD_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(flash_bwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::BWD_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(flash_bwd_q_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::BWDQ_SMEM) !=
+            cudaSuccess)
       return PF_ERR_CUDA;
     attr = true;
   }
-  launch_k(kern, dim3(B * nkv * p.nqb), dim3(kBwdThreads), Cfg::BWD_SMEM, s, p);
+  if (sep) {
+    // dQ first (it reads k / v, which the dK / dV kernel overwrites in place), then dK / dV
+    launch_k(flash_bwd_q_kernel<HD>, dim3(B * nh * p.nqb), dim3(kAttnThreads), Cfg::BWDQ_SMEM, s, p);
+    if ((rc = status())) return rc;
+    launch_k(flash_bwd_kernel<HD, true>, dim3(B * nkv * p.nqb), dim3(kAttnThreads), Cfg::BWD_SMEM, s, p);
+  } else {
+    launch_k(flash_bwd_kernel<HD, false>, dim3(B * nkv * p.nqb), dim3(kBwdThreads), Cfg::BWD_SMEM, s, p);
+  }
   if ((rc = status())) return rc;
   launch_k(flash_bwd_dq_kernel<HD>, dim3(grid_for(static_cast<long long>(T) * nh * HD / 8 / 256 + 1)), dim3(256), 0, s,
            dq_acc, dqkv, W, rope, T, S, nh, scale);

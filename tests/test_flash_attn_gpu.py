@@ -195,3 +195,50 @@ def test_flash_forward_lane_divergent_rescale(cuda, hd, causal):
         s = s.masked_fill(torch.ones(S, S, dtype=torch.bool, device=cuda).triu(1), float("-inf"))
     lse_ref = torch.logsumexp(s, -1) / np.log(2.0)
     assert (lse - lse_ref).abs().max().item() <= 1e-3 * max(1.0, lse_ref.abs().max().item())
+
+
+_BWD_PATH_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2602_05754_b200 import _native
+lib = _native.device()
+B, S, nh, nkv, hd = 2, 512, 8, 2, {hd}
+T, W = B * S, (nh + 2 * nkv) * hd
+g = torch.Generator().manual_seed(3)
+qkv = torch.randn(T, W, generator=g).bfloat16().cuda()
+dout = (torch.randn(T, nh * hd, generator=g) * 0.1).bfloat16().cuda()
+out = torch.empty(T, nh * hd, dtype=torch.bfloat16, device='cuda')
+lse = torch.empty(B, nh, S, device='cuda')
+st = torch.cuda.current_stream().cuda_stream
+assert lib.pf_flash_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), B, S, nh, nkv, hd, hd ** -0.5, 1, st) == 0
+d = torch.empty_like(qkv)
+assert lib.pf_flash_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), d.data_ptr(), B, S, nh, nkv,
+                             hd, hd ** -0.5, 1, 500000.0, st) == 0
+torch.cuda.synchronize()
+np.save(sys.argv[1], d.float().cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("hd", [128, 64])
+def test_flash_backward_separate_dq_matches_fused(cuda, tmp_path, hd):
+    """PF_ATTN_BWD=2 computes dQ in its own kernel (no fp32 atomics) before the dK / dV kernel; the
+    default keeps dQ inside the dK / dV kernel. dk / dv come from the same code (bitwise equal); dq
+    differs only by fp32 summation order."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("2", "1"):
+        f = tmp_path / f"d{mode}.npy"
+        env = dict(os.environ, PF_ATTN_BWD=mode)
+        subprocess.run([sys.executable, "-c", _BWD_PATH_SNIPPET.replace("{hd}", str(hd)), str(f)], cwd=root, env=env,
+                       check=True, timeout=300)
+        outs[mode] = np.load(f)
+    nh, nkv = 8, 2
+    a = outs["2"].reshape(outs["2"].shape[0], nh + 2 * nkv, hd)
+    b = outs["1"].reshape(a.shape)
+    assert np.array_equal(a[:, nh:], b[:, nh:])
+    dq_a, dq_b = a[:, :nh], b[:, :nh]
+    assert np.linalg.norm(dq_a - dq_b) <= 1e-2 * np.linalg.norm(dq_b)
