@@ -59,6 +59,12 @@ int pf_gemm_dw_rowpairs(const void* dY, long long ldy, const void* X, long long 
                         int N, int K, const int* entries, const int* entry_count, int* unit_stamp, int stamp_offset,
                         int stamp, void* stream);
 
+/* K3 of a cell with no frozen unit (the stage engine's dense fast path): every unit of the matrix
+ * as 256 x 256 CTA-pair tiles (cta_group::2, two unit rows x two unit columns), no work list;
+ * same unit-stamp contract (first touch in a step stores, later ones accumulate). */
+int pf_gemm_dw_dense(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                     int N, int K, int* unit_stamp, int stamp_offset, int stamp, void* stream);
+
 /* K1 gate|up projection with the SwiGLU activation fused in the CTA-pair epilogue:
  * gu[T, 2*ffn] = h[T, K] . Wgu^T (bf16, Wgu rows interleave 128-blocks [gate b | up b]),
  * a[T, ffn] = silu(gate) * up from the bf16-rounded gu (== pf_swiglu_fwd(gu)). ffn % 128 == 0. */

@@ -75,6 +75,8 @@ def device() -> ctypes.CDLL:
                                            c_vp, c_int, c_int, c_vp])
             _sig(lib, "pf_gemm_dw_rowpairs", [c_vp, c_ll, c_vp, c_ll, c_vp, c_ll, c_int, c_int, c_int, c_vp, c_vp,
                                               c_vp, c_int, c_int, c_vp])
+            _sig(lib, "pf_gemm_dw_dense", [c_vp, c_ll, c_vp, c_ll, c_vp, c_ll, c_int, c_int, c_int, c_vp, c_int,
+                                           c_int, c_vp])
             _sig(lib, "pf_device_sm_count", [], c_int)
             _sig(lib, "pf_device_last_error", [], c_cp)
             from . import _device_sigs

@@ -52,6 +52,13 @@ int pf_gemm_dw_pairs(const void* dY, long long ldy, const void* X, long long ldx
   return record(pf::gemm_dw_pairs(&it, 1, unit_stamp, stamp, static_cast<cudaStream_t>(stream)));
 }
 
+int pf_gemm_dw_dense(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
+                     int N, int K, int* unit_stamp, int stamp_offset, int stamp, void* stream) {
+  if (!dY || !X || !G) return PF_ERR_INVALID;
+  pf::DwGemm it{dY, ldy, X, ldx, G, ldg, M, N, K, nullptr, nullptr, stamp_offset};
+  return record(pf::gemm_dw_dense(&it, 1, unit_stamp, stamp, static_cast<cudaStream_t>(stream)));
+}
+
 int pf_gemm_dw_rowpairs(const void* dY, long long ldy, const void* X, long long ldx, float* G, long long ldg, int M,
                         int N, int K, const int* entries, const int* entry_count, int* unit_stamp, int stamp_offset,
                         int stamp, void* stream) {

@@ -312,6 +312,237 @@ int max_dw_clusters() {
   return n;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Dense cells (gemm_dw_dense): a microbatch cell with no frozen unit -- the LP's plans are mostly
+// 0 / 1 per cell -- needs every unit of every matrix, so its dW runs as whole 256 x 256 CTA-pair
+// tiles (tcgen05.mma.cta_group::2, M = 256 = unit rows 2i, 2i + 1, one per CTA; N = 256 = unit
+// columns 2j, 2j + 1, split across the pair's shared memory). Per SM and 16-token k-step the MMA
+// reads 4 KB of A and 4 KB of its B half for 128 x 256 x 16 of work: the operand reuse of the
+// forward / dX GEMMs, against 4 + 8 KB for the 1-CTA row-pair tile (shared-memory bound at ~0.67
+// of the tensor pipe in the dense 8B launches, profiles/r2_bench_launches_fullstep.md). Edge
+// units past M / N read TMA zero fill and are skipped by the epilogue. Same unit-stamp contract.
+constexpr int Q_STAGES = 6;
+constexpr int QB_BYTES = 128 * BK * 2;  // this CTA's 128 of the tile's 256 X columns
+constexpr int Q_STAGE_BYTES = A_BYTES + QB_BYTES;
+constexpr int Q_SMEM_BYTES = 1024 + Q_STAGES * Q_STAGE_BYTES + 1024;
+constexpr uint32_t IDESC_Q = idesc_bf16_f32(256, 256, true, true);
+
+struct DenseParams {
+  DwProblem prob[kMaxDwProblems];
+  int prefix[kMaxDwProblems + 1];  // first quad of problem i (host-computed)
+  unsigned char rows_fast[kMaxDwProblems];
+  int nprob;
+  int* unit_stamp;
+  int stamp;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_dw_quad_kernel(const __grid_constant__ DenseParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Q_STAGES * A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Q_STAGES * Q_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Q_STAGES;
+  uint64_t* tfull_bar = empty_bar + Q_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+  const int total = p.prefix[p.nprob];
+
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Q_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 2 * 32 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc_pair(tmem_slot, 512);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = warp_uniform(*tmem_slot);
+
+  // quad t -> (problem, unit row pair, unit column pair)
+  auto quad = [&](int t, int& pi, int& mrow, int& mcol) {
+    int lo = 0, hi = p.nprob - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.prefix[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    pi = lo;
+    const int q = t - p.prefix[pi];
+    if (p.rows_fast[pi]) {  // dY (T x M) is the smaller operand: sweep the unit-row pairs of a column
+      const int qm = (((p.prob[pi].M + 127) >> 7) + 1) >> 1;  // pair first, so X streams from DRAM once
+      mcol = q / qm;
+      mrow = q - mcol * qm;
+    } else {
+      const int qn = (p.prob[pi].tiles_n + 1) >> 1;
+      mrow = q / qn;
+      mcol = q - mrow * qn;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < total; t += nclusters) {
+        int pi, mrow, mcol;
+        quad(t, pi, mrow, mcol);
+        const DwProblem& pr = p.prob[pi];
+        const int mb = 2 * mrow + static_cast<int>(rank);
+        const int nb = 2 * mcol + static_cast<int>(rank);
+        const int num_kb = (pr.K + BK - 1) / BK;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Q_STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * QB_BYTES;
+          tma_load_2d_pair(a_dst, &pr.ta, &full_bar[stage], mb * 128, kb * BK);
+          tma_load_2d_pair(a_dst + 8192, &pr.ta, &full_bar[stage], mb * 128 + 64, kb * BK);
+          tma_load_2d_pair(b_dst, &pr.tb, &full_bar[stage], nb * 128, kb * BK);
+          tma_load_2d_pair(b_dst + 8192, &pr.tb, &full_bar[stage], nb * 128 + 64, kb * BK);
+          if (++stage == Q_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      pdl_trigger();
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ---------------------------------------------------------- MMA issuer (leader CTA)
+      int stage = 0;
+      uint32_t phase = 0;
+      int abuf = 0;
+      uint32_t aphase = 0;
+      for (int t = cluster; t < total; t += nclusters) {
+        int pi, mrow, mcol;
+        quad(t, pi, mrow, mcol);
+        const int num_kb = static_cast<int>(warp_uniform((p.prob[pi].K + BK - 1) / BK));
+        mbar_wait(&tempty_bar[abuf], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * 256);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * QB_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc = sdesc_sw128(a_base + k * 2048, 8192, 1024);
+            const uint64_t bdesc = sdesc_sw128(b_base + k * 2048, 8192, 1024);
+            umma_bf16_pair_w(d_tmem, adesc, bdesc, IDESC_Q, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_pair_multicast_w(&empty_bar[stage], 0x3);
+          if (++stage == Q_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair_multicast_w(&tfull_bar[abuf], 0x3);
+        abuf ^= 1;
+        if (abuf == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs): this CTA's
+    // unit row, units (mb, 2 mcol) and (mb, 2 mcol + 1)
+    const int q = warp & 3;
+    const int row = q * 32 + static_cast<int>(lane);
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
+    int abuf = 0;
+    uint32_t aphase = 0;
+    for (int t = cluster; t < total; t += nclusters) {
+      int pi, mrow, mcol;
+      quad(t, pi, mrow, mcol);
+      const DwProblem& pr = p.prob[pi];
+      const int mb = 2 * mrow + static_cast<int>(rank);
+      const int tiles_m = (pr.M + 127) >> 7;
+      const bool row_unit = mb < tiles_m;
+      const int nb0 = 2 * mcol;
+      const bool has1 = nb0 + 1 < pr.tiles_n;
+      const int u0 = mb * pr.tiles_n + nb0;
+      const bool first0 = row_unit && __ldcg(p.unit_stamp + pr.stamp_offset + u0) != p.stamp;
+      const bool first1 = row_unit && has1 && __ldcg(p.unit_stamp + pr.stamp_offset + u0 + 1) != p.stamp;
+      mbar_wait(&tfull_bar[abuf], aphase);
+      tc_fence_after();
+      const long long grow = static_cast<long long>(mb) * 128 + row;
+      const bool row_ok = row_unit && grow < pr.M;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        if (c >= 4 && !has1) break;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(abuf * 256 + c * 32),
+                           r);
+        tmem_ld_wait();
+        const int gcol = nb0 * 128 + c * 32;
+        const bool first = c < 4 ? first0 : first1;
+        if (!row_ok || gcol >= pr.N) continue;
+        float* cp = pr.C + grow * pr.ldc + gcol;
+        if (gcol + 32 <= pr.N) {
+          float4* c4 = reinterpret_cast<float4*>(cp);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 w = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                                   __uint_as_float(r[4 * j + 3]));
+            if (!first) {
+              const float4 o = c4[j];
+              w.x += o.x;
+              w.y += o.y;
+              w.z += o.z;
+              w.w += o.w;
+            }
+            c4[j] = w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (gcol + i < pr.N) cp[i] = first ? __uint_as_float(r[i]) : cp[i] + __uint_as_float(r[i]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
+      if (row_unit) {
+        named_bar_sync(1, 32 * kEpiWarps);
+        if (threadIdx.x == 64) {
+          p.unit_stamp[pr.stamp_offset + u0] = p.stamp;
+          if (has1) p.unit_stamp[pr.stamp_offset + u0 + 1] = p.stamp;
+        }
+      }
+      abuf ^= 1;
+      if (abuf == 0) aphase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
 }  // namespace
 
 int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream) {
@@ -352,6 +583,48 @@ int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaSt
     const int clusters = static_cast<int>(std::min<long long>(max_pairs, max_dw_clusters()));
     if (clusters <= 0) continue;
     launch_k(gemm_dw_pair_kernel, dim3(2 * clusters), dim3(kThreads), SMEM_BYTES, stream, p);
+    count_launch();
+    if (cudaPeekAtLastError() != cudaSuccess) return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
+int gemm_dw_dense(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream) {
+  if (n < 0 || unit_stamp == nullptr) return PF_ERR_INVALID;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_dw_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM_BYTES) !=
+        cudaSuccess)
+      return PF_ERR_CUDA;
+    attr_set = true;
+  }
+  for (int base = 0; base < n; base += kMaxDwProblems) {
+    const int cnt = std::min(kMaxDwProblems, n - base);
+    DenseParams p{};
+    p.nprob = cnt;
+    p.unit_stamp = unit_stamp;
+    p.stamp = stamp;
+    p.prefix[0] = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const DwGemm& it = items[base + i];
+      if (it.M <= 0 || it.N <= 0 || it.K <= 0 || (it.K % 8) != 0 || !it.C) return PF_ERR_INVALID;
+      DwProblem& pr = p.prob[i];
+      if (int rc = tma_desc_bf16_2d(&pr.ta, it.dy, it.K, it.M, it.ldy, 64, 64)) return rc;
+      if (int rc = tma_desc_bf16_2d(&pr.tb, it.x, it.K, it.N, it.ldx, 64, 64)) return rc;
+      pr.C = it.C;
+      pr.ldc = it.ldc;
+      pr.M = it.M;
+      pr.N = it.N;
+      pr.K = it.K;
+      pr.tiles_n = (it.N + 127) / 128;
+      pr.stamp_offset = it.stamp_offset;
+      const int tiles_m = (it.M + 127) / 128;
+      p.prefix[i + 1] = p.prefix[i] + ((tiles_m + 1) / 2) * ((pr.tiles_n + 1) / 2);
+      p.rows_fast[i] = it.M <= it.N ? 1 : 0;
+    }
+    const int clusters = std::min(p.prefix[cnt], num_sms() / 2);
+    if (clusters <= 0) continue;
+    launch_k(gemm_dw_quad_kernel, dim3(2 * clusters), dim3(kThreads), Q_SMEM_BYTES, stream, p);
     count_launch();
     if (cudaPeekAtLastError() != cudaSuccess) return PF_ERR_CUDA;
   }

@@ -74,6 +74,9 @@ int gemm_dw_units(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaSt
 int gemm_dw_pairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
 // 1-CTA 128 x 256 tiles over K5r row-pair lists: two units of one row per MMA (gemm_dw_rows.cu)
 int gemm_dw_rowpairs(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
+// Every unit of every matrix (a cell with no frozen unit): 256 x 256 CTA-pair tiles, list-free
+// (gemm_dw.cu); same unit-stamp contract.
+int gemm_dw_dense(const DwGemm* items, int n, int* unit_stamp, int stamp, cudaStream_t stream);
 
 // K1/K2 on a CTA pair (cta_group::2, 256 x 256 tiles); A must be K-major.
 int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C, int M, int N, int K, float alpha,

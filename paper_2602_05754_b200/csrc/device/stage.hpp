@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -132,6 +133,10 @@ class Stage {
 
   int units() const { return total_units_; }
   int words() const { return (total_units_ + 63) / 64; }
+  // The next dW (backward / backward_weight) is of a cell with no frozen unit: every matrix runs as
+  // whole CTA-pair tiles (gemm_dw_dense) instead of over the K5r lists. Set by the trainer from the
+  // host copy of the cell's mask; PF_DW_DENSE=0 turns the fast path off.
+  void set_dense_cell(bool dense) { dense_cell_ = dense && dense_allowed(); }
   long long param_count() const { return n_params_; }
   long long unit_param_count() const { return n_unit_params_; }
   const std::vector<UnitMatrix>& unit_matrices() const { return mats_; }
@@ -170,6 +175,7 @@ class Stage {
   // K3 over every item in one launch
   int run_dw(const std::vector<DwGemm>& items, int stamp, cudaStream_t s) {
     const int n = static_cast<int>(items.size());
+    if (dense_cell_) return gemm_dw_dense(items.data(), n, stamps_, stamp, s);
     switch (dw_kernel_) {
       case DW_ROWPAIRS: return gemm_dw_rowpairs(items.data(), n, stamps_, stamp, s);
       case DW_CTA_PAIRS: return gemm_dw_pairs(items.data(), n, stamps_, stamp, s);
@@ -206,6 +212,14 @@ class Stage {
   int pair_capacity_ = 0;
   std::vector<void*> allocations_;
   int last_unfrozen_ = 0;
+  bool dense_cell_ = false;
+  static bool dense_allowed() {
+    static const bool on = [] {
+      const char* e = std::getenv("PF_DW_DENSE");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
 };
 
 // LLaMA-shaped decoder stage (RMSNorm, RoPE, GQA causal attention, SwiGLU, LM head).

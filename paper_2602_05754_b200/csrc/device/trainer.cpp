@@ -237,6 +237,15 @@ uint64_t cell_seed(uint64_t seed, uint64_t salt, int t, int s, int m) {
 }
 }  // namespace
 
+bool Trainer::cell_dense(int local_stage, int microbatch) const {
+  const int words = stages_[static_cast<std::size_t>(local_stage)]->words();
+  const uint64_t* w = masks_host_ + mask_offsets_[static_cast<std::size_t>(local_stage)] +
+                      static_cast<long long>(microbatch - 1) * (words + 1);
+  for (int i = 0; i < words; ++i)
+    if (w[i]) return false;
+  return true;
+}
+
 FreezeMask Trainer::apf_base_mask(int li) const {
   const Stage& st = *stages_[static_cast<std::size_t>(li)];
   FreezeMask base(st.units());
@@ -509,6 +518,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
       }
     } else if (a.kind == ActionKind::Weight) {  // split backward: dW of the slot's microbatch
       const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+      st.set_dense_cell(cell_dense(ls, a.microbatch));
       PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
       PF_TRY(st.backward_weight(slot, mw, stamp, stream_));
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));
@@ -536,6 +546,7 @@ int Trainer::step(int t, const int* host_tokens, const int* host_targets, StepRe
                                                                                slots_[static_cast<std::size_t>(lp)])];
       }
       const uint64_t* mw = masks_dev_ + mask_offsets_[ls] + static_cast<long long>(a.microbatch - 1) * (st.words() + 1);
+      st.set_dense_cell(cell_dense(ls, a.microbatch));
       PF_CUDA(cudaEventRecord(ev_[2 * i], stream_));
       PF_TRY(st.backward(slot, tok, mw, dy, dx, stamp, stream_));
       PF_CUDA(cudaEventRecord(ev_[2 * i + 1], stream_));

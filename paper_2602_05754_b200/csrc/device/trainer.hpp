@@ -118,6 +118,8 @@ class Trainer {
 
  private:
   int local_index(int stage) const;
+  // the host copy of this step's mask of cell (local stage, microbatch) has no frozen unit
+  bool cell_dense(int local_stage, int microbatch) const;
   const pipefreeze::MaskStream& mask_stream();
   void solve_plan_from_monitoring();
   void build_masks(int t, pipefreeze::Phase phase, bool controller, uint64_t* out, long long* frozen,

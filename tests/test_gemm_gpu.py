@@ -285,3 +285,39 @@ def _stream_k_case(cuda, b_mn, epi, M, N, K):
         _run(A, 0, B, b_mn, C, M, N, K, epi=epi, bn=512)
         r = ref + C0.float() if epi == 1 else ref
         assert (C.float() - r).abs().max().item() <= 1e-2 * r.abs().max().item() + 1e-2
+
+
+@pytest.mark.parametrize("T,O,I", [(512, 384, 512), (320, 1000, 392), (1024, 4608, 384), (256, 256, 4608)])
+def test_gemm_dw_dense_accumulates(cuda, T, O, I):
+    """Dense-cell dW (256 x 256 CTA-pair tiles over every unit, no list): the first touch of a unit in
+    a step stores, later calls accumulate; odd unit-row / unit-column counts (O = 1000 -> 8 row
+    blocks with a partial one, I = 392 / 384 -> 4 / 3 column blocks) exercise the edge tiles."""
+    import numpy as np
+    import torch
+
+    lib, nat = _lib()
+    tm, tn = -(-O // 128), -(-I // 128)
+    U = tm * tn
+    g = torch.Generator(device="cpu").manual_seed(T + O + I + 7)
+    G = torch.full((O, I), 7.0, dtype=torch.float32, device=cuda)
+    stamps = torch.zeros(U, dtype=torch.int32, device=cuda)
+    stamps[: U // 2] = 42  # half the units already touched this step: those accumulate
+    expect = G.double().cpu().clone()
+    touched = np.zeros(U, dtype=bool)
+    touched[: U // 2] = True
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        dY = torch.randn(T, O, generator=g).to(torch.bfloat16).cuda()
+        X = torch.randn(T, I, generator=g).to(torch.bfloat16).cuda()
+        nat.check(lib.pf_gemm_dw_dense(dY.data_ptr(), dY.stride(0), X.data_ptr(), X.stride(0), G.data_ptr(),
+                                       G.stride(0), O, I, T, stamps.data_ptr(), 0, 42, stream), "pf_gemm_dw_dense")
+        full = dY.double().cpu().t() @ X.double().cpu()
+        for u in range(U):
+            r, c = divmod(u, tn)
+            rs, cs = slice(r * 128, min(O, r * 128 + 128)), slice(c * 128, min(I, c * 128 + 128))
+            expect[rs, cs] = expect[rs, cs] + full[rs, cs] if touched[u] else full[rs, cs]
+            touched[u] = True
+    torch.cuda.synchronize()
+    err = (G.double().cpu() - expect).abs().max().item()
+    assert err <= 1e-3 * expect.abs().max().item(), err
+    assert stamps.cpu().tolist() == [42] * U
