@@ -35,17 +35,18 @@ def bench(M, N, K, a_mn, b_mn, bn, epi=0, iters=20):
     return 2.0 * M * N * K / (ms * 1e-3) / 1e12, ms
 
 
-T = 4096
-shapes = [("qkv fwd", T, 3072, 2048, 0, 0), ("o fwd", T, 2048, 2048, 0, 0), ("gu fwd", T, 16384, 2048, 0, 0),
-          ("d fwd", T, 2048, 8192, 0, 0), ("lm fwd", T, 128256, 2048, 0, 0), ("gu dX", T, 2048, 16384, 0, 1),
-          ("d dX", T, 8192, 2048, 0, 1), ("qkv dX", T, 2048, 3072, 0, 1), ("lm dX", T, 2048, 128256, 0, 1),
-          ("gu dW", 16384, 2048, T, 1, 1), ("8b gu fwd", T, 28672, 4096, 0, 0), ("8b d dX", T, 14336, 4096, 0, 1)]
-for name, M, N, K, a_mn, b_mn in shapes:
-    row = [name, f"{M}x{N}x{K}"]
-    for bn in (256, 512) if not a_mn else (128,):
-        try:
-            tf, ms = bench(M, N, K, a_mn, b_mn, bn, epi=2 if a_mn else 0)
-            row.append(f"bn{bn}: {tf:7.1f} TF/s ({ms:.3f} ms)")
-        except AssertionError as e:
-            row.append(f"bn{bn}: err {e}")
-    print(" | ".join(row), flush=True)
+if __name__ == "__main__":
+    T = 4096
+    shapes = [("qkv fwd", T, 3072, 2048, 0, 0), ("o fwd", T, 2048, 2048, 0, 0), ("gu fwd", T, 16384, 2048, 0, 0),
+              ("d fwd", T, 2048, 8192, 0, 0), ("lm fwd", T, 128256, 2048, 0, 0), ("gu dX", T, 2048, 16384, 0, 1),
+              ("d dX", T, 8192, 2048, 0, 1), ("qkv dX", T, 2048, 3072, 0, 1), ("lm dX", T, 2048, 128256, 0, 1),
+              ("gu dW", 16384, 2048, T, 1, 1), ("8b gu fwd", T, 28672, 4096, 0, 0), ("8b d dX", T, 14336, 4096, 0, 1)]
+    for name, M, N, K, a_mn, b_mn in shapes:
+        row = [name, f"{M}x{N}x{K}"]
+        for bn in (256, 512) if not a_mn else (128,):
+            try:
+                tf, ms = bench(M, N, K, a_mn, b_mn, bn, epi=2 if a_mn else 0)
+                row.append(f"bn{bn}: {tf:7.1f} TF/s ({ms:.3f} ms)")
+            except AssertionError as e:
+                row.append(f"bn{bn}: err {e}")
+        print(" | ".join(row), flush=True)
