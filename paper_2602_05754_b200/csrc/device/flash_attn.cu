@@ -1148,7 +1148,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __gr
   uint64_t* dp_full = s_full + 2;
   uint64_t* p_full = dp_full + 1;
   uint64_t* dq_done = p_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+  uint64_t* dp_read = dq_done + 1;  // the softmax has dP(j) in registers: dP(j + 1) may go over it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dp_read + 1);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));
   const int lane = threadIdx.x & 31;
@@ -1169,6 +1170,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __gr
     mbar_init(dp_full, 1);
     mbar_init(p_full, kSoftThreads);
     mbar_init(dq_done, 1);
+    mbar_init(dp_read, kSoftThreads);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -1242,7 +1244,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __gr
     if (nblk > 1) issue_s(1);
     for (int j = 0; j < nblk; ++j) {
       const int st = j & 1;
-      mbar_wait(p_full, j & 1);  // dS(j) is in TMEM over S(j); dP(j) has been read
+      if (j + 1 < nblk) {  // dP(j + 1) under softmax(j), as soon as the softmax holds dP(j)
+        mbar_wait(dp_read, j & 1);
+        tc_fence_after();
+        issue_dp(j + 1);
+      }
+      mbar_wait(p_full, j & 1);  // dS(j) is in TMEM over S(j)
       tc_fence_after();
       // dQ += dS(j) K_j: 16 keys per k-step, key slice kk / 2's first 16 columns of S(j)
       const uint64_t kb_mn = mnmajor_base(smem_u32(sKV + st * 2 * TILE));
@@ -1251,7 +1258,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __gr
         umma_bf16_ts_w(tmem + DQ_COL, tmem + static_cast<uint32_t>(st * 128 + (kk >> 1) * 32 + (kk & 1) * 8),
                        mnmajor_desc(kb_mn, kk), IDESC_DQ, (j > 0 || kk > 0) ? 1u : 0u);
       umma_commit_w(&kv_empty[st]);  // K_j, V_j: dP(j) and dQ(j) were their last readers
-      if (j + 1 < nblk) issue_dp(j + 1);
       if (j + 2 < nblk) issue_s(j + 2);
     }
     umma_commit_w(dq_done);
@@ -1274,6 +1280,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) flash_bwd_q_kernel(const __gr
       tld<32>(tmem + lane_off + static_cast<uint32_t>(st * 128 + slice * 32), sr);
       tld<32>(tmem + lane_off + DP_COL + static_cast<uint32_t>(slice * 32), dr);
       tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dp_read);
       const bool diag = p.causal && j == i;
       uint32_t pk[16];
 #pragma unroll
@@ -1355,7 +1363,7 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloa
 
 // PF_ATTN_BWD=2: the separate dQ kernel (flash_bwd_q_kernel, no fp32 atomics) + the dK / dV kernel
 // without dQ, instead of the default dK / dV / dQ kernel with fp32 reductions. Measured slower at the
-// LLaMA shapes (8B: 149 + 185 us + 35 us of pre / convert vs 335-340 us; both kernels ~40% tensor
+// LLaMA shapes (8B: 143 + 169 us + 35 us of pre / convert vs 335-340 us; both kernels ~40% tensor
 // active: S / dP -> softmax -> MMA stays serial in each), kept for A/B
 // (profiles/r2_attention_experiments.md).
 bool bwd_fused_dq() {
