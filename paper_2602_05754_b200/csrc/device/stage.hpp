@@ -213,12 +213,9 @@ class Stage {
   std::vector<void*> allocations_;
   int last_unfrozen_ = 0;
   bool dense_cell_ = false;
-  static bool dense_allowed() {
-    static const bool on = [] {
-      const char* e = std::getenv("PF_DW_DENSE");
-      return !(e && e[0] == '0');
-    }();
-    return on;
+  static bool dense_allowed() {  // read per call: tests flip it within one process
+    const char* e = std::getenv("PF_DW_DENSE");
+    return !(e && e[0] == '0');
   }
 };
 

@@ -268,3 +268,60 @@ def test_trainer_p2p_links_match_host_rule(cuda, schedule, ranks, C):
     with pytest.raises(Exception):
         tr.step(1)  # remote neighbours and no init_comm(): refused, not silently local
     tr.close()
+
+
+@pytest.mark.parametrize("dense_kernel", ["1", "0"])
+def test_mixed_dense_and_partial_cells_match_torch_reference(cuda, dense_kernel, monkeypatch):
+    """One step whose microbatch cells mix partial masks (row-pair dW over K5r lists) and a cell with
+    no frozen unit (the dense CTA-pair dW, chosen per cell from the host mask), given as caller-owned
+    masks: the unit stamps must hand the accumulation across the two kernels (a unit first written by
+    a partial cell is accumulated by the dense one and vice versa). The accumulated gradient (fp32
+    grad buffer) vs the fp32 torch reference; PF_DW_DENSE=0 runs every cell on the row-pair kernel."""
+    import torch
+
+    monkeypatch.setenv("PF_DW_DENSE", dense_kernel)
+    from gpu_util import device_view
+    from llama_ref import stage_loss, unflatten
+    from paper_2602_05754_b200.engine import PRESETS, Trainer, param_layout
+
+    shape = PRESETS["tiny"]
+    M = 3
+    tr = Trainer(shape, "gpipe", 1, 1, M, lr=0.5, seed=21)
+    lay = param_layout(shape, 1, 1)
+    buf = tr.stage_buffers(0)
+    n, units = buf["n_params"], buf["n_units"]
+    words = (units + 63) // 64
+    rng = np.random.default_rng(5)
+    bits = np.stack([rng.random(units) < 0.5, np.zeros(units, dtype=bool), rng.random(units) < 0.3])
+    host = np.zeros((M, words), dtype=np.uint64)
+    for m in range(M):
+        for u in np.flatnonzero(bits[m]):
+            host[m, u // 64] |= np.uint64(1) << np.uint64(u % 64)
+    tok = rng.integers(0, shape.vocab, size=(M, shape.tokens), dtype=np.int32)
+    tgt = rng.integers(0, shape.vocab, size=(M, shape.tokens), dtype=np.int32)
+    w0 = device_view(buf["weights"], n, torch.bfloat16).clone()
+    tr.step(1, tok, tgt, masks=host)
+    torch.cuda.synchronize()
+    g_dev = unflatten(device_view(buf["grad"], n).clone(), lay)
+    params = {k: v.detach().clone().requires_grad_(True) for k, v in unflatten(w0.float(), lay).items()}
+    grads = {k: torch.zeros_like(v) for k, v in params.items()}
+    for m in range(M):
+        for v in params.values():
+            v.grad = None
+        loss = stage_loss(params, shape, range(shape.layers), torch.tensor(tok[m], device=cuda).long(),
+                          torch.tensor(tgt[m], device=cuda).long(), True, True, faithful=True)
+        loss.backward()
+        for ent in lay["units"]:
+            grads[ent["name"]] += params[ent["name"]].grad * torch.tensor(_expand_unit_mask(bits[m], ent), device=cuda)
+    checked = 0
+    for ent in lay["units"]:
+        name = ent["name"]
+        touched = torch.tensor(_expand_unit_mask(np.logical_and.reduce(bits), ent), device=cuda).bool()
+        exp, got = grads[name][touched], g_dev[name][touched]
+        if exp.abs().max().item() == 0:
+            continue
+        rel = (got - exp).norm().item() / exp.norm().item()
+        assert rel < 6e-2, (name, rel)
+        checked += 1
+    assert checked >= 8
+    tr.close()
