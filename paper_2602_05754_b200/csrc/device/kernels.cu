@@ -821,6 +821,169 @@ __global__ void __launch_bounds__(CH * 32) rmsnorm_bwd_rows_kernel(
   atomicAdd(reinterpret_cast<float4*>(dg + col + 4), make_float4(acc[4], acc[5], acc[6], acc[7]));
 }
 
+// Software-pipelined RMSNorm forward at h = 256 CH: the next batch of R rows is loaded under the
+// current batch's reduction and stores.
+template <int CH, int R>
+__global__ void __launch_bounds__(CH * 32) rmsnorm_fwd_pipe_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const __nv_bfloat16* __restrict__ g,
+                                                                   __nv_bfloat16* __restrict__ y,
+                                                                   float* __restrict__ rstd, int T, float eps) {
+  pdl_begin();
+  constexpr int H = 256 * CH;
+  __shared__ float red[2][R][CH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x * 8;
+  float gv[8];
+  load8(g + col, gv);
+  uint4 xv[R];
+  auto fetch = [&](int t0) {
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      xv[q] = t0 + q < T ? __ldcs(reinterpret_cast<const uint4*>(x + static_cast<long long>(t0 + q) * H + col))
+                         : make_uint4(0u, 0u, 0u, 0u);
+  };
+  int buf = 0;
+  int t0 = blockIdx.x * R;
+  if (t0 < T) fetch(t0);
+  for (; t0 < T; t0 += gridDim.x * R, buf ^= 1) {
+    uint4 cx[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) cx[q] = xv[q];
+    const int tn = t0 + gridDim.x * R;
+    if (tn < T) fetch(tn);
+    float ss[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&cx[q]);
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(b[i]);
+        a += f.x * f.x + f.y * f.y;
+      }
+      ss[q] = warp_sum(a);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) red[buf][q][warp] = ss[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int t = t0 + q;
+      if (t >= T) break;
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < CH; ++w) tot += red[buf][q][w];
+      const float r = rsqrtf(tot / H + eps);
+      if (threadIdx.x == 0) rstd[t] = r;
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&cx[q]);
+      float f[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 v = __bfloat1622float2(b[i]);
+        f[2 * i] = v.x * r * gv[2 * i];
+        f[2 * i + 1] = v.y * r * gv[2 * i + 1];
+      }
+      store8(y + static_cast<long long>(t) * H + col, f);
+    }
+  }
+}
+
+// Software-pipelined RMSNorm backward at h = 256 CH: the loads of the CTA's next R rows are issued
+// before the current rows' reductions, barrier and stores, so a CTA always has a batch of rows in
+// flight (the row-block kernel above waits for each batch's loads).
+template <int CH, int R>
+__global__ void __launch_bounds__(CH * 32) rmsnorm_bwd_pipe_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g, const float* __restrict__ rstd,
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ residual, __nv_bfloat16* __restrict__ dx,
+    float* __restrict__ dg, int T) {
+  pdl_begin();
+  constexpr int H = 256 * CH;
+  __shared__ float red[2][R][CH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = threadIdx.x * 8;
+  float gv[8], acc[8];
+  load8(g + col, gv);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  uint4 xv[R], dv[R], rv[R];
+  float rr[R];
+  auto fetch = [&](int t0) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const bool ok = t0 + q < T;
+      const long long off = static_cast<long long>(t0 + q) * H + col;
+      xv[q] = ok ? __ldcs(reinterpret_cast<const uint4*>(x + off)) : z;
+      dv[q] = ok ? __ldcs(reinterpret_cast<const uint4*>(dy + off)) : z;
+      rv[q] = ok && residual ? __ldcs(reinterpret_cast<const uint4*>(residual + off)) : z;
+      rr[q] = ok ? rstd[t0 + q] : 0.f;
+    }
+  };
+  int buf = 0;
+  int t0 = blockIdx.x * R;
+  if (t0 < T) fetch(t0);
+  for (; t0 < T; t0 += gridDim.x * R, buf ^= 1) {
+    uint4 cx[R], cd[R], cres[R];
+    float cr[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      cx[q] = xv[q];
+      cd[q] = dv[q];
+      cres[q] = rv[q];
+      cr[q] = rr[q];
+    }
+    const int tn = t0 + gridDim.x * R;
+    if (tn < T) fetch(tn);  // next batch in flight under this one
+    float dot[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&cx[q]);
+      const __nv_bfloat162* db = reinterpret_cast<const __nv_bfloat162*>(&cd[q]);
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 xf = __bfloat1622float2(xb[i]), df = __bfloat1622float2(db[i]);
+        a += gv[2 * i] * df.x * xf.x + gv[2 * i + 1] * df.y * xf.y;
+      }
+      dot[q] = warp_sum(a);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) red[buf][q][warp] = dot[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int t = t0 + q;
+      if (t >= T) break;
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < CH; ++w) tot += red[buf][q][w];
+      const float r = cr[q];
+      const float k = tot * r * r * r / H;
+      const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&cx[q]);
+      const __nv_bfloat162* db = reinterpret_cast<const __nv_bfloat162*>(&cd[q]);
+      const __nv_bfloat162* rb = reinterpret_cast<const __nv_bfloat162*>(&cres[q]);
+      float out[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 xf = __bfloat1622float2(xb[i]), df = __bfloat1622float2(db[i]);
+        const float2 rf = __bfloat1622float2(rb[i]);
+        out[2 * i] = rf.x + r * gv[2 * i] * df.x - k * xf.x;
+        out[2 * i + 1] = rf.y + r * gv[2 * i + 1] * df.y - k * xf.y;
+        acc[2 * i] += df.x * xf.x * r;
+        acc[2 * i + 1] += df.y * xf.y * r;
+      }
+      store8(dx + static_cast<long long>(t) * H + col, out);
+    }
+  }
+  if (dg == nullptr) return;
+  atomicAdd(reinterpret_cast<float4*>(dg + col), make_float4(acc[0], acc[1], acc[2], acc[3]));
+  atomicAdd(reinterpret_cast<float4*>(dg + col + 4), make_float4(acc[4], acc[5], acc[6], acc[7]));
+}
+
 // rotate-half RoPE on the q and k heads of the packed qkv activation, in place.
 // grid.y = token; each thread rotates 8 consecutive pairs (16-byte loads).
 __global__ void rope_fwd_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ cs, int seq, int nh,
@@ -1112,6 +1275,10 @@ int launch_embedding_bwd(const int* tok, const __nv_bfloat16* dout, float* g, in
 }
 
 // PF_NORM_ROWS=0: the warp-per-row kernels at h = 4096 too (same-process A/B in tools/norm_bench.py)
+static bool norm_batch_wait() {  // PF_NORM_ROWS=1: the row-block backward without prefetch (A/B)
+  const char* e = std::getenv("PF_NORM_ROWS");
+  return e && e[0] == '1';
+}
 static bool norm_rows_off() {
   const char* e = std::getenv("PF_NORM_ROWS");
   return e && e[0] == '0';
@@ -1131,10 +1298,20 @@ int launch_rmsnorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bflo
         launch_k(rmsnorm_fwd_reg_kernel<16>, dim3(grid), dim3(kBlock), 0, s, x, g, y, rstd, T, eps);
         return status();
       }
+      if (!norm_batch_wait()) {
+        launch_k(rmsnorm_fwd_pipe_kernel<16, 4>, dim3(std::max(1, std::min(2 * num_sms(), (T + 3) / 4))), dim3(512), 0,
+                 s, x, g, y, rstd, T, eps);
+        return status();
+      }
       launch_k(rmsnorm_fwd_rows_kernel<16, 4>, dim3(std::max(1, std::min(2 * num_sms(), (T + 3) / 4))), dim3(512), 0, s,
                x, g, y, rstd, T, eps);
       return status();
     case 5120:
+      if (!norm_batch_wait()) {
+        launch_k(rmsnorm_fwd_pipe_kernel<20, 2>, dim3(std::max(1, std::min(2 * num_sms(), (T + 1) / 2))), dim3(640), 0,
+                 s, x, g, y, rstd, T, eps);
+        return status();
+      }
       launch_k(rmsnorm_fwd_rows_kernel<20, 2>, dim3(std::max(1, std::min(2 * num_sms(), (T + 1) / 2))), dim3(640), 0, s,
                x, g, y, rstd, T, eps);
       return status();
@@ -1175,10 +1352,20 @@ int launch_rmsnorm_bwd(const __nv_bfloat16* x, const __nv_bfloat16* g, const flo
     case 2048: return launch_rmsnorm_bwd_fused<8>(x, g, rstd, dy, residual, dx, dg, T, s);
     case 4096:
       if (norm_rows_off()) return launch_rmsnorm_bwd_fused<16>(x, g, rstd, dy, residual, dx, dg, T, s);
+      if (!norm_batch_wait()) {
+        launch_k(rmsnorm_bwd_pipe_kernel<16, 2>, dim3(std::max(1, std::min(num_sms(), (T + 1) / 2))), dim3(512), 0, s,
+                 x, g, rstd, dy, residual, dx, dg, T);
+        return status();
+      }
       launch_k(rmsnorm_bwd_rows_kernel<16, 4>, dim3(std::max(1, std::min(num_sms(), (T + 3) / 4))), dim3(512), 0, s,
                x, g, rstd, dy, residual, dx, dg, T);
       return status();
     case 5120:
+      if (!norm_batch_wait()) {
+        launch_k(rmsnorm_bwd_pipe_kernel<20, 2>, dim3(std::max(1, std::min(num_sms(), (T + 1) / 2))), dim3(640), 0, s,
+                 x, g, rstd, dy, residual, dx, dg, T);
+        return status();
+      }
       launch_k(rmsnorm_bwd_rows_kernel<20, 2>, dim3(std::max(1, std::min(2 * num_sms(), (T + 1) / 2))), dim3(640), 0, s,
                x, g, rstd, dy, residual, dx, dg, T);
       return status();

@@ -6,8 +6,8 @@ from paper_2602_05754_b200 import _native  # noqa: E402
 lib = _native.device()
 s = torch.cuda.current_stream().cuda_stream
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
-for T, h, rows in [(4096, 2048, "1"), (4096, 4096, "0"), (4096, 4096, "1"), (2048, 5120, "1")]:
-    os.environ["PF_NORM_ROWS"] = rows  # 0: warp-per-row kernels at h = 4096 (A/B)
+for T, h, rows in [(4096, 4096, "1"), (4096, 4096, "2"), (2048, 5120, "1"), (2048, 5120, "2")]:
+    os.environ["PF_NORM_ROWS"] = rows  # 1: row-block backward without prefetch, 0: warp-per-row (A/B)
     x = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     dy = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     res = torch.randn(T, h, device="cuda").to(torch.bfloat16)
