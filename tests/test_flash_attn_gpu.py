@@ -242,3 +242,43 @@ def test_flash_backward_separate_dq_matches_fused(cuda, tmp_path, hd):
     assert np.array_equal(a[:, nh:], b[:, nh:])
     dq_a, dq_b = a[:, :nh], b[:, :nh]
     assert np.linalg.norm(dq_a - dq_b) <= 1e-2 * np.linalg.norm(dq_b)
+
+
+_FWD_PATH_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2602_05754_b200 import _native
+lib = _native.device()
+B, S, nh, nkv, hd = 2, 640, 8, 2, {hd}
+T, W = B * S, (nh + 2 * nkv) * hd
+g = torch.Generator().manual_seed(9)
+qkv = torch.randn(T, W, generator=g).bfloat16().cuda()
+out = torch.empty(T, nh * hd, dtype=torch.bfloat16, device='cuda')
+lse = torch.empty(B, nh, S, device='cuda')
+st = torch.cuda.current_stream().cuda_stream
+assert lib.pf_flash_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), B, S, nh, nkv, hd, hd ** -0.5, {causal}, st) == 0
+torch.cuda.synchronize()
+np.save(sys.argv[1], np.concatenate([out.float().cpu().numpy().ravel(), lse.cpu().numpy().ravel()]))
+"""
+
+
+@pytest.mark.parametrize("hd,causal", [(128, 1), (64, 1), (128, 0)])
+def test_flash_forward_two_tile_matches_one_tile(cuda, tmp_path, hd, causal):
+    """The default two-tile (ping-pong) forward and the one-tile forward (PF_ATTN_FWD=1) on the same
+    inputs; S = 640 is 5 query blocks, so the last CTA of the two-tile kernel has no tile B."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("2", "1"):
+        f = tmp_path / f"o{mode}.npy"
+        code = _FWD_PATH_SNIPPET.replace("{hd}", str(hd)).replace("{causal}", str(causal))
+        subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, env=dict(os.environ, PF_ATTN_FWD=mode),
+                       check=True, timeout=300)
+        outs[mode] = np.load(f)
+    a, b = outs["2"], outs["1"]
+    n_out = 2 * 640 * 8 * hd
+    assert np.linalg.norm(a[:n_out] - b[:n_out]) <= 1e-2 * np.linalg.norm(b[:n_out])
+    assert np.abs(a[n_out:] - b[n_out:]).max() <= 1e-3 * max(1.0, np.abs(b[n_out:]).max())
