@@ -100,6 +100,8 @@ struct alignas(64) Params2 {
   float* colsum;              // EPI_DGELU: += column sums of d(pre) (the fc1 bias gradient; nullptr: none)
   const float2* rope;         // EPI_ROPE: (cos, sin) [seq][32]
   int rope_seq, rope_cols, rope_hd;
+  int split_from;  // whole-tile work items: tiles [split_from, ntiles) run as two BN/2-wide halves
+  int items;       // work items without stream-K: split_from + 2 * (ntiles - split_from)
   int streamk;   // 0: one tile per work item; 1/2: stream-K (2: data-parallel full waves first)
   int dp_tiles;  // stream-K: tiles [0, dp_tiles) run whole, round-robin over the clusters
   long long sk_q;  // stream-K: iterations of the split region per cluster
@@ -120,9 +122,8 @@ struct SegIter {
 
 __device__ __forceinline__ bool next_seg(const Params2& p, int cluster, int nclusters, int num_kb, SegIter& it,
                                          Seg& s) {
-  const int ntiles = p.tiles_m * p.tiles_n;
   if (!p.streamk) {
-    if (it.t >= ntiles) return false;
+    if (it.t >= p.items) return false;
     s = Seg{it.t, 0, num_kb};
     it.t += nclusters;
     return true;
@@ -164,6 +165,23 @@ __device__ __forceinline__ void decode(const Params2& p, int t, int& tm, int& tn
   tn = local / gm;
 }
 
+// Work item -> tile and column range. Without stream-K, the last partial wave's tiles (index >=
+// split_from) are split into two BN/2-wide halves so the wave's pieces cover (nearly) every CTA pair:
+// 3.46 waves of 256 x 256 tiles (the LLaMA-8B N = 4096 GEMMs) become 3 full waves + one of halves.
+template <int BN>
+__device__ __forceinline__ void decode_seg(const Params2& p, int item, int& tm, int& tn, int& n_begin, int& width) {
+  if (item >= p.split_from) {
+    const int u = item - p.split_from;
+    decode(p, p.split_from + (u >> 1), tm, tn);
+    n_begin = tn * BN + (u & 1) * (BN / 2);
+    width = BN / 2;
+  } else {
+    decode(p, item, tm, tn);
+    n_begin = tn * BN;
+    width = BN;
+  }
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -179,6 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using Cfg = Cfg2<BN, EPI>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM2, BN, false, B_MN);
+  constexpr uint32_t IDESC_HALF = idesc_bf16_f32(BM2, BN / 2, false, B_MN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -240,10 +259,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       SegIter it = seg_begin(p, cluster, nclusters, num_kb);
       Seg sg;
       while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
-        int tm, tn;
-        decode(p, sg.tile, tm, tn);
+        int tm, tn, nb, width;
+        decode_seg<BN>(p, sg.tile, tm, tn, nb, width);
         const int m0 = tm * BM2 + static_cast<int>(rank) * 128;
-        const int n0 = tn * BN + static_cast<int>(rank) * (BN / 2);
+        // a half-width tile loads the same boxes (expect_tx unchanged); its MMA reads the first
+        // width / 2 columns of each CTA's half
+        const int n0 = nb + static_cast<int>(rank) * (width / 2);
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
@@ -275,6 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       SegIter it = seg_begin(p, cluster, nclusters, num_kb);
       Seg sg;
       while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
+        const uint32_t idesc = warp_uniform(sg.tile >= p.split_from ? IDESC_HALF : IDESC);
         mbar_wait(&tempty_bar[abuf], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(abuf * BN);
@@ -288,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t adesc = sdesc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t bdesc = B_MN ? sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                         : sdesc_sw128(b_base + k * 32, 16, 1024);
-            umma_bf16_pair_w(d_tmem, adesc, bdesc, IDESC, (kb != sg.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair_w(d_tmem, adesc, bdesc, idesc, (kb != sg.kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit_pair_multicast_w(&empty_bar[stage], 0x3);
           if (++stage == STAGES) {
@@ -314,8 +336,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     SegIter it = seg_begin(p, cluster, nclusters, num_kb);
     Seg sg;
     while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
-      int tm, tn;
-      decode(p, sg.tile, tm, tn);
+      int tm, tn, nb, width;
+      decode_seg<BN>(p, sg.tile, tm, tn, nb, width);
       // stream-K roles: a piece that starts mid-tile (kb0 > 0) parks its partial in this
       // cluster's slot; a head (kb1 < num_kb) adds the pieces parked by clusters
       // cluster+1 .. last_slot (the owner of the tile's last k-block), then writes C.
@@ -425,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint8_t* buf = sE + (c & 1) * Cfg::EPI_BUF;
             bulk_wait_read0();
             mbar_arrive_expect_tx(&ebar[c & 1], Cfg::EPI_BUF);
-            tma_load_2d(buf, &p.te_in, &ebar[c & 1], tn * BN + c * 32, y0);
+            tma_load_2d(buf, &p.te_in, &ebar[c & 1], nb + c * 32, y0);
           };
           if (EPI == EPI_ADD_BF16 && elected) {
             load_r(0);
@@ -433,8 +455,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           mbar_wait(&tfull_bar[abuf], aphase);
           tc_fence_after();
+          const int nchunks = width / 32;
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
+          for (int c = 0; c < nchunks; ++c) {
             const int k = c & 1;
             uint32_t r[16];
             tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -457,7 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < 8; ++i) w[i] = p.alpha * __uint_as_float(r[8 * s2 + i]);
               if (p.bias != nullptr) {  // per-column bias (ViT linear layers); N % 32 == 0 on this path
-                const uint4 braw = __ldg(reinterpret_cast<const uint4*>(p.bias + tn * BN + c * 32 + half * 16 + 8 * s2));
+                const uint4 braw = __ldg(reinterpret_cast<const uint4*>(p.bias + nb + c * 32 + half * 16 + 8 * s2));
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -482,9 +505,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             named_bar_sync(1, kEpiThreads);
             if (elected) {
-              tma_store_2d(&p.te_out, buf, tn * BN + c * 32, y0);
+              tma_store_2d(&p.te_out, buf, nb + c * 32, y0);
               bulk_commit();
-              if (EPI == EPI_ADD_BF16 && c + 2 < BN / 32) load_r(c + 2);
+              if (EPI == EPI_ADD_BF16 && c + 2 < nchunks) load_r(c + 2);
             }
           }
           tc_fence_before();
@@ -499,7 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint4 rpre[4];
       auto fetch_r = [&](int c) {
         if constexpr (EPI == EPI_ADD_BF16) {
-          const int gcol = tn * BN + c * 32;
+          const int gcol = nb + c * 32;
           if (!row_ok || gcol + 32 > p.N) return;
           const uint4* r4 = reinterpret_cast<const uint4*>(p.R + grow * p.ldr + gcol);
 #pragma unroll
@@ -783,13 +806,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         continue;
       }
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < width / 32; c += 2) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                static_cast<uint32_t>(abuf * BN + c * 32),
                            r);
         const uint4 rcur[4] = {rpre[0], rpre[1], rpre[2], rpre[3]};
-        if (EPI == EPI_ADD_BF16 && !park && c + 2 < BN / 32) fetch_r(c + 2);
+        if (EPI == EPI_ADD_BF16 && !park && c + 2 < width / 32) fetch_r(c + 2);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -813,7 +836,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
-        const int gcol = tn * BN + c * 32;
+        const int gcol = nb + c * 32;
         if (!row_ok || gcol >= p.N) continue;
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
@@ -980,6 +1003,12 @@ int& streamk_mode_ref() {
 }
 int streamk_mode() { return streamk_mode_ref(); }
 
+// PF_GEMM_TAIL_SPLIT=0: the last partial wave runs whole tiles too (A/B)
+bool tail_split_on() {
+  const char* e = std::getenv("PF_GEMM_TAIL_SPLIT");
+  return !(e && e[0] == '0');
+}
+
 // K1/K2 plain epilogues through shared memory + TMA stores (PF_GEMM_TMA_EPI=0: row-per-thread stores)
 bool tma_plain_epi() {
   static const bool on = [] {
@@ -1110,6 +1139,17 @@ int gemm_bf16_pair(const GemmOperand& A, const GemmOperand& B, const GemmOut& C,
     // TMA needs 16-byte aligned bases and row strides; otherwise the row-per-thread epilogue runs
     p.tma_epi = tma_desc_bf16_2d_sw64(&p.te_out, C.ptr, M, N, C.ld, 32, 128) == PF_OK &&
                 (epi != EPI_ADD_BF16 || tma_desc_bf16_2d_sw64(&p.te_in, p.R, M, N, p.ldr, 32, 128) == PF_OK);
+  }
+  // whole tiles, except a last partial wave of at most half the CTA pairs, which runs as half-width
+  // tiles (plain TMA-staged epilogues only; PF_GEMM_TAIL_SPLIT=0 turns it off)
+  p.split_from = ntiles;
+  p.items = ntiles;
+  if (!p.streamk && p.tma_epi && tail_split_on() && ntiles > clusters) {
+    const int rem = ntiles % clusters;
+    if (rem > 0 && 2 * rem <= clusters) {
+      p.split_from = ntiles - rem;
+      p.items = ntiles + rem;
+    }
   }
   const bool bmn = B.mn_major;
   switch (epi) {
