@@ -45,6 +45,10 @@ int tma_desc_bf16_2d_sw64(CUtensorMap* map, const void* ptr, long long rows, lon
 
 namespace {
 
+#ifndef PF_STORE_NBUF
+#define PF_STORE_NBUF 3
+#endif
+constexpr bool kStore3 = PF_STORE_NBUF == 3;
 constexpr int BM2 = 256;  // rows per CTA pair
 constexpr int BK = 64;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, alternating 32-column chunks
@@ -66,7 +70,10 @@ struct Cfg2 {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BUF =
       EPI == EPI_SWIGLU ? 3 * 8192 : ((EPI == EPI_DSWIGLU || EPI == EPI_GELU || EPI == EPI_ROPE) ? 2 * 8192 : 8192);
-  static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? 2 * EPI_BUF : 0;
+  // EPI_GELU and the TMA-staged EPI_STORE_BF16 cycle three buffers (one named barrier per chunk;
+  // EPI_DGELU measured slower with three, profiles/r2_vit_gemm_ab.txt)
+  static constexpr int EPI_NBUF = (EPI == EPI_GELU || (EPI == EPI_STORE_BF16 && kStore3)) ? 3 : 2;
+  static constexpr int EPI_BYTES = (TMA_EPI || TMA_PLAIN) ? EPI_NBUF * EPI_BUF : 0;
   // EPI_DGELU column sums: [2 accumulator buffers][4 row quarters][BN] fp32
   static constexpr int CS_BYTES = EPI == EPI_DGELU ? 2 * 4 * BN * 4 : 0;
   static constexpr int TMEM_COLS = 2 * BN;
@@ -210,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* ebar = tempty_bar + 2;  // EPI_DSWIGLU: epilogue buffer k loaded
+  uint64_t* ebar = tempty_bar + 2;  // TMA-in epilogues: epilogue buffer k loaded
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 2);
 
   const int warp = static_cast<int>(warp_uniform(threadIdx.x >> 5));  // uniform: MMA issue stays on the uniform datapath
@@ -332,7 +339,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
     int abuf = 0;
     uint32_t aphase = 0;
-    uint32_t ephase = 0;  // EPI_DSWIGLU: bit k = parity of epilogue buffer k's barrier
+    uint32_t ephase = 0;  // TMA-in epilogues: bit k = parity of epilogue buffer k's barrier
+    int ec = 0;  // EPI_GELU / EPI_STORE_BF16: epilogue buffer of the next chunk (running over tiles)
     SegIter it = seg_begin(p, cluster, nclusters, num_kb);
     Seg sg;
     while (next_seg(p, cluster, nclusters, num_kb, it, sg)) {
@@ -458,7 +466,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int nchunks = width / 32;
 #pragma unroll 1
           for (int c = 0; c < nchunks; ++c) {
-            const int k = c & 1;
+            // EPI_STORE_BF16: three buffers over a running chunk count, as EPI_GELU; EPI_ADD_BF16: two
+            const int k = (EPI == EPI_STORE_BF16 && kStore3) ? ec : c & 1;
             uint32_t r[16];
             tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(abuf * BN + c * 32 + half * 16),
@@ -467,8 +476,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if constexpr (EPI == EPI_ADD_BF16) {
               mbar_wait(&ebar[k], (ephase >> k) & 1u);
               ephase ^= 1u << k;
-            } else {
-              if (elected) bulk_wait_read1();  // the store of chunk c - 2 (this buffer) has read it
+            } else if constexpr (!kStore3) {
+              if (elected) bulk_wait_read1();
               named_bar_sync(1, kEpiThreads);
             }
             tmem_ld_wait();
@@ -503,12 +512,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                 pack_bf16x2(w[6], w[7]));
             }
             fence_proxy_async_smem();
+            if (EPI == EPI_STORE_BF16 && kStore3 && elected) bulk_wait_read1();  // store c - 2 has read buffer (c + 1) % 3
             named_bar_sync(1, kEpiThreads);
             if (elected) {
               tma_store_2d(&p.te_out, buf, nb + c * 32, y0);
               bulk_commit();
               if (EPI == EPI_ADD_BF16 && c + 2 < nchunks) load_r(c + 2);
             }
+            if constexpr (EPI == EPI_STORE_BF16 && kStore3) ec = ec == 2 ? 0 : ec + 1;
           }
           tc_fence_before();
           mbar_arrive_cluster(abuf ? leader_tempty1 : leader_tempty0);
@@ -619,6 +630,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         //   EPI_DGELU: pre arrives by TMA (chunks 0 and 1 while the MMAs run), is overwritten in
         //              place by d(pre) = bf16(alpha acc) * gelu'(pre), stored by TMA, and the buffer
         //              is refilled with chunk c + 2 (= GEMM then gelu_bwd_kernel, bit for bit)
+        // EPI_GELU cycles three buffers: chunk c may be written once the store of chunk c - 3 has read
+        // its buffer, which the elected thread checks (wait_group.read 1) before the previous chunk's
+        // barrier, so each chunk needs one CTA-wide barrier instead of two.
         const int y0 = tm * BM2 + static_cast<int>(rank) * 128;
         const bool elected = threadIdx.x == 64;
         auto load_pre = [&](int c) {  // EPI_DGELU, elected thread
@@ -635,7 +649,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          const int k = c & 1;
+          // EPI_GELU: three buffers over a running chunk count (tiles of 8 chunks); EPI_DGELU: two
+          const int k = EPI == EPI_GELU ? ec : c & 1;
           uint32_t r[16];
           tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                  static_cast<uint32_t>(abuf * BN + c * 32 + half * 16),
@@ -644,9 +659,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if constexpr (EPI == EPI_DGELU) {
             mbar_wait(&ebar[k], (ephase >> k) & 1u);
             ephase ^= 1u << k;
-          } else {
-            if (elected) bulk_wait_read1();  // the stores of chunk c - 2 (this buffer) have read it
-            named_bar_sync(1, kEpiThreads);
           }
           tmem_ld_wait();
 #pragma unroll
@@ -674,7 +686,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const __nv_bfloat162 pb = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
                 const float2 pf = __bfloat1622float2(pb);
                 pw[i] = *reinterpret_cast<const uint32_t*>(&pb);
-                aw[i] = pack_bf16x2(gelu_erf(pf.x), gelu_erf(pf.y));
+                const float2 g = gelu_erf2(pf);
+                aw[i] = pack_bf16x2(g.x, g.y);
               }
               *pp = make_uint4(pw[0], pw[1], pw[2], pw[3]);
               *reinterpret_cast<uint4*>(buf + 8192 + off) = make_uint4(aw[0], aw[1], aw[2], aw[3]);
@@ -687,7 +700,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float2 pf = __bfloat1622float2(p2[i]);
                 const float2 d = __bfloat1622float2(__floats2bfloat162_rn(p.alpha * __uint_as_float(r[8 * s2 + 2 * i]),
                                                                           p.alpha * __uint_as_float(r[8 * s2 + 2 * i + 1])));
-                const __nv_bfloat162 o = __floats2bfloat162_rn(d.x * gelu_erf_grad(pf.x), d.y * gelu_erf_grad(pf.y));
+                const float2 gd = mul2(d, gelu_erf_grad2(pf));
+                const __nv_bfloat162 o = __floats2bfloat162_rn(gd.x, gd.y);
                 dw[i] = *reinterpret_cast<const uint32_t*>(&o);
                 const float2 of = __bfloat1622float2(o);  // the stored (bf16) d(pre) feeds the bias gradient
                 r[8 * s2 + 2 * i] = __float_as_uint(of.x);
@@ -697,6 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
           fence_proxy_async_smem();
+          if (EPI == EPI_GELU && elected) bulk_wait_read1();  // store c - 2 has read buffer (c + 1) % 3
           named_bar_sync(1, kEpiThreads);
           if (EPI == EPI_DGELU && p.colsum != nullptr) {
             // column sums over this warp's 32 rows of its 16 columns, from registers (r holds the
@@ -735,6 +750,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (c + 2 < BN / 32) load_pre(c + 2);
             }
           }
+          if constexpr (EPI == EPI_GELU) ec = ec == 2 ? 0 : ec + 1;
         }
         if (EPI == EPI_DGELU && p.colsum != nullptr) {
           // one atomic per column per CTA and tile (csum is double-buffered by accumulator buffer:

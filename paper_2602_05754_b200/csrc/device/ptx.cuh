@@ -545,6 +545,34 @@ __device__ __forceinline__ float gelu_erf_grad(float v) {
   const float ph = gelu_phi(v, e);
   return ph + v * 0.39894228040143268f * e;
 }
+// The same on a pair of values with the packed FFMA2 / FMUL2 forms: half the FMA-pipe issue slots
+// of the scalar chain, two MUFU ops per value as before. The GELU GEMM epilogues and
+// gelu_{fwd,bwd}_kernel all use these forms, so they still agree bit for bit.
+__device__ __forceinline__ float2 gelu_phi2(float2 v, float2& e) {
+  const float2 a = mul2(make_float2(fabsf(v.x), fabsf(v.y)), make_float2(0.70710678118654752f, 0.70710678118654752f));
+  const float2 den = fma2(make_float2(0.3275911f, 0.3275911f), a, make_float2(1.f, 1.f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 pl = fma2(t, make_float2(1.061405429f, 1.061405429f), make_float2(-1.453152027f, -1.453152027f));
+  pl = fma2(t, pl, make_float2(1.421413741f, 1.421413741f));
+  pl = fma2(t, pl, make_float2(-0.284496736f, -0.284496736f));
+  pl = fma2(t, pl, make_float2(0.254829592f, 0.254829592f));
+  const float2 hp = mul2(mul2(t, pl), make_float2(0.5f, 0.5f));
+  // e^{-a^2} = 2^{-a^2 log2 e} on the MUFU
+  const float2 x = mul2(mul2(a, a), make_float2(-1.44269504088896341f, -1.44269504088896341f));
+  e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+  const float2 q = mul2(hp, e);
+  const float2 omq = fma2(q, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));  // 1 - q, one rounding
+  return make_float2(v.x >= 0.f ? omq.x : q.x, v.y >= 0.f ? omq.y : q.y);
+}
+__device__ __forceinline__ float2 gelu_erf2(float2 v) {
+  float2 e;
+  return mul2(v, gelu_phi2(v, e));
+}
+__device__ __forceinline__ float2 gelu_erf_grad2(float2 v) {
+  float2 e;
+  const float2 ph = gelu_phi2(v, e);
+  return fma2(mul2(v, make_float2(0.39894228040143268f, 0.39894228040143268f)), e, ph);
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

@@ -56,9 +56,26 @@ bool fuse_swiglu() {
 bool fuse_swiglu_fwd(int /*K*/) { return fuse_swiglu(); }
 bool fuse_swiglu_bwd() { return fuse_swiglu(); }
 
+// A GEMM that is one partial wave on the CTA pairs (the ViT-L/32 N = 1024 dX GEMMs: 52 256 x 256
+// tiles on 74 pairs) runs as 128 x 256 tiles of the one-CTA kernel, still one wave (100 tiles on 148
+// SMs): 12.4 vs 14.5 us (o dX), 21.7 vs 22.7 (qkv dX), 26.8 vs 28.9 (fc1 dX),
+// profiles/r2_vit_gemm_ab.txt. PF_GEMM_SMALL_ONECTA=0 keeps the pair kernel (A/B).
+static bool small_onecta(int M, int N, int epi) {
+  static const bool on = [] {
+    const char* e = std::getenv("PF_GEMM_SMALL_ONECTA");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || epi != EPI_STORE_BF16) return false;
+  const int sms = num_sms();
+  const long long pair_tiles = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
+  const long long cta_tiles = static_cast<long long>((M + 127) / 128) * ((N + 255) / 256);
+  return 4 * pair_tiles <= 3 * (sms / 2) && cta_tiles <= sms;
+}
+
 int gemm_any(const GemmOperand& A, const GemmOperand& B, void* C, long long ldc, int M, int N, int K, int epi,
              cudaStream_t s) {
-  if (use_pair() && M >= 256 && N >= 256) return gemm_bf16_pair(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, s);
+  if (use_pair() && M >= 256 && N >= 256 && !small_onecta(M, N, epi))
+    return gemm_bf16_pair(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, s);
   return gemm_bf16(A, B, GemmOut{C, ldc}, M, N, K, 1.0f, epi, N >= 256 ? 256 : 128, s);
 }
 

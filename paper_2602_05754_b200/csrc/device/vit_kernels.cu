@@ -323,7 +323,11 @@ __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ pre, __nv_bflo
     float f[8];
     load8(pre + i * 8, f);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = gelu_erf(f[k]);
+    for (int k = 0; k < 8; k += 2) {
+      const float2 g = gelu_erf2(make_float2(f[k], f[k + 1]));
+      f[k] = g.x;
+      f[k + 1] = g.y;
+    }
     store8(act + i * 8, f);
   }
 }
@@ -337,7 +341,11 @@ __global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ pre, const __n
     load8(pre + i * 8, p);
     load8(dact + i * 8, d);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] *= gelu_erf_grad(p[k]);
+    for (int k = 0; k < 8; k += 2) {
+      const float2 g = mul2(make_float2(d[k], d[k + 1]), gelu_erf_grad2(make_float2(p[k], p[k + 1])));
+      d[k] = g.x;
+      d[k + 1] = g.y;
+    }
     store8(dpre + i * 8, d);
   }
 }
