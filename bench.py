@@ -161,7 +161,10 @@ def ncu_traffic(kernel: str):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["bytes_per_launch"] if d.get("kernel") == kernel else None
+        for e in d if isinstance(d, list) else [d]:  # one entry per config's roofline kernel
+            if e.get("kernel") == kernel:
+                return e["bytes_per_launch"]
+        return None
     except (OSError, ValueError, KeyError):
         return None
 

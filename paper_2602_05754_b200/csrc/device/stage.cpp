@@ -56,10 +56,12 @@ bool fuse_swiglu() {
 bool fuse_swiglu_fwd(int /*K*/) { return fuse_swiglu(); }
 bool fuse_swiglu_bwd() { return fuse_swiglu(); }
 
-// A GEMM that is one partial wave on the CTA pairs (the ViT-L/32 N = 1024 dX GEMMs: 52 256 x 256
+// A GEMM that is one partial wave on the CTA pairs (the ViT-L/32 N = 1024 GEMMs: 52 256 x 256
 // tiles on 74 pairs) runs as 128 x 256 tiles of the one-CTA kernel, still one wave (100 tiles on 148
-// SMs): 12.4 vs 14.5 us (o dX), 21.7 vs 22.7 (qkv dX), 26.8 vs 28.9 (fc1 dX),
-// profiles/r2_vit_gemm_ab.txt. PF_GEMM_SMALL_ONECTA=0 keeps the pair kernel (A/B).
+// SMs): 12.4 vs 14.5 us (o dX), 21.7 vs 22.7 (qkv dX), 26.8 vs 28.9 (fc1 dX) back to back,
+// profiles/r2_vit_gemm_ab.txt (in the C5 step: 439.8k -> 444.7k and 438.9k -> 438.7k tok/s on two boxes). The o / fc2 forward (bias + residual) stay on the pair kernel: the
+// one-CTA kernel's row-per-thread residual reads made the C5 step slower (440.8k -> 428.3k tok/s).
+// PF_GEMM_SMALL_ONECTA=0 keeps the pair kernel (A/B).
 static bool small_onecta(int M, int N, int epi) {
   static const bool on = [] {
     const char* e = std::getenv("PF_GEMM_SMALL_ONECTA");

@@ -1,4 +1,5 @@
-"""Write profiles/roofline_traffic.json from an ncu --set full capture of the bench's roofline kernel.
+"""Add (or replace) the entry of one bench roofline kernel in profiles/roofline_traffic.json (a list, one
+entry per config's roofline kernel) from an ncu --set full capture of that kernel.
 
     python tools/ncu_traffic.py gpurun_out/roofline.ncu-rep "<kernel string from bench roofline.kernel>"
 """
@@ -28,6 +29,12 @@ d = {"kernel": kernel, "bytes_per_launch": int(rd + wr), "dram_read_bytes": int(
      "launches_captured": len(vals), "picked": "longest launch", "source": os.path.basename(rep),
      "note": "ncu --set full --clock-control none, cold-cache replay of the kernel inside the bench's timed steps"}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "roofline_traffic.json")
+try:
+    with open(path) as f:
+        old = json.load(f)
+except (OSError, ValueError):
+    old = []
+entries = [e for e in (old if isinstance(old, list) else [old]) if e.get("kernel") != kernel] + [d]
 with open(path, "w") as f:
-    json.dump(d, f, indent=1)
+    json.dump(entries, f, indent=1)
 print(json.dumps(d))
