@@ -1051,6 +1051,14 @@ int group_m_for(int tiles_m, int tiles_n, int K, bool b_mn) {
     return e ? std::atoi(e) : 0;
   }();
   if (forced > 0) return forced;
+  // Wide forward GEMMs with at most 16 tile rows take them all in one group at any K, so each weight
+  // column block is read from DRAM once (the 4096-row A stays in L2): the LLaMA-8B gate|up read its
+  // 235 MB weight twice at G = 8; C3 +0.6-0.8% tok/s (profiles/r2_gemm_fullm.md). PF_GEMM_FULLM=0: G = 8.
+  static const bool fullm = [] {
+    const char* e = std::getenv("PF_GEMM_FULLM");
+    return !(e && e[0] == '0');
+  }();
+  if (!b_mn && tiles_n >= 48 && fullm && tiles_m <= 16) return tiles_m;
   if (!b_mn && tiles_n >= 48) return K <= 2048 ? std::min(tiles_m, 16) : 8;
   return K >= 32768 ? 8 : 4;
 }
